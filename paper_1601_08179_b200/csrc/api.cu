@@ -1,0 +1,584 @@
+// C-ABI entry points (include/sc.h): context, layout, workspace, operator, BT-PCG loop,
+// conversions, NCCL bootstrap and interface-plane halo exchange.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sc.h"
+#include "sc_internal.h"
+
+using namespace sc;
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+namespace {
+struct NcclApi {
+  bool loaded = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+
+bool load_nccl() {
+  if (g_nccl.loaded) return true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    const char* env = getenv("SC_NCCL_LIB");
+    if (env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+  }
+  if (!h) return false;
+#define SYM(name, field) g_nccl.field = (decltype(g_nccl.field))dlsym(h, name); if (!g_nccl.field) return false;
+  SYM("ncclGetUniqueId", GetUniqueId)
+  SYM("ncclCommInitRank", CommInitRank)
+  SYM("ncclCommDestroy", CommDestroy)
+  SYM("ncclAllReduce", AllReduce)
+  SYM("ncclSend", Send)
+  SYM("ncclRecv", Recv)
+  SYM("ncclGroupStart", GroupStart)
+  SYM("ncclGroupEnd", GroupEnd)
+  SYM("ncclGetErrorString", GetErrorString)
+#undef SYM
+  g_nccl.loaded = true;
+  return true;
+}
+}  // namespace
+
+// ------------------------------------------------------------------ context
+struct sc_ctx {
+  sc_params prm;
+  std::vector<double> hx, hy, hz;       // global widths
+  Basis1D B;
+  Geom g;
+  sc_layout_info L;
+  double* d_tab = nullptr;              // 1-D tables
+  double* d_h = nullptr;                // local widths hx | hy | hz
+  double* d_dinv = nullptr;             // uniform D^{-1} table
+  // workspace (caller-owned)
+  double* ws = nullptr;
+  size_t ws_bytes = 0;
+  double *pinv = nullptr, *r = nullptr, *pv = nullptr, *q = nullptr, *bdev = nullptr, *xdev = nullptr;
+  double *scal = nullptr, *partials = nullptr, *halo = nullptr, *scratch = nullptr;
+  long long scratch_elems = 0;
+  long long plane_len = 0;              // entries of one interface plane
+  long long seg_off[2][4], seg_len[4];  // bottom / top plane segments
+  OwnMask own;
+  ncclComm_t comm = nullptr;
+  long long nlaunch = 0;
+  std::string err;
+  bool broken = false;
+};
+
+static const long long kAlign = 32;   // entries (256 B)
+static long long align_up(long long v) { return (v + kAlign - 1) / kAlign * kAlign; }
+
+#define CK(call)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (cudaError_t)(call);                                          \
+    if (e_ != cudaSuccess) {                                                       \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);               \
+      ctx->broken = true;                                                          \
+      return SC_ECUDA;                                                             \
+    }                                                                              \
+  } while (0)
+
+#define NK(call)                                                                   \
+  do {                                                                             \
+    ncclResult_t r_ = (call);                                                      \
+    if (r_ != ncclSuccess) {                                                       \
+      ctx->err = std::string(#call) + ": " + g_nccl.GetErrorString(r_);            \
+      ctx->broken = true;                                                          \
+      return SC_ENCCL;                                                             \
+    }                                                                              \
+  } while (0)
+
+#define LAUNCH(expr)                                                               \
+  do {                                                                             \
+    int nl_ = 0;                                                                   \
+    int e2_ = (expr);                                                              \
+    ctx->nlaunch += nl_;                                                           \
+    if (e2_ != 0) {                                                                \
+      ctx->err = std::string(#expr) + ": " + cudaGetErrorString((cudaError_t)e2_); \
+      ctx->broken = true;                                                          \
+      return SC_ECUDA;                                                             \
+    }                                                                              \
+  } while (0)
+// (launchers take `&nl_` as their last argument)
+
+static bool finite_pos(double v) { return std::isfinite(v) && v > 0; }
+
+extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
+  if (!prm || !out) return SC_EINVAL;
+  *out = nullptr;
+  const int p = prm->p;
+  if (p < 2 || p > SC_PMAX) return SC_EINVAL;
+  for (int d = 0; d < 3; ++d) {
+    if (prm->ne[d] < 1 || !prm->h[d]) return SC_EINVAL;
+    for (int e = 0; e < prm->ne[d]; ++e)
+      if (!finite_pos(prm->h[d][e])) return SC_EINVAL;
+  }
+  if (!std::isfinite(prm->lambda) || prm->lambda < 0) return SC_EINVAL;
+  if (prm->nranks < 1 || prm->rank < 0 || prm->rank >= prm->nranks) return SC_EINVAL;
+  if (prm->nranks > prm->ne[2]) return SC_EINVAL;
+  if (prm->nranks > 1 && !prm->nccl_comm) return SC_EINVAL;
+
+  sc_ctx* ctx = new sc_ctx();
+  ctx->prm = *prm;
+  for (int d = 0; d < 3; ++d) {
+    std::vector<double>& h = d == 0 ? ctx->hx : (d == 1 ? ctx->hy : ctx->hz);
+    h.assign(prm->h[d], prm->h[d] + prm->ne[d]);
+    ctx->prm.h[d] = h.data();
+  }
+  std::string berr;
+  if (!build_basis_1d(p, ctx->B, berr)) {
+    ctx->err = berr;
+    delete ctx;
+    return SC_EINVAL;
+  }
+  const int ni = p - 1;
+  // ---- slab partition: rank r owns element layers [z0, z1) (balanced, contiguous)
+  const int nzg = prm->ne[2], R = prm->nranks, r = prm->rank;
+  const int z0 = (int)((long long)nzg * r / R), z1 = (int)((long long)nzg * (r + 1) / R);
+  const int nx = prm->ne[0], ny = prm->ne[1], nz = z1 - z0;
+  Geom& g = ctx->g;
+  memset(&g, 0, sizeof(g));
+  g.p = p; g.ni = ni; g.nx = nx; g.ny = ny; g.nz = nz;
+  g.dir_bot = (r == 0); g.dir_top = (r == R - 1);
+  g.z_begin = z0;
+  g.nx1 = nx * p + 1; g.ny1 = ny * p + 1; g.nz1 = nz * p + 1;
+  g.lam_h = prm->lambda;
+  const long long n2 = (long long)ni * ni;
+  g.n_f[0] = (long long)(nx + 1) * ny * nz;
+  g.n_f[1] = (long long)nx * (ny + 1) * nz;
+  g.n_f[2] = (long long)nx * ny * (nz + 1);
+  g.n_e[0] = (long long)nx * (ny + 1) * (nz + 1);
+  g.n_e[1] = (long long)(nx + 1) * ny * (nz + 1);
+  g.n_e[2] = (long long)(nx + 1) * (ny + 1) * nz;
+  g.n_v = (long long)(nx + 1) * (ny + 1) * (nz + 1);
+  long long off = 0;
+  for (int d = 0; d < 3; ++d) { g.off_f[d] = off; off = align_up(off + g.n_f[d] * n2); }
+  for (int d = 0; d < 3; ++d) { g.off_e[d] = off; off = align_up(off + g.n_e[d] * ni); }
+  g.off_v = off;
+  off = align_up(off + g.n_v);
+  g.n_total = off;
+
+  sc_layout_info& L = ctx->L;
+  memset(&L, 0, sizeof(L));
+  L.n_total = g.n_total;
+  L.n_lattice = (long long)g.nx1 * g.ny1 * g.nz1;
+  L.n_lattice_global = (long long)(nx * p + 1) * (ny * p + 1) * ((long long)nzg * p + 1);
+  for (int d = 0; d < 3; ++d) {
+    L.off_face[d] = g.off_f[d]; L.n_faces[d] = g.n_f[d];
+    L.off_edge[d] = g.off_e[d]; L.n_edges[d] = g.n_e[d];
+  }
+  L.off_vertex = g.off_v; L.n_vertices = g.n_v;
+  L.ne_local[0] = nx; L.ne_local[1] = ny; L.ne_local[2] = nz;
+  L.z_begin = z0; L.z_end = z1; L.p = p; L.n_i = ni;
+  {  // free unknowns owned by this rank (the lower rank owns each interface plane):
+     // free lattice box gx in [1, nx p - 1], gy in [1, ny p - 1], gz in [1, gz_hi] minus element interiors
+    long long gz_hi = g.dir_top ? (long long)nz * p - 1 : (long long)nz * p;
+    long long tot = ((long long)nx * p - 1) * ((long long)ny * p - 1) * gz_hi;
+    L.n_free = tot - (long long)nx * ny * nz * (long long)ni * ni * ni;
+  }
+  // ---- device tables
+  std::vector<double> tab(TAB_SIZE, 0.0);
+  const Basis1D& B = ctx->B;
+  for (int m = 0; m < ni; ++m) {
+    tab[TAB_LAM + m] = B.lam[m];
+    tab[TAB_A0 + m] = B.a0[m];
+    tab[TAB_AP + m] = B.ap[m];
+    tab[TAB_SIG + m] = B.sigma[m];
+  }
+  for (int i = 0; i <= p; ++i) tab[TAB_W + i] = B.w[i];
+  tab[TAB_SCAL + 0] = B.K00;
+  tab[TAB_SCAL + 1] = B.K0p;
+  tab[TAB_SCAL + 2] = B.w0;
+  const int MS = SC_NIMAX * SC_NIMAX;
+  for (int a = 0; a < ni; ++a)
+    for (int b = 0; b < ni; ++b) {
+      double s_ab = B.S[a * ni + b], s_ba = B.S[b * ni + a];
+      tab[TAB_MAT + MAT_I * MS + a * ni + b] = (a == b) ? 1.0 : 0.0;
+      tab[TAB_MAT + MAT_SM * MS + a * ni + b] = s_ab * B.w[b + 1];    // (S M)[a][b]
+      tab[TAB_MAT + MAT_S * MS + a * ni + b] = s_ab;                  // S[a][b]
+      tab[TAB_MAT + MAT_ST * MS + a * ni + b] = s_ba;                 // S^T[a][b]
+      tab[TAB_MAT + MAT_MST * MS + a * ni + b] = B.w[a + 1] * s_ba;   // (M S^T)[a][b]
+    }
+  bool uniform = true;
+  for (double v : ctx->hx) uniform &= (v == ctx->hx[0]);
+  for (double v : ctx->hy) uniform &= (v == ctx->hy[0]);
+  for (double v : ctx->hz) uniform &= (v == ctx->hz[0]);
+  g.uniform = uniform;
+  if (cudaSetDevice(prm->device) != cudaSuccess) { ctx->err = "cudaSetDevice"; delete ctx; return SC_ECUDA; }
+  auto fail = [&](const char* what) { ctx->err = what; sc_destroy(ctx); return SC_ECUDA; };
+  if (cudaMalloc(&ctx->d_tab, sizeof(double) * TAB_SIZE) != cudaSuccess) return fail("cudaMalloc tab");
+  if (cudaMemcpy(ctx->d_tab, tab.data(), sizeof(double) * TAB_SIZE, cudaMemcpyHostToDevice) != cudaSuccess)
+    return fail("cudaMemcpy tab");
+  std::vector<double> hloc;
+  hloc.insert(hloc.end(), ctx->hx.begin(), ctx->hx.end());
+  hloc.insert(hloc.end(), ctx->hy.begin(), ctx->hy.end());
+  hloc.insert(hloc.end(), ctx->hz.begin() + z0, ctx->hz.begin() + z1);
+  if (cudaMalloc(&ctx->d_h, sizeof(double) * hloc.size()) != cudaSuccess) return fail("cudaMalloc h");
+  if (cudaMemcpy(ctx->d_h, hloc.data(), sizeof(double) * hloc.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+    return fail("cudaMemcpy h");
+  g.hx = ctx->d_h; g.hy = ctx->d_h + nx; g.hz = ctx->d_h + nx + ny;
+  g.tab = ctx->d_tab;
+  g.dinv = nullptr;
+  if (uniform) {
+    double h1 = ctx->hx[0], h2 = ctx->hy[0], h3 = ctx->hz[0];
+    double s = h1 * h2 * h3 * 0.125;
+    double d[4] = {s * prm->lambda, s * 4.0 / (h1 * h1), s * 4.0 / (h2 * h2), s * 4.0 / (h3 * h3)};
+    for (int q = 0; q < 4; ++q) g.d_uni[q] = d[q];
+    std::vector<double> dinv((size_t)ni * ni * ni);
+    for (int k = 0; k < ni; ++k)
+      for (int j = 0; j < ni; ++j)
+        for (int i = 0; i < ni; ++i) {
+          double D = d[0] + d[1] * B.lam[i] + d[2] * B.lam[j] + d[3] * B.lam[k];
+          if (!(D > 0)) { ctx->err = "non-positive D entry"; sc_destroy(ctx); return SC_EINVAL; }
+          dinv[i + ni * (j + (size_t)ni * k)] = 1.0 / D;
+        }
+    if (cudaMalloc(&ctx->d_dinv, sizeof(double) * dinv.size()) != cudaSuccess) return fail("cudaMalloc dinv");
+    if (cudaMemcpy(ctx->d_dinv, dinv.data(), sizeof(double) * dinv.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail("cudaMemcpy dinv");
+    g.dinv = ctx->d_dinv;
+  }
+  // ---- interface planes (z-face plane, x-edges, y-edges, vertices at fz = 0 / nz)
+  long long lens[4] = {(long long)nx * ny * n2, (long long)nx * (ny + 1) * ni, (long long)(nx + 1) * ny * ni,
+                       (long long)(nx + 1) * (ny + 1)};
+  for (int side = 0; side < 2; ++side) {
+    long long fz = side == 0 ? 0 : nz;
+    ctx->seg_off[side][0] = g.off_f[2] + fz * lens[0];
+    ctx->seg_off[side][1] = g.off_e[0] + fz * lens[1];
+    ctx->seg_off[side][2] = g.off_e[1] + fz * lens[2];
+    ctx->seg_off[side][3] = g.off_v + fz * lens[3];
+  }
+  ctx->plane_len = 0;
+  for (int q = 0; q < 4; ++q) { ctx->seg_len[q] = lens[q]; ctx->plane_len += lens[q]; }
+  memset(&ctx->own, 0, sizeof(ctx->own));
+  if (r > 0) {
+    ctx->own.n = 4;
+    for (int q = 0; q < 4; ++q) { ctx->own.lo[q] = ctx->seg_off[0][q]; ctx->own.hi[q] = ctx->seg_off[0][q] + lens[q]; }
+  }
+  if (R > 1) {
+    if (!load_nccl()) { ctx->err = "libnccl.so.2 not loadable"; sc_destroy(ctx); return SC_ENCCL; }
+    ctx->comm = (ncclComm_t)prm->nccl_comm;
+  }
+  *out = ctx;
+  return SC_OK;
+}
+
+extern "C" sc_status sc_destroy(sc_ctx* ctx) {
+  if (!ctx) return SC_OK;
+  if (ctx->d_tab) cudaFree(ctx->d_tab);
+  if (ctx->d_h) cudaFree(ctx->d_h);
+  if (ctx->d_dinv) cudaFree(ctx->d_dinv);
+  delete ctx;
+  return SC_OK;
+}
+
+extern "C" sc_status sc_layout(const sc_ctx* ctx, sc_layout_info* out) {
+  if (!ctx || !out) return SC_EINVAL;
+  *out = ctx->L;
+  return SC_OK;
+}
+
+static const long long kScratchCtas = 296;
+
+extern "C" size_t sc_workspace_bytes(const sc_ctx* ctx) {
+  if (!ctx) return 0;
+  long long n = ctx->g.n_total;
+  long long n3 = (long long)(ctx->g.p + 1) * (ctx->g.p + 1) * (ctx->g.p + 1);
+  long long tot = 6 * n + align_up(SCAL_COUNT) + align_up(4 * SC_RED_BLOCKS) + 4 * align_up(ctx->plane_len) +
+                  kScratchCtas * 2 * n3;
+  return (size_t)tot * sizeof(double);
+}
+
+static sc_status halo_sum(sc_ctx* ctx, double* y, cudaStream_t st);
+
+extern "C" sc_status sc_bind_workspace(sc_ctx* ctx, void* d_ws, size_t bytes) {
+  if (!ctx || !d_ws) return SC_EINVAL;
+  if (ctx->broken) return SC_ESTATE;
+  if (bytes < sc_workspace_bytes(ctx)) return SC_ENOMEM;
+  if (((uintptr_t)d_ws) % 256 != 0) return SC_EINVAL;
+  double* w = (double*)d_ws;
+  long long n = ctx->g.n_total;
+  ctx->ws = w; ctx->ws_bytes = bytes;
+  ctx->pinv = w; w += n;
+  ctx->r = w; w += n;
+  ctx->pv = w; w += n;
+  ctx->q = w; w += n;
+  ctx->bdev = w; w += n;
+  ctx->xdev = w; w += n;
+  ctx->scal = w; w += align_up(SCAL_COUNT);
+  ctx->partials = w; w += align_up(4 * SC_RED_BLOCKS);
+  ctx->halo = w; w += 4 * align_up(ctx->plane_len);
+  ctx->scratch = w;
+  long long n3 = (long long)(ctx->g.p + 1) * (ctx->g.p + 1) * (ctx->g.p + 1);
+  ctx->scratch_elems = kScratchCtas * 2 * n3;
+  CK(cudaSetDevice(ctx->prm.device));
+  cudaStream_t st = 0;
+  CK(cudaMemsetAsync(ctx->scal, 0, sizeof(double) * SCAL_COUNT, st));
+  // BT preconditioner: Pinv = 1 / diag(Rhat Htilde Rhat^T)
+  LAUNCH(launch_diag(ctx->g, ctx->pinv, st, &nl_));
+  sc_status s = halo_sum(ctx, ctx->pinv, st);
+  if (s != SC_OK) return s;
+  LAUNCH(launch_invert_diag(ctx->g, ctx->pinv, st, &nl_));
+  CK(cudaStreamSynchronize(st));
+  return SC_OK;
+}
+
+extern "C" sc_status sc_basis_1d(const sc_ctx* ctx, double* lam, double* a0, double* ap, double* S, double* w,
+                                 double* kt) {
+  if (!ctx) return SC_EINVAL;
+  const Basis1D& B = ctx->B;
+  int ni = B.ni;
+  for (int m = 0; m < ni; ++m) {
+    if (lam) lam[m] = B.lam[m];
+    if (a0) a0[m] = B.a0[m];
+    if (ap) ap[m] = B.ap[m];
+    if (S)
+      for (int i = 0; i < ni; ++i) S[m * ni + i] = B.S[m * ni + i];
+  }
+  if (w)
+    for (int i = 0; i <= B.p; ++i) w[i] = B.w[i];
+  if (kt) { kt[0] = B.K00; kt[1] = B.K0p; kt[2] = B.w0; kt[3] = B.parity_err; }
+  return SC_OK;
+}
+
+extern "C" sc_status sc_basis_1d_host(int p, double* lam, double* a0, double* ap, double* S, double* w,
+                                      double* kt) {
+  if (p < 2 || p > SC_PMAX) return SC_EINVAL;
+  sc_ctx tmp;
+  std::string err;
+  if (!build_basis_1d(p, tmp.B, err)) return SC_EINVAL;
+  return sc_basis_1d(&tmp, lam, a0, ap, S, w, kt);
+}
+
+// Interface-plane halo: after every rank has its partial sums on its bottom / top plane,
+// exchange them with the z-neighbours and add (P:107-109 gather across the slab cut).
+static sc_status halo_sum(sc_ctx* ctx, double* y, cudaStream_t st) {
+  const int R = ctx->prm.nranks, r = ctx->prm.rank;
+  if (R == 1) return SC_OK;
+  if (!ctx->halo) { ctx->err = "workspace not bound (needed for the halo exchange)"; return SC_ESTATE; }
+  const long long pl = align_up(ctx->plane_len);
+  double* recv_lo = ctx->halo;
+  double* recv_hi = ctx->halo + pl;
+  NK(g_nccl.GroupStart());
+  for (int side = 0; side < 2; ++side) {
+    int peer = side == 0 ? r - 1 : r + 1;
+    if (peer < 0 || peer >= R) continue;
+    double* rb = side == 0 ? recv_lo : recv_hi;
+    long long o = 0;
+    for (int q = 0; q < 4; ++q) {
+      NK(g_nccl.Send(y + ctx->seg_off[side][q], (size_t)ctx->seg_len[q], ncclDouble, peer, ctx->comm, st));
+      NK(g_nccl.Recv(rb + o, (size_t)ctx->seg_len[q], ncclDouble, peer, ctx->comm, st));
+      o += ctx->seg_len[q];
+    }
+  }
+  NK(g_nccl.GroupEnd());
+  if (r > 0) LAUNCH(launch_add_segments(y, recv_lo, ctx->seg_off[0], ctx->seg_len, 4, st, &nl_));
+  if (r < R - 1) LAUNCH(launch_add_segments(y, recv_hi, ctx->seg_off[1], ctx->seg_len, 4, st, &nl_));
+  return SC_OK;
+}
+
+static sc_status allreduce_scal(sc_ctx* ctx, int slot, int n, cudaStream_t st) {
+  if (ctx->prm.nranks == 1) return SC_OK;
+  NK(g_nccl.AllReduce(ctx->scal + slot, ctx->scal + slot, (size_t)n, ncclDouble, ncclSum, ctx->comm, st));
+  return SC_OK;
+}
+
+static sc_status apply_impl(sc_ctx* ctx, const double* x, double* y, const double* done, cudaStream_t st) {
+  LAUNCH(launch_apply(ctx->g, x, y, done, st, &nl_));
+  return halo_sum(ctx, y, st);
+}
+
+extern "C" sc_status sc_apply_condensed(sc_ctx* ctx, const double* d_x, double* d_y, void* stream) {
+  if (!ctx || !d_x || !d_y || d_x == d_y) return SC_EINVAL;
+  if (ctx->broken) return SC_ESTATE;
+  return apply_impl(ctx, d_x, d_y, nullptr, (cudaStream_t)stream);
+}
+
+static sc_status pcg_impl(sc_ctx* ctx, const double* b, double* x, double rtol, int maxit, sc_pcg_report* rep,
+                          cudaStream_t st) {
+  auto t0 = std::chrono::steady_clock::now();
+  const long long n = ctx->g.n_total;
+  double* done = ctx->scal + SCAL_DONE;
+  const double tol2 = rtol > 0 ? rtol * rtol : -1.0;
+  LAUNCH(launch_pcg_init(b, ctx->pinv, x, ctx->r, ctx->pv, n, ctx->own, ctx->partials, st, &nl_));
+  LAUNCH(launch_reduce2(ctx->partials, ctx->scal, SCAL_RED0, 2, nullptr, st, &nl_));
+  sc_status s = allreduce_scal(ctx, SCAL_RED0, 2, st);
+  if (s) return s;
+  LAUNCH(launch_pcg_init_finalize(ctx->scal, ctx->partials, tol2, maxit, st, &nl_));
+  const int check_every = rtol > 0 ? 8 : 0;
+  for (int it = 0; it < maxit; ++it) {
+    s = apply_impl(ctx, ctx->pv, ctx->q, done, st);
+    if (s) return s;
+    LAUNCH(launch_dot_partial(ctx->pv, ctx->q, n, ctx->own, ctx->partials, done, st, &nl_));
+    LAUNCH(launch_reduce2(ctx->partials, ctx->scal, SCAL_RED0, 1, done, st, &nl_));
+    if ((s = allreduce_scal(ctx, SCAL_RED0, 1, st))) return s;
+    LAUNCH(launch_pcg_alpha(ctx->scal, st, &nl_));
+    LAUNCH(launch_pcg_update(x, ctx->r, ctx->pv, ctx->q, ctx->pinv, n, ctx->own, ctx->scal, ctx->partials, st, &nl_));
+    LAUNCH(launch_reduce2(ctx->partials, ctx->scal, SCAL_RED0, 2, done, st, &nl_));
+    if ((s = allreduce_scal(ctx, SCAL_RED0, 2, st))) return s;
+    LAUNCH(launch_pcg_beta(ctx->scal, st, &nl_));
+    LAUNCH(launch_pcg_direction(ctx->pv, ctx->r, ctx->pinv, n, ctx->scal, st, &nl_));
+    if (check_every && (it + 1) % check_every == 0) {
+      double dflag = 0;
+      CK(cudaMemcpyAsync(&dflag, done, sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (dflag != 0.0) break;
+    }
+  }
+  double sc[SCAL_COUNT];
+  CK(cudaMemcpyAsync(sc, ctx->scal, sizeof(sc), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  auto t1 = std::chrono::steady_clock::now();
+  if (rep) {
+    rep->iters = (int)sc[SCAL_ITERS];
+    rep->r0norm = std::sqrt(sc[SCAL_RR0]);
+    rep->relres = sc[SCAL_RR0] > 0 ? std::sqrt(sc[SCAL_RR] / sc[SCAL_RR0]) : 0.0;
+    rep->converged = (sc[SCAL_RR0] == 0.0) || (tol2 > 0 && sc[SCAL_RR] <= tol2 * sc[SCAL_RR0]);
+    rep->t_solve_s = std::chrono::duration<double>(t1 - t0).count();
+  }
+  if (sc[SCAL_BREAK] != 0.0) { ctx->err = "PCG breakdown: p^T A p <= 0"; return SC_EBREAKDOWN; }
+  return SC_OK;
+}
+
+extern "C" sc_status sc_pcg_solve(sc_ctx* ctx, const double* d_b, double* d_x, double rtol, int maxit,
+                                  sc_pcg_report* rep, void* stream) {
+  if (!ctx || !d_b || !d_x || d_b == d_x || maxit < 0 || !std::isfinite(rtol)) return SC_EINVAL;
+  if (ctx->broken) return SC_ESTATE;
+  if (!ctx->ws) { ctx->err = "workspace not bound"; return SC_ESTATE; }
+  return pcg_impl(ctx, d_b, d_x, rtol, maxit, rep, (cudaStream_t)stream);
+}
+
+extern "C" sc_status sc_pcg_solve_host(sc_ctx* ctx, const double* h_b, double* h_x, double rtol, int maxit,
+                                       sc_pcg_report* rep, void* stream) {
+  if (!ctx || !h_b || !h_x || maxit < 0 || !std::isfinite(rtol)) return SC_EINVAL;
+  if (ctx->broken) return SC_ESTATE;
+  if (!ctx->ws) { ctx->err = "workspace not bound"; return SC_ESTATE; }
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t bytes = sizeof(double) * ctx->g.n_total;
+  CK(cudaMemcpyAsync(ctx->bdev, h_b, bytes, cudaMemcpyHostToDevice, st));
+  sc_status s = pcg_impl(ctx, ctx->bdev, ctx->xdev, rtol, maxit, rep, st);
+  if (s != SC_OK && s != SC_EBREAKDOWN) return s;
+  CK(cudaMemcpyAsync(h_x, ctx->xdev, bytes, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return s;
+}
+
+extern "C" sc_status sc_condense_rhs(sc_ctx* ctx, const double* d_f, double* d_b, void* stream) {
+  if (!ctx || !d_f || !d_b) return SC_EINVAL;
+  if (ctx->broken) return SC_ESTATE;
+  if (!ctx->ws) { ctx->err = "workspace not bound"; return SC_ESTATE; }
+  cudaStream_t st = (cudaStream_t)stream;
+  LAUNCH(launch_condense(ctx->g, d_f, d_b, ctx->scratch, ctx->scratch_elems, st, &nl_));
+  return halo_sum(ctx, d_b, st);
+}
+
+extern "C" sc_status sc_recover(sc_ctx* ctx, const double* d_f, const double* d_x, double* d_u, void* stream) {
+  if (!ctx || !d_f || !d_x || !d_u) return SC_EINVAL;
+  if (ctx->broken) return SC_ESTATE;
+  if (!ctx->ws) { ctx->err = "workspace not bound"; return SC_ESTATE; }
+  LAUNCH(launch_recover(ctx->g, d_f, d_x, d_u, ctx->scratch, ctx->scratch_elems, (cudaStream_t)stream, &nl_));
+  return SC_OK;
+}
+
+static int to_mat(int mode, bool to) {
+  if (mode == SC_PERM) return MAT_I;
+  if (mode == SC_PRIMAL) return to ? MAT_SM : MAT_ST;
+  return to ? MAT_S : MAT_MST;
+}
+
+extern "C" sc_status sc_to_transformed(sc_ctx* ctx, const double* d_lattice, double* d_skel, int mode, void* stream) {
+  if (!ctx || !d_lattice || !d_skel || mode < 0 || mode > 2) return SC_EINVAL;
+  if (ctx->broken) return SC_ESTATE;
+  LAUNCH(launch_convert(ctx->g, d_lattice, d_skel, 1, to_mat(mode, true), stream, &nl_));
+  return SC_OK;
+}
+
+extern "C" sc_status sc_from_transformed(sc_ctx* ctx, const double* d_skel, double* d_lattice, int mode, void* stream) {
+  if (!ctx || !d_lattice || !d_skel || mode < 0 || mode > 2) return SC_EINVAL;
+  if (ctx->broken) return SC_ESTATE;
+  LAUNCH(launch_convert(ctx->g, d_skel, d_lattice, 0, to_mat(mode, false), stream, &nl_));
+  return SC_OK;
+}
+
+extern "C" sc_status sc_fill_random(sc_ctx* ctx, uint64_t seed, double* d_skel, void* stream) {
+  if (!ctx || !d_skel) return SC_EINVAL;
+  if (ctx->broken) return SC_ESTATE;
+  LAUNCH(launch_fill_random(ctx->g, seed, d_skel, stream, &nl_));
+  return SC_OK;
+}
+
+extern "C" sc_status sc_dot(sc_ctx* ctx, const double* d_a, const double* d_b, double* h_out, void* stream) {
+  if (!ctx || !d_a || !d_b || !h_out) return SC_EINVAL;
+  if (ctx->broken) return SC_ESTATE;
+  if (!ctx->ws) { ctx->err = "workspace not bound"; return SC_ESTATE; }
+  cudaStream_t st = (cudaStream_t)stream;
+  double* part = ctx->partials + 2 * SC_RED_BLOCKS;   // keep PCG partials untouched
+  LAUNCH(launch_dot_partial(d_a, d_b, ctx->g.n_total, ctx->own, part, nullptr, st, &nl_));
+  // use partial slots [2R, 3R) -> reduce into scal[RED2]
+  LAUNCH(launch_reduce2(part, ctx->scal, SCAL_RED2, 1, nullptr, st, &nl_));
+  sc_status s = allreduce_scal(ctx, SCAL_RED2, 1, st);
+  if (s) return s;
+  CK(cudaMemcpyAsync(h_out, ctx->scal + SCAL_RED2, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return SC_OK;
+}
+
+extern "C" sc_status sc_preconditioner(sc_ctx* ctx, double* d_pinv, void* stream) {
+  if (!ctx || !d_pinv) return SC_EINVAL;
+  if (!ctx->ws) { ctx->err = "workspace not bound"; return SC_ESTATE; }
+  CK(cudaMemcpyAsync(d_pinv, ctx->pinv, sizeof(double) * ctx->g.n_total, cudaMemcpyDeviceToDevice,
+                     (cudaStream_t)stream));
+  return SC_OK;
+}
+
+extern "C" sc_status sc_nccl_unique_id(unsigned char h_id[128]) {
+  if (!h_id) return SC_EINVAL;
+  if (!load_nccl()) return SC_ENCCL;
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != ncclSuccess) return SC_ENCCL;
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  memcpy(h_id, &id, 128);
+  return SC_OK;
+}
+
+extern "C" sc_status sc_nccl_comm_init(const unsigned char h_id[128], int nranks, int rank, int device, void** comm_out) {
+  if (!h_id || !comm_out || nranks < 1 || rank < 0 || rank >= nranks) return SC_EINVAL;
+  if (!load_nccl()) return SC_ENCCL;
+  if (cudaSetDevice(device) != cudaSuccess) return SC_ECUDA;
+  ncclUniqueId id;
+  memcpy(&id, h_id, 128);
+  ncclComm_t c;
+  if (g_nccl.CommInitRank(&c, nranks, id, rank) != ncclSuccess) return SC_ENCCL;
+  *comm_out = (void*)c;
+  return SC_OK;
+}
+
+extern "C" sc_status sc_nccl_comm_destroy(void* comm) {
+  if (!comm) return SC_OK;
+  if (!load_nccl()) return SC_ENCCL;
+  return g_nccl.CommDestroy((ncclComm_t)comm) == ncclSuccess ? SC_OK : SC_ENCCL;
+}
+
+extern "C" long long sc_launch_count(const sc_ctx* ctx) { return ctx ? ctx->nlaunch : 0; }
+
+extern "C" const char* sc_last_error(const sc_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+extern "C" const char* sc_version(void) {
+  return "sc 0.1 (sm_100a, fp64, TPT condensed operator v1, BT-PCG)";
+}

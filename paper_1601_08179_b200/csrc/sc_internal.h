@@ -1,0 +1,104 @@
+// Internal declarations shared by the host (api.cu, basis1d.cpp) and the kernels.
+#pragma once
+
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#define SC_PMAX 32
+#define SC_NIMAX (SC_PMAX - 1)
+
+namespace sc {
+
+// 1-D transformed basis (host, double), see basis1d.cpp.
+struct Basis1D {
+  int p = 0, ni = 0;
+  double x[SC_PMAX + 1], w[SC_PMAX + 1];
+  double K[(SC_PMAX + 1) * (SC_PMAX + 1)];
+  double lam[SC_NIMAX], a0[SC_NIMAX], ap[SC_NIMAX];
+  double S[SC_NIMAX * SC_NIMAX];      // S_II, row-major, rows = M-orthonormal eigenvectors
+  int sigma[SC_NIMAX];                // ap = sigma * a0 (parity of eigenvector m)
+  double K00 = 0, K0p = 0, w0 = 0;
+  double parity_err = 0, eig_err = 0;
+};
+
+bool build_basis_1d(int p, Basis1D& B, std::string& err);
+
+// Device-side description of the rank-local slab (passed by value to kernels).
+struct Geom {
+  int p, ni, nx, ny, nz;        // local element counts
+  int dir_bot, dir_top;         // z-planes 0 / nz are Dirichlet (physical boundary)
+  long long off_f[3], off_e[3], off_v, n_total;
+  long long n_f[3], n_e[3], n_v;
+  int nx1, ny1, nz1;            // local lattice dims
+  int z_begin;                  // global element layer of local layer 0
+  int uniform;                  // all elements share one geometry (D^{-1} table valid)
+  double lam_h;                 // Helmholtz lambda
+  const double* hx;             // device arrays of local element widths
+  const double* hy;
+  const double* hz;
+  const double* tab;            // device 1-D tables, see TAB_* offsets
+  const double* dinv;           // uniform grids: D^{-1}(i,j,k), i fastest (n_I^3); else null
+  double d_uni[4];              // uniform grids: d_e
+};
+
+// Offsets into the device 1-D table (doubles).
+enum {
+  TAB_LAM = 0,
+  TAB_A0 = TAB_LAM + SC_NIMAX,
+  TAB_AP = TAB_A0 + SC_NIMAX,
+  TAB_SIG = TAB_AP + SC_NIMAX,
+  TAB_W = TAB_SIG + SC_NIMAX,                 // GLL weights w[0..p]
+  TAB_SCAL = TAB_W + SC_PMAX + 1,             // K00, K0p, w0
+  TAB_MAT = TAB_SCAL + 8,                     // 5 matrices n_I x n_I for conversions
+  TAB_SIZE = TAB_MAT + 5 * SC_NIMAX * SC_NIMAX
+};
+// Conversion matrices: 0 identity, 1 S M (to primal = S^{-T}), 2 S (to dual),
+// 3 S^T (from primal), 4 M S^T (from dual = S^{-1}).
+enum { MAT_I = 0, MAT_SM = 1, MAT_S = 2, MAT_ST = 3, MAT_MST = 4 };
+
+// PCG device scalars (doubles in the workspace).
+enum {
+  SCAL_RZ = 0, SCAL_RZNEW, SCAL_PQ, SCAL_ALPHA, SCAL_BETA, SCAL_RR, SCAL_RR0,
+  SCAL_DONE, SCAL_ITERS, SCAL_BREAK, SCAL_TOL2, SCAL_MAXIT, SCAL_RED0, SCAL_RED1, SCAL_RED2,
+  SCAL_COUNT = 32
+};
+
+#define SC_RED_BLOCKS 1184   // fixed grid of the deterministic 2-stage reductions (8 x 148)
+
+// ---- kernel launchers (kernels_*.cu); all return cudaError_t as int ----
+int launch_apply(const Geom& g, const double* x, double* y, const double* done, void* stream, int* nlaunch);
+int launch_diag(const Geom& g, double* diag, void* stream, int* nlaunch);
+int launch_invert_diag(const Geom& g, double* diag, void* stream, int* nlaunch);
+int launch_convert(const Geom& g, const double* in, double* out, int to_skel, int mat, void* stream, int* nlaunch);
+int launch_fill_random(const Geom& g, uint64_t seed, double* v, void* stream, int* nlaunch);
+int launch_condense(const Geom& g, const double* f, double* b, double* scratch, long long scratch_elems,
+                    void* stream, int* nlaunch);
+int launch_recover(const Geom& g, const double* f, const double* x, double* u, double* scratch,
+                   long long scratch_elems, void* stream, int* nlaunch);
+
+// PCG vector kernels (kernels_vec.cu). `own_lo/own_hi`: [lo, hi) skeleton ranges excluded
+// from dot products (interface plane owned by the lower rank), up to 4 ranges.
+struct OwnMask { long long lo[4], hi[4]; int n; };
+int launch_dot_partial(const double* a, const double* b, long long n, OwnMask m, double* partials,
+                       const double* done, void* stream, int* nlaunch);
+int launch_reduce_partials(const double* partials, int nparts, double* out, const double* done,
+                           void* stream, int* nlaunch);
+int launch_pcg_init(const double* b, const double* pinv, double* x, double* r, double* p, long long n,
+                    OwnMask m, double* partials, void* stream, int* nlaunch);
+int launch_pcg_init_finalize(double* scal, const double* partials, double tol2, int maxit, void* stream, int* nlaunch);
+int launch_pcg_alpha(double* scal, void* stream, int* nlaunch);
+int launch_pcg_update(double* x, double* r, const double* p, const double* q, const double* pinv,
+                      long long n, OwnMask m, const double* scal, double* partials, void* stream, int* nlaunch);
+int launch_pcg_beta(double* scal, void* stream, int* nlaunch);
+int launch_pcg_direction(double* p, const double* r, const double* pinv, long long n, const double* scal,
+                         void* stream, int* nlaunch);
+int launch_reduce2(const double* partials, double* scal, int slot0, int nvals, const double* done,
+                   void* stream, int* nlaunch);
+
+}  // namespace sc
+
+namespace sc {
+int launch_add_segments(double* y, const double* add, const long long* off, const long long* len, int n,
+                        void* stream, int* nlaunch);
+}

@@ -1,0 +1,270 @@
+"""GPU parity: the CUDA path (libsc.so through the C-ABI) against the CPU oracle.
+
+Tolerances (BASELINE.json north_star): relative L2 <= 1e-12 for one operator application,
+<= 1e-10 for the PCG solution, iteration counts within +-1.  Comparisons are made in the
+nodal basis (convention-free) through sc_to/from_transformed, plus a
+stricter transformed-basis check with the a0 > 0 sign rule (c2).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import basis, mesh, operator, pcg, solve
+from synth import small_grid, lattice_random, sine_f, sine_u, cfg1, cfg2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import __graft_entry__
+    __graft_entry__.build()
+    assert torch.cuda.is_available()
+
+
+def ctx_for(g):
+    from paper_1601_08179_b200 import context_for_grid
+    return context_for_grid(g, device=0)
+
+
+def gpu_apply_nodal(ctx, x_lat):
+    from paper_1601_08179_b200 import SC_PRIMAL, SC_DUAL
+    xt = ctx.skeleton()
+    ctx.sc_to_transformed(torch.from_numpy(np.ascontiguousarray(x_lat)).cuda(), xt, SC_PRIMAL)
+    yt = ctx.skeleton()
+    ctx.sc_apply_condensed(xt, yt)
+    y = ctx.lattice()
+    ctx.sc_from_transformed(yt, y, SC_DUAL)
+    return y.cpu().numpy(), xt, yt
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def nonuniform(p, ne, lam, seed=0):
+    rng = np.random.default_rng(seed)
+    g = small_grid(p, ne, lam)
+    g.hx = rng.uniform(0.3, 1.7, ne[0]); g.hy = rng.uniform(0.3, 1.7, ne[1]); g.hz = rng.uniform(0.3, 1.7, ne[2])
+    return g
+
+
+def test_random_fill_bitwise():
+    from paper_1601_08179_b200 import SC_PERM
+    for g in (cfg1(), small_grid(3, (3, 2, 4), 0.0)):
+        ctx = ctx_for(g)
+        v = ctx.skeleton()
+        ctx.sc_fill_random(7, v)
+        lat = ctx.lattice()
+        ctx.sc_from_transformed(v, lat, SC_PERM)
+        ref = lattice_random(7, g.ne, g.p).ravel()
+        assert np.array_equal(lat.cpu().numpy(), ref)
+
+
+def test_perm_roundtrip_and_padding():
+    from paper_1601_08179_b200 import SC_PERM
+    g = small_grid(4, (3, 2, 2), 1.0)
+    ctx = ctx_for(g)
+    v = ctx.skeleton()
+    ctx.sc_fill_random(3, v)
+    lat = ctx.lattice()
+    ctx.sc_from_transformed(v, lat, SC_PERM)
+    v2 = ctx.skeleton(fill=5.0)
+    ctx.sc_to_transformed(lat, v2, SC_PERM)
+    assert torch.equal(v, v2)
+    L = ctx.layout
+    assert L.n_free == int(mesh.free_skeleton_mask(g).sum())
+    assert int((v != 0).sum()) == L.n_free
+
+
+@pytest.mark.parametrize("p,ne,lam", [(2, (2, 2, 2), 1.0), (3, (3, 2, 2), 0.0), (4, (2, 2, 2), 1.0),
+                                      (5, (2, 3, 2), 0.7), (6, (2, 2, 3), 0.0), (8, (3, 3, 3), 0.0),
+                                      (8, (1, 2, 3), 1.0), (12, (2, 2, 2), 1.0), (16, (2, 2, 2), 0.0)])
+def test_operator_parity_nodal(p, ne, lam):
+    g = small_grid(p, ne, lam, lengths=(1.0, 1.5, 0.8))
+    op = operator.AssembledCondensedOperator(g)
+    x = lattice_random(11 + p, g.ne, g.p).ravel()
+    ref = op.apply(x)
+    ctx = ctx_for(g)
+    y, _, _ = gpu_apply_nodal(ctx, x)
+    assert rel(y, ref) <= 1e-12
+
+
+@pytest.mark.parametrize("p", [3, 7])
+def test_operator_parity_nonuniform_geometry(p):
+    g = nonuniform(p, (3, 2, 3), 0.4, seed=p)
+    op = operator.AssembledCondensedOperator(g)
+    x = lattice_random(5, g.ne, g.p).ravel()
+    ctx = ctx_for(g)
+    y, _, _ = gpu_apply_nodal(ctx, x)
+    assert rel(y, op.apply(x)) <= 1e-12
+
+
+@pytest.mark.parametrize("p", [4, 8])
+def test_operator_transformed_basis_strict(p):
+    """Transformed-basis values agree directly when both sides use the a0 > 0 convention."""
+    from paper_1601_08179_b200 import SC_PERM
+    g = small_grid(p, (2, 3, 2), 1.0)
+    op = operator.AssembledCondensedOperator(g)
+    x = lattice_random(2, g.ne, g.p).ravel()
+    y_ref_t = solve.transform(g, op.apply(x), "dual")
+    ctx = ctx_for(g)
+    _, xt, yt = gpu_apply_nodal(ctx, x)
+    lat = ctx.lattice()
+    ctx.sc_from_transformed(yt, lat, SC_PERM)
+    skel = mesh.skeleton_mask(g)
+    assert rel(lat.cpu().numpy()[skel], y_ref_t[skel]) <= 1e-12
+
+
+def test_operator_symmetry_and_dirichlet():
+    g = small_grid(5, (2, 2, 3), 0.0)
+    ctx = ctx_for(g)
+    a, b = ctx.skeleton(), ctx.skeleton()
+    ctx.sc_fill_random(1, a)
+    ctx.sc_fill_random(2, b)
+    Aa, Ab = ctx.skeleton(), ctx.skeleton()
+    ctx.sc_apply_condensed(a, Aa)
+    ctx.sc_apply_condensed(b, Ab)
+    s1, s2 = ctx.sc_dot(b, Aa), ctx.sc_dot(a, Ab)
+    assert abs(s1 - s2) <= 1e-12 * abs(s1)
+    assert ctx.sc_dot(a, Aa) > 0
+    # single element: every skeleton entity is Dirichlet -> output identically zero
+    g1 = small_grid(3, (1, 1, 1), 1.0)
+    c1 = ctx_for(g1)
+    v = c1.skeleton(fill=1.0)
+    out = c1.skeleton(fill=3.0)
+    c1.sc_apply_condensed(v, out)
+    assert float(out.abs().max()) == 0.0
+
+
+def test_preconditioner_matches_oracle_block_diagonal():
+    """Pinv = 1/diag of the assembled transformed operator == inverse diagonal of the
+    transformed nodal block-Jacobi blocks."""
+    from paper_1601_08179_b200 import SC_PERM
+    g = small_grid(4, (3, 2, 2), 0.3, lengths=(2.0, 1.0, 1.0))
+    op = operator.AssembledCondensedOperator(g)
+    P = solve.BlockJacobi(op)
+    _, S = basis.interior_eigen(g.p)
+    ref = np.zeros(g.n_lattice)
+    nI = g.p - 1
+    for idx, Binv in P.diagonal_blocks():
+        B = np.linalg.inv(Binv)
+        m = len(idx)
+        T = np.ones((1, 1)) if m == 1 else (S if m == nI else np.kron(S, S))
+        ref[idx] = 1.0 / np.diag(T @ B @ T.T)
+    ctx = ctx_for(g)
+    pv = ctx.skeleton()
+    ctx.sc_preconditioner(pv)
+    lat = ctx.lattice()
+    ctx.sc_from_transformed(pv, lat, SC_PERM)
+    assert rel(lat.cpu().numpy(), ref) <= 1e-12
+
+
+def test_condense_rhs_parity():
+    from paper_1601_08179_b200 import SC_DUAL
+    for g in (cfg1(), small_grid(6, (2, 3, 2), 0.0, lengths=(1.0, 2.0, 1.0))):
+        X, Y, Z = mesh.lattice_coordinates(g)
+        f = np.cos(X + 0.5 * Y) * np.exp(Z) + sine_f(X, Y, Z, g.lam)
+        op = operator.AssembledCondensedOperator(g)
+        b_ref = solve.condensed_rhs(op, f)
+        ctx = ctx_for(g)
+        bt = ctx.skeleton()
+        ctx.sc_condense_rhs(torch.from_numpy(f).cuda(), bt)
+        lat = ctx.lattice()
+        ctx.sc_from_transformed(bt, lat, SC_DUAL)
+        assert rel(lat.cpu().numpy(), b_ref) <= 1e-12
+
+
+def test_recover_parity():
+    from paper_1601_08179_b200 import SC_PRIMAL
+    g = small_grid(5, (2, 2, 3), 1.0)
+    X, Y, Z = mesh.lattice_coordinates(g)
+    f = np.sin(2 * X) * np.cos(Y + Z) + 1.0
+    op = operator.AssembledCondensedOperator(g)
+    uB = lattice_random(4, g.ne, g.p).ravel()
+    u_ref = solve.recover(op, f, uB)
+    ctx = ctx_for(g)
+    xt = ctx.skeleton()
+    ctx.sc_to_transformed(torch.from_numpy(uB).cuda(), xt, SC_PRIMAL)
+    u = ctx.lattice()
+    ctx.sc_recover(torch.from_numpy(f).cuda(), xt, u)
+    assert rel(u.cpu().numpy(), u_ref) <= 1e-12
+
+
+def _oracle_pcg(g, op, b, rtol, fixed=None):
+    P = solve.BlockJacobi(op)
+    return pcg.pcg(op.apply, P.apply, b, rtol=rtol, norm=solve.transformed_norm(g, op.skel),
+                   fixed_iters=fixed)
+
+
+@pytest.mark.parametrize("which", ["cfg1", "cfg2"])
+def test_pcg_parity_manufactured(which):
+    """BASELINE configs[0] / configs[1]: BT-PCG to 1e-10 vs the oracle's block-Jacobi PCG."""
+    g = cfg1() if which == "cfg1" else cfg2()
+    X, Y, Z = mesh.lattice_coordinates(g)
+    f = sine_f(X, Y, Z, g.lam)
+    op = operator.AssembledCondensedOperator(g)
+    b = solve.condensed_rhs(op, f)
+    res = _oracle_pcg(g, op, b, 1e-10)
+    ctx = ctx_for(g)
+    f_d = torch.from_numpy(f).cuda()
+    bt = ctx.skeleton()
+    ctx.sc_condense_rhs(f_d, bt)
+    xt = ctx.skeleton()
+    rep = ctx.sc_pcg_solve(bt, xt, rtol=1e-10, maxit=1000)
+    assert rep.converged and abs(rep.iters - res.iters) <= 1, (rep.iters, res.iters)
+    assert rep.relres <= 1e-10
+    x_gpu = ctx.to_lattice_nodal(xt).cpu().numpy()
+    ref = res.x if rep.iters == res.iters else _oracle_pcg(g, op, b, 0, fixed=rep.iters).x
+    assert rel(x_gpu, ref) <= 1e-10
+    u = ctx.lattice()
+    ctx.sc_recover(f_d, xt, u)
+    err = np.abs(u.cpu().numpy() - sine_u(X, Y, Z)).max()
+    assert err < (1e-4 if which == "cfg1" else 1e-9), err
+
+
+def test_pcg_parity_random_rhs_nonuniform():
+    from paper_1601_08179_b200 import SC_DUAL
+    g = nonuniform(4, (3, 3, 2), 0.0, seed=9)
+    op = operator.AssembledCondensedOperator(g)
+    ctx = ctx_for(g)
+    bt = ctx.skeleton()
+    ctx.sc_fill_random(5, bt)
+    lat = ctx.lattice()
+    ctx.sc_from_transformed(bt, lat, SC_DUAL)
+    b = lat.cpu().numpy()
+    res = _oracle_pcg(g, op, b, 1e-10)
+    xt = ctx.skeleton()
+    rep = ctx.sc_pcg_solve(bt, xt, rtol=1e-10, maxit=2000)
+    assert rep.converged and abs(rep.iters - res.iters) <= 1
+    ref = res.x if rep.iters == res.iters else _oracle_pcg(g, op, b, 0, fixed=rep.iters).x
+    assert rel(ctx.to_lattice_nodal(xt).cpu().numpy(), ref) <= 1e-10
+
+
+def test_pcg_fixed_iterations_and_zero_rhs():
+    g = small_grid(3, (2, 2, 2), 1.0)
+    ctx = ctx_for(g)
+    b = ctx.skeleton()
+    x = ctx.skeleton(fill=1.0)
+    rep = ctx.sc_pcg_solve(b, x, rtol=1e-10, maxit=50)
+    assert rep.iters == 0 and rep.converged and float(x.abs().max()) == 0.0
+    ctx.sc_fill_random(1, b)
+    rep = ctx.sc_pcg_solve(b, x, rtol=0.0, maxit=7)
+    assert rep.iters == 7 and not rep.converged
+
+
+def test_spectral_convergence_gpu():
+    errs = []
+    for p in (2, 3, 4, 5, 6, 7):
+        g = small_grid(p, (2, 2, 2), 1.0)
+        X, Y, Z = mesh.lattice_coordinates(g)
+        f = torch.from_numpy(sine_f(X, Y, Z, 1.0)).cuda()
+        ctx = ctx_for(g)
+        bt, xt, u = ctx.skeleton(), ctx.skeleton(), ctx.lattice()
+        ctx.sc_condense_rhs(f, bt)
+        rep = ctx.sc_pcg_solve(bt, xt, rtol=1e-13, maxit=1000)
+        assert rep.converged
+        ctx.sc_recover(f, xt, u)
+        errs.append(np.abs(u.cpu().numpy() - sine_u(X, Y, Z)).max())
+    errs = np.array(errs)
+    assert np.all(errs[1:] < errs[:-1] / 10.0), errs
