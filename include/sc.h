@@ -130,6 +130,23 @@ sc_status sc_apply_condensed(sc_ctx* ctx, const double* d_x, double* d_y, void* 
 sc_status sc_pcg_solve(sc_ctx* ctx, const double* d_b, double* d_x, double rtol, int maxit,
                        sc_pcg_report* rep, void* stream);
 
+/* Split form of sc_pcg_solve for fixed-iteration runs (benchmarks, checkpointing):
+ * sc_pcg_start initialises r = b, x = 0, p = Pinv r and the device scalars (rtol / maxit
+ * as in sc_pcg_solve); sc_pcg_iterate enqueues `niter` further iterations without any
+ * host synchronisation (iterations after convergence are no-ops on the device);
+ * sc_pcg_status synchronises the stream and fills `rep`.  d_x must stay valid between
+ * the calls. */
+sc_status sc_pcg_start(sc_ctx* ctx, const double* d_b, double* d_x, double rtol, int maxit, void* stream);
+sc_status sc_pcg_iterate(sc_ctx* ctx, int niter, void* stream);
+sc_status sc_pcg_status(sc_ctx* ctx, sc_pcg_report* rep, void* stream);
+
+/* Kernel timing of the condensed-operator kernel with CUDA events recorded on the launch
+ * stream around every launch while enabled (at most 8192 launches are recorded).
+ * sc_profile_read synchronises the device and returns the summed duration in ms and the
+ * number of launches since the last enable, then clears the record. */
+sc_status sc_profile_enable(sc_ctx* ctx, int on);
+sc_status sc_profile_read(sc_ctx* ctx, double* h_total_ms, long long* h_count);
+
 /* Same as sc_pcg_solve, but h_b / h_x are HOST buffers (pinned for best speed); the
  * host->device and device->host copies happen inside the call, on `stream`, using the
  * workspace.  For end-to-end timing through the public API. */

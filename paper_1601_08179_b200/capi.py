@@ -52,6 +52,11 @@ SIGNATURES = {
     "sc_pcg_solve": ([_P, _P, _P, ctypes.c_double, ctypes.c_int, ctypes.POINTER(ScPcgReport), _P], ctypes.c_int),
     "sc_pcg_solve_host": ([_P, _P, _P, ctypes.c_double, ctypes.c_int, ctypes.POINTER(ScPcgReport), _P],
                           ctypes.c_int),
+    "sc_pcg_start": ([_P, _P, _P, ctypes.c_double, ctypes.c_int, _P], ctypes.c_int),
+    "sc_pcg_iterate": ([_P, ctypes.c_int, _P], ctypes.c_int),
+    "sc_pcg_status": ([_P, ctypes.POINTER(ScPcgReport), _P], ctypes.c_int),
+    "sc_profile_enable": ([_P, ctypes.c_int], ctypes.c_int),
+    "sc_profile_read": ([_P, _D, ctypes.POINTER(ctypes.c_longlong)], ctypes.c_int),
     "sc_condense_rhs": ([_P, _P, _P, _P], ctypes.c_int),
     "sc_recover": ([_P, _P, _P, _P, _P], ctypes.c_int),
     "sc_to_transformed": ([_P, _P, _P, ctypes.c_int, _P], ctypes.c_int),

@@ -78,6 +78,11 @@ struct sc_ctx {
   OwnMask own;
   ncclComm_t comm = nullptr;
   long long nlaunch = 0;
+  double* x_cur = nullptr;              // PCG iterate between sc_pcg_start / sc_pcg_iterate
+  double tol2 = -1.0;
+  bool prof_on = false;
+  std::vector<cudaEvent_t> prof_ev;     // pairs (start, stop)
+  int prof_n = 0;
   std::string err;
   bool broken = false;
 };
@@ -284,6 +289,7 @@ extern "C" sc_status sc_destroy(sc_ctx* ctx) {
   if (ctx->d_tab) cudaFree(ctx->d_tab);
   if (ctx->d_h) cudaFree(ctx->d_h);
   if (ctx->d_dinv) cudaFree(ctx->d_dinv);
+  for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);
   delete ctx;
   return SC_OK;
 }
@@ -400,7 +406,10 @@ static sc_status allreduce_scal(sc_ctx* ctx, int slot, int n, cudaStream_t st) {
 }
 
 static sc_status apply_impl(sc_ctx* ctx, const double* x, double* y, const double* done, cudaStream_t st) {
-  LAUNCH(launch_apply(ctx->g, x, y, done, st, &nl_));
+  const bool rec = ctx->prof_on && ctx->prof_n < (int)ctx->prof_ev.size() / 2;
+  cudaEvent_t* ev = rec ? &ctx->prof_ev[2 * ctx->prof_n] : nullptr;
+  LAUNCH(launch_apply(ctx->g, x, y, done, st, &nl_, ev));
+  if (rec) ctx->prof_n++;
   return halo_sum(ctx, y, st);
 }
 
@@ -410,30 +419,62 @@ extern "C" sc_status sc_apply_condensed(sc_ctx* ctx, const double* d_x, double* 
   return apply_impl(ctx, d_x, d_y, nullptr, (cudaStream_t)stream);
 }
 
-static sc_status pcg_impl(sc_ctx* ctx, const double* b, double* x, double rtol, int maxit, sc_pcg_report* rep,
-                          cudaStream_t st) {
-  auto t0 = std::chrono::steady_clock::now();
+static sc_status pcg_start_impl(sc_ctx* ctx, const double* b, double* x, double rtol, int maxit, cudaStream_t st) {
   const long long n = ctx->g.n_total;
-  double* done = ctx->scal + SCAL_DONE;
-  const double tol2 = rtol > 0 ? rtol * rtol : -1.0;
+  ctx->tol2 = rtol > 0 ? rtol * rtol : -1.0;
+  ctx->x_cur = x;
   LAUNCH(launch_pcg_init(b, ctx->pinv, x, ctx->r, ctx->pv, n, ctx->own, ctx->partials, st, &nl_));
   LAUNCH(launch_reduce2(ctx->partials, ctx->scal, SCAL_RED0, 2, nullptr, st, &nl_));
   sc_status s = allreduce_scal(ctx, SCAL_RED0, 2, st);
   if (s) return s;
-  LAUNCH(launch_pcg_init_finalize(ctx->scal, ctx->partials, tol2, maxit, st, &nl_));
+  LAUNCH(launch_pcg_init_finalize(ctx->scal, ctx->partials, ctx->tol2, maxit, st, &nl_));
+  return SC_OK;
+}
+
+// One BT-PCG iteration (rows a3-a10): q = A p; alpha = rz / p.q; x += alpha p; r -= alpha q;
+// z = Pinv r; beta = r.z / rz_old; p = z + beta p.  Scalars stay on the device.
+static sc_status pcg_iteration(sc_ctx* ctx, cudaStream_t st) {
+  const long long n = ctx->g.n_total;
+  double* done = ctx->scal + SCAL_DONE;
+  double* x = ctx->x_cur;
+  sc_status s = apply_impl(ctx, ctx->pv, ctx->q, done, st);
+  if (s) return s;
+  LAUNCH(launch_dot_partial(ctx->pv, ctx->q, n, ctx->own, ctx->partials, done, st, &nl_));
+  LAUNCH(launch_reduce2(ctx->partials, ctx->scal, SCAL_RED0, 1, done, st, &nl_));
+  if ((s = allreduce_scal(ctx, SCAL_RED0, 1, st))) return s;
+  LAUNCH(launch_pcg_alpha(ctx->scal, st, &nl_));
+  LAUNCH(launch_pcg_update(x, ctx->r, ctx->pv, ctx->q, ctx->pinv, n, ctx->own, ctx->scal, ctx->partials, st, &nl_));
+  LAUNCH(launch_reduce2(ctx->partials, ctx->scal, SCAL_RED0, 2, done, st, &nl_));
+  if ((s = allreduce_scal(ctx, SCAL_RED0, 2, st))) return s;
+  LAUNCH(launch_pcg_beta(ctx->scal, st, &nl_));
+  LAUNCH(launch_pcg_direction(ctx->pv, ctx->r, ctx->pinv, n, ctx->scal, st, &nl_));
+  return SC_OK;
+}
+
+static sc_status pcg_report_impl(sc_ctx* ctx, sc_pcg_report* rep, cudaStream_t st, double t_s) {
+  double sc[SCAL_COUNT];
+  CK(cudaMemcpyAsync(sc, ctx->scal, sizeof(sc), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (rep) {
+    rep->iters = (int)sc[SCAL_ITERS];
+    rep->r0norm = std::sqrt(sc[SCAL_RR0]);
+    rep->relres = sc[SCAL_RR0] > 0 ? std::sqrt(sc[SCAL_RR] / sc[SCAL_RR0]) : 0.0;
+    rep->converged = (sc[SCAL_RR0] == 0.0) || (ctx->tol2 > 0 && sc[SCAL_RR] <= ctx->tol2 * sc[SCAL_RR0]);
+    rep->t_solve_s = t_s;
+  }
+  if (sc[SCAL_BREAK] != 0.0) { ctx->err = "PCG breakdown: p^T A p <= 0"; return SC_EBREAKDOWN; }
+  return SC_OK;
+}
+
+static sc_status pcg_impl(sc_ctx* ctx, const double* b, double* x, double rtol, int maxit, sc_pcg_report* rep,
+                          cudaStream_t st) {
+  auto t0 = std::chrono::steady_clock::now();
+  double* done = ctx->scal + SCAL_DONE;
+  sc_status s = pcg_start_impl(ctx, b, x, rtol, maxit, st);
+  if (s) return s;
   const int check_every = rtol > 0 ? 8 : 0;
   for (int it = 0; it < maxit; ++it) {
-    s = apply_impl(ctx, ctx->pv, ctx->q, done, st);
-    if (s) return s;
-    LAUNCH(launch_dot_partial(ctx->pv, ctx->q, n, ctx->own, ctx->partials, done, st, &nl_));
-    LAUNCH(launch_reduce2(ctx->partials, ctx->scal, SCAL_RED0, 1, done, st, &nl_));
-    if ((s = allreduce_scal(ctx, SCAL_RED0, 1, st))) return s;
-    LAUNCH(launch_pcg_alpha(ctx->scal, st, &nl_));
-    LAUNCH(launch_pcg_update(x, ctx->r, ctx->pv, ctx->q, ctx->pinv, n, ctx->own, ctx->scal, ctx->partials, st, &nl_));
-    LAUNCH(launch_reduce2(ctx->partials, ctx->scal, SCAL_RED0, 2, done, st, &nl_));
-    if ((s = allreduce_scal(ctx, SCAL_RED0, 2, st))) return s;
-    LAUNCH(launch_pcg_beta(ctx->scal, st, &nl_));
-    LAUNCH(launch_pcg_direction(ctx->pv, ctx->r, ctx->pinv, n, ctx->scal, st, &nl_));
+    if ((s = pcg_iteration(ctx, st))) return s;
     if (check_every && (it + 1) % check_every == 0) {
       double dflag = 0;
       CK(cudaMemcpyAsync(&dflag, done, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -441,18 +482,59 @@ static sc_status pcg_impl(sc_ctx* ctx, const double* b, double* x, double rtol, 
       if (dflag != 0.0) break;
     }
   }
-  double sc[SCAL_COUNT];
-  CK(cudaMemcpyAsync(sc, ctx->scal, sizeof(sc), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   auto t1 = std::chrono::steady_clock::now();
-  if (rep) {
-    rep->iters = (int)sc[SCAL_ITERS];
-    rep->r0norm = std::sqrt(sc[SCAL_RR0]);
-    rep->relres = sc[SCAL_RR0] > 0 ? std::sqrt(sc[SCAL_RR] / sc[SCAL_RR0]) : 0.0;
-    rep->converged = (sc[SCAL_RR0] == 0.0) || (tol2 > 0 && sc[SCAL_RR] <= tol2 * sc[SCAL_RR0]);
-    rep->t_solve_s = std::chrono::duration<double>(t1 - t0).count();
+  return pcg_report_impl(ctx, rep, st, std::chrono::duration<double>(t1 - t0).count());
+}
+
+extern "C" sc_status sc_pcg_start(sc_ctx* ctx, const double* d_b, double* d_x, double rtol, int maxit, void* stream) {
+  if (!ctx || !d_b || !d_x || d_b == d_x || maxit < 0 || !std::isfinite(rtol)) return SC_EINVAL;
+  if (ctx->broken) return SC_ESTATE;
+  if (!ctx->ws) { ctx->err = "workspace not bound"; return SC_ESTATE; }
+  return pcg_start_impl(ctx, d_b, d_x, rtol, maxit, (cudaStream_t)stream);
+}
+
+extern "C" sc_status sc_pcg_iterate(sc_ctx* ctx, int niter, void* stream) {
+  if (!ctx || niter < 0) return SC_EINVAL;
+  if (ctx->broken) return SC_ESTATE;
+  if (!ctx->x_cur) { ctx->err = "sc_pcg_start not called"; return SC_ESTATE; }
+  for (int it = 0; it < niter; ++it) {
+    sc_status s = pcg_iteration(ctx, (cudaStream_t)stream);
+    if (s) return s;
   }
-  if (sc[SCAL_BREAK] != 0.0) { ctx->err = "PCG breakdown: p^T A p <= 0"; return SC_EBREAKDOWN; }
+  return SC_OK;
+}
+
+extern "C" sc_status sc_pcg_status(sc_ctx* ctx, sc_pcg_report* rep, void* stream) {
+  if (!ctx || !rep) return SC_EINVAL;
+  if (ctx->broken) return SC_ESTATE;
+  if (!ctx->x_cur) { ctx->err = "sc_pcg_start not called"; return SC_ESTATE; }
+  return pcg_report_impl(ctx, rep, (cudaStream_t)stream, 0.0);
+}
+
+extern "C" sc_status sc_profile_enable(sc_ctx* ctx, int on) {
+  if (!ctx) return SC_EINVAL;
+  if (on && ctx->prof_ev.empty()) {
+    ctx->prof_ev.resize(2 * 8192);
+    for (auto& e : ctx->prof_ev) CK(cudaEventCreate(&e));
+  }
+  ctx->prof_on = on != 0;
+  ctx->prof_n = 0;
+  return SC_OK;
+}
+
+extern "C" sc_status sc_profile_read(sc_ctx* ctx, double* h_total_ms, long long* h_count) {
+  if (!ctx || !h_total_ms || !h_count) return SC_EINVAL;
+  double tot = 0.0;
+  for (int i = 0; i < ctx->prof_n; ++i) {
+    CK(cudaEventSynchronize(ctx->prof_ev[2 * i + 1]));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->prof_ev[2 * i], ctx->prof_ev[2 * i + 1]));
+    tot += ms;
+  }
+  *h_total_ms = tot;
+  *h_count = ctx->prof_n;
+  ctx->prof_n = 0;
   return SC_OK;
 }
 

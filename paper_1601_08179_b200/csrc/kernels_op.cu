@@ -214,10 +214,12 @@ static size_t apply_smem_bytes(int ni) {
   return sizeof(double) * (size_t)(nsh + 6 * n2 + 3 * ni + kc * n2);
 }
 
-int launch_apply(const Geom& g, const double* x, double* y, const double* done, void* stream, int* nl) {
+int launch_apply(const Geom& g, const double* x, double* y, const double* done, void* stream, int* nl, void* events) {
   cudaStream_t st = (cudaStream_t)stream;
+  cudaEvent_t* ev = (cudaEvent_t*)events;
   cudaError_t err = cudaMemsetAsync(y, 0, sizeof(double) * g.n_total, st);
   if (err != cudaSuccess) return err;
+  if (ev) cudaEventRecord(ev[0], st);
   long long ne = (long long)g.nx * g.ny * g.nz;
   if (ne == 0) return cudaSuccess;
   size_t smem = apply_smem_bytes(g.ni);
@@ -228,6 +230,7 @@ int launch_apply(const Geom& g, const double* x, double* y, const double* done, 
   }
   k_apply_v1<<<(unsigned)ne, 256, smem, st>>>(g, x, y, done);
   (*nl)++;
+  if (ev) cudaEventRecord(ev[1], st);
   return cudaGetLastError();
 }
 

@@ -67,7 +67,8 @@ enum {
 #define SC_RED_BLOCKS 1184   // fixed grid of the deterministic 2-stage reductions (8 x 148)
 
 // ---- kernel launchers (kernels_*.cu); all return cudaError_t as int ----
-int launch_apply(const Geom& g, const double* x, double* y, const double* done, void* stream, int* nlaunch);
+int launch_apply(const Geom& g, const double* x, double* y, const double* done, void* stream, int* nlaunch,
+                 void* events = nullptr);
 int launch_diag(const Geom& g, double* diag, void* stream, int* nlaunch);
 int launch_invert_diag(const Geom& g, double* diag, void* stream, int* nlaunch);
 int launch_convert(const Geom& g, const double* in, double* out, int to_skel, int mat, void* stream, int* nlaunch);

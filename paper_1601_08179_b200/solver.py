@@ -96,6 +96,29 @@ class Context:
         _check(self.lib, self.ctx, "sc_pcg_solve_host", st)
         return rep
 
+    def sc_pcg_start(self, b, x, rtol=0.0, maxit=1 << 30, stream=None):
+        _check(self.lib, self.ctx, "sc_pcg_start",
+               self.lib.sc_pcg_start(self.ctx, ptr(b), ptr(x), float(rtol), int(maxit), self._s(stream)))
+
+    def sc_pcg_iterate(self, niter, stream=None):
+        _check(self.lib, self.ctx, "sc_pcg_iterate", self.lib.sc_pcg_iterate(self.ctx, int(niter), self._s(stream)))
+
+    def sc_pcg_status(self, stream=None):
+        rep = ScPcgReport()
+        _check(self.lib, self.ctx, "sc_pcg_status", self.lib.sc_pcg_status(self.ctx, ctypes.byref(rep),
+                                                                            self._s(stream)))
+        return rep
+
+    def sc_profile_enable(self, on=True):
+        _check(self.lib, self.ctx, "sc_profile_enable", self.lib.sc_profile_enable(self.ctx, int(bool(on))))
+
+    def sc_profile_read(self):
+        ms = ctypes.c_double()
+        n = ctypes.c_longlong()
+        _check(self.lib, self.ctx, "sc_profile_read", self.lib.sc_profile_read(self.ctx, ctypes.byref(ms),
+                                                                                ctypes.byref(n)))
+        return ms.value, n.value
+
     def sc_condense_rhs(self, f, b, stream=None):
         _check(self.lib, self.ctx, "sc_condense_rhs",
                self.lib.sc_condense_rhs(self.ctx, ptr(f), ptr(b), self._s(stream)))
