@@ -67,6 +67,12 @@ struct sc_ctx {
   double* d_tab = nullptr;              // 1-D tables
   double* d_h = nullptr;                // local widths hx | hy | hz
   double* d_dinv = nullptr;             // uniform D^{-1} table
+  // v2 tile-column operator state (kernels_col.cu)
+  bool use_col = false;
+  int col_ntx = 0, col_nty = 0;
+  void* d_colstate = nullptr;
+  int* d_flags = nullptr;
+  double* d_corner = nullptr;
   // workspace (caller-owned)
   double* ws = nullptr;
   size_t ws_bytes = 0;
@@ -259,6 +265,27 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
       return fail("cudaMemcpy dinv");
     g.dinv = ctx->d_dinv;
   }
+  // ---- v2 tile-column operator (n_I <= 8): tile grid, look-back flags, corner records
+  {
+    const char* env = getenv("SC_APPLY_V1");
+    bool sig_ok = true;
+    for (int m = 0; m < ni; ++m) sig_ok &= (B.sigma[m] == ((m & 1) ? -1 : 1));
+    if (col_supported(ni) && sig_ok && !(env && env[0] == '1')) {
+      int tx, ty;
+      col_tile(ni, &tx, &ty);
+      ctx->col_ntx = (nx + tx - 1) / tx;
+      ctx->col_nty = (ny + ty - 1) / ty;
+      size_t nflags = (size_t)ctx->col_ntx * ctx->col_nty * (nz + 1);
+      size_t ncorner = (size_t)(ctx->col_ntx + 1) * (ctx->col_nty + 1) * (nz + 1) * 3 * (ni + 1);
+      if (cudaMalloc(&ctx->d_colstate, 64) != cudaSuccess) return fail("cudaMalloc colstate");
+      if (cudaMalloc(&ctx->d_flags, sizeof(int) * nflags) != cudaSuccess) return fail("cudaMalloc flags");
+      if (cudaMalloc(&ctx->d_corner, sizeof(double) * ncorner) != cudaSuccess) return fail("cudaMalloc corner");
+      if (cudaMemset(ctx->d_colstate, 0, 64) != cudaSuccess) return fail("memset colstate");
+      if (cudaMemset(ctx->d_flags, 0, sizeof(int) * nflags) != cudaSuccess) return fail("memset flags");
+      if (cudaMemset(ctx->d_corner, 0, sizeof(double) * ncorner) != cudaSuccess) return fail("memset corner");
+      ctx->use_col = true;
+    }
+  }
   // ---- interface planes (z-face plane, x-edges, y-edges, vertices at fz = 0 / nz)
   long long lens[4] = {(long long)nx * ny * n2, (long long)nx * (ny + 1) * ni, (long long)(nx + 1) * ny * ni,
                        (long long)(nx + 1) * (ny + 1)};
@@ -289,6 +316,9 @@ extern "C" sc_status sc_destroy(sc_ctx* ctx) {
   if (ctx->d_tab) cudaFree(ctx->d_tab);
   if (ctx->d_h) cudaFree(ctx->d_h);
   if (ctx->d_dinv) cudaFree(ctx->d_dinv);
+  if (ctx->d_colstate) cudaFree(ctx->d_colstate);
+  if (ctx->d_flags) cudaFree(ctx->d_flags);
+  if (ctx->d_corner) cudaFree(ctx->d_corner);
   for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);
   delete ctx;
   return SC_OK;
@@ -408,7 +438,11 @@ static sc_status allreduce_scal(sc_ctx* ctx, int slot, int n, cudaStream_t st) {
 static sc_status apply_impl(sc_ctx* ctx, const double* x, double* y, const double* done, cudaStream_t st) {
   const bool rec = ctx->prof_on && ctx->prof_n < (int)ctx->prof_ev.size() / 2;
   cudaEvent_t* ev = rec ? &ctx->prof_ev[2 * ctx->prof_n] : nullptr;
-  LAUNCH(launch_apply(ctx->g, x, y, done, st, &nl_, ev));
+  if (ctx->use_col)
+    LAUNCH(launch_apply_col_raw(ctx->g, x, y, done, ctx->d_colstate, ctx->d_flags, ctx->d_corner, ctx->col_ntx,
+                                ctx->col_nty, st, &nl_, ev));
+  else
+    LAUNCH(launch_apply(ctx->g, x, y, done, st, &nl_, ev));
   if (rec) ctx->prof_n++;
   return halo_sum(ctx, y, st);
 }
