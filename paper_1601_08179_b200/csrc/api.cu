@@ -73,6 +73,7 @@ struct sc_ctx {
   void* d_colstate = nullptr;
   int* d_flags = nullptr;
   double* d_corner = nullptr;
+  double* d_pending = nullptr;
   // workspace (caller-owned)
   double* ws = nullptr;
   size_t ws_bytes = 0;
@@ -271,8 +272,8 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
     bool sig_ok = true;
     for (int m = 0; m < ni; ++m) sig_ok &= (B.sigma[m] == ((m & 1) ? -1 : 1));
     if (col_supported(ni) && sig_ok && !(env && env[0] == '1')) {
-      int tx, ty;
-      col_tile(ni, &tx, &ty);
+      int tx, ty, pend;
+      col_tile(ni, &tx, &ty, &pend);
       ctx->col_ntx = (nx + tx - 1) / tx;
       ctx->col_nty = (ny + ty - 1) / ty;
       size_t nflags = (size_t)ctx->col_ntx * ctx->col_nty * (nz + 1);
@@ -280,6 +281,8 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
       if (cudaMalloc(&ctx->d_colstate, 64) != cudaSuccess) return fail("cudaMalloc colstate");
       if (cudaMalloc(&ctx->d_flags, sizeof(int) * nflags) != cudaSuccess) return fail("cudaMalloc flags");
       if (cudaMalloc(&ctx->d_corner, sizeof(double) * ncorner) != cudaSuccess) return fail("cudaMalloc corner");
+      size_t npend = (size_t)ctx->col_ntx * ctx->col_nty * 2 * pend;
+      if (cudaMalloc(&ctx->d_pending, sizeof(double) * npend) != cudaSuccess) return fail("cudaMalloc pending");
       if (cudaMemset(ctx->d_colstate, 0, 64) != cudaSuccess) return fail("memset colstate");
       if (cudaMemset(ctx->d_flags, 0, sizeof(int) * nflags) != cudaSuccess) return fail("memset flags");
       if (cudaMemset(ctx->d_corner, 0, sizeof(double) * ncorner) != cudaSuccess) return fail("memset corner");
@@ -319,6 +322,7 @@ extern "C" sc_status sc_destroy(sc_ctx* ctx) {
   if (ctx->d_colstate) cudaFree(ctx->d_colstate);
   if (ctx->d_flags) cudaFree(ctx->d_flags);
   if (ctx->d_corner) cudaFree(ctx->d_corner);
+  if (ctx->d_pending) cudaFree(ctx->d_pending);
   for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);
   delete ctx;
   return SC_OK;
@@ -439,7 +443,8 @@ static sc_status apply_impl(sc_ctx* ctx, const double* x, double* y, const doubl
   const bool rec = ctx->prof_on && ctx->prof_n < (int)ctx->prof_ev.size() / 2;
   cudaEvent_t* ev = rec ? &ctx->prof_ev[2 * ctx->prof_n] : nullptr;
   if (ctx->use_col)
-    LAUNCH(launch_apply_col_raw(ctx->g, x, y, done, ctx->d_colstate, ctx->d_flags, ctx->d_corner, ctx->col_ntx,
+    LAUNCH(launch_apply_col_raw(ctx->g, x, y, done, ctx->d_colstate, ctx->d_flags, ctx->d_corner, ctx->d_pending,
+                                ctx->col_ntx,
                                 ctx->col_nty, st, &nl_, ev));
   else
     LAUNCH(launch_apply(ctx->g, x, y, done, st, &nl_, ev));

@@ -43,16 +43,19 @@ struct ColParams {
   ColState* st;
   int* flags;            // [nitems][nz+1]
   double* corner;        // [(nty+1)][(ntx+1)][nz+1][3][NI+1]
+  double* pending;       // [nitems][2][PEND]
   int ntx, nty, nitems;
 };
 
 template <int NI>
 struct CS {
   static constexpr int N2 = NI * NI;
-  static constexpr int LPE = NI <= 1 ? 1 : (NI <= 2 ? 2 : (NI <= 4 ? 4 : 8));
-  static constexpr int NT = 128;
-  static constexpr int NE = NT / LPE;
-  static constexpr int TX = NE == 128 ? 16 : (NE >= 32 ? 8 : 4);
+  static constexpr int LPE = NI <= 1 ? 1 : (NI <= 2 ? 2 : (NI <= 4 ? 4 : 8));   // k lanes per element
+  static constexpr int JS = NI >= 2 ? 2 : 1;                                     // j-splits per k-plane
+  static constexpr int JH = (NI + JS - 1) / JS;                                  // j rows per thread (j = JS jj + jh)
+  static constexpr int NT = 256;
+  static constexpr int NE = NT / (LPE * JS);
+  static constexpr int TX = NE >= 256 ? 16 : (NE >= 32 ? 8 : 4);
   static constexpr int TY = NE / TX;
   static constexpr int XF = TY * (TX + 1) * N2;
   static constexpr int YF = (TY + 1) * TX * N2;
@@ -64,17 +67,39 @@ struct CS {
   static constexpr int PVV = (TY + 1) * (TX + 1);
   static constexpr int PLANE = PZF + PXE + PYE + PVV;
   static constexpr int QZ = NE * 2 * N2;
+  // even/odd reduction buffers (aliased with QZ: used after the z outputs are consumed)
+  static constexpr int R_XJ = 0;                                   // x-faces over j: [TY][TX+1][2][NI]
+  static constexpr int R_XK = R_XJ + TY * (TX + 1) * 2 * NI;       // x-faces over k
+  static constexpr int R_YI = R_XK + TY * (TX + 1) * 2 * NI;       // y-faces over i: [TY+1][TX][2][NI]
+  static constexpr int R_YK = R_YI + (TY + 1) * TX * 2 * NI;       // y-faces over k
+  static constexpr int R_ZI = R_YK + (TY + 1) * TX * 2 * NI;       // z-faces over i: [2][TY][TX][2][NI]
+  static constexpr int R_ZJ = R_ZI + 2 * TY * TX * 2 * NI;         // z-faces over j
+  static constexpr int R_ZE = R_ZJ + 2 * TY * TX * 2 * NI;         // z-edges: [TY+1][TX+1][2]
+  static constexpr int R_XE = R_ZE + (TY + 1) * (TX + 1) * 2;      // x-edges: [2][TY+1][TX][2]
+  static constexpr int R_YE = R_XE + 2 * (TY + 1) * TX * 2;        // y-edges: [2][TY][TX+1][2]
+  static constexpr int RED = R_YE + 2 * TY * (TX + 1) * 2;
+  static constexpr int RQ = QZ > RED ? QZ : RED;
   static constexpr int DINV = NI * NI * NI;
-  static constexpr int O_IS = 0;
-  static constexpr int O_IP = O_IS + SIDE;
-  static constexpr int O_AS = O_IP + 2 * PLANE;
-  static constexpr int O_AP = O_AS + SIDE;
-  static constexpr int O_QZ = O_AP + 2 * PLANE;
-  static constexpr int O_DINV = O_QZ + QZ;
+  static constexpr int O_IS = 0;                     // 2 side input buffers
+  static constexpr int O_IP = O_IS + 2 * SIDE;       // 2 plane input buffers
+  static constexpr int O_AS = O_IP + 2 * PLANE;      // side accumulator
+  static constexpr int O_AP = O_AS + SIDE;           // 2 plane accumulators
+  static constexpr int O_RQ = O_AP + 2 * PLANE;      // QZ staging / reduction buffers
+  static constexpr int O_DINV = O_RQ + RQ;
   static constexpr int O_D = O_DINV + DINV;          // per-element d: NE x 4
   static constexpr int O_TAB = O_D + 4 * NE;         // a0, ap, lam (3 x 32)
   static constexpr int TOTAL = O_TAB + 3 * 32;
   static constexpr int NSH = 6 * N2 + 12 * NI + 8;   // element shell nodes
+  // parked own partials of the W / S boundary entities (global, per tile, 2 step slots)
+  static constexpr int PD_XF = 0;                                  // W column x-faces  [TY][N2]
+  static constexpr int PD_YF = PD_XF + TY * N2;                    // S row y-faces     [TX N2]
+  static constexpr int PD_XE = PD_YF + TX * N2;                    // S row x-edges     [TX NI]
+  static constexpr int PD_YE = PD_XE + TX * NI;                    // W column y-edges  [TY][NI]
+  static constexpr int PD_ZEW = PD_YE + TY * NI;                   // W column z-edges  [TY+1][NI]
+  static constexpr int PD_ZES = PD_ZEW + (TY + 1) * NI;            // S row z-edges     [TX NI]
+  static constexpr int PD_VW = PD_ZES + TX * NI;                   // W column vertices [TY+1]
+  static constexpr int PD_VS = PD_VW + TY + 1;                     // S row vertices    [TX]
+  static constexpr int PEND = PD_VS + TX;
   // sub-array offsets inside a side / plane block
   static constexpr int S_XF = 0, S_YF = XF, S_ZE = XF + YF;
   static constexpr int P_ZF = 0, P_XE = PZF, P_YE = PZF + PXE, P_VV = PZF + PXE + PYE;
@@ -98,6 +123,14 @@ struct Plane {
 };
 
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 __device__ __forceinline__ void flag_release(int* f, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
@@ -134,234 +167,222 @@ struct Addr {
   }
 };
 
-// Load one z-plane (fz) of the tile into smem (Dirichlet entities read as 0).
+// Row-contiguous async loads of one z-plane (fz) / one element layer (ez) of the tile into
+// shared memory.  Every tile row of an entity class is one contiguous range in both the
+// skeleton vector and the smem buffer; a warp copies a row with 8-byte cp.async (Dirichlet
+// entities, which sit at the two ends of a row or fill a whole row, are written as 0).
 template <int NI>
 __device__ void load_plane(const ColParams& P, Plane<NI> pl, int x0, int y0, int tw, int th, int fz) {
   using C = CS<NI>;
+  constexpr int N2 = C::N2, NW = C::NT / 32;
   const Geom& g = P.g;
   Addr A{g};
   const bool zd = zdir(g, fz);
-  const int tid = threadIdx.x;
-  // z-faces: TY rows x TX faces (contiguous tw*N2 per row)
-  for (int t = tid; t < C::TY * C::TX * C::N2; t += C::NT) {
-    int q = t % C::N2, ix = (t / C::N2) % C::TX, iy = t / (C::N2 * C::TX);
-    double v = 0.0;
-    if (ix < tw && iy < th && !zd) v = P.x[A.zf(x0 + ix, y0 + iy, fz) + q];
-    pl.zf(iy, ix)[q] = v;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int x1 = x0 + tw;
+  for (int row = warp; row < th; row += NW) {                      // z-faces
+    double* sb = pl.zf(row, 0);
+    const double* gb = P.x + A.zf(x0, y0 + row, fz);
+    for (int t = lane; t < tw * N2; t += 32) {
+      if (zd) sb[t] = 0.0; else cp_async8(sb + t, gb + t);
+    }
   }
-  for (int t = tid; t < (C::TY + 1) * C::TX * NI; t += C::NT) {   // x-edges (ex, fy)
-    int c = t % NI, ix = (t / NI) % C::TX, iy = t / (NI * C::TX);
-    int fy = y0 + iy;
-    double v = 0.0;
-    if (ix < tw && iy <= th && !zd && fy != 0 && fy != g.ny) v = P.x[A.xe(x0 + ix, fy, fz) + c];
-    pl.xe(iy, ix)[c] = v;
+  for (int row = warp; row <= th; row += NW) {                     // x-edges (ex, fy)
+    const int fy = y0 + row;
+    const bool rd = zd || fy == 0 || fy == g.ny;
+    double* sb = pl.xe(row, 0);
+    const double* gb = P.x + A.xe(x0, fy, fz);
+    for (int t = lane; t < tw * NI; t += 32) {
+      if (rd) sb[t] = 0.0; else cp_async8(sb + t, gb + t);
+    }
   }
-  for (int t = tid; t < C::TY * (C::TX + 1) * NI; t += C::NT) {   // y-edges (fx, ey)
-    int c = t % NI, ix = (t / NI) % (C::TX + 1), iy = t / (NI * (C::TX + 1));
-    int fx = x0 + ix;
-    double v = 0.0;
-    if (ix <= tw && iy < th && !zd && fx != 0 && fx != g.nx) v = P.x[A.ye(fx, y0 + iy, fz) + c];
-    pl.ye(iy, ix)[c] = v;
+  for (int row = warp; row < th; row += NW) {                      // y-edges (fx, ey)
+    double* sb = pl.ye(row, 0);
+    const double* gb = P.x + A.ye(x0, y0 + row, fz);
+    const int zlo = (x0 == 0) ? NI : 0, zhi = (x1 == g.nx) ? tw * NI : (tw + 1) * NI;
+    for (int t = lane; t < (tw + 1) * NI; t += 32) {
+      if (zd || t < zlo || t >= zhi) sb[t] = 0.0; else cp_async8(sb + t, gb + t);
+    }
   }
-  for (int t = tid; t < (C::TY + 1) * (C::TX + 1); t += C::NT) {   // vertices
-    int ix = t % (C::TX + 1), iy = t / (C::TX + 1);
-    int fx = x0 + ix, fy = y0 + iy;
-    double v = 0.0;
-    if (ix <= tw && iy <= th && !zd && fx != 0 && fx != g.nx && fy != 0 && fy != g.ny) v = P.x[A.vv(fx, fy, fz)];
-    *pl.vv(iy, ix) = v;
+  for (int row = warp; row <= th; row += NW) {                     // vertices (fx, fy)
+    const int fy = y0 + row;
+    const bool rd = zd || fy == 0 || fy == g.ny;
+    double* sb = pl.vv(row, 0);
+    const double* gb = P.x + A.vv(x0, fy, fz);
+    for (int t = lane; t <= tw; t += 32) {
+      if (rd || (t == 0 && x0 == 0) || (t == tw && x1 == g.nx)) sb[t] = 0.0; else cp_async8(sb + t, gb + t);
+    }
   }
 }
 
 template <int NI>
 __device__ void load_side(const ColParams& P, Side<NI> sd, int x0, int y0, int tw, int th, int ez) {
   using C = CS<NI>;
+  constexpr int N2 = C::N2, NW = C::NT / 32;
   const Geom& g = P.g;
   Addr A{g};
-  const int tid = threadIdx.x;
-  for (int t = tid; t < C::TY * (C::TX + 1) * C::N2; t += C::NT) {   // x-faces (fx, ey)
-    int q = t % C::N2, ix = (t / C::N2) % (C::TX + 1), iy = t / (C::N2 * (C::TX + 1));
-    int fx = x0 + ix;
-    double v = 0.0;
-    if (ix <= tw && iy < th && fx != 0 && fx != g.nx) v = P.x[A.xf(fx, y0 + iy, ez) + q];
-    sd.xf(iy, ix)[q] = v;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int x1 = x0 + tw;
+  for (int row = warp; row < th; row += NW) {                      // x-faces (fx, ey)
+    double* sb = sd.xf(row, 0);
+    const double* gb = P.x + A.xf(x0, y0 + row, ez);
+    const int zlo = (x0 == 0) ? N2 : 0, zhi = (x1 == g.nx) ? tw * N2 : (tw + 1) * N2;
+    for (int t = lane; t < (tw + 1) * N2; t += 32) {
+      if (t < zlo || t >= zhi) sb[t] = 0.0; else cp_async8(sb + t, gb + t);
+    }
   }
-  for (int t = tid; t < (C::TY + 1) * C::TX * C::N2; t += C::NT) {   // y-faces (ex, fy)
-    int q = t % C::N2, ix = (t / C::N2) % C::TX, iy = t / (C::N2 * C::TX);
-    int fy = y0 + iy;
-    double v = 0.0;
-    if (ix < tw && iy <= th && fy != 0 && fy != g.ny) v = P.x[A.yf(x0 + ix, fy, ez) + q];
-    sd.yf(iy, ix)[q] = v;
+  for (int row = warp; row <= th; row += NW) {                     // y-faces (ex, fy)
+    const int fy = y0 + row;
+    const bool rd = fy == 0 || fy == g.ny;
+    double* sb = sd.yf(row, 0);
+    const double* gb = P.x + A.yf(x0, fy, ez);
+    for (int t = lane; t < tw * N2; t += 32) {
+      if (rd) sb[t] = 0.0; else cp_async8(sb + t, gb + t);
+    }
   }
-  for (int t = tid; t < (C::TY + 1) * (C::TX + 1) * NI; t += C::NT) {   // z-edges (fx, fy)
-    int c = t % NI, ix = (t / NI) % (C::TX + 1), iy = t / (NI * (C::TX + 1));
-    int fx = x0 + ix, fy = y0 + iy;
-    double v = 0.0;
-    if (ix <= tw && iy <= th && fx != 0 && fx != g.nx && fy != 0 && fy != g.ny) v = P.x[A.ze(fx, fy, ez) + c];
-    sd.ze(iy, ix)[c] = v;
+  for (int row = warp; row <= th; row += NW) {                     // z-edges (fx, fy)
+    const int fy = y0 + row;
+    const bool rd = fy == 0 || fy == g.ny;
+    double* sb = sd.ze(row, 0);
+    const double* gb = P.x + A.ze(x0, fy, ez);
+    const int zlo = (x0 == 0) ? NI : 0, zhi = (x1 == g.nx) ? tw * NI : (tw + 1) * NI;
+    for (int t = lane; t < (tw + 1) * NI; t += 32) {
+      if (rd || t < zlo || t >= zhi) sb[t] = 0.0; else cp_async8(sb + t, gb + t);
+    }
   }
 }
 
-// Primary part (Htilde_BB) contribution of element (ix, iy) at its shell node s, accumulated
-// into the tile accumulators (arrowhead Ktilde rows: 0 = (K00, a0, K0p),
-// p = (K0p, ap, K00), interior m = (a0_m @0, Lam_m @m, ap_m @p)).
-template <int NI>
-__device__ void primary_node(int s, int ix, int iy, const double* d, Side<NI> in, Plane<NI> inb, Plane<NI> intp,
-                             Side<NI> ac, Plane<NI> acb, Plane<NI> actp, const double* a0, const double* ap,
-                             const double* lam, double K00, double K0p, double w0) {
-  using C = CS<NI>;
-  constexpr int N2 = C::N2;
-  const double w02 = w0 * w0;
-  if (s < 6 * N2) {
-    const int f = s / N2, q = s % N2, a = q % NI, b = q / NI;
-    double u, opp, diag, e1, e2;
-    double* out;
-    if (f < 2) {            // x-face: coords (a = j, b = k)
-      const int ib = f;
-      u = in.xf(iy, ix + ib)[q];
-      opp = in.xf(iy, ix + 1 - ib)[q];
-      diag = d[0] * w0 + d[1] * K00 + d[2] * w0 * lam[a] + d[3] * w0 * lam[b];
-      // d2 term: z-edges (ib, jb=0/1) along k; d3 term: y-edges (ib, kb=0/1) along j
-      e1 = d[2] * w0 * (a0[a] * in.ze(iy, ix + ib)[b] + ap[a] * in.ze(iy + 1, ix + ib)[b]);
-      e2 = d[3] * w0 * (a0[b] * inb.ye(iy, ix + ib)[a] + ap[b] * intp.ye(iy, ix + ib)[a]);
-      out = ac.xf(iy, ix + ib) + q;
-      *out += diag * u + d[1] * K0p * opp + e1 + e2;
-    } else if (f < 4) {     // y-face: coords (a = i, b = k)
-      const int jb = f - 2;
-      u = in.yf(iy + jb, ix)[q];
-      opp = in.yf(iy + 1 - jb, ix)[q];
-      diag = d[0] * w0 + d[1] * w0 * lam[a] + d[2] * K00 + d[3] * w0 * lam[b];
-      e1 = d[1] * w0 * (a0[a] * in.ze(iy + jb, ix)[b] + ap[a] * in.ze(iy + jb, ix + 1)[b]);
-      e2 = d[3] * w0 * (a0[b] * inb.xe(iy + jb, ix)[a] + ap[b] * intp.xe(iy + jb, ix)[a]);
-      out = ac.yf(iy + jb, ix) + q;
-      *out += diag * u + d[2] * K0p * opp + e1 + e2;
-    } else {                // z-face: coords (a = i, b = j)
-      const int kb = f - 4;
-      Plane<NI> pu = kb ? intp : inb, po = kb ? inb : intp;
-      u = pu.zf(iy, ix)[q];
-      opp = po.zf(iy, ix)[q];
-      diag = d[0] * w0 + d[1] * w0 * lam[a] + d[2] * w0 * lam[b] + d[3] * K00;
-      e1 = d[1] * w0 * (a0[a] * pu.ye(iy, ix)[b] + ap[a] * pu.ye(iy, ix + 1)[b]);
-      e2 = d[2] * w0 * (a0[b] * pu.xe(iy, ix)[a] + ap[b] * pu.xe(iy + 1, ix)[a]);
-      out = (kb ? actp : acb).zf(iy, ix) + q;
-      *out += diag * u + d[3] * K0p * opp + e1 + e2;
-    }
-    return;
-  }
-  s -= 6 * N2;
-  if (s < 12 * NI) {
-    const int e = s / NI, c = s % NI, grp = e >> 2, b0 = e & 1, b1 = (e >> 1) & 1;
-    if (grp == 0) {         // x-edge (jb = b0, kb = b1), coord i = c
-      const int jb = b0, kb = b1;
-      Plane<NI> pk = kb ? intp : inb;
-      const double u = pk.xe(iy + jb, ix)[c];
-      // along x: vertices (ib = 0/1, jb, kb)
-      double tx = a0[c] * *pk.vv(iy + jb, ix) + lam[c] * u + ap[c] * *pk.vv(iy + jb, ix + 1);
-      // y-line at (i = c, k = kb p): x-edges (jb'=0/1, kb) ends, z-face (kb) interior (i = c, j = a)
-      const double* fz = pk.zf(iy, ix);
-      const double* ry = jb ? ap : a0;
-      double ty = (jb ? K0p : K00) * pk.xe(iy, ix)[c] + (jb ? K00 : K0p) * pk.xe(iy + 1, ix)[c];
-#pragma unroll
-      for (int a = 0; a < NI; ++a) ty += ry[a] * fz[c + NI * a];
-      // z-line at (i = c, j = jb p): x-edges (jb, kb'=0/1) ends, y-face (jb) interior (i = c, k = a)
-      const double* fy = in.yf(iy + jb, ix);
-      const double* rz = kb ? ap : a0;
-      double tz = (kb ? K0p : K00) * inb.xe(iy + jb, ix)[c] + (kb ? K00 : K0p) * intp.xe(iy + jb, ix)[c];
-#pragma unroll
-      for (int a = 0; a < NI; ++a) tz += rz[a] * fy[c + NI * a];
-      (kb ? actp : acb).xe(iy + jb, ix)[c] += d[0] * w02 * u + d[1] * w02 * tx + d[2] * w0 * ty + d[3] * w0 * tz;
-    } else if (grp == 1) {  // y-edge (ib = b0, kb = b1), coord j = c
-      const int ib = b0, kb = b1;
-      Plane<NI> pk = kb ? intp : inb;
-      const double u = pk.ye(iy, ix + ib)[c];
-      // x-line at (j = c, k = kb p): y-edges (ib'=0/1, kb), z-face (kb) interior (i = a, j = c)
-      const double* fz = pk.zf(iy, ix);
-      const double* rx = ib ? ap : a0;
-      double tx = (ib ? K0p : K00) * pk.ye(iy, ix)[c] + (ib ? K00 : K0p) * pk.ye(iy, ix + 1)[c];
-#pragma unroll
-      for (int a = 0; a < NI; ++a) tx += rx[a] * fz[a + NI * c];
-      double ty = a0[c] * *pk.vv(iy, ix + ib) + lam[c] * u + ap[c] * *pk.vv(iy + 1, ix + ib);
-      // z-line at (i = ib p, j = c): y-edges (ib, kb'=0/1), x-face (ib) interior (j = c, k = a)
-      const double* fx = in.xf(iy, ix + ib);
-      const double* rz = kb ? ap : a0;
-      double tz = (kb ? K0p : K00) * inb.ye(iy, ix + ib)[c] + (kb ? K00 : K0p) * intp.ye(iy, ix + ib)[c];
-#pragma unroll
-      for (int a = 0; a < NI; ++a) tz += rz[a] * fx[c + NI * a];
-      (kb ? actp : acb).ye(iy, ix + ib)[c] += d[0] * w02 * u + d[1] * w0 * tx + d[2] * w02 * ty + d[3] * w0 * tz;
-    } else {                // z-edge (ib = b0, jb = b1), coord k = c
-      const int ib = b0, jb = b1;
-      const double u = in.ze(iy + jb, ix + ib)[c];
-      // x-line at (j = jb p, k = c): z-edges (ib'=0/1, jb), y-face (jb) interior (i = a, k = c)
-      const double* fy = in.yf(iy + jb, ix);
-      const double* rx = ib ? ap : a0;
-      double tx = (ib ? K0p : K00) * in.ze(iy + jb, ix)[c] + (ib ? K00 : K0p) * in.ze(iy + jb, ix + 1)[c];
-#pragma unroll
-      for (int a = 0; a < NI; ++a) tx += rx[a] * fy[a + NI * c];
-      // y-line at (i = ib p, k = c): z-edges (ib, jb'=0/1), x-face (ib) interior (j = a, k = c)
-      const double* fx = in.xf(iy, ix + ib);
-      const double* ry = jb ? ap : a0;
-      double ty = (jb ? K0p : K00) * in.ze(iy, ix + ib)[c] + (jb ? K00 : K0p) * in.ze(iy + 1, ix + ib)[c];
-#pragma unroll
-      for (int a = 0; a < NI; ++a) ty += ry[a] * fx[a + NI * c];
-      double tz = a0[c] * *inb.vv(iy + jb, ix + ib) + lam[c] * u + ap[c] * *intp.vv(iy + jb, ix + ib);
-      ac.ze(iy + jb, ix + ib)[c] += d[0] * w02 * u + d[1] * w0 * tx + d[2] * w0 * ty + d[3] * w02 * tz;
-    }
-    return;
-  }
-  s -= 12 * NI;
-  {                         // vertex (ib, jb, kb)
-    const int ib = s & 1, jb = (s >> 1) & 1, kb = (s >> 2) & 1;
-    Plane<NI> pk = kb ? intp : inb;
-    const double u = *pk.vv(iy + jb, ix + ib);
-    const double* rx = ib ? ap : a0;
-    const double* ry = jb ? ap : a0;
-    const double* rz = kb ? ap : a0;
-    double tx = (ib ? K0p : K00) * *pk.vv(iy + jb, ix) + (ib ? K00 : K0p) * *pk.vv(iy + jb, ix + 1);
-    double ty = (jb ? K0p : K00) * *pk.vv(iy, ix + ib) + (jb ? K00 : K0p) * *pk.vv(iy + 1, ix + ib);
-    double tz = (kb ? K0p : K00) * *inb.vv(iy + jb, ix + ib) + (kb ? K00 : K0p) * *intp.vv(iy + jb, ix + ib);
-    const double* ex = pk.xe(iy + jb, ix);
-    const double* ey = pk.ye(iy, ix + ib);
-    const double* ez = in.ze(iy + jb, ix + ib);
-#pragma unroll
-    for (int a = 0; a < NI; ++a) {
-      tx += rx[a] * ex[a];
-      ty += ry[a] * ey[a];
-      tz += rz[a] * ez[a];
-    }
-    *(kb ? actp : acb).vv(iy + jb, ix + ib) += d[0] * w02 * w0 * u + w02 * (d[1] * tx + d[2] * ty + d[3] * tz);
-  }
-}
-
-// ---- finalize helpers: write / publish / consume one entity vector ----------------------
 // Corner record address: corner point (cx, cy) of the tile grid, step l, slot (0 SW, 1 S, 2 W).
 __device__ __forceinline__ double* corner_rec(const ColParams& P, int cx, int cy, int l, int slot) {
   const int ni = P.g.ni;
   return P.corner + ((((long long)cy * (P.ntx + 1) + cx) * (P.g.nz + 1) + l) * 3 + slot) * (ni + 1);
 }
 
+// Even/odd partial sums of a0-weighted lines: returns (R+, R-) with
+// R+ = sum_{a even} a0_a f[a*stride], R- = sum_{a odd} a0_a f[a*stride].
+// Row 0 of Ktilde applied to the interior of a line is R+ + R-, row p is R+ - R-.
 template <int NI>
-__global__ void __launch_bounds__(128) k_apply_col(ColParams P) {
+__device__ __forceinline__ void eo_reduce(const double* f, int stride, const double* a0, double* out) {
+  double rp = 0.0, rm = 0.0;
+#pragma unroll
+  for (int a = 0; a < NI; ++a) {
+    if (a & 1) rm += a0[a] * f[a * stride];
+    else rp += a0[a] * f[a * stride];
+  }
+  out[0] = rp;
+  out[1] = rm;
+}
+
+// Row-0 / row-p application from an (R+, R-) pair: hi = 0 -> R+ + R-, hi = 1 -> R+ - R-.
+__device__ __forceinline__ double eo_row(const double* r, int hi) { return hi ? r[0] - r[1] : r[0] + r[1]; }
+
+// Deferred look-back for step ls of tile item: wait for the W, S, SW tiles' flags of step ls,
+// then write the tile's W / S boundary entities of that step as own (parked) partial + the
+// neighbours' partials (y-in-place, or the corner records on the 4-tile corner line).
+// Dirichlet entities were already written as 0.
+template <int NI>
+__device__ void finish_boundary(const ColParams& P, long long item, int ls, int x0, int y0, int tw, int th,
+                                const int* flag_w, const int* flag_s, const int* flag_sw, int epoch) {
   using C = CS<NI>;
-  constexpr int N2 = C::N2, TX = C::TX, TY = C::TY, NT = C::NT, LPE = C::LPE;
+  constexpr int N2 = C::N2, NT = C::NT, TX = C::TX, TY = C::TY, NW = NT / 32;
+  const Geom& g = P.g;
+  Addr A{g};
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool last = (ls == g.nz), pzd = zdir(g, ls);
+  const int x1 = x0 + tw, y1 = y0 + th;
+  const bool hasE = x1 < g.nx, hasN = y1 < g.ny, hasW = x0 > 0, hasS = y0 > 0;
+  if (!hasW && !hasS) return;
+  if (tid == 0) {
+    if (flag_w) while (flag_acquire(flag_w + ls) != epoch) __nanosleep(32);
+    if (flag_s) while (flag_acquire(flag_s + ls) != epoch) __nanosleep(32);
+    if (flag_sw) while (flag_acquire(flag_sw + ls) != epoch) __nanosleep(32);
+  }
+  __syncthreads();
+  const double* pd = P.pending + (item * 2 + (ls & 1)) * (long long)C::PEND;
+  if (!last) {
+    if (hasW)
+      for (int row = warp; row < th; row += NW) {                     // x-faces, W column
+        double* yo = P.y + A.xf(x0, y0 + row, ls);
+        for (int t = lane; t < N2; t += 32) yo[t] = ld_cg(pd + C::PD_XF + row * N2 + t) + ld_cg(yo + t);
+      }
+    if (hasS) {                                                       // y-faces, S row
+      double* yo = P.y + A.yf(x0, y0, ls);
+      for (int t = tid; t < tw * N2; t += NT) yo[t] = ld_cg(pd + C::PD_YF + t) + ld_cg(yo + t);
+    }
+    for (int row = warp; row <= th; row += NW) {                      // z-edges on W column / S row
+      const int fy = y0 + row;
+      if (fy == 0 || fy == g.ny || (row == th && hasN)) continue;
+      double* yo = P.y + A.ze(x0, fy, ls);
+      if (hasW && lane < NI) {
+        double v = ld_cg(pd + C::PD_ZEW + row * NI + lane);
+        if (row == 0 && hasS) {
+          const int cx = x0 / TX, cy = fy / TY;
+          v += ld_cg(corner_rec(P, cx, cy, ls, 0) + lane) + ld_cg(corner_rec(P, cx, cy, ls, 1) + lane) +
+               ld_cg(corner_rec(P, cx, cy, ls, 2) + lane);
+        } else {
+          v += ld_cg(yo + lane);
+        }
+        yo[lane] = v;
+      }
+      if (row == 0 && hasS)                                           // S row: ix in [1, tw - 1]
+        for (int t = NI + lane; t < tw * NI; t += 32) yo[t] = ld_cg(pd + C::PD_ZES + t - NI) + ld_cg(yo + t);
+    }
+  }
+  if (!pzd) {
+    if (hasS) {                                                       // x-edges, S row
+      double* yo = P.y + A.xe(x0, y0, ls);
+      for (int t = tid; t < tw * NI; t += NT) yo[t] = ld_cg(pd + C::PD_XE + t) + ld_cg(yo + t);
+    }
+    if (hasW)
+      for (int row = warp; row < th; row += NW) {                     // y-edges, W column
+        double* yo = P.y + A.ye(x0, y0 + row, ls);
+        for (int t = lane; t < NI; t += 32) yo[t] = ld_cg(pd + C::PD_YE + row * NI + t) + ld_cg(yo + t);
+      }
+    for (int row = warp; row <= th; row += NW) {                      // vertices on W column / S row
+      const int fy = y0 + row;
+      if (fy == 0 || fy == g.ny || (row == th && hasN)) continue;
+      double* yo = P.y + A.vv(x0, fy, ls);
+      if (hasW && lane == 0) {
+        double v = ld_cg(pd + C::PD_VW + row);
+        if (row == 0 && hasS) {
+          const int cx = x0 / TX, cy = fy / TY;
+          v += ld_cg(corner_rec(P, cx, cy, ls, 0) + NI) + ld_cg(corner_rec(P, cx, cy, ls, 1) + NI) +
+               ld_cg(corner_rec(P, cx, cy, ls, 2) + NI);
+        } else {
+          v += ld_cg(yo);
+        }
+        yo[0] = v;
+      }
+      if (row == 0 && hasS)
+        for (int t = 1 + lane; t < tw; t += 32) yo[t] = ld_cg(pd + C::PD_VS + t - 1) + ld_cg(yo + t);
+    }
+  }
+}
+
+template <int NI, bool UNIFORM>
+__global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
+  using C = CS<NI>;
+  constexpr int N2 = C::N2, TX = C::TX, TY = C::TY, NT = C::NT, LPE = C::LPE, JS = C::JS, JH = C::JH;
   if (P.done != nullptr && *P.done != 0.0) return;
   const Geom& g = P.g;
   extern __shared__ double sm[];
   double* sDinv = sm + C::O_DINV;
   double* sD = sm + C::O_D;
   double* sA0 = sm + C::O_TAB;
-  double* sAp = sA0 + 32;
-  double* sLam = sAp + 32;
+  double* sLam = sA0 + 64;
+  double* const rq = sm + C::O_RQ;
   __shared__ unsigned long long sTicket;
   __shared__ int sEpoch;
   const int tid = threadIdx.x;
   if (tid == 0) sEpoch = *(volatile int*)&P.st->epoch + 1;
   Addr A{g};
   const double K00 = g.tab[TAB_SCAL + 0], K0p = g.tab[TAB_SCAL + 1], w0 = g.tab[TAB_SCAL + 2];
+  const double w02 = w0 * w0;
   for (int t = tid; t < NI; t += NT) {
     sA0[t] = g.tab[TAB_A0 + t];
-    sAp[t] = g.tab[TAB_AP + t];
     sLam[t] = g.tab[TAB_LAM + t];
   }
-  if (g.dinv)
+  if (UNIFORM)
     for (int t = tid; t < C::DINV; t += NT) sDinv[t] = g.dinv[t];
   // padding entries of y are written as 0 by the first CTA
   if (blockIdx.x == 0) {
@@ -372,13 +393,19 @@ __global__ void __launch_bounds__(128) k_apply_col(ColParams P) {
     for (int q = 0; q < 7; ++q)
       for (long long i = ends[q] + tid; i < nexts[q]; i += NT) P.y[i] = 0.0;
   }
-  Side<NI> in{sm + C::O_IS}, ac{sm + C::O_AS};
-  double* const qz = sm + C::O_QZ;
+  Side<NI> ac{sm + C::O_AS};
   // ---- per-thread constants of the volume phase: thread (e, k)
-  const int ve = tid / LPE, vk = tid % LPE;
+  const int ve = tid / (LPE * JS), vk = tid % LPE, vjh = (tid / LPE) % JS;
   const bool vact = vk < NI;
   const int vix = ve % TX, viy = ve / TX;
   const double sk = (vk & 1) ? -1.0 : 1.0;
+  const int kk = vact ? vk : 0;
+  // ---- lane tables of the edge / vertex primary part (no runtime division in the node loops)
+  constexpr int NW = NT / 32;
+  constexpr int EPW = 32 / NI;                               // edges per warp pass
+  const int warp = tid >> 5, lane = tid & 31;
+  const int esub = lane / NI, ec = lane % NI;
+  const bool evalid = lane < EPW * NI;
 
   for (;;) {
     __syncthreads();
@@ -394,36 +421,52 @@ __global__ void __launch_bounds__(128) k_apply_col(ColParams P) {
     const int* const flag_w = tx > 0 ? P.flags + (item - 1) * (g.nz + 1) : nullptr;
     const int* const flag_s = ty > 0 ? P.flags + (item - P.ntx) * (g.nz + 1) : nullptr;
     const int* const flag_sw = (tx > 0 && ty > 0) ? P.flags + (item - P.ntx - 1) * (g.nz + 1) : nullptr;
+    const bool eact = vact && vix < tw && viy < th;
 
-    // plane 0: input + accumulator
+    // prologue: planes 0, 1 and side 0 as one cp.async group
     load_plane<NI>(P, Plane<NI>{sm + C::O_IP}, x0, y0, tw, th, 0);
+    load_side<NI>(P, Side<NI>{sm + C::O_IS}, x0, y0, tw, th, 0);
+    load_plane<NI>(P, Plane<NI>{sm + C::O_IP + C::PLANE}, x0, y0, tw, th, 1);
+    cp_commit();
     for (int t = tid; t < C::PLANE; t += NT) sm[C::O_AP + t] = 0.0;
 
     for (int l = 0; l <= g.nz; ++l) {
       const bool last = (l == g.nz);         // final step: only plane nz remains
-      Plane<NI> inb{sm + C::O_IP + (l & 1) * C::PLANE}, intp{sm + C::O_IP + ((l + 1) & 1) * C::PLANE};
-      Plane<NI> acb{sm + C::O_AP + (l & 1) * C::PLANE}, actp{sm + C::O_AP + ((l + 1) & 1) * C::PLANE};
+      const Side<NI> in{sm + C::O_IS + (l & 1) * C::SIDE};
+      const Plane<NI> inb{sm + C::O_IP + (l & 1) * C::PLANE}, intp{sm + C::O_IP + ((l + 1) & 1) * C::PLANE};
+      const Plane<NI> acb{sm + C::O_AP + (l & 1) * C::PLANE}, actp{sm + C::O_AP + ((l + 1) & 1) * C::PLANE};
+      // early prefetch: side l+1 (overlaps this step's compute)
+      if (l + 1 < g.nz) load_side<NI>(P, Side<NI>{sm + C::O_IS + ((l + 1) & 1) * C::SIDE}, x0, y0, tw, th, l + 1);
+      cp_commit();
+      cp_wait<1>();
+      __syncthreads();
       if (!last) {
-        load_side<NI>(P, in, x0, y0, tw, th, l);
-        load_plane<NI>(P, intp, x0, y0, tw, th, l + 1);
-        for (int t = tid; t < C::SIDE; t += NT) sm[C::O_AS + t] = 0.0;
+        for (int t = tid; t < C::SIDE; t += NT) ac.b[t] = 0.0;
         for (int t = tid; t < C::PLANE; t += NT) actp.b[t] = 0.0;
-        for (int t = tid; t < C::NE; t += NT) {
-          int ex = x0 + min(t % TX, tw - 1), ey = y0 + min(t / TX, th - 1);
-          double d[4];
-          metric(g, ex, ey, l, d);
-          for (int q = 0; q < 4; ++q) sD[t * 4 + q] = d[q];
+        if (UNIFORM) {
+          for (int t = tid; t < 4 * C::NE; t += NT) sD[t] = g.d_uni[t & 3];
+        } else {
+          for (int t = tid; t < C::NE; t += NT) {
+            int ex = x0 + min(t % TX, tw - 1), ey = y0 + min(t / TX, th - 1);
+            double d[4];
+            metric(g, ex, ey, l, d);
+            for (int q = 0; q < 4; ++q) sD[t * 4 + q] = d[q];
+          }
         }
         __syncthreads();
-        // ================= volume phase: faces-in, D^{-1}, faces-out (even/odd) ==============
+        // ============ condensed part (faces-in, D^{-1}, faces-out; even / odd form of Table 2)
+        //              fused with the primary part of the element's x- and y-faces ============
+        // Thread (e, jh, k): k-plane of element e, rows j = 2 jj + jh (all of one parity, so
+        // sigma_j is a per-thread constant and the y-reduction yields one parity class).
         {
-          const bool eact = vact && vix < tw && viy < th;
           const double* d = sD + ve * 4;
-          const double d1 = d[1], d2 = d[2], d3 = d[3];
-          const int kk = vact ? vk : 0;
+          const double d0 = d[0], d1 = d[1], d2 = d[2], d3 = d[3];
           const double ak = eact ? sA0[kk] : 0.0;
-          double pxp[NI], pxm[NI], pyp[NI], pym[NI];
-          double qxp[NI], qxm[NI], qyp[NI], qym[NI];
+          const double akd3 = ak * d3;
+          const double lamk = sLam[kk];
+          const double sj = (JS == 2 && vjh) ? -1.0 : 1.0;
+          double pxp[JH], pxm[JH], ajr[JH], py[NI];
+          double qxp[JH], qxm[JH], qy[NI];
           const double* W = in.xf(viy, vix);
           const double* E = in.xf(viy, vix + 1);
           const double* S = in.yf(viy, vix);
@@ -431,42 +474,93 @@ __global__ void __launch_bounds__(128) k_apply_col(ColParams P) {
           const double* B = inb.zf(viy, vix);
           const double* T = intp.zf(viy, vix);
 #pragma unroll
-          for (int j = 0; j < NI; ++j) {
-            double w = eact ? W[j + NI * kk] : 0.0, e = eact ? E[j + NI * kk] : 0.0;
-            pxp[j] = d1 * (w + e);
-            pxm[j] = d1 * (w - e);
-            double s = eact ? S[j + NI * kk] : 0.0, n = eact ? N[j + NI * kk] : 0.0;
-            pyp[j] = d2 * (s + n);
-            pym[j] = d2 * (s - n);
-            qxp[j] = qxm[j] = qyp[j] = qym[j] = 0.0;
+          for (int jj = 0; jj < JH; ++jj) {
+            const int j = JS * jj + vjh;
+            const bool ok = eact && j < NI;
+            const double w = ok ? W[j + NI * kk] : 0.0, e = ok ? E[j + NI * kk] : 0.0;
+            pxp[jj] = d1 * (w + e);
+            pxm[jj] = d1 * (w - e);
+            ajr[jj] = ok ? sA0[j] : 0.0;
+            qxp[jj] = qxm[jj] = 0.0;
           }
-          const double d0 = d[0];
 #pragma unroll
-          for (int j = 0; j < NI; ++j) {
+          for (int i = 0; i < NI; ++i) {
+            py[i] = eact ? d2 * fma(sj, N[i + NI * kk], S[i + NI * kk]) : 0.0;
+            qy[i] = 0.0;
+          }
+          double* const qz = rq;
+#pragma unroll
+          for (int jj = 0; jj < JH; ++jj) {
+            const int j = min(JS * jj + vjh, NI - 1);
+            const bool jok = (JS * jj + vjh) < NI;
+            const double aj = ajr[jj];
+            const double* Bj = B + NI * j;
+            const double* Tj = T + NI * j;
+            const double* Dj = sDinv + NI * j + N2 * kk;
 #pragma unroll
             for (int i = 0; i < NI; ++i) {
-              const int q = i + NI * j;
-              const double pz = d3 * (B[q] + sk * T[q]);
-              const double u = sA0[i] * ((i & 1) ? pxm[j] : pxp[j]) + sA0[j] * ((j & 1) ? pym[i] : pyp[i]) + ak * pz;
-              const double dinv = g.dinv ? sDinv[q + N2 * kk]
-                                         : 1.0 / (d0 + d1 * sLam[i] + d2 * sLam[j] + d3 * sLam[kk]);
-              const double v = u * dinv;
-              if (i & 1) qxm[j] += sA0[i] * v; else qxp[j] += sA0[i] * v;
-              if (j & 1) qym[i] += sA0[j] * v; else qyp[i] += sA0[j] * v;
+              const double pz = fma(sk, Tj[i], Bj[i]);
+              const double u = fma(sA0[i], (i & 1) ? pxm[jj] : pxp[jj], fma(aj, py[i], akd3 * pz));
+              double v;
+              if (UNIFORM) v = u * Dj[i];
+              else v = u / (d0 + d1 * sLam[i] + d2 * sLam[j] + d3 * lamk);
+              if (i & 1) qxm[jj] = fma(sA0[i], v, qxm[jj]); else qxp[jj] = fma(sA0[i], v, qxp[jj]);
+              qy[i] = fma(aj, v, qy[i]);
               double c = ak * v;
               if (LPE >= 4) c += __shfl_xor_sync(0xffffffffu, c, 2);
               if (LPE >= 8) c += __shfl_xor_sync(0xffffffffu, c, 4);
-              if (vk < 2 && eact) qz[(ve * 2 + vk) * N2 + q] = c;
+              if (vk < 2 && eact && jok) qz[(ve * 2 + vk) * N2 + i + NI * j] = c;
             }
           }
-          // x / y outputs: low faces first, high faces after a barrier (race-free accumulation)
+          // y-reduction: this thread holds Q_y^{sigma = (-1)^jh}(i) for all i; fetch the other class
+          double qyo[NI];
+#pragma unroll
+          for (int i = 0; i < NI; ++i) qyo[i] = (JS == 2) ? __shfl_xor_sync(0xffffffffu, qy[i], LPE) : 0.0;
+          // primary part of the element's four side faces at this k (Eq. 26 generalised):
+          //   W/E node (j,k): (d0 w0 + d1 K00 + d2 w0 Lam_j + d3 w0 Lam_k) u + d1 K0p u_opp
+          //                   + d2 w0 a0_j (Z(ib,0)[k] + s_j Z(ib,1)[k]) + d3 w0 a0_k (Y(ib,0)[j] + s_k Y(ib,1)[j])
+          //   S/N node (i,k): (d0 w0 + d1 w0 Lam_i + d2 K00 + d3 w0 Lam_k) u + d2 K0p u_opp
+          //                   + d1 w0 a0_i (Z(0,jb)[k] + s_i Z(1,jb)[k]) + d3 w0 a0_k (X(jb,0)[i] + s_k X(jb,1)[i])
+          // This thread owns rows j = i = 2 jj + jh of the four faces.
+          const double z00 = in.ze(viy, vix)[kk], z10 = in.ze(viy, vix + 1)[kk];
+          const double z01 = in.ze(viy + 1, vix)[kk], z11 = in.ze(viy + 1, vix + 1)[kk];
+          const double base = d0 * w0 + d3 * w0 * lamk;
+          const double wak = d3 * w0 * ak;
+          double oW[JH], oE[JH], oS[JH], oN[JH];
+#pragma unroll
+          for (int jj = 0; jj < JH; ++jj) {
+            const int r = min(JS * jj + vjh, NI - 1);         // row index (j for W/E, i for S/N)
+            const double ar = sA0[r], lr = sLam[r];
+            const double w = W[r + NI * kk], e = E[r + NI * kk], s = S[r + NI * kk], n = N[r + NI * kk];
+            const double dxy = base + d1 * K00 + d2 * w0 * lr;
+            const double dyx = base + d2 * K00 + d1 * w0 * lr;
+            oW[jj] = dxy * w + d1 * K0p * e + d2 * w0 * ar * fma(sj, z01, z00) +
+                     wak * fma(sk, intp.ye(viy, vix)[r], inb.ye(viy, vix)[r]);
+            oE[jj] = dxy * e + d1 * K0p * w + d2 * w0 * ar * fma(sj, z11, z10) +
+                     wak * fma(sk, intp.ye(viy, vix + 1)[r], inb.ye(viy, vix + 1)[r]);
+            oS[jj] = dyx * s + d2 * K0p * n + d1 * w0 * ar * fma(sj, z10, z00) +
+                     wak * fma(sk, intp.xe(viy, vix)[r], inb.xe(viy, vix)[r]);
+            oN[jj] = dyx * n + d2 * K0p * s + d1 * w0 * ar * fma(sj, z11, z01) +
+                     wak * fma(sk, intp.xe(viy + 1, vix)[r], inb.xe(viy + 1, vix)[r]);
+          }
+          // outputs: low faces first, high faces after a barrier (race-free accumulation)
+          double qyp_r[JH], qym_r[JH];
+#pragma unroll
+          for (int jj = 0; jj < JH; ++jj) {
+            const int i0 = min(JS * jj, NI - 1), i1 = min(JS * jj + 1, NI - 1);
+            // row i = 2 jj + jh: Q+ is held by the jh = 0 thread, Q- by the jh = 1 thread
+            qyp_r[jj] = (JS == 1 || vjh == 0) ? qy[i0] : qyo[i1];
+            qym_r[jj] = (JS == 1) ? 0.0 : (vjh == 0 ? qyo[i0] : qy[i1]);
+          }
           if (eact) {
             double* aW = ac.xf(viy, vix);
             double* aS = ac.yf(viy, vix);
 #pragma unroll
-            for (int j = 0; j < NI; ++j) {
-              aW[j + NI * kk] -= d1 * (qxp[j] + qxm[j]);
-              aS[j + NI * kk] -= d2 * (qyp[j] + qym[j]);
+            for (int jj = 0; jj < JH; ++jj) {
+              const int r = JS * jj + vjh;
+              if (r >= NI) continue;
+              aW[r + NI * kk] += oW[jj] - d1 * (qxp[jj] + qxm[jj]);
+              aS[r + NI * kk] += oS[jj] - d2 * (qyp_r[jj] + qym_r[jj]);
             }
           }
           __syncthreads();
@@ -474,202 +568,340 @@ __global__ void __launch_bounds__(128) k_apply_col(ColParams P) {
             double* aE = ac.xf(viy, vix + 1);
             double* aN = ac.yf(viy + 1, vix);
 #pragma unroll
-            for (int j = 0; j < NI; ++j) {
-              aE[j + NI * kk] -= d1 * (qxp[j] - qxm[j]);
-              aN[j + NI * kk] -= d2 * (qyp[j] - qym[j]);
+            for (int jj = 0; jj < JH; ++jj) {
+              const int r = JS * jj + vjh;
+              if (r >= NI) continue;
+              aE[r + NI * kk] += oE[jj] - d1 * (qxp[jj] - qxm[jj]);
+              aN[r + NI * kk] += oN[jj] - d2 * (qyp_r[jj] - qym_r[jj]);
             }
           }
         }
         __syncthreads();
-        // z outputs from the parity sums
+        // z outputs: B -= d3 (Q+ + Q-), T -= d3 (Q+ - Q-), plus the primary part of the element's
+        // B and T faces: (d0 w0 + d1 w0 Lam_i + d2 w0 Lam_j + d3 K00) u + d3 K0p u_opp
+        //   + d1 w0 a0_i (Y(0,kb)[j] + s_i Y(1,kb)[j]) + d2 w0 a0_j (X(0,kb)[i] + s_j X(1,kb)[i])
         for (int t = tid; t < C::NE * N2; t += NT) {
           const int e = t / N2, q = t % N2, ix = e % TX, iy = e / TX;
           if (ix >= tw || iy >= th) continue;
-          const double d3 = sD[e * 4 + 3];
-          const double qp = qz[(e * 2) * N2 + q], qm = NI > 1 ? qz[(e * 2 + 1) * N2 + q] : 0.0;
-          acb.zf(iy, ix)[q] -= d3 * (qp + qm);
-          actp.zf(iy, ix)[q] -= d3 * (qp - qm);
+          const int a = q % NI, b = q / NI;
+          const double* d = sD + e * 4;
+          const double qp = rq[(e * 2) * N2 + q], qm = NI > 1 ? rq[(e * 2 + 1) * N2 + q] : 0.0;
+          const double ub = inb.zf(iy, ix)[q], ut = intp.zf(iy, ix)[q];
+          const double sa = (a & 1) ? -1.0 : 1.0, sb = (b & 1) ? -1.0 : 1.0;
+          const double dz = d[0] * w0 + (d[1] * sLam[a] + d[2] * sLam[b]) * w0 + d[3] * K00;
+          const double c1 = d[1] * w0 * sA0[a], c2 = d[2] * w0 * sA0[b];
+          const double pb = dz * ub + d[3] * K0p * ut + c1 * fma(sa, inb.ye(iy, ix + 1)[b], inb.ye(iy, ix)[b]) +
+                            c2 * fma(sb, inb.xe(iy + 1, ix)[a], inb.xe(iy, ix)[a]);
+          const double pt = dz * ut + d[3] * K0p * ub + c1 * fma(sa, intp.ye(iy, ix + 1)[b], intp.ye(iy, ix)[b]) +
+                            c2 * fma(sb, intp.xe(iy + 1, ix)[a], intp.xe(iy, ix)[a]);
+          acb.zf(iy, ix)[q] += pb - d[3] * (qp + qm);
+          actp.zf(iy, ix)[q] += pt - d[3] * (qp - qm);
         }
         __syncthreads();
-        // ================= primary part, four colour phases ==================================
-        for (int col = 0; col < 4; ++col) {
-          const int cx = col & 1, cy = col >> 1;
-          constexpr int NPC = ((TX + 1) / 2) * ((TY + 1) / 2);   // elements per colour
-          for (int t = tid; t < NPC * C::NSH; t += NT) {
-            const int ec = t / C::NSH, s = t % C::NSH;
-            const int ix = cx + 2 * (ec % ((TX + 1) / 2)), iy = cy + 2 * (ec / ((TX + 1) / 2));
-            if (ix >= tw || iy >= th) continue;
-            primary_node<NI>(s, ix, iy, sD + (iy * TX + ix) * 4, in, inb, intp, ac, acb, actp, sA0, sAp, sLam, K00, K0p,
-                             w0);
+        // ============ even / odd line reductions of faces and edges (primary part) ============
+        {
+          constexpr int NXR = TY * (TX + 1) * NI, NYR = (TY + 1) * TX * NI, NZR = TY * TX * NI;
+          constexpr int NZE = (TY + 1) * (TX + 1), NXE = (TY + 1) * TX, NYE = TY * (TX + 1);
+          constexpr int TOT = 2 * NXR + 2 * NYR + 4 * NZR + NZE + 2 * NXE + 2 * NYE;
+          for (int t = tid; t < TOT; t += NT) {
+            int r = t;
+            if (r < 2 * NXR) {                       // x-face (iy, ix): over j (keep k = c) / over k (keep j = c)
+              const int dir = r / NXR, rr = r % NXR, c = rr % NI, f = rr / NI;
+              const double* F = in.b + C::S_XF + f * N2;
+              double* o = rq + (dir == 0 ? C::R_XJ : C::R_XK) + f * 2 * NI;
+              eo_reduce<NI>(dir == 0 ? F + NI * c : F + c, dir == 0 ? 1 : NI, sA0, o + 2 * c);
+              continue;
+            }
+            r -= 2 * NXR;
+            if (r < 2 * NYR) {                       // y-face (iy, ix): over i (keep k) / over k (keep i)
+              const int dir = r / NYR, rr = r % NYR, c = rr % NI, f = rr / NI;
+              const double* F = in.b + C::S_YF + f * N2;
+              double* o = rq + (dir == 0 ? C::R_YI : C::R_YK) + f * 2 * NI;
+              eo_reduce<NI>(dir == 0 ? F + NI * c : F + c, dir == 0 ? 1 : NI, sA0, o + 2 * c);
+              continue;
+            }
+            r -= 2 * NYR;
+            if (r < 4 * NZR) {                       // z-face plane kb: over i (keep j) / over j (keep i)
+              const int dir = r / (2 * NZR), rr = r % (2 * NZR), kb = rr / NZR, r3 = rr % NZR, c = r3 % NI,
+                        f = r3 / NI;
+              const double* F = (kb ? intp : inb).b + C::P_ZF + f * N2;
+              double* o = rq + (dir == 0 ? C::R_ZI : C::R_ZJ) + (kb * TY * TX + f) * 2 * NI;
+              eo_reduce<NI>(dir == 0 ? F + NI * c : F + c, dir == 0 ? 1 : NI, sA0, o + 2 * c);
+              continue;
+            }
+            r -= 4 * NZR;
+            if (r < NZE) {                           // z-edges of layer l
+              eo_reduce<NI>(in.b + C::S_ZE + r * NI, 1, sA0, rq + C::R_ZE + r * 2);
+              continue;
+            }
+            r -= NZE;
+            if (r < 2 * NXE) {                       // x-edges of planes l, l+1
+              const int kb = r / NXE, e = r % NXE;
+              eo_reduce<NI>((kb ? intp : inb).b + C::P_XE + e * NI, 1, sA0, rq + C::R_XE + r * 2);
+              continue;
+            }
+            r -= 2 * NXE;
+            {                                        // y-edges of planes l, l+1
+              const int kb = r / NYE, e = r % NYE;
+              eo_reduce<NI>((kb ? intp : inb).b + C::P_YE + e * NI, 1, sA0, rq + C::R_YE + r * 2);
+            }
           }
-          __syncthreads();
         }
-      }
-      // ================= finalize: publish, write owned, look-back, write boundary ==========
-      // Entities finished at this step: side entities of layer l (if !last) and plane l.
-      const bool pzd = zdir(g, l);
-      // (a) publish partials of entities owned by a higher-ticket tile
-      if (!last) {
-        for (int t = tid; t < th * N2; t += NT) {          // x-faces at fx = x0 + tw (E boundary)
-          const int iy = t / N2, q = t % N2, fx = x0 + tw;
-          if (fx < g.nx) P.y[A.xf(fx, y0 + iy, l) + q] = ac.xf(iy, tw)[q];
-        }
-        for (int t = tid; t < tw * N2; t += NT) {          // y-faces at fy = y0 + th (N boundary)
-          const int ix = t / N2, q = t % N2, fy = y0 + th;
-          if (fy < g.ny) P.y[A.yf(x0 + ix, fy, l) + q] = ac.yf(th, ix)[q];
-        }
-      }
-      // z-edges (layer l) + vertices (plane l) on the tile boundary lines; x-edges / y-edges (plane l)
-      for (int t = tid; t < (TX + 1) * (TY + 1) * (NI + 1); t += NT) {
-        const int c = t % (NI + 1), ix = (t / (NI + 1)) % (TX + 1), iy = t / ((NI + 1) * (TX + 1));
-        if (ix > tw || iy > th) continue;
-        const int fx = x0 + ix, fy = y0 + iy;
-        const bool ex_ = (ix == tw && fx < g.nx), ny_ = (iy == th && fy < g.ny);
-        const bool wx = (ix == 0 && fx > 0), sy = (iy == 0 && fy > 0);
-        if (!ex_ && !ny_) continue;                         // owned here
-        const bool isv = (c == NI);
-        if (!isv && last) continue;
-        if (isv ? (pzd || fx == 0 || fx == g.nx || fy == 0 || fy == g.ny)
-                : (fx == 0 || fx == g.nx || fy == 0 || fy == g.ny))
-          continue;                                         // Dirichlet: nothing to publish
-        const double v = isv ? *acb.vv(iy, ix) : ac.ze(iy, ix)[c];
-        if (ex_ && ny_) {
-          corner_rec(P, (fx) / TX, (fy) / TY, l, 0)[c] = v;         // I am SW of the owner
-        } else if (ex_ && sy) {
-          corner_rec(P, fx / TX, fy / TY, l, 2)[c] = v;             // I am W of the owner
-        } else if (ny_ && wx) {
-          corner_rec(P, fx / TX, fy / TY, l, 1)[c] = v;             // I am S of the owner
-        } else {
-          if (isv) P.y[A.vv(fx, fy, l)] = v;
-          else P.y[A.ze(fx, fy, l) + c] = v;
-        }
-      }
-      for (int t = tid; t < tw * NI; t += NT) {            // x-edges at fy = y0 + th, plane l
-        const int ix = t / NI, c = t % NI, fy = y0 + th;
-        if (fy < g.ny && !pzd) P.y[A.xe(x0 + ix, fy, l) + c] = acb.xe(th, ix)[c];
-      }
-      for (int t = tid; t < th * NI; t += NT) {            // y-edges at fx = x0 + tw, plane l
-        const int iy = t / NI, c = t % NI, fx = x0 + tw;
-        if (fx < g.nx && !pzd) P.y[A.ye(fx, y0 + iy, l) + c] = acb.ye(iy, tw)[c];
-      }
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) flag_release(flag_me + l, epoch);
-      // (b) owned entities without a lower-ticket contributor
-      if (!last) {
-        for (int t = tid; t < th * (TX + 1) * N2; t += NT) {   // x-faces
-          const int q = t % N2, ix = (t / N2) % (TX + 1), iy = t / (N2 * (TX + 1));
-          const int fx = x0 + ix;
-          if (ix > tw) continue;
-          if (ix == tw && fx < g.nx) continue;                 // published
-          if (ix == 0 && fx > 0) continue;                     // needs W
-          P.y[A.xf(fx, y0 + iy, l) + q] = (fx == 0 || fx == g.nx) ? 0.0 : ac.xf(iy, ix)[q];
-        }
-        for (int t = tid; t < (TY + 1) * tw * N2; t += NT) {   // y-faces
-          const int q = t % N2, ix = (t / N2) % tw, iy = t / (N2 * tw);
-          const int fy = y0 + iy;
-          if (iy > th) continue;
-          if (iy == th && fy < g.ny) continue;
-          if (iy == 0 && fy > 0) continue;
-          P.y[A.yf(x0 + ix, fy, l) + q] = (fy == 0 || fy == g.ny) ? 0.0 : ac.yf(iy, ix)[q];
-        }
-      }
-      for (int t = tid; t < th * tw * N2; t += NT) {           // z-faces of plane l
-        const int q = t % N2, ix = (t / N2) % tw, iy = t / (N2 * tw);
-        P.y[A.zf(x0 + ix, y0 + iy, l) + q] = pzd ? 0.0 : acb.zf(iy, ix)[q];
-      }
-      for (int t = tid; t < (TX + 1) * (TY + 1) * (NI + 1); t += NT) {   // z-edges + vertices
-        const int c = t % (NI + 1), ix = (t / (NI + 1)) % (TX + 1), iy = t / ((NI + 1) * (TX + 1));
-        if (ix > tw || iy > th) continue;
-        const bool isv = (c == NI);
-        if (!isv && last) continue;
-        const int fx = x0 + ix, fy = y0 + iy;
-        const bool ex_ = (ix == tw && fx < g.nx), ny_ = (iy == th && fy < g.ny);
-        const bool wx = (ix == 0 && fx > 0), sy = (iy == 0 && fy > 0);
-        if (ex_ || ny_) continue;
-        const bool dr = (fx == 0 || fx == g.nx || fy == 0 || fy == g.ny) || (isv && pzd);
-        if (!dr && (wx || sy)) continue;                       // needs look-back
-        const double v = dr ? 0.0 : (isv ? *acb.vv(iy, ix) : ac.ze(iy, ix)[c]);
-        if (isv) P.y[A.vv(fx, fy, l)] = v;
-        else P.y[A.ze(fx, fy, l) + c] = v;
-      }
-      for (int t = tid; t < (TY + 1) * tw * NI; t += NT) {     // x-edges of plane l
-        const int c = t % NI, ix = (t / NI) % tw, iy = t / (NI * tw);
-        if (iy > th) continue;
-        const int fy = y0 + iy;
-        if (iy == th && fy < g.ny) continue;
-        const bool dr = pzd || fy == 0 || fy == g.ny;
-        if (!dr && iy == 0 && fy > 0) continue;
-        P.y[A.xe(x0 + ix, fy, l) + c] = dr ? 0.0 : acb.xe(iy, ix)[c];
-      }
-      for (int t = tid; t < th * (TX + 1) * NI; t += NT) {     // y-edges of plane l
-        const int c = t % NI, ix = (t / NI) % (TX + 1), iy = t / (NI * (TX + 1));
-        if (ix > tw) continue;
-        const int fx = x0 + ix;
-        if (ix == tw && fx < g.nx) continue;
-        const bool dr = pzd || fx == 0 || fx == g.nx;
-        if (!dr && ix == 0 && fx > 0) continue;
-        P.y[A.ye(fx, y0 + iy, l) + c] = dr ? 0.0 : acb.ye(iy, ix)[c];
-      }
-      // (c) look-back: wait for the W, S, SW tiles of this step
-      if (tid == 0) {
-        if (flag_w) while (flag_acquire(flag_w + l) != epoch) __nanosleep(64);
-        if (flag_s) while (flag_acquire(flag_s + l) != epoch) __nanosleep(64);
-        if (flag_sw) while (flag_acquire(flag_sw + l) != epoch) __nanosleep(64);
-      }
-      __syncthreads();
-      if (!last) {
-        if (x0 > 0)
-          for (int t = tid; t < th * N2; t += NT) {            // x-faces at fx = x0
-            const int iy = t / N2, q = t % N2;
-            const long long a = A.xf(x0, y0 + iy, l) + q;
-            P.y[a] = ac.xf(iy, 0)[q] + ld_cg(P.y + a);
+        __syncthreads();
+        // ============ primary part Htilde_BB, entity-centric over the tile's elements ============
+        // (Mtilde = diag(w0, 1..1, w0); Ktilde arrowhead: row 0 = (K00, a0, K0p),
+        //  row p = (K0p, ap, K00), interior row m = (a0_m @0, Lam_m @m, ap_m @p).)
+        // Faces: a warp (or a lane group) per face, lanes over the in-face nodes; edges: lane
+        // groups of n_I per edge; vertices: a lane each.  Each accumulator entry is owned by
+        // exactly one lane, which sums the contributions of the tile's adjacent elements.
+        {
+          auto present = [&](int ix, int iy) { return ix >= 0 && iy >= 0 && ix < tw && iy < th; };
+          auto dd = [&](int ix, int iy) { return sD + (iy * TX + ix) * 4; };
+          // ---- z-edges (fx = ix, fy = iy), coord k = c
+          for (int e0 = warp * EPW; e0 < (TY + 1) * (TX + 1); e0 += NW * EPW) {
+            const int e = e0 + esub, ix = e % (TX + 1), iy = e / (TX + 1), c = ec;
+            if (!evalid || e >= (TY + 1) * (TX + 1) || ix > tw || iy > th) continue;
+            const double u = in.ze(iy, ix)[c];
+            const double tz = sA0[c] * (*inb.vv(iy, ix) + ((c & 1) ? -*intp.vv(iy, ix) : *intp.vv(iy, ix))) + sLam[c] * u;
+            double y = 0.0;
+#pragma unroll
+            for (int el = 0; el < 4; ++el) {
+              const int ib = el & 1, jb = el >> 1, ex = ix - ib, ey = iy - jb;
+              if (!present(ex, ey)) continue;
+              const double* d = dd(ex, ey);
+              const double txl = (ib ? K0p : K00) * in.ze(iy, ex)[c] + (ib ? K00 : K0p) * in.ze(iy, ex + 1)[c] +
+                                 eo_row(rq + C::R_YI + (iy * TX + ex) * 2 * NI + 2 * c, ib);
+              const double tyl = (jb ? K0p : K00) * in.ze(ey, ix)[c] + (jb ? K00 : K0p) * in.ze(ey + 1, ix)[c] +
+                                 eo_row(rq + C::R_XJ + (ey * (TX + 1) + ix) * 2 * NI + 2 * c, jb);
+              y += d[0] * w02 * u + d[1] * w0 * txl + d[2] * w0 * tyl + d[3] * w02 * tz;
+            }
+            ac.ze(iy, ix)[c] += y;
           }
-        if (y0 > 0)
-          for (int t = tid; t < tw * N2; t += NT) {            // y-faces at fy = y0
-            const int ix = t / N2, q = t % N2;
-            const long long a = A.yf(x0 + ix, y0, l) + q;
-            P.y[a] = ac.yf(0, ix)[q] + ld_cg(P.y + a);
+          // ---- x-edges (ex = ix, fy = iy) of planes l, l+1, coord i = c
+          for (int e0 = warp * EPW; e0 < 2 * (TY + 1) * TX; e0 += NW * EPW) {
+            const int e = e0 + esub, kb = e / ((TY + 1) * TX), ff = e % ((TY + 1) * TX), ix = ff % TX, iy = ff / TX;
+            const int c = ec;
+            if (!evalid || e >= 2 * (TY + 1) * TX || ix >= tw || iy > th) continue;
+            const Plane<NI> pk = kb ? intp : inb;
+            const double u = pk.xe(iy, ix)[c];
+            const double txl = sA0[c] * (*pk.vv(iy, ix) + ((c & 1) ? -*pk.vv(iy, ix + 1) : *pk.vv(iy, ix + 1))) + sLam[c] * u;
+            const double tzl = (kb ? K0p : K00) * inb.xe(iy, ix)[c] + (kb ? K00 : K0p) * intp.xe(iy, ix)[c] +
+                               eo_row(rq + C::R_YK + (iy * TX + ix) * 2 * NI + 2 * c, kb);
+            double y = 0.0;
+#pragma unroll
+            for (int el = 0; el < 2; ++el) {
+              const int jb = el, ey = iy - jb;
+              if (!present(ix, ey)) continue;
+              const double* d = dd(ix, ey);
+              const double tyl = (jb ? K0p : K00) * pk.xe(ey, ix)[c] + (jb ? K00 : K0p) * pk.xe(ey + 1, ix)[c] +
+                                 eo_row(rq + C::R_ZJ + (kb * TY * TX + ey * TX + ix) * 2 * NI + 2 * c, jb);
+              y += d[0] * w02 * u + d[1] * w02 * txl + d[2] * w0 * tyl + d[3] * w0 * tzl;
+            }
+            (kb ? actp : acb).xe(iy, ix)[c] += y;
           }
-      }
-      for (int t = tid; t < (TX + 1) * (TY + 1) * (NI + 1); t += NT) {
-        const int c = t % (NI + 1), ix = (t / (NI + 1)) % (TX + 1), iy = t / ((NI + 1) * (TX + 1));
-        if (ix > tw || iy > th) continue;
-        const bool isv = (c == NI);
-        if (!isv && last) continue;
-        const int fx = x0 + ix, fy = y0 + iy;
-        const bool ex_ = (ix == tw && fx < g.nx), ny_ = (iy == th && fy < g.ny);
-        const bool wx = (ix == 0 && fx > 0), sy = (iy == 0 && fy > 0);
-        if (ex_ || ny_) continue;
-        const bool dr = (fx == 0 || fx == g.nx || fy == 0 || fy == g.ny) || (isv && pzd);
-        if (dr || !(wx || sy)) continue;
-        double v = isv ? *acb.vv(iy, ix) : ac.ze(iy, ix)[c];
-        const long long a = isv ? A.vv(fx, fy, l) : A.ze(fx, fy, l) + c;
-        if (wx && sy) {
-          const int cx = fx / TX, cy = fy / TY;
-          v += ld_cg(corner_rec(P, cx, cy, l, 0) + c) + ld_cg(corner_rec(P, cx, cy, l, 1) + c) +
-               ld_cg(corner_rec(P, cx, cy, l, 2) + c);
-        } else {
-          v += ld_cg(P.y + a);
+          // ---- y-edges (fx = ix, ey = iy) of planes l, l+1, coord j = c
+          for (int e0 = warp * EPW; e0 < 2 * TY * (TX + 1); e0 += NW * EPW) {
+            const int e = e0 + esub, kb = e / (TY * (TX + 1)), ff = e % (TY * (TX + 1)), ix = ff % (TX + 1),
+                      iy = ff / (TX + 1);
+            const int c = ec;
+            if (!evalid || e >= 2 * TY * (TX + 1) || ix > tw || iy >= th) continue;
+            const Plane<NI> pk = kb ? intp : inb;
+            const double u = pk.ye(iy, ix)[c];
+            const double tyl = sA0[c] * (*pk.vv(iy, ix) + ((c & 1) ? -*pk.vv(iy + 1, ix) : *pk.vv(iy + 1, ix))) + sLam[c] * u;
+            const double tzl = (kb ? K0p : K00) * inb.ye(iy, ix)[c] + (kb ? K00 : K0p) * intp.ye(iy, ix)[c] +
+                               eo_row(rq + C::R_XK + (iy * (TX + 1) + ix) * 2 * NI + 2 * c, kb);
+            double y = 0.0;
+#pragma unroll
+            for (int el = 0; el < 2; ++el) {
+              const int ib = el, ex = ix - ib;
+              if (!present(ex, iy)) continue;
+              const double* d = dd(ex, iy);
+              const double txl = (ib ? K0p : K00) * pk.ye(iy, ex)[c] + (ib ? K00 : K0p) * pk.ye(iy, ex + 1)[c] +
+                                 eo_row(rq + C::R_ZI + (kb * TY * TX + iy * TX + ex) * 2 * NI + 2 * c, ib);
+              y += d[0] * w02 * u + d[1] * w0 * txl + d[2] * w02 * tyl + d[3] * w0 * tzl;
+            }
+            (kb ? actp : acb).ye(iy, ix)[c] += y;
+          }
+          // ---- vertices (fx = ix, fy = iy) of planes l, l+1
+          for (int v = tid; v < 2 * (TY + 1) * (TX + 1); v += NT) {
+            const int kb = v / ((TY + 1) * (TX + 1)), ff = v % ((TY + 1) * (TX + 1)), ix = ff % (TX + 1),
+                      iy = ff / (TX + 1);
+            if (ix > tw || iy > th) continue;
+            const Plane<NI> pk = kb ? intp : inb;
+            const double u = *pk.vv(iy, ix);
+            const double tzl = (kb ? K0p : K00) * *inb.vv(iy, ix) + (kb ? K00 : K0p) * *intp.vv(iy, ix) +
+                               eo_row(rq + C::R_ZE + (iy * (TX + 1) + ix) * 2, kb);
+            double y = 0.0;
+#pragma unroll
+            for (int el = 0; el < 4; ++el) {
+              const int ib = el & 1, jb = el >> 1, ex = ix - ib, ey = iy - jb;
+              if (!present(ex, ey)) continue;
+              const double* d = dd(ex, ey);
+              const double txl = (ib ? K0p : K00) * *pk.vv(iy, ex) + (ib ? K00 : K0p) * *pk.vv(iy, ex + 1) +
+                                 eo_row(rq + C::R_XE + (kb * (TY + 1) * TX + iy * TX + ex) * 2, ib);
+              const double tyl = (jb ? K0p : K00) * *pk.vv(ey, ix) + (jb ? K00 : K0p) * *pk.vv(ey + 1, ix) +
+                                 eo_row(rq + C::R_YE + (kb * TY * (TX + 1) + ey * (TX + 1) + ix) * 2, jb);
+              y += d[0] * w02 * w0 * u + w02 * (d[1] * txl + d[2] * tyl + d[3] * tzl);
+            }
+            *(kb ? actp : acb).vv(iy, ix) += y;
+          }
         }
-        P.y[a] = v;
+        __syncthreads();
       }
-      if (!pzd) {
-        if (y0 > 0)
-          for (int t = tid; t < tw * NI; t += NT) {            // x-edges at fy = y0, plane l
-            const int ix = t / NI, c = t % NI;
-            const long long a = A.xe(x0 + ix, y0, l) + c;
-            P.y[a] = acb.xe(0, ix)[c] + ld_cg(P.y + a);
+      // late prefetch: plane l+2 into the buffer of plane l (no longer read)
+      if (l + 2 <= g.nz) load_plane<NI>(P, Plane<NI>{sm + C::O_IP + (l & 1) * C::PLANE}, x0, y0, tw, th, l + 2);
+      cp_commit();
+      // ================= finalize step l: publish / write owned / park ==========================
+      // Ownership: the highest-ticket contributing tile (tiles are ticketed x-fastest): a tile
+      // owns its W / S boundaries (finished one step later from parked partials) and publishes
+      // its E / N boundaries (y-in-place; the three 4-tile rim corners go to corner records).
+      // Every loop below is a warp per contiguous row with range-only classification.
+      {
+        const bool pzd = zdir(g, l);
+        const int x1 = x0 + tw, y1 = y0 + th;
+        const bool hasE = x1 < g.nx, hasN = y1 < g.ny, hasW = x0 > 0, hasS = y0 > 0;
+        const bool dW = (x0 == 0), dE = (x1 == g.nx);                 // Dirichlet row ends
+        double* const pd = P.pending + (item * 2 + (l & 1)) * (long long)C::PEND;
+        // ---- (a) publish
+        if (!last) {
+          if (hasE)
+            for (int row = warp; row < th; row += NW) {
+              double* yo = P.y + A.xf(x1, y0 + row, l);
+              const double* s = ac.xf(row, tw);
+              for (int t = lane; t < N2; t += 32) yo[t] = s[t];
+            }
+          if (hasN) {
+            double* yo = P.y + A.yf(x0, y1, l);
+            const double* s = ac.yf(th, 0);
+            for (int t = tid; t < tw * N2; t += NT) yo[t] = s[t];
           }
-        if (x0 > 0)
-          for (int t = tid; t < th * NI; t += NT) {            // y-edges at fx = x0, plane l
-            const int iy = t / NI, c = t % NI;
-            const long long a = A.ye(x0, y0 + iy, l) + c;
-            P.y[a] = acb.ye(iy, 0)[c] + ld_cg(P.y + a);
+        }
+        if (!pzd) {
+          if (hasN) {
+            double* yo = P.y + A.xe(x0, y1, l);
+            const double* s = acb.xe(th, 0);
+            for (int t = tid; t < tw * NI; t += NT) yo[t] = s[t];
           }
+          if (hasE)
+            for (int row = warp; row < th; row += NW) {
+              double* yo = P.y + A.ye(x1, y0 + row, l);
+              const double* s = acb.ye(row, tw);
+              for (int t = lane; t < NI; t += 32) yo[t] = s[t];
+            }
+        }
+        // z-edges (layer l, c < NI) / vertices (plane l, c == NI) on the E column and N row
+        if (warp == 0) {
+          const int nE = hasE ? th + 1 : 0, nN = hasN ? tw : 0;
+          for (int t = lane; t < (nE + nN) * (NI + 1); t += 32) {
+            const int ent = t / (NI + 1), c = t - ent * (NI + 1);
+            const bool isv = (c == NI);
+            if (isv ? pzd : last) continue;
+            int ix, iy;
+            if (ent < nE) { ix = tw; iy = ent; } else { ix = ent - nE; iy = th; }
+            const int fx = x0 + ix, fy = y0 + iy;
+            if (fx == 0 || fy == 0 || fy == g.ny) continue;          // Dirichlet
+            const bool ex_ = (ix == tw && hasE), ny_ = (iy == th && hasN);
+            const double v = isv ? *acb.vv(iy, ix) : ac.ze(iy, ix)[c];
+            if (ex_ && ny_) corner_rec(P, fx / TX, fy / TY, l, 0)[c] = v;                   // SW of owner
+            else if (ex_ && iy == 0 && hasS) corner_rec(P, fx / TX, fy / TY, l, 2)[c] = v;   // W of owner
+            else if (ny_ && ix == 0 && hasW) corner_rec(P, fx / TX, fy / TY, l, 1)[c] = v;   // S of owner
+            else if (isv) P.y[A.vv(fx, fy, l)] = v;
+            else P.y[A.ze(fx, fy, l) + c] = v;
+          }
+        }
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) flag_release(flag_me + l, epoch);
+        // ---- (b) owned entities (incl. Dirichlet zeros) and (b') parked W / S partials
+        if (!last) {
+          for (int row = warp; row < th; row += NW) {                 // x-faces
+            double* yo = P.y + A.xf(x0, y0 + row, l);
+            const double* s = ac.xf(row, 0);
+            const int t0 = hasW ? N2 : 0, t1 = hasE ? tw * N2 : (tw + 1) * N2;
+            for (int t = t0 + lane; t < t1; t += 32)
+              yo[t] = ((dW && t < N2) || (dE && t >= tw * N2)) ? 0.0 : s[t];
+            if (hasW)
+              for (int t = lane; t < N2; t += 32) pd[C::PD_XF + row * N2 + t] = s[t];
+          }
+          for (int row = warp; row <= th; row += NW) {                // y-faces
+            const int fy = y0 + row;
+            const double* s = ac.yf(row, 0);
+            if (row == th && hasN) continue;
+            if (row == 0 && hasS) {
+              for (int t = lane; t < tw * N2; t += 32) pd[C::PD_YF + t] = s[t];
+              continue;
+            }
+            const bool rd = fy == 0 || fy == g.ny;
+            double* yo = P.y + A.yf(x0, fy, l);
+            for (int t = lane; t < tw * N2; t += 32) yo[t] = rd ? 0.0 : s[t];
+          }
+          for (int row = warp; row <= th; row += NW) {                // z-edges
+            const int fy = y0 + row;
+            const bool rd = fy == 0 || fy == g.ny;
+            const double* s = ac.ze(row, 0);
+            double* yo = P.y + A.ze(x0, fy, l);
+            const bool pubrow = (row == th && hasN), parkrow = (row == 0 && hasS && !rd);
+            // entity ix = 0 (t < NI), interior 1..tw-1, ix = tw (t >= tw NI)
+            for (int t = lane; t < (tw + 1) * NI; t += 32) {
+              const bool lo = t < NI, hi = t >= tw * NI;
+              if (pubrow || (hi && hasE)) continue;                     // published
+              if (rd || (lo && dW) || (hi && dE)) { yo[t] = 0.0; continue; }
+              if (lo && hasW) { pd[C::PD_ZEW + row * NI + t] = s[t]; continue; }   // W column
+              if (parkrow) { pd[C::PD_ZES + t - NI] = s[t]; continue; }          // S row
+              yo[t] = s[t];
+            }
+          }
+        }
+        for (int row = warp; row < th; row += NW) {                   // z-faces of plane l
+          double* yo = P.y + A.zf(x0, y0 + row, l);
+          const double* s = acb.zf(row, 0);
+          for (int t = lane; t < tw * N2; t += 32) yo[t] = pzd ? 0.0 : s[t];
+        }
+        for (int row = warp; row <= th; row += NW) {                  // x-edges of plane l
+          const int fy = y0 + row;
+          if (row == th && hasN && !pzd) continue;
+          const double* s = acb.xe(row, 0);
+          const bool rd = pzd || fy == 0 || fy == g.ny;
+          if (row == 0 && hasS && !rd) {
+            for (int t = lane; t < tw * NI; t += 32) pd[C::PD_XE + t] = s[t];
+            continue;
+          }
+          double* yo = P.y + A.xe(x0, fy, l);
+          for (int t = lane; t < tw * NI; t += 32) yo[t] = rd ? 0.0 : s[t];
+        }
+        for (int row = warp; row < th; row += NW) {                   // y-edges of plane l
+          double* yo = P.y + A.ye(x0, y0 + row, l);
+          const double* s = acb.ye(row, 0);
+          for (int t = lane; t < (tw + 1) * NI; t += 32) {
+            const bool lo = t < NI, hi = t >= tw * NI;
+            if (hi && hasE && !pzd) continue;
+            if (pzd || (lo && dW) || (hi && dE)) { yo[t] = 0.0; continue; }
+            if (lo && hasW) { pd[C::PD_YE + row * NI + t] = s[t]; continue; }
+            yo[t] = s[t];
+          }
+        }
+        for (int row = warp; row <= th; row += NW) {                  // vertices of plane l
+          const int fy = y0 + row;
+          const bool rd = pzd || fy == 0 || fy == g.ny;
+          const double* s = acb.vv(row, 0);
+          double* yo = P.y + A.vv(x0, fy, l);
+          const bool pubrow = (row == th && hasN && !pzd), parkrow = (row == 0 && hasS && !rd);
+          for (int t = lane; t <= tw; t += 32) {
+            const bool lo = t == 0, hi = t == tw;
+            if (pubrow || (hi && hasE && !pzd)) continue;
+            if (rd || (lo && dW) || (hi && dE)) { yo[t] = 0.0; continue; }
+            if (lo && hasW) { pd[C::PD_VW + row] = s[t]; continue; }
+            if (parkrow) { pd[C::PD_VS + t - 1] = s[t]; continue; }
+            yo[t] = s[t];
+          }
+        }
       }
+      // (c, d) finish the W / S boundary entities of the PREVIOUS step
+      if (l >= 1) finish_boundary<NI>(P, item, l - 1, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch);
       __syncthreads();
     }
+    finish_boundary<NI>(P, item, g.nz, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch);
+    __syncthreads();
   }
   if (tid == 0) {
     __threadfence();
@@ -682,14 +914,14 @@ __global__ void __launch_bounds__(128) k_apply_col(ColParams P) {
   }
 }
 
-template <int NI>
-static int launch_col_t(const ColParams& P, cudaStream_t st, int* nl, int* grid_out) {
+template <int NI, bool U>
+static int launch_col_u(const ColParams& P, cudaStream_t st, int* nl, int* grid_out) {
   using C = CS<NI>;
   const size_t smem = sizeof(double) * C::TOTAL;
   static int max_active = -1, nsm = 0;
   if (max_active < 0) {
-    cudaFuncSetAttribute(k_apply_col<NI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_active, k_apply_col<NI>, C::NT, smem);
+    cudaFuncSetAttribute(k_apply_col<NI, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_active, k_apply_col<NI, U>, C::NT, smem);
     int dev;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -698,28 +930,34 @@ static int launch_col_t(const ColParams& P, cudaStream_t st, int* nl, int* grid_
   int grid = max_active * nsm;
   if (grid > P.nitems) grid = P.nitems;
   *grid_out = grid;
-  k_apply_col<NI><<<grid, C::NT, smem, st>>>(P);
+  k_apply_col<NI, U><<<grid, C::NT, smem, st>>>(P);
   (*nl)++;
   return cudaGetLastError();
 }
 
+template <int NI>
+static int launch_col_t(const ColParams& P, cudaStream_t st, int* nl, int* grid_out) {
+  return P.g.dinv ? launch_col_u<NI, true>(P, st, nl, grid_out) : launch_col_u<NI, false>(P, st, nl, grid_out);
+}
+
 bool col_supported(int ni) { return ni >= 1 && ni <= 8; }
 
-void col_tile(int ni, int* tx, int* ty) {
+void col_tile(int ni, int* tx, int* ty, int* pend) {
   switch (ni) {
-#define TCASE(N) case N: *tx = CS<N>::TX; *ty = CS<N>::TY; return;
+#define TCASE(N) case N: *tx = CS<N>::TX; *ty = CS<N>::TY; *pend = CS<N>::PEND; return;
     TCASE(1) TCASE(2) TCASE(3) TCASE(4) TCASE(5) TCASE(6) TCASE(7) TCASE(8)
 #undef TCASE
-    default: *tx = *ty = 0;
+    default: *tx = *ty = *pend = 0;
   }
 }
 
 int launch_apply_col(const ColParams& P, void* stream, int* nl, int* grid_out, void* events);
 
 int launch_apply_col_raw(const Geom& g, const double* x, double* y, const double* done, void* state, int* flags,
-                         double* corner, int ntx, int nty, void* stream, int* nl, void* events) {
+                         double* corner, double* pending, int ntx, int nty, void* stream, int* nl, void* events) {
   ColParams P;
   P.g = g; P.x = x; P.y = y; P.done = done; P.st = (ColState*)state; P.flags = flags; P.corner = corner;
+  P.pending = pending;
   P.ntx = ntx; P.nty = nty; P.nitems = ntx * nty;
   int grid = 0;
   return launch_apply_col(P, stream, nl, &grid, events);

@@ -103,9 +103,10 @@ namespace sc {
 struct ColState;
 // v2 tile-column operator (kernels_col.cu), n_I <= 8.
 bool col_supported(int ni);
-void col_tile(int ni, int* tx, int* ty);
+void col_tile(int ni, int* tx, int* ty, int* pend);
 int launch_apply_col_raw(const Geom& g, const double* x, double* y, const double* done, void* state, int* flags,
-                         double* corner, int ntx, int nty, void* stream, int* nlaunch, void* events);
+                         double* corner, double* pending, int ntx, int nty, void* stream, int* nlaunch,
+                         void* events);
 int launch_add_segments(double* y, const double* add, const long long* off, const long long* len, int n,
                         void* stream, int* nlaunch);
 }
