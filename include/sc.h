@@ -99,6 +99,10 @@ typedef enum { SC_PERM = 0, SC_PRIMAL = 1, SC_DUAL = 2 } sc_basis_mode;
  * preconditioner table; allocate small device tables.  Synchronous. */
 sc_status sc_setup(const sc_params* prm, sc_ctx** out);
 sc_status sc_destroy(sc_ctx* ctx);
+
+/* Host-only: validate params and return the rank-local slab layout sc_setup would use
+ * (no GPU, no allocation; nccl_comm may be NULL).  Used by multi-rank host logic and tests. */
+sc_status sc_layout_query(const sc_params* prm, sc_layout_info* out);
 sc_status sc_layout(const sc_ctx* ctx, sc_layout_info* out);
 
 /* Workspace for sc_pcg_solve and sc_apply_condensed (caller-owned device memory,

@@ -48,10 +48,14 @@ def skeleton_mask(grid):
 
 
 def dirichlet_mask(grid):
-    """True at lattice nodes on the domain boundary (homogeneous Dirichlet)."""
+    """True at lattice nodes on the domain boundary (homogeneous Dirichlet).
+
+    grid.extra["dirichlet_z"] = (lo, hi) can declare the z = 0 / z = top planes as interior
+    cuts (a slab of a larger domain), which are then not Dirichlet."""
     gx, gy, gz = lattice_ijk(grid)
     nx1, ny1, nz1 = lattice_dims(grid)
-    return (gx == 0) | (gx == nx1 - 1) | (gy == 0) | (gy == ny1 - 1) | (gz == 0) | (gz == nz1 - 1)
+    zlo, zhi = grid.extra.get("dirichlet_z", (True, True))
+    return (gx == 0) | (gx == nx1 - 1) | (gy == 0) | (gy == ny1 - 1) | ((gz == 0) & zlo) | ((gz == nz1 - 1) & zhi)
 
 
 def free_skeleton_mask(grid):

@@ -43,6 +43,7 @@ _D = ctypes.POINTER(ctypes.c_double)
 SIGNATURES = {
     "sc_setup": ([ctypes.POINTER(ScParams), ctypes.POINTER(_P)], ctypes.c_int),
     "sc_destroy": ([_P], ctypes.c_int),
+    "sc_layout_query": ([ctypes.POINTER(ScParams), ctypes.POINTER(ScLayoutInfo)], ctypes.c_int),
     "sc_layout": ([_P, ctypes.POINTER(ScLayoutInfo)], ctypes.c_int),
     "sc_workspace_bytes": ([_P], ctypes.c_size_t),
     "sc_bind_workspace": ([_P, _P, ctypes.c_size_t], ctypes.c_int),

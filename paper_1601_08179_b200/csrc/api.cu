@@ -132,9 +132,10 @@ static long long align_up(long long v) { return (v + kAlign - 1) / kAlign * kAli
 
 static bool finite_pos(double v) { return std::isfinite(v) && v > 0; }
 
-extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
-  if (!prm || !out) return SC_EINVAL;
-  *out = nullptr;
+// Validate the parameters and compute the rank-local slab geometry and skeleton layout
+// (host only; shared by sc_setup and sc_layout_query).
+static sc_status layout_compute(const sc_params* prm, bool need_comm, Geom& g, sc_layout_info& L) {
+  if (!prm) return SC_EINVAL;
   const int p = prm->p;
   if (p < 2 || p > SC_PMAX) return SC_EINVAL;
   for (int d = 0; d < 3; ++d) {
@@ -145,27 +146,12 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
   if (!std::isfinite(prm->lambda) || prm->lambda < 0) return SC_EINVAL;
   if (prm->nranks < 1 || prm->rank < 0 || prm->rank >= prm->nranks) return SC_EINVAL;
   if (prm->nranks > prm->ne[2]) return SC_EINVAL;
-  if (prm->nranks > 1 && !prm->nccl_comm) return SC_EINVAL;
-
-  sc_ctx* ctx = new sc_ctx();
-  ctx->prm = *prm;
-  for (int d = 0; d < 3; ++d) {
-    std::vector<double>& h = d == 0 ? ctx->hx : (d == 1 ? ctx->hy : ctx->hz);
-    h.assign(prm->h[d], prm->h[d] + prm->ne[d]);
-    ctx->prm.h[d] = h.data();
-  }
-  std::string berr;
-  if (!build_basis_1d(p, ctx->B, berr)) {
-    ctx->err = berr;
-    delete ctx;
-    return SC_EINVAL;
-  }
+  if (need_comm && prm->nranks > 1 && !prm->nccl_comm) return SC_EINVAL;
   const int ni = p - 1;
-  // ---- slab partition: rank r owns element layers [z0, z1) (balanced, contiguous)
+  // slab partition: rank r owns element layers [z0, z1) (balanced, contiguous)
   const int nzg = prm->ne[2], R = prm->nranks, r = prm->rank;
   const int z0 = (int)((long long)nzg * r / R), z1 = (int)((long long)nzg * (r + 1) / R);
   const int nx = prm->ne[0], ny = prm->ne[1], nz = z1 - z0;
-  Geom& g = ctx->g;
   memset(&g, 0, sizeof(g));
   g.p = p; g.ni = ni; g.nx = nx; g.ny = ny; g.nz = nz;
   g.dir_bot = (r == 0); g.dir_top = (r == R - 1);
@@ -186,8 +172,6 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
   g.off_v = off;
   off = align_up(off + g.n_v);
   g.n_total = off;
-
-  sc_layout_info& L = ctx->L;
   memset(&L, 0, sizeof(L));
   L.n_total = g.n_total;
   L.n_lattice = (long long)g.nx1 * g.ny1 * g.nz1;
@@ -205,6 +189,46 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
     long long tot = ((long long)nx * p - 1) * ((long long)ny * p - 1) * gz_hi;
     L.n_free = tot - (long long)nx * ny * nz * (long long)ni * ni * ni;
   }
+  return SC_OK;
+}
+
+extern "C" sc_status sc_layout_query(const sc_params* prm, sc_layout_info* out) {
+  if (!prm || !out) return SC_EINVAL;
+  Geom g;
+  return layout_compute(prm, false, g, *out);
+}
+
+extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
+  if (!prm || !out) return SC_EINVAL;
+  *out = nullptr;
+  {
+    Geom gq;
+    sc_layout_info lq;
+    sc_status st = layout_compute(prm, true, gq, lq);
+    if (st != SC_OK) return st;
+  }
+  const int p = prm->p;
+  sc_ctx* ctx = new sc_ctx();
+  ctx->prm = *prm;
+  for (int d = 0; d < 3; ++d) {
+    std::vector<double>& h = d == 0 ? ctx->hx : (d == 1 ? ctx->hy : ctx->hz);
+    h.assign(prm->h[d], prm->h[d] + prm->ne[d]);
+    ctx->prm.h[d] = h.data();
+  }
+  std::string berr;
+  if (!build_basis_1d(p, ctx->B, berr)) {
+    ctx->err = berr;
+    delete ctx;
+    return SC_EINVAL;
+  }
+  const int ni = p - 1;
+  Geom& g = ctx->g;
+  sc_layout_info& L = ctx->L;
+  layout_compute(prm, true, g, L);
+  const int R = prm->nranks, r = prm->rank;
+  const int z0 = L.z_begin, z1 = L.z_end;
+  const int nx = g.nx, ny = g.ny, nz = g.nz;
+  const long long n2 = (long long)ni * ni;
   // ---- device tables
   std::vector<double> tab(TAB_SIZE, 0.0);
   const Basis1D& B = ctx->B;

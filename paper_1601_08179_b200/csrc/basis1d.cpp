@@ -6,7 +6,7 @@
 // PAPER.md P:381-395  Mtilde = diag(M00, I, Mpp); Ktilde arrowhead with
 //                     Ktilde_I0 = S_II K_I0 (a0), Ktilde_Ip = S_II K_Ip (ap), Ktilde_II = Lambda.
 //
-// Construction (independent of the oracle): Newton on L_p' for the GLL nodes, the
+// Construction (independent of any test-side construction): Newton on L_p' for the GLL nodes, the
 // closed-form GLL differentiation matrix, K = D^T W D, reflection symmetrisation, a cyclic
 // Jacobi eigen-solver on W^{-1/2} K_II W^{-1/2}, parity projection of every eigenvector
 // (the centro-symmetric pencil has even/odd eigenvectors), ascending Lambda,

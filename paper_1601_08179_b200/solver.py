@@ -33,6 +33,27 @@ def basis_1d_host(p):
                 parity_err=kt[3])
 
 
+def layout_query(p, ne, widths, lam, rank=0, nranks=1):
+    """sc_layout_query: the slab layout sc_setup would use on this rank (host only, no GPU)."""
+    lib = capi.load()
+    hs = [np.ascontiguousarray(np.asarray(w, dtype=np.float64)) for w in widths]
+    prm = ScParams()
+    prm.p = int(p)
+    for d in range(3):
+        prm.ne[d] = int(ne[d])
+        prm.h[d] = hs[d].ctypes.data
+    prm.lam = float(lam)
+    prm.device = 0
+    prm.nccl_comm = None
+    prm.rank = int(rank)
+    prm.nranks = int(nranks)
+    L = ScLayoutInfo()
+    st = lib.sc_layout_query(ctypes.byref(prm), ctypes.byref(L))
+    if st != capi.SC_OK:
+        raise ScError("sc_layout_query", st)
+    return L
+
+
 class Context:
     """sc_setup + workspace.  widths: (hx[nx], hy[ny], hz[nz]) global element widths."""
 
