@@ -13,7 +13,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-LIBDIR = os.path.join(HERE, "_lib")
+LIBDIR = os.environ.get("SC_LIBDIR", os.path.join(HERE, "_lib"))
 LIB = os.path.join(LIBDIR, "libsc.so")
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
@@ -57,6 +57,8 @@ def build(verbose=False, force=False, jobs=8):
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     inc = ["-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-I" + nccl_include()]
     common = [ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3"]
+    if os.environ.get("SC_EXP"):
+        common.append("-DSC_EXP=" + os.environ["SC_EXP"])
     objs = []
     procs = []
     for src in sources():

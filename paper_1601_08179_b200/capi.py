@@ -9,7 +9,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libsc.so")
+LIB_PATH = os.environ.get("SC_LIB_PATH", os.path.join(HERE, "_lib", "libsc.so"))
 
 SC_OK, SC_EINVAL, SC_ENOMEM, SC_ECUDA, SC_ENCCL, SC_EBREAKDOWN, SC_ESTATE = range(7)
 SC_PERM, SC_PRIMAL, SC_DUAL = 0, 1, 2

@@ -173,6 +173,9 @@ struct Addr {
 // entities, which sit at the two ends of a row or fill a whole row, are written as 0).
 template <int NI>
 __device__ void load_plane(const ColParams& P, Plane<NI> pl, int x0, int y0, int tw, int th, int fz) {
+#if defined(SC_EXP) && SC_EXP == 5
+  return;
+#endif
   using C = CS<NI>;
   constexpr int N2 = C::N2, NW = C::NT / 32;
   const Geom& g = P.g;
@@ -217,6 +220,9 @@ __device__ void load_plane(const ColParams& P, Plane<NI> pl, int x0, int y0, int
 
 template <int NI>
 __device__ void load_side(const ColParams& P, Side<NI> sd, int x0, int y0, int tw, int th, int ez) {
+#if defined(SC_EXP) && SC_EXP == 5
+  return;
+#endif
   using C = CS<NI>;
   constexpr int N2 = C::N2, NW = C::NT / 32;
   const Geom& g = P.g;
@@ -279,84 +285,90 @@ __device__ __forceinline__ double eo_row(const double* r, int hi) { return hi ? 
 // Deferred look-back for step ls of tile item: wait for the W, S, SW tiles' flags of step ls,
 // then write the tile's W / S boundary entities of that step as own (parked) partial + the
 // neighbours' partials (y-in-place, or the corner records on the 4-tile corner line).
-// Dirichlet entities were already written as 0.
+// All entries of a step form one flat list; every thread first issues all of its loads
+// (one L2 round trip per step), then all of its stores.  Dirichlet entities were already
+// written as 0 and are skipped.
 template <int NI>
 __device__ void finish_boundary(const ColParams& P, long long item, int ls, int x0, int y0, int tw, int th,
                                 const int* flag_w, const int* flag_s, const int* flag_sw, int epoch) {
   using C = CS<NI>;
-  constexpr int N2 = C::N2, NT = C::NT, TX = C::TX, TY = C::TY, NW = NT / 32;
+  constexpr int N2 = C::N2, NT = C::NT, TX = C::TX, TY = C::TY;
+  constexpr int MAXE = (C::PEND + NT - 1) / NT;
   const Geom& g = P.g;
   Addr A{g};
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x;
   const bool last = (ls == g.nz), pzd = zdir(g, ls);
   const int x1 = x0 + tw, y1 = y0 + th;
   const bool hasE = x1 < g.nx, hasN = y1 < g.ny, hasW = x0 > 0, hasS = y0 > 0;
   if (!hasW && !hasS) return;
+#if !defined(SC_EXP) || SC_EXP != 8
   if (tid == 0) {
     if (flag_w) while (flag_acquire(flag_w + ls) != epoch) __nanosleep(32);
     if (flag_s) while (flag_acquire(flag_s + ls) != epoch) __nanosleep(32);
     if (flag_sw) while (flag_acquire(flag_sw + ls) != epoch) __nanosleep(32);
   }
   __syncthreads();
+#endif
   const double* pd = P.pending + (item * 2 + (ls & 1)) * (long long)C::PEND;
-  if (!last) {
-    if (hasW)
-      for (int row = warp; row < th; row += NW) {                     // x-faces, W column
-        double* yo = P.y + A.xf(x0, y0 + row, ls);
-        for (int t = lane; t < N2; t += 32) yo[t] = ld_cg(pd + C::PD_XF + row * N2 + t) + ld_cg(yo + t);
-      }
-    if (hasS) {                                                       // y-faces, S row
-      double* yo = P.y + A.yf(x0, y0, ls);
-      for (int t = tid; t < tw * N2; t += NT) yo[t] = ld_cg(pd + C::PD_YF + t) + ld_cg(yo + t);
-    }
-    for (int row = warp; row <= th; row += NW) {                      // z-edges on W column / S row
-      const int fy = y0 + row;
+  // segment sizes of the flat list (0 when the segment does not apply at this step)
+  const int n0 = (!last && hasW) ? th * N2 : 0;            // W col x-faces
+  const int n1 = (!last && hasS) ? tw * N2 : 0;            // S row y-faces
+  const int n2 = (!last && hasW) ? (th + 1) * NI : 0;      // W col z-edges
+  const int n3 = (!last && hasS) ? (tw - 1) * NI : 0;      // S row z-edges, ix in [1, tw-1]
+  const int n4 = (!pzd && hasS) ? tw * NI : 0;             // S row x-edges
+  const int n5 = (!pzd && hasW) ? th * NI : 0;             // W col y-edges
+  const int n6 = (!pzd && hasW) ? th + 1 : 0;              // W col vertices
+  const int n7 = (!pzd && hasS) ? tw - 1 : 0;              // S row vertices, ix in [1, tw-1]
+  const int ntot = n0 + n1 + n2 + n3 + n4 + n5 + n6 + n7;
+  double val[MAXE];
+  double* dst[MAXE];
+#pragma unroll
+  for (int k = 0; k < MAXE; ++k) {
+    dst[k] = nullptr;
+    val[k] = 0.0;
+    int t = tid + k * NT;
+    if (t >= ntot) continue;
+    double* d = nullptr;
+    int po = -1;                 // offset of the own parked partial
+    int corner = -1;             // corner line entry: value index into the corner records
+    if (t < n0) {
+      d = P.y + A.xf(x0, y0 + t / N2, ls) + t % N2; po = C::PD_XF + t;
+    } else if ((t -= n0) < n1) {
+      d = P.y + A.yf(x0, y0, ls) + t; po = C::PD_YF + t;
+    } else if ((t -= n1) < n2) {
+      const int row = t / NI, c = t % NI, fy = y0 + row;
       if (fy == 0 || fy == g.ny || (row == th && hasN)) continue;
-      double* yo = P.y + A.ze(x0, fy, ls);
-      if (hasW && lane < NI) {
-        double v = ld_cg(pd + C::PD_ZEW + row * NI + lane);
-        if (row == 0 && hasS) {
-          const int cx = x0 / TX, cy = fy / TY;
-          v += ld_cg(corner_rec(P, cx, cy, ls, 0) + lane) + ld_cg(corner_rec(P, cx, cy, ls, 1) + lane) +
-               ld_cg(corner_rec(P, cx, cy, ls, 2) + lane);
-        } else {
-          v += ld_cg(yo + lane);
-        }
-        yo[lane] = v;
-      }
-      if (row == 0 && hasS)                                           // S row: ix in [1, tw - 1]
-        for (int t = NI + lane; t < tw * NI; t += 32) yo[t] = ld_cg(pd + C::PD_ZES + t - NI) + ld_cg(yo + t);
+      d = P.y + A.ze(x0, fy, ls) + c; po = C::PD_ZEW + t;
+      if (row == 0 && hasS) corner = c;
+    } else if ((t -= n2) < n3) {
+      d = P.y + A.ze(x0, y0, ls) + NI + t; po = C::PD_ZES + t;
+    } else if ((t -= n3) < n4) {
+      d = P.y + A.xe(x0, y0, ls) + t; po = C::PD_XE + t;
+    } else if ((t -= n4) < n5) {
+      d = P.y + A.ye(x0, y0 + t / NI, ls) + t % NI; po = C::PD_YE + t;
+    } else if ((t -= n5) < n6) {
+      const int fy = y0 + t;
+      if (fy == 0 || fy == g.ny || (t == th && hasN)) continue;
+      d = P.y + A.vv(x0, fy, ls); po = C::PD_VW + t;
+      if (t == 0 && hasS) corner = NI;
+    } else {
+      t -= n6;
+      d = P.y + A.vv(x0, y0, ls) + 1 + t; po = C::PD_VS + t;
     }
+    double v = ld_cg(pd + po);
+    if (corner >= 0) {
+      const int cx = x0 / TX, cy = y0 / TY;
+      v += ld_cg(corner_rec(P, cx, cy, ls, 0) + corner) + ld_cg(corner_rec(P, cx, cy, ls, 1) + corner) +
+           ld_cg(corner_rec(P, cx, cy, ls, 2) + corner);
+    } else {
+      v += ld_cg(d);
+    }
+    val[k] = v;
+    dst[k] = d;
   }
-  if (!pzd) {
-    if (hasS) {                                                       // x-edges, S row
-      double* yo = P.y + A.xe(x0, y0, ls);
-      for (int t = tid; t < tw * NI; t += NT) yo[t] = ld_cg(pd + C::PD_XE + t) + ld_cg(yo + t);
-    }
-    if (hasW)
-      for (int row = warp; row < th; row += NW) {                     // y-edges, W column
-        double* yo = P.y + A.ye(x0, y0 + row, ls);
-        for (int t = lane; t < NI; t += 32) yo[t] = ld_cg(pd + C::PD_YE + row * NI + t) + ld_cg(yo + t);
-      }
-    for (int row = warp; row <= th; row += NW) {                      // vertices on W column / S row
-      const int fy = y0 + row;
-      if (fy == 0 || fy == g.ny || (row == th && hasN)) continue;
-      double* yo = P.y + A.vv(x0, fy, ls);
-      if (hasW && lane == 0) {
-        double v = ld_cg(pd + C::PD_VW + row);
-        if (row == 0 && hasS) {
-          const int cx = x0 / TX, cy = fy / TY;
-          v += ld_cg(corner_rec(P, cx, cy, ls, 0) + NI) + ld_cg(corner_rec(P, cx, cy, ls, 1) + NI) +
-               ld_cg(corner_rec(P, cx, cy, ls, 2) + NI);
-        } else {
-          v += ld_cg(yo);
-        }
-        yo[0] = v;
-      }
-      if (row == 0 && hasS)
-        for (int t = 1 + lane; t < tw; t += 32) yo[t] = ld_cg(pd + C::PD_VS + t - 1) + ld_cg(yo + t);
-    }
-  }
+#pragma unroll
+  for (int k = 0; k < MAXE; ++k)
+    if (dst[k]) *dst[k] = val[k];
 }
 
 template <int NI, bool UNIFORM>
@@ -454,6 +466,7 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
           }
         }
         __syncthreads();
+#if !defined(SC_EXP) || SC_EXP != 3
         // ============ condensed part (faces-in, D^{-1}, faces-out; even / odd form of Table 2)
         //              fused with the primary part of the element's x- and y-faces ============
         // Thread (e, jh, k): k-plane of element e, rows j = 2 jj + jh (all of one parity, so
@@ -577,6 +590,8 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
           }
         }
         __syncthreads();
+#endif
+#if !defined(SC_EXP) || SC_EXP != 4
         // z outputs: B -= d3 (Q+ + Q-), T -= d3 (Q+ - Q-), plus the primary part of the element's
         // B and T faces: (d0 w0 + d1 w0 Lam_i + d2 w0 Lam_j + d3 K00) u + d3 K0p u_opp
         //   + d1 w0 a0_i (Y(0,kb)[j] + s_i Y(1,kb)[j]) + d2 w0 a0_j (X(0,kb)[i] + s_j X(1,kb)[i])
@@ -598,7 +613,9 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
           actp.zf(iy, ix)[q] += pt - d[3] * (qp - qm);
         }
         __syncthreads();
+#endif
         // ============ even / odd line reductions of faces and edges (primary part) ============
+#if !defined(SC_EXP) || SC_EXP != 2
         {
           constexpr int NXR = TY * (TX + 1) * NI, NYR = (TY + 1) * TX * NI, NZR = TY * TX * NI;
           constexpr int NZE = (TY + 1) * (TX + 1), NXE = (TY + 1) * TX, NYE = TY * (TX + 1);
@@ -648,7 +665,9 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
           }
         }
         __syncthreads();
+#endif
         // ============ primary part Htilde_BB, entity-centric over the tile's elements ============
+#if !defined(SC_EXP) || SC_EXP != 2
         // (Mtilde = diag(w0, 1..1, w0); Ktilde arrowhead: row 0 = (K00, a0, K0p),
         //  row p = (K0p, ap, K00), interior row m = (a0_m @0, Lam_m @m, ap_m @p).)
         // Faces: a warp (or a lane group) per face, lanes over the in-face nodes; edges: lane
@@ -746,6 +765,7 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
             *(kb ? actp : acb).vv(iy, ix) += y;
           }
         }
+#endif
         __syncthreads();
       }
       // late prefetch: plane l+2 into the buffer of plane l (no longer read)
@@ -762,6 +782,7 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
         const bool hasE = x1 < g.nx, hasN = y1 < g.ny, hasW = x0 > 0, hasS = y0 > 0;
         const bool dW = (x0 == 0), dE = (x1 == g.nx);                 // Dirichlet row ends
         double* const pd = P.pending + (item * 2 + (l & 1)) * (long long)C::PEND;
+#if !defined(SC_EXP) || SC_EXP != 1
         // ---- (a) publish
         if (!last) {
           if (hasE)
@@ -809,95 +830,127 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
             else P.y[A.ze(fx, fy, l) + c] = v;
           }
         }
-        __threadfence();
+#endif
+        // publication: the CTA barrier orders every thread's stores before thread 0's GPU-scope
+        // fence + release store of the flag (cumulativity of bar.sync + fence.acq_rel.gpu)
         __syncthreads();
-        if (tid == 0) flag_release(flag_me + l, epoch);
-        // ---- (b) owned entities (incl. Dirichlet zeros) and (b') parked W / S partials
-        if (!last) {
-          for (int row = warp; row < th; row += NW) {                 // x-faces
-            double* yo = P.y + A.xf(x0, y0 + row, l);
-            const double* s = ac.xf(row, 0);
-            const int t0 = hasW ? N2 : 0, t1 = hasE ? tw * N2 : (tw + 1) * N2;
-            for (int t = t0 + lane; t < t1; t += 32)
-              yo[t] = ((dW && t < N2) || (dE && t >= tw * N2)) ? 0.0 : s[t];
-            if (hasW)
-              for (int t = lane; t < N2; t += 32) pd[C::PD_XF + row * N2 + t] = s[t];
-          }
-          for (int row = warp; row <= th; row += NW) {                // y-faces
-            const int fy = y0 + row;
-            const double* s = ac.yf(row, 0);
-            if (row == th && hasN) continue;
-            if (row == 0 && hasS) {
-              for (int t = lane; t < tw * N2; t += 32) pd[C::PD_YF + t] = s[t];
-              continue;
+        if (tid == 0) {
+          __threadfence();
+          flag_release(flag_me + l, epoch);
+        }
+#if !defined(SC_EXP) || SC_EXP != 1
+#if defined(SC_EXP) && SC_EXP == 7
+        if (false)
+#endif
+        // ---- (b) owned entities (incl. Dirichlet zeros) and (b') parked W / S partials.
+        // Flat loops over the whole tile of each class (all warps busy); smem rows and global
+        // rows are both contiguous, so entry (row, c) is base + row * stride + c on both sides.
+        {
+          const unsigned nxf = (unsigned)(g.nx + 1) * N2, nyf = (unsigned)g.nx * N2;
+          const unsigned nxe = (unsigned)g.nx * NI, nye = (unsigned)(g.nx + 1) * NI;
+          const unsigned nze = (unsigned)(g.nx + 1) * NI, nvv = (unsigned)(g.nx + 1);
+          if (!last) {
+            {   // x-faces: rows iy < th, entries c < (tw + 1) N2
+              constexpr unsigned RL = (TX + 1) * N2;
+              double* yo = P.y + A.xf(x0, y0, l);
+              const unsigned t1 = hasE ? tw * N2 : (tw + 1) * N2;
+              for (unsigned t = tid; t < th * RL; t += NT) {
+                const unsigned row = t / RL, c = t - row * RL;
+                if (c >= t1) continue;
+                const double v = ac.b[C::S_XF + t];
+                if (c < N2 && hasW) { pd[C::PD_XF + row * N2 + c] = v; continue; }
+                yo[row * nxf + c] = ((dW && c < N2) || (dE && c >= tw * N2)) ? 0.0 : v;
+              }
             }
-            const bool rd = fy == 0 || fy == g.ny;
-            double* yo = P.y + A.yf(x0, fy, l);
-            for (int t = lane; t < tw * N2; t += 32) yo[t] = rd ? 0.0 : s[t];
+            {   // y-faces: rows iy <= th
+              constexpr unsigned RL = TX * N2;
+              double* yo = P.y + A.yf(x0, y0, l);
+              for (unsigned t = tid; t < (th + 1) * RL; t += NT) {
+                const unsigned row = t / RL, c = t - row * RL;
+                if (c >= tw * N2 || (row == th && hasN)) continue;
+                const double v = ac.b[C::S_YF + t];
+                if (row == 0 && hasS) { pd[C::PD_YF + c] = v; continue; }
+                const int fy = y0 + row;
+                yo[row * nyf + c] = (fy == 0 || fy == g.ny) ? 0.0 : v;
+              }
+            }
+            {   // z-edges: rows iy <= th, entries c < (tw + 1) NI
+              constexpr unsigned RL = (TX + 1) * NI;
+              double* yo = P.y + A.ze(x0, y0, l);
+              for (unsigned t = tid; t < (th + 1) * RL; t += NT) {
+                const unsigned row = t / RL, c = t - row * RL;
+                if (c >= (tw + 1) * NI) continue;
+                const bool lo = c < NI, hi = c >= tw * NI;
+                if ((row == th && hasN) || (hi && hasE)) continue;               // published
+                const int fy = y0 + row;
+                const bool rd = fy == 0 || fy == g.ny;
+                const double v = ac.b[C::S_ZE + t];
+                if (rd || (lo && dW) || (hi && dE)) { yo[row * nze + c] = 0.0; continue; }
+                if (lo && hasW) { pd[C::PD_ZEW + row * NI + c] = v; continue; }    // W column
+                if (row == 0 && hasS) { pd[C::PD_ZES + c - NI] = v; continue; }   // S row
+                yo[row * nze + c] = v;
+              }
+            }
           }
-          for (int row = warp; row <= th; row += NW) {                // z-edges
-            const int fy = y0 + row;
-            const bool rd = fy == 0 || fy == g.ny;
-            const double* s = ac.ze(row, 0);
-            double* yo = P.y + A.ze(x0, fy, l);
-            const bool pubrow = (row == th && hasN), parkrow = (row == 0 && hasS && !rd);
-            // entity ix = 0 (t < NI), interior 1..tw-1, ix = tw (t >= tw NI)
-            for (int t = lane; t < (tw + 1) * NI; t += 32) {
-              const bool lo = t < NI, hi = t >= tw * NI;
-              if (pubrow || (hi && hasE)) continue;                     // published
-              if (rd || (lo && dW) || (hi && dE)) { yo[t] = 0.0; continue; }
-              if (lo && hasW) { pd[C::PD_ZEW + row * NI + t] = s[t]; continue; }   // W column
-              if (parkrow) { pd[C::PD_ZES + t - NI] = s[t]; continue; }          // S row
-              yo[t] = s[t];
+          {   // z-faces of plane l
+            constexpr unsigned RL = TX * N2;
+            double* yo = P.y + A.zf(x0, y0, l);
+            for (unsigned t = tid; t < th * RL; t += NT) {
+              const unsigned row = t / RL, c = t - row * RL;
+              if (c < tw * N2) yo[row * nyf + c] = pzd ? 0.0 : acb.b[C::P_ZF + t];
+            }
+          }
+          {   // x-edges of plane l: rows iy <= th
+            constexpr unsigned RL = TX * NI;
+            double* yo = P.y + A.xe(x0, y0, l);
+            for (unsigned t = tid; t < (th + 1) * RL; t += NT) {
+              const unsigned row = t / RL, c = t - row * RL;
+              if (c >= tw * NI || (row == th && hasN && !pzd)) continue;
+              const int fy = y0 + row;
+              const bool rd = pzd || fy == 0 || fy == g.ny;
+              const double v = acb.b[C::P_XE + t];
+              if (row == 0 && hasS && !rd) { pd[C::PD_XE + c] = v; continue; }
+              yo[row * nxe + c] = rd ? 0.0 : v;
+            }
+          }
+          {   // y-edges of plane l: rows iy < th, entries c < (tw + 1) NI
+            constexpr unsigned RL = (TX + 1) * NI;
+            double* yo = P.y + A.ye(x0, y0, l);
+            for (unsigned t = tid; t < th * RL; t += NT) {
+              const unsigned row = t / RL, c = t - row * RL;
+              if (c >= (tw + 1) * NI) continue;
+              const bool lo = c < NI, hi = c >= tw * NI;
+              if (hi && hasE && !pzd) continue;
+              const double v = acb.b[C::P_YE + t];
+              if (pzd || (lo && dW) || (hi && dE)) { yo[row * nye + c] = 0.0; continue; }
+              if (lo && hasW) { pd[C::PD_YE + row * NI + c] = v; continue; }
+              yo[row * nye + c] = v;
+            }
+          }
+          {   // vertices of plane l: rows iy <= th, entries c <= tw
+            constexpr unsigned RL = TX + 1;
+            double* yo = P.y + A.vv(x0, y0, l);
+            for (unsigned t = tid; t < (th + 1) * RL; t += NT) {
+              const unsigned row = t / RL, c = t - row * RL;
+              if (c > (unsigned)tw) continue;
+              const bool lo = c == 0, hi = c == (unsigned)tw;
+              if ((row == th && hasN && !pzd) || (hi && hasE && !pzd)) continue;
+              const int fy = y0 + row;
+              const bool rd = pzd || fy == 0 || fy == g.ny;
+              const double v = acb.b[C::P_VV + t];
+              if (rd || (lo && dW) || (hi && dE)) { yo[row * nvv + c] = 0.0; continue; }
+              if (lo && hasW) { pd[C::PD_VW + row] = v; continue; }
+              if (row == 0 && hasS) { pd[C::PD_VS + c - 1] = v; continue; }
+              yo[row * nvv + c] = v;
             }
           }
         }
-        for (int row = warp; row < th; row += NW) {                   // z-faces of plane l
-          double* yo = P.y + A.zf(x0, y0 + row, l);
-          const double* s = acb.zf(row, 0);
-          for (int t = lane; t < tw * N2; t += 32) yo[t] = pzd ? 0.0 : s[t];
-        }
-        for (int row = warp; row <= th; row += NW) {                  // x-edges of plane l
-          const int fy = y0 + row;
-          if (row == th && hasN && !pzd) continue;
-          const double* s = acb.xe(row, 0);
-          const bool rd = pzd || fy == 0 || fy == g.ny;
-          if (row == 0 && hasS && !rd) {
-            for (int t = lane; t < tw * NI; t += 32) pd[C::PD_XE + t] = s[t];
-            continue;
-          }
-          double* yo = P.y + A.xe(x0, fy, l);
-          for (int t = lane; t < tw * NI; t += 32) yo[t] = rd ? 0.0 : s[t];
-        }
-        for (int row = warp; row < th; row += NW) {                   // y-edges of plane l
-          double* yo = P.y + A.ye(x0, y0 + row, l);
-          const double* s = acb.ye(row, 0);
-          for (int t = lane; t < (tw + 1) * NI; t += 32) {
-            const bool lo = t < NI, hi = t >= tw * NI;
-            if (hi && hasE && !pzd) continue;
-            if (pzd || (lo && dW) || (hi && dE)) { yo[t] = 0.0; continue; }
-            if (lo && hasW) { pd[C::PD_YE + row * NI + t] = s[t]; continue; }
-            yo[t] = s[t];
-          }
-        }
-        for (int row = warp; row <= th; row += NW) {                  // vertices of plane l
-          const int fy = y0 + row;
-          const bool rd = pzd || fy == 0 || fy == g.ny;
-          const double* s = acb.vv(row, 0);
-          double* yo = P.y + A.vv(x0, fy, l);
-          const bool pubrow = (row == th && hasN && !pzd), parkrow = (row == 0 && hasS && !rd);
-          for (int t = lane; t <= tw; t += 32) {
-            const bool lo = t == 0, hi = t == tw;
-            if (pubrow || (hi && hasE && !pzd)) continue;
-            if (rd || (lo && dW) || (hi && dE)) { yo[t] = 0.0; continue; }
-            if (lo && hasW) { pd[C::PD_VW + row] = s[t]; continue; }
-            if (parkrow) { pd[C::PD_VS + t - 1] = s[t]; continue; }
-            yo[t] = s[t];
-          }
-        }
+#endif
       }
       // (c, d) finish the W / S boundary entities of the PREVIOUS step
+#if !defined(SC_EXP) || (SC_EXP != 1 && SC_EXP != 6)
       if (l >= 1) finish_boundary<NI>(P, item, l - 1, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch);
+#endif
       __syncthreads();
     }
     finish_boundary<NI>(P, item, g.nz, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch);
