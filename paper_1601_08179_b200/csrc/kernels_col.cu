@@ -124,6 +124,20 @@ struct Plane {
 
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 
+#if defined(SC_EXP) && SC_EXP == 9
+__device__ unsigned long long g_phase_cycles[16];
+#define SC_PHASE(k)                                                     \
+  do {                                                                  \
+    if (threadIdx.x == 0) {                                             \
+      long long t_ = clock64();                                         \
+      atomicAdd(&g_phase_cycles[k], (unsigned long long)(t_ - ph_t0));  \
+      ph_t0 = t_;                                                       \
+    }                                                                   \
+  } while (0)
+#else
+#define SC_PHASE(k) do {} while (0)
+#endif
+
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
@@ -387,6 +401,7 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
   __shared__ int sEpoch;
   const int tid = threadIdx.x;
   if (tid == 0) sEpoch = *(volatile int*)&P.st->epoch + 1;
+  long long ph_t0 = clock64();
   Addr A{g};
   const double K00 = g.tab[TAB_SCAL + 0], K0p = g.tab[TAB_SCAL + 1], w0 = g.tab[TAB_SCAL + 2];
   const double w02 = w0 * w0;
@@ -452,6 +467,7 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
       cp_commit();
       cp_wait<1>();
       __syncthreads();
+      SC_PHASE(0);
       if (!last) {
         for (int t = tid; t < C::SIDE; t += NT) ac.b[t] = 0.0;
         for (int t = tid; t < C::PLANE; t += NT) actp.b[t] = 0.0;
@@ -466,6 +482,7 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
           }
         }
         __syncthreads();
+        SC_PHASE(1);
 #if !defined(SC_EXP) || SC_EXP != 3
         // ============ condensed part (faces-in, D^{-1}, faces-out; even / odd form of Table 2)
         //              fused with the primary part of the element's x- and y-faces ============
@@ -577,6 +594,7 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
             }
           }
           __syncthreads();
+          SC_PHASE(2);
           if (eact) {
             double* aE = ac.xf(viy, vix + 1);
             double* aN = ac.yf(viy + 1, vix);
@@ -590,6 +608,7 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
           }
         }
         __syncthreads();
+        SC_PHASE(3);
 #endif
 #if !defined(SC_EXP) || SC_EXP != 4
         // z outputs: B -= d3 (Q+ + Q-), T -= d3 (Q+ - Q-), plus the primary part of the element's
@@ -613,6 +632,7 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
           actp.zf(iy, ix)[q] += pt - d[3] * (qp - qm);
         }
         __syncthreads();
+        SC_PHASE(4);
 #endif
         // ============ even / odd line reductions of faces and edges (primary part) ============
 #if !defined(SC_EXP) || SC_EXP != 2
@@ -665,6 +685,7 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
           }
         }
         __syncthreads();
+        SC_PHASE(5);
 #endif
         // ============ primary part Htilde_BB, entity-centric over the tile's elements ============
 #if !defined(SC_EXP) || SC_EXP != 2
@@ -767,6 +788,7 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
         }
 #endif
         __syncthreads();
+        SC_PHASE(6);
       }
       // late prefetch: plane l+2 into the buffer of plane l (no longer read)
       if (l + 2 <= g.nz) load_plane<NI>(P, Plane<NI>{sm + C::O_IP + (l & 1) * C::PLANE}, x0, y0, tw, th, l + 2);
@@ -834,6 +856,7 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
         // publication: the CTA barrier orders every thread's stores before thread 0's GPU-scope
         // fence + release store of the flag (cumulativity of bar.sync + fence.acq_rel.gpu)
         __syncthreads();
+        SC_PHASE(7);
         if (tid == 0) {
           __threadfence();
           flag_release(flag_me + l, epoch);
@@ -952,6 +975,7 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
       if (l >= 1) finish_boundary<NI>(P, item, l - 1, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch);
 #endif
       __syncthreads();
+      SC_PHASE(8);
     }
     finish_boundary<NI>(P, item, g.nz, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch);
     __syncthreads();
@@ -992,6 +1016,12 @@ template <int NI>
 static int launch_col_t(const ColParams& P, cudaStream_t st, int* nl, int* grid_out) {
   return P.g.dinv ? launch_col_u<NI, true>(P, st, nl, grid_out) : launch_col_u<NI, false>(P, st, nl, grid_out);
 }
+
+#if defined(SC_EXP) && SC_EXP == 9
+extern "C" int sc_exp_phase_cycles(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 16);
+}
+#endif
 
 bool col_supported(int ni) { return ni >= 1 && ni <= 8; }
 
