@@ -67,8 +67,9 @@ struct sc_ctx {
   double* d_tab = nullptr;              // 1-D tables
   double* d_h = nullptr;                // local widths hx | hy | hz
   double* d_dinv = nullptr;             // uniform D^{-1} table
-  // v2 tile-column operator state (kernels_col.cu)
+  // v3 tile-column operator state (kernels_col.cu)
   bool use_col = false;
+  std::vector<unsigned char> col_coef;  // kernel-parameter coefficient block
   int col_ntx = 0, col_nty = 0;
   void* d_colstate = nullptr;
   int* d_flags = nullptr;
@@ -290,12 +291,13 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
       return fail("cudaMemcpy dinv");
     g.dinv = ctx->d_dinv;
   }
-  // ---- v2 tile-column operator (n_I <= 8): tile grid, look-back flags, corner records
+  // ---- v3 tile-column operator (n_I <= 7, uniform geometry): tile grid, look-back flags, corner records
   {
     const char* env = getenv("SC_APPLY_V1");
     bool sig_ok = true;
     for (int m = 0; m < ni; ++m) sig_ok &= (B.sigma[m] == ((m & 1) ? -1 : 1));
-    if (col_supported(ni) && sig_ok && !(env && env[0] == '1')) {
+    if (col_supported(ni) && uniform && sig_ok && !(env && env[0] == '1')) {
+      col_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->col_coef);
       int tx, ty, pend;
       col_tile(ni, &tx, &ty, &pend);
       ctx->col_ntx = (nx + tx - 1) / tx;
@@ -469,7 +471,7 @@ static sc_status apply_impl(sc_ctx* ctx, const double* x, double* y, const doubl
   if (ctx->use_col)
     LAUNCH(launch_apply_col_raw(ctx->g, x, y, done, ctx->d_colstate, ctx->d_flags, ctx->d_corner, ctx->d_pending,
                                 ctx->col_ntx,
-                                ctx->col_nty, st, &nl_, ev));
+                                ctx->col_nty, ctx->col_coef.data(), st, &nl_, ev));
   else
     LAUNCH(launch_apply(ctx->g, x, y, done, st, &nl_, ev));
   if (rec) ctx->prof_n++;

@@ -1,27 +1,31 @@
-// Condensed operator v2 (rows a3-a8 of SURVEY §8(a)): tile-column kernel.
+// Condensed operator v3 (rows a3-a8 of SURVEY §8(a)): tile-column kernel, parity-class warps.
 //
-// Work decomposition.  The slab's elements are cut into xy-tiles of TX x TY elements; a work
-// item is one tile-column (all nz element layers of the tile).  A persistent CTA takes items
-// in ticket order and marches up the column one element layer at a time.  All entities of
-// the skeleton are assembled on chip except those on tile side boundaries, which are
-// finished with a decoupled look-back: the lower-ticket contributor stores its partial sum
-// straight into y (or, on the 4-tile corner lines, into a small corner record), publishes a
-// per-(item, layer) flag, and the owner (highest-ticket contributor) adds it and writes the
-// final value.  Items only ever wait on lower tickets, which are held by running CTAs, so
-// the scheme is deadlock free.  Every skeleton entry is written exactly once (no memset, no
-// atomics) and read from HBM once (re-reads of shared entities hit L2).
+// Work decomposition.  The slab's elements are cut into xy-tiles of TX x TY = 8 x 4 elements;
+// a work item is one tile-column (all nz element layers of the tile).  A persistent CTA (one
+// per SM, 8 warps) takes items in ticket order and marches up the column one element layer at
+// a time.  Every entity of the skeleton is assembled on chip except those on tile side
+// boundaries, which are finished with a decoupled look-back: the lower-ticket contributor
+// stores its partial sum straight into y (or, on the 4-tile corner lines, into a small corner
+// record), publishes a per-(item, layer) flag, and the owner (highest-ticket contributor) adds
+// it and writes the final value one step later.  Every skeleton entry is written exactly once
+// (no memset, no atomics) and read from HBM once.
 //
-// Per element (transformed basis, §6, Table 2, Eq. 26):
-//   faces-in + D^{-1} + faces-out in the even/odd form: with ap = sigma .* a0 (sigma_m = (-1)^m,
-//   the parity of the m-th M-orthonormal eigenvector), the six rank-1 face terms combine to
-//     u(i,j,k) = a_i Px^{s_i}(j,k) + a_j Py^{s_j}(i,k) + a_k Pz^{s_k}(i,j),  P^{+-} = d (F_lo +- F_hi)
-//   and the six faces-out reductions to even/odd partial sums Q^{+-}, F_lo -= d (Q+ + Q-),
-//   F_hi -= d (Q+ - Q-): 7 instead of 13 FP64 instructions per interior point, same result.
-//   Thread (e, k) owns the k-plane of element e: x- and y-reductions stay in registers, the
-//   z-reduction is a parity-preserving butterfly (xor 2, xor 4) across the k lanes.
-//   The primary part Htilde_BB is applied per element and accumulated in shared memory in
-//   four colour phases (elements of one colour share no entity).
+// Condensed part (faces-in, D^{-1}, faces-out; §6 Table 2) in the even/odd
+// form: with ap = sigma .* a0 (sigma_m = (-1)^m, the parity of the m-th M-orthonormal
+// eigenvector, R2),
+//     u(i,j,k) = c1_i Px^{s_i}(j,k) + c2_j Py^{s_j}(i,k) + c3_k Pz^{s_k}(i,j),
+//     Px^{s} = W + (-1)^s E,  Py^{s} = S + (-1)^s N,  Pz^{s} = B + (-1)^s T,  c_d = d_d a0,
+//     v = u D^{-1},  Qx^{s}(j,k) = sum_{i of parity s} c1_i v,  W -= Qx^0 + Qx^1, E -= Qx^0 - Qx^1
+// (and likewise in y and z): 7 FP64 instructions per interior point instead of 13, same result.
+// The interior points of an element split into 8 parity classes (s_i, s_j, s_k); warp w of the
+// CTA owns one class for all 32 elements of the tile (lane = element).  Every faces-out sum of
+// a class then stays in one thread's registers, and every coefficient (c_d, D^{-1}) is warp-
+// uniform and compile-time indexed, so it is read straight from the kernel-parameter constant
+// bank.  The two parity classes of a direction add into the assembled face buffers in two
+// barrier-separated rounds; the two elements of an x- (y-) face are summed with a lane shuffle.
+// The primary part (Htilde_BB, Eq. 26 generalised) is applied entity-centrically.
 #include <cuda_runtime.h>
+#include <string.h>
 #include "sc_device.cuh"
 
 namespace sc {
@@ -35,6 +39,17 @@ struct ColState {
   int epoch;
 };
 
+// Uniform-geometry coefficients, passed by value and copied to shared memory per CTA.
+struct ColCoef {
+  double c[3][8];          // c[d][m] = d_{d+1} a0_m                       (condensed part)
+  double e[3][8];          // e[d][m] = d_{d+1} w0 a0_m                    (face-edge coupling)
+  double a[8];             // a0_m                                         (face line sums)
+  double fd[3][64];        // face self terms: fd[0](j,k) = d0 w0 + d1 K00 + d2 w0 Lam_j + d3 w0 Lam_k,
+                           //   fd[1](i,k), fd[2](i,j) likewise (first index fastest)
+  double k0p[3];           // d_{d+1} K0p                                  (opposite-face coupling)
+  double dinv[512];        // D^{-1}(i,j,k) = 1 / (d0 + d1 Lam_i + d2 Lam_j + d3 Lam_k), i fastest
+};
+
 struct ColParams {
   Geom g;
   const double* x;
@@ -45,18 +60,14 @@ struct ColParams {
   double* corner;        // [(nty+1)][(ntx+1)][nz+1][3][NI+1]
   double* pending;       // [nitems][2][PEND]
   int ntx, nty, nitems;
+  ColCoef cf;
 };
 
 template <int NI>
 struct CS {
   static constexpr int N2 = NI * NI;
-  static constexpr int LPE = NI <= 1 ? 1 : (NI <= 2 ? 2 : (NI <= 4 ? 4 : 8));   // k lanes per element
-  static constexpr int JS = NI >= 2 ? 2 : 1;                                     // j-splits per k-plane
-  static constexpr int JH = (NI + JS - 1) / JS;                                  // j rows per thread (j = JS jj + jh)
-  static constexpr int NT = 256;
-  static constexpr int NE = NT / (LPE * JS);
-  static constexpr int TX = NE >= 256 ? 16 : (NE >= 32 ? 8 : 4);
-  static constexpr int TY = NE / TX;
+  static constexpr int NT = 256;                      // 8 warps = 8 parity classes
+  static constexpr int TX = 8, TY = 4, NE = TX * TY;  // one element per lane
   static constexpr int XF = TY * (TX + 1) * N2;
   static constexpr int YF = (TY + 1) * TX * N2;
   static constexpr int ZE = (TY + 1) * (TX + 1) * NI;
@@ -66,8 +77,7 @@ struct CS {
   static constexpr int PYE = TY * (TX + 1) * NI;
   static constexpr int PVV = (TY + 1) * (TX + 1);
   static constexpr int PLANE = PZF + PXE + PYE + PVV;
-  static constexpr int QZ = NE * 2 * N2;
-  // even/odd reduction buffers (aliased with QZ: used after the z outputs are consumed)
+  // even/odd line reductions of the faces and edges (primary part of the edges / vertices)
   static constexpr int R_XJ = 0;                                   // x-faces over j: [TY][TX+1][2][NI]
   static constexpr int R_XK = R_XJ + TY * (TX + 1) * 2 * NI;       // x-faces over k
   static constexpr int R_YI = R_XK + TY * (TX + 1) * 2 * NI;       // y-faces over i: [TY+1][TX][2][NI]
@@ -78,18 +88,14 @@ struct CS {
   static constexpr int R_XE = R_ZE + (TY + 1) * (TX + 1) * 2;      // x-edges: [2][TY+1][TX][2]
   static constexpr int R_YE = R_XE + 2 * (TY + 1) * TX * 2;        // y-edges: [2][TY][TX+1][2]
   static constexpr int RED = R_YE + 2 * TY * (TX + 1) * 2;
-  static constexpr int RQ = QZ > RED ? QZ : RED;
-  static constexpr int DINV = NI * NI * NI;
   static constexpr int O_IS = 0;                     // 2 side input buffers
   static constexpr int O_IP = O_IS + 2 * SIDE;       // 2 plane input buffers
   static constexpr int O_AS = O_IP + 2 * PLANE;      // side accumulator
   static constexpr int O_AP = O_AS + SIDE;           // 2 plane accumulators
-  static constexpr int O_RQ = O_AP + 2 * PLANE;      // QZ staging / reduction buffers
-  static constexpr int O_DINV = O_RQ + RQ;
-  static constexpr int O_D = O_DINV + DINV;          // per-element d: NE x 4
-  static constexpr int O_TAB = O_D + 4 * NE;         // a0, ap, lam (3 x 32)
-  static constexpr int TOTAL = O_TAB + 3 * 32;
-  static constexpr int NSH = 6 * N2 + 12 * NI + 8;   // element shell nodes
+  static constexpr int O_RQ = O_AP + 2 * PLANE;      // reduction buffers
+  static constexpr int O_TAB = O_RQ + RED;           // a0, lam (2 x 32)
+  static constexpr int O_CF = O_TAB + 2 * 32;        // ColCoef copy
+  static constexpr int TOTAL = O_CF + (int)(sizeof(ColCoef) / sizeof(double));
   // parked own partials of the W / S boundary entities (global, per tile, 2 step slots)
   static constexpr int PD_XF = 0;                                  // W column x-faces  [TY][N2]
   static constexpr int PD_YF = PD_XF + TY * N2;                    // S row y-faces     [TX N2]
@@ -385,32 +391,325 @@ __device__ void finish_boundary(const ColParams& P, long long item, int ls, int 
     if (dst[k]) *dst[k] = val[k];
 }
 
-template <int NI, bool UNIFORM>
-__global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
+
+// ---- condensed part of one parity class (s_i, s_j, s_k) = (SI, SJ, SK) ---------------------
+// Lane = element (ix, iy) of the tile.  All loops are unrolled with compile-time indices, so
+// P.cf.* are constant-bank operands.  Outputs: round r of direction d is executed by the
+// classes with s_d == r; round 0 initialises ac.xf / ac.yf / actp.zf, round 1 adds.
+__device__ __forceinline__ void bar_named(int id) { asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory"); }
+
+// All eight classes run the same code (class parities are warp-uniform runtime values): a
+// class-specialised, fully unrolled variant per warp does not fit the instruction cache.
+// Face entry (a, b) of the class sits at base + 2 aa + 2 NI bb (a = s_a + 2 aa, b = s_b + 2 bb),
+// so every shared-memory access below has a compile-time offset from a per-thread base.
+template <int NI>
+__device__ __forceinline__ void vol_class(const int cls, const ColCoef* cf, const Side<NI>& in, const Plane<NI>& inb,
+                                          const Plane<NI>& intp, const Side<NI>& ac, const Plane<NI>& acb,
+                                          const Plane<NI>& actp, double* rq, int ix, int iy, int tw, int th) {
+  constexpr int M = (NI + 1) / 2, N2 = NI * NI, TX = CS<NI>::TX;
+  constexpr int DO = NI >= 2 ? 1 : 0;   // parity class that adds the primary part and line sums
+  const int si = cls >> 2, sj = (cls >> 1) & 1, sk = cls & 1;
+  const int CI = (NI - si + 1) >> 1, CJ = (NI - sj + 1) >> 1, CK = (NI - sk + 1) >> 1;
+  const double gi = si ? -1.0 : 1.0, gj = sj ? -1.0 : 1.0, gk = sk ? -1.0 : 1.0;
+  const bool act = ix < tw && iy < th;
+  const bool lastx = ix == tw - 1, lasty = iy == th - 1;
+  const double* W = in.xf(iy, ix) + sj + NI * sk;
+  const double* E = W + N2;
+  const double* S = in.yf(iy, ix) + si + NI * sk;
+  const double* N = S + TX * N2;
+  const double* B = inb.zf(iy, ix) + si + NI * sj;
+  const double* T = intp.zf(iy, ix) + si + NI * sj;
+  double* const fX = ac.xf(iy, ix) + sj + NI * sk;
+  double* const fY = ac.yf(iy, ix) + si + NI * sk;
+  double* const fB = acb.zf(iy, ix) + si + NI * sj;
+  double* const fT = actp.zf(iy, ix) + si + NI * sj;
+
+  // ---- phase A: primary part of the faces (Eq. 26 generalised: self, opposite face, the four
+  // bounding edges) and the parity component of the faces' a0-weighted line sums used by the
+  // edge / vertex rows, by the class with s_d == DO of each direction d.  Initialises ac.xf,
+  // ac.yf and actp.zf (plain stores), adds into acb.zf.
+  if (si == DO) {   // x-faces: face ix = W of element ix, E of element ix-1
+    const double* Z0 = in.ze(iy, ix) + sk;
+    const double* Z1 = in.ze(iy + 1, ix) + sk;
+    const double* Yb = inb.ye(iy, ix) + sj;
+    const double* Yt = intp.ye(iy, ix) + sj;
+    const double* fd = cf->fd[0] + sj + NI * sk;
+    double* oj = rq + CS<NI>::R_XJ + (iy * (TX + 1) + ix) * 2 * NI + 2 * sk + sj;   // over j, keep k
+    double* ok = rq + CS<NI>::R_XK + (iy * (TX + 1) + ix) * 2 * NI + 2 * sj + sk;   // over k, keep j
+#pragma unroll
+    for (int kk = 0; kk < M; ++kk) {
+      if (kk >= CK) continue;
+      const double zw = fma(gj, Z1[2 * kk], Z0[2 * kk]), ze = fma(gj, Z1[NI + 2 * kk], Z0[NI + 2 * kk]);
+      const double ek = cf->e[2][sk + 2 * kk], ak = cf->a[sk + 2 * kk];
+      double rwj = 0.0, rej = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < M; ++jj) {
+        if (jj >= CJ) continue;
+        const int o = 2 * jj + 2 * NI * kk;
+        const double w = W[o], e = E[o], f = fd[o], ej = cf->e[1][sj + 2 * jj], aj = cf->a[sj + 2 * jj];
+        const double yw = fma(gk, Yt[2 * jj], Yb[2 * jj]), ye = fma(gk, Yt[NI + 2 * jj], Yb[NI + 2 * jj]);
+        const double Wp = fma(f, w, fma(cf->k0p[0], e, fma(ej, zw, ek * yw)));
+        const double Ep = fma(f, e, fma(cf->k0p[0], w, fma(ej, ze, ek * ye)));
+        rwj = fma(aj, w, rwj);
+        rej = fma(aj, e, rej);
+        const double Em = __shfl_up_sync(0xffffffffu, Ep, 1);
+        if (act) {
+          fX[o] = ix > 0 ? Wp + Em : Wp;
+          if (lastx) fX[o + N2] = Ep;
+          if (kk == 0) {   // over k, keep j: one pass per j
+            double rwk = 0.0, rek = 0.0;
+#pragma unroll
+            for (int k2 = 0; k2 < M; ++k2)
+              if (k2 < CK) {
+                rwk = fma(cf->a[sk + 2 * k2], W[2 * jj + 2 * NI * k2], rwk);
+                rek = fma(cf->a[sk + 2 * k2], E[2 * jj + 2 * NI * k2], rek);
+              }
+            ok[4 * jj] = rwk;
+            if (lastx) ok[2 * NI + 4 * jj] = rek;
+          }
+        }
+      }
+      if (act) {
+        oj[4 * kk] = rwj;
+        if (lastx) oj[2 * NI + 4 * kk] = rej;
+        if (NI == 1) {   // no odd interior index: the odd parity components are 0
+          oj[1] = ok[1] = 0.0;
+          if (lastx) oj[2 * NI + 1] = ok[2 * NI + 1] = 0.0;
+        }
+      }
+      (void)ak;
+    }
+  }
+  if (sj == DO) {   // y-faces: face row iy = S of element row iy, N of row iy-1
+    const double* Z0 = in.ze(iy, ix) + sk;
+    const double* Z1 = in.ze(iy + 1, ix) + sk;
+    const double* Xb = inb.xe(iy, ix) + si;
+    const double* Xt = intp.xe(iy, ix) + si;
+    const double* fd = cf->fd[1] + si + NI * sk;
+    double* oi = rq + CS<NI>::R_YI + (iy * TX + ix) * 2 * NI + 2 * sk + si;   // over i, keep k
+    double* ok = rq + CS<NI>::R_YK + (iy * TX + ix) * 2 * NI + 2 * si + sk;   // over k, keep i
+#pragma unroll
+    for (int kk = 0; kk < M; ++kk) {
+      if (kk >= CK) continue;
+      const double zs = fma(gi, Z0[NI + 2 * kk], Z0[2 * kk]), zn = fma(gi, Z1[NI + 2 * kk], Z1[2 * kk]);
+      const double ek = cf->e[2][sk + 2 * kk];
+      double rsi = 0.0, rni = 0.0;
+#pragma unroll
+      for (int ii = 0; ii < M; ++ii) {
+        if (ii >= CI) continue;
+        const int o = 2 * ii + 2 * NI * kk;
+        const double sv = S[o], nv = N[o], f = fd[o], ei_ = cf->e[0][si + 2 * ii], ai = cf->a[si + 2 * ii];
+        const double xs = fma(gk, Xt[2 * ii], Xb[2 * ii]), xn = fma(gk, Xt[TX * NI + 2 * ii], Xb[TX * NI + 2 * ii]);
+        const double Sp = fma(f, sv, fma(cf->k0p[1], nv, fma(ei_, zs, ek * xs)));
+        const double Np = fma(f, nv, fma(cf->k0p[1], sv, fma(ei_, zn, ek * xn)));
+        rsi = fma(ai, sv, rsi);
+        rni = fma(ai, nv, rni);
+        const double Nm = __shfl_up_sync(0xffffffffu, Np, TX);
+        if (act) {
+          fY[o] = iy > 0 ? Sp + Nm : Sp;
+          if (lasty) fY[o + TX * N2] = Np;
+          if (kk == 0) {
+            double rsk = 0.0, rnk = 0.0;
+#pragma unroll
+            for (int k2 = 0; k2 < M; ++k2)
+              if (k2 < CK) {
+                rsk = fma(cf->a[sk + 2 * k2], S[2 * ii + 2 * NI * k2], rsk);
+                rnk = fma(cf->a[sk + 2 * k2], N[2 * ii + 2 * NI * k2], rnk);
+              }
+            ok[4 * ii] = rsk;
+            if (lasty) ok[TX * 2 * NI + 4 * ii] = rnk;
+          }
+        }
+      }
+      if (act) {
+        oi[4 * kk] = rsi;
+        if (lasty) oi[TX * 2 * NI + 4 * kk] = rni;
+        if (NI == 1) {
+          oi[1] = ok[1] = 0.0;
+          if (lasty) oi[TX * 2 * NI + 1] = ok[TX * 2 * NI + 1] = 0.0;
+        }
+      }
+    }
+  }
+  if (sk == DO && act) {   // z-faces: B of this layer (plane l), T (plane l+1)
+    const double* Yb = inb.ye(iy, ix) + sj;
+    const double* Yt = intp.ye(iy, ix) + sj;
+    const double* Xb = inb.xe(iy, ix) + si;
+    const double* Xt = intp.xe(iy, ix) + si;
+    const double* fd = cf->fd[2] + si + NI * sj;
+    constexpr int PO = CS<NI>::NE * 2 * NI;
+    double* oi = rq + CS<NI>::R_ZI + (iy * TX + ix) * 2 * NI + 2 * sj + si;    // over i, keep j (l+1 at + PO)
+    double* oj = rq + CS<NI>::R_ZJ + (iy * TX + ix) * 2 * NI + 2 * si + sj;    // over j, keep i
+#pragma unroll
+    for (int jj = 0; jj < M; ++jj) {
+      if (jj >= CJ) continue;
+      const double yb = fma(gi, Yb[NI + 2 * jj], Yb[2 * jj]), yt = fma(gi, Yt[NI + 2 * jj], Yt[2 * jj]);
+      const double ej = cf->e[1][sj + 2 * jj], aj = cf->a[sj + 2 * jj];
+      double rbi = 0.0, rti = 0.0;
+#pragma unroll
+      for (int ii = 0; ii < M; ++ii) {
+        if (ii >= CI) continue;
+        const int o = 2 * ii + 2 * NI * jj;
+        const double bv = B[o], tv = T[o], f = fd[o], ei_ = cf->e[0][si + 2 * ii], ai = cf->a[si + 2 * ii];
+        const double xb = fma(gj, Xb[TX * NI + 2 * ii], Xb[2 * ii]), xt = fma(gj, Xt[TX * NI + 2 * ii], Xt[2 * ii]);
+        fB[o] += fma(f, bv, fma(cf->k0p[2], tv, fma(ei_, yb, ej * xb)));
+        fT[o] = fma(f, tv, fma(cf->k0p[2], bv, fma(ei_, yt, ej * xt)));
+        rbi = fma(ai, bv, rbi);
+        rti = fma(ai, tv, rti);
+        if (jj == 0) {
+          double rbj = 0.0, rtj = 0.0;
+#pragma unroll
+          for (int j2 = 0; j2 < M; ++j2)
+            if (j2 < CJ) {
+              rbj = fma(cf->a[sj + 2 * j2], B[2 * ii + 2 * NI * j2], rbj);
+              rtj = fma(cf->a[sj + 2 * j2], T[2 * ii + 2 * NI * j2], rtj);
+            }
+          oj[4 * ii] = rbj;
+          oj[PO + 4 * ii] = rtj;
+        }
+      }
+      oi[4 * jj] = rbi;
+      oi[PO + 4 * jj] = rti;
+      if (NI == 1) oi[1] = oi[PO + 1] = oj[1] = oj[PO + 1] = 0.0;
+      (void)aj;
+    }
+  }
+
+  // ---- phase B: condensed part of the class (registers only)
+  const double* Dv = cf->dinv + si + NI * sj + N2 * sk;
+  double qx[M][M], qy[M][M], qz[M][M];
+  {
+    double c1[M], c2[M], c3[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      c1[m] = cf->c[0][si + 2 * m];
+      c2[m] = cf->c[1][sj + 2 * m];
+      c3[m] = cf->c[2][sk + 2 * m];
+    }
+    double py[M][M];
+#pragma unroll
+    for (int ii = 0; ii < M; ++ii)
+#pragma unroll
+      for (int kk = 0; kk < M; ++kk) {
+        py[ii][kk] = (ii < CI && kk < CK) ? fma(gj, N[2 * ii + 2 * NI * kk], S[2 * ii + 2 * NI * kk]) : 0.0;
+        qy[ii][kk] = 0.0;
+      }
+#pragma unroll
+    for (int jj = 0; jj < M; ++jj) {
+#pragma unroll
+      for (int kk = 0; kk < M; ++kk) qx[jj][kk] = 0.0;
+#pragma unroll
+      for (int ii = 0; ii < M; ++ii) qz[jj][ii] = 0.0;
+      if (jj >= CJ) continue;
+      double px[M], pz[M];
+#pragma unroll
+      for (int kk = 0; kk < M; ++kk)
+        px[kk] = kk < CK ? fma(gi, E[2 * jj + 2 * NI * kk], W[2 * jj + 2 * NI * kk]) : 0.0;
+#pragma unroll
+      for (int ii = 0; ii < M; ++ii)
+        pz[ii] = ii < CI ? fma(gk, T[2 * ii + 2 * NI * jj], B[2 * ii + 2 * NI * jj]) : 0.0;
+#pragma unroll
+      for (int ii = 0; ii < M; ++ii) {
+        if (ii >= CI) continue;
+#pragma unroll
+        for (int kk = 0; kk < M; ++kk) {
+          if (kk >= CK) continue;
+          const double u = fma(c1[ii], px[kk], fma(c2[jj], py[ii][kk], c3[kk] * pz[ii]));
+          const double v = u * Dv[2 * ii + 2 * NI * jj + 2 * N2 * kk];
+          qx[jj][kk] = fma(c1[ii], v, qx[jj][kk]);
+          qy[ii][kk] = fma(c2[jj], v, qy[ii][kk]);
+          qz[jj][ii] = fma(c3[kk], v, qz[jj][ii]);
+        }
+      }
+    }
+  }
+  // ---- output rounds: barrier (phase A complete), then round r of direction d by the classes
+  // with s_d == r; W -= Q^0 + Q^1, E -= Q^0 - Q^1 (two elements of a face summed by shuffle).
+#pragma unroll 1
+  for (int r = 0; r < 2; ++r) {
+    bar_named(1);
+    if (r == si) {
+#pragma unroll
+      for (int jj = 0; jj < M; ++jj) {
+        if (jj >= CJ) continue;
+#pragma unroll
+        for (int kk = 0; kk < M; ++kk) {
+          if (kk >= CK) continue;
+          const int o = 2 * jj + 2 * NI * kk;
+          const double Q = qx[jj][kk];
+          const double Qm = __shfl_up_sync(0xffffffffu, Q, 1);
+          if (act) {
+            fX[o] -= ix > 0 ? fma(gi, Qm, Q) : Q;
+            if (lastx) fX[o + N2] -= gi * Q;
+          }
+        }
+      }
+    }
+    if (r == sj) {
+#pragma unroll
+      for (int ii = 0; ii < M; ++ii) {
+        if (ii >= CI) continue;
+#pragma unroll
+        for (int kk = 0; kk < M; ++kk) {
+          if (kk >= CK) continue;
+          const int o = 2 * ii + 2 * NI * kk;
+          const double Q = qy[ii][kk];
+          const double Qm = __shfl_up_sync(0xffffffffu, Q, TX);
+          if (act) {
+            fY[o] -= iy > 0 ? fma(gj, Qm, Q) : Q;
+            if (lasty) fY[o + TX * N2] -= gj * Q;
+          }
+        }
+      }
+    }
+    if (r == sk && act) {
+#pragma unroll
+      for (int jj = 0; jj < M; ++jj) {
+        if (jj >= CJ) continue;
+#pragma unroll
+        for (int ii = 0; ii < M; ++ii) {
+          if (ii >= CI) continue;
+          const int o = 2 * ii + 2 * NI * jj;
+          const double Q = qz[jj][ii];
+          fB[o] -= Q;
+          fT[o] -= gk * Q;
+        }
+      }
+    }
+  }
+}
+
+// warps w and w+4 share an SM sub-partition: pair the largest class with the smallest (class
+// bits s_i s_j s_k; at n_I = 7 the point counts are 64+27, 48+36, 48+36, 48+36).
+__device__ __constant__ int kWarpClass[8] = {0, 1, 2, 4, 7, 6, 5, 3};
+
+template <int NI>
+__global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ ColParams P) {
   using C = CS<NI>;
-  constexpr int N2 = C::N2, TX = C::TX, TY = C::TY, NT = C::NT, LPE = C::LPE, JS = C::JS, JH = C::JH;
+  constexpr int N2 = C::N2, TX = C::TX, TY = C::TY, NT = C::NT;
   if (P.done != nullptr && *P.done != 0.0) return;
   const Geom& g = P.g;
   extern __shared__ double sm[];
-  double* sDinv = sm + C::O_DINV;
-  double* sD = sm + C::O_D;
   double* sA0 = sm + C::O_TAB;
-  double* sLam = sA0 + 64;
+  double* sLam = sA0 + 32;
+  ColCoef* sCf = reinterpret_cast<ColCoef*>(sm + C::O_CF);
   double* const rq = sm + C::O_RQ;
   __shared__ unsigned long long sTicket;
   __shared__ int sEpoch;
   const int tid = threadIdx.x;
   if (tid == 0) sEpoch = *(volatile int*)&P.st->epoch + 1;
   long long ph_t0 = clock64();
+  (void)ph_t0;
   Addr A{g};
   const double K00 = g.tab[TAB_SCAL + 0], K0p = g.tab[TAB_SCAL + 1], w0 = g.tab[TAB_SCAL + 2];
   const double w02 = w0 * w0;
+  const double dA = g.d_uni[0], dB = g.d_uni[1], dC = g.d_uni[2], dD = g.d_uni[3];
+  for (int t = tid; t < (int)(sizeof(ColCoef) / sizeof(double)); t += NT)
+    sm[C::O_CF + t] = reinterpret_cast<const double*>(&P.cf)[t];
   for (int t = tid; t < NI; t += NT) {
     sA0[t] = g.tab[TAB_A0 + t];
     sLam[t] = g.tab[TAB_LAM + t];
   }
-  if (UNIFORM)
-    for (int t = tid; t < C::DINV; t += NT) sDinv[t] = g.dinv[t];
   // padding entries of y are written as 0 by the first CTA
   if (blockIdx.x == 0) {
     long long ends[7] = {g.off_f[0] + g.n_f[0] * N2, g.off_f[1] + g.n_f[1] * N2, g.off_f[2] + g.n_f[2] * N2,
@@ -421,18 +720,16 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
       for (long long i = ends[q] + tid; i < nexts[q]; i += NT) P.y[i] = 0.0;
   }
   Side<NI> ac{sm + C::O_AS};
-  // ---- per-thread constants of the volume phase: thread (e, k)
-  const int ve = tid / (LPE * JS), vk = tid % LPE, vjh = (tid / LPE) % JS;
-  const bool vact = vk < NI;
-  const int vix = ve % TX, viy = ve / TX;
-  const double sk = (vk & 1) ? -1.0 : 1.0;
-  const int kk = vact ? vk : 0;
   // ---- lane tables of the edge / vertex primary part (no runtime division in the node loops)
   constexpr int NW = NT / 32;
   constexpr int EPW = 32 / NI;                               // edges per warp pass
   const int warp = tid >> 5, lane = tid & 31;
+  const int vix = lane % TX, viy = lane / TX;                // element of this lane (condensed part)
   const int esub = lane / NI, ec = lane % NI;
   const bool evalid = lane < EPW * NI;
+  // face-pass constants
+  const double cx0 = dA * w0 + dB * K00, cy0 = dA * w0 + dC * K00, cz0 = dA * w0 + dD * K00;
+  const double d1w0 = dB * w0, d2w0 = dC * w0, d3w0 = dD * w0;
 
   for (;;) {
     __syncthreads();
@@ -448,7 +745,6 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
     const int* const flag_w = tx > 0 ? P.flags + (item - 1) * (g.nz + 1) : nullptr;
     const int* const flag_s = ty > 0 ? P.flags + (item - P.ntx) * (g.nz + 1) : nullptr;
     const int* const flag_sw = (tx > 0 && ty > 0) ? P.flags + (item - P.ntx - 1) * (g.nz + 1) : nullptr;
-    const bool eact = vact && vix < tw && viy < th;
 
     // prologue: planes 0, 1 and side 0 as one cp.async group
     load_plane<NI>(P, Plane<NI>{sm + C::O_IP}, x0, y0, tw, th, 0);
@@ -469,224 +765,31 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
       __syncthreads();
       SC_PHASE(0);
       if (!last) {
-        for (int t = tid; t < C::SIDE; t += NT) ac.b[t] = 0.0;
-        for (int t = tid; t < C::PLANE; t += NT) actp.b[t] = 0.0;
-        if (UNIFORM) {
-          for (int t = tid; t < 4 * C::NE; t += NT) sD[t] = g.d_uni[t & 3];
-        } else {
-          for (int t = tid; t < C::NE; t += NT) {
-            int ex = x0 + min(t % TX, tw - 1), ey = y0 + min(t / TX, th - 1);
-            double d[4];
-            metric(g, ex, ey, l, d);
-            for (int q = 0; q < 4; ++q) sD[t * 4 + q] = d[q];
-          }
-        }
-        __syncthreads();
-        SC_PHASE(1);
-#if !defined(SC_EXP) || SC_EXP != 3
-        // ============ condensed part (faces-in, D^{-1}, faces-out; even / odd form of Table 2)
-        //              fused with the primary part of the element's x- and y-faces ============
-        // Thread (e, jh, k): k-plane of element e, rows j = 2 jj + jh (all of one parity, so
-        // sigma_j is a per-thread constant and the y-reduction yields one parity class).
+        // accumulators written with += below: z-edges of the side, edges / vertices of plane l+1
+        for (int t = tid; t < C::ZE; t += NT) ac.b[C::S_ZE + t] = 0.0;
+        for (int t = tid; t < C::PLANE - C::PZF; t += NT) actp.b[C::P_XE + t] = 0.0;
+        // even / odd line sums of the edges (the faces' line sums come from the class warps)
         {
-          const double* d = sD + ve * 4;
-          const double d0 = d[0], d1 = d[1], d2 = d[2], d3 = d[3];
-          const double ak = eact ? sA0[kk] : 0.0;
-          const double akd3 = ak * d3;
-          const double lamk = sLam[kk];
-          const double sj = (JS == 2 && vjh) ? -1.0 : 1.0;
-          double pxp[JH], pxm[JH], ajr[JH], py[NI];
-          double qxp[JH], qxm[JH], qy[NI];
-          const double* W = in.xf(viy, vix);
-          const double* E = in.xf(viy, vix + 1);
-          const double* S = in.yf(viy, vix);
-          const double* N = in.yf(viy + 1, vix);
-          const double* B = inb.zf(viy, vix);
-          const double* T = intp.zf(viy, vix);
-#pragma unroll
-          for (int jj = 0; jj < JH; ++jj) {
-            const int j = JS * jj + vjh;
-            const bool ok = eact && j < NI;
-            const double w = ok ? W[j + NI * kk] : 0.0, e = ok ? E[j + NI * kk] : 0.0;
-            pxp[jj] = d1 * (w + e);
-            pxm[jj] = d1 * (w - e);
-            ajr[jj] = ok ? sA0[j] : 0.0;
-            qxp[jj] = qxm[jj] = 0.0;
-          }
-#pragma unroll
-          for (int i = 0; i < NI; ++i) {
-            py[i] = eact ? d2 * fma(sj, N[i + NI * kk], S[i + NI * kk]) : 0.0;
-            qy[i] = 0.0;
-          }
-          double* const qz = rq;
-#pragma unroll
-          for (int jj = 0; jj < JH; ++jj) {
-            const int j = min(JS * jj + vjh, NI - 1);
-            const bool jok = (JS * jj + vjh) < NI;
-            const double aj = ajr[jj];
-            const double* Bj = B + NI * j;
-            const double* Tj = T + NI * j;
-            const double* Dj = sDinv + NI * j + N2 * kk;
-#pragma unroll
-            for (int i = 0; i < NI; ++i) {
-              const double pz = fma(sk, Tj[i], Bj[i]);
-              const double u = fma(sA0[i], (i & 1) ? pxm[jj] : pxp[jj], fma(aj, py[i], akd3 * pz));
-              double v;
-              if (UNIFORM) v = u * Dj[i];
-              else v = u / (d0 + d1 * sLam[i] + d2 * sLam[j] + d3 * lamk);
-              if (i & 1) qxm[jj] = fma(sA0[i], v, qxm[jj]); else qxp[jj] = fma(sA0[i], v, qxp[jj]);
-              qy[i] = fma(aj, v, qy[i]);
-              double c = ak * v;
-              if (LPE >= 4) c += __shfl_xor_sync(0xffffffffu, c, 2);
-              if (LPE >= 8) c += __shfl_xor_sync(0xffffffffu, c, 4);
-              if (vk < 2 && eact && jok) qz[(ve * 2 + vk) * N2 + i + NI * j] = c;
-            }
-          }
-          // y-reduction: this thread holds Q_y^{sigma = (-1)^jh}(i) for all i; fetch the other class
-          double qyo[NI];
-#pragma unroll
-          for (int i = 0; i < NI; ++i) qyo[i] = (JS == 2) ? __shfl_xor_sync(0xffffffffu, qy[i], LPE) : 0.0;
-          // primary part of the element's four side faces at this k (Eq. 26 generalised):
-          //   W/E node (j,k): (d0 w0 + d1 K00 + d2 w0 Lam_j + d3 w0 Lam_k) u + d1 K0p u_opp
-          //                   + d2 w0 a0_j (Z(ib,0)[k] + s_j Z(ib,1)[k]) + d3 w0 a0_k (Y(ib,0)[j] + s_k Y(ib,1)[j])
-          //   S/N node (i,k): (d0 w0 + d1 w0 Lam_i + d2 K00 + d3 w0 Lam_k) u + d2 K0p u_opp
-          //                   + d1 w0 a0_i (Z(0,jb)[k] + s_i Z(1,jb)[k]) + d3 w0 a0_k (X(jb,0)[i] + s_k X(jb,1)[i])
-          // This thread owns rows j = i = 2 jj + jh of the four faces.
-          const double z00 = in.ze(viy, vix)[kk], z10 = in.ze(viy, vix + 1)[kk];
-          const double z01 = in.ze(viy + 1, vix)[kk], z11 = in.ze(viy + 1, vix + 1)[kk];
-          const double base = d0 * w0 + d3 * w0 * lamk;
-          const double wak = d3 * w0 * ak;
-          double oW[JH], oE[JH], oS[JH], oN[JH];
-#pragma unroll
-          for (int jj = 0; jj < JH; ++jj) {
-            const int r = min(JS * jj + vjh, NI - 1);         // row index (j for W/E, i for S/N)
-            const double ar = sA0[r], lr = sLam[r];
-            const double w = W[r + NI * kk], e = E[r + NI * kk], s = S[r + NI * kk], n = N[r + NI * kk];
-            const double dxy = base + d1 * K00 + d2 * w0 * lr;
-            const double dyx = base + d2 * K00 + d1 * w0 * lr;
-            oW[jj] = dxy * w + d1 * K0p * e + d2 * w0 * ar * fma(sj, z01, z00) +
-                     wak * fma(sk, intp.ye(viy, vix)[r], inb.ye(viy, vix)[r]);
-            oE[jj] = dxy * e + d1 * K0p * w + d2 * w0 * ar * fma(sj, z11, z10) +
-                     wak * fma(sk, intp.ye(viy, vix + 1)[r], inb.ye(viy, vix + 1)[r]);
-            oS[jj] = dyx * s + d2 * K0p * n + d1 * w0 * ar * fma(sj, z10, z00) +
-                     wak * fma(sk, intp.xe(viy, vix)[r], inb.xe(viy, vix)[r]);
-            oN[jj] = dyx * n + d2 * K0p * s + d1 * w0 * ar * fma(sj, z11, z01) +
-                     wak * fma(sk, intp.xe(viy + 1, vix)[r], inb.xe(viy + 1, vix)[r]);
-          }
-          // outputs: low faces first, high faces after a barrier (race-free accumulation)
-          double qyp_r[JH], qym_r[JH];
-#pragma unroll
-          for (int jj = 0; jj < JH; ++jj) {
-            const int i0 = min(JS * jj, NI - 1), i1 = min(JS * jj + 1, NI - 1);
-            // row i = 2 jj + jh: Q+ is held by the jh = 0 thread, Q- by the jh = 1 thread
-            qyp_r[jj] = (JS == 1 || vjh == 0) ? qy[i0] : qyo[i1];
-            qym_r[jj] = (JS == 1) ? 0.0 : (vjh == 0 ? qyo[i0] : qy[i1]);
-          }
-          if (eact) {
-            double* aW = ac.xf(viy, vix);
-            double* aS = ac.yf(viy, vix);
-#pragma unroll
-            for (int jj = 0; jj < JH; ++jj) {
-              const int r = JS * jj + vjh;
-              if (r >= NI) continue;
-              aW[r + NI * kk] += oW[jj] - d1 * (qxp[jj] + qxm[jj]);
-              aS[r + NI * kk] += oS[jj] - d2 * (qyp_r[jj] + qym_r[jj]);
-            }
-          }
-          __syncthreads();
-          SC_PHASE(2);
-          if (eact) {
-            double* aE = ac.xf(viy, vix + 1);
-            double* aN = ac.yf(viy + 1, vix);
-#pragma unroll
-            for (int jj = 0; jj < JH; ++jj) {
-              const int r = JS * jj + vjh;
-              if (r >= NI) continue;
-              aE[r + NI * kk] += oE[jj] - d1 * (qxp[jj] - qxm[jj]);
-              aN[r + NI * kk] += oN[jj] - d2 * (qyp_r[jj] - qym_r[jj]);
-            }
-          }
-        }
-        __syncthreads();
-        SC_PHASE(3);
-#endif
-#if !defined(SC_EXP) || SC_EXP != 4
-        // z outputs: B -= d3 (Q+ + Q-), T -= d3 (Q+ - Q-), plus the primary part of the element's
-        // B and T faces: (d0 w0 + d1 w0 Lam_i + d2 w0 Lam_j + d3 K00) u + d3 K0p u_opp
-        //   + d1 w0 a0_i (Y(0,kb)[j] + s_i Y(1,kb)[j]) + d2 w0 a0_j (X(0,kb)[i] + s_j X(1,kb)[i])
-        for (int t = tid; t < C::NE * N2; t += NT) {
-          const int e = t / N2, q = t % N2, ix = e % TX, iy = e / TX;
-          if (ix >= tw || iy >= th) continue;
-          const int a = q % NI, b = q / NI;
-          const double* d = sD + e * 4;
-          const double qp = rq[(e * 2) * N2 + q], qm = NI > 1 ? rq[(e * 2 + 1) * N2 + q] : 0.0;
-          const double ub = inb.zf(iy, ix)[q], ut = intp.zf(iy, ix)[q];
-          const double sa = (a & 1) ? -1.0 : 1.0, sb = (b & 1) ? -1.0 : 1.0;
-          const double dz = d[0] * w0 + (d[1] * sLam[a] + d[2] * sLam[b]) * w0 + d[3] * K00;
-          const double c1 = d[1] * w0 * sA0[a], c2 = d[2] * w0 * sA0[b];
-          const double pb = dz * ub + d[3] * K0p * ut + c1 * fma(sa, inb.ye(iy, ix + 1)[b], inb.ye(iy, ix)[b]) +
-                            c2 * fma(sb, inb.xe(iy + 1, ix)[a], inb.xe(iy, ix)[a]);
-          const double pt = dz * ut + d[3] * K0p * ub + c1 * fma(sa, intp.ye(iy, ix + 1)[b], intp.ye(iy, ix)[b]) +
-                            c2 * fma(sb, intp.xe(iy + 1, ix)[a], intp.xe(iy, ix)[a]);
-          acb.zf(iy, ix)[q] += pb - d[3] * (qp + qm);
-          actp.zf(iy, ix)[q] += pt - d[3] * (qp - qm);
-        }
-        __syncthreads();
-        SC_PHASE(4);
-#endif
-        // ============ even / odd line reductions of faces and edges (primary part) ============
-#if !defined(SC_EXP) || SC_EXP != 2
-        {
-          constexpr int NXR = TY * (TX + 1) * NI, NYR = (TY + 1) * TX * NI, NZR = TY * TX * NI;
           constexpr int NZE = (TY + 1) * (TX + 1), NXE = (TY + 1) * TX, NYE = TY * (TX + 1);
-          constexpr int TOT = 2 * NXR + 2 * NYR + 4 * NZR + NZE + 2 * NXE + 2 * NYE;
-          for (int t = tid; t < TOT; t += NT) {
+          for (int t = tid; t < NZE + 2 * NXE + 2 * NYE; t += NT) {
             int r = t;
-            if (r < 2 * NXR) {                       // x-face (iy, ix): over j (keep k = c) / over k (keep j = c)
-              const int dir = r / NXR, rr = r % NXR, c = rr % NI, f = rr / NI;
-              const double* F = in.b + C::S_XF + f * N2;
-              double* o = rq + (dir == 0 ? C::R_XJ : C::R_XK) + f * 2 * NI;
-              eo_reduce<NI>(dir == 0 ? F + NI * c : F + c, dir == 0 ? 1 : NI, sA0, o + 2 * c);
-              continue;
-            }
-            r -= 2 * NXR;
-            if (r < 2 * NYR) {                       // y-face (iy, ix): over i (keep k) / over k (keep i)
-              const int dir = r / NYR, rr = r % NYR, c = rr % NI, f = rr / NI;
-              const double* F = in.b + C::S_YF + f * N2;
-              double* o = rq + (dir == 0 ? C::R_YI : C::R_YK) + f * 2 * NI;
-              eo_reduce<NI>(dir == 0 ? F + NI * c : F + c, dir == 0 ? 1 : NI, sA0, o + 2 * c);
-              continue;
-            }
-            r -= 2 * NYR;
-            if (r < 4 * NZR) {                       // z-face plane kb: over i (keep j) / over j (keep i)
-              const int dir = r / (2 * NZR), rr = r % (2 * NZR), kb = rr / NZR, r3 = rr % NZR, c = r3 % NI,
-                        f = r3 / NI;
-              const double* F = (kb ? intp : inb).b + C::P_ZF + f * N2;
-              double* o = rq + (dir == 0 ? C::R_ZI : C::R_ZJ) + (kb * TY * TX + f) * 2 * NI;
-              eo_reduce<NI>(dir == 0 ? F + NI * c : F + c, dir == 0 ? 1 : NI, sA0, o + 2 * c);
-              continue;
-            }
-            r -= 4 * NZR;
-            if (r < NZE) {                           // z-edges of layer l
-              eo_reduce<NI>(in.b + C::S_ZE + r * NI, 1, sA0, rq + C::R_ZE + r * 2);
-              continue;
-            }
+            if (r < NZE) { eo_reduce<NI>(in.b + C::S_ZE + r * NI, 1, sA0, rq + C::R_ZE + r * 2); continue; }
             r -= NZE;
-            if (r < 2 * NXE) {                       // x-edges of planes l, l+1
-              const int kb = r / NXE, e = r % NXE;
+            if (r < 2 * NXE) {
+              const int kb = r / NXE, e = r - kb * NXE;
               eo_reduce<NI>((kb ? intp : inb).b + C::P_XE + e * NI, 1, sA0, rq + C::R_XE + r * 2);
               continue;
             }
             r -= 2 * NXE;
-            {                                        // y-edges of planes l, l+1
-              const int kb = r / NYE, e = r % NYE;
-              eo_reduce<NI>((kb ? intp : inb).b + C::P_YE + e * NI, 1, sA0, rq + C::R_YE + r * 2);
-            }
+            const int kb = r / NYE, e = r - kb * NYE;
+            eo_reduce<NI>((kb ? intp : inb).b + C::P_YE + e * NI, 1, sA0, rq + C::R_YE + r * 2);
           }
         }
+        SC_PHASE(1);
+        // ============ condensed part: parity-class warps, two output rounds ============
+        vol_class<NI>(kWarpClass[warp], sCf, in, inb, intp, ac, acb, actp, rq, vix, viy, tw, th);
         __syncthreads();
-        SC_PHASE(5);
-#endif
+        SC_PHASE(2);
         // ============ primary part Htilde_BB, entity-centric over the tile's elements ============
 #if !defined(SC_EXP) || SC_EXP != 2
         // (Mtilde = diag(w0, 1..1, w0); Ktilde arrowhead: row 0 = (K00, a0, K0p),
@@ -696,7 +799,6 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
         // exactly one lane, which sums the contributions of the tile's adjacent elements.
         {
           auto present = [&](int ix, int iy) { return ix >= 0 && iy >= 0 && ix < tw && iy < th; };
-          auto dd = [&](int ix, int iy) { return sD + (iy * TX + ix) * 4; };
           // ---- z-edges (fx = ix, fy = iy), coord k = c
           for (int e0 = warp * EPW; e0 < (TY + 1) * (TX + 1); e0 += NW * EPW) {
             const int e = e0 + esub, ix = e % (TX + 1), iy = e / (TX + 1), c = ec;
@@ -708,12 +810,12 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
             for (int el = 0; el < 4; ++el) {
               const int ib = el & 1, jb = el >> 1, ex = ix - ib, ey = iy - jb;
               if (!present(ex, ey)) continue;
-              const double* d = dd(ex, ey);
+              
               const double txl = (ib ? K0p : K00) * in.ze(iy, ex)[c] + (ib ? K00 : K0p) * in.ze(iy, ex + 1)[c] +
                                  eo_row(rq + C::R_YI + (iy * TX + ex) * 2 * NI + 2 * c, ib);
               const double tyl = (jb ? K0p : K00) * in.ze(ey, ix)[c] + (jb ? K00 : K0p) * in.ze(ey + 1, ix)[c] +
                                  eo_row(rq + C::R_XJ + (ey * (TX + 1) + ix) * 2 * NI + 2 * c, jb);
-              y += d[0] * w02 * u + d[1] * w0 * txl + d[2] * w0 * tyl + d[3] * w02 * tz;
+              y += dA * w02 * u + dB * w0 * txl + dC * w0 * tyl + dD * w02 * tz;
             }
             ac.ze(iy, ix)[c] += y;
           }
@@ -732,10 +834,10 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
             for (int el = 0; el < 2; ++el) {
               const int jb = el, ey = iy - jb;
               if (!present(ix, ey)) continue;
-              const double* d = dd(ix, ey);
+              
               const double tyl = (jb ? K0p : K00) * pk.xe(ey, ix)[c] + (jb ? K00 : K0p) * pk.xe(ey + 1, ix)[c] +
                                  eo_row(rq + C::R_ZJ + (kb * TY * TX + ey * TX + ix) * 2 * NI + 2 * c, jb);
-              y += d[0] * w02 * u + d[1] * w02 * txl + d[2] * w0 * tyl + d[3] * w0 * tzl;
+              y += dA * w02 * u + dB * w02 * txl + dC * w0 * tyl + dD * w0 * tzl;
             }
             (kb ? actp : acb).xe(iy, ix)[c] += y;
           }
@@ -755,10 +857,10 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
             for (int el = 0; el < 2; ++el) {
               const int ib = el, ex = ix - ib;
               if (!present(ex, iy)) continue;
-              const double* d = dd(ex, iy);
+              
               const double txl = (ib ? K0p : K00) * pk.ye(iy, ex)[c] + (ib ? K00 : K0p) * pk.ye(iy, ex + 1)[c] +
                                  eo_row(rq + C::R_ZI + (kb * TY * TX + iy * TX + ex) * 2 * NI + 2 * c, ib);
-              y += d[0] * w02 * u + d[1] * w0 * txl + d[2] * w02 * tyl + d[3] * w0 * tzl;
+              y += dA * w02 * u + dB * w0 * txl + dC * w02 * tyl + dD * w0 * tzl;
             }
             (kb ? actp : acb).ye(iy, ix)[c] += y;
           }
@@ -776,12 +878,12 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
             for (int el = 0; el < 4; ++el) {
               const int ib = el & 1, jb = el >> 1, ex = ix - ib, ey = iy - jb;
               if (!present(ex, ey)) continue;
-              const double* d = dd(ex, ey);
+              
               const double txl = (ib ? K0p : K00) * *pk.vv(iy, ex) + (ib ? K00 : K0p) * *pk.vv(iy, ex + 1) +
                                  eo_row(rq + C::R_XE + (kb * (TY + 1) * TX + iy * TX + ex) * 2, ib);
               const double tyl = (jb ? K0p : K00) * *pk.vv(ey, ix) + (jb ? K00 : K0p) * *pk.vv(ey + 1, ix) +
                                  eo_row(rq + C::R_YE + (kb * TY * (TX + 1) + ey * (TX + 1) + ix) * 2, jb);
-              y += d[0] * w02 * w0 * u + w02 * (d[1] * txl + d[2] * tyl + d[3] * tzl);
+              y += dA * w02 * w0 * u + w02 * (dB * txl + dC * tyl + dD * tzl);
             }
             *(kb ? actp : acb).vv(iy, ix) += y;
           }
@@ -991,14 +1093,16 @@ __global__ void __launch_bounds__(256, 2) k_apply_col(ColParams P) {
   }
 }
 
-template <int NI, bool U>
-static int launch_col_u(const ColParams& P, cudaStream_t st, int* nl, int* grid_out) {
+
+template <int NI>
+static int launch_col_t(const ColParams& P, cudaStream_t st, int* nl, int* grid_out) {
   using C = CS<NI>;
+  static_assert(sizeof(double) * C::TOTAL <= 227 * 1024, "shared memory budget");
   const size_t smem = sizeof(double) * C::TOTAL;
   static int max_active = -1, nsm = 0;
   if (max_active < 0) {
-    cudaFuncSetAttribute(k_apply_col<NI, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_active, k_apply_col<NI, U>, C::NT, smem);
+    cudaFuncSetAttribute(k_apply_col<NI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_active, k_apply_col<NI>, C::NT, smem);
     int dev;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -1007,14 +1111,9 @@ static int launch_col_u(const ColParams& P, cudaStream_t st, int* nl, int* grid_
   int grid = max_active * nsm;
   if (grid > P.nitems) grid = P.nitems;
   *grid_out = grid;
-  k_apply_col<NI, U><<<grid, C::NT, smem, st>>>(P);
+  k_apply_col<NI><<<grid, C::NT, smem, st>>>(P);
   (*nl)++;
   return cudaGetLastError();
-}
-
-template <int NI>
-static int launch_col_t(const ColParams& P, cudaStream_t st, int* nl, int* grid_out) {
-  return P.g.dinv ? launch_col_u<NI, true>(P, st, nl, grid_out) : launch_col_u<NI, false>(P, st, nl, grid_out);
 }
 
 #if defined(SC_EXP) && SC_EXP == 9
@@ -1023,27 +1122,44 @@ extern "C" int sc_exp_phase_cycles(unsigned long long* out) {
 }
 #endif
 
-bool col_supported(int ni) { return ni >= 1 && ni <= 8; }
+bool col_supported(int ni) { return ni >= 1 && ni <= 7; }
 
 void col_tile(int ni, int* tx, int* ty, int* pend) {
   switch (ni) {
 #define TCASE(N) case N: *tx = CS<N>::TX; *ty = CS<N>::TY; *pend = CS<N>::PEND; return;
-    TCASE(1) TCASE(2) TCASE(3) TCASE(4) TCASE(5) TCASE(6) TCASE(7) TCASE(8)
+    TCASE(1) TCASE(2) TCASE(3) TCASE(4) TCASE(5) TCASE(6) TCASE(7)
 #undef TCASE
     default: *tx = *ty = *pend = 0;
   }
 }
 
-int launch_apply_col(const ColParams& P, void* stream, int* nl, int* grid_out, void* events);
-
-int launch_apply_col_raw(const Geom& g, const double* x, double* y, const double* done, void* state, int* flags,
-                         double* corner, double* pending, int ntx, int nty, void* stream, int* nl, void* events) {
-  ColParams P;
-  P.g = g; P.x = x; P.y = y; P.done = done; P.st = (ColState*)state; P.flags = flags; P.corner = corner;
-  P.pending = pending;
-  P.ntx = ntx; P.nty = nty; P.nitems = ntx * nty;
-  int grid = 0;
-  return launch_apply_col(P, stream, nl, &grid, events);
+// Host-side coefficient block of the uniform-geometry kernel (c[d][m] = d_{d+1} a0_m, D^{-1}).
+void col_make_coef(int ni, const double* d, const double* a0, const double* lam, double K00, double K0p, double w0,
+                   std::vector<unsigned char>& out) {
+  ColCoef cf;
+  memset(&cf, 0, sizeof(cf));
+  for (int m = 0; m < ni && m < 8; ++m) {
+    cf.a[m] = a0[m];
+    for (int q = 0; q < 3; ++q) {
+      cf.c[q][m] = d[q + 1] * a0[m];
+      cf.e[q][m] = d[q + 1] * w0 * a0[m];
+    }
+  }
+  for (int q = 0; q < 3; ++q) cf.k0p[q] = d[q + 1] * K0p;
+  if (ni <= 8)
+    for (int b = 0; b < ni; ++b)
+      for (int a = 0; a < ni; ++a) {
+        cf.fd[0][a + ni * b] = d[0] * w0 + d[1] * K00 + d[2] * w0 * lam[a] + d[3] * w0 * lam[b];
+        cf.fd[1][a + ni * b] = d[0] * w0 + d[1] * w0 * lam[a] + d[2] * K00 + d[3] * w0 * lam[b];
+        cf.fd[2][a + ni * b] = d[0] * w0 + d[1] * w0 * lam[a] + d[2] * w0 * lam[b] + d[3] * K00;
+      }
+  if (ni <= 8)
+    for (int k = 0; k < ni; ++k)
+      for (int j = 0; j < ni; ++j)
+        for (int i = 0; i < ni; ++i)
+          cf.dinv[i + ni * (j + ni * k)] = 1.0 / (d[0] + d[1] * lam[i] + d[2] * lam[j] + d[3] * lam[k]);
+  out.resize(sizeof(cf));
+  memcpy(out.data(), &cf, sizeof(cf));
 }
 
 int launch_apply_col(const ColParams& P, void* stream, int* nl, int* grid_out, void* events) {
@@ -1053,12 +1169,24 @@ int launch_apply_col(const ColParams& P, void* stream, int* nl, int* grid_out, v
   int r;
   switch (P.g.ni) {
 #define LCASE(N) case N: r = launch_col_t<N>(P, st, nl, grid_out); break;
-    LCASE(1) LCASE(2) LCASE(3) LCASE(4) LCASE(5) LCASE(6) LCASE(7) LCASE(8)
+    LCASE(1) LCASE(2) LCASE(3) LCASE(4) LCASE(5) LCASE(6) LCASE(7)
 #undef LCASE
     default: return cudaErrorInvalidValue;
   }
   if (ev) cudaEventRecord(ev[1], st);
   return r;
+}
+
+int launch_apply_col_raw(const Geom& g, const double* x, double* y, const double* done, void* state, int* flags,
+                         double* corner, double* pending, int ntx, int nty, const void* coef, void* stream, int* nl,
+                         void* events) {
+  ColParams P;
+  P.g = g; P.x = x; P.y = y; P.done = done; P.st = (ColState*)state; P.flags = flags; P.corner = corner;
+  P.pending = pending;
+  P.ntx = ntx; P.nty = nty; P.nitems = ntx * nty;
+  memcpy(&P.cf, coef, sizeof(ColCoef));
+  int grid = 0;
+  return launch_apply_col(P, stream, nl, &grid, events);
 }
 
 }  // namespace sc

@@ -101,12 +101,14 @@ int launch_reduce2(const double* partials, double* scal, int slot0, int nvals, c
 
 namespace sc {
 struct ColState;
-// v2 tile-column operator (kernels_col.cu), n_I <= 8.
+// v3 tile-column operator (kernels_col.cu), n_I <= 7, uniform geometry.
 bool col_supported(int ni);
 void col_tile(int ni, int* tx, int* ty, int* pend);
+void col_make_coef(int ni, const double* d, const double* a0, const double* lam, double K00, double K0p, double w0,
+                   std::vector<unsigned char>& out);
 int launch_apply_col_raw(const Geom& g, const double* x, double* y, const double* done, void* state, int* flags,
-                         double* corner, double* pending, int ntx, int nty, void* stream, int* nlaunch,
-                         void* events);
+                         double* corner, double* pending, int ntx, int nty, const void* coef, void* stream,
+                         int* nlaunch, void* events);
 int launch_add_segments(double* y, const double* add, const long long* off, const long long* len, int n,
                         void* stream, int* nlaunch);
 }

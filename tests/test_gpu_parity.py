@@ -270,9 +270,11 @@ def test_spectral_convergence_gpu():
     assert np.all(errs[1:] < errs[:-1] / 10.0), errs
 
 
-# ---- v2 tile-column operator: multi-tile grids (look-back across tile boundaries, ragged tiles)
-@pytest.mark.parametrize("p,ne", [(2, (19, 11, 3)), (3, (10, 7, 2)), (4, (9, 6, 2)), (5, (6, 5, 3)),
-                                  (6, (5, 6, 2)), (7, (6, 5, 2)), (8, (9, 6, 3)), (9, (5, 5, 2))])
+# ---- tile-column operator: multi-tile grids (look-back across tile boundaries, ragged tiles)
+# (the v3 tile is 8 x 4 elements: every case spans several tiles in x and y with ragged ends)
+@pytest.mark.parametrize("p,ne", [(2, (19, 11, 3)), (3, (10, 7, 2)), (4, (9, 6, 2)), (5, (10, 6, 3)),
+                                  (6, (9, 5, 2)), (7, (10, 5, 2)), (8, (9, 6, 3)), (8, (17, 9, 2)),
+                                  (9, (5, 5, 2))])
 def test_operator_parity_multitile(p, ne):
     g = small_grid(p, ne, 0.9, lengths=(1.3, 0.7, 0.5))
     op = operator.AssembledCondensedOperator(g)
@@ -283,7 +285,7 @@ def test_operator_parity_multitile(p, ne):
 
 
 def test_col_kernel_matches_v1_kernel_large():
-    """The tile-column kernel (v2) and the one-CTA-per-element kernel (v1) agree on a grid
+    """The tile-column kernel (v3) and the one-CTA-per-element kernel (v1) agree on a grid
     with many tiles in x and y and many layers (transformed basis, same ctx conventions)."""
     import os
     g = small_grid(8, (21, 14, 7), 1.0)
