@@ -131,14 +131,14 @@ struct Plane {
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 
 #if defined(SC_EXP) && SC_EXP == 9
-__device__ unsigned long long g_phase_cycles[16];
-#define SC_PHASE(k)                                                     \
-  do {                                                                  \
-    if (threadIdx.x == 0) {                                             \
-      long long t_ = clock64();                                         \
-      atomicAdd(&g_phase_cycles[k], (unsigned long long)(t_ - ph_t0));  \
-      ph_t0 = t_;                                                       \
-    }                                                                   \
+__device__ unsigned long long g_phase_cycles[8 * 16];   // [warp][phase]
+#define SC_PHASE(k)                                                                         \
+  do {                                                                                      \
+    if ((threadIdx.x & 31) == 0) {                                                          \
+      long long t_ = clock64();                                                             \
+      atomicAdd(&g_phase_cycles[(threadIdx.x >> 5) * 16 + (k)], (unsigned long long)(t_ - ph_t0)); \
+      ph_t0 = t_;                                                                           \
+    }                                                                                       \
   } while (0)
 #else
 #define SC_PHASE(k) do {} while (0)
@@ -191,94 +191,134 @@ struct Addr {
 // shared memory.  Every tile row of an entity class is one contiguous range in both the
 // skeleton vector and the smem buffer; a warp copies a row with 8-byte cp.async (Dirichlet
 // entities, which sit at the two ends of a row or fill a whole row, are written as 0).
+
+// ---- row-structured I/O ----------------------------------------------------------------
+// Every tile row of an entity class is one contiguous range in both the skeleton vector and
+// the shared-memory buffer.  Rows are dealt to the 8 warps round-robin; a warp moves a row with
+// one 8-byte cp.async per lane and iteration (Dirichlet sub-ranges are written as 0), so the
+// per-entry cost is an address increment, a compare and the copy.
+__device__ __forceinline__ void cp8(unsigned s, const double* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(g) : "memory");
+}
+__device__ __forceinline__ void row_load(double* sb, const double* gb, int len, int zlo, int zhi, int lane) {
+  for (int t = lane; t < zlo; t += 32) sb[t] = 0.0;
+  for (int t = zhi + lane; t < len; t += 32) sb[t] = 0.0;
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sb);
+  int t = zlo + lane;
+  for (; t + 96 < zhi; t += 128) {
+    cp8(s + 8u * t, gb + t);
+    cp8(s + 8u * (t + 32), gb + t + 32);
+    cp8(s + 8u * (t + 64), gb + t + 64);
+    cp8(s + 8u * (t + 96), gb + t + 96);
+  }
+  for (; t < zhi; t += 32) cp8(s + 8u * t, gb + t);
+}
+
+// Row descriptors of a tile (built once per work item, shared memory).  Rows of the side
+// (element layer) block: x-faces (th), y-faces (th+1), z-edges (th+1); rows of the plane block:
+// z-faces (th), x-edges (th+1), y-edges (th), vertices (th+1).  The skeleton offset of a row at
+// layer / plane l is g + l gs.  Load: [0, zlo) and [zhi, len) are Dirichlet entries (written as
+// 0).  Finalize: W end [0, a), middle [a, b), E end [b, len), each with a mode (copy to y, zero,
+// park in `pending` at offset p + c, or skip = published by the corner pass).
+enum { M_SKIP = 0, M_Y = 1, M_ZERO = 2, M_PARK = 3 };
+struct RowIO {
+  long long g, gs;
+  int s, len, zlo, zhi;
+  short a, b, pw, pm;
+  unsigned char mw, mm, me, pad;
+};
+
 template <int NI>
-__device__ void load_plane(const ColParams& P, Plane<NI> pl, int x0, int y0, int tw, int th, int fz) {
-#if defined(SC_EXP) && SC_EXP == 5
-  return;
-#endif
+__device__ void build_rows(const ColParams& P, RowIO* io, int x0, int y0, int tw, int th, int* ns_out) {
   using C = CS<NI>;
-  constexpr int N2 = C::N2, NW = C::NT / 32;
+  constexpr int N2 = NI * NI, TX = C::TX;
   const Geom& g = P.g;
-  Addr A{g};
-  const bool zd = zdir(g, fz);
+  const int nx = g.nx, ny = g.ny;
+  const bool hasW = x0 > 0, hasE = x0 + tw < nx, hasS = y0 > 0, hasN = y0 + th < ny;
+  const int ns = 3 * th + 2, np = 4 * th + 2;
+  *ns_out = ns;
+  const int r = threadIdx.x;
+  if (r >= ns + np) return;
+  RowIO d;
+  d.a = 0; d.pw = 0; d.pm = 0; d.mw = M_SKIP; d.me = M_SKIP; d.pad = 0;
+  if (r < th) {                                            // x-faces row r
+    d.g = g.off_f[0] + ((long long)x0 + (long long)(nx + 1) * (y0 + r)) * N2;
+    d.gs = (long long)(nx + 1) * ny * N2;
+    d.s = C::S_XF + r * (TX + 1) * N2; d.len = (tw + 1) * N2;
+    d.zlo = hasW ? 0 : N2; d.zhi = hasE ? d.len : tw * N2;
+    d.a = N2; d.b = tw * N2;
+    d.mw = hasW ? M_PARK : M_ZERO; d.pw = C::PD_XF + r * N2; d.mm = M_Y; d.me = hasE ? M_Y : M_ZERO;
+  } else if (r < 2 * th + 1) {                             // y-faces row q
+    const int q = r - th, fy = y0 + q;
+    const bool z = fy == 0 || fy == ny;
+    d.g = g.off_f[1] + ((long long)x0 + (long long)nx * fy) * N2;
+    d.gs = (long long)nx * (ny + 1) * N2;
+    d.s = C::S_YF + q * TX * N2; d.len = tw * N2;
+    d.zlo = z ? d.len : 0; d.zhi = d.len;
+    d.b = d.len;
+    d.mm = z ? M_ZERO : ((q == 0 && hasS) ? M_PARK : M_Y); d.pm = C::PD_YF;
+  } else if (r < ns) {                                     // z-edges row q
+    const int q = r - 2 * th - 1, fy = y0 + q;
+    const bool z = fy == 0 || fy == ny, nrow = q == th && hasN, srow = q == 0 && hasS;
+    d.g = g.off_e[2] + ((long long)x0 + (long long)(nx + 1) * fy) * NI;
+    d.gs = (long long)(nx + 1) * (ny + 1) * NI;
+    d.s = C::S_ZE + q * (TX + 1) * NI; d.len = (tw + 1) * NI;
+    d.zlo = z ? d.len : (hasW ? 0 : NI); d.zhi = hasE ? d.len : tw * NI;
+    d.a = NI; d.b = tw * NI;
+    d.mw = z ? M_ZERO : (nrow ? M_SKIP : (hasW ? M_PARK : M_ZERO)); d.pw = C::PD_ZEW + q * NI;
+    d.mm = z ? M_ZERO : (srow ? M_PARK : M_Y); d.pm = C::PD_ZES - NI;
+    d.me = (z || !hasE) ? M_ZERO : ((nrow || srow) ? M_SKIP : M_Y);
+  } else {
+    const int u = r - ns;
+    if (u < th) {                                          // z-faces row u
+      d.g = g.off_f[2] + ((long long)x0 + (long long)nx * (y0 + u)) * N2;
+      d.gs = (long long)nx * ny * N2;
+      d.s = C::P_ZF + u * TX * N2; d.len = tw * N2;
+      d.zlo = 0; d.zhi = d.len; d.b = d.len; d.mm = M_Y;
+    } else if (u < 2 * th + 1) {                           // x-edges row q
+      const int q = u - th, fy = y0 + q;
+      const bool z = fy == 0 || fy == ny;
+      d.g = g.off_e[0] + ((long long)x0 + (long long)nx * fy) * NI;
+      d.gs = (long long)nx * (ny + 1) * NI;
+      d.s = C::P_XE + q * TX * NI; d.len = tw * NI;
+      d.zlo = z ? d.len : 0; d.zhi = d.len; d.b = d.len;
+      d.mm = z ? M_ZERO : ((q == 0 && hasS) ? M_PARK : M_Y); d.pm = C::PD_XE;
+    } else if (u < 3 * th + 1) {                           // y-edges row q
+      const int q = u - 2 * th - 1;
+      d.g = g.off_e[1] + ((long long)x0 + (long long)(nx + 1) * (y0 + q)) * NI;
+      d.gs = (long long)(nx + 1) * ny * NI;
+      d.s = C::P_YE + q * (TX + 1) * NI; d.len = (tw + 1) * NI;
+      d.zlo = hasW ? 0 : NI; d.zhi = hasE ? d.len : tw * NI;
+      d.a = NI; d.b = tw * NI;
+      d.mw = hasW ? M_PARK : M_ZERO; d.pw = C::PD_YE + q * NI; d.mm = M_Y; d.me = hasE ? M_Y : M_ZERO;
+    } else {                                               // vertices row q
+      const int q = u - 3 * th - 1, fy = y0 + q;
+      const bool z = fy == 0 || fy == ny, nrow = q == th && hasN, srow = q == 0 && hasS;
+      d.g = g.off_v + (long long)x0 + (long long)(nx + 1) * fy;
+      d.gs = (long long)(nx + 1) * (ny + 1);
+      d.s = C::P_VV + q * (TX + 1); d.len = tw + 1;
+      d.zlo = z ? d.len : (hasW ? 0 : 1); d.zhi = hasE ? d.len : tw;
+      d.a = 1; d.b = tw;
+      d.mw = z ? M_ZERO : (nrow ? M_SKIP : (hasW ? M_PARK : M_ZERO)); d.pw = C::PD_VW + q;
+      d.mm = z ? M_ZERO : (srow ? M_PARK : M_Y); d.pm = C::PD_VS - 1;
+      d.me = (z || !hasE) ? M_ZERO : ((nrow || srow) ? M_SKIP : M_Y);
+    }
+  }
+  io[r] = d;
+}
+
+// Rows [r0, r1) of the descriptor table into the block at `base` for layer / plane l (one warp
+// per row); zero_all: the whole block is Dirichlet (a Dirichlet z-plane).
+__device__ __forceinline__ void load_rows(const double* x, const RowIO* io, int r0, int r1, double* base, int l,
+                                          bool zero_all) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int x1 = x0 + tw;
-  for (int row = warp; row < th; row += NW) {                      // z-faces
-    double* sb = pl.zf(row, 0);
-    const double* gb = P.x + A.zf(x0, y0 + row, fz);
-    for (int t = lane; t < tw * N2; t += 32) {
-      if (zd) sb[t] = 0.0; else cp_async8(sb + t, gb + t);
-    }
-  }
-  for (int row = warp; row <= th; row += NW) {                     // x-edges (ex, fy)
-    const int fy = y0 + row;
-    const bool rd = zd || fy == 0 || fy == g.ny;
-    double* sb = pl.xe(row, 0);
-    const double* gb = P.x + A.xe(x0, fy, fz);
-    for (int t = lane; t < tw * NI; t += 32) {
-      if (rd) sb[t] = 0.0; else cp_async8(sb + t, gb + t);
-    }
-  }
-  for (int row = warp; row < th; row += NW) {                      // y-edges (fx, ey)
-    double* sb = pl.ye(row, 0);
-    const double* gb = P.x + A.ye(x0, y0 + row, fz);
-    const int zlo = (x0 == 0) ? NI : 0, zhi = (x1 == g.nx) ? tw * NI : (tw + 1) * NI;
-    for (int t = lane; t < (tw + 1) * NI; t += 32) {
-      if (zd || t < zlo || t >= zhi) sb[t] = 0.0; else cp_async8(sb + t, gb + t);
-    }
-  }
-  for (int row = warp; row <= th; row += NW) {                     // vertices (fx, fy)
-    const int fy = y0 + row;
-    const bool rd = zd || fy == 0 || fy == g.ny;
-    double* sb = pl.vv(row, 0);
-    const double* gb = P.x + A.vv(x0, fy, fz);
-    for (int t = lane; t <= tw; t += 32) {
-      if (rd || (t == 0 && x0 == 0) || (t == tw && x1 == g.nx)) sb[t] = 0.0; else cp_async8(sb + t, gb + t);
-    }
+  for (int r = r0 + warp; r < r1; r += 8) {
+    const RowIO& d = io[r];
+    const int len = d.len;
+    row_load(base + d.s, x + d.g + (long long)l * d.gs, len, zero_all ? len : d.zlo, d.zhi, lane);
   }
 }
 
-template <int NI>
-__device__ void load_side(const ColParams& P, Side<NI> sd, int x0, int y0, int tw, int th, int ez) {
-#if defined(SC_EXP) && SC_EXP == 5
-  return;
-#endif
-  using C = CS<NI>;
-  constexpr int N2 = C::N2, NW = C::NT / 32;
-  const Geom& g = P.g;
-  Addr A{g};
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int x1 = x0 + tw;
-  for (int row = warp; row < th; row += NW) {                      // x-faces (fx, ey)
-    double* sb = sd.xf(row, 0);
-    const double* gb = P.x + A.xf(x0, y0 + row, ez);
-    const int zlo = (x0 == 0) ? N2 : 0, zhi = (x1 == g.nx) ? tw * N2 : (tw + 1) * N2;
-    for (int t = lane; t < (tw + 1) * N2; t += 32) {
-      if (t < zlo || t >= zhi) sb[t] = 0.0; else cp_async8(sb + t, gb + t);
-    }
-  }
-  for (int row = warp; row <= th; row += NW) {                     // y-faces (ex, fy)
-    const int fy = y0 + row;
-    const bool rd = fy == 0 || fy == g.ny;
-    double* sb = sd.yf(row, 0);
-    const double* gb = P.x + A.yf(x0, fy, ez);
-    for (int t = lane; t < tw * N2; t += 32) {
-      if (rd) sb[t] = 0.0; else cp_async8(sb + t, gb + t);
-    }
-  }
-  for (int row = warp; row <= th; row += NW) {                     // z-edges (fx, fy)
-    const int fy = y0 + row;
-    const bool rd = fy == 0 || fy == g.ny;
-    double* sb = sd.ze(row, 0);
-    const double* gb = P.x + A.ze(x0, fy, ez);
-    const int zlo = (x0 == 0) ? NI : 0, zhi = (x1 == g.nx) ? tw * NI : (tw + 1) * NI;
-    for (int t = lane; t < (tw + 1) * NI; t += 32) {
-      if (rd || t < zlo || t >= zhi) sb[t] = 0.0; else cp_async8(sb + t, gb + t);
-    }
-  }
-}
-
-// Corner record address: corner point (cx, cy) of the tile grid, step l, slot (0 SW, 1 S, 2 W).
 __device__ __forceinline__ double* corner_rec(const ColParams& P, int cx, int cy, int l, int slot) {
   const int ni = P.g.ni;
   return P.corner + ((((long long)cy * (P.ntx + 1) + cx) * (P.g.nz + 1) + l) * 3 + slot) * (ni + 1);
@@ -302,15 +342,85 @@ __device__ __forceinline__ void eo_reduce(const double* f, int stride, const dou
 // Row-0 / row-p application from an (R+, R-) pair: hi = 0 -> R+ + R-, hi = 1 -> R+ - R-.
 __device__ __forceinline__ double eo_row(const double* r, int hi) { return hi ? r[0] - r[1] : r[0] + r[1]; }
 
-// Deferred look-back for step ls of tile item: wait for the W, S, SW tiles' flags of step ls,
-// then write the tile's W / S boundary entities of that step as own (parked) partial + the
-// neighbours' partials (y-in-place, or the corner records on the 4-tile corner line).
-// All entries of a step form one flat list; every thread first issues all of its loads
-// (one L2 round trip per step), then all of its stores.  Dirichlet entities were already
-// written as 0 and are skipped.
+// Segment [a, b) of a shared-memory row to a global row: mode 0 skip, 1 copy, 2 zero.
+__device__ __forceinline__ void seg_out(double* __restrict__ dst, const double* __restrict__ s, int a, int b, int mode,
+                                        int lane) {
+  if (mode == 1) {
+    int t = a + lane;
+    for (; t + 96 < b; t += 128) {   // four independent loads in flight before the stores
+      const double v0 = s[t], v1 = s[t + 32], v2 = s[t + 64], v3 = s[t + 96];
+      dst[t] = v0; dst[t + 32] = v1; dst[t + 64] = v2; dst[t + 96] = v3;
+    }
+    for (; t < b; t += 32) dst[t] = s[t];
+  } else if (mode == 2) {
+    for (int t = a + lane; t < b; t += 32) dst[t] = 0.0;
+  }
+}
+enum { SEG_SKIP = 0, SEG_COPY = 1, SEG_ZERO = 2 };
+
+// ---- finalize step l: write every entity of the step that this tile completes or publishes.
+// Ownership: the highest-ticket contributing tile (tiles are ticketed x-fastest) owns an
+// entity.  A tile owns its W / S boundaries: its own partials are parked in `pending` and
+// finished one step later.  It publishes its E / N boundaries as partial sums straight into y,
+// except the three 4-tile corner lines it does not own, whose partials go to corner records.
+// Segments per row: W end | middle | E end, each copied, zeroed (Dirichlet), parked or skipped.
+__device__ __forceinline__ void seg_mode(double* yo, double* pk, const double* s, int a, int b, int mode, int lane) {
+  if (mode == M_Y) seg_out(yo, s, a, b, SEG_COPY, lane);
+  else if (mode == M_ZERO) seg_out(yo, s, a, b, SEG_ZERO, lane);
+  else if (mode == M_PARK) seg_out(pk, s, a, b, SEG_COPY, lane);
+}
+
+template <int NI>
+__device__ void finalize_step(const ColParams& P, long long item, int l, int x0, int y0, int tw, int th,
+                              const Side<NI>& ac, const Plane<NI>& acb, const RowIO* io, int ns) {
+  using C = CS<NI>;
+  constexpr int NW = C::NT / 32, TX = C::TX, TY = C::TY;
+  const Geom& g = P.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool last = (l == g.nz), pzd = zdir(g, l);
+  const int x1 = x0 + tw, y1 = y0 + th;
+  const bool hasE = x1 < g.nx, hasN = y1 < g.ny, hasW = x0 > 0, hasS = y0 > 0;
+  double* const pd = P.pending + (item * 2 + (l & 1)) * (long long)C::PEND;
+  const int nr = ns + 4 * th + 2;
+  for (int r = (last ? ns : 0) + warp; r < nr; r += NW) {
+    const RowIO& d = io[r];
+    const bool side = r < ns;
+    const double* s = (side ? ac.b : acb.b) + d.s;
+    double* yo = P.y + d.g + (long long)l * d.gs;
+    if (!side && pzd) { seg_out(yo, s, 0, d.len, SEG_ZERO, lane); continue; }
+    seg_mode(yo, pd + d.pw, s, 0, d.a, d.mw, lane);
+    seg_mode(yo, pd + d.pm, s, d.a, d.b, d.mm, lane);
+    seg_mode(yo, pd, s, d.b, d.len, d.me, lane);
+  }
+  // corner pass: the three 4-tile corner lines this tile contributes to but does not own
+  // (NE -> slot 0 of the NE tile's SW corner, NW -> slot 1, SE -> slot 2); z-edges (c < NI)
+  // of layer l and the vertex (c == NI) of plane l.
+  if (warp == NW - 1) {
+    const int cc = lane % (NI + 1), kind = lane / (NI + 1);
+    if (kind < 3) {
+      const bool isv = cc == NI;
+      int ix = 0, iy = 0, slot = -1;
+      if (kind == 0 && hasE && hasN) { ix = tw; iy = th; slot = 0; }
+      if (kind == 1 && hasW && hasN) { ix = 0; iy = th; slot = 1; }
+      if (kind == 2 && hasE && hasS) { ix = tw; iy = 0; slot = 2; }
+      if (slot >= 0 && !(isv ? pzd : last)) {
+        const double v = isv ? *acb.vv(iy, ix) : ac.ze(iy, ix)[cc];
+        corner_rec(P, (x0 + ix) / TX, (y0 + iy) / TY, l, slot)[cc] = v;
+      }
+    }
+  }
+}
+
+// Deferred look-back for step ls of tile item: wait for the W, S, SW tiles' flags of step ls
+// (one lane per flag), then write the tile's W / S boundary entities of that step as own
+// (parked) partial + the neighbours' partials (y-in-place, or the corner records on the 4-tile
+// corner line).  Row base addresses of the step are built once in shared memory; every
+// thread then issues all of its loads before any store.  Dirichlet entities were written as 0
+// in the finalize pass and are skipped.
 template <int NI>
 __device__ void finish_boundary(const ColParams& P, long long item, int ls, int x0, int y0, int tw, int th,
-                                const int* flag_w, const int* flag_s, const int* flag_sw, int epoch) {
+                                const int* flag_w, const int* flag_s, const int* flag_sw, int epoch,
+                                long long* sRow, const RowIO* io) {
   using C = CS<NI>;
   constexpr int N2 = C::N2, NT = C::NT, TX = C::TX, TY = C::TY;
   constexpr int MAXE = (C::PEND + NT - 1) / NT;
@@ -319,16 +429,34 @@ __device__ void finish_boundary(const ColParams& P, long long item, int ls, int 
   const int tid = threadIdx.x;
   const bool last = (ls == g.nz), pzd = zdir(g, ls);
   const int x1 = x0 + tw, y1 = y0 + th;
-  const bool hasE = x1 < g.nx, hasN = y1 < g.ny, hasW = x0 > 0, hasS = y0 > 0;
+  const bool hasN = y1 < g.ny, hasW = x0 > 0, hasS = y0 > 0;
+  (void)x1;
   if (!hasW && !hasS) return;
-#if !defined(SC_EXP) || SC_EXP != 8
-  if (tid == 0) {
-    if (flag_w) while (flag_acquire(flag_w + ls) != epoch) __nanosleep(32);
-    if (flag_s) while (flag_acquire(flag_s + ls) != epoch) __nanosleep(32);
-    if (flag_sw) while (flag_acquire(flag_sw + ls) != epoch) __nanosleep(32);
+  // row bases: [0, th) W col x-faces, [TY, TY+th] W col z-edges, [2TY+1, 2TY+1+th) W col y-edges,
+  // [3TY+1, 3TY+1+th] W col vertices, 4TY+2: S row y-faces, +1 S row z-edges, +2 S row x-edges,
+  // +3 S row vertices
+  if (tid < 32) {
+    const int lane = tid;
+    if (lane < 3) {
+      const int* f = lane == 0 ? flag_w : (lane == 1 ? flag_s : flag_sw);
+      if (f) while (flag_acquire(f + ls) != epoch) __nanosleep(32);
+    }
+    // row bases from the descriptor table (x-face rows 0.., y-face row 0 at th, z-edge rows at
+    // 2 th + 1, x-edge row 0 at ns + th, y-edge rows at ns + 2 th + 1, vertex rows at ns + 3 th + 1)
+    const int ns = 3 * th + 2;
+    auto at = [&](int r) { return io[r].g + (long long)ls * io[r].gs; };
+    if (lane < TY + 1) {
+      if (lane < th) sRow[lane] = at(lane), sRow[2 * TY + 1 + lane] = at(ns + 2 * th + 1 + lane);
+      if (lane <= th) sRow[TY + lane] = at(2 * th + 1 + lane), sRow[3 * TY + 1 + lane] = at(ns + 3 * th + 1 + lane);
+    }
+    if (lane == 0) {
+      sRow[4 * TY + 2] = at(th);
+      sRow[4 * TY + 3] = at(2 * th + 1);
+      sRow[4 * TY + 4] = at(ns + th);
+      sRow[4 * TY + 5] = at(ns + 3 * th + 1);
+    }
   }
   __syncthreads();
-#endif
   const double* pd = P.pending + (item * 2 + (ls & 1)) * (long long)C::PEND;
   // segment sizes of the flat list (0 when the segment does not apply at this step)
   const int n0 = (!last && hasW) ? th * N2 : 0;            // W col x-faces
@@ -339,42 +467,44 @@ __device__ void finish_boundary(const ColParams& P, long long item, int ls, int 
   const int n5 = (!pzd && hasW) ? th * NI : 0;             // W col y-edges
   const int n6 = (!pzd && hasW) ? th + 1 : 0;              // W col vertices
   const int n7 = (!pzd && hasS) ? tw - 1 : 0;              // S row vertices, ix in [1, tw-1]
-  const int ntot = n0 + n1 + n2 + n3 + n4 + n5 + n6 + n7;
+  const int c1 = n0, c2 = c1 + n1, c3 = c2 + n2, c4 = c3 + n3, c5 = c4 + n4, c6 = c5 + n5, c7 = c6 + n6;
+  const int ntot = c7 + n7;
   double val[MAXE];
   double* dst[MAXE];
 #pragma unroll
   for (int k = 0; k < MAXE; ++k) {
     dst[k] = nullptr;
     val[k] = 0.0;
-    int t = tid + k * NT;
+    const int t = tid + k * NT;
     if (t >= ntot) continue;
-    double* d = nullptr;
-    int po = -1;                 // offset of the own parked partial
-    int corner = -1;             // corner line entry: value index into the corner records
-    if (t < n0) {
-      d = P.y + A.xf(x0, y0 + t / N2, ls) + t % N2; po = C::PD_XF + t;
-    } else if ((t -= n0) < n1) {
-      d = P.y + A.yf(x0, y0, ls) + t; po = C::PD_YF + t;
-    } else if ((t -= n1) < n2) {
-      const int row = t / NI, c = t % NI, fy = y0 + row;
+    long long o;
+    int po, corner = -1;
+    if (t < c1) {
+      const int row = t / N2;
+      o = sRow[row] + (t - row * N2); po = C::PD_XF + t;
+    } else if (t < c2) {
+      o = sRow[4 * TY + 2] + (t - c1); po = C::PD_YF + (t - c1);
+    } else if (t < c3) {
+      const int u = t - c2, row = u / NI, fy = y0 + row;
       if (fy == 0 || fy == g.ny || (row == th && hasN)) continue;
-      d = P.y + A.ze(x0, fy, ls) + c; po = C::PD_ZEW + t;
-      if (row == 0 && hasS) corner = c;
-    } else if ((t -= n2) < n3) {
-      d = P.y + A.ze(x0, y0, ls) + NI + t; po = C::PD_ZES + t;
-    } else if ((t -= n3) < n4) {
-      d = P.y + A.xe(x0, y0, ls) + t; po = C::PD_XE + t;
-    } else if ((t -= n4) < n5) {
-      d = P.y + A.ye(x0, y0 + t / NI, ls) + t % NI; po = C::PD_YE + t;
-    } else if ((t -= n5) < n6) {
-      const int fy = y0 + t;
-      if (fy == 0 || fy == g.ny || (t == th && hasN)) continue;
-      d = P.y + A.vv(x0, fy, ls); po = C::PD_VW + t;
-      if (t == 0 && hasS) corner = NI;
+      o = sRow[TY + row] + (u - row * NI); po = C::PD_ZEW + u;
+      if (row == 0 && hasS) corner = u;
+    } else if (t < c4) {
+      o = sRow[4 * TY + 3] + NI + (t - c3); po = C::PD_ZES + (t - c3);
+    } else if (t < c5) {
+      o = sRow[4 * TY + 4] + (t - c4); po = C::PD_XE + (t - c4);
+    } else if (t < c6) {
+      const int u = t - c5, row = u / NI;
+      o = sRow[2 * TY + 1 + row] + (u - row * NI); po = C::PD_YE + u;
+    } else if (t < c7) {
+      const int row = t - c6, fy = y0 + row;
+      if (fy == 0 || fy == g.ny || (row == th && hasN)) continue;
+      o = sRow[3 * TY + 1 + row]; po = C::PD_VW + row;
+      if (row == 0 && hasS) corner = NI;
     } else {
-      t -= n6;
-      d = P.y + A.vv(x0, y0, ls) + 1 + t; po = C::PD_VS + t;
+      o = sRow[4 * TY + 5] + 1 + (t - c7); po = C::PD_VS + (t - c7);
     }
+    double* d = P.y + o;
     double v = ld_cg(pd + po);
     if (corner >= 0) {
       const int cx = x0 / TX, cy = y0 / TY;
@@ -391,7 +521,6 @@ __device__ void finish_boundary(const ColParams& P, long long item, int ls, int 
     if (dst[k]) *dst[k] = val[k];
 }
 
-
 // ---- condensed part of one parity class (s_i, s_j, s_k) = (SI, SJ, SK) ---------------------
 // Lane = element (ix, iy) of the tile.  All loops are unrolled with compile-time indices, so
 // P.cf.* are constant-bank operands.  Outputs: round r of direction d is executed by the
@@ -405,7 +534,8 @@ __device__ __forceinline__ void bar_named(int id) { asm volatile("bar.sync %0, 2
 template <int NI>
 __device__ __forceinline__ void vol_class(const int cls, const ColCoef* cf, const Side<NI>& in, const Plane<NI>& inb,
                                           const Plane<NI>& intp, const Side<NI>& ac, const Plane<NI>& acb,
-                                          const Plane<NI>& actp, double* rq, int ix, int iy, int tw, int th) {
+                                          const Plane<NI>& actp, double* rq, int ix, int iy, int tw, int th,
+                                          long long& ph_t0) {
   constexpr int M = (NI + 1) / 2, N2 = NI * NI, TX = CS<NI>::TX;
   constexpr int DO = NI >= 2 ? 1 : 0;   // parity class that adds the primary part and line sums
   const int si = cls >> 2, sj = (cls >> 1) & 1, sk = cls & 1;
@@ -427,154 +557,209 @@ __device__ __forceinline__ void vol_class(const int cls, const ColCoef* cf, cons
   // ---- phase A: primary part of the faces (Eq. 26 generalised: self, opposite face, the four
   // bounding edges) and the parity component of the faces' a0-weighted line sums used by the
   // edge / vertex rows, by the class with s_d == DO of each direction d.  Initialises ac.xf,
-  // ac.yf and actp.zf (plain stores), adds into acb.zf.
-  if (si == DO) {   // x-faces: face ix = W of element ix, E of element ix-1
+  // ac.yf and actp.zf (plain stores), adds into acb.zf.  Per direction: all shared-memory
+  // loads, then the arithmetic, then all stores.
+  const bool nonempty = CI > 0 && CJ > 0 && CK > 0;
+  if (si == DO && nonempty) {   // x-faces: face ix = W of element ix, E of element ix-1 (entries (j,k))
     const double* Z0 = in.ze(iy, ix) + sk;
     const double* Z1 = in.ze(iy + 1, ix) + sk;
     const double* Yb = inb.ye(iy, ix) + sj;
     const double* Yt = intp.ye(iy, ix) + sj;
     const double* fd = cf->fd[0] + sj + NI * sk;
-    double* oj = rq + CS<NI>::R_XJ + (iy * (TX + 1) + ix) * 2 * NI + 2 * sk + sj;   // over j, keep k
-    double* ok = rq + CS<NI>::R_XK + (iy * (TX + 1) + ix) * 2 * NI + 2 * sj + sk;   // over k, keep j
+    double w[M][M], e[M][M], f[M][M], zw[M], ze[M], yw[M], ye[M];
 #pragma unroll
-    for (int kk = 0; kk < M; ++kk) {
-      if (kk >= CK) continue;
-      const double zw = fma(gj, Z1[2 * kk], Z0[2 * kk]), ze = fma(gj, Z1[NI + 2 * kk], Z0[NI + 2 * kk]);
-      const double ek = cf->e[2][sk + 2 * kk], ak = cf->a[sk + 2 * kk];
-      double rwj = 0.0, rej = 0.0;
+    for (int m = 0; m < M; ++m) {
+      zw[m] = fma(gj, Z1[2 * m], Z0[2 * m]);
+      ze[m] = fma(gj, Z1[NI + 2 * m], Z0[NI + 2 * m]);
+      yw[m] = fma(gk, Yt[2 * m], Yb[2 * m]);
+      ye[m] = fma(gk, Yt[NI + 2 * m], Yb[NI + 2 * m]);
+    }
 #pragma unroll
-      for (int jj = 0; jj < M; ++jj) {
-        if (jj >= CJ) continue;
+    for (int jj = 0; jj < M; ++jj)
+#pragma unroll
+      for (int kk = 0; kk < M; ++kk) {
+        const bool ok = jj < CJ && kk < CK;
         const int o = 2 * jj + 2 * NI * kk;
-        const double w = W[o], e = E[o], f = fd[o], ej = cf->e[1][sj + 2 * jj], aj = cf->a[sj + 2 * jj];
-        const double yw = fma(gk, Yt[2 * jj], Yb[2 * jj]), ye = fma(gk, Yt[NI + 2 * jj], Yb[NI + 2 * jj]);
-        const double Wp = fma(f, w, fma(cf->k0p[0], e, fma(ej, zw, ek * yw)));
-        const double Ep = fma(f, e, fma(cf->k0p[0], w, fma(ej, ze, ek * ye)));
-        rwj = fma(aj, w, rwj);
-        rej = fma(aj, e, rej);
-        const double Em = __shfl_up_sync(0xffffffffu, Ep, 1);
-        if (act) {
-          fX[o] = ix > 0 ? Wp + Em : Wp;
-          if (lastx) fX[o + N2] = Ep;
-          if (kk == 0) {   // over k, keep j: one pass per j
-            double rwk = 0.0, rek = 0.0;
+        w[jj][kk] = ok ? W[o] : 0.0;
+        e[jj][kk] = ok ? E[o] : 0.0;
+        f[jj][kk] = ok ? fd[o] : 0.0;
+      }
+    double rwj[M], rej[M], rwk[M], rek[M];
 #pragma unroll
-            for (int k2 = 0; k2 < M; ++k2)
-              if (k2 < CK) {
-                rwk = fma(cf->a[sk + 2 * k2], W[2 * jj + 2 * NI * k2], rwk);
-                rek = fma(cf->a[sk + 2 * k2], E[2 * jj + 2 * NI * k2], rek);
-              }
-            ok[4 * jj] = rwk;
-            if (lastx) ok[2 * NI + 4 * jj] = rek;
+    for (int m = 0; m < M; ++m) rwj[m] = rej[m] = rwk[m] = rek[m] = 0.0;
+#pragma unroll
+    for (int jj = 0; jj < M; ++jj) {
+      const double ej = cf->e[1][sj + 2 * jj], aj = cf->a[sj + 2 * jj];
+#pragma unroll
+      for (int kk = 0; kk < M; ++kk) {
+        const double ek = cf->e[2][sk + 2 * kk], ak = cf->a[sk + 2 * kk];
+        const double wv = w[jj][kk], ev = e[jj][kk];
+        const double Wp = fma(f[jj][kk], wv, fma(cf->k0p[0], ev, fma(ej, zw[kk], ek * yw[jj])));
+        const double Ep = fma(f[jj][kk], ev, fma(cf->k0p[0], wv, fma(ej, ze[kk], ek * ye[jj])));
+        rwj[kk] = fma(aj, wv, rwj[kk]);
+        rej[kk] = fma(aj, ev, rej[kk]);
+        rwk[jj] = fma(ak, wv, rwk[jj]);
+        rek[jj] = fma(ak, ev, rek[jj]);
+        const double Em = __shfl_up_sync(0xffffffffu, Ep, 1);
+        w[jj][kk] = ix > 0 ? Wp + Em : Wp;
+        e[jj][kk] = Ep;
+      }
+    }
+    if (act) {
+      double* oj = rq + CS<NI>::R_XJ + (iy * (TX + 1) + ix) * 2 * NI + 2 * sk + sj;   // over j, keep k
+      double* okk = rq + CS<NI>::R_XK + (iy * (TX + 1) + ix) * 2 * NI + 2 * sj + sk;  // over k, keep j
+#pragma unroll
+      for (int jj = 0; jj < M; ++jj)
+#pragma unroll
+        for (int kk = 0; kk < M; ++kk)
+          if (jj < CJ && kk < CK) {
+            const int o = 2 * jj + 2 * NI * kk;
+            fX[o] = w[jj][kk];
+            if (lastx) fX[o + N2] = e[jj][kk];
           }
-        }
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        if (m < CK) { oj[4 * m] = rwj[m]; if (lastx) oj[2 * NI + 4 * m] = rej[m]; }
+        if (m < CJ) { okk[4 * m] = rwk[m]; if (lastx) okk[2 * NI + 4 * m] = rek[m]; }
       }
-      if (act) {
-        oj[4 * kk] = rwj;
-        if (lastx) oj[2 * NI + 4 * kk] = rej;
-        if (NI == 1) {   // no odd interior index: the odd parity components are 0
-          oj[1] = ok[1] = 0.0;
-          if (lastx) oj[2 * NI + 1] = ok[2 * NI + 1] = 0.0;
-        }
+      if (NI == 1) {   // no odd interior index: the odd parity components are 0
+        oj[1] = okk[1] = 0.0;
+        if (lastx) oj[2 * NI + 1] = okk[2 * NI + 1] = 0.0;
       }
-      (void)ak;
     }
   }
-  if (sj == DO) {   // y-faces: face row iy = S of element row iy, N of row iy-1
+  if (sj == DO && nonempty) {   // y-faces: face row iy = S of element row iy, N of row iy-1 (entries (i,k))
     const double* Z0 = in.ze(iy, ix) + sk;
     const double* Z1 = in.ze(iy + 1, ix) + sk;
     const double* Xb = inb.xe(iy, ix) + si;
     const double* Xt = intp.xe(iy, ix) + si;
     const double* fd = cf->fd[1] + si + NI * sk;
-    double* oi = rq + CS<NI>::R_YI + (iy * TX + ix) * 2 * NI + 2 * sk + si;   // over i, keep k
-    double* ok = rq + CS<NI>::R_YK + (iy * TX + ix) * 2 * NI + 2 * si + sk;   // over k, keep i
+    double sv_[M][M], nv_[M][M], f[M][M], zs[M], zn[M], xs[M], xn[M];
 #pragma unroll
-    for (int kk = 0; kk < M; ++kk) {
-      if (kk >= CK) continue;
-      const double zs = fma(gi, Z0[NI + 2 * kk], Z0[2 * kk]), zn = fma(gi, Z1[NI + 2 * kk], Z1[2 * kk]);
-      const double ek = cf->e[2][sk + 2 * kk];
-      double rsi = 0.0, rni = 0.0;
+    for (int m = 0; m < M; ++m) {
+      zs[m] = fma(gi, Z0[NI + 2 * m], Z0[2 * m]);
+      zn[m] = fma(gi, Z1[NI + 2 * m], Z1[2 * m]);
+      xs[m] = fma(gk, Xt[2 * m], Xb[2 * m]);
+      xn[m] = fma(gk, Xt[TX * NI + 2 * m], Xb[TX * NI + 2 * m]);
+    }
 #pragma unroll
-      for (int ii = 0; ii < M; ++ii) {
-        if (ii >= CI) continue;
+    for (int ii = 0; ii < M; ++ii)
+#pragma unroll
+      for (int kk = 0; kk < M; ++kk) {
+        const bool ok = ii < CI && kk < CK;
         const int o = 2 * ii + 2 * NI * kk;
-        const double sv = S[o], nv = N[o], f = fd[o], ei_ = cf->e[0][si + 2 * ii], ai = cf->a[si + 2 * ii];
-        const double xs = fma(gk, Xt[2 * ii], Xb[2 * ii]), xn = fma(gk, Xt[TX * NI + 2 * ii], Xb[TX * NI + 2 * ii]);
-        const double Sp = fma(f, sv, fma(cf->k0p[1], nv, fma(ei_, zs, ek * xs)));
-        const double Np = fma(f, nv, fma(cf->k0p[1], sv, fma(ei_, zn, ek * xn)));
-        rsi = fma(ai, sv, rsi);
-        rni = fma(ai, nv, rni);
-        const double Nm = __shfl_up_sync(0xffffffffu, Np, TX);
-        if (act) {
-          fY[o] = iy > 0 ? Sp + Nm : Sp;
-          if (lasty) fY[o + TX * N2] = Np;
-          if (kk == 0) {
-            double rsk = 0.0, rnk = 0.0;
-#pragma unroll
-            for (int k2 = 0; k2 < M; ++k2)
-              if (k2 < CK) {
-                rsk = fma(cf->a[sk + 2 * k2], S[2 * ii + 2 * NI * k2], rsk);
-                rnk = fma(cf->a[sk + 2 * k2], N[2 * ii + 2 * NI * k2], rnk);
-              }
-            ok[4 * ii] = rsk;
-            if (lasty) ok[TX * 2 * NI + 4 * ii] = rnk;
-          }
-        }
+        sv_[ii][kk] = ok ? S[o] : 0.0;
+        nv_[ii][kk] = ok ? N[o] : 0.0;
+        f[ii][kk] = ok ? fd[o] : 0.0;
       }
-      if (act) {
-        oi[4 * kk] = rsi;
-        if (lasty) oi[TX * 2 * NI + 4 * kk] = rni;
-        if (NI == 1) {
-          oi[1] = ok[1] = 0.0;
-          if (lasty) oi[TX * 2 * NI + 1] = ok[TX * 2 * NI + 1] = 0.0;
-        }
+    double rsi[M], rni[M], rsk[M], rnk[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) rsi[m] = rni[m] = rsk[m] = rnk[m] = 0.0;
+#pragma unroll
+    for (int ii = 0; ii < M; ++ii) {
+      const double ei_ = cf->e[0][si + 2 * ii], ai = cf->a[si + 2 * ii];
+#pragma unroll
+      for (int kk = 0; kk < M; ++kk) {
+        const double ek = cf->e[2][sk + 2 * kk], ak = cf->a[sk + 2 * kk];
+        const double sv = sv_[ii][kk], nv = nv_[ii][kk];
+        const double Sp = fma(f[ii][kk], sv, fma(cf->k0p[1], nv, fma(ei_, zs[kk], ek * xs[ii])));
+        const double Np = fma(f[ii][kk], nv, fma(cf->k0p[1], sv, fma(ei_, zn[kk], ek * xn[ii])));
+        rsi[kk] = fma(ai, sv, rsi[kk]);
+        rni[kk] = fma(ai, nv, rni[kk]);
+        rsk[ii] = fma(ak, sv, rsk[ii]);
+        rnk[ii] = fma(ak, nv, rnk[ii]);
+        const double Nm = __shfl_up_sync(0xffffffffu, Np, TX);
+        sv_[ii][kk] = iy > 0 ? Sp + Nm : Sp;
+        nv_[ii][kk] = Np;
+      }
+    }
+    if (act) {
+      double* oi = rq + CS<NI>::R_YI + (iy * TX + ix) * 2 * NI + 2 * sk + si;   // over i, keep k
+      double* okk = rq + CS<NI>::R_YK + (iy * TX + ix) * 2 * NI + 2 * si + sk;  // over k, keep i
+#pragma unroll
+      for (int ii = 0; ii < M; ++ii)
+#pragma unroll
+        for (int kk = 0; kk < M; ++kk)
+          if (ii < CI && kk < CK) {
+            const int o = 2 * ii + 2 * NI * kk;
+            fY[o] = sv_[ii][kk];
+            if (lasty) fY[o + TX * N2] = nv_[ii][kk];
+          }
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        if (m < CK) { oi[4 * m] = rsi[m]; if (lasty) oi[TX * 2 * NI + 4 * m] = rni[m]; }
+        if (m < CI) { okk[4 * m] = rsk[m]; if (lasty) okk[TX * 2 * NI + 4 * m] = rnk[m]; }
+      }
+      if (NI == 1) {
+        oi[1] = okk[1] = 0.0;
+        if (lasty) oi[TX * 2 * NI + 1] = okk[TX * 2 * NI + 1] = 0.0;
       }
     }
   }
-  if (sk == DO && act) {   // z-faces: B of this layer (plane l), T (plane l+1)
+  if (sk == DO && nonempty && act) {   // z-faces: B of this layer (plane l), T (plane l+1) (entries (i,j))
     const double* Yb = inb.ye(iy, ix) + sj;
     const double* Yt = intp.ye(iy, ix) + sj;
     const double* Xb = inb.xe(iy, ix) + si;
     const double* Xt = intp.xe(iy, ix) + si;
     const double* fd = cf->fd[2] + si + NI * sj;
+    double bv_[M][M], tv_[M][M], f[M][M], ob[M][M], yb[M], yt[M], xb[M], xt[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      yb[m] = fma(gi, Yb[NI + 2 * m], Yb[2 * m]);
+      yt[m] = fma(gi, Yt[NI + 2 * m], Yt[2 * m]);
+      xb[m] = fma(gj, Xb[TX * NI + 2 * m], Xb[2 * m]);
+      xt[m] = fma(gj, Xt[TX * NI + 2 * m], Xt[2 * m]);
+    }
+#pragma unroll
+    for (int jj = 0; jj < M; ++jj)
+#pragma unroll
+      for (int ii = 0; ii < M; ++ii) {
+        const bool ok = ii < CI && jj < CJ;
+        const int o = 2 * ii + 2 * NI * jj;
+        bv_[jj][ii] = ok ? B[o] : 0.0;
+        tv_[jj][ii] = ok ? T[o] : 0.0;
+        f[jj][ii] = ok ? fd[o] : 0.0;
+        ob[jj][ii] = ok ? fB[o] : 0.0;
+      }
+    double rbi[M], rti[M], rbj[M], rtj[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) rbi[m] = rti[m] = rbj[m] = rtj[m] = 0.0;
+#pragma unroll
+    for (int jj = 0; jj < M; ++jj) {
+      const double ej = cf->e[1][sj + 2 * jj], aj = cf->a[sj + 2 * jj];
+#pragma unroll
+      for (int ii = 0; ii < M; ++ii) {
+        const double ei_ = cf->e[0][si + 2 * ii], ai = cf->a[si + 2 * ii];
+        const double bv = bv_[jj][ii], tv = tv_[jj][ii];
+        ob[jj][ii] += fma(f[jj][ii], bv, fma(cf->k0p[2], tv, fma(ei_, yb[jj], ej * xb[ii])));
+        const double Tp = fma(f[jj][ii], tv, fma(cf->k0p[2], bv, fma(ei_, yt[jj], ej * xt[ii])));
+        rbi[jj] = fma(ai, bv, rbi[jj]);
+        rti[jj] = fma(ai, tv, rti[jj]);
+        rbj[ii] = fma(aj, bv, rbj[ii]);
+        rtj[ii] = fma(aj, tv, rtj[ii]);
+        tv_[jj][ii] = Tp;
+      }
+    }
+#pragma unroll
+    for (int jj = 0; jj < M; ++jj)
+#pragma unroll
+      for (int ii = 0; ii < M; ++ii)
+        if (ii < CI && jj < CJ) {
+          const int o = 2 * ii + 2 * NI * jj;
+          fB[o] = ob[jj][ii];
+          fT[o] = tv_[jj][ii];
+        }
     constexpr int PO = CS<NI>::NE * 2 * NI;
     double* oi = rq + CS<NI>::R_ZI + (iy * TX + ix) * 2 * NI + 2 * sj + si;    // over i, keep j (l+1 at + PO)
     double* oj = rq + CS<NI>::R_ZJ + (iy * TX + ix) * 2 * NI + 2 * si + sj;    // over j, keep i
 #pragma unroll
-    for (int jj = 0; jj < M; ++jj) {
-      if (jj >= CJ) continue;
-      const double yb = fma(gi, Yb[NI + 2 * jj], Yb[2 * jj]), yt = fma(gi, Yt[NI + 2 * jj], Yt[2 * jj]);
-      const double ej = cf->e[1][sj + 2 * jj], aj = cf->a[sj + 2 * jj];
-      double rbi = 0.0, rti = 0.0;
-#pragma unroll
-      for (int ii = 0; ii < M; ++ii) {
-        if (ii >= CI) continue;
-        const int o = 2 * ii + 2 * NI * jj;
-        const double bv = B[o], tv = T[o], f = fd[o], ei_ = cf->e[0][si + 2 * ii], ai = cf->a[si + 2 * ii];
-        const double xb = fma(gj, Xb[TX * NI + 2 * ii], Xb[2 * ii]), xt = fma(gj, Xt[TX * NI + 2 * ii], Xt[2 * ii]);
-        fB[o] += fma(f, bv, fma(cf->k0p[2], tv, fma(ei_, yb, ej * xb)));
-        fT[o] = fma(f, tv, fma(cf->k0p[2], bv, fma(ei_, yt, ej * xt)));
-        rbi = fma(ai, bv, rbi);
-        rti = fma(ai, tv, rti);
-        if (jj == 0) {
-          double rbj = 0.0, rtj = 0.0;
-#pragma unroll
-          for (int j2 = 0; j2 < M; ++j2)
-            if (j2 < CJ) {
-              rbj = fma(cf->a[sj + 2 * j2], B[2 * ii + 2 * NI * j2], rbj);
-              rtj = fma(cf->a[sj + 2 * j2], T[2 * ii + 2 * NI * j2], rtj);
-            }
-          oj[4 * ii] = rbj;
-          oj[PO + 4 * ii] = rtj;
-        }
-      }
-      oi[4 * jj] = rbi;
-      oi[PO + 4 * jj] = rti;
-      if (NI == 1) oi[1] = oi[PO + 1] = oj[1] = oj[PO + 1] = 0.0;
-      (void)aj;
+    for (int m = 0; m < M; ++m) {
+      if (m < CJ) { oi[4 * m] = rbi[m]; oi[PO + 4 * m] = rti[m]; }
+      if (m < CI) { oj[4 * m] = rbj[m]; oj[PO + 4 * m] = rtj[m]; }
     }
+    if (NI == 1) oi[1] = oi[PO + 1] = oj[1] = oj[PO + 1] = 0.0;
   }
-
+  SC_PHASE(3);
   // ---- phase B: condensed part of the class (registers only)
   const double* Dv = cf->dinv + si + NI * sj + N2 * sk;
   double qx[M][M], qy[M][M], qz[M][M];
@@ -625,57 +810,83 @@ __device__ __forceinline__ void vol_class(const int cls, const ColCoef* cf, cons
   }
   // ---- output rounds: barrier (phase A complete), then round r of direction d by the classes
   // with s_d == r; W -= Q^0 + Q^1, E -= Q^0 - Q^1 (two elements of a face summed by shuffle).
+  SC_PHASE(4);
 #pragma unroll 1
   for (int r = 0; r < 2; ++r) {
     bar_named(1);
-    if (r == si) {
+    SC_PHASE(5 + 6 * r);
+    if (r == si) {   // W -= Q(ix) + g Q(ix-1) on face ix; the last element also E -= g Q
+      double o0[M][M], o1[M][M];
 #pragma unroll
-      for (int jj = 0; jj < M; ++jj) {
-        if (jj >= CJ) continue;
+      for (int jj = 0; jj < M; ++jj)
 #pragma unroll
         for (int kk = 0; kk < M; ++kk) {
-          if (kk >= CK) continue;
+          const bool ok = act && jj < CJ && kk < CK;
+          const int o = 2 * jj + 2 * NI * kk;
+          o0[jj][kk] = ok ? fX[o] : 0.0;
+          o1[jj][kk] = (ok && lastx) ? fX[o + N2] : 0.0;
+        }
+#pragma unroll
+      for (int jj = 0; jj < M; ++jj)
+#pragma unroll
+        for (int kk = 0; kk < M; ++kk) {
+          if (jj >= CJ || kk >= CK) continue;
           const int o = 2 * jj + 2 * NI * kk;
           const double Q = qx[jj][kk];
           const double Qm = __shfl_up_sync(0xffffffffu, Q, 1);
           if (act) {
-            fX[o] -= ix > 0 ? fma(gi, Qm, Q) : Q;
-            if (lastx) fX[o + N2] -= gi * Q;
+            fX[o] = o0[jj][kk] - (ix > 0 ? fma(gi, Qm, Q) : Q);
+            if (lastx) fX[o + N2] = fma(-gi, Q, o1[jj][kk]);
           }
         }
-      }
     }
     if (r == sj) {
+      double o0[M][M], o1[M][M];
 #pragma unroll
-      for (int ii = 0; ii < M; ++ii) {
-        if (ii >= CI) continue;
+      for (int ii = 0; ii < M; ++ii)
 #pragma unroll
         for (int kk = 0; kk < M; ++kk) {
-          if (kk >= CK) continue;
+          const bool ok = act && ii < CI && kk < CK;
+          const int o = 2 * ii + 2 * NI * kk;
+          o0[ii][kk] = ok ? fY[o] : 0.0;
+          o1[ii][kk] = (ok && lasty) ? fY[o + TX * N2] : 0.0;
+        }
+#pragma unroll
+      for (int ii = 0; ii < M; ++ii)
+#pragma unroll
+        for (int kk = 0; kk < M; ++kk) {
+          if (ii >= CI || kk >= CK) continue;
           const int o = 2 * ii + 2 * NI * kk;
           const double Q = qy[ii][kk];
           const double Qm = __shfl_up_sync(0xffffffffu, Q, TX);
           if (act) {
-            fY[o] -= iy > 0 ? fma(gj, Qm, Q) : Q;
-            if (lasty) fY[o + TX * N2] -= gj * Q;
+            fY[o] = o0[ii][kk] - (iy > 0 ? fma(gj, Qm, Q) : Q);
+            if (lasty) fY[o + TX * N2] = fma(-gj, Q, o1[ii][kk]);
           }
         }
-      }
     }
     if (r == sk && act) {
+      double o0[M][M], o1[M][M];
 #pragma unroll
-      for (int jj = 0; jj < M; ++jj) {
-        if (jj >= CJ) continue;
+      for (int jj = 0; jj < M; ++jj)
 #pragma unroll
         for (int ii = 0; ii < M; ++ii) {
-          if (ii >= CI) continue;
+          const bool ok = ii < CI && jj < CJ;
           const int o = 2 * ii + 2 * NI * jj;
-          const double Q = qz[jj][ii];
-          fB[o] -= Q;
-          fT[o] -= gk * Q;
+          o0[jj][ii] = ok ? fB[o] : 0.0;
+          o1[jj][ii] = ok ? fT[o] : 0.0;
         }
-      }
+#pragma unroll
+      for (int jj = 0; jj < M; ++jj)
+#pragma unroll
+        for (int ii = 0; ii < M; ++ii)
+          if (ii < CI && jj < CJ) {
+            const int o = 2 * ii + 2 * NI * jj;
+            fB[o] = o0[jj][ii] - qz[jj][ii];
+            fT[o] = fma(-gk, qz[jj][ii], o1[jj][ii]);
+          }
     }
+    SC_PHASE(10 + 2 * r);
   }
 }
 
@@ -695,6 +906,8 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
   ColCoef* sCf = reinterpret_cast<ColCoef*>(sm + C::O_CF);
   double* const rq = sm + C::O_RQ;
   __shared__ unsigned long long sTicket;
+  __shared__ long long sRow[32];
+  __shared__ RowIO sIO[32];
   __shared__ int sEpoch;
   const int tid = threadIdx.x;
   if (tid == 0) sEpoch = *(volatile int*)&P.st->epoch + 1;
@@ -746,10 +959,14 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
     const int* const flag_s = ty > 0 ? P.flags + (item - P.ntx) * (g.nz + 1) : nullptr;
     const int* const flag_sw = (tx > 0 && ty > 0) ? P.flags + (item - P.ntx - 1) * (g.nz + 1) : nullptr;
 
-    // prologue: planes 0, 1 and side 0 as one cp.async group
-    load_plane<NI>(P, Plane<NI>{sm + C::O_IP}, x0, y0, tw, th, 0);
-    load_side<NI>(P, Side<NI>{sm + C::O_IS}, x0, y0, tw, th, 0);
-    load_plane<NI>(P, Plane<NI>{sm + C::O_IP + C::PLANE}, x0, y0, tw, th, 1);
+    // row descriptors of the tile, then the prologue: planes 0, 1 and side 0 as one cp.async group
+    int ns;
+    build_rows<NI>(P, sIO, x0, y0, tw, th, &ns);
+    const int nrw = ns + 4 * th + 2;
+    __syncthreads();
+    load_rows(P.x, sIO, ns, nrw, sm + C::O_IP, 0, zdir(g, 0));
+    load_rows(P.x, sIO, 0, ns, sm + C::O_IS, 0, false);
+    load_rows(P.x, sIO, ns, nrw, sm + C::O_IP + C::PLANE, 1, zdir(g, 1));
     cp_commit();
     for (int t = tid; t < C::PLANE; t += NT) sm[C::O_AP + t] = 0.0;
 
@@ -759,7 +976,9 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
       const Plane<NI> inb{sm + C::O_IP + (l & 1) * C::PLANE}, intp{sm + C::O_IP + ((l + 1) & 1) * C::PLANE};
       const Plane<NI> acb{sm + C::O_AP + (l & 1) * C::PLANE}, actp{sm + C::O_AP + ((l + 1) & 1) * C::PLANE};
       // early prefetch: side l+1 (overlaps this step's compute)
-      if (l + 1 < g.nz) load_side<NI>(P, Side<NI>{sm + C::O_IS + ((l + 1) & 1) * C::SIDE}, x0, y0, tw, th, l + 1);
+#if !(defined(SC_EXP) && SC_EXP == 25)
+      if (l + 1 < g.nz) load_rows(P.x, sIO, 0, ns, sm + C::O_IS + ((l + 1) & 1) * C::SIDE, l + 1, false);
+#endif
       cp_commit();
       cp_wait<1>();
       __syncthreads();
@@ -787,22 +1006,35 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
         }
         SC_PHASE(1);
         // ============ condensed part: parity-class warps, two output rounds ============
-        vol_class<NI>(kWarpClass[warp], sCf, in, inb, intp, ac, acb, actp, rq, vix, viy, tw, th);
+#if !(defined(SC_EXP) && SC_EXP == 21)
+        vol_class<NI>(kWarpClass[warp], sCf, in, inb, intp, ac, acb, actp, rq, vix, viy, tw, th, ph_t0);
+#endif
         __syncthreads();
         SC_PHASE(2);
-        // ============ primary part Htilde_BB, entity-centric over the tile's elements ============
-#if !defined(SC_EXP) || SC_EXP != 2
+        // ============ primary part Htilde_BB of the edges / vertices, entity-centric ============
         // (Mtilde = diag(w0, 1..1, w0); Ktilde arrowhead: row 0 = (K00, a0, K0p),
         //  row p = (K0p, ap, K00), interior row m = (a0_m @0, Lam_m @m, ap_m @p).)
-        // Faces: a warp (or a lane group) per face, lanes over the in-face nodes; edges: lane
-        // groups of n_I per edge; vertices: a lane each.  Each accumulator entry is owned by
-        // exactly one lane, which sums the contributions of the tile's adjacent elements.
+        // Edges: lane groups of n_I per edge; vertices: a lane each.  Each accumulator entry is
+        // owned by exactly one lane, which sums the contributions of the tile's adjacent elements.
+        // All results of a thread are computed first and added to the accumulators at the end
+        // (no shared-memory read-after-write chain between entities).
+#if !(defined(SC_EXP) && SC_EXP == 22)
         {
           auto present = [&](int ix, int iy) { return ix >= 0 && iy >= 0 && ix < tw && iy < th; };
+          constexpr int NZE = (TY + 1) * (TX + 1), NXE = 2 * (TY + 1) * TX, NYE = 2 * TY * (TX + 1);
+          constexpr int SZ = (NZE + NW * EPW - 1) / (NW * EPW), SX = (NXE + NW * EPW - 1) / (NW * EPW);
+          constexpr int SY = (NYE + NW * EPW - 1) / (NW * EPW), SV = (2 * NZE + NT - 1) / NT;
+          constexpr int SN = SZ + SX + SY + SV;
+          double res[SN];
+          int dsto[SN];
+          const double w02d0 = dA * w02;
+#pragma unroll
+          for (int s = 0; s < SN; ++s) { res[s] = 0.0; dsto[s] = -1; }
           // ---- z-edges (fx = ix, fy = iy), coord k = c
-          for (int e0 = warp * EPW; e0 < (TY + 1) * (TX + 1); e0 += NW * EPW) {
-            const int e = e0 + esub, ix = e % (TX + 1), iy = e / (TX + 1), c = ec;
-            if (!evalid || e >= (TY + 1) * (TX + 1) || ix > tw || iy > th) continue;
+#pragma unroll
+          for (int s = 0; s < SZ; ++s) {
+            const int e = (s * NW + warp) * EPW + esub, ix = e % (TX + 1), iy = e / (TX + 1), c = ec;
+            if (!evalid || e >= NZE || ix > tw || iy > th) continue;
             const double u = in.ze(iy, ix)[c];
             const double tz = sA0[c] * (*inb.vv(iy, ix) + ((c & 1) ? -*intp.vv(iy, ix) : *intp.vv(iy, ix))) + sLam[c] * u;
             double y = 0.0;
@@ -810,20 +1042,21 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
             for (int el = 0; el < 4; ++el) {
               const int ib = el & 1, jb = el >> 1, ex = ix - ib, ey = iy - jb;
               if (!present(ex, ey)) continue;
-              
               const double txl = (ib ? K0p : K00) * in.ze(iy, ex)[c] + (ib ? K00 : K0p) * in.ze(iy, ex + 1)[c] +
                                  eo_row(rq + C::R_YI + (iy * TX + ex) * 2 * NI + 2 * c, ib);
               const double tyl = (jb ? K0p : K00) * in.ze(ey, ix)[c] + (jb ? K00 : K0p) * in.ze(ey + 1, ix)[c] +
                                  eo_row(rq + C::R_XJ + (ey * (TX + 1) + ix) * 2 * NI + 2 * c, jb);
-              y += dA * w02 * u + dB * w0 * txl + dC * w0 * tyl + dD * w02 * tz;
+              y += w02d0 * u + dB * w0 * txl + dC * w0 * tyl + dD * w02 * tz;
             }
-            ac.ze(iy, ix)[c] += y;
+            res[s] = y;
+            dsto[s] = (int)(ac.ze(iy, ix) + c - sm);
           }
           // ---- x-edges (ex = ix, fy = iy) of planes l, l+1, coord i = c
-          for (int e0 = warp * EPW; e0 < 2 * (TY + 1) * TX; e0 += NW * EPW) {
-            const int e = e0 + esub, kb = e / ((TY + 1) * TX), ff = e % ((TY + 1) * TX), ix = ff % TX, iy = ff / TX;
-            const int c = ec;
-            if (!evalid || e >= 2 * (TY + 1) * TX || ix >= tw || iy > th) continue;
+#pragma unroll
+          for (int s = 0; s < SX; ++s) {
+            const int e = (s * NW + warp) * EPW + esub, kb = e / ((TY + 1) * TX), ff = e % ((TY + 1) * TX);
+            const int ix = ff % TX, iy = ff / TX, c = ec;
+            if (!evalid || e >= NXE || ix >= tw || iy > th) continue;
             const Plane<NI> pk = kb ? intp : inb;
             const double u = pk.xe(iy, ix)[c];
             const double txl = sA0[c] * (*pk.vv(iy, ix) + ((c & 1) ? -*pk.vv(iy, ix + 1) : *pk.vv(iy, ix + 1))) + sLam[c] * u;
@@ -834,19 +1067,19 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
             for (int el = 0; el < 2; ++el) {
               const int jb = el, ey = iy - jb;
               if (!present(ix, ey)) continue;
-              
               const double tyl = (jb ? K0p : K00) * pk.xe(ey, ix)[c] + (jb ? K00 : K0p) * pk.xe(ey + 1, ix)[c] +
                                  eo_row(rq + C::R_ZJ + (kb * TY * TX + ey * TX + ix) * 2 * NI + 2 * c, jb);
-              y += dA * w02 * u + dB * w02 * txl + dC * w0 * tyl + dD * w0 * tzl;
+              y += w02d0 * u + dB * w02 * txl + dC * w0 * tyl + dD * w0 * tzl;
             }
-            (kb ? actp : acb).xe(iy, ix)[c] += y;
+            res[SZ + s] = y;
+            dsto[SZ + s] = (int)((kb ? actp : acb).xe(iy, ix) + c - sm);
           }
           // ---- y-edges (fx = ix, ey = iy) of planes l, l+1, coord j = c
-          for (int e0 = warp * EPW; e0 < 2 * TY * (TX + 1); e0 += NW * EPW) {
-            const int e = e0 + esub, kb = e / (TY * (TX + 1)), ff = e % (TY * (TX + 1)), ix = ff % (TX + 1),
-                      iy = ff / (TX + 1);
-            const int c = ec;
-            if (!evalid || e >= 2 * TY * (TX + 1) || ix > tw || iy >= th) continue;
+#pragma unroll
+          for (int s = 0; s < SY; ++s) {
+            const int e = (s * NW + warp) * EPW + esub, kb = e / (TY * (TX + 1)), ff = e % (TY * (TX + 1));
+            const int ix = ff % (TX + 1), iy = ff / (TX + 1), c = ec;
+            if (!evalid || e >= NYE || ix > tw || iy >= th) continue;
             const Plane<NI> pk = kb ? intp : inb;
             const double u = pk.ye(iy, ix)[c];
             const double tyl = sA0[c] * (*pk.vv(iy, ix) + ((c & 1) ? -*pk.vv(iy + 1, ix) : *pk.vv(iy + 1, ix))) + sLam[c] * u;
@@ -857,18 +1090,18 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
             for (int el = 0; el < 2; ++el) {
               const int ib = el, ex = ix - ib;
               if (!present(ex, iy)) continue;
-              
               const double txl = (ib ? K0p : K00) * pk.ye(iy, ex)[c] + (ib ? K00 : K0p) * pk.ye(iy, ex + 1)[c] +
                                  eo_row(rq + C::R_ZI + (kb * TY * TX + iy * TX + ex) * 2 * NI + 2 * c, ib);
-              y += dA * w02 * u + dB * w0 * txl + dC * w02 * tyl + dD * w0 * tzl;
+              y += w02d0 * u + dB * w0 * txl + dC * w02 * tyl + dD * w0 * tzl;
             }
-            (kb ? actp : acb).ye(iy, ix)[c] += y;
+            res[SZ + SX + s] = y;
+            dsto[SZ + SX + s] = (int)((kb ? actp : acb).ye(iy, ix) + c - sm);
           }
           // ---- vertices (fx = ix, fy = iy) of planes l, l+1
-          for (int v = tid; v < 2 * (TY + 1) * (TX + 1); v += NT) {
-            const int kb = v / ((TY + 1) * (TX + 1)), ff = v % ((TY + 1) * (TX + 1)), ix = ff % (TX + 1),
-                      iy = ff / (TX + 1);
-            if (ix > tw || iy > th) continue;
+#pragma unroll
+          for (int s = 0; s < SV; ++s) {
+            const int v = s * NT + tid, kb = v / NZE, ff = v % NZE, ix = ff % (TX + 1), iy = ff / (TX + 1);
+            if (v >= 2 * NZE || ix > tw || iy > th) continue;
             const Plane<NI> pk = kb ? intp : inb;
             const double u = *pk.vv(iy, ix);
             const double tzl = (kb ? K0p : K00) * *inb.vv(iy, ix) + (kb ? K00 : K0p) * *intp.vv(iy, ix) +
@@ -878,208 +1111,52 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
             for (int el = 0; el < 4; ++el) {
               const int ib = el & 1, jb = el >> 1, ex = ix - ib, ey = iy - jb;
               if (!present(ex, ey)) continue;
-              
               const double txl = (ib ? K0p : K00) * *pk.vv(iy, ex) + (ib ? K00 : K0p) * *pk.vv(iy, ex + 1) +
                                  eo_row(rq + C::R_XE + (kb * (TY + 1) * TX + iy * TX + ex) * 2, ib);
               const double tyl = (jb ? K0p : K00) * *pk.vv(ey, ix) + (jb ? K00 : K0p) * *pk.vv(ey + 1, ix) +
                                  eo_row(rq + C::R_YE + (kb * TY * (TX + 1) + ey * (TX + 1) + ix) * 2, jb);
-              y += dA * w02 * w0 * u + w02 * (dB * txl + dC * tyl + dD * tzl);
+              y += w02d0 * w0 * u + w02 * (dB * txl + dC * tyl + dD * tzl);
             }
-            *(kb ? actp : acb).vv(iy, ix) += y;
+            res[SZ + SX + SY + s] = y;
+            dsto[SZ + SX + SY + s] = (int)((kb ? actp : acb).vv(iy, ix) - sm);
           }
+          double old[SN];
+#pragma unroll
+          for (int s = 0; s < SN; ++s) old[s] = dsto[s] >= 0 ? sm[dsto[s]] : 0.0;
+#pragma unroll
+          for (int s = 0; s < SN; ++s)
+            if (dsto[s] >= 0) sm[dsto[s]] = old[s] + res[s];
         }
 #endif
         __syncthreads();
         SC_PHASE(6);
       }
       // late prefetch: plane l+2 into the buffer of plane l (no longer read)
-      if (l + 2 <= g.nz) load_plane<NI>(P, Plane<NI>{sm + C::O_IP + (l & 1) * C::PLANE}, x0, y0, tw, th, l + 2);
+#if !(defined(SC_EXP) && SC_EXP == 25)
+      if (l + 2 <= g.nz) load_rows(P.x, sIO, ns, nrw, sm + C::O_IP + (l & 1) * C::PLANE, l + 2, zdir(g, l + 2));
+#endif
       cp_commit();
-      // ================= finalize step l: publish / write owned / park ==========================
-      // Ownership: the highest-ticket contributing tile (tiles are ticketed x-fastest): a tile
-      // owns its W / S boundaries (finished one step later from parked partials) and publishes
-      // its E / N boundaries (y-in-place; the three 4-tile rim corners go to corner records).
-      // Every loop below is a warp per contiguous row with range-only classification.
-      {
-        const bool pzd = zdir(g, l);
-        const int x1 = x0 + tw, y1 = y0 + th;
-        const bool hasE = x1 < g.nx, hasN = y1 < g.ny, hasW = x0 > 0, hasS = y0 > 0;
-        const bool dW = (x0 == 0), dE = (x1 == g.nx);                 // Dirichlet row ends
-        double* const pd = P.pending + (item * 2 + (l & 1)) * (long long)C::PEND;
-#if !defined(SC_EXP) || SC_EXP != 1
-        // ---- (a) publish
-        if (!last) {
-          if (hasE)
-            for (int row = warp; row < th; row += NW) {
-              double* yo = P.y + A.xf(x1, y0 + row, l);
-              const double* s = ac.xf(row, tw);
-              for (int t = lane; t < N2; t += 32) yo[t] = s[t];
-            }
-          if (hasN) {
-            double* yo = P.y + A.yf(x0, y1, l);
-            const double* s = ac.yf(th, 0);
-            for (int t = tid; t < tw * N2; t += NT) yo[t] = s[t];
-          }
-        }
-        if (!pzd) {
-          if (hasN) {
-            double* yo = P.y + A.xe(x0, y1, l);
-            const double* s = acb.xe(th, 0);
-            for (int t = tid; t < tw * NI; t += NT) yo[t] = s[t];
-          }
-          if (hasE)
-            for (int row = warp; row < th; row += NW) {
-              double* yo = P.y + A.ye(x1, y0 + row, l);
-              const double* s = acb.ye(row, tw);
-              for (int t = lane; t < NI; t += 32) yo[t] = s[t];
-            }
-        }
-        // z-edges (layer l, c < NI) / vertices (plane l, c == NI) on the E column and N row
-        if (warp == 0) {
-          const int nE = hasE ? th + 1 : 0, nN = hasN ? tw : 0;
-          for (int t = lane; t < (nE + nN) * (NI + 1); t += 32) {
-            const int ent = t / (NI + 1), c = t - ent * (NI + 1);
-            const bool isv = (c == NI);
-            if (isv ? pzd : last) continue;
-            int ix, iy;
-            if (ent < nE) { ix = tw; iy = ent; } else { ix = ent - nE; iy = th; }
-            const int fx = x0 + ix, fy = y0 + iy;
-            if (fx == 0 || fy == 0 || fy == g.ny) continue;          // Dirichlet
-            const bool ex_ = (ix == tw && hasE), ny_ = (iy == th && hasN);
-            const double v = isv ? *acb.vv(iy, ix) : ac.ze(iy, ix)[c];
-            if (ex_ && ny_) corner_rec(P, fx / TX, fy / TY, l, 0)[c] = v;                   // SW of owner
-            else if (ex_ && iy == 0 && hasS) corner_rec(P, fx / TX, fy / TY, l, 2)[c] = v;   // W of owner
-            else if (ny_ && ix == 0 && hasW) corner_rec(P, fx / TX, fy / TY, l, 1)[c] = v;   // S of owner
-            else if (isv) P.y[A.vv(fx, fy, l)] = v;
-            else P.y[A.ze(fx, fy, l) + c] = v;
-          }
-        }
+#if !(defined(SC_EXP) && SC_EXP == 23)
+      finalize_step<NI>(P, item, l, x0, y0, tw, th, ac, acb, sIO, ns);
 #endif
-        // publication: the CTA barrier orders every thread's stores before thread 0's GPU-scope
-        // fence + release store of the flag (cumulativity of bar.sync + fence.acq_rel.gpu)
-        __syncthreads();
-        SC_PHASE(7);
-        if (tid == 0) {
-          __threadfence();
-          flag_release(flag_me + l, epoch);
-        }
-#if !defined(SC_EXP) || SC_EXP != 1
-#if defined(SC_EXP) && SC_EXP == 7
-        if (false)
+      // publication: the CTA barrier orders every thread's stores before thread 0's GPU-scope
+      // fence + release store of the flag (cumulativity of bar.sync + fence.acq_rel.gpu)
+      __syncthreads();
+      SC_PHASE(7);
+      if (tid == 0) {
+#if !(defined(SC_EXP) && SC_EXP == 26)
+        __threadfence();
 #endif
-        // ---- (b) owned entities (incl. Dirichlet zeros) and (b') parked W / S partials.
-        // Flat loops over the whole tile of each class (all warps busy); smem rows and global
-        // rows are both contiguous, so entry (row, c) is base + row * stride + c on both sides.
-        {
-          const unsigned nxf = (unsigned)(g.nx + 1) * N2, nyf = (unsigned)g.nx * N2;
-          const unsigned nxe = (unsigned)g.nx * NI, nye = (unsigned)(g.nx + 1) * NI;
-          const unsigned nze = (unsigned)(g.nx + 1) * NI, nvv = (unsigned)(g.nx + 1);
-          if (!last) {
-            {   // x-faces: rows iy < th, entries c < (tw + 1) N2
-              constexpr unsigned RL = (TX + 1) * N2;
-              double* yo = P.y + A.xf(x0, y0, l);
-              const unsigned t1 = hasE ? tw * N2 : (tw + 1) * N2;
-              for (unsigned t = tid; t < th * RL; t += NT) {
-                const unsigned row = t / RL, c = t - row * RL;
-                if (c >= t1) continue;
-                const double v = ac.b[C::S_XF + t];
-                if (c < N2 && hasW) { pd[C::PD_XF + row * N2 + c] = v; continue; }
-                yo[row * nxf + c] = ((dW && c < N2) || (dE && c >= tw * N2)) ? 0.0 : v;
-              }
-            }
-            {   // y-faces: rows iy <= th
-              constexpr unsigned RL = TX * N2;
-              double* yo = P.y + A.yf(x0, y0, l);
-              for (unsigned t = tid; t < (th + 1) * RL; t += NT) {
-                const unsigned row = t / RL, c = t - row * RL;
-                if (c >= tw * N2 || (row == th && hasN)) continue;
-                const double v = ac.b[C::S_YF + t];
-                if (row == 0 && hasS) { pd[C::PD_YF + c] = v; continue; }
-                const int fy = y0 + row;
-                yo[row * nyf + c] = (fy == 0 || fy == g.ny) ? 0.0 : v;
-              }
-            }
-            {   // z-edges: rows iy <= th, entries c < (tw + 1) NI
-              constexpr unsigned RL = (TX + 1) * NI;
-              double* yo = P.y + A.ze(x0, y0, l);
-              for (unsigned t = tid; t < (th + 1) * RL; t += NT) {
-                const unsigned row = t / RL, c = t - row * RL;
-                if (c >= (tw + 1) * NI) continue;
-                const bool lo = c < NI, hi = c >= tw * NI;
-                if ((row == th && hasN) || (hi && hasE)) continue;               // published
-                const int fy = y0 + row;
-                const bool rd = fy == 0 || fy == g.ny;
-                const double v = ac.b[C::S_ZE + t];
-                if (rd || (lo && dW) || (hi && dE)) { yo[row * nze + c] = 0.0; continue; }
-                if (lo && hasW) { pd[C::PD_ZEW + row * NI + c] = v; continue; }    // W column
-                if (row == 0 && hasS) { pd[C::PD_ZES + c - NI] = v; continue; }   // S row
-                yo[row * nze + c] = v;
-              }
-            }
-          }
-          {   // z-faces of plane l
-            constexpr unsigned RL = TX * N2;
-            double* yo = P.y + A.zf(x0, y0, l);
-            for (unsigned t = tid; t < th * RL; t += NT) {
-              const unsigned row = t / RL, c = t - row * RL;
-              if (c < tw * N2) yo[row * nyf + c] = pzd ? 0.0 : acb.b[C::P_ZF + t];
-            }
-          }
-          {   // x-edges of plane l: rows iy <= th
-            constexpr unsigned RL = TX * NI;
-            double* yo = P.y + A.xe(x0, y0, l);
-            for (unsigned t = tid; t < (th + 1) * RL; t += NT) {
-              const unsigned row = t / RL, c = t - row * RL;
-              if (c >= tw * NI || (row == th && hasN && !pzd)) continue;
-              const int fy = y0 + row;
-              const bool rd = pzd || fy == 0 || fy == g.ny;
-              const double v = acb.b[C::P_XE + t];
-              if (row == 0 && hasS && !rd) { pd[C::PD_XE + c] = v; continue; }
-              yo[row * nxe + c] = rd ? 0.0 : v;
-            }
-          }
-          {   // y-edges of plane l: rows iy < th, entries c < (tw + 1) NI
-            constexpr unsigned RL = (TX + 1) * NI;
-            double* yo = P.y + A.ye(x0, y0, l);
-            for (unsigned t = tid; t < th * RL; t += NT) {
-              const unsigned row = t / RL, c = t - row * RL;
-              if (c >= (tw + 1) * NI) continue;
-              const bool lo = c < NI, hi = c >= tw * NI;
-              if (hi && hasE && !pzd) continue;
-              const double v = acb.b[C::P_YE + t];
-              if (pzd || (lo && dW) || (hi && dE)) { yo[row * nye + c] = 0.0; continue; }
-              if (lo && hasW) { pd[C::PD_YE + row * NI + c] = v; continue; }
-              yo[row * nye + c] = v;
-            }
-          }
-          {   // vertices of plane l: rows iy <= th, entries c <= tw
-            constexpr unsigned RL = TX + 1;
-            double* yo = P.y + A.vv(x0, y0, l);
-            for (unsigned t = tid; t < (th + 1) * RL; t += NT) {
-              const unsigned row = t / RL, c = t - row * RL;
-              if (c > (unsigned)tw) continue;
-              const bool lo = c == 0, hi = c == (unsigned)tw;
-              if ((row == th && hasN && !pzd) || (hi && hasE && !pzd)) continue;
-              const int fy = y0 + row;
-              const bool rd = pzd || fy == 0 || fy == g.ny;
-              const double v = acb.b[C::P_VV + t];
-              if (rd || (lo && dW) || (hi && dE)) { yo[row * nvv + c] = 0.0; continue; }
-              if (lo && hasW) { pd[C::PD_VW + row] = v; continue; }
-              if (row == 0 && hasS) { pd[C::PD_VS + c - 1] = v; continue; }
-              yo[row * nvv + c] = v;
-            }
-          }
-        }
-#endif
+        flag_release(flag_me + l, epoch);
       }
-      // (c, d) finish the W / S boundary entities of the PREVIOUS step
-#if !defined(SC_EXP) || (SC_EXP != 1 && SC_EXP != 6)
-      if (l >= 1) finish_boundary<NI>(P, item, l - 1, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch);
+      // finish the W / S boundary entities of the PREVIOUS step (deferred look-back)
+#if !(defined(SC_EXP) && SC_EXP == 24)
+      if (l >= 1) finish_boundary<NI>(P, item, l - 1, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO);
 #endif
       __syncthreads();
       SC_PHASE(8);
     }
-    finish_boundary<NI>(P, item, g.nz, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch);
+    finish_boundary<NI>(P, item, g.nz, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO);
     __syncthreads();
   }
   if (tid == 0) {
@@ -1118,7 +1195,7 @@ static int launch_col_t(const ColParams& P, cudaStream_t st, int* nl, int* grid_
 
 #if defined(SC_EXP) && SC_EXP == 9
 extern "C" int sc_exp_phase_cycles(unsigned long long* out) {
-  return (int)cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 16);
+  return (int)cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 8 * 16);
 }
 #endif
 

@@ -1,4 +1,3 @@
-export SC_EXP=9 SC_LIBDIR=/tmp/exp9 SC_LIB_PATH=/tmp/exp9/libsc.so
-python -c "from paper_1601_08179_b200 import build as b; b.build()" > /dev/null
-python tools/prof_apply.py --p 8 --n 128 --reps 2 | tail -1
-python tools/phase_exp.py 128
+export SC_EXP=9 SC_LIBDIR=exp_lib/exp9 SC_LIB_PATH=exp_lib/exp9/libsc.so
+python tools/prof_apply.py --p 8 --n ${1:-32} --reps 2 | tail -1
+python tools/phase_exp.py ${1:-32}
