@@ -307,7 +307,7 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
       if (cudaMalloc(&ctx->d_colstate, 64) != cudaSuccess) return fail("cudaMalloc colstate");
       if (cudaMalloc(&ctx->d_flags, sizeof(int) * nflags) != cudaSuccess) return fail("cudaMalloc flags");
       if (cudaMalloc(&ctx->d_corner, sizeof(double) * ncorner) != cudaSuccess) return fail("cudaMalloc corner");
-      size_t npend = (size_t)ctx->col_ntx * ctx->col_nty * 2 * pend;
+      size_t npend = (size_t)ctx->col_ntx * ctx->col_nty * 3 * pend;   // 3 step slots (look-back distance 2)
       if (cudaMalloc(&ctx->d_pending, sizeof(double) * npend) != cudaSuccess) return fail("cudaMalloc pending");
       if (cudaMemset(ctx->d_colstate, 0, 64) != cudaSuccess) return fail("memset colstate");
       if (cudaMemset(ctx->d_flags, 0, sizeof(int) * nflags) != cudaSuccess) return fail("memset flags");

@@ -4,10 +4,10 @@
 // a work item is one tile-column (all nz element layers of the tile).  A persistent CTA (one
 // per SM, 8 warps) takes items in ticket order and marches up the column one element layer at
 // a time.  Every entity of the skeleton is assembled on chip except those on tile side
-// boundaries, which are finished with a decoupled look-back: the lower-ticket contributor
+// boundaries, which are finished with a decoupled look-back (distance 2): the lower-ticket contributor
 // stores its partial sum straight into y (or, on the 4-tile corner lines, into a small corner
 // record), publishes a per-(item, layer) flag, and the owner (highest-ticket contributor) adds
-// it and writes the final value one step later.  Every skeleton entry is written exactly once
+// it and writes the final value two steps later.  Every skeleton entry is written exactly once
 // (no memset, no atomics) and read from HBM once.
 //
 // Condensed part (faces-in, D^{-1}, faces-out; §6 Table 2) in the even/odd
@@ -96,7 +96,7 @@ struct CS {
   static constexpr int O_TAB = O_RQ + RED;           // a0, lam (2 x 32)
   static constexpr int O_CF = O_TAB + 2 * 32;        // ColCoef copy
   static constexpr int TOTAL = O_CF + (int)(sizeof(ColCoef) / sizeof(double));
-  // parked own partials of the W / S boundary entities (global, per tile, 2 step slots)
+  // parked own partials of the W / S boundary entities (global, per tile, 3 step slots)
   static constexpr int PD_XF = 0;                                  // W column x-faces  [TY][N2]
   static constexpr int PD_YF = PD_XF + TY * N2;                    // S row y-faces     [TX N2]
   static constexpr int PD_XE = PD_YF + TX * N2;                    // S row x-edges     [TX NI]
@@ -380,7 +380,7 @@ __device__ void finalize_step(const ColParams& P, long long item, int l, int x0,
   const bool last = (l == g.nz), pzd = zdir(g, l);
   const int x1 = x0 + tw, y1 = y0 + th;
   const bool hasE = x1 < g.nx, hasN = y1 < g.ny, hasW = x0 > 0, hasS = y0 > 0;
-  double* const pd = P.pending + (item * 2 + (l & 1)) * (long long)C::PEND;
+  double* const pd = P.pending + (item * 3 + l % 3) * (long long)C::PEND;
   const int nr = ns + 4 * th + 2;
   for (int r = (last ? ns : 0) + warp; r < nr; r += NW) {
     const RowIO& d = io[r];
@@ -457,7 +457,7 @@ __device__ void finish_boundary(const ColParams& P, long long item, int ls, int 
     }
   }
   __syncthreads();
-  const double* pd = P.pending + (item * 2 + (ls & 1)) * (long long)C::PEND;
+  const double* pd = P.pending + (item * 3 + ls % 3) * (long long)C::PEND;
   // segment sizes of the flat list (0 when the segment does not apply at this step)
   const int n0 = (!last && hasW) ? th * N2 : 0;            // W col x-faces
   const int n1 = (!last && hasS) ? tw * N2 : 0;            // S row y-faces
@@ -559,7 +559,11 @@ __device__ __forceinline__ void vol_class(const int cls, const ColCoef* cf, cons
   // edge / vertex rows, by the class with s_d == DO of each direction d.  Initialises ac.xf,
   // ac.yf and actp.zf (plain stores), adds into acb.zf.  Per direction: all shared-memory
   // loads, then the arithmetic, then all stores.
+#if defined(SC_EXP) && SC_EXP == 30
+  const bool nonempty = false;   // ablation: no phase A
+#else
   const bool nonempty = CI > 0 && CJ > 0 && CK > 0;
+#endif
   if (si == DO && nonempty) {   // x-faces: face ix = W of element ix, E of element ix-1 (entries (j,k))
     const double* Z0 = in.ze(iy, ix) + sk;
     const double* Z1 = in.ze(iy + 1, ix) + sk;
@@ -763,6 +767,13 @@ __device__ __forceinline__ void vol_class(const int cls, const ColCoef* cf, cons
   // ---- phase B: condensed part of the class (registers only)
   const double* Dv = cf->dinv + si + NI * sj + N2 * sk;
   double qx[M][M], qy[M][M], qz[M][M];
+#if defined(SC_EXP) && SC_EXP == 31
+#pragma unroll
+  for (int a = 0; a < M; ++a)
+#pragma unroll
+    for (int b = 0; b < M; ++b) qx[a][b] = qy[a][b] = qz[a][b] = 0.0;   // ablation: no phase B
+  if (false)
+#endif
   {
     double c1[M], c2[M], c3[M];
 #pragma unroll
@@ -814,77 +825,94 @@ __device__ __forceinline__ void vol_class(const int cls, const ColCoef* cf, cons
 #pragma unroll 1
   for (int r = 0; r < 2; ++r) {
     bar_named(1);
+#if defined(SC_EXP) && SC_EXP == 32
+    continue;   // ablation: no output rounds
+#endif
     SC_PHASE(5 + 6 * r);
-    if (r == si) {   // W -= Q(ix) + g Q(ix-1) on face ix; the last element also E -= g Q
-      double o0[M][M], o1[M][M];
+    // The two classes of a direction (s_d = 0, 1) update the same entries; each round splits
+    // them in halves (class s_d takes half h = r ^ s_d), so every warp does half of each of its
+    // three directions in each round (balanced rounds, no warp idles while its SM-sub-partition
+    // partner works).  Stores are predicated: the shuffles run converged.
+    {   // x-faces, entries (jj, kk), halves by kk: W -= Q(ix) + g Q(ix-1), last element E -= g Q
+      const int h = r ^ si;
+      double o0[M][2], o1[M][2];
 #pragma unroll
       for (int jj = 0; jj < M; ++jj)
 #pragma unroll
-        for (int kk = 0; kk < M; ++kk) {
-          const bool ok = act && jj < CJ && kk < CK;
+        for (int t = 0; t < 2; ++t) {
+          const int kk = 2 * h + t;
+          const bool ok = act && jj < CJ && kk < CK && kk < M;
           const int o = 2 * jj + 2 * NI * kk;
-          o0[jj][kk] = ok ? fX[o] : 0.0;
-          o1[jj][kk] = (ok && lastx) ? fX[o + N2] : 0.0;
+          o0[jj][t] = ok ? fX[o] : 0.0;
+          o1[jj][t] = (ok && lastx) ? fX[o + N2] : 0.0;
         }
 #pragma unroll
       for (int jj = 0; jj < M; ++jj)
 #pragma unroll
-        for (int kk = 0; kk < M; ++kk) {
-          if (jj >= CJ || kk >= CK) continue;
+        for (int t = 0; t < 2; ++t) {
+          const int kk = 2 * h + t;
+          const bool ok = act && jj < CJ && kk < CK && kk < M;
           const int o = 2 * jj + 2 * NI * kk;
-          const double Q = qx[jj][kk];
+          const double Q = h ? (2 + t < M ? qx[jj][(2 + t) % M] : 0.0) : qx[jj][t % M];
           const double Qm = __shfl_up_sync(0xffffffffu, Q, 1);
-          if (act) {
-            fX[o] = o0[jj][kk] - (ix > 0 ? fma(gi, Qm, Q) : Q);
-            if (lastx) fX[o + N2] = fma(-gi, Q, o1[jj][kk]);
-          }
+          const double n0 = o0[jj][t] - (ix > 0 ? fma(gi, Qm, Q) : Q), n1 = fma(-gi, Q, o1[jj][t]);
+          if (ok) fX[o] = n0;
+          if (ok && lastx) fX[o + N2] = n1;
         }
     }
-    if (r == sj) {
-      double o0[M][M], o1[M][M];
+    {   // y-faces, entries (ii, kk), halves by kk
+      const int h = r ^ sj;
+      double o0[M][2], o1[M][2];
 #pragma unroll
       for (int ii = 0; ii < M; ++ii)
 #pragma unroll
-        for (int kk = 0; kk < M; ++kk) {
-          const bool ok = act && ii < CI && kk < CK;
+        for (int t = 0; t < 2; ++t) {
+          const int kk = 2 * h + t;
+          const bool ok = act && ii < CI && kk < CK && kk < M;
           const int o = 2 * ii + 2 * NI * kk;
-          o0[ii][kk] = ok ? fY[o] : 0.0;
-          o1[ii][kk] = (ok && lasty) ? fY[o + TX * N2] : 0.0;
+          o0[ii][t] = ok ? fY[o] : 0.0;
+          o1[ii][t] = (ok && lasty) ? fY[o + TX * N2] : 0.0;
         }
 #pragma unroll
       for (int ii = 0; ii < M; ++ii)
 #pragma unroll
-        for (int kk = 0; kk < M; ++kk) {
-          if (ii >= CI || kk >= CK) continue;
+        for (int t = 0; t < 2; ++t) {
+          const int kk = 2 * h + t;
+          const bool ok = act && ii < CI && kk < CK && kk < M;
           const int o = 2 * ii + 2 * NI * kk;
-          const double Q = qy[ii][kk];
+          const double Q = h ? (2 + t < M ? qy[ii][(2 + t) % M] : 0.0) : qy[ii][t % M];
           const double Qm = __shfl_up_sync(0xffffffffu, Q, TX);
-          if (act) {
-            fY[o] = o0[ii][kk] - (iy > 0 ? fma(gj, Qm, Q) : Q);
-            if (lasty) fY[o + TX * N2] = fma(-gj, Q, o1[ii][kk]);
-          }
+          const double n0 = o0[ii][t] - (iy > 0 ? fma(gj, Qm, Q) : Q), n1 = fma(-gj, Q, o1[ii][t]);
+          if (ok) fY[o] = n0;
+          if (ok && lasty) fY[o + TX * N2] = n1;
         }
     }
-    if (r == sk && act) {
-      double o0[M][M], o1[M][M];
+    if (act) {   // z-faces, entries (jj, ii), halves by ii: B -= Q, T -= g Q
+      const int h = r ^ sk;
+      double o0[M][2], o1[M][2];
 #pragma unroll
       for (int jj = 0; jj < M; ++jj)
 #pragma unroll
-        for (int ii = 0; ii < M; ++ii) {
-          const bool ok = ii < CI && jj < CJ;
+        for (int t = 0; t < 2; ++t) {
+          const int ii = 2 * h + t;
+          const bool ok = ii < CI && jj < CJ && ii < M;
           const int o = 2 * ii + 2 * NI * jj;
-          o0[jj][ii] = ok ? fB[o] : 0.0;
-          o1[jj][ii] = ok ? fT[o] : 0.0;
+          o0[jj][t] = ok ? fB[o] : 0.0;
+          o1[jj][t] = ok ? fT[o] : 0.0;
         }
 #pragma unroll
       for (int jj = 0; jj < M; ++jj)
 #pragma unroll
-        for (int ii = 0; ii < M; ++ii)
-          if (ii < CI && jj < CJ) {
-            const int o = 2 * ii + 2 * NI * jj;
-            fB[o] = o0[jj][ii] - qz[jj][ii];
-            fT[o] = fma(-gk, qz[jj][ii], o1[jj][ii]);
+        for (int t = 0; t < 2; ++t) {
+          const int ii = 2 * h + t;
+          const bool ok = ii < CI && jj < CJ && ii < M;
+          const int o = 2 * ii + 2 * NI * jj;
+          const double Q = h ? (2 + t < M ? qz[jj][(2 + t) % M] : 0.0) : qz[jj][t % M];
+          if (ok) {
+            fB[o] = o0[jj][t] - Q;
+            fT[o] = fma(-gk, Q, o1[jj][t]);
           }
+        }
     }
     SC_PHASE(10 + 2 * r);
   }
@@ -1131,6 +1159,15 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
         __syncthreads();
         SC_PHASE(6);
       }
+      // publication of step l-1 (deferred look-back, distance 2): its stores were issued before
+      // the CTA barrier that ended step l-1 and have drained during this step's compute, so
+      // thread 0's GPU-scope fence (cumulative over that barrier) is cheap here.
+      if (tid == 0 && l >= 1) {
+#if !(defined(SC_EXP) && SC_EXP == 26)
+        __threadfence();
+#endif
+        flag_release(flag_me + (l - 1), epoch);
+      }
       // late prefetch: plane l+2 into the buffer of plane l (no longer read)
 #if !(defined(SC_EXP) && SC_EXP == 25)
       if (l + 2 <= g.nz) load_rows(P.x, sIO, ns, nrw, sm + C::O_IP + (l & 1) * C::PLANE, l + 2, zdir(g, l + 2));
@@ -1139,23 +1176,23 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
 #if !(defined(SC_EXP) && SC_EXP == 23)
       finalize_step<NI>(P, item, l, x0, y0, tw, th, ac, acb, sIO, ns);
 #endif
-      // publication: the CTA barrier orders every thread's stores before thread 0's GPU-scope
-      // fence + release store of the flag (cumulativity of bar.sync + fence.acq_rel.gpu)
       __syncthreads();
       SC_PHASE(7);
-      if (tid == 0) {
-#if !(defined(SC_EXP) && SC_EXP == 26)
-        __threadfence();
-#endif
-        flag_release(flag_me + l, epoch);
-      }
-      // finish the W / S boundary entities of the PREVIOUS step (deferred look-back)
+      // finish the W / S boundary entities of step l-2 (their owners' partials were published
+      // during step l-1 of the W / S / SW tiles)
 #if !(defined(SC_EXP) && SC_EXP == 24)
-      if (l >= 1) finish_boundary<NI>(P, item, l - 1, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO);
+      if (l >= 2) finish_boundary<NI>(P, item, l - 2, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO);
 #endif
       __syncthreads();
       SC_PHASE(8);
     }
+    // end of the column: publish step nz, finish steps nz-1 and nz
+    if (tid == 0) {
+      __threadfence();
+      flag_release(flag_me + g.nz, epoch);
+    }
+    if (g.nz >= 1) finish_boundary<NI>(P, item, g.nz - 1, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO);
+    __syncthreads();
     finish_boundary<NI>(P, item, g.nz, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO);
     __syncthreads();
   }
