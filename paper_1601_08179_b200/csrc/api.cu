@@ -75,6 +75,7 @@ struct sc_ctx {
   int* d_flags = nullptr;
   double* d_corner = nullptr;
   double* d_pending = nullptr;
+  double* d_dotp = nullptr;             // per-tile x . y partials of the operator (PCG p . q)
   // workspace (caller-owned)
   double* ws = nullptr;
   size_t ws_bytes = 0;
@@ -309,6 +310,8 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
       if (cudaMalloc(&ctx->d_corner, sizeof(double) * ncorner) != cudaSuccess) return fail("cudaMalloc corner");
       size_t npend = (size_t)ctx->col_ntx * ctx->col_nty * 3 * pend;   // 3 step slots (look-back distance 2)
       if (cudaMalloc(&ctx->d_pending, sizeof(double) * npend) != cudaSuccess) return fail("cudaMalloc pending");
+      if (cudaMalloc(&ctx->d_dotp, sizeof(double) * ctx->col_ntx * ctx->col_nty) != cudaSuccess)
+        return fail("cudaMalloc dotp");
       if (cudaMemset(ctx->d_colstate, 0, 64) != cudaSuccess) return fail("memset colstate");
       if (cudaMemset(ctx->d_flags, 0, sizeof(int) * nflags) != cudaSuccess) return fail("memset flags");
       if (cudaMemset(ctx->d_corner, 0, sizeof(double) * ncorner) != cudaSuccess) return fail("memset corner");
@@ -349,6 +352,7 @@ extern "C" sc_status sc_destroy(sc_ctx* ctx) {
   if (ctx->d_flags) cudaFree(ctx->d_flags);
   if (ctx->d_corner) cudaFree(ctx->d_corner);
   if (ctx->d_pending) cudaFree(ctx->d_pending);
+  if (ctx->d_dotp) cudaFree(ctx->d_dotp);
   for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);
   delete ctx;
   return SC_OK;
@@ -465,13 +469,15 @@ static sc_status allreduce_scal(sc_ctx* ctx, int slot, int n, cudaStream_t st) {
   return SC_OK;
 }
 
-static sc_status apply_impl(sc_ctx* ctx, const double* x, double* y, const double* done, cudaStream_t st) {
+// y = A x.  dotp != nullptr (single GPU, tile-column operator): the kernel also leaves the
+// per-tile partials of x . y over the final entries in dotp (fused PCG p . q).
+static sc_status apply_impl(sc_ctx* ctx, const double* x, double* y, const double* done, cudaStream_t st,
+                            double* dotp = nullptr) {
   const bool rec = ctx->prof_on && ctx->prof_n < (int)ctx->prof_ev.size() / 2;
   cudaEvent_t* ev = rec ? &ctx->prof_ev[2 * ctx->prof_n] : nullptr;
   if (ctx->use_col)
     LAUNCH(launch_apply_col_raw(ctx->g, x, y, done, ctx->d_colstate, ctx->d_flags, ctx->d_corner, ctx->d_pending,
-                                ctx->col_ntx,
-                                ctx->col_nty, ctx->col_coef.data(), st, &nl_, ev));
+                                ctx->col_ntx, ctx->col_nty, ctx->col_coef.data(), dotp, st, &nl_, ev));
   else
     LAUNCH(launch_apply(ctx->g, x, y, done, st, &nl_, ev));
   if (rec) ctx->prof_n++;
@@ -502,10 +508,15 @@ static sc_status pcg_iteration(sc_ctx* ctx, cudaStream_t st) {
   const long long n = ctx->g.n_total;
   double* done = ctx->scal + SCAL_DONE;
   double* x = ctx->x_cur;
-  sc_status s = apply_impl(ctx, ctx->pv, ctx->q, done, st);
+  const bool fused = ctx->use_col && ctx->prm.nranks == 1;   // p . q fused into the operator
+  sc_status s = apply_impl(ctx, ctx->pv, ctx->q, done, st, fused ? ctx->d_dotp : nullptr);
   if (s) return s;
-  LAUNCH(launch_dot_partial(ctx->pv, ctx->q, n, ctx->own, ctx->partials, done, st, &nl_));
-  LAUNCH(launch_reduce2(ctx->partials, ctx->scal, SCAL_RED0, 1, done, st, &nl_));
+  if (fused) {
+    LAUNCH(launch_sum_ordered(ctx->d_dotp, ctx->col_ntx * ctx->col_nty, ctx->scal, SCAL_RED0, done, st, &nl_));
+  } else {
+    LAUNCH(launch_dot_partial(ctx->pv, ctx->q, n, ctx->own, ctx->partials, done, st, &nl_));
+    LAUNCH(launch_reduce2(ctx->partials, ctx->scal, SCAL_RED0, 1, done, st, &nl_));
+  }
   if ((s = allreduce_scal(ctx, SCAL_RED0, 1, st))) return s;
   LAUNCH(launch_pcg_alpha(ctx->scal, st, &nl_));
   LAUNCH(launch_pcg_update(x, ctx->r, ctx->pv, ctx->q, ctx->pinv, n, ctx->own, ctx->scal, ctx->partials, st, &nl_));

@@ -60,6 +60,7 @@ struct ColParams {
   double* corner;        // [(nty+1)][(ntx+1)][nz+1][3][NI+1]
   double* pending;       // [nitems][2][PEND]
   int ntx, nty, nitems;
+  double* dotp;          // optional: per-tile partial sums of x . y over final entries [nitems]
   ColCoef cf;
 };
 
@@ -89,8 +90,8 @@ struct CS {
   static constexpr int R_YE = R_XE + 2 * (TY + 1) * TX * 2;        // y-edges: [2][TY][TX+1][2]
   static constexpr int RED = R_YE + 2 * TY * (TX + 1) * 2;
   static constexpr int O_IS = 0;                     // 2 side input buffers
-  static constexpr int O_IP = O_IS + 2 * SIDE;       // 2 plane input buffers
-  static constexpr int O_AS = O_IP + 2 * PLANE;      // side accumulator
+  static constexpr int O_IP = O_IS + 2 * SIDE;       // 3 plane input buffers (plane q in q % 3)
+  static constexpr int O_AS = O_IP + 3 * PLANE;      // side accumulator
   static constexpr int O_AP = O_AS + SIDE;           // 2 plane accumulators
   static constexpr int O_RQ = O_AP + 2 * PLANE;      // reduction buffers
   static constexpr int O_TAB = O_RQ + RED;           // a0, lam (2 x 32)
@@ -225,7 +226,7 @@ struct RowIO {
   long long g, gs;
   int s, len, zlo, zhi;
   short a, b, pw, pm;
-  unsigned char mw, mm, me, pad;
+  unsigned char mw, mm, me, pub;   // pub: bit 1 middle, bit 2 E end are published partials (not final)
 };
 
 template <int NI>
@@ -240,7 +241,7 @@ __device__ void build_rows(const ColParams& P, RowIO* io, int x0, int y0, int tw
   const int r = threadIdx.x;
   if (r >= ns + np) return;
   RowIO d;
-  d.a = 0; d.pw = 0; d.pm = 0; d.mw = M_SKIP; d.me = M_SKIP; d.pad = 0;
+  d.a = 0; d.pw = 0; d.pm = 0; d.mw = M_SKIP; d.me = M_SKIP; d.pub = 0;
   if (r < th) {                                            // x-faces row r
     d.g = g.off_f[0] + ((long long)x0 + (long long)(nx + 1) * (y0 + r)) * N2;
     d.gs = (long long)(nx + 1) * ny * N2;
@@ -248,6 +249,7 @@ __device__ void build_rows(const ColParams& P, RowIO* io, int x0, int y0, int tw
     d.zlo = hasW ? 0 : N2; d.zhi = hasE ? d.len : tw * N2;
     d.a = N2; d.b = tw * N2;
     d.mw = hasW ? M_PARK : M_ZERO; d.pw = C::PD_XF + r * N2; d.mm = M_Y; d.me = hasE ? M_Y : M_ZERO;
+    d.pub = hasE ? 4 : 0;
   } else if (r < 2 * th + 1) {                             // y-faces row q
     const int q = r - th, fy = y0 + q;
     const bool z = fy == 0 || fy == ny;
@@ -257,6 +259,7 @@ __device__ void build_rows(const ColParams& P, RowIO* io, int x0, int y0, int tw
     d.zlo = z ? d.len : 0; d.zhi = d.len;
     d.b = d.len;
     d.mm = z ? M_ZERO : ((q == 0 && hasS) ? M_PARK : M_Y); d.pm = C::PD_YF;
+    d.pub = (q == th && hasN) ? 2 : 0;
   } else if (r < ns) {                                     // z-edges row q
     const int q = r - 2 * th - 1, fy = y0 + q;
     const bool z = fy == 0 || fy == ny, nrow = q == th && hasN, srow = q == 0 && hasS;
@@ -268,6 +271,7 @@ __device__ void build_rows(const ColParams& P, RowIO* io, int x0, int y0, int tw
     d.mw = z ? M_ZERO : (nrow ? M_SKIP : (hasW ? M_PARK : M_ZERO)); d.pw = C::PD_ZEW + q * NI;
     d.mm = z ? M_ZERO : (srow ? M_PARK : M_Y); d.pm = C::PD_ZES - NI;
     d.me = (z || !hasE) ? M_ZERO : ((nrow || srow) ? M_SKIP : M_Y);
+    d.pub = (nrow ? 2 : 0) | (hasE ? 4 : 0);
   } else {
     const int u = r - ns;
     if (u < th) {                                          // z-faces row u
@@ -283,6 +287,7 @@ __device__ void build_rows(const ColParams& P, RowIO* io, int x0, int y0, int tw
       d.s = C::P_XE + q * TX * NI; d.len = tw * NI;
       d.zlo = z ? d.len : 0; d.zhi = d.len; d.b = d.len;
       d.mm = z ? M_ZERO : ((q == 0 && hasS) ? M_PARK : M_Y); d.pm = C::PD_XE;
+      d.pub = (q == th && hasN) ? 2 : 0;
     } else if (u < 3 * th + 1) {                           // y-edges row q
       const int q = u - 2 * th - 1;
       d.g = g.off_e[1] + ((long long)x0 + (long long)(nx + 1) * (y0 + q)) * NI;
@@ -291,6 +296,7 @@ __device__ void build_rows(const ColParams& P, RowIO* io, int x0, int y0, int tw
       d.zlo = hasW ? 0 : NI; d.zhi = hasE ? d.len : tw * NI;
       d.a = NI; d.b = tw * NI;
       d.mw = hasW ? M_PARK : M_ZERO; d.pw = C::PD_YE + q * NI; d.mm = M_Y; d.me = hasE ? M_Y : M_ZERO;
+      d.pub = hasE ? 4 : 0;
     } else {                                               // vertices row q
       const int q = u - 3 * th - 1, fy = y0 + q;
       const bool z = fy == 0 || fy == ny, nrow = q == th && hasN, srow = q == 0 && hasS;
@@ -302,6 +308,7 @@ __device__ void build_rows(const ColParams& P, RowIO* io, int x0, int y0, int tw
       d.mw = z ? M_ZERO : (nrow ? M_SKIP : (hasW ? M_PARK : M_ZERO)); d.pw = C::PD_VW + q;
       d.mm = z ? M_ZERO : (srow ? M_PARK : M_Y); d.pm = C::PD_VS - 1;
       d.me = (z || !hasE) ? M_ZERO : ((nrow || srow) ? M_SKIP : M_Y);
+      d.pub = (nrow ? 2 : 0) | (hasE ? 4 : 0);
     }
   }
   io[r] = d;
@@ -369,28 +376,53 @@ __device__ __forceinline__ void seg_mode(double* yo, double* pk, const double* s
   else if (mode == M_ZERO) seg_out(yo, s, a, b, SEG_ZERO, lane);
   else if (mode == M_PARK) seg_out(pk, s, a, b, SEG_COPY, lane);
 }
+// Final entries: copy to y and accumulate x . y (x = the operator's input, same row layout).
+__device__ __forceinline__ double seg_final(double* __restrict__ dst, const double* __restrict__ s,
+                                            const double* __restrict__ xs, int a, int b, int lane) {
+  double acc = 0.0;
+  int t = a + lane;
+  for (; t + 96 < b; t += 128) {
+    const double v0 = s[t], v1 = s[t + 32], v2 = s[t + 64], v3 = s[t + 96];
+    const double u0 = xs[t], u1 = xs[t + 32], u2 = xs[t + 64], u3 = xs[t + 96];
+    dst[t] = v0; dst[t + 32] = v1; dst[t + 64] = v2; dst[t + 96] = v3;
+    acc = fma(v0, u0, acc); acc = fma(v1, u1, acc); acc = fma(v2, u2, acc); acc = fma(v3, u3, acc);
+  }
+  for (; t < b; t += 32) {
+    const double v = s[t];
+    dst[t] = v;
+    acc = fma(v, xs[t], acc);
+  }
+  return acc;
+}
 
+// Finalize of layer l (side rows, when side == true) and plane l (plane rows): accumulators
+// ac / acb, the operator's input of the same layer / plane in xin / xinb (for x . y).
 template <int NI>
 __device__ void finalize_step(const ColParams& P, long long item, int l, int x0, int y0, int tw, int th,
-                              const Side<NI>& ac, const Plane<NI>& acb, const RowIO* io, int ns) {
+                              const Side<NI>& ac, const Plane<NI>& acb, const Side<NI>& xin, const Plane<NI>& xinb,
+                              const RowIO* io, int ns, bool side_rows, double& dot) {
   using C = CS<NI>;
   constexpr int NW = C::NT / 32, TX = C::TX, TY = C::TY;
   const Geom& g = P.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool last = (l == g.nz), pzd = zdir(g, l);
+  const bool last = !side_rows, pzd = zdir(g, l);
   const int x1 = x0 + tw, y1 = y0 + th;
   const bool hasE = x1 < g.nx, hasN = y1 < g.ny, hasW = x0 > 0, hasS = y0 > 0;
   double* const pd = P.pending + (item * 3 + l % 3) * (long long)C::PEND;
+  const bool want_dot = P.dotp != nullptr;
   const int nr = ns + 4 * th + 2;
   for (int r = (last ? ns : 0) + warp; r < nr; r += NW) {
     const RowIO& d = io[r];
     const bool side = r < ns;
     const double* s = (side ? ac.b : acb.b) + d.s;
+    const double* xs = (side ? xin.b : xinb.b) + d.s;
     double* yo = P.y + d.g + (long long)l * d.gs;
     if (!side && pzd) { seg_out(yo, s, 0, d.len, SEG_ZERO, lane); continue; }
     seg_mode(yo, pd + d.pw, s, 0, d.a, d.mw, lane);
-    seg_mode(yo, pd + d.pm, s, d.a, d.b, d.mm, lane);
-    seg_mode(yo, pd, s, d.b, d.len, d.me, lane);
+    if (want_dot && d.mm == M_Y && !(d.pub & 2)) dot += seg_final(yo, s, xs, d.a, d.b, lane);
+    else seg_mode(yo, pd + d.pm, s, d.a, d.b, d.mm, lane);
+    if (want_dot && d.me == M_Y && !(d.pub & 4)) dot += seg_final(yo, s, xs, d.b, d.len, lane);
+    else seg_mode(yo, pd, s, d.b, d.len, d.me, lane);
   }
   // corner pass: the three 4-tile corner lines this tile contributes to but does not own
   // (NE -> slot 0 of the NE tile's SW corner, NW -> slot 1, SE -> slot 2); z-edges (c < NI)
@@ -420,7 +452,7 @@ __device__ void finalize_step(const ColParams& P, long long item, int l, int x0,
 template <int NI>
 __device__ void finish_boundary(const ColParams& P, long long item, int ls, int x0, int y0, int tw, int th,
                                 const int* flag_w, const int* flag_s, const int* flag_sw, int epoch,
-                                long long* sRow, const RowIO* io) {
+                                long long* sRow, const RowIO* io, double& dot) {
   using C = CS<NI>;
   constexpr int N2 = C::N2, NT = C::NT, TX = C::TX, TY = C::TY;
   constexpr int MAXE = (C::PEND + NT - 1) / NT;
@@ -516,9 +548,15 @@ __device__ void finish_boundary(const ColParams& P, long long item, int ls, int 
     val[k] = v;
     dst[k] = d;
   }
+  double xv[MAXE];
+#pragma unroll
+  for (int k = 0; k < MAXE; ++k) xv[k] = (dst[k] && P.dotp) ? ld_cg(P.x + (dst[k] - P.y)) : 0.0;
 #pragma unroll
   for (int k = 0; k < MAXE; ++k)
-    if (dst[k]) *dst[k] = val[k];
+    if (dst[k]) {
+      *dst[k] = val[k];
+      dot = fma(val[k], xv[k], dot);
+    }
 }
 
 // ---- condensed part of one parity class (s_i, s_j, s_k) = (SI, SJ, SK) ---------------------
@@ -997,15 +1035,20 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
     load_rows(P.x, sIO, ns, nrw, sm + C::O_IP + C::PLANE, 1, zdir(g, 1));
     cp_commit();
     for (int t = tid; t < C::PLANE; t += NT) sm[C::O_AP + t] = 0.0;
+    double dot = 0.0;
 
+    // Step l computes element layer l (l < nz) and finalizes layer l / plane l.  Inputs: side l
+    // in buffer l & 1, plane q in q % 3 (so plane l+2 is prefetched at the top of step l into
+    // the buffer of plane l-1); accumulators: side (one buffer), plane q in q & 1.
     for (int l = 0; l <= g.nz; ++l) {
       const bool last = (l == g.nz);         // final step: only plane nz remains
       const Side<NI> in{sm + C::O_IS + (l & 1) * C::SIDE};
-      const Plane<NI> inb{sm + C::O_IP + (l & 1) * C::PLANE}, intp{sm + C::O_IP + ((l + 1) & 1) * C::PLANE};
+      const Plane<NI> inb{sm + C::O_IP + (l % 3) * C::PLANE}, intp{sm + C::O_IP + ((l + 1) % 3) * C::PLANE};
       const Plane<NI> acb{sm + C::O_AP + (l & 1) * C::PLANE}, actp{sm + C::O_AP + ((l + 1) & 1) * C::PLANE};
-      // early prefetch: side l+1 (overlaps this step's compute)
+      // prefetch side l+1 and plane l+2 (overlap this step's compute); wait for side l, plane l+1
 #if !(defined(SC_EXP) && SC_EXP == 25)
       if (l + 1 < g.nz) load_rows(P.x, sIO, 0, ns, sm + C::O_IS + ((l + 1) & 1) * C::SIDE, l + 1, false);
+      if (l + 2 <= g.nz) load_rows(P.x, sIO, ns, nrw, sm + C::O_IP + ((l + 2) % 3) * C::PLANE, l + 2, zdir(g, l + 2));
 #endif
       cp_commit();
       cp_wait<1>();
@@ -1159,29 +1202,22 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
         __syncthreads();
         SC_PHASE(6);
       }
-      // publication of step l-1 (deferred look-back, distance 2): its stores were issued before
-      // the CTA barrier that ended step l-1 and have drained during this step's compute, so
-      // thread 0's GPU-scope fence (cumulative over that barrier) is cheap here.
+      // publication of step l-1 (look-back distance 2): its stores were issued before the CTA
+      // barrier that ended step l-1 and have drained during this step's compute
       if (tid == 0 && l >= 1) {
 #if !(defined(SC_EXP) && SC_EXP == 26)
         __threadfence();
 #endif
         flag_release(flag_me + (l - 1), epoch);
       }
-      // late prefetch: plane l+2 into the buffer of plane l (no longer read)
-#if !(defined(SC_EXP) && SC_EXP == 25)
-      if (l + 2 <= g.nz) load_rows(P.x, sIO, ns, nrw, sm + C::O_IP + (l & 1) * C::PLANE, l + 2, zdir(g, l + 2));
-#endif
-      cp_commit();
 #if !(defined(SC_EXP) && SC_EXP == 23)
-      finalize_step<NI>(P, item, l, x0, y0, tw, th, ac, acb, sIO, ns);
+      finalize_step<NI>(P, item, l, x0, y0, tw, th, ac, acb, in, inb, sIO, ns, !last, dot);
 #endif
       __syncthreads();
       SC_PHASE(7);
-      // finish the W / S boundary entities of step l-2 (their owners' partials were published
-      // during step l-1 of the W / S / SW tiles)
+      // finish the W / S boundary entities of step l-2
 #if !(defined(SC_EXP) && SC_EXP == 24)
-      if (l >= 2) finish_boundary<NI>(P, item, l - 2, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO);
+      if (l >= 2) finish_boundary<NI>(P, item, l - 2, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO, dot);
 #endif
       __syncthreads();
       SC_PHASE(8);
@@ -1191,9 +1227,22 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
       __threadfence();
       flag_release(flag_me + g.nz, epoch);
     }
-    if (g.nz >= 1) finish_boundary<NI>(P, item, g.nz - 1, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO);
+    if (g.nz >= 1) finish_boundary<NI>(P, item, g.nz - 1, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO, dot);
     __syncthreads();
-    finish_boundary<NI>(P, item, g.nz, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO);
+    finish_boundary<NI>(P, item, g.nz, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO, dot);
+    // per-tile partial of x . y (fixed order: deterministic)
+    if (P.dotp) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      __syncthreads();
+      if (lane == 0) sRow[warp] = __double_as_longlong(dot);
+      __syncthreads();
+      if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < NW; ++w) t += __longlong_as_double(sRow[w]);
+        P.dotp[item] = t;
+      }
+    }
     __syncthreads();
   }
   if (tid == 0) {
@@ -1292,12 +1341,13 @@ int launch_apply_col(const ColParams& P, void* stream, int* nl, int* grid_out, v
 }
 
 int launch_apply_col_raw(const Geom& g, const double* x, double* y, const double* done, void* state, int* flags,
-                         double* corner, double* pending, int ntx, int nty, const void* coef, void* stream, int* nl,
-                         void* events) {
+                         double* corner, double* pending, int ntx, int nty, const void* coef, double* dotp,
+                         void* stream, int* nl, void* events) {
   ColParams P;
   P.g = g; P.x = x; P.y = y; P.done = done; P.st = (ColState*)state; P.flags = flags; P.corner = corner;
   P.pending = pending;
   P.ntx = ntx; P.nty = nty; P.nitems = ntx * nty;
+  P.dotp = dotp;
   memcpy(&P.cf, coef, sizeof(ColCoef));
   int grid = 0;
   return launch_apply_col(P, stream, nl, &grid, events);

@@ -113,6 +113,17 @@ __global__ void k_reduce2(const double* __restrict__ partials, double* __restric
   }
 }
 
+// Fixed-order sum of n values (one block): thread t sums v[t], v[t + nt], ... in order, then a
+// fixed-shape block reduction.  Used for the per-tile x . y partials of the operator.
+__global__ void k_sum_ordered(const double* __restrict__ v, int n, double* __restrict__ scal, int slot,
+                              const double* __restrict__ done) {
+  if (done != nullptr && *done != 0.0) return;
+  double a[1] = {0.0};
+  for (int i = threadIdx.x; i < n; i += blockDim.x) a[0] += v[i];
+  block_sum<1>(a);
+  if (threadIdx.x == 0) scal[slot] = a[0];
+}
+
 __global__ void k_pcg_init_finalize(double* scal, double tol2, int maxit) {
   double rz = scal[SCAL_RED0], rr = scal[SCAL_RED1];
   scal[SCAL_RZ] = rz;
@@ -156,6 +167,12 @@ int launch_dot_partial(const double* a, const double* b, long long n, OwnMask m,
 int launch_reduce2(const double* partials, double* scal, int slot0, int nvals, const double* done, void* stream,
                    int* nl) {
   k_reduce2<<<1, VEC_THREADS, 0, (cudaStream_t)stream>>>(partials, scal, slot0, nvals, done);
+  (*nl)++;
+  return cudaGetLastError();
+}
+
+int launch_sum_ordered(const double* v, int n, double* scal, int slot, const double* done, void* stream, int* nl) {
+  k_sum_ordered<<<1, VEC_THREADS, 0, (cudaStream_t)stream>>>(v, n, scal, slot, done);
   (*nl)++;
   return cudaGetLastError();
 }

@@ -241,6 +241,27 @@ def test_pcg_parity_random_rhs_nonuniform():
     assert rel(ctx.to_lattice_nodal(xt).cpu().numpy(), ref) <= 1e-10
 
 
+@pytest.mark.parametrize("p,ne", [(3, (17, 9, 3)), (8, (10, 6, 3))])
+def test_pcg_parity_multitile(p, ne):
+    """BT-PCG on a uniform grid spanning several 8 x 4 tiles in x and y: exercises the
+    tile-column operator with the look-back and its fused p . q partials (single GPU)."""
+    from paper_1601_08179_b200 import SC_DUAL
+    g = small_grid(p, ne, 1.0, lengths=(1.3, 0.7, 0.5))
+    op = operator.AssembledCondensedOperator(g)
+    ctx = ctx_for(g)
+    bt = ctx.skeleton()
+    ctx.sc_fill_random(8, bt)
+    lat = ctx.lattice()
+    ctx.sc_from_transformed(bt, lat, SC_DUAL)
+    b = lat.cpu().numpy()
+    res = _oracle_pcg(g, op, b, 1e-10)
+    xt = ctx.skeleton()
+    rep = ctx.sc_pcg_solve(bt, xt, rtol=1e-10, maxit=2000)
+    assert rep.converged and abs(rep.iters - res.iters) <= 1
+    ref = res.x if rep.iters == res.iters else _oracle_pcg(g, op, b, 0, fixed=rep.iters).x
+    assert rel(ctx.to_lattice_nodal(xt).cpu().numpy(), ref) <= 1e-10
+
+
 def test_pcg_fixed_iterations_and_zero_rhs():
     g = small_grid(3, (2, 2, 2), 1.0)
     ctx = ctx_for(g)
