@@ -241,11 +241,14 @@ def test_pcg_parity_random_rhs_nonuniform():
     assert rel(ctx.to_lattice_nodal(xt).cpu().numpy(), ref) <= 1e-10
 
 
-@pytest.mark.parametrize("p,ne", [(3, (17, 9, 3)), (8, (10, 6, 3))])
-def test_pcg_parity_multitile(p, ne):
+@pytest.mark.parametrize("p,ne,fused", [(3, (17, 9, 3), "0"), (8, (10, 6, 3), "0"), (3, (17, 9, 3), "1"),
+                                        (8, (10, 6, 3), "1")])
+def test_pcg_parity_multitile(p, ne, fused, monkeypatch):
     """BT-PCG on a uniform grid spanning several 8 x 4 tiles in x and y: exercises the
-    tile-column operator with the look-back and its fused p . q partials (single GPU)."""
+    tile-column operator with the look-back, with the separate p . q dot kernel and with the
+    p . q partials fused into the operator (SC_FUSED_DOT=1, single GPU)."""
     from paper_1601_08179_b200 import SC_DUAL
+    monkeypatch.setenv("SC_FUSED_DOT", fused)
     g = small_grid(p, ne, 1.0, lengths=(1.3, 0.7, 0.5))
     op = operator.AssembledCondensedOperator(g)
     ctx = ctx_for(g)
