@@ -89,6 +89,7 @@ struct sc_ctx {
   ncclComm_t comm = nullptr;
   long long nlaunch = 0;
   double* x_cur = nullptr;              // PCG iterate between sc_pcg_start / sc_pcg_iterate
+  long long it_enq = 0;                 // iterations enqueued since sc_pcg_start (direction kernel guard)
   double tol2 = -1.0;
   bool prof_on = false;
   std::vector<cudaEvent_t> prof_ev;     // pairs (start, stop)
@@ -497,6 +498,7 @@ static sc_status pcg_start_impl(sc_ctx* ctx, const double* b, double* x, double 
   const long long n = ctx->g.n_total;
   ctx->tol2 = rtol > 0 ? rtol * rtol : -1.0;
   ctx->x_cur = x;
+  ctx->it_enq = 0;
   LAUNCH(launch_pcg_init(b, ctx->pinv, x, ctx->r, ctx->pv, n, ctx->own, ctx->partials, st, &nl_));
   LAUNCH(launch_reduce2(ctx->partials, ctx->scal, SCAL_RED0, 2, nullptr, st, &nl_));
   sc_status s = allreduce_scal(ctx, SCAL_RED0, 2, st);
@@ -525,11 +527,12 @@ static sc_status pcg_iteration(sc_ctx* ctx, cudaStream_t st) {
   }
   if ((s = allreduce_scal(ctx, SCAL_RED0, 1, st))) return s;
   LAUNCH(launch_pcg_alpha(ctx->scal, st, &nl_));
-  LAUNCH(launch_pcg_update(x, ctx->r, ctx->pv, ctx->q, ctx->pinv, n, ctx->own, ctx->scal, ctx->partials, st, &nl_));
+  LAUNCH(launch_pcg_update(ctx->r, ctx->q, ctx->pinv, n, ctx->own, ctx->scal, ctx->partials, st, &nl_));
   LAUNCH(launch_reduce2(ctx->partials, ctx->scal, SCAL_RED0, 2, done, st, &nl_));
   if ((s = allreduce_scal(ctx, SCAL_RED0, 2, st))) return s;
   LAUNCH(launch_pcg_beta(ctx->scal, st, &nl_));
-  LAUNCH(launch_pcg_direction(ctx->pv, ctx->r, ctx->pinv, n, ctx->scal, st, &nl_));
+  LAUNCH(launch_pcg_direction(x, ctx->pv, ctx->r, ctx->pinv, n, ctx->scal, ctx->it_enq, st, &nl_));
+  ctx->it_enq++;
   return SC_OK;
 }
 

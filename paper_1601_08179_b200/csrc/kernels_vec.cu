@@ -73,17 +73,15 @@ __global__ void k_pcg_init(const double* __restrict__ b, const double* __restric
   if (threadIdx.x == 0) { partials[blockIdx.x] = v[0]; partials[SC_RED_BLOCKS + blockIdx.x] = v[1]; }
 }
 
-// x += alpha p ; r -= alpha q ; z = Pinv r ; partials [r.z | r.r]
-__global__ void k_pcg_update(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
-                             const double* __restrict__ q, const double* __restrict__ pinv, long long n, OwnMask m,
-                             const double* __restrict__ scal, double* __restrict__ partials) {
+// r -= alpha q ; z = Pinv r ; partials [r.z | r.r]   (4 streams: r, q, Pinv read; r written)
+__global__ void k_pcg_update(double* __restrict__ r, const double* __restrict__ q, const double* __restrict__ pinv,
+                             long long n, OwnMask m, const double* __restrict__ scal, double* __restrict__ partials) {
   if (scal[SCAL_DONE] != 0.0) return;
   const double alpha = scal[SCAL_ALPHA];
   double v[2] = {0.0, 0.0};
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    double xi = x[i] + alpha * p[i];
     double ri = r[i] - alpha * q[i];
-    x[i] = xi; r[i] = ri;
+    r[i] = ri;
     double zi = pinv[i] * ri;
     if (owned(i, m)) { v[0] += ri * zi; v[1] += ri * ri; }
   }
@@ -91,13 +89,22 @@ __global__ void k_pcg_update(double* __restrict__ x, double* __restrict__ r, con
   if (threadIdx.x == 0) { partials[blockIdx.x] = v[0]; partials[SC_RED_BLOCKS + blockIdx.x] = v[1]; }
 }
 
-// p = Pinv r + beta p
-__global__ void k_pcg_direction(double* __restrict__ p, const double* __restrict__ r, const double* __restrict__ pinv,
-                                long long n, const double* __restrict__ scal) {
-  if (scal[SCAL_DONE] != 0.0) return;
-  const double beta = scal[SCAL_BETA];
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    p[i] = pinv[i] * r[i] + beta * p[i];
+// x += alpha p (the x update of this iteration, moved here from the update kernel so that p is
+// streamed once) ; p = Pinv r + beta p unless converged   (6 streams: x, p, r, Pinv read; x, p
+// written).  `it` is the host's 0-based index of this iteration: the kernel acts only if this
+// iteration's alpha kernel ran (iteration count == it + 1), so iterations enqueued after
+// convergence change nothing.
+__global__ void k_pcg_direction(double* __restrict__ x, double* __restrict__ p, const double* __restrict__ r,
+                                const double* __restrict__ pinv, long long n, const double* __restrict__ scal,
+                                long long it) {
+  if (scal[SCAL_ITERS] != (double)(it + 1) || scal[SCAL_BREAK] != 0.0) return;
+  const double alpha = scal[SCAL_ALPHA], beta = scal[SCAL_BETA];
+  const bool dir = scal[SCAL_DONE] == 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double pi = p[i];
+    x[i] += alpha * pi;
+    if (dir) p[i] = pinv[i] * r[i] + beta * pi;
+  }
 }
 
 // Fixed-order second stage: scal[slot0 + v] = sum_b partials[v * SC_RED_BLOCKS + b].
@@ -197,9 +204,9 @@ int launch_pcg_alpha(double* scal, void* stream, int* nl) {
   return cudaGetLastError();
 }
 
-int launch_pcg_update(double* x, double* r, const double* p, const double* q, const double* pinv, long long n,
-                      OwnMask m, const double* scal, double* partials, void* stream, int* nl) {
-  k_pcg_update<<<SC_RED_BLOCKS, VEC_THREADS, 0, (cudaStream_t)stream>>>(x, r, p, q, pinv, n, m, scal, partials);
+int launch_pcg_update(double* r, const double* q, const double* pinv, long long n, OwnMask m, const double* scal,
+                      double* partials, void* stream, int* nl) {
+  k_pcg_update<<<SC_RED_BLOCKS, VEC_THREADS, 0, (cudaStream_t)stream>>>(r, q, pinv, n, m, scal, partials);
   (*nl)++;
   return cudaGetLastError();
 }
@@ -210,9 +217,9 @@ int launch_pcg_beta(double* scal, void* stream, int* nl) {
   return cudaGetLastError();
 }
 
-int launch_pcg_direction(double* p, const double* r, const double* pinv, long long n, const double* scal,
-                         void* stream, int* nl) {
-  k_pcg_direction<<<SC_RED_BLOCKS, VEC_THREADS, 0, (cudaStream_t)stream>>>(p, r, pinv, n, scal);
+int launch_pcg_direction(double* x, double* p, const double* r, const double* pinv, long long n, const double* scal,
+                         long long it, void* stream, int* nl) {
+  k_pcg_direction<<<SC_RED_BLOCKS, VEC_THREADS, 0, (cudaStream_t)stream>>>(x, p, r, pinv, n, scal, it);
   (*nl)++;
   return cudaGetLastError();
 }

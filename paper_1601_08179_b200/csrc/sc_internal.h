@@ -89,11 +89,11 @@ int launch_pcg_init(const double* b, const double* pinv, double* x, double* r, d
                     OwnMask m, double* partials, void* stream, int* nlaunch);
 int launch_pcg_init_finalize(double* scal, const double* partials, double tol2, int maxit, void* stream, int* nlaunch);
 int launch_pcg_alpha(double* scal, void* stream, int* nlaunch);
-int launch_pcg_update(double* x, double* r, const double* p, const double* q, const double* pinv,
-                      long long n, OwnMask m, const double* scal, double* partials, void* stream, int* nlaunch);
+int launch_pcg_update(double* r, const double* q, const double* pinv, long long n, OwnMask m, const double* scal,
+                      double* partials, void* stream, int* nlaunch);
 int launch_pcg_beta(double* scal, void* stream, int* nlaunch);
-int launch_pcg_direction(double* p, const double* r, const double* pinv, long long n, const double* scal,
-                         void* stream, int* nlaunch);
+int launch_pcg_direction(double* x, double* p, const double* r, const double* pinv, long long n, const double* scal,
+                         long long it, void* stream, int* nlaunch);
 int launch_reduce2(const double* partials, double* scal, int slot0, int nvals, const double* done,
                    void* stream, int* nlaunch);
 
