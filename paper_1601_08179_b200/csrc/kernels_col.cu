@@ -68,7 +68,11 @@ template <int NI>
 struct CS {
   static constexpr int N2 = NI * NI;
   static constexpr int NT = 256;                      // 8 warps = 8 parity classes
-  static constexpr int TX = 8, TY = 4, NE = TX * TY;  // one element per lane
+  // tile: 8 x 4 elements (one per lane, a parity class per warp) for n_I >= 4; for n_I <= 3
+  // one element per thread (all classes in the thread) on larger tiles
+  static constexpr bool PER_ELEM = NI <= 3;
+  static constexpr int TX = NI <= 2 ? 16 : 8, TY = NI == 1 ? 16 : (NI <= 3 ? 8 : 4), NE = TX * TY;
+  static constexpr int MAXROWS = 7 * TY + 4;          // row descriptors per tile
   static constexpr int XF = TY * (TX + 1) * N2;
   static constexpr int YF = (TY + 1) * TX * N2;
   static constexpr int ZE = (TY + 1) * (TX + 1) * NI;
@@ -238,8 +242,7 @@ __device__ void build_rows(const ColParams& P, RowIO* io, int x0, int y0, int tw
   const bool hasW = x0 > 0, hasE = x0 + tw < nx, hasS = y0 > 0, hasN = y0 + th < ny;
   const int ns = 3 * th + 2, np = 4 * th + 2;
   *ns_out = ns;
-  const int r = threadIdx.x;
-  if (r >= ns + np) return;
+  for (int r = threadIdx.x; r < ns + np; r += CS<NI>::NT) {
   RowIO d;
   d.a = 0; d.pw = 0; d.pm = 0; d.mw = M_SKIP; d.me = M_SKIP; d.pub = 0;
   if (r < th) {                                            // x-faces row r
@@ -312,6 +315,7 @@ __device__ void build_rows(const ColParams& P, RowIO* io, int x0, int y0, int tw
     }
   }
   io[r] = d;
+  }
 }
 
 // Rows [r0, r1) of the descriptor table into the block at `base` for layer / plane l (one warp
@@ -323,6 +327,53 @@ __device__ __forceinline__ void load_rows(const double* x, const RowIO* io, int 
     const RowIO& d = io[r];
     const int len = d.len;
     row_load(base + d.s, x + d.g + (long long)l * d.gs, len, zero_all ? len : d.zlo, d.zhi, lane);
+  }
+}
+
+// Flat view of a side / plane block for the small-n_I tiles (short rows: one warp per row
+// leaves most lanes idle): block entry t -> descriptor row and column (compile-time strides),
+// -1 for padding rows.  The shared-memory position of an entry is the block base + t.
+template <int NI>
+__device__ __forceinline__ int flat_row(int t, bool plane, int th, int ns, int& col) {
+  using C = CS<NI>;
+  constexpr int N2 = C::N2, TX = C::TX;
+  int q;
+  if (!plane) {
+    if (t < C::XF) { q = t / ((TX + 1) * N2); col = t - q * ((TX + 1) * N2); return q < th ? q : -1; }
+    t -= C::XF;
+    if (t < C::YF) { q = t / (TX * N2); col = t - q * (TX * N2); return q <= th ? th + q : -1; }
+    t -= C::YF;
+    q = t / ((TX + 1) * NI); col = t - q * ((TX + 1) * NI); return q <= th ? 2 * th + 1 + q : -1;
+  }
+  if (t < C::PZF) { q = t / (TX * N2); col = t - q * (TX * N2); return q < th ? ns + q : -1; }
+  t -= C::PZF;
+  if (t < C::PXE) { q = t / (TX * NI); col = t - q * (TX * NI); return q <= th ? ns + th + q : -1; }
+  t -= C::PXE;
+  if (t < C::PYE) { q = t / ((TX + 1) * NI); col = t - q * ((TX + 1) * NI); return q < th ? ns + 2 * th + 1 + q : -1; }
+  t -= C::PYE;
+  q = t / (TX + 1); col = t - q * (TX + 1); return q <= th ? ns + 3 * th + 1 + q : -1;
+}
+
+// Side (plane == false) or plane block of layer / plane l into `base`: rows [0, ns) or
+// [ns, ns + 4 th + 2) of the descriptor table; zero_all: a Dirichlet z-plane.
+template <int NI>
+__device__ __forceinline__ void load_block(const double* x, const RowIO* io, bool plane, int ns, int th, double* base,
+                                           int l, bool zero_all) {
+  using C = CS<NI>;
+  if constexpr (C::PER_ELEM) {
+    const int nb = plane ? C::PLANE : C::SIDE;
+    for (int t = threadIdx.x; t < nb; t += C::NT) {
+      int col;
+      const int r = flat_row<NI>(t, plane, th, ns, col);
+      if (r < 0) continue;
+      const RowIO& d = io[r];
+      if (col >= d.len) continue;
+      if (zero_all || col < d.zlo || col >= d.zhi) base[t] = 0.0;
+      else cp_async8(base + t, x + d.g + (long long)l * d.gs + col);
+    }
+  } else {
+    if (plane) load_rows(x, io, ns, ns + 4 * th + 2, base, l, zero_all);
+    else load_rows(x, io, 0, ns, base, l, zero_all);
   }
 }
 
@@ -411,6 +462,47 @@ __device__ void finalize_step(const ColParams& P, long long item, int l, int x0,
   double* const pd = P.pending + (item * 3 + l % 3) * (long long)C::PEND;
   const bool want_dot = P.dotp != nullptr;
   const int nr = ns + 4 * th + 2;
+  if constexpr (C::PER_ELEM) {
+    // flat: every thread takes block entries t, t + NT, ... (side block, then plane block);
+    // all values are read before any store
+    constexpr int NF = (C::SIDE + C::PLANE + C::NT - 1) / C::NT;
+    double val[NF], xv[NF];
+    double* dst[NF];
+#pragma unroll
+    for (int k = 0; k < NF; ++k) {
+      dst[k] = nullptr;
+      val[k] = xv[k] = 0.0;
+      const int t = (last ? C::SIDE : 0) + (int)threadIdx.x + k * C::NT;
+      if (t >= C::SIDE + C::PLANE) continue;
+      const bool side = t < C::SIDE;
+      const int tb = side ? t : t - C::SIDE;
+      int col;
+      const int r = flat_row<NI>(tb, !side, th, ns, col);
+      if (r < 0) continue;
+      const RowIO& d = io[r];
+      if (col >= d.len) continue;
+      double* yo = P.y + d.g + (long long)l * d.gs + col;
+      const double s = (side ? ac.b : acb.b)[tb];
+      if (!side && pzd) { dst[k] = yo; continue; }
+      int mode, bit, po;
+      if (col < d.a) { mode = d.mw; bit = 0; po = d.pw; }
+      else if (col < d.b) { mode = d.mm; bit = 2; po = d.pm; }
+      else { mode = d.me; bit = 4; po = 0; }
+      if (mode == M_SKIP) continue;
+      if (mode == M_PARK) { dst[k] = pd + po + col; val[k] = s; continue; }
+      dst[k] = yo;
+      if (mode == M_Y) {
+        val[k] = s;
+        if (want_dot && bit && !(d.pub & bit)) xv[k] = (side ? xin.b : xinb.b)[tb];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NF; ++k)
+      if (dst[k]) {
+        *dst[k] = val[k];
+        dot = fma(val[k], xv[k], dot);
+      }
+  } else
   for (int r = (last ? ns : 0) + warp; r < nr; r += NW) {
     const RowIO& d = io[r];
     const bool side = r < ns;
@@ -956,6 +1048,164 @@ __device__ __forceinline__ void vol_class(const int cls, const ColCoef* cf, cons
   }
 }
 
+// ---- n_I <= 3: one element per thread, all parity classes in the thread --------------------
+// Same arithmetic as the class warps (faces-in, D^{-1}, faces-out of Table 2; primary part of
+// the faces, Eq. 26 generalised; a0-weighted face line sums for the edge / vertex rows), in the
+// plain (not even / odd) form.  Order: line sums of the input faces, condensed part (Q of the six
+// faces in registers), then per direction primary - Q and the stores (the faces are re-read from
+// shared memory, which keeps the register count down).  x-faces of a tile row are summed with a
+// lane shuffle (rows of TX consecutive threads in one warp), y-faces in two barrier-separated
+// rounds by element-row parity, z-faces as in the class version.
+template <int NI>
+__device__ __forceinline__ void vol_elem(const ColCoef* cf, const Side<NI>& in, const Plane<NI>& inb,
+                                         const Plane<NI>& intp, const Side<NI>& ac, const Plane<NI>& acb,
+                                         const Plane<NI>& actp, double* rq, int ix, int iy, int tw, int th) {
+  constexpr int N2 = NI * NI, TX = CS<NI>::TX, NE = CS<NI>::NE;
+  const bool act = (int)threadIdx.x < NE && ix < tw && iy < th;
+  const bool lastx = ix == tw - 1, lasty = iy == th - 1;
+  const int ex = min(ix, TX - 1), ey = min(iy, CS<NI>::TY - 1);
+  const double* W = in.xf(ey, ex);
+  const double* E = W + N2;
+  const double* S = in.yf(ey, ex);
+  const double* N = S + TX * N2;
+  const double* B = inb.zf(ey, ex);
+  const double* T = intp.zf(ey, ex);
+  // a0-weighted line sums (R+, R-) of the input faces, for the edge / vertex rows: x-face W (and
+  // E for the last element of the row), y-face S (and N), z-faces B and T
+  if (act) {
+    auto lsum = [&](const double* f, int stride_a, int stride_c, double* o) {
+#pragma unroll
+      for (int c = 0; c < NI; ++c) {
+        double rp = 0.0, rm = 0.0;
+#pragma unroll
+        for (int a = 0; a < NI; ++a) {
+          const double t = cf->a[a] * f[a * stride_a + c * stride_c];
+          if (a & 1) rm += t; else rp += t;
+        }
+        o[2 * c] = rp;
+        o[2 * c + 1] = rm;
+      }
+    };
+    double* xj = rq + CS<NI>::R_XJ + (iy * (TX + 1) + ix) * 2 * NI;
+    double* xk = rq + CS<NI>::R_XK + (iy * (TX + 1) + ix) * 2 * NI;
+    lsum(W, 1, NI, xj);        // over j, keep k
+    lsum(W, NI, 1, xk);        // over k, keep j
+    if (lastx) { lsum(E, 1, NI, xj + 2 * NI); lsum(E, NI, 1, xk + 2 * NI); }
+    double* yi = rq + CS<NI>::R_YI + (iy * TX + ix) * 2 * NI;
+    double* yk = rq + CS<NI>::R_YK + (iy * TX + ix) * 2 * NI;
+    lsum(S, 1, NI, yi);        // over i, keep k
+    lsum(S, NI, 1, yk);        // over k, keep i
+    if (lasty) { lsum(N, 1, NI, yi + TX * 2 * NI); lsum(N, NI, 1, yk + TX * 2 * NI); }
+    constexpr int PO = NE * 2 * NI;
+    double* zi = rq + CS<NI>::R_ZI + (iy * TX + ix) * 2 * NI;
+    double* zj = rq + CS<NI>::R_ZJ + (iy * TX + ix) * 2 * NI;
+    lsum(B, 1, NI, zi);        // over i, keep j
+    lsum(B, NI, 1, zj);        // over j, keep i
+    lsum(T, 1, NI, zi + PO);
+    lsum(T, NI, 1, zj + PO);
+  }
+  // condensed part: u = d1 (W + g_i E) + d2 (S + g_j N) + d3 (B + g_k T) (a0-weighted: c_d),
+  // v = u D^{-1}; Q_W += c1 v, Q_E += g_i c1 v, ...
+  double qw[N2], qe[N2], qs[N2], qn[N2], qb[N2], qt[N2];
+#pragma unroll
+  for (int q = 0; q < N2; ++q) qw[q] = qe[q] = qs[q] = qn[q] = qb[q] = qt[q] = 0.0;
+#pragma unroll
+  for (int k = 0; k < NI; ++k)
+#pragma unroll
+    for (int j = 0; j < NI; ++j)
+#pragma unroll
+      for (int i = 0; i < NI; ++i) {
+        const double gi = (i & 1) ? -1.0 : 1.0, gj = (j & 1) ? -1.0 : 1.0, gk = (k & 1) ? -1.0 : 1.0;
+        const int ox = j + NI * k, oy = i + NI * k, oz = i + NI * j;
+        const double u = fma(cf->c[0][i], fma(gi, E[ox], W[ox]),
+                             fma(cf->c[1][j], fma(gj, N[oy], S[oy]), cf->c[2][k] * fma(gk, T[oz], B[oz])));
+        const double v = u * cf->dinv[i + NI * (j + NI * k)];
+        const double vx = cf->c[0][i] * v, vy = cf->c[1][j] * v, vz = cf->c[2][k] * v;
+        qw[ox] += vx; qe[ox] = fma(gi, vx, qe[ox]);
+        qs[oy] += vy; qn[oy] = fma(gj, vy, qn[oy]);
+        qb[oz] += vz; qt[oz] = fma(gk, vz, qt[oz]);
+      }
+  const double* Z0 = in.ze(ey, ex);                    // z-edges at (fx, fy), (fx+1, fy)
+  const double* Z1 = in.ze(ey + 1, ex);                // z-edges at (fx, fy+1), (fx+1, fy+1)
+  const double* Yb = inb.ye(ey, ex);                   // y-edges of planes l, l+1 at fx, fx+1
+  const double* Yt = intp.ye(ey, ex);
+  const double* Xb = inb.xe(ey, ex);                   // x-edges of planes l, l+1 at fy, fy+1
+  const double* Xt = intp.xe(ey, ex);
+  // x-faces, entries (a, b) = (j, k): primary (self, opposite face, z-edges at k, y-edges at j)
+  // minus Q; face ix = W part of element ix + E part of element ix-1 (lane - 1)
+  {
+    double* fX = ac.xf(ey, ex);
+#pragma unroll
+    for (int b = 0; b < NI; ++b)
+#pragma unroll
+      for (int a = 0; a < NI; ++a) {
+        const int q = a + NI * b;
+        const double ga = (a & 1) ? -1.0 : 1.0, gb = (b & 1) ? -1.0 : 1.0;
+        const double w = W[q], e = E[q];
+        const double zw = fma(ga, Z1[b], Z0[b]), ze_ = fma(ga, Z1[NI + b], Z0[NI + b]);
+        const double yw = fma(gb, Yt[a], Yb[a]), ye_ = fma(gb, Yt[NI + a], Yb[NI + a]);
+        const double Wp = fma(cf->fd[0][q], w, fma(cf->k0p[0], e, fma(cf->e[1][a], zw, cf->e[2][b] * yw))) - qw[q];
+        const double Ep = fma(cf->fd[0][q], e, fma(cf->k0p[0], w, fma(cf->e[1][a], ze_, cf->e[2][b] * ye_))) - qe[q];
+        const double Em = __shfl_up_sync(0xffffffffu, Ep, 1);
+        if (act) {
+          fX[q] = ix > 0 ? Wp + Em : Wp;
+          if (lastx) fX[q + N2] = Ep;
+        }
+      }
+  }
+  // z-faces, entries (a, b) = (i, j): y-edges at j, x-edges at i; B of this layer (plane l,
+  // added), T (plane l+1, initialised)
+  if (act) {
+    double* fB = acb.zf(ey, ex);
+    double* fT = actp.zf(ey, ex);
+#pragma unroll
+    for (int b = 0; b < NI; ++b)
+#pragma unroll
+      for (int a = 0; a < NI; ++a) {
+        const int q = a + NI * b;
+        const double ga = (a & 1) ? -1.0 : 1.0, gb = (b & 1) ? -1.0 : 1.0;
+        const double bv = B[q], tv = T[q];
+        const double yb = fma(ga, Yb[NI + b], Yb[b]), yt = fma(ga, Yt[NI + b], Yt[b]);
+        const double xb = fma(gb, Xb[TX * NI + a], Xb[a]), xt = fma(gb, Xt[TX * NI + a], Xt[a]);
+        const double Bp = fma(cf->fd[2][q], bv, fma(cf->k0p[2], tv, fma(cf->e[0][a], yb, cf->e[1][b] * xb))) - qb[q];
+        const double Tp = fma(cf->fd[2][q], tv, fma(cf->k0p[2], bv, fma(cf->e[0][a], yt, cf->e[1][b] * xt))) - qt[q];
+        fB[q] += Bp;
+        fT[q] = Tp;
+      }
+  }
+  // y-faces, entries (a, b) = (i, k): z-edges at k, x-edges at i.  Round 0: even element rows
+  // (plain stores of S and N); round 1: odd rows add (the tile's last face row is plain when no
+  // even row wrote it)
+  {
+    double* fY = ac.yf(ey, ex);
+    double sp[N2], np[N2];
+#pragma unroll
+    for (int b = 0; b < NI; ++b)
+#pragma unroll
+      for (int a = 0; a < NI; ++a) {
+        const int q = a + NI * b;
+        const double ga = (a & 1) ? -1.0 : 1.0, gb = (b & 1) ? -1.0 : 1.0;
+        const double sv = S[q], nv = N[q];
+        const double zs = fma(ga, Z0[NI + b], Z0[b]), zn = fma(ga, Z1[NI + b], Z1[b]);
+        const double xs = fma(gb, Xt[a], Xb[a]), xn = fma(gb, Xt[TX * NI + a], Xb[TX * NI + a]);
+        sp[q] = fma(cf->fd[1][q], sv, fma(cf->k0p[1], nv, fma(cf->e[0][a], zs, cf->e[2][b] * xs))) - qs[q];
+        np[q] = fma(cf->fd[1][q], nv, fma(cf->k0p[1], sv, fma(cf->e[0][a], zn, cf->e[2][b] * xn))) - qn[q];
+      }
+    if (act && (iy & 1) == 0) {
+#pragma unroll
+      for (int q = 0; q < N2; ++q) { fY[q] = sp[q]; fY[q + TX * N2] = np[q]; }
+    }
+    bar_named(1);
+    if (act && (iy & 1) == 1) {
+#pragma unroll
+      for (int q = 0; q < N2; ++q) {
+        fY[q] += sp[q];
+        if (lasty) fY[q + TX * N2] = np[q]; else fY[q + TX * N2] += np[q];
+      }
+    }
+  }
+}
+
 // warps w and w+4 share an SM sub-partition: pair the largest class with the smallest (class
 // bits s_i s_j s_k; at n_I = 7 the point counts are 64+27, 48+36, 48+36, 48+36).
 __device__ __constant__ int kWarpClass[8] = {0, 1, 2, 4, 7, 6, 5, 3};
@@ -972,8 +1222,8 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
   ColCoef* sCf = reinterpret_cast<ColCoef*>(sm + C::O_CF);
   double* const rq = sm + C::O_RQ;
   __shared__ unsigned long long sTicket;
-  __shared__ long long sRow[32];
-  __shared__ RowIO sIO[32];
+  __shared__ long long sRow[C::MAXROWS];
+  __shared__ RowIO sIO[C::MAXROWS];
   __shared__ int sEpoch;
   const int tid = threadIdx.x;
   if (tid == 0) sEpoch = *(volatile int*)&P.st->epoch + 1;
@@ -1006,9 +1256,6 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
   const int vix = lane % TX, viy = lane / TX;                // element of this lane (condensed part)
   const int esub = lane / NI, ec = lane % NI;
   const bool evalid = lane < EPW * NI;
-  // face-pass constants
-  const double cx0 = dA * w0 + dB * K00, cy0 = dA * w0 + dC * K00, cz0 = dA * w0 + dD * K00;
-  const double d1w0 = dB * w0, d2w0 = dC * w0, d3w0 = dD * w0;
 
   for (;;) {
     __syncthreads();
@@ -1028,11 +1275,10 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
     // row descriptors of the tile, then the prologue: planes 0, 1 and side 0 as one cp.async group
     int ns;
     build_rows<NI>(P, sIO, x0, y0, tw, th, &ns);
-    const int nrw = ns + 4 * th + 2;
     __syncthreads();
-    load_rows(P.x, sIO, ns, nrw, sm + C::O_IP, 0, zdir(g, 0));
-    load_rows(P.x, sIO, 0, ns, sm + C::O_IS, 0, false);
-    load_rows(P.x, sIO, ns, nrw, sm + C::O_IP + C::PLANE, 1, zdir(g, 1));
+    load_block<NI>(P.x, sIO, true, ns, th, sm + C::O_IP, 0, zdir(g, 0));
+    load_block<NI>(P.x, sIO, false, ns, th, sm + C::O_IS, 0, false);
+    load_block<NI>(P.x, sIO, true, ns, th, sm + C::O_IP + C::PLANE, 1, zdir(g, 1));
     cp_commit();
     for (int t = tid; t < C::PLANE; t += NT) sm[C::O_AP + t] = 0.0;
     double dot = 0.0;
@@ -1047,8 +1293,9 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
       const Plane<NI> acb{sm + C::O_AP + (l & 1) * C::PLANE}, actp{sm + C::O_AP + ((l + 1) & 1) * C::PLANE};
       // prefetch side l+1 and plane l+2 (overlap this step's compute); wait for side l, plane l+1
 #if !(defined(SC_EXP) && SC_EXP == 25)
-      if (l + 1 < g.nz) load_rows(P.x, sIO, 0, ns, sm + C::O_IS + ((l + 1) & 1) * C::SIDE, l + 1, false);
-      if (l + 2 <= g.nz) load_rows(P.x, sIO, ns, nrw, sm + C::O_IP + ((l + 2) % 3) * C::PLANE, l + 2, zdir(g, l + 2));
+      if (l + 1 < g.nz) load_block<NI>(P.x, sIO, false, ns, th, sm + C::O_IS + ((l + 1) & 1) * C::SIDE, l + 1, false);
+      if (l + 2 <= g.nz)
+        load_block<NI>(P.x, sIO, true, ns, th, sm + C::O_IP + ((l + 2) % 3) * C::PLANE, l + 2, zdir(g, l + 2));
 #endif
       cp_commit();
       cp_wait<1>();
@@ -1078,7 +1325,10 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
         SC_PHASE(1);
         // ============ condensed part: parity-class warps, two output rounds ============
 #if !(defined(SC_EXP) && SC_EXP == 21)
-        vol_class<NI>(kWarpClass[warp], sCf, in, inb, intp, ac, acb, actp, rq, vix, viy, tw, th, ph_t0);
+        if constexpr (C::PER_ELEM)
+          vol_elem<NI>(sCf, in, inb, intp, ac, acb, actp, rq, tid % TX, tid / TX, tw, th);
+        else
+          vol_class<NI>(kWarpClass[warp], sCf, in, inb, intp, ac, acb, actp, rq, vix, viy, tw, th, ph_t0);
 #endif
         __syncthreads();
         SC_PHASE(2);

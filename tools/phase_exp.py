@@ -6,7 +6,8 @@ import torch
 from paper_1601_08179_b200 import context_for_grid, capi
 from synth import small_grid
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 128
-g = small_grid(8, (n, n, n), 1.0)
+pdeg = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+g = small_grid(pdeg, (n, n, n), 1.0)
 ctx = context_for_grid(g)
 x, y = ctx.skeleton(), ctx.skeleton()
 ctx.sc_fill_random(5, x)
