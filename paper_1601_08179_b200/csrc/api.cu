@@ -71,6 +71,7 @@ struct sc_ctx {
   bool use_col = false;
   std::vector<unsigned char> col_coef;  // kernel-parameter coefficient block
   int col_ntx = 0, col_nty = 0;
+  int col_nseg = 1, col_zseg = 0;       // z-segments per tile column (load balance over the SMs)
   void* d_colstate = nullptr;
   int* d_flags = nullptr;
   double* d_corner = nullptr;
@@ -305,14 +306,21 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
       col_tile(ni, &tx, &ty, &pend);
       ctx->col_ntx = (nx + tx - 1) / tx;
       ctx->col_nty = (ny + ty - 1) / ty;
-      size_t nflags = (size_t)ctx->col_ntx * ctx->col_nty * (nz + 1);
+      {
+        int dev = 0, nsm = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        col_choose_segments(ctx->col_ntx * ctx->col_nty, nz, nsm, &ctx->col_nseg, &ctx->col_zseg);
+      }
+      const size_t nitems = (size_t)ctx->col_ntx * ctx->col_nty * ctx->col_nseg;
+      size_t nflags = nitems * (nz + 1);
       size_t ncorner = (size_t)(ctx->col_ntx + 1) * (ctx->col_nty + 1) * (nz + 1) * 3 * (ni + 1);
       if (cudaMalloc(&ctx->d_colstate, 64) != cudaSuccess) return fail("cudaMalloc colstate");
       if (cudaMalloc(&ctx->d_flags, sizeof(int) * nflags) != cudaSuccess) return fail("cudaMalloc flags");
       if (cudaMalloc(&ctx->d_corner, sizeof(double) * ncorner) != cudaSuccess) return fail("cudaMalloc corner");
-      size_t npend = (size_t)ctx->col_ntx * ctx->col_nty * 3 * pend;   // 3 step slots (look-back distance 2)
+      size_t npend = nitems * 3 * pend;   // 3 step slots (look-back distance 2)
       if (cudaMalloc(&ctx->d_pending, sizeof(double) * npend) != cudaSuccess) return fail("cudaMalloc pending");
-      if (cudaMalloc(&ctx->d_dotp, sizeof(double) * ctx->col_ntx * ctx->col_nty) != cudaSuccess)
+      if (cudaMalloc(&ctx->d_dotp, sizeof(double) * nitems) != cudaSuccess)
         return fail("cudaMalloc dotp");
       const char* fd = getenv("SC_FUSED_DOT");
       ctx->fused_dot = fd && fd[0] == '1';
@@ -481,7 +489,8 @@ static sc_status apply_impl(sc_ctx* ctx, const double* x, double* y, const doubl
   cudaEvent_t* ev = rec ? &ctx->prof_ev[2 * ctx->prof_n] : nullptr;
   if (ctx->use_col)
     LAUNCH(launch_apply_col_raw(ctx->g, x, y, done, ctx->d_colstate, ctx->d_flags, ctx->d_corner, ctx->d_pending,
-                                ctx->col_ntx, ctx->col_nty, ctx->col_coef.data(), dotp, st, &nl_, ev));
+                                ctx->col_ntx, ctx->col_nty, ctx->col_nseg, ctx->col_zseg, ctx->col_coef.data(), dotp,
+                                st, &nl_, ev));
   else
     LAUNCH(launch_apply(ctx->g, x, y, done, st, &nl_, ev));
   if (rec) ctx->prof_n++;
@@ -520,7 +529,7 @@ static sc_status pcg_iteration(sc_ctx* ctx, cudaStream_t st) {
   sc_status s = apply_impl(ctx, ctx->pv, ctx->q, done, st, fused ? ctx->d_dotp : nullptr);
   if (s) return s;
   if (fused) {
-    LAUNCH(launch_sum_ordered(ctx->d_dotp, ctx->col_ntx * ctx->col_nty, ctx->scal, SCAL_RED0, done, st, &nl_));
+    LAUNCH(launch_sum_ordered(ctx->d_dotp, ctx->col_ntx * ctx->col_nty * ctx->col_nseg, ctx->scal, SCAL_RED0, done, st, &nl_));
   } else {
     LAUNCH(launch_dot_partial(ctx->pv, ctx->q, n, ctx->own, ctx->partials, done, st, &nl_));
     LAUNCH(launch_reduce2(ctx->partials, ctx->scal, SCAL_RED0, 1, done, st, &nl_));

@@ -25,6 +25,7 @@
 // barrier-separated rounds; the two elements of an x- (y-) face are summed with a lane shuffle.
 // The primary part (Htilde_BB, Eq. 26 generalised) is applied entity-centrically.
 #include <cuda_runtime.h>
+#include <stdlib.h>
 #include <string.h>
 #include "sc_device.cuh"
 
@@ -59,8 +60,9 @@ struct ColParams {
   int* flags;            // [nitems][nz+1]
   double* corner;        // [(nty+1)][(ntx+1)][nz+1][3][NI+1]
   double* pending;       // [nitems][2][PEND]
-  int ntx, nty, nitems;
-  double* dotp;          // optional: per-tile partial sums of x . y over final entries [nitems]
+  int ntx, nty, nitems;  // nitems = ntx nty nseg (item = seg * ntx nty + tile)
+  int nseg, zseg;        // z-segments of a tile column: element layers [s zseg, min(nz, (s+1) zseg))
+  double* dotp;          // optional: per-item partial sums of x . y over final entries [nitems]
   ColCoef cf;
 };
 
@@ -1264,9 +1266,17 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
     const long long item = (long long)sTicket;
     if (item >= P.nitems) break;
     const int epoch = sEpoch;
-    const int tx = (int)(item % P.ntx), ty = (int)(item / P.ntx);
+    const int ntile = P.ntx * P.nty;
+    const int seg = (int)(item / ntile), tile = (int)(item - (long long)seg * ntile);
+    const int tx = tile % P.ntx, ty = tile / P.ntx;
     const int x0 = tx * TX, y0 = ty * TY;
     const int tw = min(TX, g.nx - x0), th = min(TY, g.ny - y0);
+    // z-segment: steps [lfin0, lend] are finalized here; a segment above the first starts one
+    // step early (lbeg = lfin0 - 1) and recomputes element layer lbeg, whose side / plane lbeg
+    // the segment below finalizes, for the complete accumulator of plane lfin0 (no z exchange)
+    const int lfin0 = seg * P.zseg;
+    const int lbeg = seg > 0 ? lfin0 - 1 : 0;
+    const int lend = seg == P.nseg - 1 ? g.nz : min(g.nz, lfin0 + P.zseg) - 1;
     int* const flag_me = P.flags + item * (g.nz + 1);
     const int* const flag_w = tx > 0 ? P.flags + (item - 1) * (g.nz + 1) : nullptr;
     const int* const flag_s = ty > 0 ? P.flags + (item - P.ntx) * (g.nz + 1) : nullptr;
@@ -1276,25 +1286,26 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
     int ns;
     build_rows<NI>(P, sIO, x0, y0, tw, th, &ns);
     __syncthreads();
-    load_block<NI>(P.x, sIO, true, ns, th, sm + C::O_IP, 0, zdir(g, 0));
-    load_block<NI>(P.x, sIO, false, ns, th, sm + C::O_IS, 0, false);
-    load_block<NI>(P.x, sIO, true, ns, th, sm + C::O_IP + C::PLANE, 1, zdir(g, 1));
+    load_block<NI>(P.x, sIO, true, ns, th, sm + C::O_IP + (lbeg % 3) * C::PLANE, lbeg, zdir(g, lbeg));
+    load_block<NI>(P.x, sIO, false, ns, th, sm + C::O_IS + (lbeg & 1) * C::SIDE, lbeg, false);
+    load_block<NI>(P.x, sIO, true, ns, th, sm + C::O_IP + ((lbeg + 1) % 3) * C::PLANE, lbeg + 1, zdir(g, lbeg + 1));
     cp_commit();
-    for (int t = tid; t < C::PLANE; t += NT) sm[C::O_AP + t] = 0.0;
+    for (int t = tid; t < C::PLANE; t += NT) sm[C::O_AP + (lbeg & 1) * C::PLANE + t] = 0.0;
     double dot = 0.0;
 
     // Step l computes element layer l (l < nz) and finalizes layer l / plane l.  Inputs: side l
     // in buffer l & 1, plane q in q % 3 (so plane l+2 is prefetched at the top of step l into
     // the buffer of plane l-1); accumulators: side (one buffer), plane q in q & 1.
-    for (int l = 0; l <= g.nz; ++l) {
+    for (int l = lbeg; l <= lend; ++l) {
       const bool last = (l == g.nz);         // final step: only plane nz remains
       const Side<NI> in{sm + C::O_IS + (l & 1) * C::SIDE};
       const Plane<NI> inb{sm + C::O_IP + (l % 3) * C::PLANE}, intp{sm + C::O_IP + ((l + 1) % 3) * C::PLANE};
       const Plane<NI> acb{sm + C::O_AP + (l & 1) * C::PLANE}, actp{sm + C::O_AP + ((l + 1) & 1) * C::PLANE};
       // prefetch side l+1 and plane l+2 (overlap this step's compute); wait for side l, plane l+1
 #if !(defined(SC_EXP) && SC_EXP == 25)
-      if (l + 1 < g.nz) load_block<NI>(P.x, sIO, false, ns, th, sm + C::O_IS + ((l + 1) & 1) * C::SIDE, l + 1, false);
-      if (l + 2 <= g.nz)
+      if (l + 1 < g.nz && l + 1 <= lend)
+        load_block<NI>(P.x, sIO, false, ns, th, sm + C::O_IS + ((l + 1) & 1) * C::SIDE, l + 1, false);
+      if (l + 2 <= g.nz && l + 2 <= lend + 1)
         load_block<NI>(P.x, sIO, true, ns, th, sm + C::O_IP + ((l + 2) % 3) * C::PLANE, l + 2, zdir(g, l + 2));
 #endif
       cp_commit();
@@ -1454,7 +1465,8 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
       }
       // publication of step l-1 (look-back distance 2): its stores were issued before the CTA
       // barrier that ended step l-1 and have drained during this step's compute
-      if (tid == 0 && l >= 1) {
+      if (l < lfin0) continue;               // warm-up step of an upper z-segment: no output
+      if (tid == 0 && l >= lfin0 + 1) {
 #if !(defined(SC_EXP) && SC_EXP == 26)
         __threadfence();
 #endif
@@ -1467,7 +1479,7 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
       SC_PHASE(7);
       // finish the W / S boundary entities of step l-2
 #if !(defined(SC_EXP) && SC_EXP == 24)
-      if (l >= 2) finish_boundary<NI>(P, item, l - 2, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO, dot);
+      if (l >= lfin0 + 2) finish_boundary<NI>(P, item, l - 2, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO, dot);
 #endif
       __syncthreads();
       SC_PHASE(8);
@@ -1475,11 +1487,12 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
     // end of the column: publish step nz, finish steps nz-1 and nz
     if (tid == 0) {
       __threadfence();
-      flag_release(flag_me + g.nz, epoch);
+      flag_release(flag_me + lend, epoch);
     }
-    if (g.nz >= 1) finish_boundary<NI>(P, item, g.nz - 1, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO, dot);
+    if (lend - 1 >= lfin0)
+      finish_boundary<NI>(P, item, lend - 1, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO, dot);
     __syncthreads();
-    finish_boundary<NI>(P, item, g.nz, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO, dot);
+    finish_boundary<NI>(P, item, lend, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO, dot);
     // per-tile partial of x . y (fixed order: deterministic)
     if (P.dotp) {
 #pragma unroll
@@ -1546,6 +1559,26 @@ void col_tile(int ni, int* tx, int* ty, int* pend) {
   }
 }
 
+// Load balance of the persistent kernel: ntiles tile columns on nsm CTAs take
+// ceil(ntiles / nsm) rounds of nz + 1 steps; splitting each column into S z-segments gives
+// ceil(S ntiles / nsm) rounds of ceil(nz / S) + 1 (+ 1 recomputed layer) steps.  Model cost per
+// round: the steps plus ~2 steps of look-back pipeline fill.  SC_ZSEG overrides S.
+void col_choose_segments(int ntiles, int nz, int nsm, int* nseg, int* zseg) {
+  int best = 1;
+  double bcost = 1e300;
+  const char* env = getenv("SC_ZSEG");
+  const int forced = env ? atoi(env) : 0;
+  for (int S = 1; S <= 8 && S <= nz; ++S) {
+    const int zs = (nz + S - 1) / S;
+    if ((long long)zs * (S - 1) >= nz) continue;           // every segment non-empty
+    const double rounds = (double)(((long long)ntiles * S + nsm - 1) / nsm);
+    const double cost = rounds * (zs + 1 + (S > 1 ? 1 : 0) + 2);
+    if (forced ? S == forced : cost < bcost * 0.97) { bcost = cost; best = S; }
+  }
+  *nseg = best;
+  *zseg = (nz + best - 1) / best;
+}
+
 // Host-side coefficient block of the uniform-geometry kernel (c[d][m] = d_{d+1} a0_m, D^{-1}).
 void col_make_coef(int ni, const double* d, const double* a0, const double* lam, double K00, double K0p, double w0,
                    std::vector<unsigned char>& out) {
@@ -1591,12 +1624,13 @@ int launch_apply_col(const ColParams& P, void* stream, int* nl, int* grid_out, v
 }
 
 int launch_apply_col_raw(const Geom& g, const double* x, double* y, const double* done, void* state, int* flags,
-                         double* corner, double* pending, int ntx, int nty, const void* coef, double* dotp,
-                         void* stream, int* nl, void* events) {
+                         double* corner, double* pending, int ntx, int nty, int nseg, int zseg, const void* coef,
+                         double* dotp, void* stream, int* nl, void* events) {
   ColParams P;
   P.g = g; P.x = x; P.y = y; P.done = done; P.st = (ColState*)state; P.flags = flags; P.corner = corner;
   P.pending = pending;
-  P.ntx = ntx; P.nty = nty; P.nitems = ntx * nty;
+  P.ntx = ntx; P.nty = nty; P.nitems = ntx * nty * nseg;
+  P.nseg = nseg; P.zseg = zseg;
   P.dotp = dotp;
   memcpy(&P.cf, coef, sizeof(ColCoef));
   int grid = 0;

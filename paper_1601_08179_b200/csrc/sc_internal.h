@@ -107,8 +107,10 @@ void col_tile(int ni, int* tx, int* ty, int* pend);
 void col_make_coef(int ni, const double* d, const double* a0, const double* lam, double K00, double K0p, double w0,
                    std::vector<unsigned char>& out);
 int launch_apply_col_raw(const Geom& g, const double* x, double* y, const double* done, void* state, int* flags,
-                         double* corner, double* pending, int ntx, int nty, const void* coef, double* dotp,
-                         void* stream, int* nlaunch, void* events);
+                         double* corner, double* pending, int ntx, int nty, int nseg, int zseg, const void* coef,
+                         double* dotp, void* stream, int* nlaunch, void* events);
+// z-segments of the tile columns: ntiles columns of nz layers on nsm persistent CTAs
+void col_choose_segments(int ntiles, int nz, int nsm, int* nseg, int* zseg);
 // sum of v[0..n) in a fixed order into scal[slot] (deterministic), skipped when *done != 0
 int launch_sum_ordered(const double* v, int n, double* scal, int slot, const double* done, void* stream, int* nl);
 int launch_add_segments(double* y, const double* add, const long long* off, const long long* len, int n,

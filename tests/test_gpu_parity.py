@@ -330,3 +330,38 @@ def test_col_kernel_matches_v1_kernel_large():
     assert not torch.isnan(y2).any()
     d = (y1 - y2).norm() / y1.norm()
     assert float(d) <= 1e-13
+
+
+# ---- z-segmented tile columns (load balance): a segment above the first recomputes the layer
+# below its first plane; every split of the 7 layers, incl. a ragged last segment
+@pytest.mark.parametrize("p,ne", [(2, (19, 11, 7)), (3, (10, 7, 7)), (8, (9, 6, 7))])
+@pytest.mark.parametrize("nseg", ["1", "2", "3", "4", "7"])
+def test_operator_parity_zsegments(p, ne, nseg, monkeypatch):
+    monkeypatch.setenv("SC_ZSEG", nseg)
+    g = small_grid(p, ne, 0.6, lengths=(1.1, 0.9, 1.4))
+    op = operator.AssembledCondensedOperator(g)
+    x = lattice_random(40 + p, g.ne, g.p).ravel()
+    ctx = ctx_for(g)
+    y, _, _ = gpu_apply_nodal(ctx, x)
+    assert rel(y, op.apply(x)) <= 1e-12
+
+
+@pytest.mark.parametrize("nseg,fused", [("2", "0"), ("3", "1")])
+def test_pcg_parity_zsegments(nseg, fused, monkeypatch):
+    from paper_1601_08179_b200 import SC_DUAL
+    monkeypatch.setenv("SC_ZSEG", nseg)
+    monkeypatch.setenv("SC_FUSED_DOT", fused)
+    g = small_grid(4, (10, 6, 8), 1.0, lengths=(1.3, 0.7, 1.5))
+    op = operator.AssembledCondensedOperator(g)
+    ctx = ctx_for(g)
+    bt = ctx.skeleton()
+    ctx.sc_fill_random(9, bt)
+    lat = ctx.lattice()
+    ctx.sc_from_transformed(bt, lat, SC_DUAL)
+    b = lat.cpu().numpy()
+    res = _oracle_pcg(g, op, b, 1e-10)
+    xt = ctx.skeleton()
+    rep = ctx.sc_pcg_solve(bt, xt, rtol=1e-10, maxit=2000)
+    assert rep.converged and abs(rep.iters - res.iters) <= 1
+    ref = res.x if rep.iters == res.iters else _oracle_pcg(g, op, b, 0, fixed=rep.iters).x
+    assert rel(ctx.to_lattice_nodal(xt).cpu().numpy(), ref) <= 1e-10
