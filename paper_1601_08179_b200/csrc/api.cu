@@ -69,6 +69,9 @@ struct sc_ctx {
   double* d_dinv = nullptr;             // uniform D^{-1} table
   // v3 tile-column operator state (kernels_col.cu)
   bool use_col = false;
+  bool use_big = false;                 // v4 colour-scheduled element operator (n_I >= 8, uniform geometry)
+  std::vector<unsigned char> big_coef;
+  double* d_big_dt = nullptr;           // its D^{-1} table [i][k][32]
   std::vector<unsigned char> col_coef;  // kernel-parameter coefficient block
   int col_ntx = 0, col_nty = 0;
   int col_nseg = 1, col_zseg = 0;       // z-segments per tile column (load balance over the SMs)
@@ -329,6 +332,14 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
       if (cudaMemset(ctx->d_corner, 0, sizeof(double) * ncorner) != cudaSuccess) return fail("memset corner");
       ctx->use_col = true;
     }
+    if (!ctx->use_col && big_supported(ni) && uniform && sig_ok && !(env && env[0] == '1')) {
+      std::vector<double> dt;
+      big_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->big_coef, dt);
+      if (cudaMalloc(&ctx->d_big_dt, sizeof(double) * dt.size()) != cudaSuccess) return fail("cudaMalloc big dt");
+      if (cudaMemcpy(ctx->d_big_dt, dt.data(), sizeof(double) * dt.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+        return fail("cudaMemcpy big dt");
+      ctx->use_big = true;
+    }
   }
   // ---- interface planes (z-face plane, x-edges, y-edges, vertices at fz = 0 / nz)
   long long lens[4] = {(long long)nx * ny * n2, (long long)nx * (ny + 1) * ni, (long long)(nx + 1) * ny * ni,
@@ -365,6 +376,7 @@ extern "C" sc_status sc_destroy(sc_ctx* ctx) {
   if (ctx->d_corner) cudaFree(ctx->d_corner);
   if (ctx->d_pending) cudaFree(ctx->d_pending);
   if (ctx->d_dotp) cudaFree(ctx->d_dotp);
+  if (ctx->d_big_dt) cudaFree(ctx->d_big_dt);
   for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);
   delete ctx;
   return SC_OK;
@@ -491,6 +503,8 @@ static sc_status apply_impl(sc_ctx* ctx, const double* x, double* y, const doubl
     LAUNCH(launch_apply_col_raw(ctx->g, x, y, done, ctx->d_colstate, ctx->d_flags, ctx->d_corner, ctx->d_pending,
                                 ctx->col_ntx, ctx->col_nty, ctx->col_nseg, ctx->col_zseg, ctx->col_coef.data(), dotp,
                                 st, &nl_, ev));
+  else if (ctx->use_big)
+    LAUNCH(launch_apply_big(ctx->g, x, y, done, ctx->big_coef.data(), ctx->d_big_dt, st, &nl_, ev));
   else
     LAUNCH(launch_apply(ctx->g, x, y, done, st, &nl_, ev));
   if (rec) ctx->prof_n++;

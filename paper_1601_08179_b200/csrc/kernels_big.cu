@@ -1,0 +1,380 @@
+// Condensed operator v4 for n_I >= 8 (p >= 9), uniform geometry.
+//
+// One CTA (8 warps) per element.  The elements are processed in the 8 parity colours
+// (ex, ey, ez mod 2), one launch per colour: two elements of one colour share no face, edge or
+// vertex, so the assembly R^ (a8) is a plain read-modify-write of y (zeroed first) --
+// deterministic and atomic-free -- and a3 is a plain gather of the element's shell.
+//
+// Condensed part (Table 2 of PAPER.md P:425-440, faces-in / D^{-1} / faces-out, in the sigma-split
+// form ap = sigma a0):
+//   u(i,j,k) = c1_i Px^{s_i}(j,k) + c2_j Py^{s_j}(i,k) + c3_k Pz^{s_k}(i,j),   Px^s = W + (-1)^s E, ...
+//   v = u D^{-1};  Qx^s(j,k) = sum_{i: s_i = s} c1_i v,  likewise Qy (over j), Qz (over k)
+//   W -= Qx^0 + Qx^1, E -= Qx^0 - Qx^1, ...                     (c_d = d_d a0, 7 FP64 ops / point)
+// Thread mapping: lane -> j (SW = 16 or 32 lanes per j-group), (warp, half) -> a residue class of
+// i (NG = 8 H classes), fully unrolled loop over k.  The k-sums (Qz) complete in registers, the
+// i-sums (Qx) in registers over the thread's i values and then across the warps that share the
+// parity of i (fixed-order tree through shared memory), the j-sums (Qy) through a per-warp
+// shared-memory transpose.  D^{-1} is read from an L2-resident [i][k][j] table (coalesced in j).
+// Primary part (Eq. 26 generalised): faces in the closed form of kernels_col.cu, edges
+// and vertices from the arrowhead rows of Ktilde with a0-weighted line sums of faces / edges.
+#include <cuda_runtime.h>
+#include <stdlib.h>
+#include <string.h>
+#include <vector>
+#include "sc_device.cuh"
+
+namespace sc {
+
+struct BigCoef {
+  double c[3][32];   // c[d][m] = d_{d+1} a0_m          (condensed part)
+  double e[3][32];   // e[d][m] = d_{d+1} w0 a0_m       (face <- bounding edges)
+  double L[3][32];   // L[d][m] = d_{d+1} w0 Lam_m      (face self term)
+  double a0[32], lam[32];
+  double F0[3];      // d0 w0 + d_{d+1} K00             (face self term)
+  double k0p[3];     // d_{d+1} K0p                     (opposite face)
+  double d[4];
+  double K00, K0p, w0;
+};
+
+struct BigParams {
+  Geom g;
+  const double* x;
+  double* y;
+  const double* done;
+  const double* dt;   // D^{-1}(i,j,k) at (i n_I + k) 32 + j
+  BigCoef cf;
+};
+
+template <int NI>
+struct BL {
+  static constexpr int N2 = NI * NI;
+  static constexpr int SW = NI <= 16 ? 16 : 32;   // lanes per j-group
+  static constexpr int H = 32 / SW;                // j-groups per warp
+  static constexpr int NG = 8 * H;                 // residue classes of i
+  static constexpr int NIT = (NI + NG - 1) / NG;   // i values per thread
+  static constexpr int SH = 6 * N2 + 12 * NI + 8;  // shell: faces w e s n b t | 12 edges | 8 vertices
+  static constexpr int O_SH = 0;
+  static constexpr int O_P = SH;                   // Px^0 Px^1 Py^0 Py^1 Pz^0 Pz^1
+  static constexpr int O_Q = O_P + 6 * N2;         // Qx^0 Qx^1 Qy^0 Qy^1 Qz^0 Qz^1
+  static constexpr int O_LS = O_Q + 6 * N2;        // face line sums [6][2][NI][2] (R+, R-)
+  static constexpr int O_ES = O_LS + 24 * NI;      // edge line sums [12][2]
+  static constexpr int YS = SW + 1;                // row stride of the Qy transpose buffers
+  static constexpr int O_Y = O_ES + 24;            // [8 H][NI][YS]; reused by the Qx tree
+  static constexpr int TOTAL = O_Y + 8 * H * NI * YS;
+  static_assert(4 * H * NI * SW <= 8 * H * NI * YS, "Qx tree slots");
+};
+
+__device__ __forceinline__ double sgn(int m) { return (m & 1) ? -1.0 : 1.0; }
+__device__ __forceinline__ double eo_row_b(const double* r, int hi) { return hi ? r[0] - r[1] : r[0] + r[1]; }
+
+template <int NI>
+__global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ BigParams P, int colour) {
+  using B = BL<NI>;
+  constexpr int N2 = B::N2, SW = B::SW, H = B::H, NG = B::NG, YS = B::YS;
+  if (P.done != nullptr && *P.done != 0.0) return;
+  extern __shared__ double sm[];
+  __shared__ long long sBase[26];
+  __shared__ int sDir[26];
+  const Geom& g = P.g;
+  const BigCoef& cf = P.cf;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int cx = colour & 1, cy = (colour >> 1) & 1, cz = colour >> 2;
+  const int ncx = (g.nx - cx + 1) >> 1, ncy = (g.ny - cy + 1) >> 1;
+  const int bid = blockIdx.x;
+  const int ex = cx + 2 * (bid % ncx), ey = cy + 2 * ((bid / ncx) % ncy), ez = cz + 2 * (bid / (ncx * ncy));
+  if (tid < 26) {
+    bool dr;
+    sBase[tid] = entity_base(g, ex, ey, ez, tid, &dr);
+    sDir[tid] = dr;
+  }
+  __syncthreads();
+  double* const sh = sm + B::O_SH;
+  // ---- a3: the element's shell (Dirichlet entities as 0)
+#pragma unroll 4
+  for (int t = tid; t < B::SH; t += 256) {
+    int ent, loc;
+    if (t < 6 * N2) { ent = t / N2; loc = t - ent * N2; }
+    else if (t < 6 * N2 + 12 * NI) { const int u = t - 6 * N2, e = u / NI; ent = 6 + e; loc = u - e * NI; }
+    else { ent = 18 + (t - 6 * N2 - 12 * NI); loc = 0; }
+    sh[t] = sDir[ent] ? 0.0 : __ldg(P.x + sBase[ent] + loc);
+  }
+  __syncthreads();
+  // ---- faces-in operands P^s = lo + (-1)^s hi, a0-weighted line sums (R+, R-) of faces / edges
+  double* const sP = sm + B::O_P;
+  double* const sQ = sm + B::O_Q;
+  double* const sLS = sm + B::O_LS;
+  double* const sES = sm + B::O_ES;
+  for (int t = tid; t < 3 * N2; t += 256) {
+    const int f = t / N2, q = t - f * N2;
+    const double lo = sh[2 * f * N2 + q], hi = sh[(2 * f + 1) * N2 + q];
+    sP[2 * f * N2 + q] = lo + hi;
+    sP[(2 * f + 1) * N2 + q] = lo - hi;
+  }
+  for (int t = tid; t < 12 * NI + 12; t += 256) {
+    const double* F;
+    int st;
+    if (t < 12 * NI) {   // (face f, d): d = 0 sums over the first coordinate a at b = c, d = 1 over b at a = c
+      const int fd = t / NI, c = t - fd * NI, f = fd >> 1;
+      F = (fd & 1) ? sh + f * N2 + c : sh + f * N2 + NI * c;
+      st = (fd & 1) ? NI : 1;
+    } else {
+      F = sh + 6 * N2 + (t - 12 * NI) * NI;
+      st = 1;
+    }
+    double rp = 0.0, rm = 0.0;
+#pragma unroll
+    for (int a = 0; a < NI; ++a) {
+      if (a & 1) rm = fma(cf.a0[a], F[a * st], rm);
+      else rp = fma(cf.a0[a], F[a * st], rp);
+    }
+    double* o = t < 12 * NI ? sLS + 2 * t : sES + 2 * (t - 12 * NI);
+    o[0] = rp;
+    o[1] = rm;
+  }
+  __syncthreads();
+
+  // ---- a4-a6: condensed part
+  {
+    const int j = lane % SW, h = lane / SW, ig = warp * H + h;
+    const bool jok = j < NI;
+    const int jc = jok ? j : 0;
+    const double c2j = jok ? cf.c[1][jc] : 0.0;
+    const double* Pxs = sP + (ig & 1) * N2;            // Px^{s_i}; s_i = ig & 1 (NG even)
+    const double* Pyj = sP + (2 + (j & 1)) * N2;       // Py^{s_j}
+    const double* Pz0 = sP + 4 * N2;
+    const double* Pz1 = sP + 5 * N2;
+    double* const Yb = sm + B::O_Y + (warp * H + h) * NI * YS;
+    double qx[NI];
+#pragma unroll
+    for (int k = 0; k < NI; ++k) qx[k] = 0.0;
+#pragma unroll 1
+    for (int it = 0; it < B::NIT; ++it) {
+      const int i = ig + it * NG;
+      const bool iok = i < NI;
+      const unsigned am = __ballot_sync(0xffffffffu, iok);
+      if (iok) {
+        const double c1i = cf.c[0][i];
+        const double pz0 = Pz0[i + NI * jc], pz1 = Pz1[i + NI * jc];
+        const double* Pyi = Pyj + i;
+        const double* Dt = P.dt + (size_t)i * NI * 32 + jc;
+        double qz0 = 0.0, qz1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < NI; ++k) {
+          const double u = fma(c1i, Pxs[jc + NI * k], fma(c2j, Pyi[NI * k], cf.c[2][k] * ((k & 1) ? pz1 : pz0)));
+          const double v = u * __ldg(Dt + k * 32);
+          qx[k] = fma(c1i, v, qx[k]);
+          Yb[k * YS + j] = c2j * v;
+          if (k & 1) qz1 = fma(cf.c[2][k], v, qz1);
+          else qz0 = fma(cf.c[2][k], v, qz0);
+        }
+        if (jok) {
+          sQ[4 * N2 + i + NI * j] = qz0;
+          sQ[5 * N2 + i + NI * j] = qz1;
+        }
+        __syncwarp(am);
+        // Qy^s(i, k) = sum over j of parity s: one (k, s) pair per lane and pass
+        for (int pr = j; pr < 2 * NI; pr += SW) {
+          const int k = pr >> 1, s = pr & 1;
+          const double* yr = Yb + k * YS + s;
+          double a0s = 0.0, a1s = 0.0;
+#pragma unroll
+          for (int jj = 0; jj < NI; jj += 4) {
+            if (jj + s < NI) a0s += yr[jj];
+            if (jj + 2 + s < NI) a1s += yr[jj + 2];
+          }
+          sQ[(2 + s) * N2 + i + NI * k] = a0s + a1s;
+        }
+        __syncwarp(am);
+      }
+    }
+    // Qx: fixed-order tree over the warps holding the same parity of i (H == 1: warp parity;
+    // H == 2: the half), through the (now free) transpose buffers
+    constexpr int STMIN = H == 1 ? 2 : 1;
+    double* const slots = sm + B::O_Y;
+#pragma unroll 1
+    for (int st = 4; st >= STMIN; st >>= 1) {
+      __syncthreads();
+      if (warp >= st && warp < 2 * st) {
+        double* sl = slots + ((warp - st) * H + h) * NI * SW + j;
+#pragma unroll
+        for (int k = 0; k < NI; ++k) sl[k * SW] = qx[k];
+      }
+      __syncthreads();
+      if (warp < st) {
+        const double* sl = slots + (warp * H + h) * NI * SW + j;
+#pragma unroll
+        for (int k = 0; k < NI; ++k) qx[k] += sl[k * SW];
+      }
+    }
+    if (warp < STMIN && jok) {
+      double* Qx = sQ + (H == 1 ? warp : h) * N2 + j;
+#pragma unroll
+      for (int k = 0; k < NI; ++k) Qx[NI * k] = qx[k];
+    }
+  }
+  __syncthreads();
+
+  // ---- a6 + a7 + a8: outputs (primary - condensed part on faces, primary on edges / vertices),
+  // read-modify-write into y
+  const double* const Ed = sh + 6 * N2;
+  const double* const Vv = Ed + 12 * NI;
+  const double K00 = cf.K00, K0p = cf.K0p, w0 = cf.w0, w02 = w0 * w0;
+  auto out_at = [&](int t) -> double {
+    if (t < 6 * N2) {
+      const int f = t / N2, q = t - f * N2, a = q % NI, b = q / NI, d = f >> 1, hi = f & 1;
+      // (la, lb): directions of the face coordinates; bounding edges of the face (local ids - 6)
+      const int la = d == 0 ? 1 : 0, lb = d == 2 ? 1 : 2;
+      int ea0, ea1, eb0, eb1;
+      switch (f) {
+        case 0: ea0 = 8; ea1 = 10; eb0 = 4; eb1 = 6; break;
+        case 1: ea0 = 9; ea1 = 11; eb0 = 5; eb1 = 7; break;
+        case 2: ea0 = 8; ea1 = 9; eb0 = 0; eb1 = 2; break;
+        case 3: ea0 = 10; ea1 = 11; eb0 = 1; eb1 = 3; break;
+        case 4: ea0 = 4; ea1 = 5; eb0 = 0; eb1 = 1; break;
+        default: ea0 = 6; ea1 = 7; eb0 = 2; eb1 = 3; break;
+      }
+      const double fd = cf.F0[d] + cf.L[la][a] + cf.L[lb][b];
+      const double self = sh[f * N2 + q], opp = sh[(f ^ 1) * N2 + q];
+      const double ta = cf.e[la][a] * fma(sgn(a), Ed[ea1 * NI + b], Ed[ea0 * NI + b]);
+      const double tb = cf.e[lb][b] * fma(sgn(b), Ed[eb1 * NI + a], Ed[eb0 * NI + a]);
+      const double Q = fma(hi ? -1.0 : 1.0, sQ[(2 * d + 1) * N2 + q], sQ[2 * d * N2 + q]);
+      return fma(fd, self, fma(cf.k0p[d], opp, ta + tb)) - Q;
+    }
+    if (t < 6 * N2 + 12 * NI) {
+      const int u = t - 6 * N2, e = u / NI, c = u - e * NI, grp = e >> 2, b0 = e & 1, b1 = (e >> 1) & 1;
+      const double uu = Ed[e * NI + c];
+      // along the edge (interior row of Ktilde): the two end vertices
+      int v0, v1;
+      // boundary directions o1 (bit b0) and o2 (bit b1): parallel edges and the line sums
+      int p10, p11, l1, p20, p21, l2;
+      if (grp == 0) {          // x-edge (jb, kb) = (b0, b1)
+        v0 = 2 * b0 + 4 * b1; v1 = v0 + 1;
+        p10 = 2 * b1; p11 = 2 * b1 + 1; l1 = ((4 + b1) * 2 + 1) * NI + c;     // o1 = y: z-face b1, sum over j
+        p20 = b0; p21 = b0 + 2; l2 = ((2 + b0) * 2 + 1) * NI + c;             // o2 = z: y-face b0, sum over k
+      } else if (grp == 1) {   // y-edge (ib, kb) = (b0, b1)
+        v0 = b0 + 4 * b1; v1 = v0 + 2;
+        p10 = 4 + 2 * b1; p11 = 5 + 2 * b1; l1 = ((4 + b1) * 2 + 0) * NI + c;  // o1 = x: z-face b1, sum over i
+        p20 = 4 + b0; p21 = 6 + b0; l2 = (b0 * 2 + 1) * NI + c;                // o2 = z: x-face b0, sum over k
+      } else {                 // z-edge (ib, jb) = (b0, b1)
+        v0 = b0 + 2 * b1; v1 = v0 + 4;
+        p10 = 8 + 2 * b1; p11 = 9 + 2 * b1; l1 = ((2 + b1) * 2 + 0) * NI + c;  // o1 = x: y-face b1, sum over i
+        p20 = 8 + b0; p21 = 10 + b0; l2 = (b0 * 2 + 0) * NI + c;               // o2 = y: x-face b0, sum over j
+      }
+      const double tal = cf.a0[c] * fma(sgn(c), Vv[v1], Vv[v0]) + cf.lam[c] * uu;
+      const double u10 = Ed[p10 * NI + c], u11 = Ed[p11 * NI + c], u20 = Ed[p20 * NI + c], u21 = Ed[p21 * NI + c];
+      const double t1 = (b0 ? fma(K0p, u10, K00 * u11) : fma(K00, u10, K0p * u11)) + eo_row_b(sLS + 2 * l1, b0);
+      const double t2 = (b1 ? fma(K0p, u20, K00 * u21) : fma(K00, u20, K0p * u21)) + eo_row_b(sLS + 2 * l2, b1);
+      // d indices: along = grp, o1 / o2 = the other two in increasing order
+      const int o1 = grp == 0 ? 1 : 0, o2 = grp == 2 ? 1 : 2;
+      return w02 * (cf.d[0] * uu + cf.d[1 + grp] * tal) + w0 * (cf.d[1 + o1] * t1 + cf.d[1 + o2] * t2);
+    }
+    const int v = t - 6 * N2 - 12 * NI, ib = v & 1, jb = (v >> 1) & 1, kb = v >> 2;
+    const double uu = Vv[v];
+    // partner vertices along x / y / z: (lo, hi) of the pair containing v
+    const int xl = v - ib, yl = v - 2 * jb, zl = v - 4 * kb;
+    const double x0v = Vv[xl], x1v = Vv[xl + 1], y0v = Vv[yl], y1v = Vv[yl + 2], z0v = Vv[zl], z1v = Vv[zl + 4];
+    const double tx = (ib ? fma(K0p, x0v, K00 * x1v) : fma(K00, x0v, K0p * x1v)) + eo_row_b(sES + 2 * (jb + 2 * kb), ib);
+    const double ty = (jb ? fma(K0p, y0v, K00 * y1v) : fma(K00, y0v, K0p * y1v)) + eo_row_b(sES + 2 * (4 + ib + 2 * kb), jb);
+    const double tz = (kb ? fma(K0p, z0v, K00 * z1v) : fma(K00, z0v, K0p * z1v)) + eo_row_b(sES + 2 * (8 + ib + 2 * jb), kb);
+    return w02 * (w0 * cf.d[0] * uu + cf.d[1] * tx + cf.d[2] * ty + cf.d[3] * tz);
+  };
+  constexpr int NO = B::SH, PER = (NO + 255) / 256, CH = 8;
+#pragma unroll 1
+  for (int r0 = 0; r0 < PER; r0 += CH) {
+    double val[CH], old[CH];
+    double* dst[CH];
+#pragma unroll
+    for (int r = 0; r < CH; ++r) {
+      dst[r] = nullptr;
+      val[r] = 0.0;
+      const int t = tid + (r0 + r) * 256;
+      if (r0 + r >= PER || t >= NO) continue;
+      int ent, loc;
+      if (t < 6 * N2) { ent = t / N2; loc = t - ent * N2; }
+      else if (t < 6 * N2 + 12 * NI) { const int u = t - 6 * N2, e = u / NI; ent = 6 + e; loc = u - e * NI; }
+      else { ent = 18 + (t - 6 * N2 - 12 * NI); loc = 0; }
+      if (sDir[ent]) continue;
+      dst[r] = P.y + sBase[ent] + loc;
+      val[r] = out_at(t);
+    }
+#pragma unroll
+    for (int r = 0; r < CH; ++r) old[r] = dst[r] ? *dst[r] : 0.0;
+#pragma unroll
+    for (int r = 0; r < CH; ++r)
+      if (dst[r]) *dst[r] = old[r] + val[r];
+  }
+}
+
+template <int NI>
+static int launch_big_t(const BigParams& P, cudaStream_t st, int* nl) {
+  using B = BL<NI>;
+  static_assert(sizeof(double) * B::TOTAL <= 225 * 1024, "shared memory budget");
+  const size_t smem = sizeof(double) * B::TOTAL;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_apply_big<NI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  for (int c = 0; c < 8; ++c) {
+    const int cx = c & 1, cy = (c >> 1) & 1, cz = c >> 2;
+    const long long n = (long long)((P.g.nx - cx + 1) >> 1) * ((P.g.ny - cy + 1) >> 1) * ((P.g.nz - cz + 1) >> 1);
+    if (n <= 0) continue;
+    k_apply_big<NI><<<(unsigned)n, 256, smem, st>>>(P, c);
+    (*nl)++;
+  }
+  return cudaGetLastError();
+}
+
+bool big_supported(int ni) { return ni >= 8 && ni <= 31; }
+
+int launch_apply_big(const Geom& g, const double* x, double* y, const double* done, const void* coef,
+                     const double* dt, void* stream, int* nl, void* events) {
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaEvent_t* ev = (cudaEvent_t*)events;
+  cudaError_t err = cudaMemsetAsync(y, 0, sizeof(double) * g.n_total, st);
+  if (err != cudaSuccess) return err;
+  if (ev) cudaEventRecord(ev[0], st);
+  BigParams P;
+  P.g = g; P.x = x; P.y = y; P.done = done; P.dt = dt;
+  memcpy(&P.cf, coef, sizeof(BigCoef));
+  int rc = cudaErrorInvalidValue;
+  switch (g.ni) {
+#define BCASE(N) case N: rc = launch_big_t<N>(P, st, nl); break;
+    BCASE(8) BCASE(9) BCASE(10) BCASE(11) BCASE(12) BCASE(13) BCASE(14) BCASE(15) BCASE(16) BCASE(17)
+    BCASE(18) BCASE(19) BCASE(20) BCASE(21) BCASE(22) BCASE(23) BCASE(24) BCASE(25) BCASE(26) BCASE(27)
+    BCASE(28) BCASE(29) BCASE(30) BCASE(31)
+#undef BCASE
+    default: break;
+  }
+  if (ev) cudaEventRecord(ev[1], st);
+  return rc;
+}
+
+// Host-side coefficient block and D^{-1} table of the v4 operator (uniform geometry d).
+void big_make_coef(int ni, const double* d, const double* a0, const double* lam, double K00, double K0p, double w0,
+                   std::vector<unsigned char>& coef, std::vector<double>& dt) {
+  BigCoef cf;
+  memset(&cf, 0, sizeof(cf));
+  for (int q = 0; q < 3; ++q)
+    for (int m = 0; m < ni; ++m) {
+      cf.c[q][m] = d[1 + q] * a0[m];
+      cf.e[q][m] = d[1 + q] * w0 * a0[m];
+      cf.L[q][m] = d[1 + q] * w0 * lam[m];
+    }
+  for (int m = 0; m < ni; ++m) { cf.a0[m] = a0[m]; cf.lam[m] = lam[m]; }
+  for (int q = 0; q < 3; ++q) {
+    cf.F0[q] = d[0] * w0 + d[1 + q] * K00;
+    cf.k0p[q] = d[1 + q] * K0p;
+  }
+  for (int q = 0; q < 4; ++q) cf.d[q] = d[q];
+  cf.K00 = K00; cf.K0p = K0p; cf.w0 = w0;
+  coef.resize(sizeof(BigCoef));
+  memcpy(coef.data(), &cf, sizeof(BigCoef));
+  dt.assign((size_t)ni * ni * 32, 0.0);
+  for (int i = 0; i < ni; ++i)
+    for (int k = 0; k < ni; ++k)
+      for (int j = 0; j < ni; ++j)
+        dt[((size_t)i * ni + k) * 32 + j] = 1.0 / (d[0] + d[1] * lam[i] + d[2] * lam[j] + d[3] * lam[k]);
+}
+
+}  // namespace sc

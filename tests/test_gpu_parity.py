@@ -365,3 +365,58 @@ def test_pcg_parity_zsegments(nseg, fused, monkeypatch):
     assert rep.converged and abs(rep.iters - res.iters) <= 1
     ref = res.x if rep.iters == res.iters else _oracle_pcg(g, op, b, 0, fixed=rep.iters).x
     assert rel(ctx.to_lattice_nodal(xt).cpu().numpy(), ref) <= 1e-10
+
+
+# ---- v4 operator (n_I >= 8): colour-scheduled one-CTA-per-element kernels -----------------
+@pytest.mark.parametrize("p,ne", [(9, (3, 2, 3)), (12, (2, 3, 2)), (16, (3, 2, 2)), (17, (2, 2, 3)),
+                                  (18, (2, 3, 2)), (20, (2, 2, 2))])
+def test_big_operator_parity(p, ne):
+    g = small_grid(p, ne, 0.8, lengths=(1.2, 0.9, 1.1))
+    op = operator.AssembledCondensedOperator(g)
+    x = lattice_random(60 + p, g.ne, g.p).ravel()
+    ctx = ctx_for(g)
+    y, _, _ = gpu_apply_nodal(ctx, x)
+    assert rel(y, op.apply(x)) <= 1e-12
+
+
+@pytest.mark.parametrize("p", [24, 32])
+def test_big_operator_matches_v1_and_is_symmetric(p):
+    """p = 24, 32 (oracle setup takes minutes there): the v4 kernels against the independent
+    one-CTA-per-element v1 kernel (oracle-pinned up to p = 16), and x . A y = y . A x."""
+    import os
+    g = small_grid(p, (3, 2, 2), 1.0, lengths=(1.0, 0.7, 1.3))
+    os.environ["SC_APPLY_V1"] = "1"
+    try:
+        c1 = ctx_for(g)
+    finally:
+        del os.environ["SC_APPLY_V1"]
+    c4 = ctx_for(g)
+    x, z = c4.skeleton(), c4.skeleton()
+    c4.sc_fill_random(3, x)
+    c4.sc_fill_random(4, z)
+    y1, y4, w4 = c1.skeleton(), c4.skeleton(fill=float("nan")), c4.skeleton()
+    c1.sc_apply_condensed(x, y1)
+    c4.sc_apply_condensed(x, y4)
+    c4.sc_apply_condensed(z, w4)
+    torch.cuda.synchronize()
+    assert float((y1 - y4).norm() / y1.norm()) <= 1e-13
+    a, b = float(torch.dot(z, y4)), float(torch.dot(x, w4))
+    assert abs(a - b) <= 1e-12 * abs(a)
+
+
+def test_big_pcg_parity():
+    from paper_1601_08179_b200 import SC_DUAL
+    g = small_grid(12, (3, 2, 2), 1.0, lengths=(1.3, 0.7, 1.5))
+    op = operator.AssembledCondensedOperator(g)
+    ctx = ctx_for(g)
+    bt = ctx.skeleton()
+    ctx.sc_fill_random(11, bt)
+    lat = ctx.lattice()
+    ctx.sc_from_transformed(bt, lat, SC_DUAL)
+    b = lat.cpu().numpy()
+    res = _oracle_pcg(g, op, b, 1e-10)
+    xt = ctx.skeleton()
+    rep = ctx.sc_pcg_solve(bt, xt, rtol=1e-10, maxit=2000)
+    assert rep.converged and abs(rep.iters - res.iters) <= 1
+    ref = res.x if rep.iters == res.iters else _oracle_pcg(g, op, b, 0, fixed=rep.iters).x
+    assert rel(ctx.to_lattice_nodal(xt).cpu().numpy(), ref) <= 1e-10
