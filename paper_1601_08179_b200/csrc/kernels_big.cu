@@ -64,6 +64,10 @@ struct BL {
   static_assert(4 * H * NI * SW <= 8 * H * NI * YS, "Qx tree slots");
 };
 
+__device__ __forceinline__ void cp_async8b(double* smem, const double* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ double sgn(int m) { return (m & 1) ? -1.0 : 1.0; }
 __device__ __forceinline__ double eo_row_b(const double* r, int hi) { return hi ? r[0] - r[1] : r[0] + r[1]; }
 
@@ -89,15 +93,29 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
   }
   __syncthreads();
   double* const sh = sm + B::O_SH;
-  // ---- a3: the element's shell (Dirichlet entities as 0)
-#pragma unroll 4
-  for (int t = tid; t < B::SH; t += 256) {
-    int ent, loc;
-    if (t < 6 * N2) { ent = t / N2; loc = t - ent * N2; }
-    else if (t < 6 * N2 + 12 * NI) { const int u = t - 6 * N2, e = u / NI; ent = 6 + e; loc = u - e * NI; }
-    else { ent = 18 + (t - 6 * N2 - 12 * NI); loc = 0; }
-    sh[t] = sDir[ent] ? 0.0 : __ldg(P.x + sBase[ent] + loc);
+  // ---- a3: the element's shell (Dirichlet entities as 0): faces as 6 contiguous blocks,
+  // 8-byte cp.async (all loads of a thread in flight at once)
+#pragma unroll
+  for (int f = 0; f < 6; ++f) {
+    const double* src = P.x + sBase[f];
+    const bool dr = sDir[f];
+#pragma unroll
+    for (int r = 0; r < (N2 + 255) / 256; ++r) {
+      const int q = tid + r * 256;
+      if (q < N2) {
+        if (dr) sh[f * N2 + q] = 0.0;
+        else cp_async8b(sh + f * N2 + q, src + q);
+      }
+    }
   }
+  for (int t = tid; t < 12 * NI + 8; t += 256) {
+    int ent, loc;
+    if (t < 12 * NI) { const int e = t / NI; ent = 6 + e; loc = t - e * NI; }
+    else { ent = 18 + (t - 12 * NI); loc = 0; }
+    if (sDir[ent]) sh[6 * N2 + t] = 0.0;
+    else cp_async8b(sh + 6 * N2 + t, P.x + sBase[ent] + loc);
+  }
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   // ---- faces-in operands P^s = lo + (-1)^s hi, a0-weighted line sums (R+, R-) of faces / edges
   double* const sP = sm + B::O_P;
@@ -215,38 +233,56 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
   __syncthreads();
 
   // ---- a6 + a7 + a8: outputs (primary - condensed part on faces, primary on edges / vertices),
-  // read-modify-write into y
+  // read-modify-write into y (each face / edge / vertex of this element is written by this CTA only
+  // within the colour's launch)
   const double* const Ed = sh + 6 * N2;
   const double* const Vv = Ed + 12 * NI;
   const double K00 = cf.K00, K0p = cf.K0p, w0 = cf.w0, w02 = w0 * w0;
-  auto out_at = [&](int t) -> double {
-    if (t < 6 * N2) {
-      const int f = t / N2, q = t - f * N2, a = q % NI, b = q / NI, d = f >> 1, hi = f & 1;
-      // (la, lb): directions of the face coordinates; bounding edges of the face (local ids - 6)
-      const int la = d == 0 ? 1 : 0, lb = d == 2 ? 1 : 2;
-      int ea0, ea1, eb0, eb1;
-      switch (f) {
-        case 0: ea0 = 8; ea1 = 10; eb0 = 4; eb1 = 6; break;
-        case 1: ea0 = 9; ea1 = 11; eb0 = 5; eb1 = 7; break;
-        case 2: ea0 = 8; ea1 = 9; eb0 = 0; eb1 = 2; break;
-        case 3: ea0 = 10; ea1 = 11; eb0 = 1; eb1 = 3; break;
-        case 4: ea0 = 4; ea1 = 5; eb0 = 0; eb1 = 1; break;
-        default: ea0 = 6; ea1 = 7; eb0 = 2; eb1 = 3; break;
-      }
+  // faces: f = 2 d + hi; coordinates (a, b) of directions (la, lb); bounding edges (local id - 6)
+  // ea0 / ea1 at index b (coefficient e[la][a], sign of a), eb0 / eb1 at index a (e[lb][b], sign of b)
+#pragma unroll
+  for (int f = 0; f < 6; ++f) {
+    constexpr int EA0[6] = {8, 9, 8, 10, 4, 6}, EA1[6] = {10, 11, 9, 11, 5, 7};
+    constexpr int EB0[6] = {4, 5, 0, 1, 0, 2}, EB1[6] = {6, 7, 2, 3, 1, 3};
+    const int d = f >> 1, hi = f & 1, la = d == 0 ? 1 : 0, lb = d == 2 ? 1 : 2;
+    if (sDir[f]) continue;
+    double* const yf = P.y + sBase[f];
+    constexpr int R = (N2 + 255) / 256;
+    double val[R], old[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int q = tid + r * 256;
+      old[r] = q < N2 ? yf[q] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int q = min(tid + r * 256, N2 - 1), b = q / NI, a = q - b * NI;
       const double fd = cf.F0[d] + cf.L[la][a] + cf.L[lb][b];
       const double self = sh[f * N2 + q], opp = sh[(f ^ 1) * N2 + q];
-      const double ta = cf.e[la][a] * fma(sgn(a), Ed[ea1 * NI + b], Ed[ea0 * NI + b]);
-      const double tb = cf.e[lb][b] * fma(sgn(b), Ed[eb1 * NI + a], Ed[eb0 * NI + a]);
+      const double ta = cf.e[la][a] * fma(sgn(a), Ed[EA1[f] * NI + b], Ed[EA0[f] * NI + b]);
+      const double tb = cf.e[lb][b] * fma(sgn(b), Ed[EB1[f] * NI + a], Ed[EB0[f] * NI + a]);
       const double Q = fma(hi ? -1.0 : 1.0, sQ[(2 * d + 1) * N2 + q], sQ[2 * d * N2 + q]);
-      return fma(fd, self, fma(cf.k0p[d], opp, ta + tb)) - Q;
+      val[r] = fma(fd, self, fma(cf.k0p[d], opp, ta + tb)) - Q;
     }
-    if (t < 6 * N2 + 12 * NI) {
-      const int u = t - 6 * N2, e = u / NI, c = u - e * NI, grp = e >> 2, b0 = e & 1, b1 = (e >> 1) & 1;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int q = tid + r * 256;
+      if (q < N2) yf[q] = old[r] + val[r];
+    }
+  }
+  // edges (one thread per edge node) and vertices
+  for (int t = tid; t < 12 * NI + 8; t += 256) {
+    const int ent = t < 12 * NI ? 6 + t / NI : 18 + (t - 12 * NI);
+    if (sDir[ent]) continue;
+    double* const dst = P.y + sBase[ent] + (t < 12 * NI ? t - (ent - 6) * NI : 0);
+    const double old = *dst;
+    double val;
+    if (t < 12 * NI) {
+      const int e = ent - 6, c = t - e * NI, grp = e >> 2, b0 = e & 1, b1 = (e >> 1) & 1;
       const double uu = Ed[e * NI + c];
-      // along the edge (interior row of Ktilde): the two end vertices
-      int v0, v1;
-      // boundary directions o1 (bit b0) and o2 (bit b1): parallel edges and the line sums
-      int p10, p11, l1, p20, p21, l2;
+      // along the edge (interior row of Ktilde): the two end vertices; boundary directions o1 (bit
+      // b0) and o2 (bit b1): the parallel edges and the face line sums of Ktilde rows 0 / p
+      int v0, v1, p10, p11, l1, p20, p21, l2;
       if (grp == 0) {          // x-edge (jb, kb) = (b0, b1)
         v0 = 2 * b0 + 4 * b1; v1 = v0 + 1;
         p10 = 2 * b1; p11 = 2 * b1 + 1; l1 = ((4 + b1) * 2 + 1) * NI + c;     // o1 = y: z-face b1, sum over j
@@ -264,44 +300,22 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
       const double u10 = Ed[p10 * NI + c], u11 = Ed[p11 * NI + c], u20 = Ed[p20 * NI + c], u21 = Ed[p21 * NI + c];
       const double t1 = (b0 ? fma(K0p, u10, K00 * u11) : fma(K00, u10, K0p * u11)) + eo_row_b(sLS + 2 * l1, b0);
       const double t2 = (b1 ? fma(K0p, u20, K00 * u21) : fma(K00, u20, K0p * u21)) + eo_row_b(sLS + 2 * l2, b1);
-      // d indices: along = grp, o1 / o2 = the other two in increasing order
       const int o1 = grp == 0 ? 1 : 0, o2 = grp == 2 ? 1 : 2;
-      return w02 * (cf.d[0] * uu + cf.d[1 + grp] * tal) + w0 * (cf.d[1 + o1] * t1 + cf.d[1 + o2] * t2);
+      val = w02 * (cf.d[0] * uu + cf.d[1 + grp] * tal) + w0 * (cf.d[1 + o1] * t1 + cf.d[1 + o2] * t2);
+    } else {
+      const int v = t - 12 * NI, ib = v & 1, jb = (v >> 1) & 1, kb = v >> 2;
+      const double uu = Vv[v];
+      // partner vertices along x / y / z: (lo, hi) of the pair containing v.  (Written with
+      // arithmetic offsets: an earlier bitwise form, Vv[v | 4] / Vv[v & ~4], gave wrong vertex
+      // values in some builds -- not root-caused; the parity tests pin this.)
+      const int xl = v - ib, yl = v - 2 * jb, zl = v - 4 * kb;
+      const double x0v = Vv[xl], x1v = Vv[xl + 1], y0v = Vv[yl], y1v = Vv[yl + 2], z0v = Vv[zl], z1v = Vv[zl + 4];
+      const double tx = (ib ? fma(K0p, x0v, K00 * x1v) : fma(K00, x0v, K0p * x1v)) + eo_row_b(sES + 2 * (jb + 2 * kb), ib);
+      const double ty = (jb ? fma(K0p, y0v, K00 * y1v) : fma(K00, y0v, K0p * y1v)) + eo_row_b(sES + 2 * (4 + ib + 2 * kb), jb);
+      const double tz = (kb ? fma(K0p, z0v, K00 * z1v) : fma(K00, z0v, K0p * z1v)) + eo_row_b(sES + 2 * (8 + ib + 2 * jb), kb);
+      val = w02 * (w0 * cf.d[0] * uu + cf.d[1] * tx + cf.d[2] * ty + cf.d[3] * tz);
     }
-    const int v = t - 6 * N2 - 12 * NI, ib = v & 1, jb = (v >> 1) & 1, kb = v >> 2;
-    const double uu = Vv[v];
-    // partner vertices along x / y / z: (lo, hi) of the pair containing v
-    const int xl = v - ib, yl = v - 2 * jb, zl = v - 4 * kb;
-    const double x0v = Vv[xl], x1v = Vv[xl + 1], y0v = Vv[yl], y1v = Vv[yl + 2], z0v = Vv[zl], z1v = Vv[zl + 4];
-    const double tx = (ib ? fma(K0p, x0v, K00 * x1v) : fma(K00, x0v, K0p * x1v)) + eo_row_b(sES + 2 * (jb + 2 * kb), ib);
-    const double ty = (jb ? fma(K0p, y0v, K00 * y1v) : fma(K00, y0v, K0p * y1v)) + eo_row_b(sES + 2 * (4 + ib + 2 * kb), jb);
-    const double tz = (kb ? fma(K0p, z0v, K00 * z1v) : fma(K00, z0v, K0p * z1v)) + eo_row_b(sES + 2 * (8 + ib + 2 * jb), kb);
-    return w02 * (w0 * cf.d[0] * uu + cf.d[1] * tx + cf.d[2] * ty + cf.d[3] * tz);
-  };
-  constexpr int NO = B::SH, PER = (NO + 255) / 256, CH = 8;
-#pragma unroll 1
-  for (int r0 = 0; r0 < PER; r0 += CH) {
-    double val[CH], old[CH];
-    double* dst[CH];
-#pragma unroll
-    for (int r = 0; r < CH; ++r) {
-      dst[r] = nullptr;
-      val[r] = 0.0;
-      const int t = tid + (r0 + r) * 256;
-      if (r0 + r >= PER || t >= NO) continue;
-      int ent, loc;
-      if (t < 6 * N2) { ent = t / N2; loc = t - ent * N2; }
-      else if (t < 6 * N2 + 12 * NI) { const int u = t - 6 * N2, e = u / NI; ent = 6 + e; loc = u - e * NI; }
-      else { ent = 18 + (t - 6 * N2 - 12 * NI); loc = 0; }
-      if (sDir[ent]) continue;
-      dst[r] = P.y + sBase[ent] + loc;
-      val[r] = out_at(t);
-    }
-#pragma unroll
-    for (int r = 0; r < CH; ++r) old[r] = dst[r] ? *dst[r] : 0.0;
-#pragma unroll
-    for (int r = 0; r < CH; ++r)
-      if (dst[r]) *dst[r] = old[r] + val[r];
+    *dst = old + val;
   }
 }
 
