@@ -79,9 +79,17 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
   extern __shared__ double sm[];
   __shared__ long long sBase[26];
   __shared__ int sDir[26];
+  // lane-divergent coefficient lookups go through shared memory (the constant bank serialises
+  // them): L[3][32], e[3][32], a0[32], lam[32]
+  __shared__ double sT[256];
   const Geom& g = P.g;
   const BigCoef& cf = P.cf;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  sT[tid] = tid < 96 ? (&cf.L[0][0])[tid] : tid < 192 ? (&cf.e[0][0])[tid - 96] : tid < 224 ? cf.a0[tid - 192] : cf.lam[tid - 224];
+  const double* const sLt = sT;
+  const double* const sEt = sT + 96;
+  const double* const sA0t = sT + 192;
+  const double* const sLamt = sT + 224;
   const int cx = colour & 1, cy = (colour >> 1) & 1, cz = colour >> 2;
   const int ncx = (g.nx - cx + 1) >> 1, ncy = (g.ny - cy + 1) >> 1;
   const int bid = blockIdx.x;
@@ -257,10 +265,10 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int q = min(tid + r * 256, N2 - 1), b = q / NI, a = q - b * NI;
-      const double fd = cf.F0[d] + cf.L[la][a] + cf.L[lb][b];
+      const double fd = cf.F0[d] + sLt[la * 32 + a] + sLt[lb * 32 + b];
       const double self = sh[f * N2 + q], opp = sh[(f ^ 1) * N2 + q];
-      const double ta = cf.e[la][a] * fma(sgn(a), Ed[EA1[f] * NI + b], Ed[EA0[f] * NI + b]);
-      const double tb = cf.e[lb][b] * fma(sgn(b), Ed[EB1[f] * NI + a], Ed[EB0[f] * NI + a]);
+      const double ta = sEt[la * 32 + a] * fma(sgn(a), Ed[EA1[f] * NI + b], Ed[EA0[f] * NI + b]);
+      const double tb = sEt[lb * 32 + b] * fma(sgn(b), Ed[EB1[f] * NI + a], Ed[EB0[f] * NI + a]);
       const double Q = fma(hi ? -1.0 : 1.0, sQ[(2 * d + 1) * N2 + q], sQ[2 * d * N2 + q]);
       val[r] = fma(fd, self, fma(cf.k0p[d], opp, ta + tb)) - Q;
     }
@@ -296,7 +304,7 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
         p10 = 8 + 2 * b1; p11 = 9 + 2 * b1; l1 = ((2 + b1) * 2 + 0) * NI + c;  // o1 = x: y-face b1, sum over i
         p20 = 8 + b0; p21 = 10 + b0; l2 = (b0 * 2 + 0) * NI + c;               // o2 = y: x-face b0, sum over j
       }
-      const double tal = cf.a0[c] * fma(sgn(c), Vv[v1], Vv[v0]) + cf.lam[c] * uu;
+      const double tal = sA0t[c] * fma(sgn(c), Vv[v1], Vv[v0]) + sLamt[c] * uu;
       const double u10 = Ed[p10 * NI + c], u11 = Ed[p11 * NI + c], u20 = Ed[p20 * NI + c], u21 = Ed[p21 * NI + c];
       const double t1 = (b0 ? fma(K0p, u10, K00 * u11) : fma(K00, u10, K0p * u11)) + eo_row_b(sLS + 2 * l1, b0);
       const double t2 = (b1 ? fma(K0p, u20, K00 * u21) : fma(K00, u20, K0p * u21)) + eo_row_b(sLS + 2 * l2, b1);
