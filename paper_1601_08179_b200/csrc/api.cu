@@ -69,7 +69,9 @@ struct sc_ctx {
   double* d_dinv = nullptr;             // uniform D^{-1} table
   // v3 tile-column operator state (kernels_col.cu)
   bool use_col = false;
-  bool use_big = false;                 // v4 colour-scheduled element operator (n_I >= 8, uniform geometry)
+  bool use_big = false;
+  bool use_ptab = false;                // PCG reads Pinv from the per-class table (uniform geometry)
+  PinvTab ptab;                 // v4 colour-scheduled element operator (n_I >= 8, uniform geometry)
   std::vector<unsigned char> big_coef;
   double* d_big_dt = nullptr;           // its D^{-1} table [i][k][32]
   std::vector<unsigned char> col_coef;  // kernel-parameter coefficient block
@@ -394,8 +396,9 @@ extern "C" size_t sc_workspace_bytes(const sc_ctx* ctx) {
   if (!ctx) return 0;
   long long n = ctx->g.n_total;
   long long n3 = (long long)(ctx->g.p + 1) * (ctx->g.p + 1) * (ctx->g.p + 1);
+  const long long ntab = 3LL * ctx->g.ni * ctx->g.ni + 3LL * ctx->g.ni + 1;
   long long tot = 6 * n + align_up(SCAL_COUNT) + align_up(4 * SC_RED_BLOCKS) + 4 * align_up(ctx->plane_len) +
-                  kScratchCtas * 2 * n3;
+                  align_up(ntab) + kScratchCtas * 2 * n3;
   return (size_t)tot * sizeof(double);
 }
 
@@ -418,6 +421,8 @@ extern "C" sc_status sc_bind_workspace(sc_ctx* ctx, void* d_ws, size_t bytes) {
   ctx->scal = w; w += align_up(SCAL_COUNT);
   ctx->partials = w; w += align_up(4 * SC_RED_BLOCKS);
   ctx->halo = w; w += 4 * align_up(ctx->plane_len);
+  double* const ptab = w;
+  w += align_up(3LL * ctx->g.ni * ctx->g.ni + 3LL * ctx->g.ni + 1);
   ctx->scratch = w;
   long long n3 = (long long)(ctx->g.p + 1) * (ctx->g.p + 1) * (ctx->g.p + 1);
   ctx->scratch_elems = kScratchCtas * 2 * n3;
@@ -429,6 +434,43 @@ extern "C" sc_status sc_bind_workspace(sc_ctx* ctx, void* d_ws, size_t bytes) {
   sc_status s = halo_sum(ctx, ctx->pinv, st);
   if (s != SC_OK) return s;
   LAUNCH(launch_invert_diag(ctx->g, ctx->pinv, st, &nl_));
+  // uniform geometry: Pinv per (entity class, index in the entity) from one non-Dirichlet
+  // representative of each class (all of them share the value; classes without one are all
+  // Dirichlet, where r = 0)
+  ctx->use_ptab = false;
+  const char* pv_env = getenv("SC_PINV_VECTOR");
+  if (ctx->g.uniform && !(pv_env && pv_env[0] == '1')) {
+    const Geom& g = ctx->g;
+    const int ni = g.ni, n2 = ni * ni, nx = g.nx, ny = g.ny, nz = g.nz;
+    int fzf = -1;                                   // a non-Dirichlet z-plane
+    for (int fz = 0; fz <= nz && fzf < 0; ++fz)
+      if (!((fz == 0 && g.dir_bot) || (fz == nz && g.dir_top))) fzf = fz;
+    const bool ix = nx >= 2, iy = ny >= 2;
+    PinvTab& T = ctx->ptab;
+    const long long ent[7] = {
+        ix ? g.off_f[0] + (1LL) * n2 : -1,                                                        // x-face (1, 0, 0)
+        iy ? g.off_f[1] + ((long long)nx * 1) * n2 : -1,                                          // y-face (0, 1, 0)
+        fzf >= 0 ? g.off_f[2] + ((long long)nx * ny * fzf) * n2 : -1,                            // z-face (0, 0, fzf)
+        (iy && fzf >= 0) ? g.off_e[0] + ((long long)nx * (1 + (long long)(ny + 1) * fzf)) * ni : -1,   // x-edge
+        (ix && fzf >= 0) ? g.off_e[1] + (1 + (long long)(nx + 1) * ny * fzf) * ni : -1,            // y-edge
+        (ix && iy) ? g.off_e[2] + (1 + (long long)(nx + 1) * 1) * ni : -1,                        // z-edge (1, 1, 0)
+        (ix && iy && fzf >= 0) ? g.off_v + 1 + (long long)(nx + 1) * (1 + (long long)(ny + 1) * fzf) : -1};
+    const long long lens[7] = {g.n_f[0] * n2, g.n_f[1] * n2, g.n_f[2] * n2, g.n_e[0] * ni, g.n_e[1] * ni,
+                               g.n_e[2] * ni, g.n_v};
+    const long long offs[7] = {g.off_f[0], g.off_f[1], g.off_f[2], g.off_e[0], g.off_e[1], g.off_e[2], g.off_v};
+    const int per[7] = {n2, n2, n2, ni, ni, ni, 1};
+    int base = 0;
+    for (int c = 0; c < 7; ++c) {
+      T.off[c] = offs[c]; T.len[c] = lens[c]; T.n[c] = per[c]; T.base[c] = base;
+      if (ent[c] >= 0)
+        CK(cudaMemcpyAsync(ptab + base, ctx->pinv + ent[c], sizeof(double) * per[c], cudaMemcpyDeviceToDevice, st));
+      else
+        CK(cudaMemsetAsync(ptab + base, 0, sizeof(double) * per[c], st));
+      base += per[c];
+    }
+    T.tab = ptab;
+    ctx->use_ptab = true;
+  }
   CK(cudaStreamSynchronize(st));
   return SC_OK;
 }
@@ -550,11 +592,17 @@ static sc_status pcg_iteration(sc_ctx* ctx, cudaStream_t st) {
   }
   if ((s = allreduce_scal(ctx, SCAL_RED0, 1, st))) return s;
   LAUNCH(launch_pcg_alpha(ctx->scal, st, &nl_));
-  LAUNCH(launch_pcg_update(ctx->r, ctx->q, ctx->pinv, n, ctx->own, ctx->scal, ctx->partials, st, &nl_));
+  if (ctx->use_ptab)
+    LAUNCH(launch_pcg_update_tab(ctx->r, ctx->q, ctx->ptab, ctx->own, ctx->scal, ctx->partials, st, &nl_));
+  else
+    LAUNCH(launch_pcg_update(ctx->r, ctx->q, ctx->pinv, n, ctx->own, ctx->scal, ctx->partials, st, &nl_));
   LAUNCH(launch_reduce2(ctx->partials, ctx->scal, SCAL_RED0, 2, done, st, &nl_));
   if ((s = allreduce_scal(ctx, SCAL_RED0, 2, st))) return s;
   LAUNCH(launch_pcg_beta(ctx->scal, st, &nl_));
-  LAUNCH(launch_pcg_direction(x, ctx->pv, ctx->r, ctx->pinv, n, ctx->scal, ctx->it_enq, st, &nl_));
+  if (ctx->use_ptab)
+    LAUNCH(launch_pcg_direction_tab(x, ctx->pv, ctx->r, ctx->ptab, ctx->scal, ctx->it_enq, st, &nl_));
+  else
+    LAUNCH(launch_pcg_direction(x, ctx->pv, ctx->r, ctx->pinv, n, ctx->scal, ctx->it_enq, st, &nl_));
   ctx->it_enq++;
   return SC_OK;
 }

@@ -107,6 +107,56 @@ __global__ void k_pcg_direction(double* __restrict__ x, double* __restrict__ p, 
   }
 }
 
+// Table-Pinv variants (uniform geometry): entries are visited class by class (faces x/y/z, edges
+// x/y/z, vertices), each thread keeping its index inside the entity incrementally (the grid
+// stride S is fixed), so Pinv costs a cached table load instead of an 8-byte stream per entry.
+// r -= alpha q ; z = Pinv r ; partials [r.z | r.r]   (3 streams: r, q read; r written)
+__global__ void k_pcg_update_tab(double* __restrict__ r, const double* __restrict__ q, PinvTab T, OwnMask m,
+                                 const double* __restrict__ scal, double* __restrict__ partials) {
+  if (scal[SCAL_DONE] != 0.0) return;
+  const double alpha = scal[SCAL_ALPHA];
+  const long long S = (long long)gridDim.x * blockDim.x, g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  double v[2] = {0.0, 0.0};
+  for (int c = 0; c < 7; ++c) {
+    const int nc = T.n[c], step = (int)(S % nc);
+    const double* tb = T.tab + T.base[c];
+    int loc = (int)(g % nc);
+    const long long end = T.off[c] + T.len[c];
+    for (long long i = T.off[c] + g; i < end; i += S) {
+      const double ri = r[i] - alpha * q[i];
+      r[i] = ri;
+      const double zi = __ldg(tb + loc) * ri;
+      if (owned(i, m)) { v[0] += ri * zi; v[1] += ri * ri; }
+      loc += step;
+      if (loc >= nc) loc -= nc;
+    }
+  }
+  block_sum<2>(v);
+  if (threadIdx.x == 0) { partials[blockIdx.x] = v[0]; partials[SC_RED_BLOCKS + blockIdx.x] = v[1]; }
+}
+
+// x += alpha p ; p = Pinv r + beta p unless converged   (5 streams: x, p, r read; x, p written)
+__global__ void k_pcg_direction_tab(double* __restrict__ x, double* __restrict__ p, const double* __restrict__ r,
+                                    PinvTab T, const double* __restrict__ scal, long long it) {
+  if (scal[SCAL_ITERS] != (double)(it + 1) || scal[SCAL_BREAK] != 0.0) return;
+  const double alpha = scal[SCAL_ALPHA], beta = scal[SCAL_BETA];
+  const bool dir = scal[SCAL_DONE] == 0.0;
+  const long long S = (long long)gridDim.x * blockDim.x, g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (int c = 0; c < 7; ++c) {
+    const int nc = T.n[c], step = (int)(S % nc);
+    const double* tb = T.tab + T.base[c];
+    int loc = (int)(g % nc);
+    const long long end = T.off[c] + T.len[c];
+    for (long long i = T.off[c] + g; i < end; i += S) {
+      const double pi = p[i];
+      x[i] += alpha * pi;
+      if (dir) p[i] = __ldg(tb + loc) * r[i] + beta * pi;
+      loc += step;
+      if (loc >= nc) loc -= nc;
+    }
+  }
+}
+
 // Fixed-order second stage: scal[slot0 + v] = sum_b partials[v * SC_RED_BLOCKS + b].
 __global__ void k_reduce2(const double* __restrict__ partials, double* __restrict__ scal, int slot0, int nvals,
                           const double* __restrict__ done) {
@@ -220,6 +270,20 @@ int launch_pcg_beta(double* scal, void* stream, int* nl) {
 int launch_pcg_direction(double* x, double* p, const double* r, const double* pinv, long long n, const double* scal,
                          long long it, void* stream, int* nl) {
   k_pcg_direction<<<SC_RED_BLOCKS, VEC_THREADS, 0, (cudaStream_t)stream>>>(x, p, r, pinv, n, scal, it);
+  (*nl)++;
+  return cudaGetLastError();
+}
+
+int launch_pcg_update_tab(double* r, const double* q, const PinvTab& T, OwnMask m, const double* scal,
+                          double* partials, void* stream, int* nl) {
+  k_pcg_update_tab<<<SC_RED_BLOCKS, VEC_THREADS, 0, (cudaStream_t)stream>>>(r, q, T, m, scal, partials);
+  (*nl)++;
+  return cudaGetLastError();
+}
+
+int launch_pcg_direction_tab(double* x, double* p, const double* r, const PinvTab& T, const double* scal, long long it,
+                             void* stream, int* nl) {
+  k_pcg_direction_tab<<<SC_RED_BLOCKS, VEC_THREADS, 0, (cudaStream_t)stream>>>(x, p, r, T, scal, it);
   (*nl)++;
   return cudaGetLastError();
 }

@@ -81,6 +81,11 @@ int launch_recover(const Geom& g, const double* f, const double* x, double* u, d
 // PCG vector kernels (kernels_vec.cu). `own_lo/own_hi`: [lo, hi) skeleton ranges excluded
 // from dot products (interface plane owned by the lower rank), up to 4 ranges.
 struct OwnMask { long long lo[4], hi[4]; int n; };
+// Uniform geometry: the assembled diagonal (hence Pinv) of every non-Dirichlet entry depends only
+// on its entity class (x/y/z faces, x/y/z edges, vertices) and its index inside the entity, so the
+// PCG kernels read Pinv from a small table instead of streaming an N_c vector.  Dirichlet and
+// padding entries of r are 0, so the table value there is irrelevant.
+struct PinvTab { long long off[7], len[7]; int n[7], base[7]; const double* tab; };
 int launch_dot_partial(const double* a, const double* b, long long n, OwnMask m, double* partials,
                        const double* done, void* stream, int* nlaunch);
 int launch_reduce_partials(const double* partials, int nparts, double* out, const double* done,
@@ -89,6 +94,10 @@ int launch_pcg_init(const double* b, const double* pinv, double* x, double* r, d
                     OwnMask m, double* partials, void* stream, int* nlaunch);
 int launch_pcg_init_finalize(double* scal, const double* partials, double tol2, int maxit, void* stream, int* nlaunch);
 int launch_pcg_alpha(double* scal, void* stream, int* nlaunch);
+int launch_pcg_update_tab(double* r, const double* q, const PinvTab& T, OwnMask m, const double* scal,
+                          double* partials, void* stream, int* nlaunch);
+int launch_pcg_direction_tab(double* x, double* p, const double* r, const PinvTab& T, const double* scal, long long it,
+                             void* stream, int* nlaunch);
 int launch_pcg_update(double* r, const double* q, const double* pinv, long long n, OwnMask m, const double* scal,
                       double* partials, void* stream, int* nlaunch);
 int launch_pcg_beta(double* scal, void* stream, int* nlaunch);
