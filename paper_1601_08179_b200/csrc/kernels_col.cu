@@ -406,12 +406,18 @@ __device__ __forceinline__ double eo_row(const double* r, int hi) { return hi ? 
 __device__ __forceinline__ void seg_out(double* __restrict__ dst, const double* __restrict__ s, int a, int b, int mode,
                                         int lane) {
   if (mode == 1) {
-    int t = a + lane;
-    for (; t + 96 < b; t += 128) {   // four independent loads in flight before the stores
-      const double v0 = s[t], v1 = s[t + 32], v2 = s[t + 64], v3 = s[t + 96];
-      dst[t] = v0; dst[t + 32] = v1; dst[t + 64] = v2; dst[t + 96] = v3;
+    // 4 predicated loads in flight before the stores; one pass covers any segment of <= 128
+    // entries (most segments: face / edge ends and edge rows), no scalar tail loop
+    const double* sp = s + a + lane;
+    double* dp = dst + a + lane;
+    for (int n = b - a - lane; n > 0; n -= 128, sp += 128, dp += 128) {
+      const double v0 = sp[0];
+      const double v1 = n > 32 ? sp[32] : 0.0, v2 = n > 64 ? sp[64] : 0.0, v3 = n > 96 ? sp[96] : 0.0;
+      dp[0] = v0;
+      if (n > 32) dp[32] = v1;
+      if (n > 64) dp[64] = v2;
+      if (n > 96) dp[96] = v3;
     }
-    for (; t < b; t += 32) dst[t] = s[t];
   } else if (mode == 2) {
     for (int t = a + lane; t < b; t += 32) dst[t] = 0.0;
   }
