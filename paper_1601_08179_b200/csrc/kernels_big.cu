@@ -123,6 +123,32 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
     if (sDir[ent]) sh[6 * N2 + t] = 0.0;
     else cp_async8b(sh + 6 * N2 + t, P.x + sBase[ent] + loc);
   }
+  // n_I > 16 (one CTA per SM): the old values of y at this element's outputs (read-modify-write
+  // at the end) are loaded now, so their latency overlaps the whole element (no other CTA of
+  // this colour touches them).  n_I <= 16 keeps the registers for occupancy (3 CTAs per SM) and
+  // loads them in the output phase.
+  constexpr bool EARLY = NI > 16;
+  constexpr int RF = (N2 + 255) / 256, RE = (12 * NI + 8 + 255) / 256;
+  double yold[6][RF], yoldE[RE];
+  auto load_yold = [&]() {
+#pragma unroll
+    for (int f = 0; f < 6; ++f)
+#pragma unroll
+      for (int r = 0; r < RF; ++r) {
+        const int q = tid + r * 256;
+        yold[f][r] = (q < N2 && !sDir[f]) ? P.y[sBase[f] + q] : 0.0;
+      }
+#pragma unroll
+    for (int r = 0; r < RE; ++r) {
+      const int t = tid + r * 256;
+      yoldE[r] = 0.0;
+      if (t < 12 * NI + 8) {
+        const int ent = t < 12 * NI ? 6 + t / NI : 18 + (t - 12 * NI);
+        if (!sDir[ent]) yoldE[r] = P.y[sBase[ent] + (t < 12 * NI ? t - (ent - 6) * NI : 0)];
+      }
+    }
+  };
+  if constexpr (EARLY) load_yold();
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   // ---- faces-in operands P^s = lo + (-1)^s hi, a0-weighted line sums (R+, R-) of faces / edges
@@ -246,6 +272,7 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
   const double* const Ed = sh + 6 * N2;
   const double* const Vv = Ed + 12 * NI;
   const double K00 = cf.K00, K0p = cf.K0p, w0 = cf.w0, w02 = w0 * w0;
+  if constexpr (!EARLY) load_yold();
   // faces: f = 2 d + hi; coordinates (a, b) of directions (la, lb); bounding edges (local id - 6)
   // ea0 / ea1 at index b (coefficient e[la][a], sign of a), eb0 / eb1 at index a (e[lb][b], sign of b)
 #pragma unroll
@@ -255,13 +282,8 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
     const int d = f >> 1, hi = f & 1, la = d == 0 ? 1 : 0, lb = d == 2 ? 1 : 2;
     if (sDir[f]) continue;
     double* const yf = P.y + sBase[f];
-    constexpr int R = (N2 + 255) / 256;
-    double val[R], old[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int q = tid + r * 256;
-      old[r] = q < N2 ? yf[q] : 0.0;
-    }
+    constexpr int R = RF;
+    double val[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int q = min(tid + r * 256, N2 - 1), b = q / NI, a = q - b * NI;
@@ -275,15 +297,18 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int q = tid + r * 256;
-      if (q < N2) yf[q] = old[r] + val[r];
+      if (q < N2) yf[q] = yold[f][r] + val[r];
     }
   }
   // edges (one thread per edge node) and vertices
-  for (int t = tid; t < 12 * NI + 8; t += 256) {
+#pragma unroll
+  for (int rr = 0; rr < RE; ++rr) {
+    const int t = tid + rr * 256;
+    if (t >= 12 * NI + 8) continue;
     const int ent = t < 12 * NI ? 6 + t / NI : 18 + (t - 12 * NI);
     if (sDir[ent]) continue;
     double* const dst = P.y + sBase[ent] + (t < 12 * NI ? t - (ent - 6) * NI : 0);
-    const double old = *dst;
+    const double old = yoldE[rr];
     double val;
     if (t < 12 * NI) {
       const int e = ent - 6, c = t - e * NI, grp = e >> 2, b0 = e & 1, b1 = (e >> 1) & 1;

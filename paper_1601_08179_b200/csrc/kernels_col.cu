@@ -210,15 +210,14 @@ __device__ __forceinline__ void cp8(unsigned s, const double* g) {
 __device__ __forceinline__ void row_load(double* sb, const double* gb, int len, int zlo, int zhi, int lane) {
   for (int t = lane; t < zlo; t += 32) sb[t] = 0.0;
   for (int t = zhi + lane; t < len; t += 32) sb[t] = 0.0;
-  const unsigned s = (unsigned)__cvta_generic_to_shared(sb);
-  int t = zlo + lane;
-  for (; t + 96 < zhi; t += 128) {
-    cp8(s + 8u * t, gb + t);
-    cp8(s + 8u * (t + 32), gb + t + 32);
-    cp8(s + 8u * (t + 64), gb + t + 64);
-    cp8(s + 8u * (t + 96), gb + t + 96);
+  unsigned s = (unsigned)__cvta_generic_to_shared(sb + zlo + lane);
+  const double* gp = gb + zlo + lane;
+  for (int n = zhi - zlo - lane; n > 0; n -= 128, s += 1024u, gp += 128) {   // predicated 4-wide, no tail loop
+    cp8(s, gp);
+    if (n > 32) cp8(s + 256u, gp + 32);
+    if (n > 64) cp8(s + 512u, gp + 64);
+    if (n > 96) cp8(s + 768u, gp + 96);
   }
-  for (; t < zhi; t += 32) cp8(s + 8u * t, gb + t);
 }
 
 // Row descriptors of a tile (built once per work item, shared memory).  Rows of the side
