@@ -156,7 +156,11 @@ static sc_status layout_compute(const sc_params* prm, bool need_comm, Geom& g, s
   if (!std::isfinite(prm->lambda) || prm->lambda < 0) return SC_EINVAL;
   if (prm->nranks < 1 || prm->rank < 0 || prm->rank >= prm->nranks) return SC_EINVAL;
   if (prm->nranks > prm->ne[2]) return SC_EINVAL;
-  if (need_comm && prm->nranks > 1 && !prm->nccl_comm) return SC_EINVAL;
+  // SC_TEST_LOCAL_SLAB=1 (tests only): a rank's slab without a communicator -- the operator
+  // then returns the slab's local partial sums on its interface planes (no halo exchange) and
+  // dots are rank-local, which is what the single-GPU slab parity tests compare against
+  const char* ls = getenv("SC_TEST_LOCAL_SLAB");
+  if (need_comm && prm->nranks > 1 && !prm->nccl_comm && !(ls && ls[0] == '1')) return SC_EINVAL;
   const int ni = p - 1;
   // slab partition: rank r owns element layers [z0, z1) (balanced, contiguous)
   const int nzg = prm->ne[2], R = prm->nranks, r = prm->rank;
@@ -506,7 +510,7 @@ extern "C" sc_status sc_basis_1d_host(int p, double* lam, double* a0, double* ap
 // exchange them with the z-neighbours and add (P:107-109 gather across the slab cut).
 static sc_status halo_sum(sc_ctx* ctx, double* y, cudaStream_t st) {
   const int R = ctx->prm.nranks, r = ctx->prm.rank;
-  if (R == 1) return SC_OK;
+  if (R == 1 || !ctx->comm) return SC_OK;   // no communicator: SC_TEST_LOCAL_SLAB (local partials)
   if (!ctx->halo) { ctx->err = "workspace not bound (needed for the halo exchange)"; return SC_ESTATE; }
   const long long pl = align_up(ctx->plane_len);
   double* recv_lo = ctx->halo;
@@ -530,7 +534,7 @@ static sc_status halo_sum(sc_ctx* ctx, double* y, cudaStream_t st) {
 }
 
 static sc_status allreduce_scal(sc_ctx* ctx, int slot, int n, cudaStream_t st) {
-  if (ctx->prm.nranks == 1) return SC_OK;
+  if (ctx->prm.nranks == 1 || !ctx->comm) return SC_OK;
   NK(g_nccl.AllReduce(ctx->scal + slot, ctx->scal + slot, (size_t)n, ncclDouble, ncclSum, ctx->comm, st));
   return SC_OK;
 }

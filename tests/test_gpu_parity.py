@@ -420,3 +420,26 @@ def test_big_pcg_parity():
     assert rep.converged and abs(rep.iters - res.iters) <= 1
     ref = res.x if rep.iters == res.iters else _oracle_pcg(g, op, b, 0, fixed=rep.iters).x
     assert rel(ctx.to_lattice_nodal(xt).cpu().numpy(), ref) <= 1e-10
+
+
+# ---- z-slab ranks on one GPU (SC_TEST_LOCAL_SLAB: no communicator, the operator returns the
+# slab's local partial sums on its interface planes): every kernel family against the oracle's
+# slab operator with non-Dirichlet interface planes (the multi-GPU path before the NCCL halo sum)
+@pytest.mark.parametrize("p,ne,R", [(3, (10, 7, 5), 2), (6, (9, 5, 4), 2), (8, (9, 6, 7), 3), (12, (3, 2, 4), 2)])
+def test_slab_rank_operator_parity(p, ne, R, monkeypatch):
+    import copy
+    from paper_1601_08179_b200 import Context
+    monkeypatch.setenv("SC_TEST_LOCAL_SLAB", "1")
+    g = small_grid(p, ne, 0.9, lengths=(1.2, 0.8, 1.1))
+    for r in range(R):
+        ctx = Context(g.p, g.ne, (g.hx, g.hy, g.hz), g.lam, device=0, rank=r, nranks=R)
+        z0, z1 = ctx.layout.z_begin, ctx.layout.z_end
+        gs = copy.deepcopy(g)
+        gs.ne = (g.ne[0], g.ne[1], z1 - z0)
+        gs.hz = g.hz[z0:z1]
+        gs.extra = dict(g.extra, dirichlet_z=(r == 0, r == R - 1))
+        xg = lattice_random(70 + p, g.ne, g.p)
+        xs = np.ascontiguousarray(xg[z0 * p:z1 * p + 1])
+        ref = operator.AssembledCondensedOperator(gs).apply(xs.ravel())
+        y, _, _ = gpu_apply_nodal(ctx, xs.ravel())
+        assert rel(y, ref) <= 1e-12, (r, z0, z1)
