@@ -71,9 +71,10 @@ struct CS {
   static constexpr int N2 = NI * NI;
   static constexpr int NT = 256;                      // 8 warps = 8 parity classes
   // tile: 8 x 4 elements (one per lane, a parity class per warp) for n_I >= 4; for n_I <= 3
-  // one element per thread (all classes in the thread) on larger tiles
+  // one element per thread (all classes in the thread) on larger tiles: 16 x 16 (n_I = 1),
+  // 16 x 8 (n_I = 2, 3; the largest that fits the shared-memory budget at n_I = 3)
   static constexpr bool PER_ELEM = NI <= 3;
-  static constexpr int TX = NI <= 2 ? 16 : 8, TY = NI == 1 ? 16 : (NI <= 3 ? 8 : 4), NE = TX * TY;
+  static constexpr int TX = NI <= 3 ? 16 : 8, TY = NI == 1 ? 16 : (NI <= 3 ? 8 : 4), NE = TX * TY;
   static constexpr int MAXROWS = 7 * TY + 4;          // row descriptors per tile
   static constexpr int XF = TY * (TX + 1) * N2;
   static constexpr int YF = (TY + 1) * TX * N2;
