@@ -59,6 +59,8 @@ def build(verbose=False, force=False, jobs=8):
     common = [ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3"]
     if os.environ.get("SC_EXP"):
         common.append("-DSC_EXP=" + os.environ["SC_EXP"])
+    for d in os.environ.get("SC_DEFS", "").split():   # experiment builds (use with SC_LIBDIR)
+        common.append("-D" + d)
     objs = []
     procs = []
     for src in sources():

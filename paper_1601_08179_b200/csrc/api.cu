@@ -73,7 +73,6 @@ struct sc_ctx {
   bool use_ptab = false;                // PCG reads Pinv from the per-class table (uniform geometry)
   PinvTab ptab;                 // v4 colour-scheduled element operator (n_I >= 8, uniform geometry)
   std::vector<unsigned char> big_coef;
-  double* d_big_dt = nullptr;           // its D^{-1} table [i][k][32]
   std::vector<unsigned char> col_coef;  // kernel-parameter coefficient block
   int col_ntx = 0, col_nty = 0;
   int col_nseg = 1, col_zseg = 0;       // z-segments per tile column (load balance over the SMs)
@@ -339,11 +338,7 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
       ctx->use_col = true;
     }
     if (!ctx->use_col && big_supported(ni) && uniform && sig_ok && !(env && env[0] == '1')) {
-      std::vector<double> dt;
-      big_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->big_coef, dt);
-      if (cudaMalloc(&ctx->d_big_dt, sizeof(double) * dt.size()) != cudaSuccess) return fail("cudaMalloc big dt");
-      if (cudaMemcpy(ctx->d_big_dt, dt.data(), sizeof(double) * dt.size(), cudaMemcpyHostToDevice) != cudaSuccess)
-        return fail("cudaMemcpy big dt");
+      big_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->big_coef);
       ctx->use_big = true;
     }
   }
@@ -382,7 +377,6 @@ extern "C" sc_status sc_destroy(sc_ctx* ctx) {
   if (ctx->d_corner) cudaFree(ctx->d_corner);
   if (ctx->d_pending) cudaFree(ctx->d_pending);
   if (ctx->d_dotp) cudaFree(ctx->d_dotp);
-  if (ctx->d_big_dt) cudaFree(ctx->d_big_dt);
   for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);
   delete ctx;
   return SC_OK;
@@ -550,7 +544,7 @@ static sc_status apply_impl(sc_ctx* ctx, const double* x, double* y, const doubl
                                 ctx->col_ntx, ctx->col_nty, ctx->col_nseg, ctx->col_zseg, ctx->col_coef.data(), dotp,
                                 st, &nl_, ev));
   else if (ctx->use_big)
-    LAUNCH(launch_apply_big(ctx->g, x, y, done, ctx->big_coef.data(), ctx->d_big_dt, st, &nl_, ev));
+    LAUNCH(launch_apply_big(ctx->g, x, y, done, ctx->big_coef.data(), st, &nl_, ev));
   else
     LAUNCH(launch_apply(ctx->g, x, y, done, st, &nl_, ev));
   if (rec) ctx->prof_n++;

@@ -14,7 +14,7 @@
 // i (NG = 8 H classes), fully unrolled loop over k.  The k-sums (Qz) complete in registers, the
 // i-sums (Qx) in registers over the thread's i values and then across the warps that share the
 // parity of i (fixed-order tree through shared memory), the j-sums (Qy) through a per-warp
-// shared-memory transpose.  D^{-1} is read from an L2-resident [i][k][j] table (coalesced in j).
+// shared-memory transpose.  D^{-1} is recomputed per point (reciprocal + 2 Newton steps).
 // Primary part (Eq. 26 generalised): faces in the closed form of kernels_col.cu, edges
 // and vertices from the arrowhead rows of Ktilde with a0-weighted line sums of faces / edges.
 #include <cuda_runtime.h>
@@ -30,6 +30,7 @@ struct BigCoef {
   double e[3][32];   // e[d][m] = d_{d+1} w0 a0_m       (face <- bounding edges)
   double L[3][32];   // L[d][m] = d_{d+1} w0 Lam_m      (face self term)
   double a0[32], lam[32];
+  double dl[3][32];  // dl[d][m] = d_{d+1} Lam_m          (D = d0 + dl[0][i] + dl[1][j] + dl[2][k])
   double F0[3];      // d0 w0 + d_{d+1} K00             (face self term)
   double k0p[3];     // d_{d+1} K0p                     (opposite face)
   double d[4];
@@ -41,7 +42,6 @@ struct BigParams {
   const double* x;
   double* y;
   const double* done;
-  const double* dt;   // D^{-1}(i,j,k) at (i n_I + k) 32 + j
   BigCoef cf;
 };
 
@@ -90,6 +90,8 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
   const double* const sEt = sT + 96;
   const double* const sA0t = sT + 192;
   const double* const sLamt = sT + 224;
+  __shared__ double sDl1[32];   // d2 Lam_j (lane-divergent)
+  if (tid < 32) sDl1[tid] = cf.dl[1][tid];
   const int cx = colour & 1, cy = (colour >> 1) & 1, cz = colour >> 2;
   const int ncx = (g.nx - cx + 1) >> 1, ncy = (g.ny - cy + 1) >> 1;
   const int bid = blockIdx.x;
@@ -208,12 +210,22 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
         const double c1i = cf.c[0][i];
         const double pz0 = Pz0[i + NI * jc], pz1 = Pz1[i + NI * jc];
         const double* Pyi = Pyj + i;
-        const double* Dt = P.dt + (size_t)i * NI * 32 + jc;
+        // D^{-1} = 1 / (d0 + d1 Lam_i + d2 Lam_j + d3 Lam_k) recomputed per point (MUFU
+        // approximation + 2 Newton steps, within 1 ulp of the table value: SURVEY c12): with
+        // 1-3 CTAs per SM an L2 table load per point stalls the loop (measured 6-12 % slower)
+        const double dij = cf.d[0] + cf.dl[0][i] + sDl1[jc];
         double qz0 = 0.0, qz1 = 0.0;
 #pragma unroll
         for (int k = 0; k < NI; ++k) {
           const double u = fma(c1i, Pxs[jc + NI * k], fma(c2j, Pyi[NI * k], cf.c[2][k] * ((k & 1) ? pz1 : pz0)));
-          const double v = u * __ldg(Dt + k * 32);
+          const double D = dij + cf.dl[2][k];
+          double r;
+          asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(D));
+          double e = fma(-D, r, 1.0);
+          r = fma(r, e, r);
+          e = fma(-D, r, 1.0);
+          const double dinv = fma(r, e, r);
+          const double v = u * dinv;
           qx[k] = fma(c1i, v, qx[k]);
           Yb[k * YS + j] = c2j * v;
           if (k & 1) qz1 = fma(cf.c[2][k], v, qz1);
@@ -374,15 +386,15 @@ static int launch_big_t(const BigParams& P, cudaStream_t st, int* nl) {
 
 bool big_supported(int ni) { return ni >= 8 && ni <= 31; }
 
-int launch_apply_big(const Geom& g, const double* x, double* y, const double* done, const void* coef,
-                     const double* dt, void* stream, int* nl, void* events) {
+int launch_apply_big(const Geom& g, const double* x, double* y, const double* done, const void* coef, void* stream,
+                     int* nl, void* events) {
   cudaStream_t st = (cudaStream_t)stream;
   cudaEvent_t* ev = (cudaEvent_t*)events;
   cudaError_t err = cudaMemsetAsync(y, 0, sizeof(double) * g.n_total, st);
   if (err != cudaSuccess) return err;
   if (ev) cudaEventRecord(ev[0], st);
   BigParams P;
-  P.g = g; P.x = x; P.y = y; P.done = done; P.dt = dt;
+  P.g = g; P.x = x; P.y = y; P.done = done;
   memcpy(&P.cf, coef, sizeof(BigCoef));
   int rc = cudaErrorInvalidValue;
   switch (g.ni) {
@@ -397,9 +409,9 @@ int launch_apply_big(const Geom& g, const double* x, double* y, const double* do
   return rc;
 }
 
-// Host-side coefficient block and D^{-1} table of the v4 operator (uniform geometry d).
+// Host-side coefficient block of the v4 operator (uniform geometry d).
 void big_make_coef(int ni, const double* d, const double* a0, const double* lam, double K00, double K0p, double w0,
-                   std::vector<unsigned char>& coef, std::vector<double>& dt) {
+                   std::vector<unsigned char>& coef) {
   BigCoef cf;
   memset(&cf, 0, sizeof(cf));
   for (int q = 0; q < 3; ++q)
@@ -407,6 +419,7 @@ void big_make_coef(int ni, const double* d, const double* a0, const double* lam,
       cf.c[q][m] = d[1 + q] * a0[m];
       cf.e[q][m] = d[1 + q] * w0 * a0[m];
       cf.L[q][m] = d[1 + q] * w0 * lam[m];
+      cf.dl[q][m] = d[1 + q] * lam[m];
     }
   for (int m = 0; m < ni; ++m) { cf.a0[m] = a0[m]; cf.lam[m] = lam[m]; }
   for (int q = 0; q < 3; ++q) {
@@ -417,11 +430,6 @@ void big_make_coef(int ni, const double* d, const double* a0, const double* lam,
   cf.K00 = K00; cf.K0p = K0p; cf.w0 = w0;
   coef.resize(sizeof(BigCoef));
   memcpy(coef.data(), &cf, sizeof(BigCoef));
-  dt.assign((size_t)ni * ni * 32, 0.0);
-  for (int i = 0; i < ni; ++i)
-    for (int k = 0; k < ni; ++k)
-      for (int j = 0; j < ni; ++j)
-        dt[((size_t)i * ni + k) * 32 + j] = 1.0 / (d[0] + d[1] * lam[i] + d[2] * lam[j] + d[3] * lam[k]);
 }
 
 }  // namespace sc

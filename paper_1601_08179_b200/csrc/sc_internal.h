@@ -121,9 +121,9 @@ int launch_apply_col_raw(const Geom& g, const double* x, double* y, const double
 // v4 operator (n_I >= 8, uniform geometry): colour-scheduled one-CTA-per-element kernels
 bool big_supported(int ni);
 void big_make_coef(int ni, const double* d, const double* a0, const double* lam, double K00, double K0p, double w0,
-                   std::vector<unsigned char>& coef, std::vector<double>& dt);
-int launch_apply_big(const Geom& g, const double* x, double* y, const double* done, const void* coef,
-                     const double* dt, void* stream, int* nlaunch, void* events);
+                   std::vector<unsigned char>& coef);
+int launch_apply_big(const Geom& g, const double* x, double* y, const double* done, const void* coef, void* stream,
+                     int* nlaunch, void* events);
 // z-segments of the tile columns: ntiles columns of nz layers on nsm persistent CTAs
 void col_choose_segments(int ntiles, int nz, int nsm, int* nseg, int* zseg);
 // sum of v[0..n) in a fixed order into scal[slot] (deterministic), skipped when *done != 0
