@@ -70,6 +70,7 @@ struct sc_ctx {
   // v3 tile-column operator state (kernels_col.cu)
   bool use_col = false;
   bool use_big = false;
+  bool use_p2 = false;                  // p = 2 row-warp operator (kernels_p2.cu)
   bool use_ptab = false;                // PCG reads Pinv from the per-class table (uniform geometry)
   PinvTab ptab;                 // v4 colour-scheduled element operator (n_I >= 8, uniform geometry)
   std::vector<unsigned char> big_coef;
@@ -308,7 +309,11 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
     const char* env = getenv("SC_APPLY_V1");
     bool sig_ok = true;
     for (int m = 0; m < ni; ++m) sig_ok &= (B.sigma[m] == ((m & 1) ? -1 : 1));
-    if (col_supported(ni) && uniform && sig_ok && !(env && env[0] == '1')) {
+    const char* np2 = getenv("SC_NO_P2");
+    if (ni == 1 && uniform && sig_ok && !(env && env[0] == '1') && !(np2 && np2[0] == '1')) {
+      big_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->big_coef);
+      ctx->use_p2 = true;
+    } else if (col_supported(ni) && uniform && sig_ok && !(env && env[0] == '1')) {
       col_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->col_coef);
       int tx, ty, pend;
       col_tile(ni, &tx, &ty, &pend);
@@ -337,7 +342,7 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
       if (cudaMemset(ctx->d_corner, 0, sizeof(double) * ncorner) != cudaSuccess) return fail("memset corner");
       ctx->use_col = true;
     }
-    if (!ctx->use_col && big_supported(ni) && uniform && sig_ok && !(env && env[0] == '1')) {
+    if (!ctx->use_col && !ctx->use_p2 && big_supported(ni) && uniform && sig_ok && !(env && env[0] == '1')) {
       big_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->big_coef);
       ctx->use_big = true;
     }
@@ -543,6 +548,8 @@ static sc_status apply_impl(sc_ctx* ctx, const double* x, double* y, const doubl
     LAUNCH(launch_apply_col_raw(ctx->g, x, y, done, ctx->d_colstate, ctx->d_flags, ctx->d_corner, ctx->d_pending,
                                 ctx->col_ntx, ctx->col_nty, ctx->col_nseg, ctx->col_zseg, ctx->col_coef.data(), dotp,
                                 st, &nl_, ev));
+  else if (ctx->use_p2)
+    LAUNCH(launch_apply_p2(ctx->g, x, y, done, ctx->big_coef.data(), st, &nl_, ev));
   else if (ctx->use_big)
     LAUNCH(launch_apply_big(ctx->g, x, y, done, ctx->big_coef.data(), st, &nl_, ev));
   else

@@ -25,17 +25,6 @@
 
 namespace sc {
 
-struct BigCoef {
-  double c[3][32];   // c[d][m] = d_{d+1} a0_m          (condensed part)
-  double e[3][32];   // e[d][m] = d_{d+1} w0 a0_m       (face <- bounding edges)
-  double L[3][32];   // L[d][m] = d_{d+1} w0 Lam_m      (face self term)
-  double a0[32], lam[32];
-  double dl[3][32];  // dl[d][m] = d_{d+1} Lam_m          (D = d0 + dl[0][i] + dl[1][j] + dl[2][k])
-  double F0[3];      // d0 w0 + d_{d+1} K00             (face self term)
-  double k0p[3];     // d_{d+1} K0p                     (opposite face)
-  double d[4];
-  double K00, K0p, w0;
-};
 
 struct BigParams {
   Geom g;

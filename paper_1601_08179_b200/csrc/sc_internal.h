@@ -118,12 +118,27 @@ void col_make_coef(int ni, const double* d, const double* a0, const double* lam,
 int launch_apply_col_raw(const Geom& g, const double* x, double* y, const double* done, void* state, int* flags,
                          double* corner, double* pending, int ntx, int nty, int nseg, int zseg, const void* coef,
                          double* dotp, void* stream, int* nlaunch, void* events);
+// Uniform-geometry coefficient block of the element-scheduled operators (v4, p2)
+struct BigCoef {
+  double c[3][32];   // c[d][m] = d_{d+1} a0_m          (condensed part)
+  double e[3][32];   // e[d][m] = d_{d+1} w0 a0_m       (face <- bounding edges)
+  double L[3][32];   // L[d][m] = d_{d+1} w0 Lam_m      (face self term)
+  double a0[32], lam[32];
+  double dl[3][32];  // dl[d][m] = d_{d+1} Lam_m          (D = d0 + dl[0][i] + dl[1][j] + dl[2][k])
+  double F0[3];      // d0 w0 + d_{d+1} K00             (face self term)
+  double k0p[3];     // d_{d+1} K0p                     (opposite face)
+  double d[4];
+  double K00, K0p, w0;
+};
 // v4 operator (n_I >= 8, uniform geometry): colour-scheduled one-CTA-per-element kernels
 bool big_supported(int ni);
 void big_make_coef(int ni, const double* d, const double* a0, const double* lam, double K00, double K0p, double w0,
                    std::vector<unsigned char>& coef);
 int launch_apply_big(const Geom& g, const double* x, double* y, const double* done, const void* coef, void* stream,
                      int* nlaunch, void* events);
+// p = 2 operator (uniform geometry): warp = 32 consecutive elements of an x-row, colour-scheduled
+int launch_apply_p2(const Geom& g, const double* x, double* y, const double* done, const void* coef, void* stream,
+                    int* nlaunch, void* events);
 // z-segments of the tile columns: ntiles columns of nz layers on nsm persistent CTAs
 void col_choose_segments(int ntiles, int nz, int nsm, int* nseg, int* zseg);
 // sum of v[0..n) in a fixed order into scal[slot] (deterministic), skipped when *done != 0

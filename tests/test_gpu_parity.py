@@ -425,7 +425,7 @@ def test_big_pcg_parity():
 # ---- z-slab ranks on one GPU (SC_TEST_LOCAL_SLAB: no communicator, the operator returns the
 # slab's local partial sums on its interface planes): every kernel family against the oracle's
 # slab operator with non-Dirichlet interface planes (the multi-GPU path before the NCCL halo sum)
-@pytest.mark.parametrize("p,ne,R", [(3, (10, 7, 5), 2), (6, (9, 5, 4), 2), (8, (9, 6, 7), 3), (12, (3, 2, 4), 2)])
+@pytest.mark.parametrize("p,ne,R", [(2, (37, 5, 5), 2), (3, (10, 7, 5), 2), (6, (9, 5, 4), 2), (8, (9, 6, 7), 3), (12, (3, 2, 4), 2)])
 def test_slab_rank_operator_parity(p, ne, R, monkeypatch):
     import copy
     from paper_1601_08179_b200 import Context
