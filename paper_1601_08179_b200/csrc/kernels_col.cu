@@ -76,9 +76,14 @@ struct CS {
   static constexpr bool PER_ELEM = NI <= 3;
   static constexpr int TX = NI <= 3 ? 16 : 8, TY = NI == 1 ? 16 : (NI <= 3 ? 8 : 4), NE = TX * TY;
   static constexpr int MAXROWS = 7 * TY + 4;          // row descriptors per tile
-  static constexpr int XF = TY * (TX + 1) * N2;
+  // row strides of the x-face and z-edge blocks (doubles): padded to 8 mod 16 for the class
+  // warps (lane (ix, iy) at iy RS + ix N2: the two element rows of a half-warp then fall on
+  // disjoint bank pairs -- unpadded, 64-bit accesses to x-faces were 2-way conflicted)
+  static constexpr int pad8(int v) { return PER_ELEM ? v : v + ((8 - v % 16) + 16) % 16; }
+  static constexpr int XRS = pad8((TX + 1) * N2), ZRS = pad8((TX + 1) * NI);
+  static constexpr int XF = TY * XRS;
   static constexpr int YF = (TY + 1) * TX * N2;
-  static constexpr int ZE = (TY + 1) * (TX + 1) * NI;
+  static constexpr int ZE = (TY + 1) * ZRS;
   static constexpr int SIDE = XF + YF + ZE;
   static constexpr int PZF = TY * TX * N2;
   static constexpr int PXE = (TY + 1) * TX * NI;
@@ -123,9 +128,9 @@ struct CS {
 template <int NI>
 struct Side {
   double* b;
-  __device__ double* xf(int iy, int ix) const { return b + CS<NI>::S_XF + (iy * (CS<NI>::TX + 1) + ix) * CS<NI>::N2; }
+  __device__ double* xf(int iy, int ix) const { return b + CS<NI>::S_XF + iy * CS<NI>::XRS + ix * CS<NI>::N2; }
   __device__ double* yf(int iy, int ix) const { return b + CS<NI>::S_YF + (iy * CS<NI>::TX + ix) * CS<NI>::N2; }
-  __device__ double* ze(int iy, int ix) const { return b + CS<NI>::S_ZE + (iy * (CS<NI>::TX + 1) + ix) * NI; }
+  __device__ double* ze(int iy, int ix) const { return b + CS<NI>::S_ZE + iy * CS<NI>::ZRS + ix * NI; }
 };
 template <int NI>
 struct Plane {
@@ -250,7 +255,7 @@ __device__ void build_rows(const ColParams& P, RowIO* io, int x0, int y0, int tw
   if (r < th) {                                            // x-faces row r
     d.g = g.off_f[0] + ((long long)x0 + (long long)(nx + 1) * (y0 + r)) * N2;
     d.gs = (long long)(nx + 1) * ny * N2;
-    d.s = C::S_XF + r * (TX + 1) * N2; d.len = (tw + 1) * N2;
+    d.s = C::S_XF + r * C::XRS; d.len = (tw + 1) * N2;
     d.zlo = hasW ? 0 : N2; d.zhi = hasE ? d.len : tw * N2;
     d.a = N2; d.b = tw * N2;
     d.mw = hasW ? M_PARK : M_ZERO; d.pw = C::PD_XF + r * N2; d.mm = M_Y; d.me = hasE ? M_Y : M_ZERO;
@@ -270,7 +275,7 @@ __device__ void build_rows(const ColParams& P, RowIO* io, int x0, int y0, int tw
     const bool z = fy == 0 || fy == ny, nrow = q == th && hasN, srow = q == 0 && hasS;
     d.g = g.off_e[2] + ((long long)x0 + (long long)(nx + 1) * fy) * NI;
     d.gs = (long long)(nx + 1) * (ny + 1) * NI;
-    d.s = C::S_ZE + q * (TX + 1) * NI; d.len = (tw + 1) * NI;
+    d.s = C::S_ZE + q * C::ZRS; d.len = (tw + 1) * NI;
     d.zlo = z ? d.len : (hasW ? 0 : NI); d.zhi = hasE ? d.len : tw * NI;
     d.a = NI; d.b = tw * NI;
     d.mw = z ? M_ZERO : (nrow ? M_SKIP : (hasW ? M_PARK : M_ZERO)); d.pw = C::PD_ZEW + q * NI;
@@ -1327,7 +1332,7 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
           constexpr int NZE = (TY + 1) * (TX + 1), NXE = (TY + 1) * TX, NYE = TY * (TX + 1);
           for (int t = tid; t < NZE + 2 * NXE + 2 * NYE; t += NT) {
             int r = t;
-            if (r < NZE) { eo_reduce<NI>(in.b + C::S_ZE + r * NI, 1, sA0, rq + C::R_ZE + r * 2); continue; }
+            if (r < NZE) { eo_reduce<NI>(in.ze(r / (TX + 1), r % (TX + 1)), 1, sA0, rq + C::R_ZE + r * 2); continue; }
             r -= NZE;
             if (r < 2 * NXE) {
               const int kb = r / NXE, e = r - kb * NXE;
