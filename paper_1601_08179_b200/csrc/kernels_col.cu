@@ -74,6 +74,9 @@ struct CS {
   // one element per thread (all classes in the thread) on larger tiles: 16 x 16 (n_I = 1),
   // 16 x 8 (n_I = 2, 3; the largest that fits the shared-memory budget at n_I = 3)
   static constexpr bool PER_ELEM = NI <= 3;
+  // entry-per-thread loads / finalize (short rows) for n_I <= 2; row per warp (4 predicated
+  // accesses per lane and pass) from n_I = 3 on (measured: p=4 4.56 -> 3.47 ms, p=3 3.70 vs 3.78)
+  static constexpr bool FLAT_IO = NI <= 2;
   static constexpr int TX = NI <= 3 ? 16 : 8, TY = NI == 1 ? 16 : (NI <= 3 ? 8 : 4), NE = TX * TY;
   static constexpr int MAXROWS = 7 * TY + 4;          // row descriptors per tile
   // row strides of the x-face and z-edge blocks (doubles): padded to 8 mod 16 for the class
@@ -367,7 +370,7 @@ template <int NI>
 __device__ __forceinline__ void load_block(const double* x, const RowIO* io, bool plane, int ns, int th, double* base,
                                            int l, bool zero_all) {
   using C = CS<NI>;
-  if constexpr (C::PER_ELEM) {
+  if constexpr (C::FLAT_IO) {
     const int nb = plane ? C::PLANE : C::SIDE;
     for (int t = threadIdx.x; t < nb; t += C::NT) {
       int col;
@@ -475,7 +478,7 @@ __device__ void finalize_step(const ColParams& P, long long item, int l, int x0,
   double* const pd = P.pending + (item * 3 + l % 3) * (long long)C::PEND;
   const bool want_dot = P.dotp != nullptr;
   const int nr = ns + 4 * th + 2;
-  if constexpr (C::PER_ELEM) {
+  if constexpr (C::FLAT_IO) {
     // flat: every thread takes block entries t, t + NT, ... (side block, then plane block);
     // all values are read before any store
     constexpr int NF = (C::SIDE + C::PLANE + C::NT - 1) / C::NT;
