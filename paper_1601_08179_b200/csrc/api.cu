@@ -326,12 +326,12 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
         col_choose_segments(ctx->col_ntx * ctx->col_nty, nz, nsm, &ctx->col_nseg, &ctx->col_zseg);
       }
       const size_t nitems = (size_t)ctx->col_ntx * ctx->col_nty * ctx->col_nseg;
-      size_t nflags = nitems * (nz + 1);
+      size_t nflags = nitems * 2;   // one 64-bit progress word per item (kernels_col.cu)
       size_t ncorner = (size_t)(ctx->col_ntx + 1) * (ctx->col_nty + 1) * (nz + 1) * 3 * (ni + 1);
       if (cudaMalloc(&ctx->d_colstate, 64) != cudaSuccess) return fail("cudaMalloc colstate");
       if (cudaMalloc(&ctx->d_flags, sizeof(int) * nflags) != cudaSuccess) return fail("cudaMalloc flags");
       if (cudaMalloc(&ctx->d_corner, sizeof(double) * ncorner) != cudaSuccess) return fail("cudaMalloc corner");
-      size_t npend = nitems * 3 * pend;   // 3 step slots (look-back distance 2)
+      size_t npend = nitems * 4 * pend;   // kLB + 1 = 4 step slots (look-back distance 3, kernels_col.cu)
       if (cudaMalloc(&ctx->d_pending, sizeof(double) * npend) != cudaSuccess) return fail("cudaMalloc pending");
       if (cudaMalloc(&ctx->d_dotp, sizeof(double) * nitems) != cudaSuccess)
         return fail("cudaMalloc dotp");

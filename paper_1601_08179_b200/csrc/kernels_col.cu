@@ -4,7 +4,7 @@
 // a work item is one tile-column (all nz element layers of the tile).  A persistent CTA (one
 // per SM, 8 warps) takes items in ticket order and marches up the column one element layer at
 // a time.  Every entity of the skeleton is assembled on chip except those on tile side
-// boundaries, which are finished with a decoupled look-back (distance 2): the lower-ticket contributor
+// boundaries, which are finished with a decoupled look-back (distance kLB = 3): the lower-ticket contributor
 // stores its partial sum straight into y (or, on the 4-tile corner lines, into a small corner
 // record), publishes a per-(item, layer) flag, and the owner (highest-ticket contributor) adds
 // it and writes the final value two steps later.  Every skeleton entry is written exactly once
@@ -57,7 +57,7 @@ struct ColParams {
   double* y;
   const double* done;
   ColState* st;
-  int* flags;            // [nitems][nz+1]
+  unsigned long long* prog;   // [nitems] publication progress: (epoch << 32) | (last published step + 1)
   double* corner;        // [(nty+1)][(ntx+1)][nz+1][3][NI+1]
   double* pending;       // [nitems][2][PEND]
   int ntx, nty, nitems;  // nitems = ntx nty nseg (item = seg * ntx nty + tile)
@@ -66,6 +66,10 @@ struct ColParams {
   ColCoef cf;
 };
 
+// decoupled look-back distance: a tile finishes its W / S boundary entities of step l - kLB at
+// step l (neighbours publish step l - kLB at their step l - kLB + 1: kLB - 1 steps of slack);
+// own partials are parked in kSlots = kLB + 1 rotating slots
+constexpr int kLB = 3, kSlots = kLB + 1;
 template <int NI>
 struct CS {
   static constexpr int N2 = NI * NI;
@@ -112,7 +116,7 @@ struct CS {
   static constexpr int O_TAB = O_RQ + RED;           // a0, lam (2 x 32)
   static constexpr int O_CF = O_TAB + 2 * 32;        // ColCoef copy
   static constexpr int TOTAL = O_CF + (int)(sizeof(ColCoef) / sizeof(double));
-  // parked own partials of the W / S boundary entities (global, per tile, 3 step slots)
+  // parked own partials of the W / S boundary entities (global, per tile, LB + 1 step slots)
   static constexpr int PD_XF = 0;                                  // W column x-faces  [TY][N2]
   static constexpr int PD_YF = PD_XF + TY * N2;                    // S row y-faces     [TX N2]
   static constexpr int PD_XE = PD_YF + TX * N2;                    // S row x-edges     [TX NI]
@@ -168,12 +172,12 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-__device__ __forceinline__ void flag_release(int* f, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+__device__ __forceinline__ void prog_release(unsigned long long* f, unsigned long long v) {
+  asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(f), "l"(v) : "memory");
 }
-__device__ __forceinline__ int flag_acquire(const int* f) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+__device__ __forceinline__ unsigned long long prog_acquire(const unsigned long long* f) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
   return v;
 }
 
@@ -475,7 +479,7 @@ __device__ void finalize_step(const ColParams& P, long long item, int l, int x0,
   const bool last = !side_rows, pzd = zdir(g, l);
   const int x1 = x0 + tw, y1 = y0 + th;
   const bool hasE = x1 < g.nx, hasN = y1 < g.ny, hasW = x0 > 0, hasS = y0 > 0;
-  double* const pd = P.pending + (item * 3 + l % 3) * (long long)C::PEND;
+  double* const pd = P.pending + (item * kSlots + l % kSlots) * (long long)C::PEND;
   const bool want_dot = P.dotp != nullptr;
   const int nr = ns + 4 * th + 2;
   if constexpr (C::FLAT_IO) {
@@ -557,29 +561,33 @@ __device__ void finalize_step(const ColParams& P, long long item, int l, int x0,
 // corner line).  Row base addresses of the step are built once in shared memory; every
 // thread then issues all of its loads before any store.  Dirichlet entities were written as 0
 // in the finalize pass and are skipped.
+// Prologue of the look-back for step ls (warp 0): acquire the W, S, SW tiles' flags of step ls
+// (one lane per flag) and build the step's row base addresses in shared memory; the CTA barrier
+// that follows orders every thread's data loads after the acquire.  (Hoisting it to the top of
+// step ls + kLB measured slower: the acquire then delays the step's load barrier.)
 template <int NI>
-__device__ void finish_boundary(const ColParams& P, long long item, int ls, int x0, int y0, int tw, int th,
-                                const int* flag_w, const int* flag_s, const int* flag_sw, int epoch,
-                                long long* sRow, const RowIO* io, double& dot) {
+__device__ __forceinline__ void finish_prepare(const ColParams& P, int ls, int th, const unsigned long long* flag_w,
+                                               const unsigned long long* flag_s, const unsigned long long* flag_sw,
+                                               int epoch, long long* sRow, const RowIO* io, unsigned long long* sKnown) {
   using C = CS<NI>;
-  constexpr int N2 = C::N2, NT = C::NT, TX = C::TX, TY = C::TY;
-  constexpr int MAXE = (C::PEND + NT - 1) / NT;
-  const Geom& g = P.g;
-  Addr A{g};
+  constexpr int TY = C::TY;
   const int tid = threadIdx.x;
-  const bool last = (ls == g.nz), pzd = zdir(g, ls);
-  const int x1 = x0 + tw, y1 = y0 + th;
-  const bool hasN = y1 < g.ny, hasW = x0 > 0, hasS = y0 > 0;
-  (void)x1;
-  if (!hasW && !hasS) return;
-  // row bases: [0, th) W col x-faces, [TY, TY+th] W col z-edges, [2TY+1, 2TY+1+th) W col y-edges,
-  // [3TY+1, 3TY+1+th] W col vertices, 4TY+2: S row y-faces, +1 S row z-edges, +2 S row x-edges,
-  // +3 S row vertices
   if (tid < 32) {
     const int lane = tid;
     if (lane < 3) {
-      const int* f = lane == 0 ? flag_w : (lane == 1 ? flag_s : flag_sw);
-      if (f) while (flag_acquire(f + ls) != epoch) __nanosleep(32);
+      // neighbour progress words: one acquire usually reveals several published steps, which
+      // later look-backs then need not reload (the earlier acquire already orders our loads)
+      const unsigned long long* f = lane == 0 ? flag_w : (lane == 1 ? flag_s : flag_sw);
+      const unsigned long long need = ((unsigned long long)(unsigned)epoch << 32) | (unsigned)(ls + 1);
+#if defined(SC_EXP) && SC_EXP == 27
+      (void)f; (void)need;                                              // ablation: no wait
+#else
+      if (f && sKnown[lane] < need) {
+        unsigned long long v;
+        while ((v = prog_acquire(f)) < need) __nanosleep(32);
+        sKnown[lane] = v;
+      }
+#endif
     }
     // row bases from the descriptor table (x-face rows 0.., y-face row 0 at th, z-edge rows at
     // 2 th + 1, x-edge row 0 at ns + th, y-edge rows at ns + 2 th + 1, vertex rows at ns + 3 th + 1)
@@ -596,8 +604,30 @@ __device__ void finish_boundary(const ColParams& P, long long item, int ls, int 
       sRow[4 * TY + 5] = at(ns + 3 * th + 1);
     }
   }
+}
+
+template <int NI>
+__device__ void finish_boundary(const ColParams& P, long long item, int ls, int x0, int y0, int tw, int th,
+                                const unsigned long long* flag_w, const unsigned long long* flag_s,
+                                const unsigned long long* flag_sw, int epoch, long long* sRow, const RowIO* io,
+                                unsigned long long* sKnown, double& dot) {
+  using C = CS<NI>;
+  constexpr int N2 = C::N2, NT = C::NT, TX = C::TX, TY = C::TY;
+  constexpr int MAXE = (C::PEND + NT - 1) / NT;
+  const Geom& g = P.g;
+  Addr A{g};
+  const int tid = threadIdx.x;
+  const bool last = (ls == g.nz), pzd = zdir(g, ls);
+  const int x1 = x0 + tw, y1 = y0 + th;
+  const bool hasN = y1 < g.ny, hasW = x0 > 0, hasS = y0 > 0;
+  (void)x1;
+  if (!hasW && !hasS) return;
+  // row bases: [0, th) W col x-faces, [TY, TY+th] W col z-edges, [2TY+1, 2TY+1+th) W col y-edges,
+  // [3TY+1, 3TY+1+th] W col vertices, 4TY+2: S row y-faces, +1 S row z-edges, +2 S row x-edges,
+  // +3 S row vertices
+  finish_prepare<NI>(P, ls, th, flag_w, flag_s, flag_sw, epoch, sRow, io, sKnown);
   __syncthreads();
-  const double* pd = P.pending + (item * 3 + ls % 3) * (long long)C::PEND;
+  const double* pd = P.pending + (item * kSlots + ls % kSlots) * (long long)C::PEND;
   // segment sizes of the flat list (0 when the segment does not apply at this step)
   const int n0 = (!last && hasW) ? th * N2 : 0;            // W col x-faces
   const int n1 = (!last && hasS) ? tw * N2 : 0;            // S row y-faces
@@ -1241,6 +1271,7 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
   __shared__ long long sRow[C::MAXROWS];
   __shared__ RowIO sIO[C::MAXROWS];
   __shared__ int sEpoch;
+  __shared__ unsigned long long sKnown[3];   // neighbours' progress already acquired (this item)
   const int tid = threadIdx.x;
   if (tid == 0) sEpoch = *(volatile int*)&P.st->epoch + 1;
   long long ph_t0 = clock64();
@@ -1291,10 +1322,11 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
     const int lfin0 = seg * P.zseg;
     const int lbeg = seg > 0 ? lfin0 - 1 : 0;
     const int lend = seg == P.nseg - 1 ? g.nz : min(g.nz, lfin0 + P.zseg) - 1;
-    int* const flag_me = P.flags + item * (g.nz + 1);
-    const int* const flag_w = tx > 0 ? P.flags + (item - 1) * (g.nz + 1) : nullptr;
-    const int* const flag_s = ty > 0 ? P.flags + (item - P.ntx) * (g.nz + 1) : nullptr;
-    const int* const flag_sw = (tx > 0 && ty > 0) ? P.flags + (item - P.ntx - 1) * (g.nz + 1) : nullptr;
+    unsigned long long* const flag_me = P.prog + item;
+    const unsigned long long* const flag_w = tx > 0 ? P.prog + (item - 1) : nullptr;
+    const unsigned long long* const flag_s = ty > 0 ? P.prog + (item - P.ntx) : nullptr;
+    const unsigned long long* const flag_sw = (tx > 0 && ty > 0) ? P.prog + (item - P.ntx - 1) : nullptr;
+    if (tid < 3) sKnown[tid] = 0ULL;
 
     // row descriptors of the tile, then the prologue: planes 0, 1 and side 0 as one cp.async group
     int ns;
@@ -1477,36 +1509,37 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
         __syncthreads();
         SC_PHASE(6);
       }
-      // publication of step l-1 (look-back distance 2): its stores were issued before the CTA
+      // publication of step l-1: its stores were issued before the CTA
       // barrier that ended step l-1 and have drained during this step's compute
       if (l < lfin0) continue;               // warm-up step of an upper z-segment: no output
       if (tid == 0 && l >= lfin0 + 1) {
 #if !(defined(SC_EXP) && SC_EXP == 26)
         __threadfence();
 #endif
-        flag_release(flag_me + (l - 1), epoch);
+        prog_release(flag_me, ((unsigned long long)(unsigned)epoch << 32) | (unsigned)l);   // steps <= l-1
       }
 #if !(defined(SC_EXP) && SC_EXP == 23)
       finalize_step<NI>(P, item, l, x0, y0, tw, th, ac, acb, in, inb, sIO, ns, !last, dot);
 #endif
       __syncthreads();
       SC_PHASE(7);
-      // finish the W / S boundary entities of step l-2
+      // finish the W / S boundary entities of step l - LB
 #if !(defined(SC_EXP) && SC_EXP == 24)
-      if (l >= lfin0 + 2) finish_boundary<NI>(P, item, l - 2, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO, dot);
+      if (l >= lfin0 + kLB)
+        finish_boundary<NI>(P, item, l - kLB, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO, sKnown, dot);
 #endif
       __syncthreads();
       SC_PHASE(8);
     }
-    // end of the column: publish step nz, finish steps nz-1 and nz
+    // end of the column: publish the last step, finish the last LB steps
     if (tid == 0) {
       __threadfence();
-      flag_release(flag_me + lend, epoch);
+      prog_release(flag_me, ((unsigned long long)(unsigned)epoch << 32) | (unsigned)(lend + 1));
     }
-    if (lend - 1 >= lfin0)
-      finish_boundary<NI>(P, item, lend - 1, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO, dot);
-    __syncthreads();
-    finish_boundary<NI>(P, item, lend, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO, dot);
+    for (int ls = max(lfin0, lend - kLB + 1); ls <= lend; ++ls) {
+      finish_boundary<NI>(P, item, ls, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO, sKnown, dot);
+      __syncthreads();
+    }
     // per-tile partial of x . y (fixed order: deterministic)
     if (P.dotp) {
 #pragma unroll
@@ -1637,11 +1670,11 @@ int launch_apply_col(const ColParams& P, void* stream, int* nl, int* grid_out, v
   return r;
 }
 
-int launch_apply_col_raw(const Geom& g, const double* x, double* y, const double* done, void* state, int* flags,
+int launch_apply_col_raw(const Geom& g, const double* x, double* y, const double* done, void* state, void* flags,
                          double* corner, double* pending, int ntx, int nty, int nseg, int zseg, const void* coef,
                          double* dotp, void* stream, int* nl, void* events) {
   ColParams P;
-  P.g = g; P.x = x; P.y = y; P.done = done; P.st = (ColState*)state; P.flags = flags; P.corner = corner;
+  P.g = g; P.x = x; P.y = y; P.done = done; P.st = (ColState*)state; P.prog = (unsigned long long*)flags; P.corner = corner;
   P.pending = pending;
   P.ntx = ntx; P.nty = nty; P.nitems = ntx * nty * nseg;
   P.nseg = nseg; P.zseg = zseg;

@@ -115,7 +115,7 @@ bool col_supported(int ni);
 void col_tile(int ni, int* tx, int* ty, int* pend);
 void col_make_coef(int ni, const double* d, const double* a0, const double* lam, double K00, double K0p, double w0,
                    std::vector<unsigned char>& out);
-int launch_apply_col_raw(const Geom& g, const double* x, double* y, const double* done, void* state, int* flags,
+int launch_apply_col_raw(const Geom& g, const double* x, double* y, const double* done, void* state, void* flags,
                          double* corner, double* pending, int ntx, int nty, int nseg, int zseg, const void* coef,
                          double* dotp, void* stream, int* nlaunch, void* events);
 // Uniform-geometry coefficient block of the element-scheduled operators (v4, p2)
