@@ -443,3 +443,20 @@ def test_slab_rank_operator_parity(p, ne, R, monkeypatch):
         ref = operator.AssembledCondensedOperator(gs).apply(xs.ravel())
         y, _, _ = gpu_apply_nodal(ctx, xs.ravel())
         assert rel(y, ref) <= 1e-12, (r, z0, z1)
+
+
+@pytest.mark.parametrize("p,ne", [(2, (70, 9, 6)), (4, (37, 19, 6)), (8, (33, 17, 9)), (12, (5, 4, 3))])
+def test_operator_bitwise_repeatable(p, ne):
+    """Race check: repeated applications (look-back tiles, z-segments, colour launches) are
+    bitwise identical -- every assembly order in the kernels is fixed."""
+    g = small_grid(p, ne, 1.0)
+    ctx = ctx_for(g)
+    x = ctx.skeleton()
+    ctx.sc_fill_random(3, x)
+    y0 = ctx.skeleton()
+    ctx.sc_apply_condensed(x, y0)
+    for _ in range(6):
+        y = ctx.skeleton(fill=float("nan"))
+        ctx.sc_apply_condensed(x, y)
+        torch.cuda.synchronize()
+        assert torch.equal(y, y0)
