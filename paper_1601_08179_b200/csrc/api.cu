@@ -71,6 +71,7 @@ struct sc_ctx {
   bool use_col = false;
   bool use_big = false;
   bool use_p2 = false;                  // p = 2 row-warp operator (kernels_p2.cu)
+  bool use_rw = false;                  // p = 3, 4 row-warp operator (kernels_rw.cu)
   bool use_ptab = false;                // PCG reads Pinv from the per-class table (uniform geometry)
   PinvTab ptab;                 // v4 colour-scheduled element operator (n_I >= 8, uniform geometry)
   std::vector<unsigned char> big_coef;
@@ -313,6 +314,9 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
     if (ni == 1 && uniform && sig_ok && !(env && env[0] == '1') && !(np2 && np2[0] == '1')) {
       big_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->big_coef);
       ctx->use_p2 = true;
+    } else if (rw_supported(ni) && uniform && sig_ok && !(env && env[0] == '1') && !(getenv("SC_NO_RW") && getenv("SC_NO_RW")[0] == '1')) {
+      big_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->big_coef);
+      ctx->use_rw = true;
     } else if (col_supported(ni) && uniform && sig_ok && !(env && env[0] == '1')) {
       col_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->col_coef);
       int tx, ty, pend;
@@ -342,7 +346,7 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
       if (cudaMemset(ctx->d_corner, 0, sizeof(double) * ncorner) != cudaSuccess) return fail("memset corner");
       ctx->use_col = true;
     }
-    if (!ctx->use_col && !ctx->use_p2 && big_supported(ni) && uniform && sig_ok && !(env && env[0] == '1')) {
+    if (!ctx->use_col && !ctx->use_p2 && !ctx->use_rw && big_supported(ni) && uniform && sig_ok && !(env && env[0] == '1')) {
       big_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->big_coef);
       ctx->use_big = true;
     }
@@ -550,6 +554,8 @@ static sc_status apply_impl(sc_ctx* ctx, const double* x, double* y, const doubl
                                 st, &nl_, ev));
   else if (ctx->use_p2)
     LAUNCH(launch_apply_p2(ctx->g, x, y, done, ctx->big_coef.data(), st, &nl_, ev));
+  else if (ctx->use_rw)
+    LAUNCH(launch_apply_rw(ctx->g, x, y, done, ctx->big_coef.data(), st, &nl_, ev));
   else if (ctx->use_big)
     LAUNCH(launch_apply_big(ctx->g, x, y, done, ctx->big_coef.data(), st, &nl_, ev));
   else

@@ -136,6 +136,10 @@ void big_make_coef(int ni, const double* d, const double* a0, const double* lam,
                    std::vector<unsigned char>& coef);
 int launch_apply_big(const Geom& g, const double* x, double* y, const double* done, const void* coef, void* stream,
                      int* nlaunch, void* events);
+// p = 3, 4 operator (uniform geometry): row-warp scheme with shared-memory staging
+bool rw_supported(int ni);
+int launch_apply_rw(const Geom& g, const double* x, double* y, const double* done, const void* coef, void* stream,
+                    int* nlaunch, void* events);
 // p = 2 operator (uniform geometry): warp = 32 consecutive elements of an x-row, colour-scheduled
 int launch_apply_p2(const Geom& g, const double* x, double* y, const double* done, const void* coef, void* stream,
                     int* nlaunch, void* events);
