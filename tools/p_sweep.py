@@ -7,7 +7,7 @@ unknowns), lambda = 1, and a seeded uniform[-1,1] skeleton vector (counter-based
 Times `reps` back-to-back applications with CUDA events after warm-up (inputs of 0.2-1.5 GB
 per vector exceed L2).  Reports ms per application, GDOF/s = N / t, s per unknown, the
 algorithmic bytes 16 N_c / t as a fraction of the measured HBM peak, and which kernel ran
-(tile-column v3 for n_I <= 7, colour-scheduled one-CTA-per-element v4 above).
+(row-warp kernels for p <= 4, tile-column v3 for p <= 8, colour-scheduled one-CTA-per-element v4 above).
 """
 import argparse
 import json
@@ -51,7 +51,8 @@ def main():
         row = {"p": p, "n": g.ne[0], "N": g.n_lattice, "N_c": n_c, "ms_per_apply": ms,
                "gdofs": g.n_lattice / ms / 1e6, "s_per_unknown": ms * 1e-3 / g.n_lattice,
                "hbm_frac": 16.0 * n_c / (ms * 1e-3) / 1e9 / hbm,
-               "kernel": "v3 tile-column" if p - 1 <= 7 else "v4 colour element-CTA"}
+               "kernel": {2: "p2 row-warp", 3: "rw row-warp", 4: "rw row-warp"}.get(
+                   p, "v3 tile-column" if p <= 8 else "v4 colour element-CTA")}
         rows.append(row)
         print(json.dumps(row), flush=True)
         del ctx, x, y
