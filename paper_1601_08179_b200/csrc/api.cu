@@ -96,7 +96,13 @@ struct sc_ctx {
   ncclComm_t comm = nullptr;
   long long nlaunch = 0;
   double* x_cur = nullptr;              // PCG iterate between sc_pcg_start / sc_pcg_iterate
-  long long it_enq = 0;                 // iterations enqueued since sc_pcg_start (direction kernel guard)
+  // CUDA graph of kPcgChunk PCG iterations (single GPU, no kernel profiling), captured for the
+  // iterate x_cur it was built with
+  cudaGraphExec_t pcg_graph = nullptr;
+  const double* pcg_graph_x = nullptr;   // iterate the graph was captured for
+  const double* pcg_seen_x = nullptr;    // iterate of the last eager chunk
+  int pcg_graph_launches = 0;
+  cudaStream_t cap_stream = nullptr;
   double tol2 = -1.0;
   bool prof_on = false;
   std::vector<cudaEvent_t> prof_ev;     // pairs (start, stop)
@@ -386,6 +392,8 @@ extern "C" sc_status sc_destroy(sc_ctx* ctx) {
   if (ctx->d_corner) cudaFree(ctx->d_corner);
   if (ctx->d_pending) cudaFree(ctx->d_pending);
   if (ctx->d_dotp) cudaFree(ctx->d_dotp);
+  if (ctx->pcg_graph) cudaGraphExecDestroy(ctx->pcg_graph);
+  if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);
   delete ctx;
   return SC_OK;
@@ -574,7 +582,6 @@ static sc_status pcg_start_impl(sc_ctx* ctx, const double* b, double* x, double 
   const long long n = ctx->g.n_total;
   ctx->tol2 = rtol > 0 ? rtol * rtol : -1.0;
   ctx->x_cur = x;
-  ctx->it_enq = 0;
   LAUNCH(launch_pcg_init(b, ctx->pinv, x, ctx->r, ctx->pv, n, ctx->own, ctx->partials, st, &nl_));
   LAUNCH(launch_reduce2(ctx->partials, ctx->scal, SCAL_RED0, 2, nullptr, st, &nl_));
   sc_status s = allreduce_scal(ctx, SCAL_RED0, 2, st);
@@ -611,10 +618,9 @@ static sc_status pcg_iteration(sc_ctx* ctx, cudaStream_t st) {
   if ((s = allreduce_scal(ctx, SCAL_RED0, 2, st))) return s;
   LAUNCH(launch_pcg_beta(ctx->scal, st, &nl_));
   if (ctx->use_ptab)
-    LAUNCH(launch_pcg_direction_tab(x, ctx->pv, ctx->r, ctx->ptab, ctx->scal, ctx->it_enq, st, &nl_));
+    LAUNCH(launch_pcg_direction_tab(x, ctx->pv, ctx->r, ctx->ptab, ctx->scal, st, &nl_));
   else
-    LAUNCH(launch_pcg_direction(x, ctx->pv, ctx->r, ctx->pinv, n, ctx->scal, ctx->it_enq, st, &nl_));
-  ctx->it_enq++;
+    LAUNCH(launch_pcg_direction(x, ctx->pv, ctx->r, ctx->pinv, n, ctx->scal, st, &nl_));
   return SC_OK;
 }
 
@@ -633,21 +639,74 @@ static sc_status pcg_report_impl(sc_ctx* ctx, sc_pcg_report* rep, cudaStream_t s
   return SC_OK;
 }
 
+// kPcgChunk iterations, replayed from a CUDA graph when possible: every iteration's kernels take
+// only device-resident scalars and fixed buffers, so the chunk is captured once per iterate x and
+// replayed (one launch instead of ~8 per iteration; the launch-bound small configurations gain
+// most).  Multi-GPU (NCCL in the chunk) and kernel profiling run the plain launches.
+static constexpr int kPcgChunk = 8;
+static sc_status pcg_chunk(sc_ctx* ctx, cudaStream_t st) {
+  const char* ng = getenv("SC_NO_GRAPH");
+  const bool graph_ok = ctx->prm.nranks == 1 && !ctx->prof_on && !(ng && ng[0] == '1');
+  if (graph_ok && ctx->pcg_graph && ctx->pcg_graph_x == ctx->x_cur) {
+    CK(cudaGraphLaunch(ctx->pcg_graph, st));
+    ctx->nlaunch += ctx->pcg_graph_launches;
+    return SC_OK;
+  }
+  if (graph_ok && ctx->pcg_seen_x == ctx->x_cur) {
+    // second chunk with this iterate: capture on a private stream (capture is not allowed on the
+    // legacy default stream; the exec is then launched on the caller's stream).  The first chunk
+    // ran eagerly, so every lazily set kernel attribute is in place before the capture.
+    if (ctx->pcg_graph) { cudaGraphExecDestroy(ctx->pcg_graph); ctx->pcg_graph = nullptr; }
+    if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    cudaGraph_t graph = nullptr;
+    const long long nl0 = ctx->nlaunch;
+    CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+    sc_status s = SC_OK;
+    for (int k = 0; k < kPcgChunk && s == SC_OK; ++k) s = pcg_iteration(ctx, ctx->cap_stream);
+    cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &graph);
+    ctx->pcg_graph_launches = (int)(ctx->nlaunch - nl0);
+    ctx->nlaunch = nl0;
+    if (s) { if (graph) cudaGraphDestroy(graph); return s; }
+    CK(ce);
+    ce = cudaGraphInstantiate(&ctx->pcg_graph, graph, 0);
+    cudaGraphDestroy(graph);
+    CK(ce);
+    ctx->pcg_graph_x = ctx->x_cur;
+    CK(cudaGraphLaunch(ctx->pcg_graph, st));
+    ctx->nlaunch += ctx->pcg_graph_launches;
+    return SC_OK;
+  }
+  ctx->pcg_seen_x = ctx->x_cur;
+  for (int k = 0; k < kPcgChunk; ++k) {
+    sc_status s = pcg_iteration(ctx, st);
+    if (s) return s;
+  }
+  return SC_OK;
+}
+
 static sc_status pcg_impl(sc_ctx* ctx, const double* b, double* x, double rtol, int maxit, sc_pcg_report* rep,
                           cudaStream_t st) {
   auto t0 = std::chrono::steady_clock::now();
   double* done = ctx->scal + SCAL_DONE;
   sc_status s = pcg_start_impl(ctx, b, x, rtol, maxit, st);
   if (s) return s;
-  const int check_every = rtol > 0 ? 8 : 0;
-  for (int it = 0; it < maxit; ++it) {
+  const int check_every = rtol > 0 ? kPcgChunk : 0;
+  int it = 0;
+  bool stop = false;
+  auto poll = [&]() -> sc_status {
+    double dflag = 0;
+    CK(cudaMemcpyAsync(&dflag, done, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    stop = dflag != 0.0;
+    return SC_OK;
+  };
+  for (; it + kPcgChunk <= maxit && !stop; it += kPcgChunk) {
+    if ((s = pcg_chunk(ctx, st))) return s;
+    if (check_every && (s = poll())) return s;
+  }
+  for (; it < maxit && !stop; ++it) {
     if ((s = pcg_iteration(ctx, st))) return s;
-    if (check_every && (it + 1) % check_every == 0) {
-      double dflag = 0;
-      CK(cudaMemcpyAsync(&dflag, done, sizeof(double), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      if (dflag != 0.0) break;
-    }
+    if (check_every && (it + 1) % check_every == 0 && (s = poll())) return s;
   }
   CK(cudaStreamSynchronize(st));
   auto t1 = std::chrono::steady_clock::now();

@@ -91,13 +91,12 @@ __global__ void k_pcg_update(double* __restrict__ r, const double* __restrict__ 
 
 // x += alpha p (the x update of this iteration, moved here from the update kernel so that p is
 // streamed once) ; p = Pinv r + beta p unless converged   (6 streams: x, p, r, Pinv read; x, p
-// written).  `it` is the host's 0-based index of this iteration: the kernel acts only if this
-// iteration's alpha kernel ran (iteration count == it + 1), so iterations enqueued after
-// convergence change nothing.
+// written).  The kernel acts only if this iteration's alpha kernel ran (device flag SCAL_RAN),
+// so iterations enqueued after convergence change nothing and the iteration has no host-side
+// arguments (graph-capturable).
 __global__ void k_pcg_direction(double* __restrict__ x, double* __restrict__ p, const double* __restrict__ r,
-                                const double* __restrict__ pinv, long long n, const double* __restrict__ scal,
-                                long long it) {
-  if (scal[SCAL_ITERS] != (double)(it + 1) || scal[SCAL_BREAK] != 0.0) return;
+                                const double* __restrict__ pinv, long long n, const double* __restrict__ scal, int) {
+  if (scal[SCAL_RAN] == 0.0 || scal[SCAL_BREAK] != 0.0) return;
   const double alpha = scal[SCAL_ALPHA], beta = scal[SCAL_BETA];
   const bool dir = scal[SCAL_DONE] == 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -137,8 +136,8 @@ __global__ void k_pcg_update_tab(double* __restrict__ r, const double* __restric
 
 // x += alpha p ; p = Pinv r + beta p unless converged   (5 streams: x, p, r read; x, p written)
 __global__ void k_pcg_direction_tab(double* __restrict__ x, double* __restrict__ p, const double* __restrict__ r,
-                                    PinvTab T, const double* __restrict__ scal, long long it) {
-  if (scal[SCAL_ITERS] != (double)(it + 1) || scal[SCAL_BREAK] != 0.0) return;
+                                    PinvTab T, const double* __restrict__ scal) {
+  if (scal[SCAL_RAN] == 0.0 || scal[SCAL_BREAK] != 0.0) return;
   const double alpha = scal[SCAL_ALPHA], beta = scal[SCAL_BETA];
   const bool dir = scal[SCAL_DONE] == 0.0;
   const long long S = (long long)gridDim.x * blockDim.x, g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -194,12 +193,14 @@ __global__ void k_pcg_init_finalize(double* scal, double tol2, int maxit) {
 }
 
 __global__ void k_pcg_alpha(double* scal) {
+  scal[SCAL_RAN] = 0.0;
   if (scal[SCAL_DONE] != 0.0) return;
   double pq = scal[SCAL_RED0];
   if (!(pq > 0.0)) { scal[SCAL_BREAK] = 1.0; scal[SCAL_DONE] = 1.0; return; }
   scal[SCAL_PQ] = pq;
   scal[SCAL_ALPHA] = scal[SCAL_RZ] / pq;
   scal[SCAL_ITERS] += 1.0;
+  scal[SCAL_RAN] = 1.0;
 }
 
 __global__ void k_pcg_beta(double* scal) {
@@ -268,8 +269,8 @@ int launch_pcg_beta(double* scal, void* stream, int* nl) {
 }
 
 int launch_pcg_direction(double* x, double* p, const double* r, const double* pinv, long long n, const double* scal,
-                         long long it, void* stream, int* nl) {
-  k_pcg_direction<<<SC_RED_BLOCKS, VEC_THREADS, 0, (cudaStream_t)stream>>>(x, p, r, pinv, n, scal, it);
+                         void* stream, int* nl) {
+  k_pcg_direction<<<SC_RED_BLOCKS, VEC_THREADS, 0, (cudaStream_t)stream>>>(x, p, r, pinv, n, scal, 0);
   (*nl)++;
   return cudaGetLastError();
 }
@@ -281,9 +282,9 @@ int launch_pcg_update_tab(double* r, const double* q, const PinvTab& T, OwnMask 
   return cudaGetLastError();
 }
 
-int launch_pcg_direction_tab(double* x, double* p, const double* r, const PinvTab& T, const double* scal, long long it,
+int launch_pcg_direction_tab(double* x, double* p, const double* r, const PinvTab& T, const double* scal,
                              void* stream, int* nl) {
-  k_pcg_direction_tab<<<SC_RED_BLOCKS, VEC_THREADS, 0, (cudaStream_t)stream>>>(x, p, r, T, scal, it);
+  k_pcg_direction_tab<<<SC_RED_BLOCKS, VEC_THREADS, 0, (cudaStream_t)stream>>>(x, p, r, T, scal);
   (*nl)++;
   return cudaGetLastError();
 }

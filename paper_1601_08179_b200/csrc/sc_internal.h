@@ -61,6 +61,7 @@ enum { MAT_I = 0, MAT_SM = 1, MAT_S = 2, MAT_ST = 3, MAT_MST = 4 };
 enum {
   SCAL_RZ = 0, SCAL_RZNEW, SCAL_PQ, SCAL_ALPHA, SCAL_BETA, SCAL_RR, SCAL_RR0,
   SCAL_DONE, SCAL_ITERS, SCAL_BREAK, SCAL_TOL2, SCAL_MAXIT, SCAL_RED0, SCAL_RED1, SCAL_RED2,
+  SCAL_RAN,   // 1 if this iteration's alpha step ran (guards the x / p update)
   SCAL_COUNT = 32
 };
 
@@ -96,13 +97,13 @@ int launch_pcg_init_finalize(double* scal, const double* partials, double tol2, 
 int launch_pcg_alpha(double* scal, void* stream, int* nlaunch);
 int launch_pcg_update_tab(double* r, const double* q, const PinvTab& T, OwnMask m, const double* scal,
                           double* partials, void* stream, int* nlaunch);
-int launch_pcg_direction_tab(double* x, double* p, const double* r, const PinvTab& T, const double* scal, long long it,
+int launch_pcg_direction_tab(double* x, double* p, const double* r, const PinvTab& T, const double* scal,
                              void* stream, int* nlaunch);
 int launch_pcg_update(double* r, const double* q, const double* pinv, long long n, OwnMask m, const double* scal,
                       double* partials, void* stream, int* nlaunch);
 int launch_pcg_beta(double* scal, void* stream, int* nlaunch);
 int launch_pcg_direction(double* x, double* p, const double* r, const double* pinv, long long n, const double* scal,
-                         long long it, void* stream, int* nlaunch);
+                         void* stream, int* nlaunch);
 int launch_reduce2(const double* partials, double* scal, int slot0, int nvals, const double* done,
                    void* stream, int* nlaunch);
 
