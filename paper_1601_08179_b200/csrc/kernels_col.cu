@@ -1415,16 +1415,26 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
             if (!evalid || e >= NZE || ix > tw || iy > th) continue;
             const double u = in.ze(iy, ix)[c];
             const double tz = sA0[c] * (*inb.vv(iy, ix) + ((c & 1) ? -*intp.vv(iy, ix) : *intp.vv(iy, ix))) + sLam[c] * u;
-            double y = 0.0;
+            // the x-line term depends on ib only, the y-line term on jb only: each is evaluated
+            // once and weighted by the number of present elements sharing it
+            const int p00 = present(ix, iy), p10 = present(ix - 1, iy), p01 = present(ix, iy - 1),
+                      p11 = present(ix - 1, iy - 1);
+            double y = (p00 + p10 + p01 + p11) * (w02d0 * u + dD * w02 * tz);
 #pragma unroll
-            for (int el = 0; el < 4; ++el) {
-              const int ib = el & 1, jb = el >> 1, ex = ix - ib, ey = iy - jb;
-              if (!present(ex, ey)) continue;
-              const double txl = (ib ? K0p : K00) * in.ze(iy, ex)[c] + (ib ? K00 : K0p) * in.ze(iy, ex + 1)[c] +
-                                 eo_row(rq + C::R_YI + (iy * TX + ex) * 2 * NI + 2 * c, ib);
-              const double tyl = (jb ? K0p : K00) * in.ze(ey, ix)[c] + (jb ? K00 : K0p) * in.ze(ey + 1, ix)[c] +
-                                 eo_row(rq + C::R_XJ + (ey * (TX + 1) + ix) * 2 * NI + 2 * c, jb);
-              y += w02d0 * u + dB * w0 * txl + dC * w0 * tyl + dD * w02 * tz;
+            for (int b = 0; b < 2; ++b) {
+              const int nxb = b ? p10 + p11 : p00 + p01, nyb = b ? p01 + p11 : p00 + p10;
+              if (nxb) {
+                const int ex = ix - b;
+                const double txl = (b ? K0p : K00) * in.ze(iy, ex)[c] + (b ? K00 : K0p) * in.ze(iy, ex + 1)[c] +
+                                   eo_row(rq + C::R_YI + (iy * TX + ex) * 2 * NI + 2 * c, b);
+                y = fma(nxb * dB * w0, txl, y);
+              }
+              if (nyb) {
+                const int ey = iy - b;
+                const double tyl = (b ? K0p : K00) * in.ze(ey, ix)[c] + (b ? K00 : K0p) * in.ze(ey + 1, ix)[c] +
+                                   eo_row(rq + C::R_XJ + (ey * (TX + 1) + ix) * 2 * NI + 2 * c, b);
+                y = fma(nyb * dC * w0, tyl, y);
+              }
             }
             res[s] = y;
             dsto[s] = (int)(ac.ze(iy, ix) + c - sm);
@@ -1484,16 +1494,24 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
             const double u = *pk.vv(iy, ix);
             const double tzl = (kb ? K0p : K00) * *inb.vv(iy, ix) + (kb ? K00 : K0p) * *intp.vv(iy, ix) +
                                eo_row(rq + C::R_ZE + (iy * (TX + 1) + ix) * 2, kb);
-            double y = 0.0;
+            const int p00 = present(ix, iy), p10 = present(ix - 1, iy), p01 = present(ix, iy - 1),
+                      p11 = present(ix - 1, iy - 1);
+            double y = (p00 + p10 + p01 + p11) * (w02d0 * w0 * u + w02 * dD * tzl);
 #pragma unroll
-            for (int el = 0; el < 4; ++el) {
-              const int ib = el & 1, jb = el >> 1, ex = ix - ib, ey = iy - jb;
-              if (!present(ex, ey)) continue;
-              const double txl = (ib ? K0p : K00) * *pk.vv(iy, ex) + (ib ? K00 : K0p) * *pk.vv(iy, ex + 1) +
-                                 eo_row(rq + C::R_XE + (kb * (TY + 1) * TX + iy * TX + ex) * 2, ib);
-              const double tyl = (jb ? K0p : K00) * *pk.vv(ey, ix) + (jb ? K00 : K0p) * *pk.vv(ey + 1, ix) +
-                                 eo_row(rq + C::R_YE + (kb * TY * (TX + 1) + ey * (TX + 1) + ix) * 2, jb);
-              y += w02d0 * w0 * u + w02 * (dB * txl + dC * tyl + dD * tzl);
+            for (int b = 0; b < 2; ++b) {
+              const int nxb = b ? p10 + p11 : p00 + p01, nyb = b ? p01 + p11 : p00 + p10;
+              if (nxb) {
+                const int ex = ix - b;
+                const double txl = (b ? K0p : K00) * *pk.vv(iy, ex) + (b ? K00 : K0p) * *pk.vv(iy, ex + 1) +
+                                   eo_row(rq + C::R_XE + (kb * (TY + 1) * TX + iy * TX + ex) * 2, b);
+                y = fma(nxb * w02 * dB, txl, y);
+              }
+              if (nyb) {
+                const int ey = iy - b;
+                const double tyl = (b ? K0p : K00) * *pk.vv(ey, ix) + (b ? K00 : K0p) * *pk.vv(ey + 1, ix) +
+                                   eo_row(rq + C::R_YE + (kb * TY * (TX + 1) + ey * (TX + 1) + ix) * 2, b);
+                y = fma(nyb * w02 * dC, tyl, y);
+              }
             }
             res[SZ + SX + SY + s] = y;
             dsto[SZ + SX + SY + s] = (int)((kb ? actp : acb).vv(iy, ix) - sm);
