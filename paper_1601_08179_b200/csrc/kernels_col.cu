@@ -607,10 +607,11 @@ __device__ __forceinline__ void finish_prepare(const ColParams& P, int ls, int t
 }
 
 template <int NI>
-__device__ void finish_boundary(const ColParams& P, long long item, int ls, int x0, int y0, int tw, int th,
-                                const unsigned long long* flag_w, const unsigned long long* flag_s,
-                                const unsigned long long* flag_sw, int epoch, long long* sRow, const RowIO* io,
-                                unsigned long long* sKnown, double& dot) {
+__device__ void finish_gather(const ColParams& P, long long item, int ls, int x0, int y0, int tw, int th,
+                              const unsigned long long* flag_w, const unsigned long long* flag_s,
+                              const unsigned long long* flag_sw, int epoch, long long* sRow, const RowIO* io,
+                              unsigned long long* sKnown, double (&val)[(CS<NI>::PEND + CS<NI>::NT - 1) / CS<NI>::NT],
+                              double* (&dst)[(CS<NI>::PEND + CS<NI>::NT - 1) / CS<NI>::NT]) {
   using C = CS<NI>;
   constexpr int N2 = C::N2, NT = C::NT, TX = C::TX, TY = C::TY;
   constexpr int MAXE = (C::PEND + NT - 1) / NT;
@@ -639,8 +640,6 @@ __device__ void finish_boundary(const ColParams& P, long long item, int ls, int 
   const int n7 = (!pzd && hasS) ? tw - 1 : 0;              // S row vertices, ix in [1, tw-1]
   const int c1 = n0, c2 = c1 + n1, c3 = c2 + n2, c4 = c3 + n3, c5 = c4 + n4, c6 = c5 + n5, c7 = c6 + n6;
   const int ntot = c7 + n7;
-  double val[MAXE];
-  double* dst[MAXE];
 #pragma unroll
   for (int k = 0; k < MAXE; ++k) {
     dst[k] = nullptr;
@@ -686,6 +685,15 @@ __device__ void finish_boundary(const ColParams& P, long long item, int ls, int 
     val[k] = v;
     dst[k] = d;
   }
+}
+
+// Second half of the look-back: x . y partials (fused dot only) and the stores.  The values
+// were gathered before the step's finalize, so their load latency overlaps it.
+template <int NI>
+__device__ __forceinline__ void finish_scatter(const ColParams& P, const double (&val)[(CS<NI>::PEND + CS<NI>::NT - 1) / CS<NI>::NT],
+                                               double* const (&dst)[(CS<NI>::PEND + CS<NI>::NT - 1) / CS<NI>::NT],
+                                               double& dot) {
+  constexpr int MAXE = (CS<NI>::PEND + CS<NI>::NT - 1) / CS<NI>::NT;
   double xv[MAXE];
 #pragma unroll
   for (int k = 0; k < MAXE; ++k) xv[k] = (dst[k] && P.dotp) ? ld_cg(P.x + (dst[k] - P.y)) : 0.0;
@@ -695,6 +703,20 @@ __device__ void finish_boundary(const ColParams& P, long long item, int ls, int 
       *dst[k] = val[k];
       dot = fma(val[k], xv[k], dot);
     }
+}
+
+template <int NI>
+__device__ void finish_boundary(const ColParams& P, long long item, int ls, int x0, int y0, int tw, int th,
+                                const unsigned long long* flag_w, const unsigned long long* flag_s,
+                                const unsigned long long* flag_sw, int epoch, long long* sRow, const RowIO* io,
+                                unsigned long long* sKnown, double& dot) {
+  constexpr int MAXE = (CS<NI>::PEND + CS<NI>::NT - 1) / CS<NI>::NT;
+  double val[MAXE];
+  double* dst[MAXE];
+#pragma unroll
+  for (int k = 0; k < MAXE; ++k) { val[k] = 0.0; dst[k] = nullptr; }
+  finish_gather<NI>(P, item, ls, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, io, sKnown, val, dst);
+  finish_scatter<NI>(P, val, dst, dot);
 }
 
 // ---- condensed part of one parity class (s_i, s_j, s_k) = (SI, SJ, SK) ---------------------
@@ -1536,16 +1558,22 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
 #endif
         prog_release(flag_me, ((unsigned long long)(unsigned)epoch << 32) | (unsigned)l);   // steps <= l-1
       }
+      // finish the W / S boundary entities of step l - LB: gather (flags, pending + neighbour
+      // partials) before this step's finalize, so the loads overlap it; store after
+      constexpr int MAXE = (C::PEND + NT - 1) / NT;
+      double fval[MAXE];
+      double* fdst[MAXE];
+#pragma unroll
+      for (int k = 0; k < MAXE; ++k) { fval[k] = 0.0; fdst[k] = nullptr; }
+#if !(defined(SC_EXP) && SC_EXP == 24)
+      if (l >= lfin0 + kLB)
+        finish_gather<NI>(P, item, l - kLB, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO, sKnown, fval, fdst);
+#endif
 #if !(defined(SC_EXP) && SC_EXP == 23)
       finalize_step<NI>(P, item, l, x0, y0, tw, th, ac, acb, in, inb, sIO, ns, !last, dot);
 #endif
-      __syncthreads();
+      finish_scatter<NI>(P, fval, fdst, dot);
       SC_PHASE(7);
-      // finish the W / S boundary entities of step l - LB
-#if !(defined(SC_EXP) && SC_EXP == 24)
-      if (l >= lfin0 + kLB)
-        finish_boundary<NI>(P, item, l - kLB, x0, y0, tw, th, flag_w, flag_s, flag_sw, epoch, sRow, sIO, sKnown, dot);
-#endif
       __syncthreads();
       SC_PHASE(8);
     }
