@@ -1377,6 +1377,14 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
         load_block<NI>(P.x, sIO, true, ns, th, sm + C::O_IP + ((l + 2) % 3) * C::PLANE, l + 2, zdir(g, l + 2));
 #endif
       cp_commit();
+      // publication of step l-1 (its stores were issued before the barrier that ended step l-1):
+      // the GPU-scope fence overlaps this step's load wait
+      if (tid == 0 && l >= lfin0 + 1) {
+#if !(defined(SC_EXP) && SC_EXP == 26)
+        __threadfence();
+#endif
+        prog_release(flag_me, ((unsigned long long)(unsigned)epoch << 32) | (unsigned)l);   // steps <= l-1
+      }
       cp_wait<1>();
       __syncthreads();
       SC_PHASE(0);
@@ -1549,15 +1557,7 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
         __syncthreads();
         SC_PHASE(6);
       }
-      // publication of step l-1: its stores were issued before the CTA
-      // barrier that ended step l-1 and have drained during this step's compute
       if (l < lfin0) continue;               // warm-up step of an upper z-segment: no output
-      if (tid == 0 && l >= lfin0 + 1) {
-#if !(defined(SC_EXP) && SC_EXP == 26)
-        __threadfence();
-#endif
-        prog_release(flag_me, ((unsigned long long)(unsigned)epoch << 32) | (unsigned)l);   // steps <= l-1
-      }
       // finish the W / S boundary entities of step l - LB: gather (flags, pending + neighbour
       // partials) before this step's finalize, so the loads overlap it; store after
       constexpr int MAXE = (C::PEND + NT - 1) / NT;
