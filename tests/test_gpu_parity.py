@@ -460,3 +460,34 @@ def test_operator_bitwise_repeatable(p, ne):
         ctx.sc_apply_condensed(x, y)
         torch.cuda.synchronize()
         assert torch.equal(y, y0)
+
+
+def test_pcg_graph_replay_matches_eager(monkeypatch):
+    """sc_pcg_solve replays 8-iteration chunks from a CUDA graph (captured at the second chunk
+    for a given iterate buffer): repeated solves, a second iterate buffer (re-capture), a
+    tolerance that stops mid-chunk and a maxit that is not a multiple of 8 all give results
+    bitwise identical to the eager launches (SC_NO_GRAPH=1)."""
+    g = small_grid(5, (4, 3, 5), 1.0)
+
+    def run(no_graph):
+        if no_graph:
+            monkeypatch.setenv("SC_NO_GRAPH", "1")
+        else:
+            monkeypatch.delenv("SC_NO_GRAPH", raising=False)
+        ctx = ctx_for(g)
+        b1, b2 = ctx.skeleton(), ctx.skeleton()
+        ctx.sc_fill_random(21, b1)
+        ctx.sc_fill_random(22, b2)
+        x1, x2 = ctx.skeleton(), ctx.skeleton()
+        out = []
+        for b, x, rtol, maxit in ((b1, x1, 1e-10, 500), (b1, x1, 1e-10, 500), (b2, x2, 1e-9, 500),
+                                  (b2, x1, 0.0, 13), (b1, x2, 1e-10, 500)):
+            rep = ctx.sc_pcg_solve(b, x, rtol=rtol, maxit=maxit)
+            torch.cuda.synchronize()
+            out.append((rep.iters, rep.converged, x.clone()))
+        return out
+
+    eager, graph = run(True), run(False)
+    for (i0, c0, x0), (i1, c1, x1) in zip(eager, graph):
+        assert i0 == i1 and c0 == c1
+        assert torch.equal(x0, x1)
