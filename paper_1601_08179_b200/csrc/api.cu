@@ -352,8 +352,10 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
       if (cudaMemset(ctx->d_corner, 0, sizeof(double) * ncorner) != cudaSuccess) return fail("memset corner");
       ctx->use_col = true;
     }
-    if (!ctx->use_col && !ctx->use_p2 && !ctx->use_rw && big_supported(ni) && uniform && sig_ok && !(env && env[0] == '1')) {
-      big_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->big_coef);
+    // v4 also runs non-uniform grids: each CTA derives its element's coefficients from d_e
+    if (!ctx->use_col && !ctx->use_p2 && !ctx->use_rw && big_supported(ni) && sig_ok && !(env && env[0] == '1')) {
+      const double d_one[4] = {1.0, 1.0, 1.0, 1.0};
+      big_make_coef(ni, uniform ? g.d_uni : d_one, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->big_coef);
       ctx->use_big = true;
     }
   }

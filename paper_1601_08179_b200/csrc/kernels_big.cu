@@ -60,7 +60,10 @@ __device__ __forceinline__ void cp_async8b(double* smem, const double* gmem) {
 __device__ __forceinline__ double sgn(int m) { return (m & 1) ? -1.0 : 1.0; }
 __device__ __forceinline__ double eo_row_b(const double* r, int hi) { return hi ? r[0] - r[1] : r[0] + r[1]; }
 
-template <int NI>
+// UNI: uniform geometry (the d-dependent coefficients are kernel parameters, constant-bank
+// operands); otherwise each CTA derives them from its element's d_e (metric) into shared
+// memory (graded / anisotropic non-uniform grids).
+template <int NI, bool UNI>
 __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ BigParams P, int colour) {
   using B = BL<NI>;
   constexpr int N2 = B::N2, SW = B::SW, H = B::H, NG = B::NG, YS = B::YS;
@@ -74,17 +77,41 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
   const Geom& g = P.g;
   const BigCoef& cf = P.cf;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  sT[tid] = tid < 96 ? (&cf.L[0][0])[tid] : tid < 192 ? (&cf.e[0][0])[tid - 96] : tid < 224 ? cf.a0[tid - 192] : cf.lam[tid - 224];
+
+  const int cx = colour & 1, cy = (colour >> 1) & 1, cz = colour >> 2;
+  const int ncx = (g.nx - cx + 1) >> 1, ncy = (g.ny - cy + 1) >> 1;
+  const int bid = blockIdx.x;
+  const int ex = cx + 2 * (bid % ncx), ey = cy + 2 * ((bid / ncx) % ncy), ez = cz + 2 * (bid / (ncx * ncy));
+  // element geometry: d_e (uniform: the parameter block's)
+  double dd[4];
+  if constexpr (UNI) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) dd[q] = cf.d[q];
+  } else {
+    metric(g, ex, ey, ez, dd);
+  }
+  __shared__ double sCg[3 * 32], sDlg[3 * 32];   // non-uniform: c[d][m], dl[d][m] of this element
+  if constexpr (UNI) {
+    sT[tid] = tid < 96 ? (&cf.L[0][0])[tid] : tid < 192 ? (&cf.e[0][0])[tid - 96] : tid < 224 ? cf.a0[tid - 192] : cf.lam[tid - 224];
+  } else {
+    const int q = (tid >> 5) % 3, m = tid & 31;
+    sT[tid] = tid < 96 ? dd[1 + q] * cf.w0 * cf.lam[m] : tid < 192 ? dd[1 + q] * cf.w0 * cf.a0[m]
+                                                        : tid < 224 ? cf.a0[tid - 192] : cf.lam[tid - 224];
+    if (tid < 96) {
+      sCg[tid] = dd[1 + q] * cf.a0[m];
+      sDlg[tid] = dd[1 + q] * cf.lam[m];
+    }
+  }
+  auto Cc = [&](int q, int m) -> double { if constexpr (UNI) return cf.c[q][m]; else return sCg[q * 32 + m]; };
+  auto Dl = [&](int q, int m) -> double { if constexpr (UNI) return cf.dl[q][m]; else return sDlg[q * 32 + m]; };
+  const double F0[3] = {dd[0] * cf.w0 + dd[1] * cf.K00, dd[0] * cf.w0 + dd[2] * cf.K00, dd[0] * cf.w0 + dd[3] * cf.K00};
+  const double k0p[3] = {dd[1] * cf.K0p, dd[2] * cf.K0p, dd[3] * cf.K0p};
   const double* const sLt = sT;
   const double* const sEt = sT + 96;
   const double* const sA0t = sT + 192;
   const double* const sLamt = sT + 224;
   __shared__ double sDl1[32];   // d2 Lam_j (lane-divergent)
-  if (tid < 32) sDl1[tid] = cf.dl[1][tid];
-  const int cx = colour & 1, cy = (colour >> 1) & 1, cz = colour >> 2;
-  const int ncx = (g.nx - cx + 1) >> 1, ncy = (g.ny - cy + 1) >> 1;
-  const int bid = blockIdx.x;
-  const int ex = cx + 2 * (bid % ncx), ey = cy + 2 * ((bid / ncx) % ncy), ez = cz + 2 * (bid / (ncx * ncy));
+  if (tid < 32) sDl1[tid] = dd[2] * cf.lam[tid];
   if (tid < 26) {
     bool dr;
     sBase[tid] = entity_base(g, ex, ey, ez, tid, &dr);
@@ -181,7 +208,7 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
     const int j = lane % SW, h = lane / SW, ig = warp * H + h;
     const bool jok = j < NI;
     const int jc = jok ? j : 0;
-    const double c2j = jok ? cf.c[1][jc] : 0.0;
+    const double c2j = jok ? Cc(1, jc) : 0.0;
     const double* Pxs = sP + (ig & 1) * N2;            // Px^{s_i}; s_i = ig & 1 (NG even)
     const double* Pyj = sP + (2 + (j & 1)) * N2;       // Py^{s_j}
     const double* Pz0 = sP + 4 * N2;
@@ -196,18 +223,18 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
       const bool iok = i < NI;
       const unsigned am = __ballot_sync(0xffffffffu, iok);
       if (iok) {
-        const double c1i = cf.c[0][i];
+        const double c1i = Cc(0, i);
         const double pz0 = Pz0[i + NI * jc], pz1 = Pz1[i + NI * jc];
         const double* Pyi = Pyj + i;
         // D^{-1} = 1 / (d0 + d1 Lam_i + d2 Lam_j + d3 Lam_k) recomputed per point (MUFU
         // approximation + 2 Newton steps, within 1 ulp of the table value: SURVEY c12): with
         // 1-3 CTAs per SM an L2 table load per point stalls the loop (measured 6-12 % slower)
-        const double dij = cf.d[0] + cf.dl[0][i] + sDl1[jc];
+        const double dij = dd[0] + Dl(0, i) + sDl1[jc];
         double qz0 = 0.0, qz1 = 0.0;
 #pragma unroll
         for (int k = 0; k < NI; ++k) {
-          const double u = fma(c1i, Pxs[jc + NI * k], fma(c2j, Pyi[NI * k], cf.c[2][k] * ((k & 1) ? pz1 : pz0)));
-          const double D = dij + cf.dl[2][k];
+          const double u = fma(c1i, Pxs[jc + NI * k], fma(c2j, Pyi[NI * k], Cc(2, k) * ((k & 1) ? pz1 : pz0)));
+          const double D = dij + Dl(2, k);
           double r;
           asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(D));
           double e = fma(-D, r, 1.0);
@@ -217,8 +244,8 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
           const double v = u * dinv;
           qx[k] = fma(c1i, v, qx[k]);
           Yb[k * YS + j] = c2j * v;
-          if (k & 1) qz1 = fma(cf.c[2][k], v, qz1);
-          else qz0 = fma(cf.c[2][k], v, qz0);
+          if (k & 1) qz1 = fma(Cc(2, k), v, qz1);
+          else qz0 = fma(Cc(2, k), v, qz0);
         }
         if (jok) {
           sQ[4 * N2 + i + NI * j] = qz0;
@@ -288,12 +315,12 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int q = min(tid + r * 256, N2 - 1), b = q / NI, a = q - b * NI;
-      const double fd = cf.F0[d] + sLt[la * 32 + a] + sLt[lb * 32 + b];
+      const double fd = F0[d] + sLt[la * 32 + a] + sLt[lb * 32 + b];
       const double self = sh[f * N2 + q], opp = sh[(f ^ 1) * N2 + q];
       const double ta = sEt[la * 32 + a] * fma(sgn(a), Ed[EA1[f] * NI + b], Ed[EA0[f] * NI + b]);
       const double tb = sEt[lb * 32 + b] * fma(sgn(b), Ed[EB1[f] * NI + a], Ed[EB0[f] * NI + a]);
       const double Q = fma(hi ? -1.0 : 1.0, sQ[(2 * d + 1) * N2 + q], sQ[2 * d * N2 + q]);
-      val[r] = fma(fd, self, fma(cf.k0p[d], opp, ta + tb)) - Q;
+      val[r] = fma(fd, self, fma(k0p[d], opp, ta + tb)) - Q;
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -335,7 +362,8 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
       const double t1 = (b0 ? fma(K0p, u10, K00 * u11) : fma(K00, u10, K0p * u11)) + eo_row_b(sLS + 2 * l1, b0);
       const double t2 = (b1 ? fma(K0p, u20, K00 * u21) : fma(K00, u20, K0p * u21)) + eo_row_b(sLS + 2 * l2, b1);
       const int o1 = grp == 0 ? 1 : 0, o2 = grp == 2 ? 1 : 2;
-      val = w02 * (cf.d[0] * uu + cf.d[1 + grp] * tal) + w0 * (cf.d[1 + o1] * t1 + cf.d[1 + o2] * t2);
+      auto dsel = [&](int q) { return q == 0 ? dd[1] : (q == 1 ? dd[2] : dd[3]); };   // no local-memory indexing
+      val = w02 * (dd[0] * uu + dsel(grp) * tal) + w0 * (dsel(o1) * t1 + dsel(o2) * t2);
     } else {
       const int v = t - 12 * NI, ib = v & 1, jb = (v >> 1) & 1, kb = v >> 2;
       const double uu = Vv[v];
@@ -347,27 +375,27 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
       const double tx = (ib ? fma(K0p, x0v, K00 * x1v) : fma(K00, x0v, K0p * x1v)) + eo_row_b(sES + 2 * (jb + 2 * kb), ib);
       const double ty = (jb ? fma(K0p, y0v, K00 * y1v) : fma(K00, y0v, K0p * y1v)) + eo_row_b(sES + 2 * (4 + ib + 2 * kb), jb);
       const double tz = (kb ? fma(K0p, z0v, K00 * z1v) : fma(K00, z0v, K0p * z1v)) + eo_row_b(sES + 2 * (8 + ib + 2 * jb), kb);
-      val = w02 * (w0 * cf.d[0] * uu + cf.d[1] * tx + cf.d[2] * ty + cf.d[3] * tz);
+      val = w02 * (w0 * dd[0] * uu + dd[1] * tx + dd[2] * ty + dd[3] * tz);
     }
     *dst = old + val;
   }
 }
 
-template <int NI>
+template <int NI, bool UNI>
 static int launch_big_t(const BigParams& P, cudaStream_t st, int* nl) {
   using B = BL<NI>;
   static_assert(sizeof(double) * B::TOTAL <= 225 * 1024, "shared memory budget");
   const size_t smem = sizeof(double) * B::TOTAL;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_apply_big<NI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_apply_big<NI, UNI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   for (int c = 0; c < 8; ++c) {
     const int cx = c & 1, cy = (c >> 1) & 1, cz = c >> 2;
     const long long n = (long long)((P.g.nx - cx + 1) >> 1) * ((P.g.ny - cy + 1) >> 1) * ((P.g.nz - cz + 1) >> 1);
     if (n <= 0) continue;
-    k_apply_big<NI><<<(unsigned)n, 256, smem, st>>>(P, c);
+    k_apply_big<NI, UNI><<<(unsigned)n, 256, smem, st>>>(P, c);
     (*nl)++;
   }
   return cudaGetLastError();
@@ -387,7 +415,7 @@ int launch_apply_big(const Geom& g, const double* x, double* y, const double* do
   memcpy(&P.cf, coef, sizeof(BigCoef));
   int rc = cudaErrorInvalidValue;
   switch (g.ni) {
-#define BCASE(N) case N: rc = launch_big_t<N>(P, st, nl); break;
+#define BCASE(N) case N: rc = g.uniform ? launch_big_t<N, true>(P, st, nl) : launch_big_t<N, false>(P, st, nl); break;
     BCASE(8) BCASE(9) BCASE(10) BCASE(11) BCASE(12) BCASE(13) BCASE(14) BCASE(15) BCASE(16) BCASE(17)
     BCASE(18) BCASE(19) BCASE(20) BCASE(21) BCASE(22) BCASE(23) BCASE(24) BCASE(25) BCASE(26) BCASE(27)
     BCASE(28) BCASE(29) BCASE(30) BCASE(31)

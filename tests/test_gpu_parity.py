@@ -90,9 +90,10 @@ def test_operator_parity_nodal(p, ne, lam):
     assert rel(y, ref) <= 1e-12
 
 
-@pytest.mark.parametrize("p", [3, 7])
+@pytest.mark.parametrize("p", [3, 7, 9, 13])
 def test_operator_parity_nonuniform_geometry(p):
-    g = nonuniform(p, (3, 2, 3), 0.4, seed=p)
+    """Per-element widths: v1 kernel for p <= 8, v4 with per-CTA coefficients for p >= 9."""
+    g = nonuniform(p, (3, 2, 3) if p < 12 else (2, 2, 3), 0.4, seed=p)
     op = operator.AssembledCondensedOperator(g)
     x = lattice_random(5, g.ne, g.p).ravel()
     ctx = ctx_for(g)
