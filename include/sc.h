@@ -129,8 +129,10 @@ sc_status sc_apply_condensed(sc_ctx* ctx, const double* d_x, double* d_y, void* 
 /* Solver BT: PCG with the diagonal preconditioner 1/diag(Rhat Htilde Rhat^T) in the
  * transformed system, x0 = 0, stop when ||r_k||_2 <= rtol ||b||_2 (recursive residual) or
  * after maxit iterations; rtol <= 0 runs exactly maxit iterations.  d_b, d_x: skeleton
- * vectors.  Synchronises the stream to poll convergence.  Non-convergence is SC_OK with
- * rep->converged = 0; p^T A p <= 0 returns SC_EBREAKDOWN. */
+ * vectors.  Synchronises the stream to poll convergence (every 8 iterations).  Non-convergence
+ * is SC_OK with rep->converged = 0; p^T A p <= 0 returns SC_EBREAKDOWN.  Single GPU: from the
+ * second 8-iteration chunk on, the chunk is replayed from a CUDA graph captured for d_x (the
+ * ctx owns the graph; a different d_x re-captures; environment SC_NO_GRAPH=1 disables it). */
 sc_status sc_pcg_solve(sc_ctx* ctx, const double* d_b, double* d_x, double rtol, int maxit,
                        sc_pcg_report* rep, void* stream);
 
