@@ -313,7 +313,14 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
   }
   // ---- v3 tile-column operator (n_I <= 7, uniform geometry): tile grid, look-back flags, corner records
   {
-    const char* env = getenv("SC_APPLY_V1");
+    // tiny grids (the launch-bound cfg1 / cfg2 sizes): the one-launch v1 kernel beats the
+    // tile-column march and the 8 colour launches (cfg2: 23 vs 41 us per application);
+    // SC_SMALL_V1=0 disables the switch (the parity tests use it to exercise the fast kernels)
+    const char* sv = getenv("SC_SMALL_V1");
+    const long long ne_local = (long long)nx * ny * nz;
+    const bool small_v1 = !(sv && sv[0] == '0') && ne_local <= (p <= 8 ? 2048 : 256);
+    const char* env0 = getenv("SC_APPLY_V1");
+    const char* env = small_v1 ? "1" : env0;
     bool sig_ok = true;
     for (int m = 0; m < ni; ++m) sig_ok &= (B.sigma[m] == ((m & 1) ? -1 : 1));
     const char* np2 = getenv("SC_NO_P2");

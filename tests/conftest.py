@@ -7,6 +7,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
+# The library runs tiny grids (<= 2048 elements at p <= 8, <= 256 above) on the one-launch v1
+# kernel; the parity tests use small grids, so they disable that switch to exercise the fast
+# kernels (tests that want the small-grid path re-enable it).
+os.environ.setdefault("SC_SMALL_V1", "0")
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built libsc.so")

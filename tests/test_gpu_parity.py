@@ -492,3 +492,16 @@ def test_pcg_graph_replay_matches_eager(monkeypatch):
     for (i0, c0, x0), (i1, c1, x1) in zip(eager, graph):
         assert i0 == i1 and c0 == c1
         assert torch.equal(x0, x1)
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2"])
+def test_small_grid_switch_parity(cfg, monkeypatch):
+    """Tiny grids run the one-launch v1 kernel by default (launch-bound sizes): operator parity
+    for cfg1 / cfg2 with the switch enabled."""
+    monkeypatch.setenv("SC_SMALL_V1", "1")
+    g = cfg1() if cfg == "cfg1" else cfg2()
+    op = operator.AssembledCondensedOperator(g)
+    x = lattice_random(3, g.ne, g.p).ravel()
+    ctx = ctx_for(g)
+    y, _, _ = gpu_apply_nodal(ctx, x)
+    assert rel(y, op.apply(x)) <= 1e-12
