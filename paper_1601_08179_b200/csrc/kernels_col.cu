@@ -1314,6 +1314,7 @@ __global__ void __launch_bounds__(256, 1) k_apply_col(const __grid_constant__ Co
                          g.off_e[0] + g.n_e[0] * NI, g.off_e[1] + g.n_e[1] * NI, g.off_e[2] + g.n_e[2] * NI,
                          g.off_v + g.n_v};
     long long nexts[7] = {g.off_f[1], g.off_f[2], g.off_e[0], g.off_e[1], g.off_e[2], g.off_v, g.n_total};
+#pragma unroll 1
     for (int q = 0; q < 7; ++q)
       for (long long i = ends[q] + tid; i < nexts[q]; i += NT) P.y[i] = 0.0;
   }
