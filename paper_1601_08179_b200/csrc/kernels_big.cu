@@ -39,7 +39,12 @@ struct BL {
   static constexpr int N2 = NI * NI;
   static constexpr int SW = NI <= 16 ? 16 : 32;   // lanes per j-group
   static constexpr int H = 32 / SW;                // j-groups per warp
-  static constexpr int NG = 8 * H;                 // residue classes of i
+  // warps per CTA: 4 where that lets two CTAs share an SM (17 <= n_I <= 23: <= 113 KB of shared
+  // memory, <= 255 registers), so one CTA's gather / tree / output phases overlap the other's
+  // condensed part; otherwise 8 (one CTA per SM at n_I >= 24, three at n_I <= 16)
+  static constexpr int NW = (NI >= 17 && NI <= 23) ? 4 : 8, NT = 32 * NW;
+  static constexpr int MINB = NW == 4 ? 2 : 1;
+  static constexpr int NG = NW * H;                // residue classes of i
   static constexpr int NIT = (NI + NG - 1) / NG;   // i values per thread
   static constexpr int SH = 6 * N2 + 12 * NI + 8;  // shell: faces w e s n b t | 12 edges | 8 vertices
   static constexpr int O_SH = 0;
@@ -49,8 +54,8 @@ struct BL {
   static constexpr int O_ES = O_LS + 24 * NI;      // edge line sums [12][2]
   static constexpr int YS = SW + 1;                // row stride of the Qy transpose buffers
   static constexpr int O_Y = O_ES + 24;            // [8 H][NI][YS]; reused by the Qx tree
-  static constexpr int TOTAL = O_Y + 8 * H * NI * YS;
-  static_assert(4 * H * NI * SW <= 8 * H * NI * YS, "Qx tree slots");
+  static constexpr int TOTAL = O_Y + NW * H * NI * YS;
+  static_assert((NW / 2) * H * NI * SW <= NW * H * NI * YS, "Qx tree slots");
 };
 
 __device__ __forceinline__ void cp_async8b(double* smem, const double* gmem) {
@@ -64,9 +69,9 @@ __device__ __forceinline__ double eo_row_b(const double* r, int hi) { return hi 
 // operands); otherwise each CTA derives them from its element's d_e (metric) into shared
 // memory (graded / anisotropic non-uniform grids).
 template <int NI, bool UNI>
-__global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ BigParams P, int colour) {
+__global__ void __launch_bounds__(BL<NI>::NT, BL<NI>::MINB) k_apply_big(const __grid_constant__ BigParams P, int colour) {
   using B = BL<NI>;
-  constexpr int N2 = B::N2, SW = B::SW, H = B::H, NG = B::NG, YS = B::YS;
+  constexpr int N2 = B::N2, SW = B::SW, H = B::H, NG = B::NG, YS = B::YS, NT = B::NT, NW = B::NW;
   if (P.done != nullptr && *P.done != 0.0) return;
   extern __shared__ double sm[];
   __shared__ long long sBase[26];
@@ -91,15 +96,17 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
     metric(g, ex, ey, ez, dd);
   }
   __shared__ double sCg[3 * 32], sDlg[3 * 32];   // non-uniform: c[d][m], dl[d][m] of this element
-  if constexpr (UNI) {
-    sT[tid] = tid < 96 ? (&cf.L[0][0])[tid] : tid < 192 ? (&cf.e[0][0])[tid - 96] : tid < 224 ? cf.a0[tid - 192] : cf.lam[tid - 224];
-  } else {
-    const int q = (tid >> 5) % 3, m = tid & 31;
-    sT[tid] = tid < 96 ? dd[1 + q] * cf.w0 * cf.lam[m] : tid < 192 ? dd[1 + q] * cf.w0 * cf.a0[m]
-                                                        : tid < 224 ? cf.a0[tid - 192] : cf.lam[tid - 224];
-    if (tid < 96) {
-      sCg[tid] = dd[1 + q] * cf.a0[m];
-      sDlg[tid] = dd[1 + q] * cf.lam[m];
+  for (int t = tid; t < 256; t += NT) {
+    if constexpr (UNI) {
+      sT[t] = t < 96 ? (&cf.L[0][0])[t] : t < 192 ? (&cf.e[0][0])[t - 96] : t < 224 ? cf.a0[t - 192] : cf.lam[t - 224];
+    } else {
+      const int q = (t >> 5) % 3, m = t & 31;
+      sT[t] = t < 96 ? dd[1 + q] * cf.w0 * cf.lam[m] : t < 192 ? dd[1 + q] * cf.w0 * cf.a0[m]
+                                                      : t < 224 ? cf.a0[t - 192] : cf.lam[t - 224];
+      if (t < 96) {
+        sCg[t] = dd[1 + q] * cf.a0[m];
+        sDlg[t] = dd[1 + q] * cf.lam[m];
+      }
     }
   }
   auto Cc = [&](int q, int m) -> double { if constexpr (UNI) return cf.c[q][m]; else return sCg[q * 32 + m]; };
@@ -126,15 +133,15 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
     const double* src = P.x + sBase[f];
     const bool dr = sDir[f];
 #pragma unroll
-    for (int r = 0; r < (N2 + 255) / 256; ++r) {
-      const int q = tid + r * 256;
+    for (int r = 0; r < (N2 + NT - 1) / NT; ++r) {
+      const int q = tid + r * NT;
       if (q < N2) {
         if (dr) sh[f * N2 + q] = 0.0;
         else cp_async8b(sh + f * N2 + q, src + q);
       }
     }
   }
-  for (int t = tid; t < 12 * NI + 8; t += 256) {
+  for (int t = tid; t < 12 * NI + 8; t += NT) {
     int ent, loc;
     if (t < 12 * NI) { const int e = t / NI; ent = 6 + e; loc = t - e * NI; }
     else { ent = 18 + (t - 12 * NI); loc = 0; }
@@ -146,19 +153,19 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
   // this colour touches them).  n_I <= 16 keeps the registers for occupancy (3 CTAs per SM) and
   // loads them in the output phase.
   constexpr bool EARLY = NI > 16;
-  constexpr int RF = (N2 + 255) / 256, RE = (12 * NI + 8 + 255) / 256;
+  constexpr int RF = (N2 + NT - 1) / NT, RE = (12 * NI + 8 + NT - 1) / NT;
   double yold[6][RF], yoldE[RE];
   auto load_yold = [&]() {
 #pragma unroll
     for (int f = 0; f < 6; ++f)
 #pragma unroll
       for (int r = 0; r < RF; ++r) {
-        const int q = tid + r * 256;
+        const int q = tid + r * NT;
         yold[f][r] = (q < N2 && !sDir[f]) ? P.y[sBase[f] + q] : 0.0;
       }
 #pragma unroll
     for (int r = 0; r < RE; ++r) {
-      const int t = tid + r * 256;
+      const int t = tid + r * NT;
       yoldE[r] = 0.0;
       if (t < 12 * NI + 8) {
         const int ent = t < 12 * NI ? 6 + t / NI : 18 + (t - 12 * NI);
@@ -174,13 +181,13 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
   double* const sQ = sm + B::O_Q;
   double* const sLS = sm + B::O_LS;
   double* const sES = sm + B::O_ES;
-  for (int t = tid; t < 3 * N2; t += 256) {
+  for (int t = tid; t < 3 * N2; t += NT) {
     const int f = t / N2, q = t - f * N2;
     const double lo = sh[2 * f * N2 + q], hi = sh[(2 * f + 1) * N2 + q];
     sP[2 * f * N2 + q] = lo + hi;
     sP[(2 * f + 1) * N2 + q] = lo - hi;
   }
-  for (int t = tid; t < 12 * NI + 12; t += 256) {
+  for (int t = tid; t < 12 * NI + 12; t += NT) {
     const double* F;
     int st;
     if (t < 12 * NI) {   // (face f, d): d = 0 sums over the first coordinate a at b = c, d = 1 over b at a = c
@@ -272,7 +279,7 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
     constexpr int STMIN = H == 1 ? 2 : 1;
     double* const slots = sm + B::O_Y;
 #pragma unroll 1
-    for (int st = 4; st >= STMIN; st >>= 1) {
+    for (int st = NW / 2; st >= STMIN; st >>= 1) {
       __syncthreads();
       if (warp >= st && warp < 2 * st) {
         double* sl = slots + ((warp - st) * H + h) * NI * SW + j;
@@ -314,7 +321,7 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
     double val[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const int q = min(tid + r * 256, N2 - 1), b = q / NI, a = q - b * NI;
+      const int q = min(tid + r * NT, N2 - 1), b = q / NI, a = q - b * NI;
       const double fd = F0[d] + sLt[la * 32 + a] + sLt[lb * 32 + b];
       const double self = sh[f * N2 + q], opp = sh[(f ^ 1) * N2 + q];
       const double ta = sEt[la * 32 + a] * fma(sgn(a), Ed[EA1[f] * NI + b], Ed[EA0[f] * NI + b]);
@@ -324,14 +331,14 @@ __global__ void __launch_bounds__(256, 1) k_apply_big(const __grid_constant__ Bi
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const int q = tid + r * 256;
+      const int q = tid + r * NT;
       if (q < N2) yf[q] = yold[f][r] + val[r];
     }
   }
   // edges (one thread per edge node) and vertices
 #pragma unroll
   for (int rr = 0; rr < RE; ++rr) {
-    const int t = tid + rr * 256;
+    const int t = tid + rr * NT;
     if (t >= 12 * NI + 8) continue;
     const int ent = t < 12 * NI ? 6 + t / NI : 18 + (t - 12 * NI);
     if (sDir[ent]) continue;
@@ -395,7 +402,7 @@ static int launch_big_t(const BigParams& P, cudaStream_t st, int* nl) {
     const int cx = c & 1, cy = (c >> 1) & 1, cz = c >> 2;
     const long long n = (long long)((P.g.nx - cx + 1) >> 1) * ((P.g.ny - cy + 1) >> 1) * ((P.g.nz - cz + 1) >> 1);
     if (n <= 0) continue;
-    k_apply_big<NI, UNI><<<(unsigned)n, 256, smem, st>>>(P, c);
+    k_apply_big<NI, UNI><<<(unsigned)n, B::NT, smem, st>>>(P, c);
     (*nl)++;
   }
   return cudaGetLastError();
