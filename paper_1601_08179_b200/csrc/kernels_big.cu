@@ -39,10 +39,10 @@ struct BL {
   static constexpr int N2 = NI * NI;
   static constexpr int SW = NI <= 16 ? 16 : 32;   // lanes per j-group
   static constexpr int H = 32 / SW;                // j-groups per warp
-  // warps per CTA: 4 where that lets two CTAs share an SM (17 <= n_I <= 23: <= 113 KB of shared
-  // memory, <= 255 registers), so one CTA's gather / tree / output phases overlap the other's
-  // condensed part; otherwise 8 (one CTA per SM at n_I >= 24, three at n_I <= 16)
-  static constexpr int NW = (NI >= 17 && NI <= 23) ? 4 : 8, NT = 32 * NW;
+  // warps per CTA: 4 up to n_I = 23 (two or more CTAs share an SM, so one CTA's gather / tree /
+  // output phases overlap another's condensed part; measured p=12 -3.6 %, p=16 -4.6 %,
+  // p=24 -15 % against 8 warps); 8 from n_I = 24 (one CTA per SM: 213 KB at n_I = 31)
+  static constexpr int NW = (NI >= 8 && NI <= 23) ? 4 : 8, NT = 32 * NW;
   static constexpr int MINB = NW == 4 ? 2 : 1;
   static constexpr int NG = NW * H;                // residue classes of i
   static constexpr int NIT = (NI + NG - 1) / NG;   // i values per thread
