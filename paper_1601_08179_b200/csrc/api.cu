@@ -311,7 +311,9 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
       return fail("cudaMemcpy dinv");
     g.dinv = ctx->d_dinv;
   }
-  // ---- v3 tile-column operator (n_I <= 7, uniform geometry): tile grid, look-back flags, corner records
+  // ---- operator kernel selection: p = 2 row-warp, p = 3, 4 row-warp with staging,
+  // 5 <= p <= 8 tile-column v3 (uniform geometry), 9 <= p <= 32 colour element v4 (any geometry),
+  // v1 for tiny grids and non-uniform p <= 8
   {
     // tiny grids (the launch-bound cfg1 / cfg2 sizes): the one-launch v1 kernel beats the
     // tile-column march and the 8 colour launches (cfg2: 23 vs 41 us per application);
@@ -324,10 +326,11 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
     bool sig_ok = true;
     for (int m = 0; m < ni; ++m) sig_ok &= (B.sigma[m] == ((m & 1) ? -1 : 1));
     const char* np2 = getenv("SC_NO_P2");
+    const char* nrw = getenv("SC_NO_RW");
     if (ni == 1 && uniform && sig_ok && !(env && env[0] == '1') && !(np2 && np2[0] == '1')) {
       big_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->big_coef);
       ctx->use_p2 = true;
-    } else if (rw_supported(ni) && uniform && sig_ok && !(env && env[0] == '1') && !(getenv("SC_NO_RW") && getenv("SC_NO_RW")[0] == '1')) {
+    } else if (rw_supported(ni) && uniform && sig_ok && !(env && env[0] == '1') && !(nrw && nrw[0] == '1')) {
       big_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->big_coef);
       ctx->use_rw = true;
     } else if (col_supported(ni) && uniform && sig_ok && !(env && env[0] == '1')) {
