@@ -25,6 +25,7 @@
 // barrier-separated rounds; the two elements of an x- (y-) face are summed with a lane shuffle.
 // The primary part (Htilde_BB, Eq. 26 generalised) is applied entity-centrically.
 #include <cuda_runtime.h>
+#include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 #include "sc_device.cuh"
@@ -223,9 +224,25 @@ __device__ __forceinline__ void cp8(unsigned s, const double* g) {
 __device__ __forceinline__ void row_load(double* sb, const double* gb, int len, int zlo, int zhi, int lane) {
   for (int t = lane; t < zlo; t += 32) sb[t] = 0.0;
   for (int t = zhi + lane; t < len; t += 32) sb[t] = 0.0;
-  unsigned s = (unsigned)__cvta_generic_to_shared(sb + zlo + lane);
-  const double* gp = gb + zlo + lane;
-  for (int n = zhi - zlo - lane; n > 0; n -= 128, s += 1024u, gp += 128) {   // predicated 4-wide, no tail loop
+  const unsigned s0 = (unsigned)__cvta_generic_to_shared(sb + zlo);
+  const double* g0 = gb + zlo;
+  const int cnt = zhi - zlo;
+  if (cnt > 8 && ((s0 ^ (unsigned)reinterpret_cast<uintptr_t>(g0)) & 15u) == 0) {
+    // both sides at the same 16-byte phase: an 8-byte head if needed, then 16-byte copies
+    const int h = (s0 & 15u) ? 1 : 0, npair = (cnt - h) >> 1;
+    if (h && lane == 0) cp8(s0, g0);
+    if (((cnt - h) & 1) && lane == 1) cp8(s0 + 8u * (cnt - 1), g0 + cnt - 1);
+    unsigned s = s0 + 8u * h + 16u * lane;
+    const double* gp = g0 + h + 2 * lane;
+    for (int n = npair - lane; n > 0; n -= 64, s += 1024u, gp += 128) {
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gp) : "memory");
+      if (n > 32) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s + 512u), "l"(gp + 64) : "memory");
+    }
+    return;
+  }
+  unsigned s = s0 + 8u * lane;
+  const double* gp = g0 + lane;
+  for (int n = cnt - lane; n > 0; n -= 128, s += 1024u, gp += 128) {   // predicated 4-wide, no tail loop
     cp8(s, gp);
     if (n > 32) cp8(s + 256u, gp + 32);
     if (n > 64) cp8(s + 512u, gp + 64);
