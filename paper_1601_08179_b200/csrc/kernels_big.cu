@@ -52,7 +52,9 @@ struct BL {
   static constexpr int O_Q = O_P + 6 * N2;         // Qx^0 Qx^1 Qy^0 Qy^1 Qz^0 Qz^1
   static constexpr int O_LS = O_Q + 6 * N2;        // face line sums [6][2][NI][2] (R+, R-)
   static constexpr int O_ES = O_LS + 24 * NI;      // edge line sums [12][2]
-  static constexpr int YS = SW + 1;                // row stride of the Qy transpose buffers
+  // row stride of the Qy transpose buffers: SW + 2, so that the reduction's lanes (k, s) read
+  // rows k at column offset s from 16 distinct bank pairs per half-warp (SW + 1: 2-way conflicts)
+  static constexpr int YS = SW + 2;
   static constexpr int O_Y = O_ES + 24;            // [8 H][NI][YS]; reused by the Qx tree
   static constexpr int TOTAL = O_Y + NW * H * NI * YS;
   static_assert((NW / 2) * H * NI * SW <= NW * H * NI * YS, "Qx tree slots");
@@ -68,7 +70,7 @@ __device__ __forceinline__ double eo_row_b(const double* r, int hi) { return hi 
 // UNI: uniform geometry (the d-dependent coefficients are kernel parameters, constant-bank
 // operands); otherwise each CTA derives them from its element's d_e (metric) into shared
 // memory (graded / anisotropic non-uniform grids).
-template <int NI, bool UNI>
+template <int NI, bool UNI, int CH>
 __global__ void __launch_bounds__(BL<NI>::NT, BL<NI>::MINB) k_apply_big(const __grid_constant__ BigParams P, int colour) {
   using B = BL<NI>;
   constexpr int N2 = B::N2, SW = B::SW, H = B::H, NG = B::NG, YS = B::YS, NT = B::NT, NW = B::NW;
@@ -136,8 +138,12 @@ __global__ void __launch_bounds__(BL<NI>::NT, BL<NI>::MINB) k_apply_big(const __
     for (int r = 0; r < (N2 + NT - 1) / NT; ++r) {
       const int q = tid + r * NT;
       if (q < N2) {
+#if defined(SC_EXP) && SC_EXP == 43
+        sh[f * N2 + q] = (double)q;   // ablation (timing only): no shell gather of the faces
+#else
         if (dr) sh[f * N2 + q] = 0.0;
         else cp_async8b(sh + f * N2 + q, src + q);
+#endif
       }
     }
   }
@@ -161,7 +167,11 @@ __global__ void __launch_bounds__(BL<NI>::NT, BL<NI>::MINB) k_apply_big(const __
 #pragma unroll
       for (int r = 0; r < RF; ++r) {
         const int q = tid + r * NT;
+#if defined(SC_EXP) && SC_EXP == 44
+        yold[f][r] = 0.0;   // ablation (timing only): no read of y before the face stores
+#else
         yold[f][r] = (q < N2 && !sDir[f]) ? P.y[sBase[f] + q] : 0.0;
+#endif
       }
 #pragma unroll
     for (int r = 0; r < RE; ++r) {
@@ -238,21 +248,58 @@ __global__ void __launch_bounds__(BL<NI>::NT, BL<NI>::MINB) k_apply_big(const __
         // 1-3 CTAs per SM an L2 table load per point stalls the loop (measured 6-12 % slower)
         const double dij = dd[0] + Dl(0, i) + sDl1[jc];
         double qz0 = 0.0, qz1 = 0.0;
+        if constexpr (CH > 0) {
+          // The k line in chunks of CH points, software-pipelined by hand: the operand loads of
+          // chunk c + 1 are issued before the transpose stores of chunk c (all in one dynamic shared
+          // array, so the compiler may not move a load above an earlier store: written point by
+          // point, the line ran as one serial load -> arithmetic -> store chain).
+          const double* const px = Pxs + jc;
+          double* const yb = Yb + j;
+          double ax[NI], ay[NI], vv[NI];
+  #pragma unroll
+          for (int k = 0; k < CH && k < NI; ++k) { ax[k] = px[NI * k]; ay[k] = Pyi[NI * k]; }
+  #pragma unroll
+          for (int c0 = 0; c0 < NI; c0 += CH) {
+  #pragma unroll
+            for (int k = c0; k < c0 + CH && k < NI; ++k) {
+              const double u = fma(c1i, ax[k], fma(c2j, ay[k], Cc(2, k) * ((k & 1) ? pz1 : pz0)));
+              const double D = dij + Dl(2, k);
+              double r;
+              asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(D));
+              double e = fma(-D, r, 1.0);
+              r = fma(r, e, r);
+              e = fma(-D, r, 1.0);
+              const double dinv = fma(r, e, r);
+              const double v = u * dinv;
+              vv[k] = v;
+              qx[k] = fma(c1i, v, qx[k]);
+              if (k & 1) qz1 = fma(Cc(2, k), v, qz1);
+              else qz0 = fma(Cc(2, k), v, qz0);
+            }
+  #pragma unroll
+            for (int k = c0 + CH; k < c0 + 2 * CH && k < NI; ++k) { ax[k] = px[NI * k]; ay[k] = Pyi[NI * k]; }
+  #pragma unroll
+            for (int k = c0; k < c0 + CH && k < NI; ++k) yb[k * YS] = c2j * vv[k];
+          }
+        } else {
+          // point by point (CH = 0): fewer registers; chosen where the pipelined form would cost
+          // a CTA per SM (launch_big_t)
 #pragma unroll
-        for (int k = 0; k < NI; ++k) {
-          const double u = fma(c1i, Pxs[jc + NI * k], fma(c2j, Pyi[NI * k], Cc(2, k) * ((k & 1) ? pz1 : pz0)));
-          const double D = dij + Dl(2, k);
-          double r;
-          asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(D));
-          double e = fma(-D, r, 1.0);
-          r = fma(r, e, r);
-          e = fma(-D, r, 1.0);
-          const double dinv = fma(r, e, r);
-          const double v = u * dinv;
-          qx[k] = fma(c1i, v, qx[k]);
-          Yb[k * YS + j] = c2j * v;
-          if (k & 1) qz1 = fma(Cc(2, k), v, qz1);
-          else qz0 = fma(Cc(2, k), v, qz0);
+          for (int k = 0; k < NI; ++k) {
+            const double u = fma(c1i, Pxs[jc + NI * k], fma(c2j, Pyi[NI * k], Cc(2, k) * ((k & 1) ? pz1 : pz0)));
+            const double D = dij + Dl(2, k);
+            double r;
+            asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(D));
+            double e = fma(-D, r, 1.0);
+            r = fma(r, e, r);
+            e = fma(-D, r, 1.0);
+            const double dinv = fma(r, e, r);
+            const double v = u * dinv;
+            qx[k] = fma(c1i, v, qx[k]);
+            Yb[k * YS + j] = c2j * v;
+            if (k & 1) qz1 = fma(Cc(2, k), v, qz1);
+            else qz0 = fma(Cc(2, k), v, qz0);
+          }
         }
         if (jok) {
           sQ[4 * N2 + i + NI * j] = qz0;
@@ -388,21 +435,33 @@ __global__ void __launch_bounds__(BL<NI>::NT, BL<NI>::MINB) k_apply_big(const __
   }
 }
 
+// Two builds of every kernel: the k line point by point (CH = 0) or software-pipelined in
+// chunks of 2 (CH = 2, more registers).  The pipelined one is used unless its register count
+// costs resident CTAs per SM (measured: p = 9 2.61 -> 2.42 ms, p = 16 1.08 -> 1.02, p = 20
+// 1.38 -> 1.17, p = 24 1.11 -> 0.94, p = 32 0.91 -> 0.86; p = 12 keeps CH = 0: 4 instead of 5
+// CTAs per SM would make it 9 % slower).
+template <int NI, bool UNI, int CH>
+static int occupancy_big(size_t smem) {
+  cudaFuncSetAttribute(k_apply_big<NI, UNI, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_apply_big<NI, UNI, CH>, BL<NI>::NT, smem) != cudaSuccess)
+    return 0;
+  return nb;
+}
+
 template <int NI, bool UNI>
 static int launch_big_t(const BigParams& P, cudaStream_t st, int* nl) {
   using B = BL<NI>;
   static_assert(sizeof(double) * B::TOTAL <= 225 * 1024, "shared memory budget");
   const size_t smem = sizeof(double) * B::TOTAL;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_apply_big<NI, UNI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  static int pipelined = -1;
+  if (pipelined < 0) pipelined = occupancy_big<NI, UNI, 2>(smem) >= occupancy_big<NI, UNI, 0>(smem) ? 1 : 0;
   for (int c = 0; c < 8; ++c) {
     const int cx = c & 1, cy = (c >> 1) & 1, cz = c >> 2;
     const long long n = (long long)((P.g.nx - cx + 1) >> 1) * ((P.g.ny - cy + 1) >> 1) * ((P.g.nz - cz + 1) >> 1);
     if (n <= 0) continue;
-    k_apply_big<NI, UNI><<<(unsigned)n, B::NT, smem, st>>>(P, c);
+    if (pipelined) k_apply_big<NI, UNI, 2><<<(unsigned)n, B::NT, smem, st>>>(P, c);
+    else k_apply_big<NI, UNI, 0><<<(unsigned)n, B::NT, smem, st>>>(P, c);
     (*nl)++;
   }
   return cudaGetLastError();
