@@ -204,24 +204,35 @@ __global__ void __launch_bounds__(256, SC_P2_MINB) k_apply_p2(const __grid_const
     }
   }
   double* Y = P.y;
-  double old[17];
+  // the last lane's ib = 1 entities (next chunk's W side) join the batch: all old values are
+  // loaded before the first store (a load after a store to y cannot be moved above it, so
+  // read-modify-writes issued one by one run as a chain of DRAM round trips)
+  const long long ae = xf(ex + 1, ey, ez);
+  const bool lx = last && !dX1;
+  long long at_[9];
+  bool mt_[9];
+  double wt_[9];
+  int nt = 0;
+  auto putt = [&](long long a, bool ok, double val) { at_[nt] = a; mt_[nt] = ok; wt_[nt] = val; ++nt; };
+  putt(ae, lx, oE);
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    putt(ye(ex + 1, ey, ez + b), lx && !dZ[b], oY[1][b]);
+    putt(ze(ex + 1, ey + b, ez), lx && !dY[b], oZ[1][b]);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) putt(vx(ex + 1, ey + b, ez + c), lx && !(dY[b] || dZ[c]), oV[1][b][c]);
+  }
+  double old[17], oldt[9];
 #pragma unroll
   for (int q = 0; q < 17; ++q) old[q] = m_[q] ? Y[a_[q]] : 0.0;
 #pragma unroll
+  for (int q = 0; q < 9; ++q) oldt[q] = mt_[q] ? Y[at_[q]] : 0.0;
+#pragma unroll
   for (int q = 0; q < 17; ++q)
     if (m_[q]) Y[a_[q]] = old[q] + w_[q];
-  if (last) {
-    const long long ae = xf(ex + 1, ey, ez);
-    if (!dX1) Y[ae] += oE;
 #pragma unroll
-    for (int b = 0; b < 2; ++b) {
-      if (!(dX1 || dZ[b])) Y[ye(ex + 1, ey, ez + b)] += oY[1][b];
-      if (!(dX1 || dY[b])) Y[ze(ex + 1, ey + b, ez)] += oZ[1][b];
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-        if (!(dX1 || dY[b] || dZ[c])) Y[vx(ex + 1, ey + b, ez + c)] += oV[1][b][c];
-    }
-  }
+  for (int q = 0; q < 9; ++q)
+    if (mt_[q]) Y[at_[q]] = oldt[q] + wt_[q];
 }
 
 int launch_apply_p2(const Geom& g, const double* x, double* y, const double* done, const void* coef, void* stream,

@@ -49,12 +49,21 @@ __device__ __forceinline__ double eorow(double rp, double rm, int hi) { return h
 
 // Row [0, cap) of per-entity blocks of `per` doubles: entities [0, n) from global `g` (entity 0
 // zero if zlo, entity n-1 zero if zhi, all zero if dir), the rest zero.
+// The same range of y (read-modify-written at the end) is prefetched into L2 (one prefetch per
+// 64 bytes): the output phase's read-modify-writes are issued one entity group after another (a
+// load of y cannot move above an earlier store to y), so each group waits for its loads.
 __device__ __forceinline__ void rw_row(double* s, const double* g, int n, int cap, int per, bool dir, bool zlo,
-                                       bool zhi, int lane) {
+                                       bool zhi, int lane, ptrdiff_t ydelta) {
   const int len = n * per, lo = zlo ? per : 0, hi = zhi ? len - per : len;
   for (int t = lane; t < cap * per; t += 32) {
-    if (t < len && !dir && t >= lo && t < hi) cp8rw(s + t, g + t);
-    else s[t] = 0.0;
+    if (t < len && !dir && t >= lo && t < hi) {
+      cp8rw(s + t, g + t);
+#if !(defined(SC_EXP) && SC_EXP == 46)
+      if ((t & 7) == 0 || t == lo) asm volatile("prefetch.global.L2 [%0];" ::"l"(g + ydelta + t));
+#endif
+    } else {
+      s[t] = 0.0;
+    }
   }
 }
 
@@ -82,23 +91,24 @@ __global__ void __launch_bounds__(128) k_apply_rw(const __grid_constant__ RWPara
   const bool zx0 = x0 == 0, zx1 = x0 + nel == nx;     // x-planes fx = 0 / nx inside this chunk
   // ---- a3: the rows of this chunk (Dirichlet entities as 0)
   const double* X = P.x;
-  rw_row(sm + L::XF, X + g.off_f[0] + (x0 + nx1 * (ey + (long long)ny * ez)) * N2, nel + 1, 33, N2, false, zx0, zx1, lane);
+  const ptrdiff_t yd = P.y - P.x;   // y row = x row + yd (same layout)
+  rw_row(sm + L::XF, X + g.off_f[0] + (x0 + nx1 * (ey + (long long)ny * ez)) * N2, nel + 1, 33, N2, false, zx0, zx1, lane, yd);
 #pragma unroll
   for (int b = 0; b < 2; ++b) {
     rw_row(sm + L::YF + b * 32 * N2, X + g.off_f[1] + (x0 + (long long)nx * (ey + b + ny1 * ez)) * N2, nel, 32, N2,
-           dY[b], false, false, lane);
+           dY[b], false, false, lane, yd);
     rw_row(sm + L::ZF + b * 32 * N2, X + g.off_f[2] + (x0 + (long long)nx * (ey + (long long)ny * (ez + b))) * N2, nel,
-           32, N2, dZ[b], false, false, lane);
+           32, N2, dZ[b], false, false, lane, yd);
     rw_row(sm + L::YE + b * 33 * NI, X + g.off_e[1] + (x0 + nx1 * (ey + (long long)ny * (ez + b))) * NI, nel + 1, 33, NI,
-           dZ[b], zx0, zx1, lane);
+           dZ[b], zx0, zx1, lane, yd);
     rw_row(sm + L::ZE + b * 33 * NI, X + g.off_e[2] + (x0 + nx1 * (ey + b + ny1 * ez)) * NI, nel + 1, 33, NI, dY[b], zx0,
-           zx1, lane);
+           zx1, lane, yd);
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       rw_row(sm + L::XE + (b + 2 * c) * 32 * NI, X + g.off_e[0] + (x0 + (long long)nx * (ey + b + ny1 * (ez + c))) * NI,
-             nel, 32, NI, dY[b] || dZ[c], false, false, lane);
+             nel, 32, NI, dY[b] || dZ[c], false, false, lane, yd);
       rw_row(sm + L::VV + (b + 2 * c) * 33, X + g.off_v + x0 + nx1 * (ey + b + ny1 * (ez + c)), nel + 1, 33, 1,
-             dY[b] || dZ[c], zx0, zx1, lane);
+             dY[b] || dZ[c], zx0, zx1, lane, yd);
     }
   }
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
