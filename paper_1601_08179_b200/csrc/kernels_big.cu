@@ -454,8 +454,10 @@ static int launch_big_t(const BigParams& P, cudaStream_t st, int* nl) {
   using B = BL<NI>;
   static_assert(sizeof(double) * B::TOTAL <= 225 * 1024, "shared memory budget");
   const size_t smem = sizeof(double) * B::TOTAL;
-  static int pipelined = -1;
-  if (pipelined < 0) pipelined = occupancy_big<NI, UNI, 2>(smem) >= occupancy_big<NI, UNI, 0>(smem) ? 1 : 0;
+  static int auto_pipe = -1;   // (the occupancy queries also set both builds' shared-memory limit)
+  if (auto_pipe < 0) auto_pipe = occupancy_big<NI, UNI, 2>(smem) >= occupancy_big<NI, UNI, 0>(smem) ? 1 : 0;
+  const char* force = getenv("SC_V4_PIPE");   // tests: 0 / 1 force a build (same arithmetic, same order)
+  const int pipelined = (force && (force[0] == '0' || force[0] == '1')) ? force[0] - '0' : auto_pipe;
   for (int c = 0; c < 8; ++c) {
     const int cx = c & 1, cy = (c >> 1) & 1, cz = c >> 2;
     const long long n = (long long)((P.g.nx - cx + 1) >> 1) * ((P.g.ny - cy + 1) >> 1) * ((P.g.nz - cz + 1) >> 1);

@@ -463,6 +463,29 @@ def test_operator_bitwise_repeatable(p, ne):
         assert torch.equal(y, y0)
 
 
+@pytest.mark.parametrize("p,ne,uniform", [(9, (5, 4, 3), True), (12, (4, 3, 3), True), (17, (3, 3, 2), True),
+                                          (13, (3, 2, 3), False)])
+def test_big_pipelined_build_bitwise(p, ne, uniform, monkeypatch):
+    """The v4 kernel has two builds of the k line (point by point; software-pipelined in chunks of
+    2), picked per n_I by occupancy.  Both perform the same operations in the same order, so
+    forcing either (SC_V4_PIPE=0 / 1) gives bitwise identical results, on uniform and non-uniform
+    grids."""
+    g = small_grid(p, ne, 1.0) if uniform else nonuniform(p, ne, 1.0, seed=p)
+    ctx = ctx_for(g)
+    x = ctx.skeleton()
+    ctx.sc_fill_random(5, x)
+    out = []
+    for mode in ("0", "1"):
+        monkeypatch.setenv("SC_V4_PIPE", mode)
+        y = ctx.skeleton(fill=float("nan"))
+        ctx.sc_apply_condensed(x, y)
+        torch.cuda.synchronize()
+        out.append(y)
+    monkeypatch.delenv("SC_V4_PIPE")
+    assert torch.isfinite(out[0]).all()
+    assert torch.equal(out[0], out[1])
+
+
 def test_pcg_graph_replay_matches_eager(monkeypatch):
     """sc_pcg_solve replays 8-iteration chunks from a CUDA graph (captured at the second chunk
     for a given iterate buffer): repeated solves, a second iterate buffer (re-capture), a
