@@ -351,7 +351,7 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
       if (cudaMalloc(&ctx->d_colstate, 64) != cudaSuccess) return fail("cudaMalloc colstate");
       if (cudaMalloc(&ctx->d_flags, sizeof(int) * nflags) != cudaSuccess) return fail("cudaMalloc flags");
       if (cudaMalloc(&ctx->d_corner, sizeof(double) * ncorner) != cudaSuccess) return fail("cudaMalloc corner");
-      size_t npend = nitems * 4 * pend;   // kLB + 1 = 4 step slots (look-back distance 3, kernels_col.cu)
+      size_t npend = nitems * col_slots() * pend;   // look-back distance + 1 step slots (kernels_col.cu)
       if (cudaMalloc(&ctx->d_pending, sizeof(double) * npend) != cudaSuccess) return fail("cudaMalloc pending");
       if (cudaMalloc(&ctx->d_dotp, sizeof(double) * nitems) != cudaSuccess)
         return fail("cudaMalloc dotp");

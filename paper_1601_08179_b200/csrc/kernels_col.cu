@@ -70,7 +70,10 @@ struct ColParams {
 // decoupled look-back distance: a tile finishes its W / S boundary entities of step l - kLB at
 // step l (neighbours publish step l - kLB at their step l - kLB + 1: kLB - 1 steps of slack);
 // own partials are parked in kSlots = kLB + 1 rotating slots
-constexpr int kLB = 3, kSlots = kLB + 1;
+#ifndef SC_KLB
+#define SC_KLB 3
+#endif
+constexpr int kLB = SC_KLB, kSlots = kLB + 1;
 template <int NI>
 struct CS {
   static constexpr int N2 = NI * NI;
@@ -691,6 +694,9 @@ __device__ void finish_gather(const ColParams& P, long long item, int ls, int x0
       o = sRow[4 * TY + 5] + 1 + (t - c7); po = C::PD_VS + (t - c7);
     }
     double* d = P.y + o;
+#if defined(SC_EXP) && SC_EXP == 28
+    val[k] = 0.0; dst[k] = d; (void)pd; (void)po; (void)corner; continue;   // ablation: no gather loads
+#endif
     double v = ld_cg(pd + po);
     if (corner >= 0) {
       const int cx = x0 / TX, cy = y0 / TY;
@@ -1674,6 +1680,8 @@ void col_tile(int ni, int* tx, int* ty, int* pend) {
 // ceil(ntiles / nsm) rounds of nz + 1 steps; splitting each column into S z-segments gives
 // ceil(S ntiles / nsm) rounds of ceil(nz / S) + 1 (+ 1 recomputed layer) steps.  Model cost per
 // round: the steps plus ~2 steps of look-back pipeline fill.  SC_ZSEG overrides S.
+int col_slots() { return kSlots; }
+
 void col_choose_segments(int ntiles, int nz, int nsm, int* nseg, int* zseg) {
   int best = 1;
   double bcost = 1e300;

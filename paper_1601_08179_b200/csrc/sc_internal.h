@@ -146,6 +146,7 @@ int launch_apply_p2(const Geom& g, const double* x, double* y, const double* don
                     int* nlaunch, void* events);
 // z-segments of the tile columns: ntiles columns of nz layers on nsm persistent CTAs
 void col_choose_segments(int ntiles, int nz, int nsm, int* nseg, int* zseg);
+int col_slots();   // step slots of the parked look-back partials (look-back distance + 1)
 // sum of v[0..n) in a fixed order into scal[slot] (deterministic), skipped when *done != 0
 int launch_sum_ordered(const double* v, int n, double* scal, int slot, const double* done, void* stream, int* nl);
 int launch_add_segments(double* y, const double* add, const long long* off, const long long* len, int n,
