@@ -1,6 +1,6 @@
 // Condensed operator v4 for n_I >= 8 (p >= 9), uniform geometry.
 //
-// One CTA (8 warps) per element.  The elements are processed in the 8 parity colours
+// One CTA (3-8 warps, BL::NW) per element.  The elements are processed in the 8 parity colours
 // (ex, ey, ez mod 2), one launch per colour: two elements of one colour share no face, edge or
 // vertex, so the assembly R^ (a8) is a plain read-modify-write of y (zeroed first) --
 // deterministic and atomic-free -- and a3 is a plain gather of the element's shell.
@@ -34,6 +34,12 @@ struct BigParams {
   BigCoef cf;
 };
 
+// Warps per CTA for 8 <= n_I <= 23 (two j-groups of 16 lanes per warp for n_I <= 16, so NG = 2 NW
+// residue classes of i).  Measured per n_I at cfg3 sizes (tools/gpu_v4_nw.sh, ms per apply for
+// 4 warps -> the table's choice): n_I = 9: 1.99 -> 1.86 (3 warps), 11: 1.74 -> 1.61 (6),
+// 12: 1.69 -> 1.51 (3), 13: 1.30 -> 1.25 (7); n_I = 10, 14: 4 warps stay best.
+constexpr int nw_small(int ni) { return ni == 9 ? 3 : ni == 11 ? 6 : ni == 12 ? 3 : ni == 13 ? 7 : 4; }
+
 template <int NI>
 struct BL {
   static constexpr int N2 = NI * NI;
@@ -42,8 +48,8 @@ struct BL {
   // warps per CTA: 4 up to n_I = 23 (two or more CTAs share an SM, so one CTA's gather / tree /
   // output phases overlap another's condensed part; measured p=12 -3.6 %, p=16 -4.6 %,
   // p=24 -15 % against 8 warps); 8 from n_I = 24 (one CTA per SM: 213 KB at n_I = 31)
-  static constexpr int NW = (NI >= 8 && NI <= 23) ? 4 : 8, NT = 32 * NW;
-  static constexpr int MINB = NW == 4 ? 2 : 1;
+  static constexpr int NW = (NI >= 8 && NI <= 23) ? nw_small(NI) : 8, NT = 32 * NW;
+  static constexpr int MINB = NW < 8 ? 2 : 1;
   static constexpr int NG = NW * H;                // residue classes of i
   static constexpr int NIT = (NI + NG - 1) / NG;   // i values per thread
   static constexpr int SH = 6 * N2 + 12 * NI + 8;  // shell: faces w e s n b t | 12 edges | 8 vertices
@@ -325,19 +331,39 @@ __global__ void __launch_bounds__(BL<NI>::NT, BL<NI>::MINB) k_apply_big(const __
     // H == 2: the half), through the (now free) transpose buffers
     constexpr int STMIN = H == 1 ? 2 : 1;
     double* const slots = sm + B::O_Y;
-#pragma unroll 1
-    for (int st = NW / 2; st >= STMIN; st >>= 1) {
-      __syncthreads();
-      if (warp >= st && warp < 2 * st) {
-        double* sl = slots + ((warp - st) * H + h) * NI * SW + j;
+    if constexpr (H == 2) {
+      // any NW: the upper ceil half of the remaining warps hands its sums to the lower half
 #pragma unroll
-        for (int k = 0; k < NI; ++k) sl[k * SW] = qx[k];
+      for (int n = NW; n > 1; n = (n + 1) >> 1) {
+        const int half = (n + 1) >> 1;
+        __syncthreads();
+        if (warp >= half && warp < n) {
+          double* sl = slots + ((warp - half) * H + h) * NI * SW + j;
+#pragma unroll
+          for (int k = 0; k < NI; ++k) sl[k * SW] = qx[k];
+        }
+        __syncthreads();
+        if (warp < n - half) {
+          const double* sl = slots + (warp * H + h) * NI * SW + j;
+#pragma unroll
+          for (int k = 0; k < NI; ++k) qx[k] += sl[k * SW];
+        }
       }
-      __syncthreads();
-      if (warp < st) {
-        const double* sl = slots + (warp * H + h) * NI * SW + j;
+    } else {
+#pragma unroll 1
+      for (int st = NW / 2; st >= STMIN; st >>= 1) {
+        __syncthreads();
+        if (warp >= st && warp < 2 * st) {
+          double* sl = slots + ((warp - st) * H + h) * NI * SW + j;
 #pragma unroll
-        for (int k = 0; k < NI; ++k) qx[k] += sl[k * SW];
+          for (int k = 0; k < NI; ++k) sl[k * SW] = qx[k];
+        }
+        __syncthreads();
+        if (warp < st) {
+          const double* sl = slots + (warp * H + h) * NI * SW + j;
+#pragma unroll
+          for (int k = 0; k < NI; ++k) qx[k] += sl[k * SW];
+        }
       }
     }
     if (warp < STMIN && jok) {
