@@ -150,6 +150,11 @@ __global__ void __launch_bounds__(128) k_apply_rw(const __grid_constant__ RWPara
         }
   }
   double* const Y = P.y;
+  // Old values of y through the read-only path: within one colour launch every y entry is read
+  // and then written once, by the same thread, so no entry is read after a write of this kernel;
+  // as non-coherent loads they may be scheduled ahead of the earlier entity groups' stores
+  // (plain loads of y must wait for every earlier store to y).
+  auto Yr = [&](long long i) { return __ldg(Y + i); };
   const long long xf0 = g.off_f[0] + (x0 + l + nx1 * (ey + (long long)ny * ez)) * N2;
   // ---- a7 + a8, faces: out = fd self + k0p opposite + bounding edges - Q
   // face f = 2 d + hi, coordinates (a, b) along (la, lb); bounding edges ea0 / ea1 at index b
@@ -183,8 +188,8 @@ __global__ void __launch_bounds__(128) k_apply_rw(const __grid_constant__ RWPara
     const bool dw = (x0 + l == 0), de = (x0 + l + 1 == nx);
 #pragma unroll
     for (int q = 0; q < N2; ++q) {
-      old[q] = (act && !dw) ? Y[xf0 + q] : 0.0;
-      olde[q] = (last && !de) ? Y[xf0 + N2 + q] : 0.0;
+      old[q] = (act && !dw) ? Yr(xf0 + q) : 0.0;
+      olde[q] = (last && !de) ? Yr(xf0 + N2 + q) : 0.0;
     }
 #pragma unroll
     for (int q = 0; q < N2; ++q) {
@@ -207,7 +212,7 @@ __global__ void __launch_bounds__(128) k_apply_rw(const __grid_constant__ RWPara
 #pragma unroll
       for (int a = 0; a < NI; ++a) o[a + NI * b] = face_out(f, a, b);
 #pragma unroll
-    for (int q = 0; q < N2; ++q) old[q] = Y[base + q];
+    for (int q = 0; q < N2; ++q) old[q] = Yr(base + q);
 #pragma unroll
     for (int q = 0; q < N2; ++q) Y[base + q] = old[q] + o[q];
   }
@@ -247,7 +252,7 @@ __global__ void __launch_bounds__(128) k_apply_rw(const __grid_constant__ RWPara
         o[c] = w02 * (d0 * u + cf.d[1] * tal) + w0 * (cf.d[2] * t1 + cf.d[3] * t2);
       }
 #pragma unroll
-      for (int c = 0; c < NI; ++c) old[c] = Y[base + c];
+      for (int c = 0; c < NI; ++c) old[c] = Yr(base + c);
 #pragma unroll
       for (int c = 0; c < NI; ++c) Y[base + c] = old[c] + o[c];
     }
@@ -275,8 +280,8 @@ __global__ void __launch_bounds__(128) k_apply_rw(const __grid_constant__ RWPara
     double old[NI], old1[NI];
 #pragma unroll
     for (int c = 0; c < NI; ++c) {
-      old[c] = (act && !d0x) ? Y[base + c] : 0.0;
-      old1[c] = (last && !d1x) ? Y[base + NI + c] : 0.0;
+      old[c] = (act && !d0x) ? Yr(base + c) : 0.0;
+      old1[c] = (last && !d1x) ? Yr(base + NI + c) : 0.0;
     }
 #pragma unroll
     for (int c = 0; c < NI; ++c) {
@@ -309,8 +314,8 @@ __global__ void __launch_bounds__(128) k_apply_rw(const __grid_constant__ RWPara
     double old[NI], old1[NI];
 #pragma unroll
     for (int c = 0; c < NI; ++c) {
-      old[c] = (act && !d0x) ? Y[base + c] : 0.0;
-      old1[c] = (last && !d1x) ? Y[base + NI + c] : 0.0;
+      old[c] = (act && !d0x) ? Yr(base + c) : 0.0;
+      old1[c] = (last && !d1x) ? Yr(base + NI + c) : 0.0;
     }
 #pragma unroll
     for (int c = 0; c < NI; ++c) {
@@ -340,7 +345,7 @@ __global__ void __launch_bounds__(128) k_apply_rw(const __grid_constant__ RWPara
       const long long base = g.off_v + x0 + l + nx1 * (ey + jb + ny1 * (ez + kb));
       const bool dyz = dY[jb] || dZ[kb];
       const bool d0x = x0 + l == 0 || dyz, d1x = x0 + l + 1 == nx || dyz;
-      const double old = (act && !d0x) ? Y[base] : 0.0, old1 = (last && !d1x) ? Y[base + 1] : 0.0;
+      const double old = (act && !d0x) ? Yr(base) : 0.0, old1 = (last && !d1x) ? Yr(base + 1) : 0.0;
       const double m = __shfl_up_sync(0xffffffffu, o[1], 1);
       if (act && !d0x) Y[base] = old + o[0] + (l > 0 ? m : 0.0);
       if (last && !d1x) Y[base + 1] = old1 + o[1];
