@@ -528,3 +528,87 @@ def test_small_grid_switch_parity(cfg, monkeypatch):
     ctx = ctx_for(g)
     y, _, _ = gpu_apply_nodal(ctx, x)
     assert rel(y, op.apply(x)) <= 1e-12
+
+
+def test_cfg5_full_size_properties():
+    """BASELINE configs[1] (cfg5: 128^3 elements, p = 8, the bench's workload and kernels) at full
+    size, where the dense oracle cannot run: properties that hold at any size.
+    (1) the tile-column kernel (v3, what bench.py times) equals the independent one-CTA-per-element
+    kernel (v1: shell gather, 13-count TPT form, fp64 atomics) on the same seeded input;
+    (2) symmetry b.(A a) = a.(A b) and a.(A a) > 0; (3) Dirichlet entries of A a are exactly 0
+    (the seeded vector is 0 there, so its zero pattern marks them); (4) BT-PCG at 5 iterations:
+    the recursively updated residual it reports equals the true residual ||b - A x|| / ||b||."""
+    import os
+    from synth import cfg5
+    g = cfg5()
+    ctx = ctx_for(g)
+    a, b = ctx.skeleton(), ctx.skeleton()
+    ctx.sc_fill_random(5, a)
+    ctx.sc_fill_random(6, b)
+    Aa, Ab = ctx.skeleton(), ctx.skeleton()
+    ctx.sc_apply_condensed(a, Aa)
+    ctx.sc_apply_condensed(b, Ab)
+    torch.cuda.synchronize()
+    s1, s2 = float(torch.dot(b, Aa)), float(torch.dot(a, Ab))
+    assert abs(s1 - s2) <= 1e-12 * abs(s1)
+    assert float(torch.dot(a, Aa)) > 0
+    dirichlet = (a == 0) & (b == 0)
+    assert int(dirichlet.sum()) > 0
+    assert float(Aa[dirichlet].abs().max()) == 0.0
+    # (4) PCG: reported (recursive) residual vs true residual
+    x = ctx.skeleton()
+    rep = ctx.sc_pcg_solve(a, x, rtol=0.0, maxit=5)
+    assert rep.iters == 5
+    r = ctx.skeleton()
+    ctx.sc_apply_condensed(x, r)
+    true_rel = float((a - r).norm() / a.norm())
+    assert abs(true_rel - rep.relres) <= 1e-8 * rep.relres
+    del Ab, b, r, x
+    torch.cuda.empty_cache()
+    # (1) v1 on the same input
+    os.environ["SC_APPLY_V1"] = "1"
+    try:
+        c1 = ctx_for(g)
+    finally:
+        del os.environ["SC_APPLY_V1"]
+    y1 = c1.skeleton()
+    c1.sc_apply_condensed(a, y1)
+    torch.cuda.synchronize()
+    d = float((y1 - Aa).norm() / Aa.norm())
+    assert d <= 1e-13, d
+
+
+@pytest.mark.parametrize("p", [2, 4, 8, 12, 16, 24, 32])
+def test_cfg3_full_size_against_v1(p):
+    """BASELINE configs[2] (cfg3, (n p)^3 ~ 2.1e8 nodes per p) at full size with the kernel
+    p_sweep.py times for each p (p2 row-warp, rw row-warp, v3 tile-column, v4 colour element-CTA):
+    equal to the independent v1 kernel on the same seeded input, symmetric, and exactly 0 on the
+    Dirichlet entries."""
+    import os
+    from synth import cfg3
+    g = cfg3(p)
+    ctx = ctx_for(g)
+    a, b = ctx.skeleton(), ctx.skeleton()
+    ctx.sc_fill_random(3, a)
+    ctx.sc_fill_random(4, b)
+    Aa, Ab = ctx.skeleton(), ctx.skeleton(fill=float("nan"))
+    ctx.sc_apply_condensed(a, Aa)
+    ctx.sc_apply_condensed(b, Ab)
+    torch.cuda.synchronize()
+    s1, s2 = float(torch.dot(b, Aa)), float(torch.dot(a, Ab))
+    assert abs(s1 - s2) <= 1e-12 * abs(s1)
+    dirichlet = (a == 0) & (b == 0)
+    assert float(Aa[dirichlet].abs().max()) == 0.0
+    del b, Ab
+    os.environ["SC_APPLY_V1"] = "1"
+    try:
+        c1 = ctx_for(g)
+    finally:
+        del os.environ["SC_APPLY_V1"]
+    y1 = c1.skeleton()
+    c1.sc_apply_condensed(a, y1)
+    torch.cuda.synchronize()
+    d = float((y1 - Aa).norm() / Aa.norm())
+    assert d <= 1e-13, d
+    del c1, ctx
+    torch.cuda.empty_cache()
