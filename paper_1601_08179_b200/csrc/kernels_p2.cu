@@ -76,6 +76,19 @@ __global__ void __launch_bounds__(256, SC_P2_MINB) k_apply_p2(const __grid_const
       V0[b][c] = ld(vx(ex, ey + b, ez + c), dX0 || dY[b] || dZ[c]);
     }
   }
+  // the y lines this warp read-modify-writes at the end: prefetched into L2 now (lanes 0 / 16
+  // cover the 256 bytes of the warp's 32 consecutive entries of each of the 17 entity rows)
+  if ((lane & 15) == 0 && act) {
+    const double* Yp = P.y;
+    auto pf = [&](long long a) { asm volatile("prefetch.global.L2 [%0];" ::"l"(Yp + a)); };
+    pf(xf(ex, ey, ez)); pf(yf(ex, ey, ez)); pf(yf(ex, ey + 1, ez)); pf(zf(ex, ey, ez)); pf(zf(ex, ey, ez + 1));
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      pf(ye(ex, ey, ez + b)); pf(ze(ex, ey + b, ez));
+#pragma unroll
+      for (int c = 0; c < 2; ++c) { pf(xe(ex, ey + b, ez + c)); pf(vx(ex, ey + b, ez + c)); }
+    }
+  }
   double E = __shfl_down_sync(0xffffffffu, W, 1), Y1[2], Z1[2], V1[2][2];
 #pragma unroll
   for (int b = 0; b < 2; ++b) {
