@@ -189,7 +189,19 @@ __global__ void __launch_bounds__(BL<NI>::NT, BL<NI>::MINB) k_apply_big(const __
       }
     }
   };
-  if constexpr (EARLY) load_yold();
+  if constexpr (EARLY) {
+    load_yold();
+  } else {
+    // the old values are loaded in the output phase (registers kept for occupancy): prefetch
+    // their lines into L2 now, one prefetch per 128 bytes of each face block, one per edge end
+    auto pf = [&](long long a) { asm volatile("prefetch.global.L2 [%0];" ::"l"(P.y + a)); };
+#pragma unroll
+    for (int f = 0; f < 6; ++f)
+      if (!sDir[f])
+        for (int q = 16 * tid; q < N2 + 15; q += 16 * NT) pf(sBase[f] + (q < N2 ? q : N2 - 1));
+    if (tid < 24 && !sDir[6 + (tid >> 1)]) pf(sBase[6 + (tid >> 1)] + ((tid & 1) ? NI - 1 : 0));
+    if (tid >= 32 && tid < 40 && !sDir[18 + tid - 32]) pf(sBase[18 + tid - 32]);
+  }
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   // ---- faces-in operands P^s = lo + (-1)^s hi, a0-weighted line sums (R+, R-) of faces / edges
