@@ -30,15 +30,17 @@ struct P2Params {
 #ifndef SC_P2_MINB
 #define SC_P2_MINB 2
 #endif
-__global__ void __launch_bounds__(256, SC_P2_MINB) k_apply_p2(const __grid_constant__ P2Params P, int colour) {
-  if (P.done != nullptr && *P.done != 0.0) return;
+#ifndef SC_P2_ITEMS
+#define SC_P2_ITEMS 2
+#endif
+// Warp item wid of colour `colour`: 32 consecutive elements of one x-row (see the file comment).
+__device__ __forceinline__ void p2_item(const P2Params& P, int colour, long long wid) {
   const Geom& g = P.g;
   const BigCoef& cf = P.cf;
   const int nx = g.nx, ny = g.ny, nz = g.nz;
   const int cp = colour & 1, ry = (colour >> 1) & 1, rz = colour >> 2;
   const int nch = (nx + 31) >> 5;
   const int cc = (nch - cp + 1) >> 1, cy = (ny - ry + 1) >> 1, cz = (nz - rz + 1) >> 1;
-  const long long wid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (wid >= (long long)cc * cy * cz) return;   // warp-uniform
   const int lane = threadIdx.x & 31;
   const int chunk = cp + 2 * (int)(wid % cc);
@@ -248,6 +250,46 @@ __global__ void __launch_bounds__(256, SC_P2_MINB) k_apply_p2(const __grid_const
     if (mt_[q]) Y[at_[q]] = oldt[q] + wt_[q];
 }
 
+// L2 prefetch of the 17 x rows (and y rows) of warp item wid: issued one item ahead, so the next
+// item's loads find their lines in L2.
+__device__ __forceinline__ void p2_prefetch(const P2Params& P, int colour, long long wid) {
+  const Geom& g = P.g;
+  const int nx = g.nx, ny = g.ny, nz = g.nz;
+  const int cp = colour & 1, ry = (colour >> 1) & 1, rz = colour >> 2;
+  const int nch = (nx + 31) >> 5;
+  const int cc = (nch - cp + 1) >> 1, cy = (ny - ry + 1) >> 1, cz = (nz - rz + 1) >> 1;
+  if (wid >= (long long)cc * cy * cz) return;
+  const int lane = threadIdx.x & 31;
+  const int chunk = cp + 2 * (int)(wid % cc);
+  const int ey = ry + 2 * (int)((wid / cc) % cy), ez = rz + 2 * (int)(wid / ((long long)cc * cy));
+  const int ex = chunk * 32 + lane;
+  if ((lane & 15) != 0 || ex >= nx) return;
+  const long long nx1 = nx + 1, ny1 = ny + 1;
+  const long long a[17] = {
+      g.off_f[0] + ex + nx1 * (ey + (long long)ny * ez), g.off_f[1] + ex + (long long)nx * (ey + ny1 * ez),
+      g.off_f[1] + ex + (long long)nx * (ey + 1 + ny1 * ez), g.off_f[2] + ex + (long long)nx * (ey + (long long)ny * ez),
+      g.off_f[2] + ex + (long long)nx * (ey + (long long)ny * (ez + 1)),
+      g.off_e[1] + ex + nx1 * (ey + (long long)ny * ez), g.off_e[1] + ex + nx1 * (ey + (long long)ny * (ez + 1)),
+      g.off_e[2] + ex + nx1 * (ey + ny1 * ez), g.off_e[2] + ex + nx1 * (ey + 1 + ny1 * ez),
+      g.off_e[0] + ex + (long long)nx * (ey + ny1 * ez), g.off_e[0] + ex + (long long)nx * (ey + ny1 * (ez + 1)),
+      g.off_e[0] + ex + (long long)nx * (ey + 1 + ny1 * ez), g.off_e[0] + ex + (long long)nx * (ey + 1 + ny1 * (ez + 1)),
+      g.off_v + ex + nx1 * (ey + ny1 * ez), g.off_v + ex + nx1 * (ey + ny1 * (ez + 1)),
+      g.off_v + ex + nx1 * (ey + 1 + ny1 * ez), g.off_v + ex + nx1 * (ey + 1 + ny1 * (ez + 1))};
+#pragma unroll
+  for (int q = 0; q < 17; ++q) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.x + a[q]));
+}
+
+// SC_P2_ITEMS consecutive warp items per warp, each prefetching the next one's x rows.
+__global__ void __launch_bounds__(256, SC_P2_MINB) k_apply_p2(const __grid_constant__ P2Params P, int colour) {
+  if (P.done != nullptr && *P.done != 0.0) return;
+  const long long w0 = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * SC_P2_ITEMS;
+#pragma unroll 1
+  for (int t = 0; t < SC_P2_ITEMS; ++t) {
+    if (t + 1 < SC_P2_ITEMS) p2_prefetch(P, colour, w0 + t + 1);
+    p2_item(P, colour, w0 + t);
+  }
+}
+
 int launch_apply_p2(const Geom& g, const double* x, double* y, const double* done, const void* coef, void* stream,
                     int* nl, void* events) {
   cudaStream_t st = (cudaStream_t)stream;
@@ -263,7 +305,8 @@ int launch_apply_p2(const Geom& g, const double* x, double* y, const double* don
     const int cp = c & 1, ry = (c >> 1) & 1, rz = c >> 2;
     const long long warps = (long long)((nch - cp + 1) >> 1) * ((g.ny - ry + 1) >> 1) * ((g.nz - rz + 1) >> 1);
     if (warps <= 0) continue;
-    k_apply_p2<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(P, c);
+    const long long wgroups = (warps + SC_P2_ITEMS - 1) / SC_P2_ITEMS;
+    k_apply_p2<<<(unsigned)((wgroups + 7) / 8), 256, 0, st>>>(P, c);
     (*nl)++;
   }
   if (ev) cudaEventRecord(ev[1], st);
