@@ -83,7 +83,7 @@ struct sc_ctx {
   double* d_corner = nullptr;
   double* d_pending = nullptr;
   double* d_dotp = nullptr;             // per-tile x . y partials of the operator (PCG p . q)
-  bool fused_dot = false;               // SC_FUSED_DOT=1: use them instead of the dot kernel
+  bool fused_dot = true;                // p . q from the operator's per-tile partials (SC_FUSED_DOT=0: dot kernel)
   // workspace (caller-owned)
   double* ws = nullptr;
   size_t ws_bytes = 0;
@@ -356,7 +356,7 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
       if (cudaMalloc(&ctx->d_dotp, sizeof(double) * nitems) != cudaSuccess)
         return fail("cudaMalloc dotp");
       const char* fd = getenv("SC_FUSED_DOT");
-      ctx->fused_dot = fd && fd[0] == '1';
+      ctx->fused_dot = !(fd && fd[0] == '0');
       if (cudaMemset(ctx->d_colstate, 0, 64) != cudaSuccess) return fail("memset colstate");
       if (cudaMemset(ctx->d_flags, 0, sizeof(int) * nflags) != cudaSuccess) return fail("memset flags");
       if (cudaMemset(ctx->d_corner, 0, sizeof(double) * ncorner) != cudaSuccess) return fail("memset corner");
@@ -608,9 +608,10 @@ static sc_status pcg_iteration(sc_ctx* ctx, cudaStream_t st) {
   const long long n = ctx->g.n_total;
   double* done = ctx->scal + SCAL_DONE;
   double* x = ctx->x_cur;
-  // p . q fused into the operator (single GPU): measured slower than the separate dot kernel
-  // at cfg5 (10.67 vs 9.55 + 0.9 ms: the extra loads sit on the operator's critical path), so it
-  // is opt-in (SC_FUSED_DOT=1) until the operator's finalize / finish phases are overlapped.
+  // p . q fused into the tile-column operator (single GPU): each tile accumulates x . y over the
+  // entries it finalizes, one fixed-order sum follows.  At cfg5 12.47 -> 11.74 ms per iteration
+  // against the separate dot kernel (which streams p and q once more); SC_FUSED_DOT=0 disables it.
+  // (Early in round 1, with a slower operator, it measured slower: 10.67 vs 9.55 + 0.9 ms.)
   const bool fused = ctx->use_col && ctx->prm.nranks == 1 && ctx->fused_dot;
   sc_status s = apply_impl(ctx, ctx->pv, ctx->q, done, st, fused ? ctx->d_dotp : nullptr);
   if (s) return s;

@@ -247,7 +247,8 @@ def test_pcg_parity_random_rhs_nonuniform():
 def test_pcg_parity_multitile(p, ne, fused, monkeypatch):
     """BT-PCG on a uniform grid spanning several 8 x 4 tiles in x and y: exercises the
     tile-column operator with the look-back, with the separate p . q dot kernel and with the
-    p . q partials fused into the operator (SC_FUSED_DOT=1, single GPU)."""
+    p . q partials fused into the operator (the default for the tile-column kernel on one GPU;
+    SC_FUSED_DOT=0 selects the separate dot kernel)."""
     from paper_1601_08179_b200 import SC_DUAL
     monkeypatch.setenv("SC_FUSED_DOT", fused)
     g = small_grid(p, ne, 1.0, lengths=(1.3, 0.7, 0.5))
