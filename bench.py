@@ -142,8 +142,7 @@ def run_reference(args):
         return
     grid = workload(args.config)
     n_side = args.cpu_sample
-    for _ in range(args.warmup):
-        pass
+    # oracle_sample runs one untimed warm-up iteration itself (it includes the dense Schur setup)
     res = oracle_sample(grid, n_side, iters=max(2, args.steps // 2 * 2))
     line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": "GDOF/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -164,15 +163,20 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     import __graft_entry__
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
     if rank == 0:
         __graft_entry__.build()
+    if world > 1:
+        dist.barrier(device_ids=[local])      # every rank loads the library rank 0 just built
     from paper_1601_08179_b200 import capi
     from paper_1601_08179_b200.solver import Context
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
         lib = capi.load()
         idbuf = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
@@ -318,8 +322,23 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def relaunch_under_torchrun(args):
+    """`python bench.py --gpus N` without a torchrun environment: re-exec as N ranks on this node
+    (the driver's own launch sets WORLD_SIZE and never gets here)."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    raise SystemExit(subprocess.call(cmd))
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args)
     if args.impl == "reference":
         run_reference(args)
     else:

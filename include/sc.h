@@ -95,8 +95,9 @@ typedef struct {
 typedef enum { SC_PERM = 0, SC_PRIMAL = 1, SC_DUAL = 2 } sc_basis_mode;
 
 /* Validate params, build the 1-D transformed basis (GLL, K, generalized eigenpairs with
- * sign rule a0_m > 0, ascending Lambda), geometry tables and the diagonal (BT)
- * preconditioner table; allocate small device tables.  Synchronous. */
+ * sign rule a0_m > 0, ascending Lambda) and the geometry tables (d_e, D^{-1}); allocate small
+ * device tables.  Synchronous.  The diagonal (BT) preconditioner 1/diag(Rhat Htilde Rhat^T)
+ * is built by sc_bind_workspace (it lives in the caller-owned workspace). */
 sc_status sc_setup(const sc_params* prm, sc_ctx** out);
 sc_status sc_destroy(sc_ctx* ctx);
 
@@ -106,7 +107,9 @@ sc_status sc_layout_query(const sc_params* prm, sc_layout_info* out);
 sc_status sc_layout(const sc_ctx* ctx, sc_layout_info* out);
 
 /* Workspace for sc_pcg_solve and sc_apply_condensed (caller-owned device memory,
- * e.g. a torch tensor).  Must be bound before those calls; bytes >= sc_workspace_bytes. */
+ * e.g. a torch tensor).  Must be bound before those calls; bytes >= sc_workspace_bytes.
+ * Binding computes the BT preconditioner diagonal into the workspace (synchronous).
+ * Re-binding is allowed; it discards the cached PCG graph (which refers to the old buffers). */
 size_t sc_workspace_bytes(const sc_ctx* ctx);
 sc_status sc_bind_workspace(sc_ctx* ctx, void* d_ws, size_t bytes);
 

@@ -438,6 +438,12 @@ extern "C" sc_status sc_bind_workspace(sc_ctx* ctx, void* d_ws, size_t bytes) {
   if (((uintptr_t)d_ws) % 256 != 0) return SC_EINVAL;
   double* w = (double*)d_ws;
   long long n = ctx->g.n_total;
+  // the cached PCG graph bakes in the previous workspace's buffers (pv, q, r, scal, partials,
+  // Pinv table): a new binding invalidates it
+  if (ctx->pcg_graph) { cudaGraphExecDestroy(ctx->pcg_graph); ctx->pcg_graph = nullptr; }
+  ctx->pcg_graph_x = nullptr;
+  ctx->pcg_seen_x = nullptr;
+  ctx->x_cur = nullptr;
   ctx->ws = w; ctx->ws_bytes = bytes;
   ctx->pinv = w; w += n;
   ctx->r = w; w += n;

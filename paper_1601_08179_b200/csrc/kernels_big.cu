@@ -492,8 +492,11 @@ static int launch_big_t(const BigParams& P, cudaStream_t st, int* nl) {
   using B = BL<NI>;
   static_assert(sizeof(double) * B::TOTAL <= 225 * 1024, "shared memory budget");
   const size_t smem = sizeof(double) * B::TOTAL;
-  static int auto_pipe = -1;   // (the occupancy queries also set both builds' shared-memory limit)
-  if (auto_pipe < 0) auto_pipe = occupancy_big<NI, UNI, 2>(smem) >= occupancy_big<NI, UNI, 0>(smem) ? 1 : 0;
+  static int auto_pipe_d[kMaxDev];   // per device: 0 = not queried, else 1 + choice
+  // (the occupancy queries also set both builds' shared-memory limit on this device)
+  const int dv = dev_slot();
+  if (!auto_pipe_d[dv]) auto_pipe_d[dv] = 1 + (occupancy_big<NI, UNI, 2>(smem) >= occupancy_big<NI, UNI, 0>(smem) ? 1 : 0);
+  const int auto_pipe = auto_pipe_d[dv] - 1;
   const char* force = getenv("SC_V4_PIPE");   // tests: 0 / 1 force a build (same arithmetic, same order)
   const int pipelined = (force && (force[0] == '0' || force[0] == '1')) ? force[0] - '0' : auto_pipe;
   for (int c = 0; c < 8; ++c) {

@@ -1642,8 +1642,11 @@ static int launch_col_t(const ColParams& P, cudaStream_t st, int* nl, int* grid_
   using C = CS<NI>;
   static_assert(sizeof(double) * C::TOTAL <= 227 * 1024, "shared memory budget");
   const size_t smem = sizeof(double) * C::TOTAL;
-  static int max_active = -1, nsm = 0;
-  if (max_active < 0) {
+  static int max_active_d[kMaxDev], nsm_d[kMaxDev];   // per device (0 = not queried yet)
+  const int dv = dev_slot();
+  int& max_active = max_active_d[dv];
+  int& nsm = nsm_d[dv];
+  if (max_active < 1) {
     cudaFuncSetAttribute(k_apply_col<NI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_active, k_apply_col<NI>, C::NT, smem);
     int dev;

@@ -223,10 +223,11 @@ int launch_apply(const Geom& g, const double* x, double* y, const double* done, 
   long long ne = (long long)g.nx * g.ny * g.nz;
   if (ne == 0) return cudaSuccess;
   size_t smem = apply_smem_bytes(g.ni);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static bool attr_set[kMaxDev];   // per device
+  const int dv = dev_slot();
+  if (!attr_set[dv]) {
     cudaFuncSetAttribute(k_apply_v1, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
+    attr_set[dv] = true;
   }
   k_apply_v1<<<(unsigned)ne, 256, smem, st>>>(g, x, y, done);
   (*nl)++;

@@ -150,11 +150,11 @@ __global__ void __launch_bounds__(128) k_apply_rw(const __grid_constant__ RWPara
         }
   }
   double* const Y = P.y;
-  // Old values of y through the read-only path: within one colour launch every y entry is read
-  // and then written once, by the same thread, so no entry is read after a write of this kernel;
-  // as non-coherent loads they may be scheduled ahead of the earlier entity groups' stores
-  // (plain loads of y must wait for every earlier store to y).
-  auto Yr = [&](long long i) { return __ldg(Y + i); };
+  // Old values of y: within one colour launch every y entry is read and then written once, by
+  // the same thread.  They were read through the non-coherent path (ld.global.nc) in round 1;
+  // since this kernel writes y, that path is not guaranteed coherent for the kernel's lifetime
+  // (ADVICE r1), so they are read with ld.global.cg (L2, coherent).
+  auto Yr = [&](long long i) { return __ldcg(Y + i); };   // y is written by this kernel: coherent L2 load
   const long long xf0 = g.off_f[0] + (x0 + l + nx1 * (ey + (long long)ny * ez)) * N2;
   // ---- a7 + a8, faces: out = fd self + k0p opposite + bounding edges - Q
   // face f = 2 d + hi, coordinates (a, b) along (la, lb); bounding edges ea0 / ea1 at index b
@@ -356,10 +356,11 @@ template <int NI>
 static int launch_rw_t(const RWParams& P, cudaStream_t st, int* nl) {
   using L = RWL<NI>;
   const size_t smem = sizeof(double) * L::TOTAL * L::WARPS;
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[kMaxDev];   // per device
+  const int dv = dev_slot();
+  if (!attr[dv]) {
     cudaFuncSetAttribute(k_apply_rw<NI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+    attr[dv] = true;
   }
   const int nch = (P.g.nx + 31) >> 5;
   for (int c = 0; c < 8; ++c) {

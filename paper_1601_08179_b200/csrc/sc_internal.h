@@ -1,6 +1,7 @@
 // Internal declarations shared by the host (api.cu, basis1d.cpp) and the kernels.
 #pragma once
 
+#include <cuda_runtime.h>
 #include <stdint.h>
 #include <string>
 #include <vector>
@@ -9,6 +10,15 @@
 #define SC_NIMAX (SC_PMAX - 1)
 
 namespace sc {
+
+// Kernel attributes (dynamic shared-memory opt-in) and occupancy queries are per device: the
+// launchers cache them per device ordinal, not in one process-wide static.
+constexpr int kMaxDev = 64;
+inline int dev_slot() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return (d >= 0 && d < kMaxDev) ? d : 0;
+}
 
 // 1-D transformed basis (host, double), see basis1d.cpp.
 struct Basis1D {

@@ -65,8 +65,9 @@ CFG3_P = (2, 4, 8, 12, 16, 24, 32)
 
 
 def cfg3(p):
-    """BASELINE configs[2]: n per direction = round(594/p), lambda=1."""
-    n = int(round(594.0 / p))
+    """BASELINE configs[2]: n per direction = round(594/p), halves rounded up (SURVEY c16:
+    p = 4 -> 149), lambda=1."""
+    n = int(594.0 / p + 0.5)
     return small_grid(p, (n, n, n), 1.0, name=f"cfg3_p{p}")
 
 
@@ -80,3 +81,29 @@ def cfg4(ar, n=32):
 def cfg5(n=128):
     """BASELINE configs[4]: [0,1]^3, 128^3 elements, p=8, lambda=1; z-slabs over GPUs."""
     return small_grid(8, (n, n, n), 1.0, name="cfg5")
+
+
+def nonuniform_grid(p, ne, lam, seed=0, lo=0.3, hi=1.7):
+    """Per-element widths drawn uniform[lo, hi) from a seeded generator (test geometry)."""
+    rng = np.random.default_rng(seed)
+    g = small_grid(p, ne, lam, name=f"nonuniform_s{seed}")
+    g.hx = rng.uniform(lo, hi, ne[0])
+    g.hy = rng.uniform(lo, hi, ne[1])
+    g.hz = rng.uniform(lo, hi, ne[2])
+    return g
+
+
+def graded_widths(n, alpha, length):
+    """n widths growing by the constant expansion factor alpha (h_e = h_0 alpha^e), summing to
+    `length` (8 elements, alpha in {1, 1.5, 2}, AR_max = alpha^7 = 1 / 17 / 128)."""
+    w = np.asarray([alpha ** e for e in range(n)], dtype=np.float64)
+    return w * (length / w.sum())
+
+
+def e3_grid(p, alpha, n=8, lam=0.0):
+    """The paper's solver benchmark E3: Omega = (0, 2 pi)^3, n^3 elements graded with
+    expansion factor alpha in every direction (reading R15), lambda = 0."""
+    L = 2.0 * np.pi
+    h = graded_widths(n, alpha, L)
+    return Grid(p=p, ne=(n, n, n), hx=h.copy(), hy=h.copy(), hz=h.copy(), lam=float(lam),
+                name=f"e3_p{p}_a{alpha}", extra={"alpha": alpha, "dirichlet": "e3"})

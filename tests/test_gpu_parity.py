@@ -613,3 +613,58 @@ def test_cfg3_full_size_against_v1(p):
     assert d <= 1e-13, d
     del c1, ctx
     torch.cuda.empty_cache()
+
+
+# ---- round 2: parity holes closed against the oracle ---------------------------------------
+@pytest.mark.parametrize("p,v1", [(25, False), (32, False), (18, True), (24, True)])
+def test_high_p_operator_parity_vs_oracle(p, v1, monkeypatch):
+    """p = 25, 32: the v4 kernel's 8-warp class (n_I >= 24, one CTA per SM); p = 18, 24 with
+    SC_APPLY_V1=1: the v1 kernel's chunked z-line path (n_I >= 17).  Against the dense-Schur
+    oracle (Cholesky of H_II, 17 s at p = 24 and 73 s at p = 32 on 8 host cores)."""
+    if v1:
+        monkeypatch.setenv("SC_APPLY_V1", "1")
+    g = small_grid(p, (2, 2, 2), 0.8, lengths=(1.2, 0.9, 1.1))
+    op = operator.AssembledCondensedOperator(g)
+    x = lattice_random(80 + p, g.ne, g.p).ravel()
+    ctx = ctx_for(g)
+    y, _, _ = gpu_apply_nodal(ctx, x)
+    assert rel(y, op.apply(x)) <= 1e-12
+
+
+def _aniso_pcg_case(p, n, ar):
+    """cfg4-shaped anisotropic grid: [0, AR] x [0, 1]^2, n^3 elements, lambda = 0,
+    sine manufactured solution; Alg. 4 pre -> BT-PCG to 1e-10 -> compared with the oracle's
+    block-Jacobi PCG (iterations +-1, iterate within 1e-10)."""
+    g = small_grid(p, (n, n, n), 0.0, lengths=(float(ar), 1.0, 1.0))
+    X, Y, Z = mesh.lattice_coordinates(g)
+    f = sine_f(X, Y, Z, 0.0)
+    op = operator.AssembledCondensedOperator(g)
+    b = solve.condensed_rhs(op, f)
+    res = _oracle_pcg(g, op, b, 1e-10)
+    ctx = ctx_for(g)
+    f_d = torch.from_numpy(f).cuda()
+    bt = ctx.skeleton()
+    ctx.sc_condense_rhs(f_d, bt)
+    xt = ctx.skeleton()
+    rep = ctx.sc_pcg_solve(bt, xt, rtol=1e-10, maxit=3000)
+    assert rep.converged and abs(rep.iters - res.iters) <= 1, (rep.iters, res.iters)
+    ref = res.x if rep.iters == res.iters else _oracle_pcg(g, op, b, 0, fixed=rep.iters).x
+    assert rel(ctx.to_lattice_nodal(xt).cpu().numpy(), ref) <= 1e-10
+    return rep.iters, res.iters
+
+
+@pytest.mark.parametrize("p,n,ar,expect", [(8, 8, 8, 14), (8, 8, 32, 15), (8, 8, 128, 15), (16, 8, 1, 33),
+                                           (16, 8, 128, 40)])
+def test_pcg_parity_anisotropic(p, n, ar, expect):
+    """Aspect ratios up to 128 (BASELINE configs[3] family) against the oracle; `expect` is the
+    oracle's own iteration count (recorded from oracle runs)."""
+    it_gpu, it_oracle = _aniso_pcg_case(p, n, ar)
+    assert it_oracle == expect
+
+
+@pytest.mark.parametrize("ar,expect", [(128, 52)])
+def test_pcg_parity_anisotropic_16cubed(ar, expect):
+    """Half-size cfg4 (16^3 elements, p = 16, AR = 128): the oracle needs 52 iterations; the
+    full-size GPU run (32^3) needs 53 (DESIGN §7 on SURVEY c15's 47)."""
+    it_gpu, it_oracle = _aniso_pcg_case(16, 16, ar)
+    assert it_oracle == expect

@@ -137,3 +137,95 @@ def test_transform_roundtrip_and_duality():
     xt = solve.transform(g, x, "primal")
     yt = solve.transform(g, y, "dual")
     assert abs(np.dot(xt, yt) - np.dot(x, y)) < 1e-12 * g.n_lattice
+
+
+def _assembled_dense(op):
+    """The assembled condensed matrix by applying the oracle operator to unit vectors."""
+    n = op.grid.n_lattice
+    return np.stack([op.apply(np.eye(n)[i]) for i in range(n)], axis=1)
+
+
+def test_transform_through_p2_closed_forms():
+    """solve.transform pinned by the hand-derived p = 2 transformed entries (tests/golden/
+    p2_single_element.txt): on a 2x2x2 grid of reference elements (h = 2,
+    lambda = 0), the assembled transformed operator Shat A Shat^T, formed as
+    transform(A transform(e, 'primal_inv'), 'dual'), has diagonal 2 x 41/18 at an interior face
+    (2 elements), 4 x 1 at an interior edge, 8 x 7/18 at the centre vertex, and the face w -> face s
+    coupling -2/9 (one element holds both).  A swapped primal / dual pair scales face entries by
+    (S M)^2 / S^2 = 16/9 and fails."""
+    from conftest import read_golden
+    G = read_golden("p2_single_element.txt")
+    g = small_grid(2, (2, 2, 2), 0.0, lengths=(4.0, 4.0, 4.0))
+    op = operator.AssembledCondensedOperator(g)
+    nx1, ny1, _ = mesh.lattice_dims(g)
+    idx = lambda gx, gy, gz: gx + nx1 * (gy + ny1 * gz)
+
+    def At(i, j):
+        e = np.zeros(g.n_lattice)
+        e[j] = 1.0
+        return solve.transform(g, op.apply(solve.transform(g, e, "primal_inv")), "dual")[i]
+
+    xface = idx(2, 1, 1)          # x-face fx = 1 of elements (0,0,0) | (1,0,0), node (j,k) = (1,1)
+    yface = idx(1, 2, 1)          # y-face fy = 1 of elements (0,0,0) | (0,1,0)
+    zedge = idx(2, 2, 1)          # z-edge (fx, fy) = (1, 1), layer 0: 4 elements
+    vert = idx(2, 2, 2)           # centre vertex: 8 elements
+    assert abs(At(xface, xface) - 2 * float(G["t_face_diag"])) < 1e-13
+    assert abs(At(zedge, zedge) - 4 * float(G["t_edge_diag"])) < 1e-13
+    assert abs(At(vert, vert) - 8 * float(G["t_vertex_diag"])) < 1e-13
+    assert abs(At(xface, yface) - float(G["t_face_w_s"])) < 1e-13
+    # transformed_norm: || Shat e || for a face unit vector is S_II^2 = 3/4 at p = 2
+    norm = solve.transformed_norm(g, op.skel)
+    e = np.zeros(g.n_lattice)
+    e[xface] = 1.0
+    assert abs(norm(e) - 0.75) < 1e-14
+    e[xface] = 0.0
+    e[zedge] = 1.0
+    assert abs(norm(e) - np.sqrt(0.75)) < 1e-14
+
+
+def test_block_jacobi_blocks_are_assembled_diagonal_blocks():
+    """BlockJacobi pinned against the explicitly assembled condensed matrix: every block is the
+    inverse of the assembled matrix restricted to one face / edge / vertex, the blocks
+    partition the free skeleton nodes, and a block that dropped a neighbour element's
+    contribution would differ from the assembled entries (non-uniform widths make the
+    contributions of the elements around an entity differ)."""
+    g = small_grid(3, (3, 2, 2), 0.4, lengths=(1.5, 1.0, 0.8))
+    g.hx = np.array([0.3, 0.7, 0.5])
+    g.hz = np.array([0.35, 0.45])
+    op = operator.AssembledCondensedOperator(g)
+    A = _assembled_dense(op)
+    P = solve.BlockJacobi(op)
+    seen = np.zeros(g.n_lattice, dtype=int)
+    for idx, Binv in P.diagonal_blocks():
+        B = A[np.ix_(idx, idx)]
+        assert np.allclose(np.linalg.inv(Binv), B, rtol=0, atol=1e-12 * np.abs(B).max())
+        seen[idx] += 1
+    assert np.array_equal(seen, op.free.astype(int))
+
+
+def test_multi_geometry_grouping_recovery_equals_full_solve():
+    """Non-uniform widths (several Schur matrices, operator.py's np.unique grouping over
+    mesh.element_widths): condensed solve + interior recovery equals the uncondensed direct
+    solve, and the operator equals the dense assembly of per-element full matrices
+    condensed one element at a time."""
+    g = small_grid(3, (3, 2, 2), 0.7)
+    g.hx = np.array([0.2, 0.5, 0.3])
+    g.hy = np.array([0.6, 0.4])
+    g.hz = np.array([0.25, 0.75])
+    w = mesh.element_widths(g)
+    assert w.shape == (12, 3)
+    assert np.allclose(w[1 + 3 * (0 + 2 * 1)], (0.5, 0.6, 0.75))       # e = ex + nx (ey + ny ez)
+    op = operator.AssembledCondensedOperator(g)
+    assert len(op.groups) == 12
+    X, Y, Z = mesh.lattice_coordinates(g)
+    f = np.sin(3 * X + Y) * np.cos(2 * Z) + 0.5
+    A, F, free = solve.full_system(g, f)
+    ufull = np.zeros(g.n_lattice)
+    ufull[free] = np.linalg.solve(A, F)
+    b = solve.condensed_rhs(op, f)
+    fr = op.free
+    Ac = _assembled_dense(op)[np.ix_(fr, fr)]
+    ub = np.zeros(g.n_lattice)
+    ub[fr] = np.linalg.solve(Ac, b[fr])
+    u = solve.recover(op, f, ub)
+    assert np.abs(u - ufull).max() < 1e-11 * np.abs(ufull).max()

@@ -64,13 +64,18 @@ int main() {
   cudaEventCreate(&e1);
   const int blocks = nsm * 8, threads = 256, iters = 2000;
   float ms;
-  // DFMA
+  // DFMA (best of 10 launches)
   k_dfma<<<blocks, threads>>>(out, 10);
-  cudaEventRecord(e0);
-  k_dfma<<<blocks, threads>>>(out, iters);
-  cudaEventRecord(e1);
-  cudaEventSynchronize(e1);
-  cudaEventElapsedTime(&ms, e0, e1);
+  float best = 1e30f;
+  for (int rep = 0; rep < 10; ++rep) {
+    cudaEventRecord(e0);
+    k_dfma<<<blocks, threads>>>(out, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  ms = best;
   double nfma = (double)blocks * threads * iters * 16 * 8;
   printf("DFMA: %.2f TFLOP/s fp64 (%.1f FMA/clk/SM at %.0f MHz nominal)\n", 2 * nfma / ms / 1e9,
          nfma / (ms * 1e-3) / nsm / (clk * 1e3), clk / 1e3);
