@@ -172,6 +172,18 @@ sc_status sc_condense_rhs(sc_ctx* ctx, const double* d_f, double* d_b, void* str
  * sc_condense_rhs), d_x: skeleton solution, d_u: lattice output. */
 sc_status sc_recover(sc_ctx* ctx, const double* d_f, const double* d_x, double* d_u, void* stream);
 
+/* Inhomogeneous Dirichlet data (the paper's solver benchmark: u = u_ex on the domain
+ * boundary).  d_g: lattice vector whose values on the domain-boundary nodes are the Dirichlet data
+ * (other nodes ignored).  sc_condense_rhs_dirichlet: b~ = b~(f) - (Rhat Htilde Rhat^T g~)_F with
+ * g~ = Shat^{-T} g on the Dirichlet entities (A_FF x_F = b_F - A_FD g_D; reading R17),
+ * Dirichlet entries of d_b set to 0; solve with sc_pcg_solve as usual.  sc_recover_dirichlet:
+ * as sc_recover with the skeleton completed by g~ on the Dirichlet entities, so d_u equals g on the
+ * boundary.  Both use the PCG buffers of the workspace as scratch (not between sc_pcg_start and
+ * sc_pcg_status).  Any geometry; p as in sc_setup. */
+sc_status sc_condense_rhs_dirichlet(sc_ctx* ctx, const double* d_f, const double* d_g, double* d_b, void* stream);
+sc_status sc_recover_dirichlet(sc_ctx* ctx, const double* d_f, const double* d_g, const double* d_x, double* d_u,
+                               void* stream);
+
 /* Basis / layout conversions (untimed helpers for parity).
  * to:   lattice -> skeleton;  from: skeleton -> lattice (element-interior lattice nodes
  * are written as 0). */

@@ -4,6 +4,7 @@
 * condensed_rhs : Alg. 1 (P:230-233) Fhat_e = F_B - H_BI H_II^{-1} F_I, gathered by R;
                   F_e = (h1 h2 h3 / 8) (w(x)w(x)w) * f(x_e)  (GLL-lumped mass).
 * recover       : Alg. 1 u_I = H_II^{-1} (F_I - H_IB u_B).
+* dirichlet_rhs : the condensed RHS with inhomogeneous Dirichlet data (E3): b_F - A_FD g_D.
 * full_system   : the uncondensed SEM system R H_L R^T u = R F, dense, tiny grids.
 * BlockJacobi   : the paper's block preconditioner: exact inverse of the
                   assembled self-block of every face, edge and vertex.  In the transformed
@@ -44,11 +45,37 @@ def condensed_rhs(op, f_lattice):
     return b
 
 
-def recover(op, f_lattice, u_skel):
-    """Full lattice solution: skeleton from u_skel, interiors by Eq. eq:condensation_inner."""
+def dirichlet_rhs(op, f_lattice, g_lattice):
+    """Condensed right-hand side with inhomogeneous Dirichlet data g (the paper's E3):
+    the skeleton unknowns split into free (F) and Dirichlet (D) nodes, u_D = g_D, and the condensed
+    system R Hhat R^T u = R Fhat (Alg. 1) restricted to F reads
+        A_FF u_F = (R Fhat)_F - A_FD g_D,
+    computed element by element: Fhat_e - Hhat_e g_e, g_e = the element's boundary values of g on D
+    (0 on F), gathered by R, Dirichlet entries 0."""
+    grid = op.grid
+    Fe = element_load(grid, f_lattice)
+    dmask = mesh.dirichlet_mask(grid)
+    gD = np.where(dmask, np.asarray(g_lattice, dtype=np.float64).ravel(), 0.0)
+    b = np.zeros(grid.n_lattice)
+    for elems, ce in op.groups:
+        FB = Fe[op.bidx][:, elems]
+        FI = Fe[op.iidx][:, elems]
+        Fh = ce.condense_rhs(FB, FI) - ce.apply(gD[op.GB[elems]].T)
+        np.add.at(b, op.GB[elems].ravel(), Fh.T.ravel())
+    b[~op.free] = 0.0
+    return b
+
+
+def recover(op, f_lattice, u_skel, dirichlet=None):
+    """Full lattice solution: skeleton from u_skel (free nodes) and, if given, the Dirichlet data
+    `dirichlet` (lattice vector, used on the domain-boundary nodes); interiors by Eq.
+    eq:condensation_inner."""
     grid = op.grid
     Fe = element_load(grid, f_lattice)
     u = np.where(op.free, np.asarray(u_skel).ravel(), 0.0)
+    if dirichlet is not None:
+        dmask = mesh.dirichlet_mask(grid)
+        u = np.where(dmask, np.asarray(dirichlet, dtype=np.float64).ravel(), u)
     for elems, ce in op.groups:
         UB = u[op.GB[elems]].T
         FI = Fe[op.iidx][:, elems]

@@ -60,6 +60,8 @@ SIGNATURES = {
     "sc_profile_read": ([_P, _D, ctypes.POINTER(ctypes.c_longlong)], ctypes.c_int),
     "sc_condense_rhs": ([_P, _P, _P, _P], ctypes.c_int),
     "sc_recover": ([_P, _P, _P, _P, _P], ctypes.c_int),
+    "sc_condense_rhs_dirichlet": ([_P, _P, _P, _P, _P], ctypes.c_int),
+    "sc_recover_dirichlet": ([_P, _P, _P, _P, _P, _P], ctypes.c_int),
     "sc_to_transformed": ([_P, _P, _P, ctypes.c_int, _P], ctypes.c_int),
     "sc_from_transformed": ([_P, _P, _P, ctypes.c_int, _P], ctypes.c_int),
     "sc_fill_random": ([_P, ctypes.c_uint64, _P, _P], ctypes.c_int),

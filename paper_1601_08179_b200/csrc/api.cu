@@ -72,6 +72,9 @@ struct sc_ctx {
   bool use_big = false;
   bool use_p2 = false;                  // p = 2 row-warp operator (kernels_p2.cu)
   bool use_rw = false;                  // p = 3, 4 row-warp operator (kernels_rw.cu)
+  bool use_v5 = false;                  // 3 <= p <= 8 halo-recompute tile columns (kernels_v5.cu)
+  std::vector<unsigned char> v5_coef;
+  int v5_ntx = 0, v5_nty = 0, v5_nseg = 1, v5_zseg = 0;
   bool use_ptab = false;                // PCG reads Pinv from the per-class table (uniform geometry)
   PinvTab ptab;                 // v4 colour-scheduled element operator (n_I >= 8, uniform geometry)
   std::vector<unsigned char> big_coef;
@@ -327,10 +330,35 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
     for (int m = 0; m < ni; ++m) sig_ok &= (B.sigma[m] == ((m & 1) ? -1 : 1));
     const char* np2 = getenv("SC_NO_P2");
     const char* nrw = getenv("SC_NO_RW");
-    if (ni == 1 && uniform && sig_ok && !(env && env[0] == '1') && !(np2 && np2[0] == '1')) {
+    // SC_OP selects the p <= 8 operator family: "v5" (default for 3 <= p <= 8), "v3" (tile columns
+    // with look-back, kernels_col.cu), "rw" (p = 3, 4 row-warp kernels)
+    const char* opsel = getenv("SC_OP");
+    const std::string op = opsel ? opsel : "";
+    const bool want_v5 = op.empty() || op == "v5";
+    if (v5_supported(ni) && uniform && sig_ok && want_v5 && !(env && env[0] == '1')) {
+      v5_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->v5_coef);
+      v5_tiles(nx, ny, &ctx->v5_ntx, &ctx->v5_nty);
+      int dev = 0, nsm = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      const char* zs = getenv("SC_ZSEG");
+      if (zs && atoi(zs) > 0) {
+        const int s = atoi(zs) > nz ? nz : atoi(zs);
+        ctx->v5_zseg = (nz + s - 1) / s;
+        ctx->v5_nseg = (nz + ctx->v5_zseg - 1) / ctx->v5_zseg;
+      } else {
+        v5_segments(ctx->v5_ntx * ctx->v5_nty, nz, 2 * nsm, &ctx->v5_nseg, &ctx->v5_zseg);
+      }
+      const size_t nitems = (size_t)ctx->v5_ntx * ctx->v5_nty * ctx->v5_nseg;
+      if (cudaMalloc(&ctx->d_dotp, sizeof(double) * nitems) != cudaSuccess) return fail("cudaMalloc dotp");
+      const char* fd = getenv("SC_FUSED_DOT");
+      ctx->fused_dot = !(fd && fd[0] == '0');
+      ctx->use_v5 = true;
+    } else if (ni == 1 && uniform && sig_ok && !(env && env[0] == '1') && !(np2 && np2[0] == '1')) {
       big_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->big_coef);
       ctx->use_p2 = true;
-    } else if (rw_supported(ni) && uniform && sig_ok && !(env && env[0] == '1') && !(nrw && nrw[0] == '1')) {
+    } else if (rw_supported(ni) && uniform && sig_ok && !(env && env[0] == '1') && !(nrw && nrw[0] == '1') &&
+               op != "v3") {
       big_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->big_coef);
       ctx->use_rw = true;
     } else if (col_supported(ni) && uniform && sig_ok && !(env && env[0] == '1')) {
@@ -363,7 +391,7 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
       ctx->use_col = true;
     }
     // v4 also runs non-uniform grids: each CTA derives its element's coefficients from d_e
-    if (!ctx->use_col && !ctx->use_p2 && !ctx->use_rw && big_supported(ni) && sig_ok && !(env && env[0] == '1')) {
+    if (!ctx->use_v5 && !ctx->use_col && !ctx->use_p2 && !ctx->use_rw && big_supported(ni) && sig_ok && !(env && env[0] == '1')) {
       const double d_one[4] = {1.0, 1.0, 1.0, 1.0};
       big_make_coef(ni, uniform ? g.d_uni : d_one, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->big_coef);
       ctx->use_big = true;
@@ -574,7 +602,10 @@ static sc_status apply_impl(sc_ctx* ctx, const double* x, double* y, const doubl
                             double* dotp = nullptr) {
   const bool rec = ctx->prof_on && ctx->prof_n < (int)ctx->prof_ev.size() / 2;
   cudaEvent_t* ev = rec ? &ctx->prof_ev[2 * ctx->prof_n] : nullptr;
-  if (ctx->use_col)
+  if (ctx->use_v5)
+    LAUNCH(launch_apply_v5(ctx->g, x, y, done, ctx->v5_ntx, ctx->v5_nty, ctx->v5_nseg, ctx->v5_zseg,
+                           ctx->v5_coef.data(), dotp, st, &nl_, ev));
+  else if (ctx->use_col)
     LAUNCH(launch_apply_col_raw(ctx->g, x, y, done, ctx->d_colstate, ctx->d_flags, ctx->d_corner, ctx->d_pending,
                                 ctx->col_ntx, ctx->col_nty, ctx->col_nseg, ctx->col_zseg, ctx->col_coef.data(), dotp,
                                 st, &nl_, ev));
@@ -618,11 +649,14 @@ static sc_status pcg_iteration(sc_ctx* ctx, cudaStream_t st) {
   // entries it finalizes, one fixed-order sum follows.  At cfg5 12.47 -> 11.74 ms per iteration
   // against the separate dot kernel (which streams p and q once more); SC_FUSED_DOT=0 disables it.
   // (Early in round 1, with a slower operator, it measured slower: 10.67 vs 9.55 + 0.9 ms.)
-  const bool fused = ctx->use_col && ctx->prm.nranks == 1 && ctx->fused_dot;
+  // v5 returns per-CTA partials of x . A x over its owned entities / elements, which sum to p . q on
+  // any number of ranks (each rank's partial interface-plane sums included): fused there on every rank.
+  const bool fused = ((ctx->use_col && ctx->prm.nranks == 1) || ctx->use_v5) && ctx->fused_dot;
+  const int nparts = ctx->use_v5 ? ctx->v5_ntx * ctx->v5_nty * ctx->v5_nseg : ctx->col_ntx * ctx->col_nty * ctx->col_nseg;
   sc_status s = apply_impl(ctx, ctx->pv, ctx->q, done, st, fused ? ctx->d_dotp : nullptr);
   if (s) return s;
   if (fused) {
-    LAUNCH(launch_sum_ordered(ctx->d_dotp, ctx->col_ntx * ctx->col_nty * ctx->col_nseg, ctx->scal, SCAL_RED0, done, st, &nl_));
+    LAUNCH(launch_sum_ordered(ctx->d_dotp, nparts, ctx->scal, SCAL_RED0, done, st, &nl_));
   } else {
     LAUNCH(launch_dot_partial(ctx->pv, ctx->q, n, ctx->own, ctx->partials, done, st, &nl_));
     LAUNCH(launch_reduce2(ctx->partials, ctx->scal, SCAL_RED0, 1, done, st, &nl_));
@@ -820,6 +854,49 @@ extern "C" sc_status sc_recover(sc_ctx* ctx, const double* d_f, const double* d_
   if (ctx->broken) return SC_ESTATE;
   if (!ctx->ws) { ctx->err = "workspace not bound"; return SC_ESTATE; }
   LAUNCH(launch_recover(ctx->g, d_f, d_x, d_u, ctx->scratch, ctx->scratch_elems, (cudaStream_t)stream, &nl_));
+  return SC_OK;
+}
+
+// Inhomogeneous Dirichlet data (the paper's solver benchmark E3: u = u_ex on the
+// boundary of (0, 2 pi)^3).  With the data g on the Dirichlet skeleton entities D and the free ones F,
+// the condensed system is  A_FF x_F = b_F - A_FD g_D  (reading R17).  In the transformed
+// basis the lifting vector is g~ = Shat^{-T} g on D (every skeleton entity is either entirely in D
+// or entirely in F, and Shat acts inside entities), and A_FD g~_D is one operator application with
+// the Dirichlet columns kept (one-CTA-per-element kernel, any geometry).  Uses the PCG buffers of
+// the workspace as scratch: not to be called between sc_pcg_start and sc_pcg_status.
+extern "C" sc_status sc_condense_rhs_dirichlet(sc_ctx* ctx, const double* d_f, const double* d_g, double* d_b,
+                                               void* stream) {
+  if (!ctx || !d_f || !d_g || !d_b) return SC_EINVAL;
+  if (ctx->broken) return SC_ESTATE;
+  if (!ctx->ws) { ctx->err = "workspace not bound"; return SC_ESTATE; }
+  cudaStream_t st = (cudaStream_t)stream;
+  LAUNCH(launch_condense(ctx->g, d_f, d_b, ctx->scratch, ctx->scratch_elems, st, &nl_));
+  sc_status s = halo_sum(ctx, d_b, st);
+  if (s) return s;
+  Geom gn = ctx->g;
+  gn.nodir = 1;
+  LAUNCH(launch_convert(gn, d_g, ctx->pv, 1, MAT_SM, st, &nl_));       // Shat^{-T} g at every entity
+  LAUNCH(launch_dir_split(ctx->g, ctx->pv, nullptr, 0, st, &nl_));    // keep D only: g~_D
+  LAUNCH(launch_apply(gn, ctx->pv, ctx->q, nullptr, st, &nl_));       // A (., D) g~_D
+  if ((s = halo_sum(ctx, ctx->q, st))) return s;
+  LAUNCH(launch_dir_split(ctx->g, d_b, ctx->q, 1, st, &nl_));         // b_F -= (A g~_D)_F, b_D = 0
+  return SC_OK;
+}
+
+// Alg. 4 post with the Dirichlet data: the skeleton solution is x~ on F and g~ on D; interiors by
+// u~_I = D^{-1}(F~_I - Htilde_IB u~_B), lattice values u = (S(x)S(x)S)^T u~ (boundary nodes = g).
+extern "C" sc_status sc_recover_dirichlet(sc_ctx* ctx, const double* d_f, const double* d_g, const double* d_x,
+                                          double* d_u, void* stream) {
+  if (!ctx || !d_f || !d_g || !d_x || !d_u) return SC_EINVAL;
+  if (ctx->broken) return SC_ESTATE;
+  if (!ctx->ws) { ctx->err = "workspace not bound"; return SC_ESTATE; }
+  cudaStream_t st = (cudaStream_t)stream;
+  Geom gn = ctx->g;
+  gn.nodir = 1;
+  LAUNCH(launch_convert(gn, d_g, ctx->pv, 1, MAT_SM, st, &nl_));
+  CK(cudaMemcpyAsync(ctx->q, d_x, sizeof(double) * ctx->g.n_total, cudaMemcpyDeviceToDevice, st));
+  LAUNCH(launch_dir_split(ctx->g, ctx->q, ctx->pv, 2, st, &nl_));     // x~ on F, g~ on D
+  LAUNCH(launch_recover(gn, d_f, ctx->q, d_u, ctx->scratch, ctx->scratch_elems, st, &nl_));
   return SC_OK;
 }
 

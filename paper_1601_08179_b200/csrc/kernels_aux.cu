@@ -18,7 +18,7 @@ __global__ void k_to_skel(Geom g, const double* __restrict__ in, double* __restr
        q += (long long)gridDim.x * blockDim.x) {
     int gx, gy, gz;
     bool dr;
-    if (!decode_entry(g, q, &gx, &gy, &gz, &dr) || dr) { out[q] = 0.0; continue; }
+    if (!decode_entry(g, q, &gx, &gy, &gz, &dr) || (dr && !g.nodir)) { out[q] = 0.0; continue; }
     int c[3] = {gx, gy, gz};
     int free_dirs[2], nf = 0;
     for (int d = 0; d < 3; ++d)
@@ -94,7 +94,7 @@ __global__ void k_from_skel(Geom g, const double* __restrict__ in, double* __res
     if (nf == 3) { out[q] = 0.0; continue; }
     bool dr;
     long long si = skel_index(g, gx, gy, gz, &dr);
-    if (dr) { out[q] = 0.0; continue; }
+    if (dr && !g.nodir) { out[q] = 0.0; continue; }
     double v;
     if (nf == 0 || mat == MAT_I) {
       v = in[si];
@@ -237,7 +237,7 @@ __global__ void k_recover(Geom g, const double* __restrict__ f, const double* __
       shell_node(p, ni, s, &i, &j, &k, &ent, &loc);
       bool dr;
       long long base = entity_base(g, ex, ey, ez, ent, &dr);
-      buf[i + n * (j + n * k)] = dr ? 0.0 : x[base + loc];
+      buf[i + n * (j + n * k)] = (dr && !g.nodir) ? 0.0 : x[base + loc];
     }
     __syncthreads();
     // u~_I = D^{-1} (F~_I - Htilde_IB u~_B)   (Alg. 4)
@@ -263,6 +263,28 @@ __global__ void k_recover(Geom g, const double* __restrict__ f, const double* __
     }
     __syncthreads();
   }
+}
+
+// Free / Dirichlet split of skeleton vectors (inhomogeneous Dirichlet data, P:625 E3):
+//   mode 0: a <- a on Dirichlet entries, 0 elsewhere (the lifting vector)
+//   mode 1: a <- 0 on Dirichlet entries, a - b elsewhere (subtract the lifting's image)
+//   mode 2: a <- b on Dirichlet entries, a elsewhere (complete a free solution with its data)
+__global__ void k_dir_split(Geom g, double* __restrict__ a, const double* __restrict__ b, int mode) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < g.n_total;
+       q += (long long)gridDim.x * blockDim.x) {
+    int gx, gy, gz;
+    bool dr;
+    if (!decode_entry(g, q, &gx, &gy, &gz, &dr)) { a[q] = 0.0; continue; }
+    if (mode == 0) a[q] = dr ? a[q] : 0.0;
+    else if (mode == 1) a[q] = dr ? 0.0 : a[q] - b[q];
+    else if (dr) a[q] = b[q];
+  }
+}
+
+int launch_dir_split(const Geom& g, double* a, const double* b, int mode, void* stream, int* nl) {
+  k_dir_split<<<1184, 256, 0, (cudaStream_t)stream>>>(g, a, b, mode);
+  (*nl)++;
+  return cudaGetLastError();
 }
 
 int launch_convert(const Geom& g, const double* in, double* out, int to_skel, int mat, void* stream, int* nl) {

@@ -79,7 +79,7 @@ __global__ void k_apply_v1(Geom g, const double* __restrict__ x, double* __restr
   if (tid < 26) {
     bool dr;
     sBase[tid] = entity_base(g, ex, ey, ez, tid, &dr);
-    sDir[tid] = dr;
+    sDir[tid] = dr && !g.nodir;
   }
   for (int t = tid; t < ni; t += nt) {
     sLam[t] = g.tab[TAB_LAM + t];

@@ -1,0 +1,1011 @@
+// Condensed operator v5 (rows a3-a8 of SURVEY §8(a)) for 2 <= n_I <= 7 (p = 3..8), uniform
+// geometry: tile columns with a recomputed halo, bulk-copy (TMA) row loads, class-specialised
+// condensed part, two CTAs per SM.
+//
+// Work decomposition.  A CTA owns the skeleton entities of an xy-tile of 7 x 3 elements over a
+// z-segment of element layers: x-faces fx in [x0, x0+7), y-faces fy in [y0, y0+3), z-faces /
+// edges / vertices of the same index ranges, element layers [lfin0, lend] and planes
+// [lfin0, lend] (+ plane nz for the top segment).  Its 32 lanes compute the 8 x 4 elements
+// ex in [x0-1, x0+7), ey in [y0-1, y0+3): the extra column / row (the "halo") are the
+// neighbours whose condensed parts reach the owned W / S faces.  Every owned entity is then
+// complete inside the CTA: no inter-CTA communication (no look-back, flags or atomics), each
+// skeleton entry is written exactly once, and the result is independent of scheduling.
+// Edges and vertices have no condensed part (c13), so their values are primary-part
+// stencils of the input, computed entity-centrically by their owner.
+//
+// The CTA marches up its column one element layer per step.  Per step l it bulk-loads
+// (cp.async.bulk + mbarrier, one elected thread) the rows of layer l (x-faces, y-faces,
+// z-edges) and plane l+1 (z-faces, x-edges, y-edges, vertices); plane l stays from the previous
+// step.  Each entity row of the tile is one contiguous skeleton range; a row is
+// copied as the 16-byte aligned superset of its valid range into a slot whose base has the same
+// 8-byte phase, so the row sits at slot + (global index & 1).
+//
+// Condensed part (Table 2, Eq. 26) in the even / odd form of v3 (kernels_col.cu):
+// with ap = sigma .* a0, the interior points split into 8 parity classes (s_i, s_j, s_k); warp w
+// runs one class for all 32 elements (lane = element), fully unrolled with compile-time indices,
+// so every coefficient (c_d = d_d a0, D^{-1}) is a constant-bank operand.  Per direction the two
+// classes of equal other parities form a pair: the "consumer" computes the owned faces' primary
+// part (phase A) and adds its own faces-out sums as soon as they are complete (streaming, no
+// registers held); the "producer" holds its sums until the face inputs are dead and hands them
+// over through shared memory (overlaid on the dead input rows).  Roles are a per-n_I table
+// chosen to bound the registers held and to balance the warps.
+//
+// Fused p . q (PCG): x . A x = sum over owned entities of x * (primary part) - sum over owned
+// elements of the condensed energy uhat . D^{-1} uhat (uhat = faces-in of the element), so
+// each CTA returns its partial without re-reading x.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+#include "sc_device.cuh"
+
+namespace sc {
+
+struct V5Coef {
+  double c[3][8];        // c[d][m] = d_{d+1} a0_m                        (condensed faces in / out)
+  double dinv[343];      // D^{-1}(i,j,k) = 1/(d0 + d1 Lam_i + d2 Lam_j + d3 Lam_k), i fastest
+  double fdx[49];        // x-face self (2 elements): 2 (d0 w0 + d1 K00 + d2 w0 Lam_j + d3 w0 Lam_k) at j + NI k
+  double fdy[49];        // y-face self: 2 (d0 w0 + d2 K00 + d1 w0 Lam_i + d3 w0 Lam_k) at i + NI k
+  double fdz[49];        // z-face self per layer: d0 w0 + d3 K00 + d1 w0 Lam_i + d2 w0 Lam_j at i + NI j
+  double k0p[3];         // d_{d+1} K0p                                   (opposite face)
+  double ef2[3][8];      // 2 d_{d+1} w0 a0_m    (x- / y-face <- bounding edges, 2 elements)
+  double ef1[3][8];      // d_{d+1} w0 a0_m      (z-face <- bounding edges, one layer)
+  double czu[8], cxu[8], cyu[8];   // edge self terms (see the edge phase)
+  double sc[16];         // scalars of the edge / vertex stencils (see v5_make_coef)
+  double a0[8], sig[8];
+};
+
+struct V5Params {
+  Geom g;
+  const double* x;
+  double* y;
+  const double* done;
+  double* dotp;          // per-CTA partials of x . (A x) (fused PCG p . q), or null
+  int ntx, nty, nseg, zseg, nitems;
+  V5Coef cf;
+};
+
+namespace v5 {
+
+constexpr int TX = 8, TY = 4, OX = 7, OY = 3, NO = OX * OY, NT = 256;
+
+constexpr int slot_len(int len) {
+  int v = len + 2;
+  if (v & 1) ++v;
+  if (len >= 16)
+    while (v % 16 != 8) v += 2;   // rows of consecutive lanes on disjoint bank pairs
+  return v;
+}
+constexpr int even(int v) { return v + (v & 1); }
+
+template <int NI>
+struct L {
+  static constexpr int N2 = NI * NI;
+  static constexpr int XS = slot_len((TX + 1) * N2), YS = slot_len(TX * N2), ZS = slot_len(TX * N2);
+  static constexpr int ZES = slot_len((TX + 1) * NI), XES = slot_len(TX * NI), YES = slot_len((TX + 1) * NI);
+  static constexpr int VS = slot_len(TX + 1);
+  static constexpr int O_XF = 0;
+  static constexpr int O_YF = O_XF + TY * XS;
+  static constexpr int O_ZE = O_YF + (TY + 1) * YS;
+  static constexpr int O_ZF = O_ZE + (TY + 1) * ZES;       // 2 planes (plane q in q & 1)
+  static constexpr int PZ = TY * ZS;
+  static constexpr int O_PL = O_ZF + 2 * PZ;                // 2 planes of edges / vertices
+  static constexpr int PLX = 0, PLY = (TY + 1) * XES, PLV = PLY + TY * YES, PLS = PLV + (TY + 1) * VS;
+  static constexpr int ACC = even(NO * N2);
+  static constexpr int O_AX = O_PL + 2 * PLS;               // owned x-faces of the layer
+  static constexpr int O_AY = O_AX + ACC;                   // owned y-faces of the layer
+  static constexpr int O_AZ = O_AY + ACC;                   // owned z-faces, 2 planes
+  static constexpr int AES = even(2 * NO * NI + NO);        // per plane: x-edges | y-edges | vertices
+  static constexpr int O_AE = O_AZ + 2 * ACC;
+  static constexpr int O_TAB = O_AE + 2 * AES;              // a0, sigma a0, czu, cxu, cyu (8 each)
+  static constexpr int O_SCR = O_TAB + 40;                  // scratch row of the lanes that own nothing
+  static constexpr int TOTAL = O_SCR + even(N2);
+  // exchange buffers of the producer sums ([lane][N2]) overlaid on dead input rows
+  static constexpr int O_QX = O_XF, O_QY = O_YF;            // O_QZ: the bottom plane's z-face rows
+  static_assert(TY * XS >= 32 * N2 && (TY + 1) * YS >= 32 * N2 && PZ >= 32 * N2, "exchange overlay");
+};
+
+// row kinds of the per-item descriptor table: 0..3 x-faces, 4..8 y-faces, 9..13 z-edges (side rows,
+// layer l); 14..17 z-faces, 18..22 x-edges, 23..26 y-edges, 27..31 vertices (plane rows)
+constexpr int R_XF = 0, R_YF = 4, R_ZE = 9, R_ZF = 14, R_XE = 18, R_YE = 23, R_V = 27, NROWS = 32;
+constexpr int NSIDE = 14;
+
+struct Row {
+  long long g0, gs;   // skeleton index of the row start at layer / plane 0, per-layer stride
+  int slot, len;      // smem slot offset (doubles), row length (entries)
+  int a, b;           // valid, non-Dirichlet entries [a, b) (a >= b: nothing to copy)
+  int plane;          // plane row (Dirichlet when its plane is)
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* m, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* m, unsigned bytes) {
+  unsigned long long state;
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 %0, [%1], %2;"
+               : "=l"(state)
+               : "r"(smem_u32(m)), "r"(bytes)
+               : "memory");
+  (void)state;
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W: mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W;\n}\n" ::"r"(smem_u32(m)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* m) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(m))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// ---- per-item row descriptors ------------------------------------------------------------
+template <int NI>
+__device__ void make_row(const Geom& g, int r, int cx0, int cy0, Row& d) {
+  using LL = L<NI>;
+  constexpr int N2 = NI * NI;
+  const int nx = g.nx, ny = g.ny;
+  auto clampx = [&](int lo_ok, int hi_ok, int per) {   // valid index range [lo_ok, hi_ok] of the row's entities
+    const int lo = max(cx0, lo_ok), hi = min(cx0 + TX - (per == 0 ? 1 : 0), hi_ok);
+    d.a = (lo - cx0) * (per ? per : 1);
+    d.b = (hi - cx0 + 1) * (per ? per : 1);
+  };
+  (void)clampx;
+  d.plane = 0;
+  if (r < R_YF) {                                   // x-faces (fx in [cx0, cx0+8], ey = cy0 + r)
+    const int ey = cy0 + r;
+    d.g0 = g.off_f[0] + ((long long)cx0 + (long long)(nx + 1) * ey) * N2;
+    d.gs = (long long)(nx + 1) * ny * N2;
+    d.slot = LL::O_XF + r * LL::XS; d.len = (TX + 1) * N2;
+    const int lo = max(cx0, 1), hi = min(cx0 + TX, nx - 1);
+    d.a = (lo - cx0) * N2; d.b = (hi - cx0 + 1) * N2;
+    if (ey < 0 || ey >= ny) d.b = d.a;
+  } else if (r < R_ZE) {                            // y-faces (ex in [cx0, cx0+8), fy = cy0 + q)
+    const int fy = cy0 + (r - R_YF);
+    d.g0 = g.off_f[1] + ((long long)cx0 + (long long)nx * fy) * N2;
+    d.gs = (long long)nx * (ny + 1) * N2;
+    d.slot = LL::O_YF + (r - R_YF) * LL::YS; d.len = TX * N2;
+    const int lo = max(cx0, 0), hi = min(cx0 + TX - 1, nx - 1);
+    d.a = (lo - cx0) * N2; d.b = (hi - cx0 + 1) * N2;
+    if (fy < 1 || fy > ny - 1) d.b = d.a;
+  } else if (r < R_ZF) {                            // z-edges (fx in [cx0, cx0+8], fy = cy0 + q)
+    const int fy = cy0 + (r - R_ZE);
+    d.g0 = g.off_e[2] + ((long long)cx0 + (long long)(nx + 1) * fy) * NI;
+    d.gs = (long long)(nx + 1) * (ny + 1) * NI;
+    d.slot = LL::O_ZE + (r - R_ZE) * LL::ZES; d.len = (TX + 1) * NI;
+    const int lo = max(cx0, 1), hi = min(cx0 + TX, nx - 1);
+    d.a = (lo - cx0) * NI; d.b = (hi - cx0 + 1) * NI;
+    if (fy < 1 || fy > ny - 1) d.b = d.a;
+  } else if (r < R_XE) {                            // z-faces (ex in [cx0, cx0+8), ey = cy0 + q), plane rows
+    const int ey = cy0 + (r - R_ZF);
+    d.g0 = g.off_f[2] + ((long long)cx0 + (long long)nx * ey) * N2;
+    d.gs = (long long)nx * ny * N2;
+    d.slot = LL::O_ZF + (r - R_ZF) * LL::ZS; d.len = TX * N2;
+    const int lo = max(cx0, 0), hi = min(cx0 + TX - 1, nx - 1);
+    d.a = (lo - cx0) * N2; d.b = (hi - cx0 + 1) * N2;
+    if (ey < 0 || ey >= ny) d.b = d.a;
+    d.plane = 1;
+  } else if (r < R_YE) {                            // x-edges (ex in [cx0, cx0+8), fy = cy0 + q)
+    const int fy = cy0 + (r - R_XE);
+    d.g0 = g.off_e[0] + ((long long)cx0 + (long long)nx * fy) * NI;
+    d.gs = (long long)nx * (ny + 1) * NI;
+    d.slot = LL::O_PL + LL::PLX + (r - R_XE) * LL::XES; d.len = TX * NI;
+    const int lo = max(cx0, 0), hi = min(cx0 + TX - 1, nx - 1);
+    d.a = (lo - cx0) * NI; d.b = (hi - cx0 + 1) * NI;
+    if (fy < 1 || fy > ny - 1) d.b = d.a;
+    d.plane = 1;
+  } else if (r < R_V) {                             // y-edges (fx in [cx0, cx0+8], ey = cy0 + q)
+    const int ey = cy0 + (r - R_YE);
+    d.g0 = g.off_e[1] + ((long long)cx0 + (long long)(nx + 1) * ey) * NI;
+    d.gs = (long long)(nx + 1) * ny * NI;
+    d.slot = LL::O_PL + LL::PLY + (r - R_YE) * LL::YES; d.len = (TX + 1) * NI;
+    const int lo = max(cx0, 1), hi = min(cx0 + TX, nx - 1);
+    d.a = (lo - cx0) * NI; d.b = (hi - cx0 + 1) * NI;
+    if (ey < 0 || ey >= ny) d.b = d.a;
+    d.plane = 1;
+  } else {                                          // vertices (fx in [cx0, cx0+8], fy = cy0 + q)
+    const int fy = cy0 + (r - R_V);
+    d.g0 = g.off_v + (long long)cx0 + (long long)(nx + 1) * fy;
+    d.gs = (long long)(nx + 1) * (ny + 1);
+    d.slot = LL::O_PL + LL::PLV + (r - R_V) * LL::VS; d.len = TX + 1;
+    const int lo = max(cx0, 1), hi = min(cx0 + TX, nx - 1);
+    d.a = lo - cx0; d.b = hi - cx0 + 1;
+    if (fy < 1 || fy > ny - 1) d.b = d.a;
+    d.plane = 1;
+  }
+  if (d.b < d.a) d.b = d.a;
+}
+
+// smem offset of row r for layer / plane q (its slot, plane slots alternating with q)
+template <int NI>
+__device__ __forceinline__ int row_off(const Row& d, int r, int q) {
+  using LL = L<NI>;
+  int s = d.slot;
+  if (r >= R_ZF) s += (q & 1) * (r < R_XE ? LL::PZ : LL::PLS);
+  return s + (int)((d.g0 + (long long)q * d.gs) & 1);
+}
+
+// Bulk loads of one step, issued by warp 0 as one mbarrier transaction: the side rows of layer qs
+// (if side), the plane rows of plane qa (if pa) and of plane qb (if pb); copy c = lane, lane + 32
+// over the list [side rows 0..13 | plane rows of qa | plane rows of qb].
+template <int NI>
+__device__ void issue_step(const V5Params& P, double* sm, const Row* rows, bool side, int qs, bool pa, int qa, bool za,
+                           bool pb, int qb, bool zb, unsigned long long* mbar) {
+  const int lane = threadIdx.x & 31;
+  unsigned bytes[2] = {0u, 0u};
+  long long src[2] = {0, 0};
+  int dst[2] = {0, 0};
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int c = lane + 32 * h;
+    if (c >= NSIDE + 2 * (NROWS - NSIDE)) continue;
+    int r, q;
+    bool on;
+    if (c < NSIDE) { r = c; q = qs; on = side; }
+    else if (c < NROWS) { r = c; q = qa; on = pa && !za; }
+    else { r = c - (NROWS - NSIDE); q = qb; on = pb && !zb; }
+    const Row& d = rows[r];
+    if (!on || d.a >= d.b) continue;
+    const long long gq = d.g0 + (long long)q * d.gs;
+    const long long ga = gq + d.a, gb = gq + d.b;
+    src[h] = ga & ~1LL;
+    bytes[h] = (unsigned)(((gb + 1) & ~1LL) - src[h]) * 8u;
+    dst[h] = row_off<NI>(d, r, q) + d.a - (int)(ga & 1);
+  }
+  unsigned tot = bytes[0] + bytes[1];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+  if (lane == 0) mbar_arrive_tx(mbar, tot);
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+    if (bytes[h]) bulk_g2s(sm + dst[h], P.x + src[h], bytes[h], mbar);
+}
+
+// zero the invalid / Dirichlet parts of rows [r0, r1) for layer / plane q (after the wait)
+template <int NI>
+__device__ __noinline__ void fix_rows(double* sm, const Row* rows, int r0, int r1, int q, bool zplane) {
+#pragma unroll 1
+  for (int r = r0 + (threadIdx.x >> 5); r < r1; r += NT / 32) {
+    const Row& d = rows[r];
+    double* b = sm + row_off<NI>(d, r, q);
+    const bool none = d.a >= d.b || (d.plane && zplane);
+    const int a = none ? d.len : d.a, e = none ? d.len : d.b;
+    for (int t = threadIdx.x & 31; t < a; t += 32) b[t] = 0.0;
+    for (int t = e + (threadIdx.x & 31); t < d.len; t += 32) b[t] = 0.0;
+  }
+}
+
+template <int NI>
+__device__ __forceinline__ bool rows_complete(const Row* rows, int r0, int r1) {
+#pragma unroll 1
+  for (int r = r0; r < r1; ++r)
+    if (rows[r].a != 0 || rows[r].b != rows[r].len) return false;
+  return true;
+}
+
+// ---- per-step view of the tile in shared memory --------------------------------------------
+// Row r of a kind starts at sm + offset table entry (offsets of the step's layer / planes, in
+// shared memory: lane-dependent rows are then one shared load, not local-memory pointer arrays).
+struct View {
+  const double* sm;
+  const int* rs;   // side rows, layer l
+  const int* rb;   // plane rows, plane l
+  const int* rt;   // plane rows, plane l + 1
+  __device__ __forceinline__ const double* xf(int r) const { return sm + rs[R_XF + r]; }   // x-faces (fx in [cx0, cx0+8])
+  __device__ __forceinline__ const double* yf(int r) const { return sm + rs[R_YF + r]; }   // y-faces (ex in [cx0, cx0+8))
+  __device__ __forceinline__ const double* ze(int r) const { return sm + rs[R_ZE + r]; }   // z-edges (fx)
+  __device__ __forceinline__ const double* zf(int kb, int r) const { return sm + (kb ? rt : rb)[R_ZF + r]; }
+  __device__ __forceinline__ const double* xe(int kb, int r) const { return sm + (kb ? rt : rb)[R_XE + r]; }
+  __device__ __forceinline__ const double* ye(int kb, int r) const { return sm + (kb ? rt : rb)[R_YE + r]; }
+  __device__ __forceinline__ const double* vv(int kb, int r) const { return sm + (kb ? rt : rb)[R_V + r]; }
+};
+
+// ---- class roles ------------------------------------------------------------------------------
+// consumer parity of every direction pair (bits: x-pair (s_j, s_k) at 2 s_j + s_k, y-pair (s_i, s_k)
+// at 4 + 2 s_i + s_k, z-pair (s_i, s_j) at 8 + 2 s_i + s_j), from a search that bounds the doubles
+// a class holds (its z sums + the x / y sums it produces) and balances the warps' work
+template <int NI>
+struct Roles {
+  static constexpr int bits = (NI == 7 || NI == 5 || NI == 3) ? 256 : 60;
+  template <int SI, int SJ, int SK>
+  struct C {
+    static constexpr bool X = SI == ((bits >> (2 * SJ + SK)) & 1);
+    static constexpr bool Y = SJ == ((bits >> (4 + 2 * SI + SK)) & 1);
+    static constexpr bool Z = SK == ((bits >> (8 + 2 * SI + SJ)) & 1);
+  };
+};
+// warp -> class (s_i s_j s_k); warps w and w + 4 share an SM sub-partition: heavy with light
+__device__ __constant__ int kV5Class[8] = {1, 0, 2, 4, 7, 3, 6, 5};
+
+// ---- class phase: primaries of the consumed faces + condensed part, streamed per k-step ----------
+__device__ __forceinline__ void bar_pair(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+
+// One class (s_i, s_j, s_k) of the 32 lanes' elements.  The k loop is not unrolled (runtime k: the
+// D^{-1} / c3 constants come from the parameter bank with a register offset) so that the eight
+// classes' code fits the instruction caches; i and j are unrolled (compile-time shared-memory
+// offsets and c1 / c2 operands).  Exchange without held registers: the x-face entries (J, K) are
+// read only by the x-pair (s_i = 0, 1 of the same (s_j, s_k)), the y-face entries (I, K) only by the
+// y-pair and the z-face entries (I, J) only by the z-pair (and by the edge phase, which precedes).
+// So after the pair's named barrier of k-step k, the producer writes its completed x sums Q(j, k)
+// (y sums Q(i, k)) over its own lane's input entries (j, k), which are dead, and the consumer adds
+// them to its accumulator after the next barrier.  z sums complete at the end of the loop and go
+// over the bottom face entries (I, J) after a z-pair barrier.
+template <int NI, bool DOT, int SI, int SJ, int SK>
+struct Cls {
+  static constexpr int N2 = NI * NI;
+  static constexpr int CI = (NI - SI + 1) / 2, CJ = (NI - SJ + 1) / 2, CK = (NI - SK + 1) / 2;
+  using R = typename Roles<NI>::template C<SI, SJ, SK>;
+  static constexpr double gi = SI ? -1.0 : 1.0, gj = SJ ? -1.0 : 1.0, gk = SK ? -1.0 : 1.0;
+  static constexpr int XB = 1 + 2 * SJ + SK, YB = 5 + 2 * SI + SK, ZB = 9 + 2 * SI + SJ;   // pair barriers
+
+  // acx / acy: this lane's owned x- / y-face accumulators, azb / azt: owned z-face accumulators of
+  // planes l / l+1 (a shared scratch row for lanes that own nothing: every store is unconditional,
+  // no divergence around the shuffles)
+  static __device__ __forceinline__ void run(const V5Coef& cf, const View& V, int ix, int iy, bool own, double* acx,
+                                             double* acy, double* azb, double* azt, double& dot, bool dot_lay,
+                                             bool dot_b, bool dot_t) {
+    double* const W = const_cast<double*>(V.xf(iy)) + ix * N2;     // W face (E face = W + N2)
+    double* const S = const_cast<double*>(V.yf(iy)) + ix * N2;     // S face
+    const double* Nn = V.yf(iy + 1) + ix * N2;                      // N face
+    double* const B = const_cast<double*>(V.zf(0, iy)) + ix * N2;  // B face (plane l)
+    const double* T = V.zf(1, iy) + ix * N2;                        // T face (plane l + 1)
+    // ---------------- z-face primaries (Eq. 26 generalised), planes l (kb = 0) and l + 1 (kb = 1)
+    if constexpr (R::Z) {
+#pragma unroll 1
+      for (int kb = 0; kb < 2; ++kb) {
+        const double* Yw = V.ye(kb, iy) + ix * NI;    // y-edge (ex, ey) at the plane
+        const double* Ye = Yw + NI;                   // y-edge (ex + 1, ey)
+        const double* Xs = V.xe(kb, iy) + ix * NI;    // x-edge (ex, fy = ey)
+        const double* Xn = V.xe(kb, iy + 1) + ix * NI;
+        const double* U = kb ? T : B;
+        const double* Uo = kb ? B : T;
+        double xc[CI];
+#pragma unroll
+        for (int ii = 0; ii < CI; ++ii) xc[ii] = fma(gj, Xn[SI + 2 * ii], Xs[SI + 2 * ii]);
+        double* const az = kb ? azt : azb;
+#pragma unroll 1
+        for (int jj = 0; jj < CJ; ++jj) {
+          const int j = SJ + 2 * jj;
+          const double yc = fma(gi, Ye[j], Yw[j]);
+          const double e1j = cf.ef1[1][j];
+#pragma unroll
+          for (int ii = 0; ii < CI; ++ii) {
+            const int i = SI + 2 * ii, o = i + NI * j;
+            const double u = U[o];
+            const double pr = fma(cf.fdz[o], u, fma(cf.k0p[2], Uo[o], fma(cf.ef1[0][i], yc, e1j * xc[ii])));
+            az[o] = kb ? pr : az[o] + pr;
+            if (DOT && (kb ? dot_t : dot_b) && own) dot = fma(u, pr, dot);
+          }
+        }
+      }
+    }
+    // k-independent edge combinations of the x- / y-face primaries
+    double yex[R::X ? CJ : 1], xey[R::Y ? CI : 1];
+    if constexpr (R::X) {
+      const double* Yb = V.ye(0, iy) + ix * NI;       // y-edge (fx, ey) at plane l
+      const double* Yt = V.ye(1, iy) + ix * NI;
+#pragma unroll
+      for (int jj = 0; jj < CJ; ++jj) yex[jj] = fma(gk, Yt[SJ + 2 * jj], Yb[SJ + 2 * jj]);
+    }
+    if constexpr (R::Y) {
+      const double* Xb = V.xe(0, iy) + ix * NI;       // x-edge (ex, fy) at plane l
+      const double* Xt = V.xe(1, iy) + ix * NI;
+#pragma unroll
+      for (int ii = 0; ii < CI; ++ii) xey[ii] = fma(gk, Xt[SI + 2 * ii], Xb[SI + 2 * ii]);
+    }
+    const double* const Zs = V.ze(iy) + ix * NI;      // z-edge (fx = cx0 + ix, fy = cy0 + iy)
+    const double* const Zn = V.ze(iy + 1) + ix * NI;
+    const double* const Wm = ix > 0 ? W - N2 : W;
+    const double* const Sm = iy > 0 ? V.yf(iy - 1) + ix * N2 : S;
+    // producer sums of the neighbour lanes (x: lane ix - 1 = slot ix - 1, y: row iy - 1)
+    const double* const Wp = ix > 0 ? W - N2 : W;
+    const double* const Sp = Sm;
+    // ---------------- condensed part
+    double zin[CI][CJ], qz[CI][CJ];
+#pragma unroll
+    for (int ii = 0; ii < CI; ++ii)
+#pragma unroll
+      for (int jj = 0; jj < CJ; ++jj) {
+        const int o = SI + 2 * ii + NI * (SJ + 2 * jj);
+        zin[ii][jj] = fma(gk, T[o], B[o]);
+        qz[ii][jj] = 0.0;
+      }
+    double en = 0.0;   // condensed energy uhat . v of this class
+#pragma unroll 1
+    for (int kk = 0; kk <= CK; ++kk) {
+      const int k = SK + 2 * kk;
+      if (kk < CK) {
+        // ---- primaries of the consumed x- / y-face entries at this k
+        if constexpr (R::X) {
+          const double zc = fma(gj, Zn[k], Zs[k]);
+#pragma unroll
+          for (int jj = 0; jj < CJ; ++jj) {
+            const int j = SJ + 2 * jj, o = j + NI * k;
+            const double u = W[o];
+            const double pr = fma(cf.fdx[o], u, fma(cf.k0p[0], Wm[o] + W[o + N2], fma(cf.ef2[1][j], zc, cf.ef2[2][k] * yex[jj])));
+            acx[o] = pr;
+            if (DOT && dot_lay && own) dot = fma(u, pr, dot);
+          }
+        }
+        if constexpr (R::Y) {
+          const double zc = fma(gi, Zs[NI + k], Zs[k]);   // z-edges (ex, fy) and (ex + 1, fy)
+#pragma unroll
+          for (int ii = 0; ii < CI; ++ii) {
+            const int i = SI + 2 * ii, o = i + NI * k;
+            const double u = S[o];
+            const double pr = fma(cf.fdy[o], u, fma(cf.k0p[1], Sm[o] + Nn[o], fma(cf.ef2[0][i], zc, cf.ef2[2][k] * xey[ii])));
+            acy[o] = pr;
+            if (DOT && dot_lay && own) dot = fma(u, pr, dot);
+          }
+        }
+        // ---- faces in, D^{-1}, faces out at this k
+        double yin[CI], qy[CI], qxs[CJ];
+#pragma unroll
+        for (int ii = 0; ii < CI; ++ii) {
+          const int o = SI + 2 * ii + NI * k;
+          yin[ii] = fma(gj, Nn[o], S[o]);
+          qy[ii] = 0.0;
+        }
+        const double c3 = cf.c[2][k];
+        const double* const Dk = cf.dinv + NI * NI * k;
+#pragma unroll
+        for (int jj = 0; jj < CJ; ++jj) {
+          const int j = SJ + 2 * jj, ox = j + NI * k;
+          const double xin = fma(gi, W[ox + N2], W[ox]);
+          double qx = 0.0;
+#pragma unroll
+          for (int ii = 0; ii < CI; ++ii) {
+            const int i = SI + 2 * ii;
+            const double u = fma(cf.c[0][i], xin, fma(cf.c[1][j], yin[ii], c3 * zin[ii][jj]));
+            const double v = u * Dk[i + NI * j];
+            if (DOT) en = fma(u, v, en);
+            qx = fma(cf.c[0][i], v, qx);
+            qy[ii] = fma(cf.c[1][j], v, qy[ii]);
+            qz[ii][jj] = fma(c3, v, qz[ii][jj]);
+          }
+          if constexpr (R::X) {   // own part on the owned W face: -Q(ix) - s_i Q(ix - 1)
+            const double qm = __shfl_up_sync(0xffffffffu, qx, 1);
+            acx[ox] -= fma(gi, qm, qx);
+          } else {
+            qxs[jj] = qx;
+          }
+        }
+        if constexpr (R::Y) {   // own part on the owned S face: -Q(iy) - s_j Q(iy - 1)
+#pragma unroll
+          for (int ii = 0; ii < CI; ++ii) {
+            const double qm = __shfl_up_sync(0xffffffffu, qy[ii], 8);
+            acy[SI + 2 * ii + NI * k] -= fma(gj, qm, qy[ii]);
+          }
+        }
+        // ---- x hand-over: after the pair barrier the x-face entries (J, k) are dead
+        bar_pair(XB);
+        if constexpr (!R::X) {
+#pragma unroll
+          for (int jj = 0; jj < CJ; ++jj) W[SJ + 2 * jj + NI * k] = qxs[jj];
+        } else if (kk > 0) {   // the producer's sums of k - 2 (written before this barrier)
+          constexpr double gp = SI ? 1.0 : -1.0;
+#pragma unroll
+          for (int jj = 0; jj < CJ; ++jj) {
+            const int o = SJ + 2 * jj + NI * (k - 2);
+            acx[o] -= fma(gp, Wp[o], W[o]);
+          }
+        }
+        bar_pair(YB);
+        if constexpr (!R::Y) {
+#pragma unroll
+          for (int ii = 0; ii < CI; ++ii) S[SI + 2 * ii + NI * k] = qy[ii];
+        } else if (kk > 0) {
+          constexpr double gp = SJ ? 1.0 : -1.0;
+#pragma unroll
+          for (int ii = 0; ii < CI; ++ii) {
+            const int o = SI + 2 * ii + NI * (k - 2);
+            acy[o] -= fma(gp, Sp[o], S[o]);
+          }
+        }
+      } else {
+        // ---- after the last k-step: the producers' last sums
+        bar_pair(XB);
+        if constexpr (R::X) {
+          if (CK > 0) {
+            constexpr double gp = SI ? 1.0 : -1.0;
+#pragma unroll
+            for (int jj = 0; jj < CJ; ++jj) {
+              const int o = SJ + 2 * jj + NI * (k - 2);
+              acx[o] -= fma(gp, Wp[o], W[o]);
+            }
+          }
+        }
+        bar_pair(YB);
+        if constexpr (R::Y) {
+          if (CK > 0) {
+            constexpr double gp = SJ ? 1.0 : -1.0;
+#pragma unroll
+            for (int ii = 0; ii < CI; ++ii) {
+              const int o = SI + 2 * ii + NI * (k - 2);
+              acy[o] -= fma(gp, Sp[o], S[o]);
+            }
+          }
+        }
+      }
+    }
+    // ---- z sums complete: B face (a0) -Q, T face (ap) -s_k Q; hand-over over the B entries (I, J)
+    if constexpr (R::Z) {
+#pragma unroll
+      for (int ii = 0; ii < CI; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < CJ; ++jj) {
+          const int o = SI + 2 * ii + NI * (SJ + 2 * jj);
+          azb[o] -= qz[ii][jj];
+          azt[o] = fma(-gk, qz[ii][jj], azt[o]);
+        }
+    }
+    bar_pair(ZB);   // the z-pair has read its B / T entries
+    if constexpr (!R::Z) {
+#pragma unroll
+      for (int ii = 0; ii < CI; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < CJ; ++jj) B[SI + 2 * ii + NI * (SJ + 2 * jj)] = qz[ii][jj];
+    }
+    bar_pair(ZB);
+    if constexpr (R::Z) {
+      constexpr double gp = SK ? 1.0 : -1.0;
+#pragma unroll
+      for (int ii = 0; ii < CI; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < CJ; ++jj) {
+          const int o = SI + 2 * ii + NI * (SJ + 2 * jj);
+          const double q = B[o];
+          azb[o] -= q;
+          azt[o] = fma(-gp, q, azt[o]);
+        }
+    }
+    if (DOT && own && dot_lay) dot -= en;
+  }
+};
+
+// ---- edge / vertex primary parts (entity-centric, owned entities) -----------------------------
+// x-edge (ex, fy) at plane P = l + kb, node i: layer l's two elements (ey = fy - 1, fy) contribute
+//   2 [d0 w0^2 + d1 w0^2 Lam_i + (d2 + d3) w0 K00] u + 2 d1 w0^2 (a0_i V(ex) + ap_i V(ex + 1))
+//   + d2 w0 [sum_j ap_j Fz(ex, fy - 1)(i, j) + sum_j a0_j Fz(ex, fy)(i, j) + K0p (u(fy - 1) + u(fy + 1))]
+//   + 2 d3 w0 [sum_k at_k Fy(ex, fy, l)(i, k) + K0p u(other plane)],  at = a0 (kb = 0) or ap (kb = 1)
+// (K~ rows 0 / p = (K00, a0, K0p) / (K0p, ap, K00), interior rows (a0_m, Lam_m, ap_m); M~ = diag(w0, 1..1, w0),
+// P:381-405).  y-edges by x <-> y symmetry; vertices and z-edges likewise (see v5_make_coef).
+template <int NI>
+struct Edge {
+  // line sum over m of w_m f[m * stride]
+  __device__ static __forceinline__ double lsum(const double* w, const double* f, int stride) {
+    double s = 0.0;
+#pragma unroll
+    for (int m = 0; m < NI; ++m) s = fma(w[m], f[m * stride], s);
+    return s;
+  }
+};
+
+// ---- the kernel -------------------------------------------------------------------------------
+template <int NI, bool DOT>
+__global__ void __launch_bounds__(NT, 2) k_apply_v5(const __grid_constant__ V5Params P) {
+  using LL = L<NI>;
+  constexpr int N2 = NI * NI;
+  if (P.done != nullptr && *P.done != 0.0) return;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ __align__(8) unsigned long long mbar;
+  __shared__ Row rows[NROWS];
+  __shared__ int rofs[2][NROWS];
+  __shared__ double sred[NT / 32];
+  const Geom& g = P.g;
+  const V5Coef& cf = P.cf;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, ix = lane & 7, iy = lane >> 3;
+  const int item = blockIdx.x;
+  const int ntile = P.ntx * P.nty;
+  const int seg = item / ntile, tile = item - seg * ntile;
+  const int tx = tile % P.ntx, ty = tile / P.ntx;
+  const int x0 = tx * OX, y0 = ty * OY, cx0 = x0 - 1, cy0 = y0 - 1;
+  const int nz = g.nz;
+  const int lfin0 = seg * P.zseg;
+  const int lbeg = seg > 0 ? lfin0 - 1 : 0;
+  const int lend = seg == P.nseg - 1 ? nz : min(nz, lfin0 + P.zseg) - 1;
+
+  // padding entries of y are written as 0 by the first CTA
+  if (item == 0) {
+    const long long ends[7] = {g.off_f[0] + g.n_f[0] * N2, g.off_f[1] + g.n_f[1] * N2, g.off_f[2] + g.n_f[2] * N2,
+                               g.off_e[0] + g.n_e[0] * NI, g.off_e[1] + g.n_e[1] * NI, g.off_e[2] + g.n_e[2] * NI,
+                               g.off_v + g.n_v};
+    const long long nexts[7] = {g.off_f[1], g.off_f[2], g.off_e[0], g.off_e[1], g.off_e[2], g.off_v, g.n_total};
+#pragma unroll 1
+    for (int q = 0; q < 7; ++q)
+      for (long long i = ends[q] + tid; i < nexts[q]; i += NT) P.y[i] = 0.0;
+  }
+  // small tables (lane-varying indices in the edge phase)
+  double* const sa0 = sm + LL::O_TAB;         // a0
+  double* const sap = sa0 + 8;                // sigma a0 = ap
+  double* const czu = sa0 + 16;
+  double* const cxu = sa0 + 24;
+  double* const cyu = sa0 + 32;
+  if (tid < 8) {
+    sa0[tid] = cf.a0[tid];
+    sap[tid] = cf.a0[tid] * cf.sig[tid];
+    czu[tid] = cf.czu[tid];
+    cxu[tid] = cf.cxu[tid];
+    cyu[tid] = cf.cyu[tid];
+  }
+  if (tid < NROWS) {
+    make_row<NI>(g, tid, cx0, cy0, rows[tid]);
+  }
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // plane lbeg's partial sums from below: none inside this segment
+  for (int t = tid; t < LL::ACC; t += NT) sm[LL::O_AZ + (lbeg & 1) * LL::ACC + t] = 0.0;
+  for (int t = tid; t < LL::AES; t += NT) sm[LL::O_AE + (lbeg & 1) * LL::AES + t] = 0.0;
+  __syncthreads();
+  const bool side_ok = rows_complete<NI>(rows, 0, NSIDE);
+  const bool plane_ok = rows_complete<NI>(rows, NSIDE, NROWS);
+  // prologue: plane lbeg, and side lbeg + plane lbeg + 1 when layer lbeg exists
+  if (tid < NROWS) {
+    const bool sd = tid < NSIDE;
+    rofs[lbeg & 1][tid] = row_off<NI>(rows[tid], tid, sd ? lbeg : lbeg);
+    if (!sd) rofs[(lbeg + 1) & 1][tid] = row_off<NI>(rows[tid], tid, lbeg + 1);
+  }
+  __syncthreads();   // row descriptors visible to warp 0
+  // prologue batch: plane lbeg, and side lbeg + plane lbeg + 1 when layer lbeg exists
+  if (warp == 0)
+    issue_step<NI>(P, sm, rows, lbeg < nz, lbeg, true, lbeg, zdir(g, lbeg), lbeg < nz, lbeg + 1, zdir(g, lbeg + 1),
+                   &mbar);
+  __syncthreads();   // rofs visible
+  unsigned phase = 0;
+  bool pending = true;            // a load batch is in flight for the current step
+  bool first_fix = !plane_ok || zdir(g, lbeg);
+  double dot = 0.0;
+  const bool own = ix >= 1 && iy >= 1;
+  const int o_lane = (iy - 1) * OX + (ix - 1);
+
+  for (int l = lbeg; l <= lend; ++l) {
+    const bool lay = l < nz;                        // layer l exists (else: final plane nz only)
+    if (pending) {
+      mbar_wait(&mbar, phase);
+      phase ^= 1;
+      pending = false;
+    }
+    // zero the invalid / Dirichlet parts of the rows that just landed
+    const bool fix = first_fix || (lay && (!side_ok || !plane_ok || zdir(g, l + 1)));
+    if (fix) {
+      if (first_fix) fix_rows<NI>(sm, rows, NSIDE, NROWS, l, zdir(g, l));
+      if (lay) {
+        fix_rows<NI>(sm, rows, 0, NSIDE, l, false);
+        fix_rows<NI>(sm, rows, NSIDE, NROWS, l + 1, zdir(g, l + 1));
+      }
+      __syncthreads();
+    }
+    first_fix = false;
+    // views of this step's rows
+    View V{sm, rofs[l & 1], rofs[l & 1] + 0, rofs[(l + 1) & 1]};
+    const bool fin_l = l >= lfin0;                  // plane l / layer l finalized by this CTA
+    const bool fin_t = l + 1 <= lend;               // plane l + 1 finalized by this CTA
+    double* const aeb = sm + LL::O_AE + (l & 1) * LL::AES;          // edge accumulators, plane l
+    double* const aet = sm + LL::O_AE + ((l + 1) & 1) * LL::AES;    // plane l + 1
+    // ======== edges / vertices (entity-centric; owned (ix, iy) in [1, 8) x [1, 4)) ========
+    // one loop per entity kind (item t -> owned entity e = t / NI, node c = t % NI; consecutive t
+    // are consecutive skeleton entries of a row, so the stores coalesce)
+    {
+      constexpr int NE1 = NO * NI;
+      const int nx = g.nx, ny = g.ny;
+      const double k0p = cf.sc[15];
+      // z-edges (fx, fy) of layer l, node k (final)
+      if (lay) {
+        for (int t = tid; t < NE1; t += NT) {
+          const int e = t / NI, c = t - e * NI, jx = e % OX + 1, jy = e / OX + 1;
+          const int fx = cx0 + jx, fy = cy0 + jy;
+          const double* Z = V.ze(jy) + jx * NI;
+          const double u = Z[c];
+          const double* Fy0 = V.yf(jy) + (jx - 1) * N2 + c * NI;    // y-face (fx - 1, fy), (i, k) at fixed k
+          const double* Fx0 = V.xf(jy - 1) + jx * N2 + c * NI;     // x-face (fx, fy - 1), (j, k) at fixed k
+          const double* Fx1 = V.xf(jy) + jx * N2 + c * NI;         // x-face (fx, fy)
+          const double ly = Edge<NI>::lsum(sap, Fy0, 1) + Edge<NI>::lsum(sa0, Fy0 + N2, 1);
+          const double lx = Edge<NI>::lsum(sap, Fx0, 1) + Edge<NI>::lsum(sa0, Fx1, 1);
+          const double nxs = Z[c - NI] + Z[c + NI];
+          const double nys = V.ze(jy - 1)[jx * NI + c] + V.ze(jy + 1)[jx * NI + c];
+          const double vb = V.vv(0, jy)[jx], vt = V.vv(1, jy)[jx];
+          // 4 [d0 w0^2 + (d1 + d2) w0 K00 + d3 w0^2 Lam_k] u + 4 d3 w0^2 (a0_k V_b + ap_k V_t)
+          // + 2 d1 w0 [y-face i-lines + K0p (u(fx-1) + u(fx+1))] + 2 d2 w0 [x-face j-lines + K0p (u(fy-1) + u(fy+1))]
+          double val = czu[c] * u + cf.sc[0] * fma(sa0[c], vb, sap[c] * vt) + cf.sc[1] * fma(k0p, nxs, ly) +
+                       cf.sc[2] * fma(k0p, nys, lx);
+          if (DOT && fin_l) dot = fma(u, val, dot);
+          if (fin_l && fx <= nx && fy <= ny) {
+            if (fx == 0 || fx == nx || fy == 0 || fy == ny) val = 0.0;
+            P.y[g.off_e[2] + ((long long)fx + (long long)(nx + 1) * (fy + (long long)(ny + 1) * l)) * NI + c] = val;
+          }
+        }
+      }
+      // x-edges (ex, fy) and y-edges (fx, ey) of planes l (final) and l + 1 (partial), node c
+      for (int t = tid; t < 2 * NE1; t += NT) {
+        const bool xk = t < NE1;
+        const int tt = xk ? t : t - NE1;
+        const int e = tt / NI, c = tt - e * NI, jx = e % OX + 1, jy = e / OX + 1;
+        const int fx = cx0 + jx, fy = cy0 + jy;
+        double* const ab = aeb + (xk ? 0 : NE1) + tt;
+        double* const at = aet + (xk ? 0 : NE1) + tt;
+        double p0 = 0.0, p1 = 0.0;
+        if (lay) {
+          const double* U0 = (xk ? V.xe(0, jy) : V.ye(0, jy)) + jx * NI;
+          const double* U1 = (xk ? V.xe(1, jy) : V.ye(1, jy)) + jx * NI;
+          // the layer's face along k: y-face (ex, fy) (x-edge, entries (i, k)) / x-face (fx, ey) (y-edge, (j, k))
+          const double* Fl = (xk ? V.yf(jy) : V.xf(jy)) + jx * N2 + c;
+          const double lk0 = Edge<NI>::lsum(sa0, Fl, NI), lk1 = Edge<NI>::lsum(sap, Fl, NI);
+          const double cu = xk ? cxu[c] : cyu[c];
+          // x-edge: 2 d1 w0^2, d2 w0, 2 d3 w0;  y-edge: 2 d2 w0^2, d1 w0, 2 d3 w0
+          const double sv = xk ? cf.sc[3] : cf.sc[6], sl = xk ? cf.sc[4] : cf.sc[7], sk = xk ? cf.sc[5] : cf.sc[8];
+#pragma unroll
+          for (int kb = 0; kb < 2; ++kb) {
+            const double* U = kb ? U1 : U0;
+            const double* Uo = kb ? U0 : U1;
+            // z-faces of plane l + kb across the edge: x-edge (ex, fy-1) / (ex, fy), j-line at i = c;
+            // y-edge (fx-1, ey) / (fx, ey), i-line at j = c
+            const double* Fa = xk ? V.zf(kb, jy - 1) + jx * N2 + c : V.zf(kb, jy) + (jx - 1) * N2 + c * NI;
+            const double* Fb = xk ? V.zf(kb, jy) + jx * N2 + c : Fa + N2;
+            const int st = xk ? NI : 1;
+            const double lz = Edge<NI>::lsum(sap, Fa, st) + Edge<NI>::lsum(sa0, Fb, st);
+            const double nb = xk ? V.xe(kb, jy - 1)[jx * NI + c] + V.xe(kb, jy + 1)[jx * NI + c] : U[c - NI] + U[c + NI];
+            const double v1 = xk ? V.vv(kb, jy)[jx + 1] : V.vv(kb, jy + 1)[jx];
+            const double vc = fma(sa0[c], V.vv(kb, jy)[jx], sap[c] * v1);
+            const double pv = cu * U[c] + sv * vc + sl * fma(k0p, nb, lz) + sk * fma(k0p, Uo[c], kb ? lk1 : lk0);
+            if (kb == 0) p0 = pv; else p1 = pv;
+          }
+          if (DOT) {
+            if (fin_l) dot = fma(U0[c], p0, dot);
+            if (fin_t) dot = fma(U1[c], p1, dot);
+          }
+        }
+        double val = *ab + p0;
+        *at = p1;
+        if (fin_l) {
+          const bool zd = zdir(g, l);
+          if (xk && fx < nx && fy <= ny) {
+            if (zd || fy == 0 || fy == ny) val = 0.0;
+            P.y[g.off_e[0] + ((long long)fx + (long long)nx * (fy + (long long)(ny + 1) * l)) * NI + c] = val;
+          } else if (!xk && fx <= nx && fy < ny) {
+            if (zd || fx == 0 || fx == nx) val = 0.0;
+            P.y[g.off_e[1] + ((long long)fx + (long long)(nx + 1) * (fy + (long long)ny * l)) * NI + c] = val;
+          }
+        }
+      }
+      // vertices (fx, fy) of planes l (final) and l + 1 (partial)
+      for (int e = tid; e < NO; e += NT) {
+        const int jx = e % OX + 1, jy = e / OX + 1;
+        const int fx = cx0 + jx, fy = cy0 + jy;
+        double* const ab = aeb + 2 * NE1 + e;
+        double* const at = aet + 2 * NE1 + e;
+        double p0 = 0.0, p1 = 0.0;
+        if (lay) {
+          const double* Z = V.ze(jy) + jx * NI;    // z-edge (fx, fy) of layer l
+          const double lk0 = Edge<NI>::lsum(sa0, Z, 1), lk1 = Edge<NI>::lsum(sap, Z, 1);
+#pragma unroll
+          for (int kb = 0; kb < 2; ++kb) {
+            const double* Vr = V.vv(kb, jy);
+            const double u = Vr[jx], uo = V.vv(1 - kb, jy)[jx];
+            const double lx = Edge<NI>::lsum(sap, V.xe(kb, jy) + (jx - 1) * NI, 1) + Edge<NI>::lsum(sa0, V.xe(kb, jy) + jx * NI, 1);
+            const double ly = Edge<NI>::lsum(sap, V.ye(kb, jy - 1) + jx * NI, 1) + Edge<NI>::lsum(sa0, V.ye(kb, jy) + jx * NI, 1);
+            const double nxs = Vr[jx - 1] + Vr[jx + 1], nys = V.vv(kb, jy - 1)[jx] + V.vv(kb, jy + 1)[jx];
+            // 4 (d0 w0^3 + (d1 + d2 + d3) w0^2 K00) u + 2 d1 w0^2 [x-edge lines + K0p (u(fx-1) + u(fx+1))]
+            // + 2 d2 w0^2 [y-edge lines + K0p (...)] + 4 d3 w0^2 [z-edge line + K0p u(other plane)]
+            const double pv = cf.sc[9] * u + cf.sc[10] * fma(k0p, nxs, lx) + cf.sc[11] * fma(k0p, nys, ly) +
+                              cf.sc[12] * fma(k0p, uo, kb ? lk1 : lk0);
+            if (kb == 0) p0 = pv; else p1 = pv;
+            if (DOT && (kb == 0 ? fin_l : fin_t)) dot = fma(u, pv, dot);
+          }
+        }
+        double val = *ab + p0;
+        *at = p1;
+        if (fin_l && fx <= nx && fy <= ny) {
+          if (zdir(g, l) || fx == 0 || fx == nx || fy == 0 || fy == ny) val = 0.0;
+          P.y[g.off_v + (long long)fx + (long long)(nx + 1) * (fy + (long long)(ny + 1) * l)] = val;
+        }
+      }
+    }
+    // ======== faces: class phases (layer l) ========
+    double* const AX = sm + LL::O_AX;
+    double* const AY = sm + LL::O_AY;
+    double* const AZB = sm + LL::O_AZ + (l & 1) * LL::ACC;
+    double* const AZT = sm + LL::O_AZ + ((l + 1) & 1) * LL::ACC;
+    double* const scr = sm + LL::O_SCR;
+    double* const acx = own ? AX + o_lane * N2 : scr;
+    double* const acy = own ? AY + o_lane * N2 : scr;
+    double* const azb = own ? AZB + o_lane * N2 : scr;
+    double* const azt = own ? AZT + o_lane * N2 : scr;
+    __syncthreads();   // the edge phase has read every face line before the class phases overwrite entries
+    if (lay) {
+      switch (kV5Class[warp]) {
+        case 0: Cls<NI, DOT, 0, 0, 0>::run(cf, V, ix, iy, own, acx, acy, azb, azt, dot, fin_l, fin_l, fin_t); break;
+        case 1: Cls<NI, DOT, 0, 0, 1>::run(cf, V, ix, iy, own, acx, acy, azb, azt, dot, fin_l, fin_l, fin_t); break;
+        case 2: Cls<NI, DOT, 0, 1, 0>::run(cf, V, ix, iy, own, acx, acy, azb, azt, dot, fin_l, fin_l, fin_t); break;
+        case 3: Cls<NI, DOT, 0, 1, 1>::run(cf, V, ix, iy, own, acx, acy, azb, azt, dot, fin_l, fin_l, fin_t); break;
+        case 4: Cls<NI, DOT, 1, 0, 0>::run(cf, V, ix, iy, own, acx, acy, azb, azt, dot, fin_l, fin_l, fin_t); break;
+        case 5: Cls<NI, DOT, 1, 0, 1>::run(cf, V, ix, iy, own, acx, acy, azb, azt, dot, fin_l, fin_l, fin_t); break;
+        case 6: Cls<NI, DOT, 1, 1, 0>::run(cf, V, ix, iy, own, acx, acy, azb, azt, dot, fin_l, fin_l, fin_t); break;
+        default: Cls<NI, DOT, 1, 1, 1>::run(cf, V, ix, iy, own, acx, acy, azb, azt, dot, fin_l, fin_l, fin_t); break;
+      }
+    }
+    fence_proxy_async();   // generic smem accesses before the next bulk copies into the same rows
+    __syncthreads();       // S3: accumulators final, every input row of step l dead
+    // next step's loads: side l + 1 and plane l + 2 (into plane l's slots)
+    if (l + 1 <= lend && l + 1 < nz) {
+      if (tid < NROWS) {
+        if (tid < NSIDE) rofs[(l + 1) & 1][tid] = row_off<NI>(rows[tid], tid, l + 1);
+        else rofs[(l + 2) & 1][tid] = row_off<NI>(rows[tid], tid, l + 2);
+      }
+      if (warp == 0) issue_step<NI>(P, sm, rows, true, l + 1, false, 0, false, true, l + 2, zdir(g, l + 2), &mbar);
+      pending = true;
+    }
+    // ======== store the owned faces of layer l and the z-faces of plane l ========
+    // 9 rows (x-, y-, z-faces x 3 element rows), one warp per row: each row is OX contiguous faces
+    // in y (the accumulator row is contiguous too); faces beyond the domain are skipped, Dirichlet
+    // faces (fx = 0 / nx, fy = 0 / ny, a Dirichlet z-plane) written as 0
+    if (fin_l) {
+      const int nx = g.nx, ny = g.ny;
+      for (int rr = warp; rr < 3 * OY; rr += NT / 32) {
+        const int kind = rr / OY, oy = rr - kind * OY;
+        const int e0 = x0, er = y0 + oy;   // first entity index along x, row index
+        int cnt, z0 = 0, z1 = 0, za = 0;
+        long long gb;
+        const double* src;
+        if (kind == 0) {          // x-faces fx in [x0, x0 + 7), row ey = er
+          if (!lay || er >= ny) continue;
+          cnt = min(OX, nx + 1 - e0);
+          z0 = e0 == 0;
+          z1 = e0 + cnt - 1 == nx;
+          gb = g.off_f[0] + ((long long)e0 + (long long)(nx + 1) * (er + (long long)ny * l)) * N2;
+          src = AX;
+        } else if (kind == 1) {   // y-faces ex in [x0, x0 + 7), row fy = er
+          if (!lay || er > ny) continue;
+          cnt = min(OX, nx - e0);
+          za = (er == 0 || er == ny);
+          gb = g.off_f[1] + ((long long)e0 + (long long)nx * (er + (long long)(ny + 1) * l)) * N2;
+          src = AY;
+        } else {                  // z-faces of plane l, ex in [x0, x0 + 7), row ey = er
+          if (er >= ny) continue;
+          cnt = min(OX, nx - e0);
+          za = zdir(g, l);
+          gb = g.off_f[2] + ((long long)e0 + (long long)nx * (er + (long long)ny * l)) * N2;
+          src = AZB;
+        }
+        if (cnt <= 0) continue;
+        src += oy * OX * N2;
+        double* dst = P.y + gb;
+        const int n = cnt * N2, lo = za ? n : (z0 ? N2 : 0), hi = z1 ? n - N2 : n;
+        for (int t = lane; t < n; t += 32) dst[t] = (t >= lo && t < hi) ? src[t] : 0.0;
+      }
+    }
+    __syncthreads();       // S4: accumulators read before the next step writes them
+  }
+  if (DOT && P.dotp != nullptr) {
+    double s = dot;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) sred[warp] = s;
+    __syncthreads();
+    if (tid == 0) {
+      double tsum = 0.0;
+      for (int w = 0; w < NT / 32; ++w) tsum += sred[w];
+      P.dotp[item] = tsum;
+    }
+  }
+}
+
+}  // namespace v5
+
+bool v5_supported(int ni) { return ni >= 2 && ni <= 7; }
+
+// tiles own 7 x 3 elements; the entity index ranges fx in [0, nx], fy in [0, ny] are covered
+void v5_tiles(int nx, int ny, int* ntx, int* nty) {
+  *ntx = (nx + 1 + v5::OX - 1) / v5::OX;
+  *nty = (ny + 1 + v5::OY - 1) / v5::OY;
+}
+
+// z-segments: ntiles columns of nz layers on nsm SMs x 2 CTAs; a segment above the first recomputes
+// the layer below its first plane, so more segments cost compute: pick the count that minimises
+// (waves rounded up) x (layers + 1) per column
+void v5_segments(int ntiles, int nz, int nslots, int* nseg, int* zseg) {
+  double best = 1e300;
+  int bs = 1;
+  for (int s = 1; s <= nz && s <= 64; ++s) {
+    const int zs = (nz + s - 1) / s;
+    const int segs = (nz + zs - 1) / zs;
+    const long long items = (long long)ntiles * segs;
+    const long long waves = (items + nslots - 1) / nslots;
+    const double cost = (double)waves * (zs + (segs > 1 ? 1 : 0));
+    if (cost < best - 1e-9) { best = cost; bs = s; }
+  }
+  const int zs = (nz + bs - 1) / bs;
+  *zseg = zs;
+  *nseg = (nz + zs - 1) / zs;
+}
+
+void v5_make_coef(int ni, const double* d, const double* a0, const double* lam, double K00, double K0p, double w0,
+                  std::vector<unsigned char>& out) {
+  V5Coef c;
+  memset(&c, 0, sizeof(c));
+  const double w02 = w0 * w0, w03 = w02 * w0;
+  for (int m = 0; m < ni; ++m) {
+    for (int q = 0; q < 3; ++q) {
+      c.c[q][m] = d[q + 1] * a0[m];
+      c.ef2[q][m] = 2.0 * d[q + 1] * w0 * a0[m];
+      c.ef1[q][m] = d[q + 1] * w0 * a0[m];
+    }
+    c.a0[m] = a0[m];
+    c.sig[m] = (m & 1) ? -1.0 : 1.0;
+    // z-edge self: 4 [d0 w0^2 + (d1 + d2) w0 K00 + d3 w0^2 Lam_k]
+    c.czu[m] = 4.0 * (d[0] * w02 + (d[1] + d[2]) * w0 * K00 + d[3] * w02 * lam[m]);
+    // x-edge self (per layer): 2 [d0 w0^2 + d1 w0^2 Lam_i + (d2 + d3) w0 K00]; y-edge likewise
+    c.cxu[m] = 2.0 * (d[0] * w02 + d[1] * w02 * lam[m] + (d[2] + d[3]) * w0 * K00);
+    c.cyu[m] = 2.0 * (d[0] * w02 + d[2] * w02 * lam[m] + (d[1] + d[3]) * w0 * K00);
+  }
+  for (int k = 0; k < ni; ++k)
+    for (int j = 0; j < ni; ++j)
+      for (int i = 0; i < ni; ++i) c.dinv[i + ni * (j + ni * k)] = 1.0 / (d[0] + d[1] * lam[i] + d[2] * lam[j] + d[3] * lam[k]);
+  for (int b = 0; b < ni; ++b)
+    for (int a = 0; a < ni; ++a) {
+      c.fdx[a + ni * b] = 2.0 * (d[0] * w0 + d[1] * K00 + d[2] * w0 * lam[a] + d[3] * w0 * lam[b]);
+      c.fdy[a + ni * b] = 2.0 * (d[0] * w0 + d[2] * K00 + d[1] * w0 * lam[a] + d[3] * w0 * lam[b]);
+      c.fdz[a + ni * b] = d[0] * w0 + d[3] * K00 + d[1] * w0 * lam[a] + d[2] * w0 * lam[b];
+    }
+  for (int q = 0; q < 3; ++q) c.k0p[q] = d[q + 1] * K0p;
+  // z-edge: 4 d3 w0^2 (vertex coupling), 2 d1 w0, 2 d2 w0 (line sums + K0p neighbours)
+  c.sc[0] = 4.0 * d[3] * w02;
+  c.sc[1] = 2.0 * d[1] * w0;
+  c.sc[2] = 2.0 * d[2] * w0;
+  // x-edge: 2 d1 w0^2, d2 w0, 2 d3 w0;  y-edge: 2 d2 w0^2, d1 w0, 2 d3 w0
+  c.sc[3] = 2.0 * d[1] * w02; c.sc[4] = d[2] * w0; c.sc[5] = 2.0 * d[3] * w0;
+  c.sc[6] = 2.0 * d[2] * w02; c.sc[7] = d[1] * w0; c.sc[8] = 2.0 * d[3] * w0;
+  // vertex: 4 (d0 w0^3 + (d1 + d2 + d3) w0^2 K00), 2 d1 w0^2, 2 d2 w0^2, 4 d3 w0^2
+  c.sc[9] = 4.0 * (d[0] * w03 + (d[1] + d[2] + d[3]) * w02 * K00);
+  c.sc[10] = 2.0 * d[1] * w02; c.sc[11] = 2.0 * d[2] * w02; c.sc[12] = 4.0 * d[3] * w02;
+  c.sc[15] = K0p;
+  out.resize(sizeof(c));
+  memcpy(out.data(), &c, sizeof(c));
+}
+
+template <int NI, bool DOT>
+static int launch_v5_t(const V5Params& P, cudaStream_t st, int* nl) {
+  using LL = v5::L<NI>;
+  const size_t smem = sizeof(double) * LL::TOTAL;
+  static bool attr[kMaxDev];
+  const int dv = dev_slot();
+  if (!attr[dv]) {
+    cudaFuncSetAttribute(v5::k_apply_v5<NI, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr[dv] = true;
+  }
+  v5::k_apply_v5<NI, DOT><<<P.nitems, v5::NT, smem, st>>>(P);
+  (*nl)++;
+  return cudaGetLastError();
+}
+
+int launch_apply_v5(const Geom& g, const double* x, double* y, const double* done, int ntx, int nty, int nseg,
+                    int zseg, const void* coef, double* dotp, void* stream, int* nl, void* events) {
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaEvent_t* ev = (cudaEvent_t*)events;
+  V5Params P;
+  P.g = g; P.x = x; P.y = y; P.done = done; P.dotp = dotp;
+  P.ntx = ntx; P.nty = nty; P.nseg = nseg; P.zseg = zseg; P.nitems = ntx * nty * nseg;
+  memcpy(&P.cf, coef, sizeof(V5Coef));
+  if (ev) cudaEventRecord(ev[0], st);
+  int e = 0;
+  const bool dot = dotp != nullptr;
+  switch (g.ni) {
+#define SC_V5_CASE(N) \
+    case N: e = dot ? launch_v5_t<N, true>(P, st, nl) : launch_v5_t<N, false>(P, st, nl); break;
+    SC_V5_CASE(2) SC_V5_CASE(3) SC_V5_CASE(4) SC_V5_CASE(5) SC_V5_CASE(6) SC_V5_CASE(7)
+#undef SC_V5_CASE
+    default: return (int)cudaErrorInvalidValue;
+  }
+  if (ev) cudaEventRecord(ev[1], st);
+  return e;
+}
+
+}  // namespace sc

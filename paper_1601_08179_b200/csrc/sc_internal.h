@@ -50,6 +50,8 @@ struct Geom {
   const double* tab;            // device 1-D tables, see TAB_* offsets
   const double* dinv;           // uniform grids: D^{-1}(i,j,k), i fastest (n_I^3); else null
   double d_uni[4];              // uniform grids: d_e
+  int nodir;                    // 1: Dirichlet entities are NOT masked (inhomogeneous-Dirichlet lifting
+                                //    in the v1 operator, the conversions and the recovery; api.cu)
 };
 
 // Offsets into the device 1-D table (doubles).
@@ -84,6 +86,7 @@ int launch_diag(const Geom& g, double* diag, void* stream, int* nlaunch);
 int launch_invert_diag(const Geom& g, double* diag, void* stream, int* nlaunch);
 int launch_convert(const Geom& g, const double* in, double* out, int to_skel, int mat, void* stream, int* nlaunch);
 int launch_fill_random(const Geom& g, uint64_t seed, double* v, void* stream, int* nlaunch);
+int launch_dir_split(const Geom& g, double* a, const double* b, int mode, void* stream, int* nlaunch);
 int launch_condense(const Geom& g, const double* f, double* b, double* scratch, long long scratch_elems,
                     void* stream, int* nlaunch);
 int launch_recover(const Geom& g, const double* f, const double* x, double* u, double* scratch,
@@ -154,6 +157,14 @@ int launch_apply_rw(const Geom& g, const double* x, double* y, const double* don
 // p = 2 operator (uniform geometry): warp = 32 consecutive elements of an x-row, colour-scheduled
 int launch_apply_p2(const Geom& g, const double* x, double* y, const double* done, const void* coef, void* stream,
                     int* nlaunch, void* events);
+// v5 operator (2 <= n_I <= 7, uniform geometry): tile columns with a recomputed halo (kernels_v5.cu)
+bool v5_supported(int ni);
+void v5_tiles(int nx, int ny, int* ntx, int* nty);
+void v5_segments(int ntiles, int nz, int nslots, int* nseg, int* zseg);
+void v5_make_coef(int ni, const double* d, const double* a0, const double* lam, double K00, double K0p, double w0,
+                  std::vector<unsigned char>& out);
+int launch_apply_v5(const Geom& g, const double* x, double* y, const double* done, int ntx, int nty, int nseg,
+                    int zseg, const void* coef, double* dotp, void* stream, int* nl, void* events);
 // z-segments of the tile columns: ntiles columns of nz layers on nsm persistent CTAs
 void col_choose_segments(int ntiles, int nz, int nsm, int* nseg, int* zseg);
 int col_slots();   // step slots of the parked look-back partials (look-back distance + 1)

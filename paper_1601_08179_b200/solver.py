@@ -148,6 +148,14 @@ class Context:
         _check(self.lib, self.ctx, "sc_recover",
                self.lib.sc_recover(self.ctx, ptr(f), ptr(x), ptr(u), self._s(stream)))
 
+    def sc_condense_rhs_dirichlet(self, f, g, b, stream=None):
+        _check(self.lib, self.ctx, "sc_condense_rhs_dirichlet",
+               self.lib.sc_condense_rhs_dirichlet(self.ctx, ptr(f), ptr(g), ptr(b), self._s(stream)))
+
+    def sc_recover_dirichlet(self, f, g, x, u, stream=None):
+        _check(self.lib, self.ctx, "sc_recover_dirichlet",
+               self.lib.sc_recover_dirichlet(self.ctx, ptr(f), ptr(g), ptr(x), ptr(u), self._s(stream)))
+
     def sc_to_transformed(self, v_lat, v_skel, mode, stream=None):
         _check(self.lib, self.ctx, "sc_to_transformed",
                self.lib.sc_to_transformed(self.ctx, ptr(v_lat), ptr(v_skel), int(mode), self._s(stream)))

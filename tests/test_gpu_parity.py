@@ -664,7 +664,71 @@ def test_pcg_parity_anisotropic(p, n, ar, expect):
 
 @pytest.mark.parametrize("ar,expect", [(128, 52)])
 def test_pcg_parity_anisotropic_16cubed(ar, expect):
-    """Half-size cfg4 (16^3 elements, p = 16, AR = 128): the oracle needs 52 iterations; the
-    full-size GPU run (32^3) needs 53 (DESIGN §7 on SURVEY c15's 47)."""
-    it_gpu, it_oracle = _aniso_pcg_case(16, 16, ar)
-    assert it_oracle == expect
+    """Half-size cfg4 (16^3 elements, p = 16, AR = 128).  Here the +-1 iteration bar does not
+    apply (reading R16): both residual histories agree to 1e-5 for the first 12
+    iterations, then rounding (different summation orders in the operator, the dots and the
+    preconditioner) decides, and from iteration ~40 on both recursive residuals oscillate around
+    the tolerance (2e-10 plateau), so the first crossing of 1e-10 is a matter of rounding (measured:
+    oracle 52, GPU 54).  What is unique is checked instead: the early history, convergence within a
+    few iterations of the oracle, and that the GPU's answer solves the oracle's system to 1e-9."""
+    p, n = 16, 16
+    g = small_grid(p, (n, n, n), 0.0, lengths=(float(ar), 1.0, 1.0))
+    X, Y, Z = mesh.lattice_coordinates(g)
+    f = sine_f(X, Y, Z, 0.0)
+    op = operator.AssembledCondensedOperator(g)
+    b = solve.condensed_rhs(op, f)
+    res = _oracle_pcg(g, op, b, 1e-10)
+    assert res.iters == expect
+    h0 = np.array(res.history) / res.history[0]
+    ctx = ctx_for(g)
+    f_d = torch.from_numpy(f).cuda()
+    bt = ctx.skeleton()
+    ctx.sc_condense_rhs(f_d, bt)
+    for k in (1, 4, 8, 12):
+        xt = ctx.skeleton()
+        rep = ctx.sc_pcg_solve(bt, xt, rtol=0.0, maxit=k)
+        assert abs(rep.relres - h0[k]) <= 1e-5 * h0[k], (k, rep.relres, h0[k])
+    xt = ctx.skeleton()
+    rep = ctx.sc_pcg_solve(bt, xt, rtol=1e-10, maxit=3000)
+    assert rep.converged and abs(rep.iters - res.iters) <= 4, (rep.iters, res.iters)
+    x_gpu = ctx.to_lattice_nodal(xt).cpu().numpy()
+    r = np.where(op.free, b - op.apply(x_gpu), 0.0)
+    norm = solve.transformed_norm(g, op.skel)
+    assert norm(r) <= 1e-9 * norm(b)
+
+
+# ---- the paper's solver workload E3 (P:625-687): graded grids, Eq. eq:solution, Dirichlet data --
+@pytest.mark.parametrize("p,alpha,n", [(4, 2.0, 3), (6, 1.5, 3), (9, 2.0, 2), (12, 1.5, 2)])
+def test_e3_dirichlet_pipeline_parity(p, alpha, n):
+    """sc_condense_rhs_dirichlet -> BT-PCG (rtol 1e-12, the paper's tolerance) ->
+    sc_recover_dirichlet against the oracle's dirichlet_rhs / block-Jacobi PCG / recover with the
+    same data, on graded grids (expansion factor alpha; v1 for p <= 8, v4 above)."""
+    from paper_1601_08179_b200 import SC_DUAL
+    from synth import e3_grid, e3_u, e3_f
+    g = e3_grid(p, alpha, n=n)
+    X, Y, Z = mesh.lattice_coordinates(g)
+    k = 1.0
+    f = e3_f(X, Y, Z, 0.0, k=k)
+    gv = e3_u(X, Y, Z, k=k)
+    op = operator.AssembledCondensedOperator(g)
+    b = solve.dirichlet_rhs(op, f, gv)
+    res = _oracle_pcg(g, op, b, 1e-12)
+    u_ref = solve.recover(op, f, res.x, dirichlet=gv)
+    ctx = ctx_for(g)
+    f_d, g_d = torch.from_numpy(f).cuda(), torch.from_numpy(gv).cuda()
+    bt = ctx.skeleton()
+    ctx.sc_condense_rhs_dirichlet(f_d, g_d, bt)
+    lat = ctx.lattice()
+    ctx.sc_from_transformed(bt, lat, SC_DUAL)
+    assert rel(lat.cpu().numpy(), b) <= 1e-12
+    xt = ctx.skeleton()
+    rep = ctx.sc_pcg_solve(bt, xt, rtol=1e-12, maxit=3000)
+    assert rep.converged and abs(rep.iters - res.iters) <= 1, (rep.iters, res.iters)
+    ref = res.x if rep.iters == res.iters else _oracle_pcg(g, op, b, 0, fixed=rep.iters).x
+    assert rel(ctx.to_lattice_nodal(xt).cpu().numpy(), ref) <= 1e-10
+    u = ctx.lattice()
+    ctx.sc_recover_dirichlet(f_d, g_d, xt, u)
+    u = u.cpu().numpy()
+    assert rel(u, u_ref) <= 1e-10
+    dmask = mesh.dirichlet_mask(g)
+    assert np.abs(u[dmask] - gv[dmask]).max() <= 1e-12 * np.abs(gv).max()
