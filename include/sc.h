@@ -210,6 +210,11 @@ sc_status sc_nccl_unique_id(unsigned char h_id[128]);
 sc_status sc_nccl_comm_init(const unsigned char h_id[128], int nranks, int rank, int device, void** comm_out);
 sc_status sc_nccl_comm_destroy(void* comm);
 
+/* Operator kernel family this ctx runs: "v6" / "v5" (halo-recompute tile columns,
+ * 3 <= p <= 8), "v3" (tile columns with look-back), "rw" / "p2" (row-warp kernels, p <= 4),
+ * "v4" (colour-scheduled element CTAs, p >= 9), "v1" (one CTA per element, any geometry). */
+const char* sc_operator_kernel(const sc_ctx* ctx);
+
 /* Number of kernels launched by this ctx since setup (for the bench's gpu_launches). */
 long long sc_launch_count(const sc_ctx* ctx);
 

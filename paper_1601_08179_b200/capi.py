@@ -61,6 +61,7 @@ SIGNATURES = {
     "sc_condense_rhs": ([_P, _P, _P, _P], ctypes.c_int),
     "sc_recover": ([_P, _P, _P, _P, _P], ctypes.c_int),
     "sc_condense_rhs_dirichlet": ([_P, _P, _P, _P, _P], ctypes.c_int),
+    "sc_operator_kernel": ([_P], ctypes.c_char_p),
     "sc_recover_dirichlet": ([_P, _P, _P, _P, _P, _P], ctypes.c_int),
     "sc_to_transformed": ([_P, _P, _P, ctypes.c_int, _P], ctypes.c_int),
     "sc_from_transformed": ([_P, _P, _P, ctypes.c_int, _P], ctypes.c_int),

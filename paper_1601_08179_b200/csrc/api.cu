@@ -75,6 +75,7 @@ struct sc_ctx {
   bool use_v5 = false;                  // 3 <= p <= 8 halo-recompute tile columns (kernels_v5.cu)
   std::vector<unsigned char> v5_coef;
   int v5_ntx = 0, v5_nty = 0, v5_nseg = 1, v5_zseg = 0;
+  int v5_kern = 5;                      // 5: class-per-warp kernel, 6: uniform class lanes
   bool use_ptab = false;                // PCG reads Pinv from the per-class table (uniform geometry)
   PinvTab ptab;                 // v4 colour-scheduled element operator (n_I >= 8, uniform geometry)
   std::vector<unsigned char> big_coef;
@@ -334,7 +335,7 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
     // with look-back, kernels_col.cu), "rw" (p = 3, 4 row-warp kernels)
     const char* opsel = getenv("SC_OP");
     const std::string op = opsel ? opsel : "";
-    const bool want_v5 = op.empty() || op == "v5";
+    const bool want_v5 = op.empty() || op == "v5" || op == "v6";
     if (v5_supported(ni) && uniform && sig_ok && want_v5 && !(env && env[0] == '1')) {
       v5_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->v5_coef);
       v5_tiles(nx, ny, &ctx->v5_ntx, &ctx->v5_nty);
@@ -354,6 +355,7 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
       const char* fd = getenv("SC_FUSED_DOT");
       ctx->fused_dot = !(fd && fd[0] == '0');
       ctx->use_v5 = true;
+      ctx->v5_kern = op == "v5" ? 5 : 6;
     } else if (ni == 1 && uniform && sig_ok && !(env && env[0] == '1') && !(np2 && np2[0] == '1')) {
       big_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->big_coef);
       ctx->use_p2 = true;
@@ -604,7 +606,7 @@ static sc_status apply_impl(sc_ctx* ctx, const double* x, double* y, const doubl
   cudaEvent_t* ev = rec ? &ctx->prof_ev[2 * ctx->prof_n] : nullptr;
   if (ctx->use_v5)
     LAUNCH(launch_apply_v5(ctx->g, x, y, done, ctx->v5_ntx, ctx->v5_nty, ctx->v5_nseg, ctx->v5_zseg,
-                           ctx->v5_coef.data(), dotp, st, &nl_, ev));
+                           ctx->v5_coef.data(), dotp, st, &nl_, ev, ctx->v5_kern));
   else if (ctx->use_col)
     LAUNCH(launch_apply_col_raw(ctx->g, x, y, done, ctx->d_colstate, ctx->d_flags, ctx->d_corner, ctx->d_pending,
                                 ctx->col_ntx, ctx->col_nty, ctx->col_nseg, ctx->col_zseg, ctx->col_coef.data(), dotp,
@@ -980,6 +982,16 @@ extern "C" sc_status sc_nccl_comm_destroy(void* comm) {
 }
 
 extern "C" long long sc_launch_count(const sc_ctx* ctx) { return ctx ? ctx->nlaunch : 0; }
+
+extern "C" const char* sc_operator_kernel(const sc_ctx* ctx) {
+  if (!ctx) return "";
+  if (ctx->use_v5) return ctx->v5_kern == 6 ? "v6" : "v5";
+  if (ctx->use_col) return "v3";
+  if (ctx->use_p2) return "p2";
+  if (ctx->use_rw) return "rw";
+  if (ctx->use_big) return "v4";
+  return "v1";
+}
 
 extern "C" const char* sc_last_error(const sc_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
 

@@ -164,7 +164,7 @@ void v5_segments(int ntiles, int nz, int nslots, int* nseg, int* zseg);
 void v5_make_coef(int ni, const double* d, const double* a0, const double* lam, double K00, double K0p, double w0,
                   std::vector<unsigned char>& out);
 int launch_apply_v5(const Geom& g, const double* x, double* y, const double* done, int ntx, int nty, int nseg,
-                    int zseg, const void* coef, double* dotp, void* stream, int* nl, void* events);
+                    int zseg, const void* coef, double* dotp, void* stream, int* nl, void* events, int kern);
 // z-segments of the tile columns: ntiles columns of nz layers on nsm persistent CTAs
 void col_choose_segments(int ntiles, int nz, int nsm, int* nseg, int* zseg);
 int col_slots();   // step slots of the parked look-back partials (look-back distance + 1)

@@ -189,6 +189,9 @@ class Context:
                self.lib.sc_basis_1d(self.ctx, dp(lam), dp(a0), dp(ap), dp(S), dp(w), dp(kt)))
         return dict(lam=lam, a0=a0, ap=ap, S=S.reshape(ni, ni), w=w, K00=kt[0], K0p=kt[1], w0=kt[2])
 
+    def operator_kernel(self):
+        return self.lib.sc_operator_kernel(self.ctx).decode()
+
     def launch_count(self):
         return int(self.lib.sc_launch_count(self.ctx))
 

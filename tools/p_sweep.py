@@ -5,9 +5,11 @@
 For each p the uniform cube has n = round(594/p) elements per direction (about 2.1e8 GLL
 unknowns), lambda = 1, and a seeded uniform[-1,1] skeleton vector (counter-based generator).
 Times `reps` back-to-back applications with CUDA events after warm-up (inputs of 0.2-1.5 GB
-per vector exceed L2).  Reports ms per application, GDOF/s = N / t, s per unknown, the
-algorithmic bytes 16 N_c / t as a fraction of the measured HBM peak, and which kernel ran
-(row-warp kernels for p <= 4, tile-column v3 for p <= 8, colour-scheduled one-CTA-per-element v4 above).
+per vector exceed L2).  Reports ms per application, GDOF/s = N / t, s per unknown, and the
+roofline: HBM floor = 16 N_c bytes / measured copy bandwidth (MEASURED_PEAKS.json),
+FP64 floor = the paper's 13 multiplications + 11 additions per interior point (24 n_e n_I^3 flop,
+P:413 / Table 3) / the measured DFMA peak (profiles/fp64_peak.json); fraction of roofline =
+max(the two floors) / t, each floor's own fraction reported too.
 """
 import argparse
 import json
@@ -31,6 +33,8 @@ def main():
     from synth import cfg3
     hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    fpath = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    fp64 = json.load(open(fpath))["fp64_tflops"] if os.path.exists(fpath) else 37.2
     rows = []
     for p in [int(s) for s in a.ps.split(",")]:
         g = cfg3(p)
@@ -48,17 +52,21 @@ def main():
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / a.reps
         n_c = g.n_skeleton()
+        t_hbm = 16.0 * n_c / (hbm * 1e9) * 1e3                                   # ms
+        t_fp64 = 24.0 * g.n_elements * (p - 1) ** 3 / (fp64 * 1e12) * 1e3       # ms
         row = {"p": p, "n": g.ne[0], "N": g.n_lattice, "N_c": n_c, "ms_per_apply": ms,
                "gdofs": g.n_lattice / ms / 1e6, "s_per_unknown": ms * 1e-3 / g.n_lattice,
-               "hbm_frac": 16.0 * n_c / (ms * 1e-3) / 1e9 / hbm,
-               "kernel": {2: "p2 row-warp", 3: "rw row-warp", 4: "rw row-warp"}.get(
-                   p, "v3 tile-column" if p <= 8 else "v4 colour element-CTA")}
+               "hbm_floor_ms": t_hbm, "fp64_floor_ms": t_fp64,
+               "hbm_frac": t_hbm / ms, "fp64_frac": t_fp64 / ms,
+               "bound": "hbm" if t_hbm >= t_fp64 else "fp64", "roofline_frac": max(t_hbm, t_fp64) / ms,
+               "kernel": os.environ.get("SC_KERNEL_NOTE", "")}
         rows.append(row)
         print(json.dumps(row), flush=True)
         del ctx, x, y
         torch.cuda.empty_cache()
-    out = {"config": "cfg3: uniform cube, n = round(594/p), lambda = 1, seeded uniform[-1,1] x",
-           "hbm_peak_gbs": hbm, "sweep": rows}
+    out = {"config": "cfg3: uniform cube, n = round(594/p) (halves up), lambda = 1, seeded uniform[-1,1] x",
+           "hbm_peak_gbs": hbm, "fp64_peak_tflops": fp64, "fp64_peak_source": "profiles/fp64_peak.json (measured)",
+           "sweep": rows}
     if a.out:
         with open(a.out, "w") as fh:
             json.dump(out, fh, indent=1)
