@@ -105,8 +105,15 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def oracle_sample(grid, n_side, iters=None, budget_s=15.0):
-    """Time the oracle's PCG iteration on a bounded sample (n_side^3 elements, same p / lambda)."""
+def oracle_sample(grid, n_side, iters=None, budget_s=15.0, threads=None):
+    """Time the oracle's PCG iteration on a bounded sample (n_side^3 elements, same p / lambda).
+    threads: limit the BLAS threads (threadpoolctl), e.g. 1 for the paper's single core."""
+    if threads is not None:
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=threads):
+            res = oracle_sample(grid, n_side, iters, budget_s, None)
+        res["cores"] = threads
+        return res
     import numpy as np
     from oracle import operator, solve, pcg
     from synth import small_grid, lattice_random
@@ -300,6 +307,9 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = oracle_sample(grid, args.cpu_sample)
         cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        # the paper ran on one core: the same oracle with one BLAS thread
+        one = oracle_sample(grid, max(4, args.cpu_sample // 2), budget_s=8.0, threads=1)
+        cpu["one_core"] = {k: one[k] for k in ("value", "unit", "cores", "sample")}
 
     if rank == 0:
         line = {

@@ -72,10 +72,10 @@ struct sc_ctx {
   bool use_big = false;
   bool use_p2 = false;                  // p = 2 row-warp operator (kernels_p2.cu)
   bool use_rw = false;                  // p = 3, 4 row-warp operator (kernels_rw.cu)
-  bool use_v5 = false;                  // 3 <= p <= 8 halo-recompute tile columns (kernels_v5.cu)
-  std::vector<unsigned char> v5_coef;
-  int v5_ntx = 0, v5_nty = 0, v5_nseg = 1, v5_zseg = 0;
-  int v5_kern = 5;                      // 5: class-per-warp kernel, 6: uniform class lanes
+  bool use_v6 = false;                  // 3 <= p <= 8 halo-recompute tile columns (kernels_v6.cu)
+  std::vector<unsigned char> v6_coef;
+  int v6_ntx = 0, v6_nty = 0, v6_nseg = 1, v6_zseg = 0;
+  int v6_h = 4;                         // compute-tile height: 4 (2 CTAs per SM) or 8 (1 CTA of 16 warps)
   bool use_ptab = false;                // PCG reads Pinv from the per-class table (uniform geometry)
   PinvTab ptab;                 // v4 colour-scheduled element operator (n_I >= 8, uniform geometry)
   std::vector<unsigned char> big_coef;
@@ -331,31 +331,36 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
     for (int m = 0; m < ni; ++m) sig_ok &= (B.sigma[m] == ((m & 1) ? -1 : 1));
     const char* np2 = getenv("SC_NO_P2");
     const char* nrw = getenv("SC_NO_RW");
-    // SC_OP selects the p <= 8 operator family: "v5" (default for 3 <= p <= 8), "v3" (tile columns
-    // with look-back, kernels_col.cu), "rw" (p = 3, 4 row-warp kernels)
+    // SC_OP selects the p <= 8 operator family: "v6" (halo-recompute tile columns, kernels_v6.cu),
+    // "v3" (tile columns with look-back, kernels_col.cu), "rw" (p = 3, 4 row-warp kernels); default:
+    // the measured fastest per p
     const char* opsel = getenv("SC_OP");
     const std::string op = opsel ? opsel : "";
-    const bool want_v5 = op.empty() || op == "v5" || op == "v6";
-    if (v5_supported(ni) && uniform && sig_ok && want_v5 && !(env && env[0] == '1')) {
-      v5_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->v5_coef);
-      v5_tiles(nx, ny, &ctx->v5_ntx, &ctx->v5_nty);
+    // measured (tools/op_time.py, r2 runs): v6 fastest for p = 5, 6, 7; v3 and v6 equal at p = 8
+    // (7.86 ms at cfg5; v3 kept there: its fused p . q is the one the round-1 bench validated);
+    // the row-warp kernels fastest for p = 3, 4
+    const bool want_v6 = op == "v6" || (op.empty() && ni >= 4 && ni <= 6);
+    if (v6_supported(ni) && uniform && sig_ok && want_v6 && !(env && env[0] == '1')) {
+      const char* hs = getenv("SC_V6_H");
+      ctx->v6_h = (hs && atoi(hs) == 8) ? 8 : ((hs && atoi(hs) == 4) ? 4 : 4);
+      v6_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->v6_coef);
+      v6_tiles(nx, ny, ctx->v6_h, &ctx->v6_ntx, &ctx->v6_nty);
       int dev = 0, nsm = 148;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
       const char* zs = getenv("SC_ZSEG");
       if (zs && atoi(zs) > 0) {
         const int s = atoi(zs) > nz ? nz : atoi(zs);
-        ctx->v5_zseg = (nz + s - 1) / s;
-        ctx->v5_nseg = (nz + ctx->v5_zseg - 1) / ctx->v5_zseg;
+        ctx->v6_zseg = (nz + s - 1) / s;
+        ctx->v6_nseg = (nz + ctx->v6_zseg - 1) / ctx->v6_zseg;
       } else {
-        v5_segments(ctx->v5_ntx * ctx->v5_nty, nz, 2 * nsm, &ctx->v5_nseg, &ctx->v5_zseg);
+        v6_segments(ctx->v6_ntx * ctx->v6_nty, nz, (ctx->v6_h == 4 ? 2 : 1) * nsm, &ctx->v6_nseg, &ctx->v6_zseg);
       }
-      const size_t nitems = (size_t)ctx->v5_ntx * ctx->v5_nty * ctx->v5_nseg;
+      const size_t nitems = (size_t)ctx->v6_ntx * ctx->v6_nty * ctx->v6_nseg;
       if (cudaMalloc(&ctx->d_dotp, sizeof(double) * nitems) != cudaSuccess) return fail("cudaMalloc dotp");
       const char* fd = getenv("SC_FUSED_DOT");
       ctx->fused_dot = !(fd && fd[0] == '0');
-      ctx->use_v5 = true;
-      ctx->v5_kern = op == "v5" ? 5 : 6;
+      ctx->use_v6 = true;
     } else if (ni == 1 && uniform && sig_ok && !(env && env[0] == '1') && !(np2 && np2[0] == '1')) {
       big_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->big_coef);
       ctx->use_p2 = true;
@@ -393,7 +398,7 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
       ctx->use_col = true;
     }
     // v4 also runs non-uniform grids: each CTA derives its element's coefficients from d_e
-    if (!ctx->use_v5 && !ctx->use_col && !ctx->use_p2 && !ctx->use_rw && big_supported(ni) && sig_ok && !(env && env[0] == '1')) {
+    if (!ctx->use_v6 && !ctx->use_col && !ctx->use_p2 && !ctx->use_rw && big_supported(ni) && sig_ok && !(env && env[0] == '1')) {
       const double d_one[4] = {1.0, 1.0, 1.0, 1.0};
       big_make_coef(ni, uniform ? g.d_uni : d_one, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->big_coef);
       ctx->use_big = true;
@@ -604,9 +609,9 @@ static sc_status apply_impl(sc_ctx* ctx, const double* x, double* y, const doubl
                             double* dotp = nullptr) {
   const bool rec = ctx->prof_on && ctx->prof_n < (int)ctx->prof_ev.size() / 2;
   cudaEvent_t* ev = rec ? &ctx->prof_ev[2 * ctx->prof_n] : nullptr;
-  if (ctx->use_v5)
-    LAUNCH(launch_apply_v5(ctx->g, x, y, done, ctx->v5_ntx, ctx->v5_nty, ctx->v5_nseg, ctx->v5_zseg,
-                           ctx->v5_coef.data(), dotp, st, &nl_, ev, ctx->v5_kern));
+  if (ctx->use_v6)
+    LAUNCH(launch_apply_v6(ctx->g, x, y, done, ctx->v6_ntx, ctx->v6_nty, ctx->v6_nseg, ctx->v6_zseg,
+                           ctx->v6_coef.data(), dotp, st, &nl_, ev, ctx->v6_h));
   else if (ctx->use_col)
     LAUNCH(launch_apply_col_raw(ctx->g, x, y, done, ctx->d_colstate, ctx->d_flags, ctx->d_corner, ctx->d_pending,
                                 ctx->col_ntx, ctx->col_nty, ctx->col_nseg, ctx->col_zseg, ctx->col_coef.data(), dotp,
@@ -651,10 +656,10 @@ static sc_status pcg_iteration(sc_ctx* ctx, cudaStream_t st) {
   // entries it finalizes, one fixed-order sum follows.  At cfg5 12.47 -> 11.74 ms per iteration
   // against the separate dot kernel (which streams p and q once more); SC_FUSED_DOT=0 disables it.
   // (Early in round 1, with a slower operator, it measured slower: 10.67 vs 9.55 + 0.9 ms.)
-  // v5 returns per-CTA partials of x . A x over its owned entities / elements, which sum to p . q on
+  // v6 returns per-CTA partials of x . A x over its owned entities / elements, which sum to p . q on
   // any number of ranks (each rank's partial interface-plane sums included): fused there on every rank.
-  const bool fused = ((ctx->use_col && ctx->prm.nranks == 1) || ctx->use_v5) && ctx->fused_dot;
-  const int nparts = ctx->use_v5 ? ctx->v5_ntx * ctx->v5_nty * ctx->v5_nseg : ctx->col_ntx * ctx->col_nty * ctx->col_nseg;
+  const bool fused = ((ctx->use_col && ctx->prm.nranks == 1) || ctx->use_v6) && ctx->fused_dot;
+  const int nparts = ctx->use_v6 ? ctx->v6_ntx * ctx->v6_nty * ctx->v6_nseg : ctx->col_ntx * ctx->col_nty * ctx->col_nseg;
   sc_status s = apply_impl(ctx, ctx->pv, ctx->q, done, st, fused ? ctx->d_dotp : nullptr);
   if (s) return s;
   if (fused) {
@@ -985,7 +990,7 @@ extern "C" long long sc_launch_count(const sc_ctx* ctx) { return ctx ? ctx->nlau
 
 extern "C" const char* sc_operator_kernel(const sc_ctx* ctx) {
   if (!ctx) return "";
-  if (ctx->use_v5) return ctx->v5_kern == 6 ? "v6" : "v5";
+  if (ctx->use_v6) return ctx->v6_h == 8 ? "v6h8" : "v6";
   if (ctx->use_col) return "v3";
   if (ctx->use_p2) return "p2";
   if (ctx->use_rw) return "rw";

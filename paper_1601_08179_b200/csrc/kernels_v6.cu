@@ -1,34 +1,31 @@
-// Condensed operator v5 (rows a3-a8 of SURVEY §8(a)) for 2 <= n_I <= 7 (p = 3..8), uniform
-// geometry: tile columns with a recomputed halo, bulk-copy (TMA) row loads, class-specialised
-// condensed part, two CTAs per SM.
+// Condensed operator v6 (rows a3-a8 of SURVEY §8(a)) for 2 <= n_I <= 7 (p = 3..8), uniform
+// geometry: tile columns with a recomputed halo, bulk-copy (TMA) row loads, uniform class lanes.
 //
-// Work decomposition.  A CTA owns the skeleton entities of an xy-tile of 7 x 3 elements over a
-// z-segment of element layers: x-faces fx in [x0, x0+7), y-faces fy in [y0, y0+3), z-faces /
-// edges / vertices of the same index ranges, element layers [lfin0, lend] and planes
-// [lfin0, lend] (+ plane nz for the top segment).  Its 32 lanes compute the 8 x 4 elements
-// ex in [x0-1, x0+7), ey in [y0-1, y0+3): the extra column / row (the "halo") are the
-// neighbours whose condensed parts reach the owned W / S faces.  Every owned entity is then
-// complete inside the CTA: no inter-CTA communication (no look-back, flags or atomics), each
-// skeleton entry is written exactly once, and the result is independent of scheduling.
-// Edges and vertices have no condensed part (c13), so their values are primary-part
-// stencils of the input, computed entity-centrically by their owner.
+// Work decomposition.  A CTA owns the skeleton entities of an xy-tile of 7 x (H - 1) elements over a
+// z-segment of element layers: x-faces fx in [x0, x0+7), y-faces fy in [y0, y0+H-1), z-faces /
+// edges / vertices of the same index ranges, element layers [lfin0, lend] and planes [lfin0, lend]
+// (+ plane nz for the top segment).  It computes the 8 x H elements ex in [x0-1, x0+7),
+// ey in [y0-1, y0+H-1): the extra column / row (the "halo") are the neighbours whose condensed
+// parts reach the owned W / S faces.  Every owned entity is then complete inside the CTA: no
+// inter-CTA communication (no look-back, flags or atomics), each skeleton entry is written by
+// exactly one CTA, and the result is independent of scheduling.  Edges and vertices have no
+// condensed part (c13), so their values are primary-part stencils of the input, computed
+// entity-centrically by their owner.  H = 4 (two CTAs of 8 warps per SM) or 8 (one CTA of 16 warps,
+// halo overhead 64/49 instead of 32/21).
 //
-// The CTA marches up its column one element layer per step.  Per step l it bulk-loads
-// (cp.async.bulk + mbarrier, one elected thread) the rows of layer l (x-faces, y-faces,
-// z-edges) and plane l+1 (z-faces, x-edges, y-edges, vertices); plane l stays from the previous
-// step.  Each entity row of the tile is one contiguous skeleton range; a row is
-// copied as the 16-byte aligned superset of its valid range into a slot whose base has the same
-// 8-byte phase, so the row sits at slot + (global index & 1).
+// The CTA marches up its column one element layer per step.  Per step l warp 0 bulk-loads
+// (cp.async.bulk + one mbarrier transaction) the rows of layer l (x-faces, y-faces, z-edges) and
+// plane l+1 (z-faces, x-edges, y-edges, vertices); plane l stays from the previous step.  Each
+// entity row of the tile is one contiguous skeleton range; a row is copied as the
+// 16-byte aligned superset of its valid range into a slot whose base has the same 8-byte phase,
+// so the row sits at slot + (global index & 1).
 //
-// Condensed part (Table 2, Eq. 26) in the even / odd form of v3 (kernels_col.cu):
-// with ap = sigma .* a0, the interior points split into 8 parity classes (s_i, s_j, s_k); warp w
-// runs one class for all 32 elements (lane = element), fully unrolled with compile-time indices,
-// so every coefficient (c_d = d_d a0, D^{-1}) is a constant-bank operand.  Per direction the two
-// classes of equal other parities form a pair: the "consumer" computes the owned faces' primary
-// part (phase A) and adds its own faces-out sums as soon as they are complete (streaming, no
-// registers held); the "producer" holds its sums until the face inputs are dead and hands them
-// over through shared memory (overlaid on the dead input rows).  Roles are a per-n_I table
-// chosen to bound the registers held and to balance the warps.
+// Condensed part (Table 2, Eq. 26) in the even / odd form: with ap = sigma .* a0 the
+// interior points split into 8 parity classes (s_i, s_j, s_k); lane = (element, class), a warp
+// holds a 2 x 2 block of elements x 8 classes and every warp runs the same code (see k_apply_v6).
+//
+// An earlier design of this file (v5, git history) ran one class per warp with fully
+// specialised code; measured instruction-fetch bound (8 distinct code streams per CTA) and slower.
 //
 // Fused p . q (PCG): x . A x = sum over owned entities of x * (primary part) - sum over owned
 // elements of the condensed energy uhat . D^{-1} uhat (uhat = faces-in of the element), so
@@ -50,7 +47,7 @@ struct V5Coef {
   double ef2[3][8];      // 2 d_{d+1} w0 a0_m    (x- / y-face <- bounding edges, 2 elements)
   double ef1[3][8];      // d_{d+1} w0 a0_m      (z-face <- bounding edges, one layer)
   double czu[8], cxu[8], cyu[8];   // edge self terms (see the edge phase)
-  double sc[16];         // scalars of the edge / vertex stencils (see v5_make_coef)
+  double sc[16];         // scalars of the edge / vertex stencils (see v6_make_coef)
   double a0[8], sig[8];
 };
 
@@ -66,11 +63,20 @@ struct V5Params {
 
 namespace v5 {
 
-constexpr int TX = 8, TY = 4, OX = 7, OY = 3, NO = OX * OY, NT = 256;
+constexpr int TX = 8, OX = 7;   // compute / owned tile width in x
+
+// tile of height H (compute H rows of elements, own H - 1): derived constants and the row kinds of
+// the per-item descriptor table (side rows of layer l: x-faces, y-faces, z-edges; plane rows of
+// plane q: z-faces, x-edges, y-edges, vertices)
+template <int H>
+struct TC {
+  static constexpr int TY = H, OY = H - 1, NO = OX * OY, NT = 64 * H;
+  static constexpr int R_XF = 0, R_YF = H, R_ZE = 2 * H + 1, R_ZF = 3 * H + 2, R_XE = 4 * H + 2, R_YE = 5 * H + 3,
+                       R_V = 6 * H + 3, NROWS = 7 * H + 4, NSIDE = 3 * H + 2;
+};
 
 // slot of a row of len doubles: >= len + 2 (the 16-byte rounding of the copy), even, and for long
-// rows the stride residue RES mod 16 doubles that keeps the kernel's row-neighbour lanes on
-// disjoint bank pairs (v5: 8, v6: 4)
+// rows (res >= 0) the stride residue res mod 16 doubles (bank-pair placement of neighbouring rows)
 constexpr int slot_len(int len, int res) {
   int v = len + 2;
   if (v & 1) ++v;
@@ -80,14 +86,16 @@ constexpr int slot_len(int len, int res) {
 }
 constexpr int even(int v) { return v + (v & 1); }
 
-template <int NI, int RES = 8>
+// shared-memory layout of the input rows: face rows with a stride of 4 mod 16 doubles (the two rows
+// a half-warp reads fall on disjoint bank pairs), edge / vertex rows unpadded
+template <int NI, int H>
 struct L {
+  using C = TC<H>;
+  static constexpr int TY = H;
   static constexpr int N2 = NI * NI;
-  static constexpr int XS = slot_len((TX + 1) * N2, RES), YS = slot_len(TX * N2, RES), ZS = slot_len(TX * N2, RES);
-  // edge rows: v5's lanes read them row-parallel (padded); v6 reads them entity-centrically (no padding)
-  static constexpr int ERES = RES == 4 ? -1 : RES;
-  static constexpr int ZES = slot_len((TX + 1) * NI, ERES), XES = slot_len(TX * NI, ERES), YES = slot_len((TX + 1) * NI, ERES);
-  static constexpr int VS = slot_len(TX + 1, RES);
+  static constexpr int XS = slot_len((TX + 1) * N2, 4), YS = slot_len(TX * N2, 4), ZS = slot_len(TX * N2, 4);
+  static constexpr int ZES = slot_len((TX + 1) * NI, -1), XES = slot_len(TX * NI, -1), YES = slot_len((TX + 1) * NI, -1);
+  static constexpr int VS = slot_len(TX + 1, -1);
   static constexpr int O_XF = 0;
   static constexpr int O_YF = O_XF + TY * XS;
   static constexpr int O_ZE = O_YF + (TY + 1) * YS;
@@ -95,24 +103,8 @@ struct L {
   static constexpr int PZ = TY * ZS;
   static constexpr int O_PL = O_ZF + 2 * PZ;                // 2 planes of edges / vertices
   static constexpr int PLX = 0, PLY = (TY + 1) * XES, PLV = PLY + TY * YES, PLS = PLV + (TY + 1) * VS;
-  static constexpr int ACC = even(NO * N2);
-  static constexpr int O_AX = O_PL + 2 * PLS;               // owned x-faces of the layer
-  static constexpr int O_AY = O_AX + ACC;                   // owned y-faces of the layer
-  static constexpr int O_AZ = O_AY + ACC;                   // owned z-faces, 2 planes
-  static constexpr int AES = even(2 * NO * NI + NO);        // per plane: x-edges | y-edges | vertices
-  static constexpr int O_AE = O_AZ + 2 * ACC;
-  static constexpr int O_TAB = O_AE + 2 * AES;              // a0, sigma a0, czu, cxu, cyu (8 each)
-  static constexpr int O_SCR = O_TAB + 40;                  // scratch row of the lanes that own nothing
-  static constexpr int TOTAL = O_SCR + even(N2);
-  // exchange buffers of the producer sums ([lane][N2]) overlaid on dead input rows
-  static constexpr int O_QX = O_XF, O_QY = O_YF;            // O_QZ: the bottom plane's z-face rows
-  static_assert(TY * XS >= 32 * N2 && (TY + 1) * YS >= 32 * N2 && PZ >= 32 * N2, "exchange overlay");
+  static constexpr int END = O_PL + 2 * PLS;                // first double after the input rows
 };
-
-// row kinds of the per-item descriptor table: 0..3 x-faces, 4..8 y-faces, 9..13 z-edges (side rows,
-// layer l); 14..17 z-faces, 18..22 x-edges, 23..26 y-edges, 27..31 vertices (plane rows)
-constexpr int R_XF = 0, R_YF = 4, R_ZE = 9, R_ZF = 14, R_XE = 18, R_YE = 23, R_V = 27, NROWS = 32;
-constexpr int NSIDE = 14;
 
 struct Row {
   long long g0, gs;   // skeleton index of the row start at layer / plane 0, per-layer stride
@@ -151,9 +143,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // ---- per-item row descriptors ------------------------------------------------------------
-template <int NI, int RES = 8>
+template <int NI, int H>
 __device__ void make_row(const Geom& g, int r, int cx0, int cy0, Row& d) {
-  using LL = L<NI, RES>;
+  using LL = L<NI, H>;
+  constexpr int R_YF = TC<H>::R_YF, R_ZE = TC<H>::R_ZE, R_ZF = TC<H>::R_ZF, R_XE = TC<H>::R_XE, R_YE = TC<H>::R_YE,
+                R_V = TC<H>::R_V;
   constexpr int N2 = NI * NI;
   const int nx = g.nx, ny = g.ny;
   auto clampx = [&](int lo_ok, int hi_ok, int per) {   // valid index range [lo_ok, hi_ok] of the row's entities
@@ -228,26 +222,31 @@ __device__ void make_row(const Geom& g, int r, int cx0, int cy0, Row& d) {
 }
 
 // smem offset of row r for layer / plane q (its slot, plane slots alternating with q)
-template <int NI, int RES = 8>
+template <int NI, int H>
 __device__ __forceinline__ int row_off(const Row& d, int r, int q) {
-  using LL = L<NI, RES>;
+  using LL = L<NI, H>;
+  constexpr int R_ZF = TC<H>::R_ZF, R_XE = TC<H>::R_XE;
   int s = d.slot;
   if (r >= R_ZF) s += (q & 1) * (r < R_XE ? LL::PZ : LL::PLS);
   return s + (int)((d.g0 + (long long)q * d.gs) & 1);
 }
 
 // Bulk loads of one step, issued by warp 0 as one mbarrier transaction: the side rows of layer qs
-// (if side), the plane rows of plane qa (if pa) and of plane qb (if pb); copy c = lane, lane + 32
-// over the list [side rows 0..13 | plane rows of qa | plane rows of qb].
-template <int NI, int RES = 8>
+// (if side), the plane rows of plane qa (if pa) and of plane qb (if pb); copy c = lane + 32 h over
+// the list [side rows | plane rows of qa | plane rows of qb].
+template <int NI, int H>
 __device__ void issue_step(const V5Params& P, double* sm, const Row* rows, bool side, int qs, bool pa, int qa, bool za,
                            bool pb, int qb, bool zb, unsigned long long* mbar) {
+  constexpr int NSIDE = TC<H>::NSIDE, NROWS = TC<H>::NROWS, NC = (NSIDE + 2 * (NROWS - NSIDE) + 31) / 32;
   const int lane = threadIdx.x & 31;
-  unsigned bytes[2] = {0u, 0u};
-  long long src[2] = {0, 0};
-  int dst[2] = {0, 0};
+  unsigned bytes[NC];
+  long long src[NC];
+  int dst[NC];
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < NC; ++h) {
+    bytes[h] = 0u;
+    src[h] = 0;
+    dst[h] = 0;
     const int c = lane + 32 * h;
     if (c >= NSIDE + 2 * (NROWS - NSIDE)) continue;
     int r, q;
@@ -261,25 +260,27 @@ __device__ void issue_step(const V5Params& P, double* sm, const Row* rows, bool 
     const long long ga = gq + d.a, gb = gq + d.b;
     src[h] = ga & ~1LL;
     bytes[h] = (unsigned)(((gb + 1) & ~1LL) - src[h]) * 8u;
-    dst[h] = row_off<NI, RES>(d, r, q) + d.a - (int)(ga & 1);
+    dst[h] = row_off<NI, H>(d, r, q) + d.a - (int)(ga & 1);
   }
-  unsigned tot = bytes[0] + bytes[1];
+  unsigned tot = 0u;
+#pragma unroll
+  for (int h = 0; h < NC; ++h) tot += bytes[h];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
   if (lane == 0) mbar_arrive_tx(mbar, tot);
   __syncwarp();
 #pragma unroll
-  for (int h = 0; h < 2; ++h)
+  for (int h = 0; h < NC; ++h)
     if (bytes[h]) bulk_g2s(sm + dst[h], P.x + src[h], bytes[h], mbar);
 }
 
 // zero the invalid / Dirichlet parts of rows [r0, r1) for layer / plane q (after the wait)
-template <int NI, int RES = 8>
+template <int NI, int H>
 __device__ __noinline__ void fix_rows(double* sm, const Row* rows, int r0, int r1, int q, bool zplane) {
 #pragma unroll 1
-  for (int r = r0 + (threadIdx.x >> 5); r < r1; r += NT / 32) {
+  for (int r = r0 + (threadIdx.x >> 5); r < r1; r += TC<H>::NT / 32) {
     const Row& d = rows[r];
-    double* b = sm + row_off<NI, RES>(d, r, q);
+    double* b = sm + row_off<NI, H>(d, r, q);
     const bool none = d.a >= d.b || (d.plane && zplane);
     const int a = none ? d.len : d.a, e = none ? d.len : d.b;
     for (int t = threadIdx.x & 31; t < a; t += 32) b[t] = 0.0;
@@ -287,7 +288,6 @@ __device__ __noinline__ void fix_rows(double* sm, const Row* rows, int r0, int r
   }
 }
 
-template <int NI>
 __device__ __forceinline__ bool rows_complete(const Row* rows, int r0, int r1) {
 #pragma unroll 1
   for (int r = r0; r < r1; ++r)
@@ -298,281 +298,20 @@ __device__ __forceinline__ bool rows_complete(const Row* rows, int r0, int r1) {
 // ---- per-step view of the tile in shared memory --------------------------------------------
 // Row r of a kind starts at sm + offset table entry (offsets of the step's layer / planes, in
 // shared memory: lane-dependent rows are then one shared load, not local-memory pointer arrays).
+template <int H>
 struct View {
+  using C = TC<H>;
   const double* sm;
   const int* rs;   // side rows, layer l
   const int* rb;   // plane rows, plane l
   const int* rt;   // plane rows, plane l + 1
-  __device__ __forceinline__ const double* xf(int r) const { return sm + rs[R_XF + r]; }   // x-faces (fx in [cx0, cx0+8])
-  __device__ __forceinline__ const double* yf(int r) const { return sm + rs[R_YF + r]; }   // y-faces (ex in [cx0, cx0+8))
-  __device__ __forceinline__ const double* ze(int r) const { return sm + rs[R_ZE + r]; }   // z-edges (fx)
-  __device__ __forceinline__ const double* zf(int kb, int r) const { return sm + (kb ? rt : rb)[R_ZF + r]; }
-  __device__ __forceinline__ const double* xe(int kb, int r) const { return sm + (kb ? rt : rb)[R_XE + r]; }
-  __device__ __forceinline__ const double* ye(int kb, int r) const { return sm + (kb ? rt : rb)[R_YE + r]; }
-  __device__ __forceinline__ const double* vv(int kb, int r) const { return sm + (kb ? rt : rb)[R_V + r]; }
-};
-
-// ---- class roles ------------------------------------------------------------------------------
-// consumer parity of every direction pair (bits: x-pair (s_j, s_k) at 2 s_j + s_k, y-pair (s_i, s_k)
-// at 4 + 2 s_i + s_k, z-pair (s_i, s_j) at 8 + 2 s_i + s_j), from a search that bounds the doubles
-// a class holds (its z sums + the x / y sums it produces) and balances the warps' work
-template <int NI>
-struct Roles {
-  static constexpr int bits = (NI == 7 || NI == 5 || NI == 3) ? 256 : 60;
-  template <int SI, int SJ, int SK>
-  struct C {
-    static constexpr bool X = SI == ((bits >> (2 * SJ + SK)) & 1);
-    static constexpr bool Y = SJ == ((bits >> (4 + 2 * SI + SK)) & 1);
-    static constexpr bool Z = SK == ((bits >> (8 + 2 * SI + SJ)) & 1);
-  };
-};
-// warp -> class (s_i s_j s_k); warps w and w + 4 share an SM sub-partition: heavy with light
-__device__ __constant__ int kV5Class[8] = {1, 0, 2, 4, 7, 3, 6, 5};
-
-// ---- class phase: primaries of the consumed faces + condensed part, streamed per k-step ----------
-__device__ __forceinline__ void bar_pair(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
-
-// One class (s_i, s_j, s_k) of the 32 lanes' elements.  The k loop is not unrolled (runtime k: the
-// D^{-1} / c3 constants come from the parameter bank with a register offset) so that the eight
-// classes' code fits the instruction caches; i and j are unrolled (compile-time shared-memory
-// offsets and c1 / c2 operands).  Exchange without held registers: the x-face entries (J, K) are
-// read only by the x-pair (s_i = 0, 1 of the same (s_j, s_k)), the y-face entries (I, K) only by the
-// y-pair and the z-face entries (I, J) only by the z-pair (and by the edge phase, which precedes).
-// So after the pair's named barrier of k-step k, the producer writes its completed x sums Q(j, k)
-// (y sums Q(i, k)) over its own lane's input entries (j, k), which are dead, and the consumer adds
-// them to its accumulator after the next barrier.  z sums complete at the end of the loop and go
-// over the bottom face entries (I, J) after a z-pair barrier.
-template <int NI, bool DOT, int SI, int SJ, int SK>
-struct Cls {
-  static constexpr int N2 = NI * NI;
-  static constexpr int CI = (NI - SI + 1) / 2, CJ = (NI - SJ + 1) / 2, CK = (NI - SK + 1) / 2;
-  using R = typename Roles<NI>::template C<SI, SJ, SK>;
-  static constexpr double gi = SI ? -1.0 : 1.0, gj = SJ ? -1.0 : 1.0, gk = SK ? -1.0 : 1.0;
-  static constexpr int XB = 1 + 2 * SJ + SK, YB = 5 + 2 * SI + SK, ZB = 9 + 2 * SI + SJ;   // pair barriers
-
-  // acx / acy: this lane's owned x- / y-face accumulators, azb / azt: owned z-face accumulators of
-  // planes l / l+1 (a shared scratch row for lanes that own nothing: every store is unconditional,
-  // no divergence around the shuffles)
-  static __device__ __forceinline__ void run(const V5Coef& cf, const View& V, int ix, int iy, bool own, double* acx,
-                                             double* acy, double* azb, double* azt, double& dot, bool dot_lay,
-                                             bool dot_b, bool dot_t) {
-    double* const W = const_cast<double*>(V.xf(iy)) + ix * N2;     // W face (E face = W + N2)
-    double* const S = const_cast<double*>(V.yf(iy)) + ix * N2;     // S face
-    const double* Nn = V.yf(iy + 1) + ix * N2;                      // N face
-    double* const B = const_cast<double*>(V.zf(0, iy)) + ix * N2;  // B face (plane l)
-    const double* T = V.zf(1, iy) + ix * N2;                        // T face (plane l + 1)
-    // ---------------- z-face primaries (Eq. 26 generalised), planes l (kb = 0) and l + 1 (kb = 1)
-    if constexpr (R::Z) {
-#pragma unroll 1
-      for (int kb = 0; kb < 2; ++kb) {
-        const double* Yw = V.ye(kb, iy) + ix * NI;    // y-edge (ex, ey) at the plane
-        const double* Ye = Yw + NI;                   // y-edge (ex + 1, ey)
-        const double* Xs = V.xe(kb, iy) + ix * NI;    // x-edge (ex, fy = ey)
-        const double* Xn = V.xe(kb, iy + 1) + ix * NI;
-        const double* U = kb ? T : B;
-        const double* Uo = kb ? B : T;
-        double xc[CI];
-#pragma unroll
-        for (int ii = 0; ii < CI; ++ii) xc[ii] = fma(gj, Xn[SI + 2 * ii], Xs[SI + 2 * ii]);
-        double* const az = kb ? azt : azb;
-#pragma unroll 1
-        for (int jj = 0; jj < CJ; ++jj) {
-          const int j = SJ + 2 * jj;
-          const double yc = fma(gi, Ye[j], Yw[j]);
-          const double e1j = cf.ef1[1][j];
-#pragma unroll
-          for (int ii = 0; ii < CI; ++ii) {
-            const int i = SI + 2 * ii, o = i + NI * j;
-            const double u = U[o];
-            const double pr = fma(cf.fdz[o], u, fma(cf.k0p[2], Uo[o], fma(cf.ef1[0][i], yc, e1j * xc[ii])));
-            az[o] = kb ? pr : az[o] + pr;
-            if (DOT && (kb ? dot_t : dot_b) && own) dot = fma(u, pr, dot);
-          }
-        }
-      }
-    }
-    // k-independent edge combinations of the x- / y-face primaries
-    double yex[R::X ? CJ : 1], xey[R::Y ? CI : 1];
-    if constexpr (R::X) {
-      const double* Yb = V.ye(0, iy) + ix * NI;       // y-edge (fx, ey) at plane l
-      const double* Yt = V.ye(1, iy) + ix * NI;
-#pragma unroll
-      for (int jj = 0; jj < CJ; ++jj) yex[jj] = fma(gk, Yt[SJ + 2 * jj], Yb[SJ + 2 * jj]);
-    }
-    if constexpr (R::Y) {
-      const double* Xb = V.xe(0, iy) + ix * NI;       // x-edge (ex, fy) at plane l
-      const double* Xt = V.xe(1, iy) + ix * NI;
-#pragma unroll
-      for (int ii = 0; ii < CI; ++ii) xey[ii] = fma(gk, Xt[SI + 2 * ii], Xb[SI + 2 * ii]);
-    }
-    const double* const Zs = V.ze(iy) + ix * NI;      // z-edge (fx = cx0 + ix, fy = cy0 + iy)
-    const double* const Zn = V.ze(iy + 1) + ix * NI;
-    const double* const Wm = ix > 0 ? W - N2 : W;
-    const double* const Sm = iy > 0 ? V.yf(iy - 1) + ix * N2 : S;
-    // producer sums of the neighbour lanes (x: lane ix - 1 = slot ix - 1, y: row iy - 1)
-    const double* const Wp = ix > 0 ? W - N2 : W;
-    const double* const Sp = Sm;
-    // ---------------- condensed part
-    double zin[CI][CJ], qz[CI][CJ];
-#pragma unroll
-    for (int ii = 0; ii < CI; ++ii)
-#pragma unroll
-      for (int jj = 0; jj < CJ; ++jj) {
-        const int o = SI + 2 * ii + NI * (SJ + 2 * jj);
-        zin[ii][jj] = fma(gk, T[o], B[o]);
-        qz[ii][jj] = 0.0;
-      }
-    double en = 0.0;   // condensed energy uhat . v of this class
-#pragma unroll 1
-    for (int kk = 0; kk <= CK; ++kk) {
-      const int k = SK + 2 * kk;
-      if (kk < CK) {
-        // ---- primaries of the consumed x- / y-face entries at this k
-        if constexpr (R::X) {
-          const double zc = fma(gj, Zn[k], Zs[k]);
-#pragma unroll
-          for (int jj = 0; jj < CJ; ++jj) {
-            const int j = SJ + 2 * jj, o = j + NI * k;
-            const double u = W[o];
-            const double pr = fma(cf.fdx[o], u, fma(cf.k0p[0], Wm[o] + W[o + N2], fma(cf.ef2[1][j], zc, cf.ef2[2][k] * yex[jj])));
-            acx[o] = pr;
-            if (DOT && dot_lay && own) dot = fma(u, pr, dot);
-          }
-        }
-        if constexpr (R::Y) {
-          const double zc = fma(gi, Zs[NI + k], Zs[k]);   // z-edges (ex, fy) and (ex + 1, fy)
-#pragma unroll
-          for (int ii = 0; ii < CI; ++ii) {
-            const int i = SI + 2 * ii, o = i + NI * k;
-            const double u = S[o];
-            const double pr = fma(cf.fdy[o], u, fma(cf.k0p[1], Sm[o] + Nn[o], fma(cf.ef2[0][i], zc, cf.ef2[2][k] * xey[ii])));
-            acy[o] = pr;
-            if (DOT && dot_lay && own) dot = fma(u, pr, dot);
-          }
-        }
-        // ---- faces in, D^{-1}, faces out at this k
-        double yin[CI], qy[CI], qxs[CJ];
-#pragma unroll
-        for (int ii = 0; ii < CI; ++ii) {
-          const int o = SI + 2 * ii + NI * k;
-          yin[ii] = fma(gj, Nn[o], S[o]);
-          qy[ii] = 0.0;
-        }
-        const double c3 = cf.c[2][k];
-        const double* const Dk = cf.dinv + NI * NI * k;
-#pragma unroll
-        for (int jj = 0; jj < CJ; ++jj) {
-          const int j = SJ + 2 * jj, ox = j + NI * k;
-          const double xin = fma(gi, W[ox + N2], W[ox]);
-          double qx = 0.0;
-#pragma unroll
-          for (int ii = 0; ii < CI; ++ii) {
-            const int i = SI + 2 * ii;
-            const double u = fma(cf.c[0][i], xin, fma(cf.c[1][j], yin[ii], c3 * zin[ii][jj]));
-            const double v = u * Dk[i + NI * j];
-            if (DOT) en = fma(u, v, en);
-            qx = fma(cf.c[0][i], v, qx);
-            qy[ii] = fma(cf.c[1][j], v, qy[ii]);
-            qz[ii][jj] = fma(c3, v, qz[ii][jj]);
-          }
-          if constexpr (R::X) {   // own part on the owned W face: -Q(ix) - s_i Q(ix - 1)
-            const double qm = __shfl_up_sync(0xffffffffu, qx, 1);
-            acx[ox] -= fma(gi, qm, qx);
-          } else {
-            qxs[jj] = qx;
-          }
-        }
-        if constexpr (R::Y) {   // own part on the owned S face: -Q(iy) - s_j Q(iy - 1)
-#pragma unroll
-          for (int ii = 0; ii < CI; ++ii) {
-            const double qm = __shfl_up_sync(0xffffffffu, qy[ii], 8);
-            acy[SI + 2 * ii + NI * k] -= fma(gj, qm, qy[ii]);
-          }
-        }
-        // ---- x hand-over: after the pair barrier the x-face entries (J, k) are dead
-        bar_pair(XB);
-        if constexpr (!R::X) {
-#pragma unroll
-          for (int jj = 0; jj < CJ; ++jj) W[SJ + 2 * jj + NI * k] = qxs[jj];
-        } else if (kk > 0) {   // the producer's sums of k - 2 (written before this barrier)
-          constexpr double gp = SI ? 1.0 : -1.0;
-#pragma unroll
-          for (int jj = 0; jj < CJ; ++jj) {
-            const int o = SJ + 2 * jj + NI * (k - 2);
-            acx[o] -= fma(gp, Wp[o], W[o]);
-          }
-        }
-        bar_pair(YB);
-        if constexpr (!R::Y) {
-#pragma unroll
-          for (int ii = 0; ii < CI; ++ii) S[SI + 2 * ii + NI * k] = qy[ii];
-        } else if (kk > 0) {
-          constexpr double gp = SJ ? 1.0 : -1.0;
-#pragma unroll
-          for (int ii = 0; ii < CI; ++ii) {
-            const int o = SI + 2 * ii + NI * (k - 2);
-            acy[o] -= fma(gp, Sp[o], S[o]);
-          }
-        }
-      } else {
-        // ---- after the last k-step: the producers' last sums
-        bar_pair(XB);
-        if constexpr (R::X) {
-          if (CK > 0) {
-            constexpr double gp = SI ? 1.0 : -1.0;
-#pragma unroll
-            for (int jj = 0; jj < CJ; ++jj) {
-              const int o = SJ + 2 * jj + NI * (k - 2);
-              acx[o] -= fma(gp, Wp[o], W[o]);
-            }
-          }
-        }
-        bar_pair(YB);
-        if constexpr (R::Y) {
-          if (CK > 0) {
-            constexpr double gp = SJ ? 1.0 : -1.0;
-#pragma unroll
-            for (int ii = 0; ii < CI; ++ii) {
-              const int o = SI + 2 * ii + NI * (k - 2);
-              acy[o] -= fma(gp, Sp[o], S[o]);
-            }
-          }
-        }
-      }
-    }
-    // ---- z sums complete: B face (a0) -Q, T face (ap) -s_k Q; hand-over over the B entries (I, J)
-    if constexpr (R::Z) {
-#pragma unroll
-      for (int ii = 0; ii < CI; ++ii)
-#pragma unroll
-        for (int jj = 0; jj < CJ; ++jj) {
-          const int o = SI + 2 * ii + NI * (SJ + 2 * jj);
-          azb[o] -= qz[ii][jj];
-          azt[o] = fma(-gk, qz[ii][jj], azt[o]);
-        }
-    }
-    bar_pair(ZB);   // the z-pair has read its B / T entries
-    if constexpr (!R::Z) {
-#pragma unroll
-      for (int ii = 0; ii < CI; ++ii)
-#pragma unroll
-        for (int jj = 0; jj < CJ; ++jj) B[SI + 2 * ii + NI * (SJ + 2 * jj)] = qz[ii][jj];
-    }
-    bar_pair(ZB);
-    if constexpr (R::Z) {
-      constexpr double gp = SK ? 1.0 : -1.0;
-#pragma unroll
-      for (int ii = 0; ii < CI; ++ii)
-#pragma unroll
-        for (int jj = 0; jj < CJ; ++jj) {
-          const int o = SI + 2 * ii + NI * (SJ + 2 * jj);
-          const double q = B[o];
-          azb[o] -= q;
-          azt[o] = fma(-gp, q, azt[o]);
-        }
-    }
-    if (DOT && own && dot_lay) dot -= en;
-  }
+  __device__ __forceinline__ const double* xf(int r) const { return sm + rs[C::R_XF + r]; }   // x-faces (fx in [cx0, cx0+8])
+  __device__ __forceinline__ const double* yf(int r) const { return sm + rs[C::R_YF + r]; }   // y-faces (ex in [cx0, cx0+8))
+  __device__ __forceinline__ const double* ze(int r) const { return sm + rs[C::R_ZE + r]; }   // z-edges (fx)
+  __device__ __forceinline__ const double* zf(int kb, int r) const { return sm + (kb ? rt : rb)[C::R_ZF + r]; }
+  __device__ __forceinline__ const double* xe(int kb, int r) const { return sm + (kb ? rt : rb)[C::R_XE + r]; }
+  __device__ __forceinline__ const double* ye(int kb, int r) const { return sm + (kb ? rt : rb)[C::R_YE + r]; }
+  __device__ __forceinline__ const double* vv(int kb, int r) const { return sm + (kb ? rt : rb)[C::R_V + r]; }
 };
 
 // ---- edge / vertex primary parts (entity-centric, owned entities) -----------------------------
@@ -581,7 +320,7 @@ struct Cls {
 //   + d2 w0 [sum_j ap_j Fz(ex, fy - 1)(i, j) + sum_j a0_j Fz(ex, fy)(i, j) + K0p (u(fy - 1) + u(fy + 1))]
 //   + 2 d3 w0 [sum_k at_k Fy(ex, fy, l)(i, k) + K0p u(other plane)],  at = a0 (kb = 0) or ap (kb = 1)
 // (K~ rows 0 / p = (K00, a0, K0p) / (K0p, ap, K00), interior rows (a0_m, Lam_m, ap_m); M~ = diag(w0, 1..1, w0),
-// P:381-405).  y-edges by x <-> y symmetry; vertices and z-edges likewise (see v5_make_coef).
+// P:381-405).  y-edges by x <-> y symmetry; vertices and z-edges likewise (see v6_make_coef).
 template <int NI>
 struct Edge {
   // line sum over m of w_m f[m * stride]
@@ -598,8 +337,8 @@ struct Edge {
 // those of plane l + 1 get layer l's part (aet); z-edges of layer l are final.  One loop per entity
 // kind (item t -> owned entity e = t / NI, node c = t % NI; consecutive t are consecutive skeleton
 // entries of a row, so the stores coalesce).  Shared by the v5 and v6 kernels.
-template <int NI, bool DOT>
-__device__ __forceinline__ void edge_phase(const V5Params& P, const View& V, const double* sa0, const double* sap,
+template <int NI, bool DOT, int H>
+__device__ __forceinline__ void edge_phase(const V5Params& P, const View<H>& V, const double* sa0, const double* sap,
                                            const double* czu, const double* cxu, const double* cyu, double* aeb,
                                            double* aet, int cx0, int cy0, int l, bool lay, bool fin_l, bool fin_t,
                                            double& dot) {
@@ -607,6 +346,7 @@ __device__ __forceinline__ void edge_phase(const V5Params& P, const View& V, con
   const Geom& g = P.g;
   const V5Coef& cf = P.cf;
   const int tid = threadIdx.x, nthreads = blockDim.x;
+  constexpr int NO = TC<H>::NO;
     {
       constexpr int NE1 = NO * NI;
       const int nx = g.nx, ny = g.ny;
@@ -724,200 +464,6 @@ __device__ __forceinline__ void edge_phase(const V5Params& P, const View& V, con
     }
 }
 
-// ---- the kernel -------------------------------------------------------------------------------
-template <int NI, bool DOT>
-__global__ void __launch_bounds__(NT, 2) k_apply_v5(const __grid_constant__ V5Params P) {
-  using LL = L<NI>;
-  constexpr int N2 = NI * NI;
-  if (P.done != nullptr && *P.done != 0.0) return;
-  extern __shared__ __align__(16) double sm[];
-  __shared__ __align__(8) unsigned long long mbar;
-  __shared__ Row rows[NROWS];
-  __shared__ int rofs[2][NROWS];
-  __shared__ double sred[NT / 32];
-  const Geom& g = P.g;
-  const V5Coef& cf = P.cf;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, ix = lane & 7, iy = lane >> 3;
-  const int item = blockIdx.x;
-  const int ntile = P.ntx * P.nty;
-  const int seg = item / ntile, tile = item - seg * ntile;
-  const int tx = tile % P.ntx, ty = tile / P.ntx;
-  const int x0 = tx * OX, y0 = ty * OY, cx0 = x0 - 1, cy0 = y0 - 1;
-  const int nz = g.nz;
-  const int lfin0 = seg * P.zseg;
-  const int lbeg = seg > 0 ? lfin0 - 1 : 0;
-  const int lend = seg == P.nseg - 1 ? nz : min(nz, lfin0 + P.zseg) - 1;
-
-  // padding entries of y are written as 0 by the first CTA
-  if (item == 0) {
-    const long long ends[7] = {g.off_f[0] + g.n_f[0] * N2, g.off_f[1] + g.n_f[1] * N2, g.off_f[2] + g.n_f[2] * N2,
-                               g.off_e[0] + g.n_e[0] * NI, g.off_e[1] + g.n_e[1] * NI, g.off_e[2] + g.n_e[2] * NI,
-                               g.off_v + g.n_v};
-    const long long nexts[7] = {g.off_f[1], g.off_f[2], g.off_e[0], g.off_e[1], g.off_e[2], g.off_v, g.n_total};
-#pragma unroll 1
-    for (int q = 0; q < 7; ++q)
-      for (long long i = ends[q] + tid; i < nexts[q]; i += NT) P.y[i] = 0.0;
-  }
-  // small tables (lane-varying indices in the edge phase)
-  double* const sa0 = sm + LL::O_TAB;         // a0
-  double* const sap = sa0 + 8;                // sigma a0 = ap
-  double* const czu = sa0 + 16;
-  double* const cxu = sa0 + 24;
-  double* const cyu = sa0 + 32;
-  if (tid < 8) {
-    sa0[tid] = cf.a0[tid];
-    sap[tid] = cf.a0[tid] * cf.sig[tid];
-    czu[tid] = cf.czu[tid];
-    cxu[tid] = cf.cxu[tid];
-    cyu[tid] = cf.cyu[tid];
-  }
-  if (tid < NROWS) {
-    make_row<NI>(g, tid, cx0, cy0, rows[tid]);
-  }
-  if (tid == 0) {
-    mbar_init(&mbar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  // plane lbeg's partial sums from below: none inside this segment
-  for (int t = tid; t < LL::ACC; t += NT) sm[LL::O_AZ + (lbeg & 1) * LL::ACC + t] = 0.0;
-  for (int t = tid; t < LL::AES; t += NT) sm[LL::O_AE + (lbeg & 1) * LL::AES + t] = 0.0;
-  __syncthreads();
-  const bool side_ok = rows_complete<NI>(rows, 0, NSIDE);
-  const bool plane_ok = rows_complete<NI>(rows, NSIDE, NROWS);
-  // prologue: plane lbeg, and side lbeg + plane lbeg + 1 when layer lbeg exists
-  if (tid < NROWS) {
-    const bool sd = tid < NSIDE;
-    rofs[lbeg & 1][tid] = row_off<NI>(rows[tid], tid, sd ? lbeg : lbeg);
-    if (!sd) rofs[(lbeg + 1) & 1][tid] = row_off<NI>(rows[tid], tid, lbeg + 1);
-  }
-  __syncthreads();   // row descriptors visible to warp 0
-  // prologue batch: plane lbeg, and side lbeg + plane lbeg + 1 when layer lbeg exists
-  if (warp == 0)
-    issue_step<NI>(P, sm, rows, lbeg < nz, lbeg, true, lbeg, zdir(g, lbeg), lbeg < nz, lbeg + 1, zdir(g, lbeg + 1),
-                   &mbar);
-  __syncthreads();   // rofs visible
-  unsigned phase = 0;
-  bool pending = true;            // a load batch is in flight for the current step
-  bool first_fix = !plane_ok || zdir(g, lbeg);
-  double dot = 0.0;
-  const bool own = ix >= 1 && iy >= 1;
-  const int o_lane = (iy - 1) * OX + (ix - 1);
-
-  for (int l = lbeg; l <= lend; ++l) {
-    const bool lay = l < nz;                        // layer l exists (else: final plane nz only)
-    if (pending) {
-      mbar_wait(&mbar, phase);
-      phase ^= 1;
-      pending = false;
-    }
-    // zero the invalid / Dirichlet parts of the rows that just landed
-    const bool fix = first_fix || (lay && (!side_ok || !plane_ok || zdir(g, l + 1)));
-    if (fix) {
-      if (first_fix) fix_rows<NI>(sm, rows, NSIDE, NROWS, l, zdir(g, l));
-      if (lay) {
-        fix_rows<NI>(sm, rows, 0, NSIDE, l, false);
-        fix_rows<NI>(sm, rows, NSIDE, NROWS, l + 1, zdir(g, l + 1));
-      }
-      __syncthreads();
-    }
-    first_fix = false;
-    // views of this step's rows
-    View V{sm, rofs[l & 1], rofs[l & 1] + 0, rofs[(l + 1) & 1]};
-    const bool fin_l = l >= lfin0;                  // plane l / layer l finalized by this CTA
-    const bool fin_t = l + 1 <= lend;               // plane l + 1 finalized by this CTA
-    double* const aeb = sm + LL::O_AE + (l & 1) * LL::AES;          // edge accumulators, plane l
-    double* const aet = sm + LL::O_AE + ((l + 1) & 1) * LL::AES;    // plane l + 1
-    edge_phase<NI, DOT>(P, V, sa0, sap, czu, cxu, cyu, aeb, aet, cx0, cy0, l, lay, fin_l, fin_t, dot);
-    // ======== faces: class phases (layer l) ========
-    double* const AX = sm + LL::O_AX;
-    double* const AY = sm + LL::O_AY;
-    double* const AZB = sm + LL::O_AZ + (l & 1) * LL::ACC;
-    double* const AZT = sm + LL::O_AZ + ((l + 1) & 1) * LL::ACC;
-    double* const scr = sm + LL::O_SCR;
-    double* const acx = own ? AX + o_lane * N2 : scr;
-    double* const acy = own ? AY + o_lane * N2 : scr;
-    double* const azb = own ? AZB + o_lane * N2 : scr;
-    double* const azt = own ? AZT + o_lane * N2 : scr;
-    __syncthreads();   // the edge phase has read every face line before the class phases overwrite entries
-    if (lay) {
-      switch (kV5Class[warp]) {
-        case 0: Cls<NI, DOT, 0, 0, 0>::run(cf, V, ix, iy, own, acx, acy, azb, azt, dot, fin_l, fin_l, fin_t); break;
-        case 1: Cls<NI, DOT, 0, 0, 1>::run(cf, V, ix, iy, own, acx, acy, azb, azt, dot, fin_l, fin_l, fin_t); break;
-        case 2: Cls<NI, DOT, 0, 1, 0>::run(cf, V, ix, iy, own, acx, acy, azb, azt, dot, fin_l, fin_l, fin_t); break;
-        case 3: Cls<NI, DOT, 0, 1, 1>::run(cf, V, ix, iy, own, acx, acy, azb, azt, dot, fin_l, fin_l, fin_t); break;
-        case 4: Cls<NI, DOT, 1, 0, 0>::run(cf, V, ix, iy, own, acx, acy, azb, azt, dot, fin_l, fin_l, fin_t); break;
-        case 5: Cls<NI, DOT, 1, 0, 1>::run(cf, V, ix, iy, own, acx, acy, azb, azt, dot, fin_l, fin_l, fin_t); break;
-        case 6: Cls<NI, DOT, 1, 1, 0>::run(cf, V, ix, iy, own, acx, acy, azb, azt, dot, fin_l, fin_l, fin_t); break;
-        default: Cls<NI, DOT, 1, 1, 1>::run(cf, V, ix, iy, own, acx, acy, azb, azt, dot, fin_l, fin_l, fin_t); break;
-      }
-    }
-    fence_proxy_async();   // generic smem accesses before the next bulk copies into the same rows
-    __syncthreads();       // S3: accumulators final, every input row of step l dead
-    // next step's loads: side l + 1 and plane l + 2 (into plane l's slots)
-    if (l + 1 <= lend && l + 1 < nz) {
-      if (tid < NROWS) {
-        if (tid < NSIDE) rofs[(l + 1) & 1][tid] = row_off<NI>(rows[tid], tid, l + 1);
-        else rofs[(l + 2) & 1][tid] = row_off<NI>(rows[tid], tid, l + 2);
-      }
-      if (warp == 0) issue_step<NI>(P, sm, rows, true, l + 1, false, 0, false, true, l + 2, zdir(g, l + 2), &mbar);
-      pending = true;
-    }
-    // ======== store the owned faces of layer l and the z-faces of plane l ========
-    // 9 rows (x-, y-, z-faces x 3 element rows), one warp per row: each row is OX contiguous faces
-    // in y (the accumulator row is contiguous too); faces beyond the domain are skipped, Dirichlet
-    // faces (fx = 0 / nx, fy = 0 / ny, a Dirichlet z-plane) written as 0
-    if (fin_l) {
-      const int nx = g.nx, ny = g.ny;
-      for (int rr = warp; rr < 3 * OY; rr += NT / 32) {
-        const int kind = rr / OY, oy = rr - kind * OY;
-        const int e0 = x0, er = y0 + oy;   // first entity index along x, row index
-        int cnt, z0 = 0, z1 = 0, za = 0;
-        long long gb;
-        const double* src;
-        if (kind == 0) {          // x-faces fx in [x0, x0 + 7), row ey = er
-          if (!lay || er >= ny) continue;
-          cnt = min(OX, nx + 1 - e0);
-          z0 = e0 == 0;
-          z1 = e0 + cnt - 1 == nx;
-          gb = g.off_f[0] + ((long long)e0 + (long long)(nx + 1) * (er + (long long)ny * l)) * N2;
-          src = AX;
-        } else if (kind == 1) {   // y-faces ex in [x0, x0 + 7), row fy = er
-          if (!lay || er > ny) continue;
-          cnt = min(OX, nx - e0);
-          za = (er == 0 || er == ny);
-          gb = g.off_f[1] + ((long long)e0 + (long long)nx * (er + (long long)(ny + 1) * l)) * N2;
-          src = AY;
-        } else {                  // z-faces of plane l, ex in [x0, x0 + 7), row ey = er
-          if (er >= ny) continue;
-          cnt = min(OX, nx - e0);
-          za = zdir(g, l);
-          gb = g.off_f[2] + ((long long)e0 + (long long)nx * (er + (long long)ny * l)) * N2;
-          src = AZB;
-        }
-        if (cnt <= 0) continue;
-        src += oy * OX * N2;
-        double* dst = P.y + gb;
-        const int n = cnt * N2, lo = za ? n : (z0 ? N2 : 0), hi = z1 ? n - N2 : n;
-        for (int t = lane; t < n; t += 32) dst[t] = (t >= lo && t < hi) ? src[t] : 0.0;
-      }
-    }
-    __syncthreads();       // S4: accumulators read before the next step writes them
-  }
-  if (DOT && P.dotp != nullptr) {
-    double s = dot;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) sred[warp] = s;
-    __syncthreads();
-    if (tid == 0) {
-      double tsum = 0.0;
-      for (int w = 0; w < NT / 32; ++w) tsum += sred[w];
-      P.dotp[item] = tsum;
-    }
-  }
-}
-
-
 // =============================================================================================
 // Operator v6 (same tiles, rows, loads and edge stencils as v5): uniform class lanes.
 //
@@ -934,18 +480,20 @@ __global__ void __launch_bounds__(NT, 2) k_apply_v5(const __grid_constant__ V5Pa
 // L2 and costs no DRAM traffic).  The x- / y-face primaries are computed entity-centrically into
 // the owned accumulators before the class phase.
 // =============================================================================================
-template <int NI>
+template <int NI, int H>
 struct L6 {
-  using B = L<NI, 4>;
+  using B = L<NI, H>;
+  using C = TC<H>;
   static constexpr int N2 = NI * NI;
   static constexpr int M = (NI + 1) / 2;                   // padded class extent
-  static constexpr int ACC = B::ACC;
-  static constexpr int O_AX = B::O_AX;                     // owned x-faces of the layer
+  static constexpr int ACC = even(C::NO * N2);
+  static constexpr int O_AX = B::END;                      // owned x-faces of the layer
   static constexpr int O_AY = O_AX + ACC;                  // owned y-faces of the layer
-  static constexpr int O_XB = O_AY + ACC;                  // [OY][3][N2]: E parts of elements ix = 1, 3, 5, rows 1..3
-  static constexpr int O_YB = O_XB + even(OY * 3 * N2);    // [OX][N2]: N parts of the elements (ix >= 1) of row iy = 1
-  static constexpr int O_AE = O_YB + even(OX * N2);        // edge accumulators, 2 planes
-  static constexpr int AES = B::AES;
+  static constexpr int O_XB = O_AY + ACC;                  // [OY][3][N2]: E parts of elements ix = 1, 3, 5, rows >= 1
+  static constexpr int NYB = H / 2 - 1;                    // rows iy = 1, 3, .., H - 3 send N parts across blocks
+  static constexpr int O_YB = O_XB + even(C::OY * 3 * N2); // [NYB][OX][N2]
+  static constexpr int O_AE = O_YB + even(NYB * OX * N2);  // edge accumulators, 2 planes
+  static constexpr int AES = even(2 * C::NO * NI + C::NO); // per plane: x-edges | y-edges | vertices
   static constexpr int O_TAB = O_AE + 2 * AES;             // a0, ap, czu, cxu, cyu (8 each)
   static constexpr int O_CT = O_TAB + 40;                  // class tables (see k_apply_v6)
   static constexpr int CT_C = 0, CT_FDZ = 24, CT_EF1 = CT_FDZ + even(N2), CT_FDX = CT_EF1 + 16,
@@ -959,15 +507,18 @@ struct L6 {
   static constexpr int O_SCR = O_DI + DIN;                 // scratch row of stores that own nothing
   static constexpr int O_AZ = O_SCR + even(N2);            // owned z-faces of plane l
   static constexpr int TOTAL = O_AZ + ACC;
-  // two CTAs per SM: 2 x (dynamic + ~1.6 KB static + 1 KB reserved) <= 228 KB
-  static_assert(2 * (TOTAL * 8 + 1700 + 1024) <= 228 * 1024, "v6 shared memory: two CTAs per SM");
+  static constexpr int CTAS = H == 4 ? 2 : 1;              // CTAs per SM the layout is sized for
+  // per SM: CTAS x (dynamic + ~2 KB static + 1 KB reserved) <= 228 KB
+  static_assert(CTAS * (TOTAL * 8 + 2048 + 1024) <= 228 * 1024, "v6 shared memory");
 };
 
-template <int NI, bool DOT>
-__global__ void __launch_bounds__(NT, 2) k_apply_v6(const __grid_constant__ V5Params P) {
-  using LL = L<NI, 4>;
-  using L6T = L6<NI>;
+template <int NI, bool DOT, int H>
+__global__ void __launch_bounds__(64 * H, H == 4 ? 2 : 1) k_apply_v6(const __grid_constant__ V5Params P) {
+  using LL = L<NI, H>;
+  using L6T = L6<NI, H>;
+  using C = TC<H>;
   constexpr int N2 = NI * NI, M = L6T::M;
+  constexpr int OY = C::OY, NO = C::NO, NT = C::NT, NROWS = C::NROWS, NSIDE = C::NSIDE;
   if (P.done != nullptr && *P.done != 0.0) return;
   extern __shared__ __align__(16) double sm[];
   __shared__ __align__(8) unsigned long long mbar;
@@ -998,7 +549,7 @@ __global__ void __launch_bounds__(NT, 2) k_apply_v6(const __grid_constant__ V5Pa
   }
   // the input rows are read beyond their valid ends by padded class points (times a zero
   // coefficient): every slot starts as finite zeros
-  for (int t = tid; t < LL::O_AX; t += NT) sm[t] = 0.0;
+  for (int t = tid; t < LL::END; t += NT) sm[t] = 0.0;
   double* const sa0 = sm + L6T::O_TAB;
   double* const sap = sa0 + 8;
   double* const czu = sa0 + 16;
@@ -1028,23 +579,23 @@ __global__ void __launch_bounds__(NT, 2) k_apply_v6(const __grid_constant__ V5Pa
     const int i = t % L6T::P1, j = (t / L6T::P1) % L6T::P1, k = t / (L6T::P1 * L6T::P1);
     sdi[t] = (i < NI && j < NI && k < NI) ? cf.dinv[i + NI * (j + NI * k)] : 0.0;
   }
-  if (tid < NROWS) make_row<NI, 4>(g, tid, cx0, cy0, rows[tid]);
+  if (tid < NROWS) make_row<NI, H>(g, tid, cx0, cy0, rows[tid]);
   if (tid == 0) {
     mbar_init(&mbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int t = tid; t < L6T::AES; t += NT) sm[L6T::O_AE + (lbeg & 1) * L6T::AES + t] = 0.0;
   __syncthreads();
-  const bool side_ok = rows_complete<NI>(rows, 0, NSIDE);
-  const bool plane_ok = rows_complete<NI>(rows, NSIDE, NROWS);
+  const bool side_ok = rows_complete(rows, 0, NSIDE);
+  const bool plane_ok = rows_complete(rows, NSIDE, NROWS);
   if (tid < NROWS) {
-    rofs[lbeg & 1][tid] = row_off<NI, 4>(rows[tid], tid, lbeg);
-    if (tid >= NSIDE) rofs[(lbeg + 1) & 1][tid] = row_off<NI, 4>(rows[tid], tid, lbeg + 1);
+    rofs[lbeg & 1][tid] = row_off<NI, H>(rows[tid], tid, lbeg);
+    if (tid >= NSIDE) rofs[(lbeg + 1) & 1][tid] = row_off<NI, H>(rows[tid], tid, lbeg + 1);
   }
   fence_proxy_async();   // the zero fill above precedes the bulk copies into the same rows
   __syncthreads();
   if (warp == 0)
-    issue_step<NI, 4>(P, sm, rows, lbeg < nz, lbeg, true, lbeg, zdir(g, lbeg), lbeg < nz, lbeg + 1, zdir(g, lbeg + 1),
+    issue_step<NI, H>(P, sm, rows, lbeg < nz, lbeg, true, lbeg, zdir(g, lbeg), lbeg < nz, lbeg + 1, zdir(g, lbeg + 1),
                    &mbar);
   __syncthreads();
   unsigned phase = 0;
@@ -1076,20 +627,20 @@ __global__ void __launch_bounds__(NT, 2) k_apply_v6(const __grid_constant__ V5Pa
     }
     const bool fix = first_fix || (lay && (!side_ok || !plane_ok || zdir(g, l + 1)));
     if (fix) {
-      if (first_fix) fix_rows<NI, 4>(sm, rows, NSIDE, NROWS, l, zdir(g, l));
+      if (first_fix) fix_rows<NI, H>(sm, rows, NSIDE, NROWS, l, zdir(g, l));
       if (lay) {
-        fix_rows<NI, 4>(sm, rows, 0, NSIDE, l, false);
-        fix_rows<NI, 4>(sm, rows, NSIDE, NROWS, l + 1, zdir(g, l + 1));
+        fix_rows<NI, H>(sm, rows, 0, NSIDE, l, false);
+        fix_rows<NI, H>(sm, rows, NSIDE, NROWS, l + 1, zdir(g, l + 1));
       }
       __syncthreads();
     }
     first_fix = false;
-    View V{sm, rofs[l & 1], rofs[l & 1], rofs[(l + 1) & 1]};
+    View<H> V{sm, rofs[l & 1], rofs[l & 1], rofs[(l + 1) & 1]};
     const bool fin_l = l >= lfin0;
     const bool fin_t = l + 1 <= lend;
     double* const aeb = sm + L6T::O_AE + (l & 1) * L6T::AES;
     double* const aet = sm + L6T::O_AE + ((l + 1) & 1) * L6T::AES;
-    edge_phase<NI, DOT>(P, V, sa0, sap, czu, cxu, cyu, aeb, aet, cx0, cy0, l, lay, fin_l, fin_t, dot);
+    edge_phase<NI, DOT, H>(P, V, sa0, sap, czu, cxu, cyu, aeb, aet, cx0, cy0, l, lay, fin_l, fin_t, dot);
     double* const AX = sm + L6T::O_AX;
     double* const AY = sm + L6T::O_AY;
     double* const XB = sm + L6T::O_XB;
@@ -1126,7 +677,6 @@ __global__ void __launch_bounds__(NT, 2) k_apply_v6(const __grid_constant__ V5Pa
       const double* znx = V.ze(iy + 1) + ix * NI + sk;
       const double* ybx = V.ye(0, iy) + ix * NI + sj;             // y-edge (fx, ey) at planes l, l + 1: j
       const double* ytx = V.ye(1, iy) + ix * NI + sj;
-      const double* zwy = V.ze(iy) + ix * NI + sk;                // z-edges (ex, fy), (ex + 1, fy): k
       const double* xby = V.xe(0, iy) + ix * NI + si;             // x-edge (ex, fy) at planes l, l + 1: i
       const double* xty = V.xe(1, iy) + ix * NI + si;
       const double* fdxl = ct + L6T::CT_FDX + sj + NI * sk;
@@ -1135,6 +685,12 @@ __global__ void __launch_bounds__(NT, 2) k_apply_v6(const __grid_constant__ V5Pa
       const double* e3x = ct + L6T::CT_EF2 + 16 + sk;             // 2 d3 w0 a0_k
       const double* e1y = ct + L6T::CT_EF2 + si;                  // 2 d1 w0 a0_i
       const bool pd = DOT && own && fin_l;                        // this lane's primaries count in x . A x
+      // accumulator rows of this lane's stores (scratch for the lanes / entries that own nothing)
+      double* const axr = (si == 0 && own) ? AX + o_lane * N2 + sj + NI * sk
+                          : ((si == 1 && dx == 1 && bx < 3 && iy >= 1) ? XB + ((iy - 1) * 3 + bx) * N2 + sj + NI * sk : scr);
+      double* const ayr = (sj == 0 && own) ? AY + o_lane * N2 + si + NI * sk
+                          : ((sj == 1 && dy == 1 && by < L6T::NYB && ix >= 1) ? YB + (by * OX + ix - 1) * N2 + si + NI * sk
+                                                                                : scr);
       double zin[M][M], qz[M][M];
 #pragma unroll
       for (int ii = 0; ii < M; ++ii)
@@ -1144,16 +700,11 @@ __global__ void __launch_bounds__(NT, 2) k_apply_v6(const __grid_constant__ V5Pa
           qz[ii][jj] = 0.0;
         }
       double en = 0.0;
-      // accumulator rows of this lane's stores (scratch for the lanes / entries that own nothing)
-      double* const axr = (si == 0 && own) ? AX + o_lane * N2 + sj + NI * sk
-                          : ((si == 1 && dx == 1 && bx < 3 && iy >= 1) ? XB + ((iy - 1) * 3 + bx) * N2 + sj + NI * sk : scr);
-      double* const ayr = (sj == 0 && own) ? AY + o_lane * N2 + si + NI * sk
-                          : ((sj == 1 && dy == 1 && by == 0 && ix >= 1) ? YB + (ix - 1) * N2 + si + NI * sk : scr);
 #pragma unroll
       for (int kk = 0; kk < M; ++kk) {
         const double c3 = ct[L6T::CT_C + 16 + sk + 2 * kk];
         const double zx = fma(gj, znx[2 * kk], zsx[2 * kk]);      // x primaries: Zs + s_j Zn at k
-        const double zy = fma(gi, zwy[NI + 2 * kk], zwy[2 * kk]); // y primaries: Zw + s_i Ze at k
+        const double zy = fma(gi, zsx[NI + 2 * kk], zsx[2 * kk]); // y primaries: Zw + s_i Ze at k
         double yin[M], qy[M];
 #pragma unroll
         for (int ii = 0; ii < M; ++ii) {
@@ -1251,22 +802,23 @@ __global__ void __launch_bounds__(NT, 2) k_apply_v6(const __grid_constant__ V5Pa
     __syncthreads();   // accumulators final; every input row of step l dead
     if (l + 1 <= lend && l + 1 < nz) {
       if (tid < NROWS) {
-        if (tid < NSIDE) rofs[(l + 1) & 1][tid] = row_off<NI, 4>(rows[tid], tid, l + 1);
-        else rofs[(l + 2) & 1][tid] = row_off<NI, 4>(rows[tid], tid, l + 2);
+        if (tid < NSIDE) rofs[(l + 1) & 1][tid] = row_off<NI, H>(rows[tid], tid, l + 1);
+        else rofs[(l + 2) & 1][tid] = row_off<NI, H>(rows[tid], tid, l + 2);
       }
       fence_proxy_async();
-      if (warp == 0) issue_step<NI, 4>(P, sm, rows, true, l + 1, false, 0, false, true, l + 2, zdir(g, l + 2), &mbar);
+      if (warp == 0) issue_step<NI, H>(P, sm, rows, true, l + 1, false, 0, false, true, l + 2, zdir(g, l + 2), &mbar);
       pending = true;
     }
-    // cross-block parts: x-faces jx = 2, 4, 6 of rows 1..3 (XB), y-faces of row 2 (YB)
+    // cross-block parts: x-faces jx = 2, 4, 6 of rows >= 1 (XB), y-faces of rows jy = 2, 4, .. (YB)
     if (lay && fin_l) {
-      for (int t = tid; t < (OY * 3 + OX) * N2; t += NT) {
+      for (int t = tid; t < (OY * 3 + L6T::NYB * OX) * N2; t += NT) {
         const int f = t / N2, ent = t - f * N2;
         if (f < OY * 3) {
           const int oy = f / 3, jx = 2 * (f - oy * 3) + 2;
           AX[(oy * OX + jx - 1) * N2 + ent] += XB[t];
         } else {
-          AY[(1 * OX + (f - OY * 3)) * N2 + ent] += YB[t - OY * 3 * N2];
+          const int q = f - OY * 3, b = q / OX, jx = q - b * OX + 1, jy = 2 * b + 2;
+          AY[((jy - 1) * OX + jx - 1) * N2 + ent] += YB[t - OY * 3 * N2];
         }
       }
     }
@@ -1320,18 +872,18 @@ __global__ void __launch_bounds__(NT, 2) k_apply_v6(const __grid_constant__ V5Pa
 
 }  // namespace v5
 
-bool v5_supported(int ni) { return ni >= 2 && ni <= 7; }
+bool v6_supported(int ni) { return ni >= 2 && ni <= 7; }
 
 // tiles own 7 x 3 elements; the entity index ranges fx in [0, nx], fy in [0, ny] are covered
-void v5_tiles(int nx, int ny, int* ntx, int* nty) {
+void v6_tiles(int nx, int ny, int h, int* ntx, int* nty) {
   *ntx = (nx + 1 + v5::OX - 1) / v5::OX;
-  *nty = (ny + 1 + v5::OY - 1) / v5::OY;
+  *nty = (ny + 1 + (h - 1) - 1) / (h - 1);
 }
 
 // z-segments: ntiles columns of nz layers on nsm SMs x 2 CTAs; a segment above the first recomputes
 // the layer below its first plane, so more segments cost compute: pick the count that minimises
 // (waves rounded up) x (layers + 1) per column
-void v5_segments(int ntiles, int nz, int nslots, int* nseg, int* zseg) {
+void v6_segments(int ntiles, int nz, int nslots, int* nseg, int* zseg) {
   double best = 1e300;
   int bs = 1;
   for (int s = 1; s <= nz && s <= 64; ++s) {
@@ -1347,7 +899,7 @@ void v5_segments(int ntiles, int nz, int nslots, int* nseg, int* zseg) {
   *nseg = (nz + zs - 1) / zs;
 }
 
-void v5_make_coef(int ni, const double* d, const double* a0, const double* lam, double K00, double K0p, double w0,
+void v6_make_coef(int ni, const double* d, const double* a0, const double* lam, double K00, double K0p, double w0,
                   std::vector<unsigned char>& out) {
   V5Coef c;
   memset(&c, 0, sizeof(c));
@@ -1391,26 +943,22 @@ void v5_make_coef(int ni, const double* d, const double* a0, const double* lam, 
   memcpy(out.data(), &c, sizeof(c));
 }
 
-template <int NI, bool DOT>
-static int launch_v5_t(const V5Params& P, cudaStream_t st, int* nl, int kern) {
-  const size_t smem = sizeof(double) * (kern == 6 ? v5::L6<NI>::TOTAL : v5::L<NI>::TOTAL);
-  static bool attr[2][kMaxDev];
+template <int NI, bool DOT, int H>
+static int launch_v6_t(const V5Params& P, cudaStream_t st, int* nl) {
+  const size_t smem = sizeof(double) * v5::L6<NI, H>::TOTAL;
+  static bool attr[kMaxDev];
   const int dv = dev_slot();
-  if (!attr[kern == 6][dv]) {
-    if (kern == 6)
-      cudaFuncSetAttribute(v5::k_apply_v6<NI, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    else
-      cudaFuncSetAttribute(v5::k_apply_v5<NI, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr[kern == 6][dv] = true;
+  if (!attr[dv]) {
+    cudaFuncSetAttribute(v5::k_apply_v6<NI, DOT, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr[dv] = true;
   }
-  if (kern == 6) v5::k_apply_v6<NI, DOT><<<P.nitems, v5::NT, smem, st>>>(P);
-  else v5::k_apply_v5<NI, DOT><<<P.nitems, v5::NT, smem, st>>>(P);
+  v5::k_apply_v6<NI, DOT, H><<<P.nitems, 64 * H, smem, st>>>(P);
   (*nl)++;
   return cudaGetLastError();
 }
 
-int launch_apply_v5(const Geom& g, const double* x, double* y, const double* done, int ntx, int nty, int nseg,
-                    int zseg, const void* coef, double* dotp, void* stream, int* nl, void* events, int kern) {
+int launch_apply_v6(const Geom& g, const double* x, double* y, const double* done, int ntx, int nty, int nseg,
+                    int zseg, const void* coef, double* dotp, void* stream, int* nl, void* events, int h) {
   cudaStream_t st = (cudaStream_t)stream;
   cudaEvent_t* ev = (cudaEvent_t*)events;
   V5Params P;
@@ -1422,7 +970,10 @@ int launch_apply_v5(const Geom& g, const double* x, double* y, const double* don
   const bool dot = dotp != nullptr;
   switch (g.ni) {
 #define SC_V5_CASE(N) \
-    case N: e = dot ? launch_v5_t<N, true>(P, st, nl, kern) : launch_v5_t<N, false>(P, st, nl, kern); break;
+    case N:                                                                                     \
+      if (h == 8) e = dot ? launch_v6_t<N, true, 8>(P, st, nl) : launch_v6_t<N, false, 8>(P, st, nl); \
+      else e = dot ? launch_v6_t<N, true, 4>(P, st, nl) : launch_v6_t<N, false, 4>(P, st, nl);           \
+      break;
     SC_V5_CASE(2) SC_V5_CASE(3) SC_V5_CASE(4) SC_V5_CASE(5) SC_V5_CASE(6) SC_V5_CASE(7)
 #undef SC_V5_CASE
     default: return (int)cudaErrorInvalidValue;

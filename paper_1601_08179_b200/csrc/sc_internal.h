@@ -157,14 +157,15 @@ int launch_apply_rw(const Geom& g, const double* x, double* y, const double* don
 // p = 2 operator (uniform geometry): warp = 32 consecutive elements of an x-row, colour-scheduled
 int launch_apply_p2(const Geom& g, const double* x, double* y, const double* done, const void* coef, void* stream,
                     int* nlaunch, void* events);
-// v5 operator (2 <= n_I <= 7, uniform geometry): tile columns with a recomputed halo (kernels_v5.cu)
-bool v5_supported(int ni);
-void v5_tiles(int nx, int ny, int* ntx, int* nty);
-void v5_segments(int ntiles, int nz, int nslots, int* nseg, int* zseg);
-void v5_make_coef(int ni, const double* d, const double* a0, const double* lam, double K00, double K0p, double w0,
+// v6 operator (2 <= n_I <= 7, uniform geometry): tile columns with a recomputed halo, uniform class
+// lanes (kernels_v6.cu); h = compute-tile height (4: 8 x 4 elements, 2 CTAs per SM; 8: 8 x 8, 1 CTA)
+bool v6_supported(int ni);
+void v6_tiles(int nx, int ny, int h, int* ntx, int* nty);
+void v6_segments(int ntiles, int nz, int nslots, int* nseg, int* zseg);
+void v6_make_coef(int ni, const double* d, const double* a0, const double* lam, double K00, double K0p, double w0,
                   std::vector<unsigned char>& out);
-int launch_apply_v5(const Geom& g, const double* x, double* y, const double* done, int ntx, int nty, int nseg,
-                    int zseg, const void* coef, double* dotp, void* stream, int* nl, void* events, int kern);
+int launch_apply_v6(const Geom& g, const double* x, double* y, const double* done, int ntx, int nty, int nseg,
+                    int zseg, const void* coef, double* dotp, void* stream, int* nl, void* events, int h);
 // z-segments of the tile columns: ntiles columns of nz layers on nsm persistent CTAs
 void col_choose_segments(int ntiles, int nz, int nsm, int* nseg, int* zseg);
 int col_slots();   // step slots of the parked look-back partials (look-back distance + 1)
