@@ -210,7 +210,19 @@ sc_status sc_nccl_unique_id(unsigned char h_id[128]);
 sc_status sc_nccl_comm_init(const unsigned char h_id[128], int nranks, int rank, int device, void** comm_out);
 sc_status sc_nccl_comm_destroy(void* comm);
 
-/* Operator kernel family this ctx runs: "v6" / "v5" (halo-recompute tile columns,
+/* In-process loopback group (tests): creates nranks communicator handles in comms_out[0..nranks-1]
+ * that stand in for NCCL communicators in sc_params.nccl_comm when the ranks are host threads
+ * of ONE process (one context and stream per thread, any device).  The halo exchange and the
+ * scalar all-reduce then move data with cudaMemcpyAsync between host barriers, summing the
+ * scalars in rank order -- every collective becomes a host synchronisation point, so this is
+ * for exercising the multi-rank path on one GPU, not for speed.  Every rank of the
+ * group must take part in each collective.  The caller owns the handles and frees them all at
+ * once with sc_loopback_comms_destroy after every context using them is destroyed.
+ * SC_EINVAL on nranks < 1, NULL pointers or handles not from one create call. */
+sc_status sc_loopback_comms_create(int nranks, void** comms_out);
+sc_status sc_loopback_comms_destroy(void** comms, int nranks);
+
+/* Operator kernel family this ctx runs: "v6" / "v6h8" (halo-recompute tile columns,
  * 3 <= p <= 8), "v3" (tile columns with look-back), "rw" / "p2" (row-warp kernels, p <= 4),
  * "v4" (colour-scheduled element CTAs, p >= 9), "v1" (one CTA per element, any geometry). */
 const char* sc_operator_kernel(const sc_ctx* ctx);

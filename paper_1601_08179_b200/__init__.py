@@ -9,11 +9,11 @@ from . import capi
 from .capi import SC_PERM, SC_PRIMAL, SC_DUAL, ScError
 
 __all__ = ["capi", "SC_PERM", "SC_PRIMAL", "SC_DUAL", "ScError", "Context", "context_for_grid",
-           "basis_1d_host", "layout_query"]
+           "basis_1d_host", "layout_query", "LoopbackGroup"]
 
 
 def __getattr__(name):
-    if name in ("Context", "context_for_grid", "basis_1d_host", "layout_query"):
+    if name in ("Context", "context_for_grid", "basis_1d_host", "layout_query", "LoopbackGroup"):
         from . import solver
         return getattr(solver, name)
     raise AttributeError(name)

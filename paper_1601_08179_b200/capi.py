@@ -72,6 +72,8 @@ SIGNATURES = {
     "sc_nccl_comm_init": ([ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)],
                           ctypes.c_int),
     "sc_nccl_comm_destroy": ([_P], ctypes.c_int),
+    "sc_loopback_comms_create": ([ctypes.c_int, ctypes.POINTER(_P)], ctypes.c_int),
+    "sc_loopback_comms_destroy": ([ctypes.POINTER(_P), ctypes.c_int], ctypes.c_int),
     "sc_launch_count": ([_P], ctypes.c_longlong),
     "sc_last_error": ([_P], ctypes.c_char_p),
     "sc_version": ([], ctypes.c_char_p),

@@ -6,6 +6,9 @@
 
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
+#include <mutex>
+#include <set>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -55,6 +58,43 @@ bool load_nccl() {
   g_nccl.loaded = true;
   return true;
 }
+// ---------------------------------------------------------------- loopback group
+// In-process stand-in for the NCCL communicator (sc_loopback_comms_create): G ranks are
+// host threads of one process, each with its own context and stream; the halo and the scalar
+// all-reduce move data with cudaMemcpyAsync (UVA, any device) between host barriers.  Test
+// infrastructure for the multi-rank path on one GPU -- every collective is a host sync point.
+struct LoopGroup {
+  int nranks = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long gen = 0;
+  std::vector<const double*> seg;        // [rank][side][q] published segment pointers
+  std::vector<const double*> val;        // [rank] published scalar pointers
+  bool broken = false;                   // a rank missed a barrier: every later collective fails
+  bool barrier() {                       // false after a 120 s timeout (a rank left the group)
+    std::unique_lock<std::mutex> lk(mu);
+    if (broken) return false;
+    long long g = gen;
+    if (++arrived == nranks) { arrived = 0; ++gen; cv.notify_all(); return true; }
+    if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return gen != g || broken; }) || broken) {
+      broken = true;
+      cv.notify_all();
+      return false;
+    }
+    return true;
+  }
+};
+struct LoopComm {
+  LoopGroup* grp;
+  int rank;
+};
+std::mutex g_loop_mu;
+std::set<const void*> g_loop_comms;      // live LoopComm handles (distinguishes them from ncclComm_t)
+bool is_loop_comm(const void* c) {
+  std::lock_guard<std::mutex> lk(g_loop_mu);
+  return c && g_loop_comms.count(c);
+}
 }  // namespace
 
 // ------------------------------------------------------------------ context
@@ -98,6 +138,7 @@ struct sc_ctx {
   long long seg_off[2][4], seg_len[4];  // bottom / top plane segments
   OwnMask own;
   ncclComm_t comm = nullptr;
+  LoopComm* loop = nullptr;             // in-process loopback group instead of NCCL (tests)
   long long nlaunch = 0;
   double* x_cur = nullptr;              // PCG iterate between sc_pcg_start / sc_pcg_iterate
   // CUDA graph of kPcgChunk PCG iterations (single GPU, no kernel profiling), captured for the
@@ -421,7 +462,10 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
     ctx->own.n = 4;
     for (int q = 0; q < 4; ++q) { ctx->own.lo[q] = ctx->seg_off[0][q]; ctx->own.hi[q] = ctx->seg_off[0][q] + lens[q]; }
   }
-  if (R > 1) {
+  if (R > 1 && is_loop_comm(prm->nccl_comm)) {
+    ctx->loop = (LoopComm*)prm->nccl_comm;
+    if (ctx->loop->rank != r || ctx->loop->grp->nranks != R) { sc_destroy(ctx); return SC_EINVAL; }
+  } else if (R > 1) {
     if (!load_nccl()) { ctx->err = "libnccl.so.2 not loadable"; sc_destroy(ctx); return SC_ENCCL; }
     ctx->comm = (ncclComm_t)prm->nccl_comm;
   }
@@ -574,11 +618,33 @@ extern "C" sc_status sc_basis_1d_host(int p, double* lam, double* a0, double* ap
 // exchange them with the z-neighbours and add (P:107-109 gather across the slab cut).
 static sc_status halo_sum(sc_ctx* ctx, double* y, cudaStream_t st) {
   const int R = ctx->prm.nranks, r = ctx->prm.rank;
-  if (R == 1 || !ctx->comm) return SC_OK;   // no communicator: SC_TEST_LOCAL_SLAB (local partials)
+  if (R == 1 || (!ctx->comm && !ctx->loop)) return SC_OK;   // SC_TEST_LOCAL_SLAB: local partials
   if (!ctx->halo) { ctx->err = "workspace not bound (needed for the halo exchange)"; return SC_ESTATE; }
   const long long pl = align_up(ctx->plane_len);
   double* recv_lo = ctx->halo;
   double* recv_hi = ctx->halo + pl;
+  if (ctx->loop) {
+    // loopback: publish this rank's plane segments, copy the neighbours' once every rank's
+    // partials are complete, and add only after every rank has copied.
+    LoopGroup* G = ctx->loop->grp;
+    CK(cudaStreamSynchronize(st));
+    for (int side = 0; side < 2; ++side)
+      for (int q = 0; q < 4; ++q) G->seg[(r * 2 + side) * 4 + q] = y + ctx->seg_off[side][q];
+    if (!G->barrier()) { ctx->err = "loopback barrier timed out"; return SC_ESTATE; }
+    for (int side = 0; side < 2; ++side) {
+      int peer = side == 0 ? r - 1 : r + 1;
+      if (peer < 0 || peer >= R) continue;
+      double* rb = side == 0 ? recv_lo : recv_hi;
+      long long o = 0;
+      for (int q = 0; q < 4; ++q) {
+        CK(cudaMemcpyAsync(rb + o, G->seg[(peer * 2 + (1 - side)) * 4 + q], sizeof(double) * ctx->seg_len[q],
+                           cudaMemcpyDefault, st));
+        o += ctx->seg_len[q];
+      }
+    }
+    CK(cudaStreamSynchronize(st));
+    if (!G->barrier()) { ctx->err = "loopback barrier timed out"; return SC_ESTATE; }
+  } else {
   NK(g_nccl.GroupStart());
   for (int side = 0; side < 2; ++side) {
     int peer = side == 0 ? r - 1 : r + 1;
@@ -592,13 +658,32 @@ static sc_status halo_sum(sc_ctx* ctx, double* y, cudaStream_t st) {
     }
   }
   NK(g_nccl.GroupEnd());
+  }
   if (r > 0) LAUNCH(launch_add_segments(y, recv_lo, ctx->seg_off[0], ctx->seg_len, 4, st, &nl_));
   if (r < R - 1) LAUNCH(launch_add_segments(y, recv_hi, ctx->seg_off[1], ctx->seg_len, 4, st, &nl_));
   return SC_OK;
 }
 
 static sc_status allreduce_scal(sc_ctx* ctx, int slot, int n, cudaStream_t st) {
-  if (ctx->prm.nranks == 1 || !ctx->comm) return SC_OK;
+  if (ctx->prm.nranks == 1 || (!ctx->comm && !ctx->loop)) return SC_OK;
+  if (ctx->loop) {
+    // loopback: every rank sums the published values in rank order (identical on all ranks)
+    LoopGroup* G = ctx->loop->grp;
+    const int R = ctx->prm.nranks;
+    double sum[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tmp[8];
+    if (n > 8) return SC_EINVAL;
+    CK(cudaStreamSynchronize(st));
+    G->val[ctx->prm.rank] = ctx->scal + slot;
+    if (!G->barrier()) { ctx->err = "loopback barrier timed out"; return SC_ESTATE; }
+    for (int q = 0; q < R; ++q) {
+      CK(cudaMemcpy(tmp, G->val[q], sizeof(double) * n, cudaMemcpyDefault));
+      for (int i = 0; i < n; ++i) sum[i] += tmp[i];
+    }
+    if (!G->barrier()) { ctx->err = "loopback barrier timed out"; return SC_ESTATE; }
+    CK(cudaMemcpyAsync(ctx->scal + slot, sum, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    return SC_OK;
+  }
   NK(g_nccl.AllReduce(ctx->scal + slot, ctx->scal + slot, (size_t)n, ncclDouble, ncclSum, ctx->comm, st));
   return SC_OK;
 }
@@ -984,6 +1069,36 @@ extern "C" sc_status sc_nccl_comm_destroy(void* comm) {
   if (!comm) return SC_OK;
   if (!load_nccl()) return SC_ENCCL;
   return g_nccl.CommDestroy((ncclComm_t)comm) == ncclSuccess ? SC_OK : SC_ENCCL;
+}
+
+extern "C" sc_status sc_loopback_comms_create(int nranks, void** comms_out) {
+  if (nranks < 1 || !comms_out) return SC_EINVAL;
+  LoopGroup* G = new LoopGroup;
+  G->nranks = nranks;
+  G->seg.assign((size_t)nranks * 8, nullptr);
+  G->val.assign((size_t)nranks, nullptr);
+  std::lock_guard<std::mutex> lk(g_loop_mu);
+  for (int r = 0; r < nranks; ++r) {
+    LoopComm* c = new LoopComm{G, r};
+    g_loop_comms.insert(c);
+    comms_out[r] = c;
+  }
+  return SC_OK;
+}
+
+extern "C" sc_status sc_loopback_comms_destroy(void** comms, int nranks) {
+  if (!comms || nranks < 1) return SC_EINVAL;
+  std::lock_guard<std::mutex> lk(g_loop_mu);
+  LoopGroup* G = nullptr;
+  for (int r = 0; r < nranks; ++r) {
+    if (!comms[r] || !g_loop_comms.count(comms[r])) return SC_EINVAL;
+    LoopComm* c = (LoopComm*)comms[r];
+    G = c->grp;
+    g_loop_comms.erase(c);
+    delete c;
+  }
+  delete G;
+  return SC_OK;
 }
 
 extern "C" long long sc_launch_count(const sc_ctx* ctx) { return ctx ? ctx->nlaunch : 0; }

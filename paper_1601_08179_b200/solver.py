@@ -218,6 +218,26 @@ class Context:
             pass
 
 
+class LoopbackGroup:
+    """sc_loopback_comms_create: nranks in-process communicator handles for ranks that are host
+    threads of this process (tests of the multi-rank path on one GPU).  comms[r] goes into
+    Context(..., nccl_comm=comms[r], rank=r, nranks=nranks)."""
+
+    def __init__(self, nranks):
+        self.lib = capi.load()
+        self.nranks = int(nranks)
+        self._arr = (ctypes.c_void_p * self.nranks)()
+        st = self.lib.sc_loopback_comms_create(self.nranks, self._arr)
+        if st != capi.SC_OK:
+            raise ScError("sc_loopback_comms_create", st)
+        self.comms = [ctypes.c_void_p(self._arr[r]) for r in range(self.nranks)]
+
+    def close(self):
+        if self._arr is not None:
+            self.lib.sc_loopback_comms_destroy(self._arr, self.nranks)
+            self._arr = None
+
+
 def context_for_grid(grid, device=0, **kw):
     """Context from a synth.Grid (p, ne, hx, hy, hz, lam)."""
     return Context(grid.p, grid.ne, (grid.hx, grid.hy, grid.hz), grid.lam, device=device, **kw)

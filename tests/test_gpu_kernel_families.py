@@ -1,0 +1,131 @@
+"""Every p <= 8 operator family against the oracle, each selected explicitly (SC_OP) and checked to be
+the one that ran (sc_operator_kernel): v6 (halo-recompute tile columns, uniform class lanes, both
+tile heights), v3 (tile columns with look-back), rw (row-warp p = 3, 4).  Multi-tile ragged grids,
+z-segments, z-slab ranks, PCG with the fused p . q partials, bitwise repeatability."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import operator, pcg, solve
+from synth import small_grid, lattice_random
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import __graft_entry__
+    __graft_entry__.build()
+    assert torch.cuda.is_available()
+
+
+def _ctx(g, monkeypatch, op, h=None, **kw):
+    from paper_1601_08179_b200 import Context
+    monkeypatch.setenv("SC_OP", op)
+    if h is not None:
+        monkeypatch.setenv("SC_V6_H", str(h))
+    ctx = Context(g.p, g.ne, (g.hx, g.hy, g.hz), g.lam, device=0, **kw)
+    want = {"v6": "v6h8" if h == 8 else "v6", "v3": "v3", "rw": "rw"}[op]
+    assert ctx.operator_kernel() == want, (ctx.operator_kernel(), want)
+    return ctx
+
+
+def _apply_nodal(ctx, x_lat):
+    from paper_1601_08179_b200 import SC_PRIMAL, SC_DUAL
+    xt = ctx.skeleton()
+    ctx.sc_to_transformed(torch.from_numpy(np.ascontiguousarray(x_lat)).cuda(), xt, SC_PRIMAL)
+    yt = ctx.skeleton()
+    ctx.sc_apply_condensed(xt, yt)
+    y = ctx.lattice()
+    ctx.sc_from_transformed(yt, y, SC_DUAL)
+    return y.cpu().numpy()
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+CASES = [(3, (17, 9, 3), "rw", None), (3, (17, 9, 3), "v6", None), (4, (9, 8, 3), "rw", None),
+         (4, (9, 8, 3), "v6", None), (5, (15, 7, 3), "v6", None), (5, (15, 7, 3), "v3", None),
+         (6, (9, 10, 2), "v6", None), (7, (16, 4, 3), "v6", None), (7, (16, 4, 3), "v3", None),
+         (8, (9, 7, 3), "v6", None), (8, (9, 7, 3), "v3", None), (7, (8, 15, 2), "v6", 8),
+         (5, (15, 16, 2), "v6", 8)]
+
+
+@pytest.mark.parametrize("p,ne,op,h", CASES)
+def test_family_operator_parity(p, ne, op, h, monkeypatch):
+    g = small_grid(p, ne, 0.7, lengths=(1.2, 0.9, 0.6))
+    ref_op = operator.AssembledCondensedOperator(g)
+    x = lattice_random(90 + p, g.ne, g.p).ravel()
+    ctx = _ctx(g, monkeypatch, op, h)
+    assert _rel(_apply_nodal(ctx, x), ref_op.apply(x)) <= 1e-12
+
+
+@pytest.mark.parametrize("p,ne,op,h,zseg", [(6, (10, 5, 7), "v6", None, "3"), (7, (9, 8, 6), "v6", 8, "2"),
+                                             (8, (9, 4, 7), "v6", None, "4")])
+def test_family_zsegments(p, ne, op, h, zseg, monkeypatch):
+    monkeypatch.setenv("SC_ZSEG", zseg)
+    g = small_grid(p, ne, 0.5, lengths=(1.1, 0.8, 1.3))
+    ref_op = operator.AssembledCondensedOperator(g)
+    x = lattice_random(7, g.ne, g.p).ravel()
+    ctx = _ctx(g, monkeypatch, op, h)
+    assert _rel(_apply_nodal(ctx, x), ref_op.apply(x)) <= 1e-12
+
+
+@pytest.mark.parametrize("p,ne,op,h", [(5, (15, 7, 4), "v6", None), (8, (10, 6, 3), "v6", None),
+                                       (7, (9, 9, 3), "v6", 8), (8, (10, 6, 3), "v3", None)])
+def test_family_pcg_fused_dot(p, ne, op, h, monkeypatch):
+    """BT-PCG with p . q from the operator's per-CTA x . A x partials (the default)."""
+    from paper_1601_08179_b200 import SC_DUAL
+    g = small_grid(p, ne, 1.0, lengths=(1.3, 0.7, 0.5))
+    ref_op = operator.AssembledCondensedOperator(g)
+    ctx = _ctx(g, monkeypatch, op, h)
+    bt = ctx.skeleton()
+    ctx.sc_fill_random(8, bt)
+    lat = ctx.lattice()
+    ctx.sc_from_transformed(bt, lat, SC_DUAL)
+    b = lat.cpu().numpy()
+    P = solve.BlockJacobi(ref_op)
+    norm = solve.transformed_norm(g, ref_op.skel)
+    res = pcg.pcg(ref_op.apply, P.apply, b, rtol=1e-10, norm=norm)
+    xt = ctx.skeleton()
+    rep = ctx.sc_pcg_solve(bt, xt, rtol=1e-10, maxit=2000)
+    assert rep.converged and abs(rep.iters - res.iters) <= 1, (rep.iters, res.iters)
+    ref = res.x if rep.iters == res.iters else pcg.pcg(ref_op.apply, P.apply, b, rtol=0, norm=norm,
+                                                       fixed_iters=rep.iters).x
+    assert _rel(ctx.to_lattice_nodal(xt).cpu().numpy(), ref) <= 1e-10
+
+
+@pytest.mark.parametrize("p,ne,R,h", [(6, (9, 5, 5), 2, None), (7, (10, 7, 6), 3, None), (5, (9, 10, 5), 2, 8)])
+def test_family_v6_slab_ranks(p, ne, R, h, monkeypatch):
+    """z-slab ranks (SC_TEST_LOCAL_SLAB: local partial sums on the interface planes) against the
+    oracle's slab operator with non-Dirichlet interface planes."""
+    import copy
+    monkeypatch.setenv("SC_TEST_LOCAL_SLAB", "1")
+    g = small_grid(p, ne, 0.9, lengths=(1.2, 0.8, 1.1))
+    for r in range(R):
+        ctx = _ctx(g, monkeypatch, "v6", h, rank=r, nranks=R)
+        z0, z1 = ctx.layout.z_begin, ctx.layout.z_end
+        gs = copy.deepcopy(g)
+        gs.ne = (g.ne[0], g.ne[1], z1 - z0)
+        gs.hz = g.hz[z0:z1]
+        gs.extra = dict(g.extra, dirichlet_z=(r == 0, r == R - 1))
+        xg = lattice_random(70 + p, g.ne, g.p)
+        xs = np.ascontiguousarray(xg[z0 * p:z1 * p + 1])
+        ref = operator.AssembledCondensedOperator(gs).apply(xs.ravel())
+        assert _rel(_apply_nodal(ctx, xs.ravel()), ref) <= 1e-12, (r, z0, z1)
+
+
+@pytest.mark.parametrize("h", [None, 8])
+def test_family_v6_bitwise_repeatable(h, monkeypatch):
+    g = small_grid(7, (30, 13, 9), 1.0)
+    ctx = _ctx(g, monkeypatch, "v6", h)
+    x = ctx.skeleton()
+    ctx.sc_fill_random(3, x)
+    y0 = ctx.skeleton()
+    ctx.sc_apply_condensed(x, y0)
+    for _ in range(4):
+        y = ctx.skeleton(fill=float("nan"))
+        ctx.sc_apply_condensed(x, y)
+        torch.cuda.synchronize()
+        assert torch.equal(y, y0)

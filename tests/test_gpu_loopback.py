@@ -1,0 +1,175 @@
+"""Multi-rank path on one GPU: z-slab ranks as host threads of this process, joined by the
+library's in-process loopback group (sc_loopback_comms_create) in place of an NCCL
+communicator.  Every collective the multi-rank solver uses runs for real -- the interface-plane
+halo (P:107-109 gather across the slab cut, k_add_segments), the OwnMask dots and the scalar
+all-reduces of BT-PCG, the preconditioner's halo -- and the stitched global results are
+compared with the global oracle.  Only the transport differs from NCCL
+(cudaMemcpyAsync between host barriers).
+"""
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import operator, pcg, solve
+from synth import small_grid, lattice_random
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import __graft_entry__
+    __graft_entry__.build()
+    assert torch.cuda.is_available()
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def run_ranks(R, fn):
+    """fn(rank) on R host threads, each on its own CUDA stream; re-raises the first failure."""
+    out, err = [None] * R, [None] * R
+
+    def work(r):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                out[r] = fn(r)
+            s.synchronize()
+        except BaseException as e:  # noqa: BLE001 -- re-raised below
+            err[r] = e
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(R)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=900)
+        assert not t.is_alive(), "rank thread hung"
+    for e in err:
+        if e is not None:
+            raise e
+    return out
+
+
+def stitch(g, parts):
+    """Global nodal lattice from rank slabs (interface planes must agree on both ranks)."""
+    p = g.p
+    nz1 = g.ne[2] * p + 1
+    glob = np.full((nz1,) + parts[0]["shape"][1:], np.nan)
+    for d in parts:
+        z0, z1 = d["z"]
+        v = d["v"].reshape(d["shape"])
+        seen = ~np.isnan(glob[z0 * p:z1 * p + 1])
+        assert np.array_equal(glob[z0 * p:z1 * p + 1][seen], v[seen]), "interface planes differ across ranks"
+        glob[z0 * p:z1 * p + 1] = v
+    return glob.ravel()
+
+
+CASES = [(5, (10, 6, 6), 2, "v6"), (6, (9, 5, 7), 3, "v6"), (8, (9, 5, 5), 3, None), (3, (12, 7, 6), 3, None),
+         (2, (11, 6, 5), 2, None), (10, (3, 3, 4), 2, None)]
+
+
+@pytest.mark.parametrize("p,ne,R,kernel", CASES)
+def test_loopback_ranks_against_global_oracle(p, ne, R, kernel):
+    from paper_1601_08179_b200 import Context, LoopbackGroup, SC_PERM
+    g = small_grid(p, ne, 0.8, lengths=(1.1, 0.9, 1.3))
+    op = operator.AssembledCondensedOperator(g)
+    xg = lattice_random(40 + p, g.ne, g.p)
+    fg = lattice_random(60 + p, g.ne, g.p, skeleton_only=False, zero_dirichlet=False)
+    y_ref = op.apply(xg.ravel())
+    b_ref = solve.condensed_rhs(op, fg.ravel())
+    P = solve.BlockJacobi(op)
+    res = pcg.pcg(op.apply, P.apply, b_ref, rtol=1e-10, norm=solve.transformed_norm(g, op.skel))
+    grp = LoopbackGroup(R)
+
+    def rank(r):
+        ctx = Context(g.p, g.ne, (g.hx, g.hy, g.hz), g.lam, device=0, nccl_comm=grp.comms[r], rank=r, nranks=R)
+        try:
+            z0, z1 = ctx.layout.z_begin, ctx.layout.z_end
+            sl = lambda a: torch.from_numpy(np.ascontiguousarray(a[z0 * p:z1 * p + 1]).ravel()).cuda()
+            shape = (int((z1 - z0) * p + 1),) + xg.shape[1:]
+            part = lambda v: dict(z=(z0, z1), shape=shape, v=v.cpu().numpy())
+            xt = ctx.from_lattice_nodal(sl(xg))
+            yt = ctx.skeleton()
+            ctx.sc_apply_condensed(xt, yt)
+            energy = ctx.sc_dot(xt, yt)
+            pv = ctx.skeleton()
+            ctx.sc_preconditioner(pv)
+            pl = ctx.lattice()
+            ctx.sc_from_transformed(pv, pl, SC_PERM)
+            f = sl(fg)
+            bt = ctx.skeleton()
+            ctx.sc_condense_rhs(f, bt)
+            x = ctx.skeleton()
+            rep = ctx.sc_pcg_solve(bt, x, rtol=1e-10, maxit=2000)
+            u = ctx.lattice()
+            ctx.sc_recover(f, x, u)
+            return dict(kernel=ctx.operator_kernel(), y=part(ctx.to_lattice_nodal(yt, dual=True)), energy=energy,
+                        pinv=part(pl), b=part(ctx.to_lattice_nodal(bt, dual=True)), x=part(ctx.to_lattice_nodal(x)),
+                        u=part(u), iters=rep.iters, conv=rep.converged, relres=rep.relres)
+        finally:
+            ctx.close()
+
+    try:
+        out = run_ranks(R, rank)
+    finally:
+        grp.close()
+    if kernel:
+        assert all(o["kernel"].startswith(kernel) for o in out), [o["kernel"] for o in out]
+    # halo-summed operator, condensed right-hand side
+    assert _rel(stitch(g, [o["y"] for o in out]), y_ref) <= 1e-12
+    assert _rel(stitch(g, [o["b"] for o in out]), b_ref) <= 1e-12
+    # OwnMask dot + all-reduce: x . Ax, identical on every rank (rank-ordered sum)
+    e_ref = float(xg.ravel() @ y_ref)
+    assert len({o["energy"] for o in out}) == 1
+    assert abs(out[0]["energy"] - e_ref) <= 1e-12 * abs(e_ref)
+    # preconditioner halo: stitched Pinv is the single-context one
+    ctx1 = Context(g.p, g.ne, (g.hx, g.hy, g.hz), g.lam, device=0)
+    pv1 = ctx1.skeleton()
+    ctx1.sc_preconditioner(pv1)
+    pl1 = ctx1.lattice()
+    ctx1.sc_from_transformed(pv1, pl1, SC_PERM)
+    assert _rel(stitch(g, [o["pinv"] for o in out]), pl1.cpu().numpy()) <= 1e-13
+    ctx1.close()
+    # BT-PCG: same decisions on every rank, iterations and solution against the oracle
+    assert len({(o["iters"], o["conv"], o["relres"]) for o in out}) == 1
+    assert out[0]["conv"] and abs(out[0]["iters"] - res.iters) <= 1, (out[0]["iters"], res.iters)
+    it = out[0]["iters"]
+    ref = res.x if it == res.iters else pcg.pcg(op.apply, P.apply, b_ref, rtol=0,
+                                               norm=solve.transformed_norm(g, op.skel), fixed_iters=it).x
+    assert _rel(stitch(g, [o["x"] for o in out]), ref) <= 1e-10
+    u_ref = solve.recover(op, fg.ravel(), ref)
+    assert _rel(stitch(g, [o["u"] for o in out]), u_ref) <= 1e-10
+
+
+def test_loopback_pcg_graph_free_and_repeatable():
+    """Two solves on the same ranks give bitwise-identical iterates (the loopback sums in rank
+    order, every kernel assembles in a fixed order)."""
+    from paper_1601_08179_b200 import Context, LoopbackGroup
+    g = small_grid(6, (9, 6, 6), 1.0)
+    R = 2
+    grp = LoopbackGroup(R)
+
+    def rank(r):
+        ctx = Context(g.p, g.ne, (g.hx, g.hy, g.hz), g.lam, device=0, nccl_comm=grp.comms[r], rank=r, nranks=R)
+        try:
+            b = ctx.skeleton()
+            ctx.sc_fill_random(11, b)
+            xs = []
+            for _ in range(2):
+                x = ctx.skeleton()
+                rep = ctx.sc_pcg_solve(b, x, rtol=1e-9, maxit=500)
+                xs.append((rep.iters, x.cpu()))
+            return xs
+        finally:
+            ctx.close()
+
+    try:
+        out = run_ranks(R, rank)
+    finally:
+        grp.close()
+    for xs in out:
+        assert xs[0][0] == xs[1][0] and torch.equal(xs[0][1], xs[1][1])

@@ -353,9 +353,10 @@ def test_pcg_parity_zsegments(nseg, fused, monkeypatch):
     from paper_1601_08179_b200 import SC_DUAL
     monkeypatch.setenv("SC_ZSEG", nseg)
     monkeypatch.setenv("SC_FUSED_DOT", fused)
-    g = small_grid(4, (10, 6, 8), 1.0, lengths=(1.3, 0.7, 1.5))
+    g = small_grid(6, (10, 6, 8), 1.0, lengths=(1.3, 0.7, 1.5))   # p = 6: a tile-column kernel (v6)
     op = operator.AssembledCondensedOperator(g)
     ctx = ctx_for(g)
+    assert ctx.operator_kernel() in ("v6", "v3")
     bt = ctx.skeleton()
     ctx.sc_fill_random(9, bt)
     lat = ctx.lattice()
