@@ -551,11 +551,17 @@ extern "C" sc_status sc_bind_workspace(sc_ctx* ctx, void* d_ws, size_t bytes) {
   // Dirichlet, where r = 0)
   ctx->use_ptab = false;
   const char* pv_env = getenv("SC_PINV_VECTOR");
-  if (ctx->g.uniform && !(pv_env && pv_env[0] == '1')) {
+  // Multi-rank: the representative is a slab-interior z-plane (1..nz-1) on every rank, so all
+  // ranks hold bitwise the same table (an interface plane's halo-summed value is rounded in a
+  // different order than an interior plane's) and the replicated interface entries of z and p
+  // stay identical across ranks; that needs every slab >= 2 element layers thick.
+  const bool multi = ctx->prm.nranks > 1;
+  if (ctx->g.uniform && !(pv_env && pv_env[0] == '1') && (!multi || ctx->prm.ne[2] / ctx->prm.nranks >= 2)) {
     const Geom& g = ctx->g;
     const int ni = g.ni, n2 = ni * ni, nx = g.nx, ny = g.ny, nz = g.nz;
-    int fzf = -1;                                   // a non-Dirichlet z-plane
-    for (int fz = 0; fz <= nz && fzf < 0; ++fz)
+    int fzf = -1;                                   // a non-Dirichlet z-plane, slab-interior first
+    for (int fz = 1; fz < nz && fzf < 0; ++fz) fzf = fz;
+    for (int fz = 0; fz <= nz && fzf < 0 && !multi; ++fz)
       if (!((fz == 0 && g.dir_bot) || (fz == nz && g.dir_top))) fzf = fz;
     const bool ix = nx >= 2, iy = ny >= 2;
     PinvTab& T = ctx->ptab;
