@@ -698,6 +698,34 @@ def test_pcg_parity_anisotropic_16cubed(ar, expect):
     assert norm(r) <= 1e-9 * norm(b)
 
 
+# ---- E4: the alpha = 1 case of E3 at p = 16 for growing n_e (the small sizes) --------
+@pytest.mark.parametrize("n", [2, 4])
+def test_e4_p16_pipeline_parity(n):
+    """SURVEY §8 f4 at the sizes the oracle finishes: p = 16, n_e = n^3, uniform (alpha = 1) mesh
+    of (0, 2 pi)^3, Eq. eq:solution with k = 5, lambda = 0, inhomogeneous Dirichlet data, rtol
+    1e-12 -- condense, BT-PCG and recover against the oracle."""
+    from synth import e3_grid, e3_u, e3_f
+    g = e3_grid(16, 1.0, n=n)
+    X, Y, Z = mesh.lattice_coordinates(g)
+    f = e3_f(X, Y, Z, 0.0, k=5.0)
+    gv = e3_u(X, Y, Z, k=5.0)
+    op = operator.AssembledCondensedOperator(g)
+    b = solve.dirichlet_rhs(op, f, gv)
+    res = _oracle_pcg(g, op, b, 1e-12)
+    ctx = ctx_for(g)
+    f_d, g_d = torch.from_numpy(f).cuda(), torch.from_numpy(gv).cuda()
+    bt = ctx.skeleton()
+    ctx.sc_condense_rhs_dirichlet(f_d, g_d, bt)
+    xt = ctx.skeleton()
+    rep = ctx.sc_pcg_solve(bt, xt, rtol=1e-12, maxit=3000)
+    assert rep.converged and abs(rep.iters - res.iters) <= 1, (rep.iters, res.iters)
+    ref = res.x if rep.iters == res.iters else _oracle_pcg(g, op, b, 0, fixed=rep.iters).x
+    assert rel(ctx.to_lattice_nodal(xt).cpu().numpy(), ref) <= 1e-10
+    u = ctx.lattice()
+    ctx.sc_recover_dirichlet(f_d, g_d, xt, u)
+    assert rel(u.cpu().numpy(), solve.recover(op, f, ref, dirichlet=gv)) <= 1e-10
+
+
 # ---- the paper's solver workload E3 (P:625-687): graded grids, Eq. eq:solution, Dirichlet data --
 @pytest.mark.parametrize("p,alpha,n", [(4, 2.0, 3), (6, 1.5, 3), (9, 2.0, 2), (12, 1.5, 2)])
 def test_e3_dirichlet_pipeline_parity(p, alpha, n):
