@@ -222,6 +222,31 @@ sc_status sc_nccl_comm_destroy(void* comm);
 sc_status sc_loopback_comms_create(int nranks, void** comms_out);
 sc_status sc_loopback_comms_destroy(void** comms, int nranks);
 
+/* ---- Operator variants of the paper's operator comparison (§7 "Efficiency of operators",
+ * P:493-504, Table 3), in the NODAL GLL basis:  d_y = Rhat Hhat Rhat^T d_x  with the element
+ * Schur complement Hhat_e = H_BB - H_BI H_II^{-1} H_IB.  d_x, d_y: skeleton vectors in
+ * the entity layout of sc_layout (nodal values, no basis change); Dirichlet entries ignored on input
+ * and written as 0; multi-GPU halo exchange as in sc_apply_condensed.  Results equal those of the
+ * transformed operator converted to the nodal basis, up to rounding.
+ *
+ * sc_apply_tpc -- variant TPC: Alg. 3 (`alg:face_to_eigenspace`) with the
+ *   Table 1 tensor-product suboperators, 37 n_I^3 multiplications for the condensed part plus the
+ *   nodal primary part (12 n_I^3, Eqs. eq:east_east_primary_part / eq:east_west_primary_part); one
+ *   CTA per element, assembly by fp64 atomics into d_y (zeroed first).  Any geometry.
+ * sc_mmc_bytes / sc_mmc_bind / sc_apply_mmc -- variant MMC (Alg. 2 `alg:face_to_face`):
+ *   sc_mmc_bind precomputes the element matrix Hhat_e (all 6 n_I^2 + 12 n_I + 8 shell nodes; one
+ *   matrix for a uniform grid, one per element otherwise: the paper's memory argument) into
+ *   the caller-owned device buffer d_buf of at least sc_mmc_bytes(ctx) bytes (SC_ENOMEM if smaller:
+ *   the memory guard), synchronously; the buffer also holds the gathered element shells.  The buffer
+ *   must stay valid while sc_apply_mmc is used; re-binding replaces it.  sc_apply_mmc gathers every
+ *   element's shell (R^T), applies all elements with ONE cuBLAS DGEMM (a strided batch for
+ *   per-element matrices) and assembles (R) entity by entity in a fixed order (deterministic).
+ *   SC_ESTATE if sc_mmc_bind was not called; SC_ECUDA if libcublas.so.12 cannot be loaded. */
+sc_status sc_apply_tpc(sc_ctx* ctx, const double* d_x, double* d_y, void* stream);
+size_t sc_mmc_bytes(const sc_ctx* ctx);
+sc_status sc_mmc_bind(sc_ctx* ctx, void* d_buf, size_t bytes, void* stream);
+sc_status sc_apply_mmc(sc_ctx* ctx, const double* d_x, double* d_y, void* stream);
+
 /* Operator kernel family this ctx runs: "v6" / "v6h8" (halo-recompute tile columns,
  * 3 <= p <= 8), "v3" (tile columns with look-back), "rw" / "p2" (row-warp kernels, p <= 4),
  * "v4" (colour-scheduled element CTAs, p >= 9), "v1" (one CTA per element, any geometry). */

@@ -74,6 +74,10 @@ SIGNATURES = {
     "sc_nccl_comm_destroy": ([_P], ctypes.c_int),
     "sc_loopback_comms_create": ([ctypes.c_int, ctypes.POINTER(_P)], ctypes.c_int),
     "sc_loopback_comms_destroy": ([ctypes.POINTER(_P), ctypes.c_int], ctypes.c_int),
+    "sc_apply_tpc": ([_P, _P, _P, _P], ctypes.c_int),
+    "sc_mmc_bytes": ([_P], ctypes.c_size_t),
+    "sc_mmc_bind": ([_P, _P, ctypes.c_size_t, _P], ctypes.c_int),
+    "sc_apply_mmc": ([_P, _P, _P, _P], ctypes.c_int),
     "sc_launch_count": ([_P], ctypes.c_longlong),
     "sc_last_error": ([_P], ctypes.c_char_p),
     "sc_version": ([], ctypes.c_char_p),

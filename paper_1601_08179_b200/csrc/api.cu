@@ -97,6 +97,46 @@ bool is_loop_comm(const void* c) {
 }
 }  // namespace
 
+// ------------------------------------------------------------------ cuBLAS (dlopen)
+// MMC's "single call to DGEMM" is a plain library GEMM: cuBLAS, loaded at run time
+// (the copy torch already mapped if present), so the library does not link against one cuBLAS build.
+namespace {
+struct CublasApi {
+  bool tried = false, loaded = false;
+  int (*Create)(void**) = nullptr;
+  int (*Destroy)(void*) = nullptr;
+  int (*SetStream)(void*, cudaStream_t) = nullptr;
+  int (*Dgemm)(void*, int, int, int, int, int, const double*, const double*, int, const double*, int,
+               const double*, double*, int) = nullptr;
+  int (*DgemmStridedBatched)(void*, int, int, int, int, int, const double*, const double*, int, long long,
+                             const double*, int, long long, const double*, double*, int, long long, int) = nullptr;
+};
+CublasApi g_cublas;
+std::mutex g_cublas_mu;
+
+bool load_cublas() {
+  std::lock_guard<std::mutex> lk(g_cublas_mu);
+  if (g_cublas.tried) return g_cublas.loaded;
+  g_cublas.tried = true;
+  void* h = dlopen("libcublas.so.12", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+  if (!h) h = dlopen("libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("/usr/local/cuda/lib64/libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return false;
+#define SYM(name, field) g_cublas.field = (decltype(g_cublas.field))dlsym(h, name); if (!g_cublas.field) return false;
+  SYM("cublasCreate_v2", Create)
+  SYM("cublasDestroy_v2", Destroy)
+  SYM("cublasSetStream_v2", SetStream)
+  SYM("cublasDgemm_v2", Dgemm)
+  SYM("cublasDgemmStridedBatched", DgemmStridedBatched)
+#undef SYM
+  g_cublas.loaded = true;
+  return true;
+}
+void cublas_destroy(void* h) {
+  if (h && g_cublas.loaded) g_cublas.Destroy(h);
+}
+}  // namespace
+
 // ------------------------------------------------------------------ context
 struct sc_ctx {
   sc_params prm;
@@ -152,6 +192,14 @@ struct sc_ctx {
   bool prof_on = false;
   std::vector<cudaEvent_t> prof_ev;     // pairs (start, stop)
   int prof_n = 0;
+  // nodal-basis operator variants of PAPER.md §7 (kernels_var.cu): TPC and MMC
+  double* d_vt = nullptr;               // VT_* tables (S M, a0, ap, Lambda, nodal K, w)
+  double* mmc_H = nullptr;              // caller-owned buffer: element matrices | X | Y
+  double* mmc_X = nullptr;
+  double* mmc_Y = nullptr;
+  long long mmc_ngeom = 0;              // 1 (uniform geometry) or n_e (one matrix per element)
+  int mmc_nB = 0;                       // shell nodes per element, 6 n_I^2 + 12 n_I + 8
+  void* cublas = nullptr;               // cublasHandle_t (libcublas.so.12 loaded at run time)
   std::string err;
   bool broken = false;
 };
@@ -328,6 +376,22 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
   if (cudaMalloc(&ctx->d_tab, sizeof(double) * TAB_SIZE) != cudaSuccess) return fail("cudaMalloc tab");
   if (cudaMemcpy(ctx->d_tab, tab.data(), sizeof(double) * TAB_SIZE, cudaMemcpyHostToDevice) != cudaSuccess)
     return fail("cudaMemcpy tab");
+  {  // nodal-basis variant tables (kernels_var.cu)
+    std::vector<double> vt(VT_SIZE, 0.0);
+    for (int a = 0; a < ni; ++a) {
+      for (int b = 0; b < ni; ++b) vt[VT_SM + a * ni + b] = B.S[a * ni + b] * B.w[b + 1];
+      vt[VT_A0 + a] = B.a0[a];
+      vt[VT_AP + a] = B.ap[a];
+      vt[VT_LAM + a] = B.lam[a];
+    }
+    for (int i = 0; i <= p; ++i) {
+      vt[VT_W + i] = B.w[i];
+      for (int j = 0; j <= p; ++j) vt[VT_K + i * (p + 1) + j] = B.K[i * (p + 1) + j];
+    }
+    if (cudaMalloc(&ctx->d_vt, sizeof(double) * VT_SIZE) != cudaSuccess) return fail("cudaMalloc vt");
+    if (cudaMemcpy(ctx->d_vt, vt.data(), sizeof(double) * VT_SIZE, cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail("cudaMemcpy vt");
+  }
   std::vector<double> hloc;
   hloc.insert(hloc.end(), ctx->hx.begin(), ctx->hx.end());
   hloc.insert(hloc.end(), ctx->hy.begin(), ctx->hy.end());
@@ -483,6 +547,8 @@ extern "C" sc_status sc_destroy(sc_ctx* ctx) {
   if (ctx->d_corner) cudaFree(ctx->d_corner);
   if (ctx->d_pending) cudaFree(ctx->d_pending);
   if (ctx->d_dotp) cudaFree(ctx->d_dotp);
+  if (ctx->d_vt) cudaFree(ctx->d_vt);
+  cublas_destroy(ctx->cublas);
   if (ctx->pcg_graph) cudaGraphExecDestroy(ctx->pcg_graph);
   if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
   for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);
@@ -1105,6 +1171,87 @@ extern "C" sc_status sc_loopback_comms_destroy(void** comms, int nranks) {
   }
   delete G;
   return SC_OK;
+}
+
+// ---------------------------------------------------------------- PAPER.md §7 operator variants
+extern "C" sc_status sc_apply_tpc(sc_ctx* ctx, const double* d_x, double* d_y, void* stream) {
+  if (!ctx || !d_x || !d_y || d_x == d_y) return SC_EINVAL;
+  if (ctx->broken) return SC_ESTATE;
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool rec = ctx->prof_on && ctx->prof_n < (int)ctx->prof_ev.size() / 2;
+  cudaEvent_t* ev = rec ? &ctx->prof_ev[2 * ctx->prof_n] : nullptr;
+  LAUNCH(launch_apply_tpc(ctx->g, ctx->d_vt, d_x, d_y, st, &nl_, ev));
+  if (rec) ctx->prof_n++;
+  return halo_sum(ctx, d_y, st);
+}
+
+static int mmc_shell(const sc_ctx* ctx) {
+  const long long ni = ctx->g.ni;
+  return (int)(6 * ni * ni + 12 * ni + 8);
+}
+
+static long long mmc_ngeom(const sc_ctx* ctx) {
+  return ctx->g.uniform ? 1 : (long long)ctx->g.nx * ctx->g.ny * ctx->g.nz;
+}
+
+extern "C" size_t sc_mmc_bytes(const sc_ctx* ctx) {
+  if (!ctx) return 0;
+  const long long nB = mmc_shell(ctx), ne = (long long)ctx->g.nx * ctx->g.ny * ctx->g.nz;
+  const long long mat = align_up(nB * nB * mmc_ngeom(ctx));
+  return sizeof(double) * (size_t)(mat + 2 * align_up(nB * ne));
+}
+
+extern "C" sc_status sc_mmc_bind(sc_ctx* ctx, void* d_buf, size_t bytes, void* stream) {
+  if (!ctx || !d_buf) return SC_EINVAL;
+  if (ctx->broken) return SC_ESTATE;
+  if (bytes < sc_mmc_bytes(ctx)) {
+    ctx->err = "MMC buffer too small: need " + std::to_string(sc_mmc_bytes(ctx)) + " bytes (sc_mmc_bytes)";
+    return SC_ENOMEM;
+  }
+  if (!load_cublas()) { ctx->err = "libcublas.so.12 not loadable"; return SC_ECUDA; }
+  if (!ctx->cublas && g_cublas.Create(&ctx->cublas) != 0) { ctx->err = "cublasCreate failed"; return SC_ECUDA; }
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long nB = mmc_shell(ctx), ne = (long long)ctx->g.nx * ctx->g.ny * ctx->g.nz;
+  const long long ng = mmc_ngeom(ctx);
+  ctx->mmc_nB = (int)nB;
+  ctx->mmc_ngeom = ng;
+  ctx->mmc_H = (double*)d_buf;
+  ctx->mmc_X = ctx->mmc_H + align_up(nB * nB * ng);   // matrices packed with stride nB^2
+  ctx->mmc_Y = ctx->mmc_X + align_up(nB * ne);
+  // precomputation, O(n_I^5) per geometry (Table 3): Hhat_e column by column
+  LAUNCH(launch_mmc_columns(ctx->g, ctx->d_vt, ctx->mmc_H, (int)nB, ng, st, &nl_));
+  CK(cudaStreamSynchronize(st));
+  return SC_OK;
+}
+
+extern "C" sc_status sc_apply_mmc(sc_ctx* ctx, const double* d_x, double* d_y, void* stream) {
+  if (!ctx || !d_x || !d_y || d_x == d_y) return SC_EINVAL;
+  if (ctx->broken) return SC_ESTATE;
+  if (!ctx->mmc_H) { ctx->err = "sc_mmc_bind not called"; return SC_ESTATE; }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nB = ctx->mmc_nB;
+  const long long ne = (long long)ctx->g.nx * ctx->g.ny * ctx->g.nz;
+  const bool rec = ctx->prof_on && ctx->prof_n < (int)ctx->prof_ev.size() / 2;
+  cudaEvent_t* ev = rec ? &ctx->prof_ev[2 * ctx->prof_n] : nullptr;
+  if (ev) CK(cudaEventRecord(ev[0], st));
+  LAUNCH(launch_mmc_gather(ctx->g, d_x, ctx->mmc_X, nB, st, &nl_));
+  if (ne > 0) {
+    if (g_cublas.SetStream(ctx->cublas, st) != 0) { ctx->err = "cublasSetStream failed"; return SC_ECUDA; }
+    const double one = 1.0, zero = 0.0;
+    int rc;
+    if (ctx->mmc_ngeom == 1) {   // Y (nB x ne) = Hhat (nB x nB) X (nB x ne), column-major, one DGEMM
+      rc = g_cublas.Dgemm(ctx->cublas, 0, 0, nB, (int)ne, nB, &one, ctx->mmc_H, nB, ctx->mmc_X, nB, &zero,
+                          ctx->mmc_Y, nB);
+    } else {                     // one matrix per element: a strided batch of GEMVs
+      rc = g_cublas.DgemmStridedBatched(ctx->cublas, 0, 0, nB, 1, nB, &one, ctx->mmc_H, nB, (long long)nB * nB,
+                                        ctx->mmc_X, nB, nB, &zero, ctx->mmc_Y, nB, nB, (int)ne);
+    }
+    if (rc != 0) { ctx->err = "cublasDgemm failed (" + std::to_string(rc) + ")"; ctx->broken = true; return SC_ECUDA; }
+    ctx->nlaunch++;
+  }
+  LAUNCH(launch_mmc_assemble(ctx->g, ctx->mmc_Y, d_y, nB, st, &nl_));
+  if (ev) { CK(cudaEventRecord(ev[1], st)); ctx->prof_n++; }
+  return halo_sum(ctx, d_y, st);
 }
 
 extern "C" long long sc_launch_count(const sc_ctx* ctx) { return ctx ? ctx->nlaunch : 0; }

@@ -69,6 +69,17 @@ enum {
 // 3 S^T (from primal), 4 M S^T (from dual = S^{-1}).
 enum { MAT_I = 0, MAT_SM = 1, MAT_S = 2, MAT_ST = 3, MAT_MST = 4 };
 
+// Nodal-basis operator variants (kernels_var.cu, §7): device table layout (doubles).
+enum {
+  VT_SM = 0,                                  // (S_II M_II)[m][q] = S_mq w_q, row-major n_I x n_I
+  VT_A0 = VT_SM + SC_NIMAX * SC_NIMAX,        // a0 = S_II K_I0
+  VT_AP = VT_A0 + SC_NIMAX,                   // ap = S_II K_Ip
+  VT_LAM = VT_AP + SC_NIMAX,                  // Lambda
+  VT_K = VT_LAM + SC_NIMAX,                   // nodal K, (p+1) x (p+1) row-major
+  VT_W = VT_K + (SC_PMAX + 1) * (SC_PMAX + 1),  // GLL weights w[0..p]
+  VT_SIZE = VT_W + SC_PMAX + 1
+};
+
 // PCG device scalars (doubles in the workspace).
 enum {
   SCAL_RZ = 0, SCAL_RZNEW, SCAL_PQ, SCAL_ALPHA, SCAL_BETA, SCAL_RR, SCAL_RR0,
@@ -83,6 +94,11 @@ enum {
 int launch_apply(const Geom& g, const double* x, double* y, const double* done, void* stream, int* nlaunch,
                  void* events = nullptr);
 int launch_diag(const Geom& g, double* diag, void* stream, int* nlaunch);
+int launch_apply_tpc(const Geom& g, const double* vt, const double* x, double* y, void* stream, int* nlaunch,
+                     void* events = nullptr);
+int launch_mmc_columns(const Geom& g, const double* vt, double* H, int nB, long long ngeom, void* stream, int* nlaunch);
+int launch_mmc_gather(const Geom& g, const double* x, double* X, int nB, void* stream, int* nlaunch);
+int launch_mmc_assemble(const Geom& g, const double* Y, double* y, int nB, void* stream, int* nlaunch);
 int launch_invert_diag(const Geom& g, double* diag, void* stream, int* nlaunch);
 int launch_convert(const Geom& g, const double* in, double* out, int to_skel, int mat, void* stream, int* nlaunch);
 int launch_fill_random(const Geom& g, uint64_t seed, double* v, void* stream, int* nlaunch);

@@ -178,6 +178,26 @@ class Context:
         _check(self.lib, self.ctx, "sc_preconditioner",
                self.lib.sc_preconditioner(self.ctx, ptr(out), self._s(stream)))
 
+    # -- PAPER.md §7 operator variants (nodal basis) --------------------------
+    def sc_apply_tpc(self, x, y, stream=None):
+        _check(self.lib, self.ctx, "sc_apply_tpc", self.lib.sc_apply_tpc(self.ctx, ptr(x), ptr(y), self._s(stream)))
+
+    def sc_mmc_bytes(self):
+        return int(self.lib.sc_mmc_bytes(self.ctx))
+
+    def sc_mmc_bind(self, buf=None, stream=None):
+        """Precompute the MMC element matrices into `buf` (a device tensor of >= sc_mmc_bytes bytes;
+        allocated here when None).  The buffer is kept referenced by the context."""
+        nbytes = self.sc_mmc_bytes()
+        if buf is None:
+            buf = torch.empty(nbytes // 8 + 1, dtype=torch.float64, device=self.device)
+        self._mmc_buf = buf
+        _check(self.lib, self.ctx, "sc_mmc_bind",
+               self.lib.sc_mmc_bind(self.ctx, ptr(buf), buf.numel() * buf.element_size(), self._s(stream)))
+
+    def sc_apply_mmc(self, x, y, stream=None):
+        _check(self.lib, self.ctx, "sc_apply_mmc", self.lib.sc_apply_mmc(self.ctx, ptr(x), ptr(y), self._s(stream)))
+
     def sc_basis_1d(self):
         ni = self.p - 1
         lam, a0, ap = (np.zeros(ni) for _ in range(3))
