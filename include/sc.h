@@ -247,6 +247,21 @@ size_t sc_mmc_bytes(const sc_ctx* ctx);
 sc_status sc_mmc_bind(sc_ctx* ctx, void* d_buf, size_t bytes, void* stream);
 sc_status sc_apply_mmc(sc_ctx* ctx, const double* d_x, double* d_y, void* stream);
 
+/* Solvers UC / DC / BC of the paper's solver comparison (§8 "Performance of solvers", P:602-607,
+ * Table 4 `tab:solver_complexities`) on the NODAL condensed system:  PCG (x0 = 0, Hestenes-Stiefel as
+ * sc_pcg_solve) with operator `op` (SC_OP_TPC as in the paper, or SC_OP_MMC after sc_mmc_bind) and
+ * preconditioner `prec`: SC_PREC_NONE (UC), SC_PREC_DIAG (DC: 1/diag(Rhat Hhat Rhat^T), built per call),
+ * SC_PREC_BLOCK (BC: the exact inverse of every assembled face / edge / vertex self-block, P:597-600,
+ * applied in tensor-product form as Shat^T Ptilde Shat, 24 n_I^3 per element).  Stops when
+ * ||r_k||_2 <= rtol ||r_0||_2 for the recursively updated NODAL residual, or after maxit iterations.
+ * d_b, d_x: nodal skeleton vectors (sc_layout, SC_PERM conversions).  Uses the bound workspace (not
+ * between sc_pcg_start and sc_pcg_status); synchronises the stream every 8 iterations.  Errors as
+ * sc_pcg_solve; SC_EINVAL for an unknown op / prec, SC_ESTATE for MMC without sc_mmc_bind. */
+enum { SC_OP_TPC = 1, SC_OP_MMC = 2 };
+enum { SC_PREC_NONE = 0, SC_PREC_DIAG = 1, SC_PREC_BLOCK = 2 };
+sc_status sc_pcg_solve_nodal(sc_ctx* ctx, int op, int prec, const double* d_b, double* d_x, double rtol,
+                             int maxit, sc_pcg_report* rep, void* stream);
+
 /* Operator kernel family this ctx runs: "v6" / "v6h8" (halo-recompute tile columns,
  * 3 <= p <= 8), "v3" (tile columns with look-back), "rw" / "p2" (row-warp kernels, p <= 4),
  * "v4" (colour-scheduled element CTAs, p >= 9), "v1" (one CTA per element, any geometry). */

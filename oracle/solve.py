@@ -107,6 +107,18 @@ def entity_keys(grid, g):
     return [(int(a), int(b), int(c), int(d)) for a, b, c, d in zip(fl, gx // p, gy // p, gz // p)]
 
 
+def assembled_diagonal(op):
+    """diag(Rhat Hhat Rhat^T) on the lattice, 0 off the free skeleton: solver DC's diagonal
+    preconditioner ("DC adds diagonal preconditioning"), summed element by element from the
+    dense element Schur complements (P:107-109 assembly)."""
+    d = np.zeros(op.grid.n_lattice)
+    for elems, ce in op.groups:
+        hd = np.diag(ce.explicit())
+        for e in elems:
+            np.add.at(d, op.GB[e], hd)
+    return np.where(op.free, d, 0.0)
+
+
 class BlockJacobi:
     """Inverse of the assembled face / edge / vertex self-blocks."""
 

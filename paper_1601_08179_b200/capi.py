@@ -13,6 +13,8 @@ LIB_PATH = os.environ.get("SC_LIB_PATH", os.path.join(HERE, "_lib", "libsc.so"))
 
 SC_OK, SC_EINVAL, SC_ENOMEM, SC_ECUDA, SC_ENCCL, SC_EBREAKDOWN, SC_ESTATE = range(7)
 SC_PERM, SC_PRIMAL, SC_DUAL = 0, 1, 2
+SC_OP_TPC, SC_OP_MMC = 1, 2
+SC_PREC_NONE, SC_PREC_DIAG, SC_PREC_BLOCK = 0, 1, 2
 STATUS_NAMES = {0: "SC_OK", 1: "SC_EINVAL", 2: "SC_ENOMEM", 3: "SC_ECUDA", 4: "SC_ENCCL",
                 5: "SC_EBREAKDOWN", 6: "SC_ESTATE"}
 
@@ -78,6 +80,8 @@ SIGNATURES = {
     "sc_mmc_bytes": ([_P], ctypes.c_size_t),
     "sc_mmc_bind": ([_P, _P, ctypes.c_size_t, _P], ctypes.c_int),
     "sc_apply_mmc": ([_P, _P, _P, _P], ctypes.c_int),
+    "sc_pcg_solve_nodal": ([_P, ctypes.c_int, ctypes.c_int, _P, _P, ctypes.c_double, ctypes.c_int,
+                            ctypes.POINTER(ScPcgReport), _P], ctypes.c_int),
     "sc_launch_count": ([_P], ctypes.c_longlong),
     "sc_last_error": ([_P], ctypes.c_char_p),
     "sc_version": ([], ctypes.c_char_p),

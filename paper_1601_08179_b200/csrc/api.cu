@@ -1254,6 +1254,74 @@ extern "C" sc_status sc_apply_mmc(sc_ctx* ctx, const double* d_x, double* d_y, v
   return halo_sum(ctx, d_y, st);
 }
 
+// Solvers UC / DC / BC of PAPER.md §8 (Table 4) on the NODAL condensed system with the
+// TPC (or MMC) operator.  Hestenes-Stiefel PCG as in BT; stopping rule ||r_k||_2 <= rtol ||r_0||_2 on the
+// recursively updated NODAL residual (DESIGN reading R18).  Workspace use: q, pv, r as in BT; bdev = z,
+// xdev = the UC mask / DC inverse diagonal; the BT diagonal ctx->pinv is BC's transformed-block inverse.
+static sc_status nodal_apply(sc_ctx* ctx, int op, const double* x, double* y, cudaStream_t st) {
+  return op == SC_OP_MMC ? sc_apply_mmc(ctx, x, y, st) : sc_apply_tpc(ctx, x, y, st);
+}
+
+extern "C" sc_status sc_pcg_solve_nodal(sc_ctx* ctx, int op, int prec, const double* d_b, double* d_x, double rtol,
+                                        int maxit, sc_pcg_report* rep, void* stream) {
+  if (!ctx || !d_b || !d_x || d_b == d_x) return SC_EINVAL;
+  if ((op != SC_OP_TPC && op != SC_OP_MMC) || prec < SC_PREC_NONE || prec > SC_PREC_BLOCK) return SC_EINVAL;
+  if (ctx->broken) return SC_ESTATE;
+  if (!ctx->ws) { ctx->err = "workspace not bound"; return SC_ESTATE; }
+  if (op == SC_OP_MMC && !ctx->mmc_H) { ctx->err = "sc_mmc_bind not called"; return SC_ESTATE; }
+  cudaStream_t st = (cudaStream_t)stream;
+  auto t0 = std::chrono::steady_clock::now();
+  const long long n = ctx->g.n_total;
+  double* z = ctx->bdev;
+  double* m = ctx->xdev;
+  const double* mask = ctx->pinv;     // nonzero exactly on the free entries
+  ctx->tol2 = rtol > 0 ? rtol * rtol : -1.0;
+  if (prec == SC_PREC_DIAG) {
+    LAUNCH(launch_var_diag(ctx->g, ctx->d_vt, m, st, &nl_));
+    sc_status s = halo_sum(ctx, m, st);
+    if (s) return s;
+    LAUNCH(launch_invert_diag(ctx->g, m, st, &nl_));
+  }
+  if (prec == SC_PREC_NONE) LAUNCH(launch_unit_mask(mask, m, n, st, &nl_));   // m = 1 on free entries
+  const double* pm = prec == SC_PREC_BLOCK ? ctx->pinv : m;
+  CK(cudaMemsetAsync(z, 0, sizeof(double) * n, st));
+  LAUNCH(launch_var_init(d_b, mask, ctx->r, d_x, n, st, &nl_));
+  LAUNCH(launch_var_prec(ctx->g, prec, pm, ctx->r, z, st, &nl_));
+  LAUNCH(launch_var_direction(d_x, ctx->pv, z, n, ctx->scal, 1, st, &nl_));
+  LAUNCH(launch_dot_partial(ctx->r, z, n, ctx->own, ctx->partials, nullptr, st, &nl_));
+  LAUNCH(launch_dot_partial(ctx->r, ctx->r, n, ctx->own, ctx->partials + SC_RED_BLOCKS, nullptr, st, &nl_));
+  LAUNCH(launch_reduce2(ctx->partials, ctx->scal, SCAL_RED0, 2, nullptr, st, &nl_));
+  sc_status s = allreduce_scal(ctx, SCAL_RED0, 2, st);
+  if (s) return s;
+  LAUNCH(launch_pcg_init_finalize(ctx->scal, ctx->partials, ctx->tol2, maxit, st, &nl_));
+  double* done = ctx->scal + SCAL_DONE;
+  bool stop = false;
+  for (int it = 0; it < maxit && !stop; ++it) {
+    if ((s = nodal_apply(ctx, op, ctx->pv, ctx->q, st))) return s;
+    LAUNCH(launch_dot_partial(ctx->pv, ctx->q, n, ctx->own, ctx->partials, done, st, &nl_));
+    LAUNCH(launch_reduce2(ctx->partials, ctx->scal, SCAL_RED0, 1, done, st, &nl_));
+    if ((s = allreduce_scal(ctx, SCAL_RED0, 1, st))) return s;
+    LAUNCH(launch_pcg_alpha(ctx->scal, st, &nl_));
+    LAUNCH(launch_var_update(ctx->r, ctx->q, n, ctx->scal, st, &nl_));
+    LAUNCH(launch_var_prec(ctx->g, prec, pm, ctx->r, z, st, &nl_));
+    LAUNCH(launch_dot_partial(ctx->r, z, n, ctx->own, ctx->partials, done, st, &nl_));
+    LAUNCH(launch_dot_partial(ctx->r, ctx->r, n, ctx->own, ctx->partials + SC_RED_BLOCKS, done, st, &nl_));
+    LAUNCH(launch_reduce2(ctx->partials, ctx->scal, SCAL_RED0, 2, done, st, &nl_));
+    if ((s = allreduce_scal(ctx, SCAL_RED0, 2, st))) return s;
+    LAUNCH(launch_pcg_beta(ctx->scal, st, &nl_));
+    LAUNCH(launch_var_direction(d_x, ctx->pv, z, n, ctx->scal, 0, st, &nl_));
+    if (rtol > 0 && (it + 1) % kPcgChunk == 0) {
+      double dflag = 0;
+      CK(cudaMemcpyAsync(&dflag, done, sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      stop = dflag != 0.0;
+    }
+  }
+  CK(cudaStreamSynchronize(st));
+  auto t1 = std::chrono::steady_clock::now();
+  return pcg_report_impl(ctx, rep, st, std::chrono::duration<double>(t1 - t0).count());
+}
+
 extern "C" long long sc_launch_count(const sc_ctx* ctx) { return ctx ? ctx->nlaunch : 0; }
 
 extern "C" const char* sc_operator_kernel(const sc_ctx* ctx) {

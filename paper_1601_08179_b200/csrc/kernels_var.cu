@@ -312,6 +312,181 @@ __global__ void k_mmc_assemble(Geom g, const double* __restrict__ Y, double* __r
   }
 }
 
+// ---------------------------------------------------------------- solvers UC / DC / BC
+// DC: element contributions to diag(Rhat Hhat Rhat^T) in the nodal basis.  Primary part: the
+// diagonal of H_e = d0 M(x)M(x)M + d1 M(x)M(x)K + ... at the shell node; condensed part (face nodes
+// only): with H_EFw = d1 (S M)(x)(S M)(x)a0 (Table 1), diag(H_FwI H_II^{-1} H_IFw)(j,k) =
+// d1^2 sum_{b,c} (S M)_{b j}^2 (S M)_{c k}^2 G_w(b,c),  G_w(b,c) = sum_a a0_a^2 D^{-1}(a,b,c).
+__global__ void k_var_diag(Geom g, const double* __restrict__ vt, double* __restrict__ diag) {
+  const int p = g.p, ni = g.ni, n2 = ni * ni, nsh = 6 * n2 + 12 * ni + 8, np1 = p + 1;
+  extern __shared__ double sm[];
+  double* G = sm;                // 6 n2: G_f(b,c) per face f
+  double* SM2 = G + 6 * n2;      // (S M)^2 entrywise
+  double* K = SM2 + n2;          // (p+1)^2
+  double* w = K + np1 * np1;
+  double* a0 = w + np1;
+  double* ap = a0 + ni;
+  double* lam = ap + ni;
+  const long long e = blockIdx.x;
+  const int ex = (int)(e % g.nx), ey = (int)((e / g.nx) % g.ny), ez = (int)(e / ((long long)g.nx * g.ny));
+  double d[4];
+  metric(g, ex, ey, ez, d);
+  for (int t = threadIdx.x; t < n2; t += blockDim.x) SM2[t] = vt[VT_SM + t] * vt[VT_SM + t];
+  for (int t = threadIdx.x; t < np1 * np1; t += blockDim.x) K[t] = vt[VT_K + t];
+  for (int t = threadIdx.x; t < np1; t += blockDim.x) w[t] = vt[VT_W + t];
+  for (int t = threadIdx.x; t < ni; t += blockDim.x) {
+    a0[t] = vt[VT_A0 + t]; ap[t] = vt[VT_AP + t]; lam[t] = vt[VT_LAM + t];
+  }
+  __syncthreads();
+  // G_f(r,s): sum over the face-normal eigen-index m of a_m^2 / D, (r,s) the in-face eigen-indices
+  for (int t = threadIdx.x; t < 6 * n2; t += blockDim.x) {
+    const int f = t / n2, rr = t % n2, r = rr % ni, q = rr / ni, dir = f >> 1;
+    const double* a = (f & 1) ? ap : a0;
+    double acc = 0.0;
+    for (int m = 0; m < ni; ++m) {
+      const int ii = dir == 0 ? m : r, jj = dir == 0 ? r : (dir == 1 ? m : q), kk = dir == 2 ? m : q;
+      acc += a[m] * a[m] / (d[0] + d[1] * lam[ii] + d[2] * lam[jj] + d[3] * lam[kk]);
+    }
+    G[t] = acc;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nsh; t += blockDim.x) {
+    int i, j, k, ent, loc;
+    shell_node(p, ni, t, &i, &j, &k, &ent, &loc);
+    bool dr;
+    const long long base = entity_base(g, ex, ey, ez, ent, &dr);
+    if (dr) continue;
+    double val = d[0] * w[i] * w[j] * w[k] + d[1] * K[i * np1 + i] * w[j] * w[k] + d[2] * w[i] * K[j * np1 + j] * w[k] +
+                 d[3] * w[i] * w[j] * K[k * np1 + k];
+    if (ent < 6) {
+      const int dir = ent >> 1, u = loc % ni, v = loc / ni;   // face coords (u, v) in-plane order
+      const double* Gf = G + ent * n2;
+      double acc = 0.0;
+      for (int c = 0; c < ni; ++c)
+        for (int b = 0; b < ni; ++b) acc += SM2[b * ni + u] * SM2[c * ni + v] * Gf[b + ni * c];
+      val -= d[1 + dir] * d[1 + dir] * acc;
+    }
+    atomicAdd(&diag[base + loc], val);
+  }
+}
+
+// BC: z = Shat^T Ptilde Shat r entity by entity (the exact inverse of every assembled face / edge /
+// vertex self-block: in the transformed basis these blocks are diagonal, Ptilde = the BT
+// diagonal, DESIGN reading R12), i.e. 4 n_I^3 per face (Table 4 "BC: 24 n_I^3").
+// UC / DC: z = m .* r with m = free mask / 1/diag.
+__global__ void k_var_prec(Geom g, int mode, const double* __restrict__ m, const double* __restrict__ r,
+                           double* __restrict__ z) {
+  const int ni = g.ni, n2 = ni * ni;
+  if (mode != 2) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < g.n_total;
+         i += (long long)gridDim.x * blockDim.x)
+      z[i] = m[i] * r[i];
+    return;
+  }
+  extern __shared__ double sm[];
+  double* S = sm;            // S_II row-major
+  double* t0 = S + n2;       // n2
+  double* t1 = t0 + n2;      // n2
+  for (int t = threadIdx.x; t < n2; t += blockDim.x) S[t] = g.tab[TAB_MAT + MAT_S * SC_NIMAX * SC_NIMAX + t];
+  const long long nf = g.n_f[0] + g.n_f[1] + g.n_f[2], ned = g.n_e[0] + g.n_e[1] + g.n_e[2];
+  for (long long ent = blockIdx.x; ent < nf + ned + 1; ent += gridDim.x) {
+    __syncthreads();
+    if (ent < nf) {
+      const int c = ent < g.n_f[0] ? 0 : (ent < g.n_f[0] + g.n_f[1] ? 1 : 2);
+      const long long id = ent - (c == 0 ? 0 : (c == 1 ? g.n_f[0] : g.n_f[0] + g.n_f[1]));
+      const long long base = g.off_f[c] + id * n2;
+      for (int t = threadIdx.x; t < n2; t += blockDim.x) {      // t0 = (I (x) S) r : along the first coord
+        const int a = t % ni, q = t / ni;
+        double acc = 0.0;
+        for (int u = 0; u < ni; ++u) acc += S[a * ni + u] * r[base + u + ni * q];
+        t0[t] = acc;
+      }
+      __syncthreads();
+      for (int t = threadIdx.x; t < n2; t += blockDim.x) {      // t1 = Ptilde (S (x) I) t0
+        const int a = t % ni, b = t / ni;
+        double acc = 0.0;
+        for (int v = 0; v < ni; ++v) acc += S[b * ni + v] * t0[a + ni * v];
+        t1[t] = m[base + t] * acc;
+      }
+      __syncthreads();
+      for (int t = threadIdx.x; t < n2; t += blockDim.x) {      // t0 = (S^T (x) I) t1
+        const int a = t % ni, v = t / ni;
+        double acc = 0.0;
+        for (int b = 0; b < ni; ++b) acc += S[b * ni + v] * t1[a + ni * b];
+        t0[t] = acc;
+      }
+      __syncthreads();
+      for (int t = threadIdx.x; t < n2; t += blockDim.x) {      // z = (I (x) S^T) t0
+        const int u = t % ni, v = t / ni;
+        double acc = 0.0;
+        for (int a = 0; a < ni; ++a) acc += S[a * ni + u] * t0[a + ni * v];
+        z[base + t] = acc;
+      }
+    } else if (ent < nf + ned) {   // a whole edge class row-range per block: warp per edge
+      const long long e0 = ent - nf;
+      const int c = e0 < g.n_e[0] ? 0 : (e0 < g.n_e[0] + g.n_e[1] ? 1 : 2);
+      const long long id = e0 - (c == 0 ? 0 : (c == 1 ? g.n_e[0] : g.n_e[0] + g.n_e[1]));
+      const long long base = g.off_e[c] + id * ni;
+      for (int t = threadIdx.x; t < ni; t += blockDim.x) {
+        double acc = 0.0;
+        for (int u = 0; u < ni; ++u) acc += S[t * ni + u] * r[base + u];
+        t0[t] = m[base + t] * acc;
+      }
+      __syncthreads();
+      for (int t = threadIdx.x; t < ni; t += blockDim.x) {
+        double acc = 0.0;
+        for (int a = 0; a < ni; ++a) acc += S[a * ni + t] * t0[a];
+        z[base + t] = acc;
+      }
+    } else {                       // vertices (and the padding entries) in one grid-stride pass
+      for (long long i = threadIdx.x; i < g.n_total - g.off_v; i += blockDim.x)
+        z[g.off_v + i] = m[g.off_v + i] * r[g.off_v + i];
+    }
+  }
+}
+
+// m = 1 where mask != 0 (free entries), else 0 (UC's preconditioner).
+__global__ void k_unit_mask(const double* __restrict__ mask, double* __restrict__ m, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    m[i] = mask[i] != 0.0 ? 1.0 : 0.0;
+}
+
+// r = b on free entries (mask != 0), x = 0.
+__global__ void k_var_init(const double* __restrict__ b, const double* __restrict__ mask, double* __restrict__ r,
+                           double* __restrict__ x, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    r[i] = mask[i] != 0.0 ? b[i] : 0.0;
+    x[i] = 0.0;
+  }
+}
+
+// r -= alpha q
+__global__ void k_var_update(double* __restrict__ r, const double* __restrict__ q, long long n,
+                             const double* __restrict__ scal) {
+  if (scal[SCAL_DONE] != 0.0) return;
+  const double alpha = scal[SCAL_ALPHA];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    r[i] -= alpha * q[i];
+}
+
+// x += alpha p (if this iteration's alpha step ran) ; p = z + beta p (unless converged) ; first = 1: p = z.
+__global__ void k_var_direction(double* __restrict__ x, double* __restrict__ p, const double* __restrict__ z,
+                                long long n, const double* __restrict__ scal, int first) {
+  if (first) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+      p[i] = z[i];
+    return;
+  }
+  if (scal[SCAL_RAN] == 0.0 || scal[SCAL_BREAK] != 0.0) return;
+  const double alpha = scal[SCAL_ALPHA], beta = scal[SCAL_BETA];
+  const bool dir = scal[SCAL_DONE] == 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double pi = p[i];
+    x[i] += alpha * pi;
+    if (dir) p[i] = z[i] + beta * pi;
+  }
+}
+
 // ---------------------------------------------------------------- launchers
 // Dynamic shared-memory opt-in for the element kernels (the largest need, p = 32, is ~204 KB).
 static cudaError_t set_smem_attr(const void* fn, size_t bytes, size_t* done) {
@@ -366,6 +541,54 @@ int launch_mmc_gather(const Geom& g, const double* x, double* X, int nB, void* s
 
 int launch_mmc_assemble(const Geom& g, const double* Y, double* y, int nB, void* stream, int* nl) {
   k_mmc_assemble<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(g, Y, y, nB);
+  (*nl)++;
+  return cudaGetLastError();
+}
+
+int launch_var_diag(const Geom& g, const double* vt, double* diag, void* stream, int* nl) {
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t err = cudaMemsetAsync(diag, 0, sizeof(double) * g.n_total, st);
+  if (err != cudaSuccess) return err;
+  const long long ne = (long long)g.nx * g.ny * g.nz;
+  const int ni = g.ni, n2 = ni * ni, np1 = g.p + 1;
+  const size_t smem = sizeof(double) * (7 * n2 + np1 * np1 + np1 + 3 * ni);
+  static size_t attr[kMaxDev];
+  if ((err = set_smem_attr((const void*)k_var_diag, smem, attr)) != cudaSuccess) return err;
+  if (ne > 0) {
+    k_var_diag<<<(unsigned)ne, 256, smem, st>>>(g, vt, diag);
+    (*nl)++;
+  }
+  return cudaGetLastError();
+}
+
+int launch_var_prec(const Geom& g, int mode, const double* m, const double* r, double* z, void* stream, int* nl) {
+  const size_t smem = mode == 2 ? sizeof(double) * 3 * g.ni * g.ni : 0;
+  k_var_prec<<<mode == 2 ? 148 * 8 : SC_RED_BLOCKS, mode == 2 ? 128 : 256, smem, (cudaStream_t)stream>>>(g, mode, m, r, z);
+  (*nl)++;
+  return cudaGetLastError();
+}
+
+int launch_unit_mask(const double* mask, double* m, long long n, void* stream, int* nl) {
+  k_unit_mask<<<SC_RED_BLOCKS, 256, 0, (cudaStream_t)stream>>>(mask, m, n);
+  (*nl)++;
+  return cudaGetLastError();
+}
+
+int launch_var_init(const double* b, const double* mask, double* r, double* x, long long n, void* stream, int* nl) {
+  k_var_init<<<SC_RED_BLOCKS, 256, 0, (cudaStream_t)stream>>>(b, mask, r, x, n);
+  (*nl)++;
+  return cudaGetLastError();
+}
+
+int launch_var_update(double* r, const double* q, long long n, const double* scal, void* stream, int* nl) {
+  k_var_update<<<SC_RED_BLOCKS, 256, 0, (cudaStream_t)stream>>>(r, q, n, scal);
+  (*nl)++;
+  return cudaGetLastError();
+}
+
+int launch_var_direction(double* x, double* p, const double* z, long long n, const double* scal, int first,
+                         void* stream, int* nl) {
+  k_var_direction<<<SC_RED_BLOCKS, 256, 0, (cudaStream_t)stream>>>(x, p, z, n, scal, first);
   (*nl)++;
   return cudaGetLastError();
 }

@@ -99,6 +99,13 @@ int launch_apply_tpc(const Geom& g, const double* vt, const double* x, double* y
 int launch_mmc_columns(const Geom& g, const double* vt, double* H, int nB, long long ngeom, void* stream, int* nlaunch);
 int launch_mmc_gather(const Geom& g, const double* x, double* X, int nB, void* stream, int* nlaunch);
 int launch_mmc_assemble(const Geom& g, const double* Y, double* y, int nB, void* stream, int* nlaunch);
+int launch_var_diag(const Geom& g, const double* vt, double* diag, void* stream, int* nlaunch);
+int launch_var_prec(const Geom& g, int mode, const double* m, const double* r, double* z, void* stream, int* nlaunch);
+int launch_unit_mask(const double* mask, double* m, long long n, void* stream, int* nlaunch);
+int launch_var_init(const double* b, const double* mask, double* r, double* x, long long n, void* stream, int* nlaunch);
+int launch_var_update(double* r, const double* q, long long n, const double* scal, void* stream, int* nlaunch);
+int launch_var_direction(double* x, double* p, const double* z, long long n, const double* scal, int first,
+                         void* stream, int* nlaunch);
 int launch_invert_diag(const Geom& g, double* diag, void* stream, int* nlaunch);
 int launch_convert(const Geom& g, const double* in, double* out, int to_skel, int mat, void* stream, int* nlaunch);
 int launch_fill_random(const Geom& g, uint64_t seed, double* v, void* stream, int* nlaunch);

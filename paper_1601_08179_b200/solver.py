@@ -198,6 +198,16 @@ class Context:
     def sc_apply_mmc(self, x, y, stream=None):
         _check(self.lib, self.ctx, "sc_apply_mmc", self.lib.sc_apply_mmc(self.ctx, ptr(x), ptr(y), self._s(stream)))
 
+    def sc_pcg_solve_nodal(self, b, x, op="tpc", prec="block", rtol=1e-10, maxit=1000, stream=None):
+        """Solvers UC / DC / BC (prec "none" / "diag" / "block") on the nodal condensed system."""
+        rep = ScPcgReport()
+        opc = {"tpc": capi.SC_OP_TPC, "mmc": capi.SC_OP_MMC}[op]
+        pc = {"none": capi.SC_PREC_NONE, "diag": capi.SC_PREC_DIAG, "block": capi.SC_PREC_BLOCK}[prec]
+        st = self.lib.sc_pcg_solve_nodal(self.ctx, opc, pc, ptr(b), ptr(x), float(rtol), int(maxit),
+                                         ctypes.byref(rep), self._s(stream))
+        _check(self.lib, self.ctx, "sc_pcg_solve_nodal", st)
+        return rep
+
     def sc_basis_1d(self):
         ni = self.p - 1
         lam, a0, ap = (np.zeros(ni) for _ in range(3))

@@ -159,3 +159,66 @@ def test_tpc_multitile_launch_count():
     n0 = ctx.launch_count()
     ctx.sc_apply_mmc(x, y)
     assert ctx.launch_count() - n0 == 3
+
+
+# ---------------------------------------------------------------- solvers UC / DC / BC
+def _nodal_skel(ctx, v_lat):
+    from paper_1601_08179_b200 import SC_PERM
+    s = ctx.skeleton()
+    ctx.sc_to_transformed(torch.from_numpy(np.ascontiguousarray(v_lat)).cuda(), s, SC_PERM)
+    return s
+
+
+def _nodal_lat(ctx, v_skel):
+    from paper_1601_08179_b200 import SC_PERM
+    lat = ctx.lattice()
+    ctx.sc_from_transformed(v_skel, lat, SC_PERM)
+    return lat.cpu().numpy()
+
+
+@pytest.mark.parametrize("prec", ["none", "diag", "block"])
+@pytest.mark.parametrize("p,ne,aniso", [(4, (3, 2, 2), 1.0), (6, (2, 3, 2), 8.0), (9, (2, 2, 2), 1.0)])
+def test_nodal_solvers_against_oracle(prec, p, ne, aniso):
+    """UC / DC / BC with the TPC operator against the oracle's PCG with the same preconditioner
+    (identity / assembled diagonal / BlockJacobi), nodal Euclidean residual norm (DESIGN R18):
+    iteration count within +-1, iterate at the GPU's count within 1e-10 (readings R7, R8)."""
+    from oracle import pcg, solve
+    g = small_grid(p, ne, 1.0, lengths=(aniso, 1.0, 1.0))
+    op = operator.AssembledCondensedOperator(g)
+    b = lattice_random(17, g.ne, g.p).ravel()
+    P = {"none": lambda r: np.where(op.free, r, 0.0),
+         "diag": (lambda dg: lambda r: np.where(op.free, r / np.where(op.free, dg, 1.0), 0.0))(
+             solve.assembled_diagonal(op)),
+         "block": solve.BlockJacobi(op).apply}[prec]
+    ref = pcg.pcg(op.apply, P, np.where(op.free, b, 0.0), rtol=1e-10, maxit=2000)
+    ctx = ctx_for(g)
+    bs, xs = _nodal_skel(ctx, b), ctx.skeleton()
+    rep = ctx.sc_pcg_solve_nodal(bs, xs, op="tpc", prec=prec, rtol=1e-10, maxit=2000)
+    assert rep.converged and abs(rep.iters - ref.iters) <= 1
+    ref_k = pcg.pcg(op.apply, P, np.where(op.free, b, 0.0), fixed_iters=rep.iters)
+    assert rel(_nodal_lat(ctx, xs), ref_k.x) <= 1e-10
+
+
+def test_bc_equals_bt_iterates_and_mmc_solver():
+    """BC (nodal, block preconditioner) and BT (transformed, diagonal) produce the same iterates
+    (x_BC = Shat^T x~_BT: the block preconditioner reduces to a diagonal in the
+    transformed system); the MMC operator gives the same BC solve as TPC."""
+    from paper_1601_08179_b200 import SC_PRIMAL, SC_DUAL
+    g = small_grid(5, (3, 3, 2), 0.5)
+    ctx = ctx_for(g)
+    b = lattice_random(3, g.ne, g.p).ravel()
+    bs, xs = _nodal_skel(ctx, b), ctx.skeleton()
+    ctx.sc_pcg_solve_nodal(bs, xs, op="tpc", prec="block", rtol=0.0, maxit=15)
+    bt = ctx.skeleton()
+    ctx.sc_to_transformed(torch.from_numpy(b).cuda(), bt, SC_DUAL)
+    xt = ctx.skeleton()
+    ctx.sc_pcg_solve(bt, xt, rtol=0.0, maxit=15)
+    x_bt = ctx.lattice()
+    ctx.sc_from_transformed(xt, x_bt, SC_PRIMAL)
+    assert rel(_nodal_lat(ctx, xs), x_bt.cpu().numpy()) <= 1e-10
+    ctx.sc_mmc_bind()
+    xm = ctx.skeleton()
+    rep = ctx.sc_pcg_solve_nodal(bs, xm, op="mmc", prec="block", rtol=1e-10, maxit=500)
+    rep2 = ctx.sc_pcg_solve_nodal(bs, xs, op="tpc", prec="block", rtol=1e-10, maxit=500)
+    assert rep.converged and abs(rep.iters - rep2.iters) <= 1
+    assert rel(_nodal_lat(ctx, xm), _nodal_lat(ctx, xs)) <= 1e-9

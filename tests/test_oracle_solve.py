@@ -229,3 +229,28 @@ def test_multi_geometry_grouping_recovery_equals_full_solve():
     ub[fr] = np.linalg.solve(Ac, b[fr])
     u = solve.recover(op, f, ub)
     assert np.abs(u - ufull).max() < 1e-11 * np.abs(ufull).max()
+
+
+def test_assembled_diagonal_p2_closed_forms_and_dense():
+    """solve.assembled_diagonal (solver DC) pinned by the hand-derived nodal p = 2 Schur
+    diagonal (tests/golden/p2_single_element.txt): on a 2x2x2 grid of reference elements an interior
+    face sums 2 x 328/81, an interior edge 4 x 4/3, the centre vertex 8 x 7/18; and on a non-uniform
+    grid it equals the diagonal of the explicitly assembled matrix (a dropped neighbour fails)."""
+    from conftest import read_golden
+    G = read_golden("p2_single_element.txt")
+    g = small_grid(2, (2, 2, 2), 0.0, lengths=(4.0, 4.0, 4.0))
+    op = operator.AssembledCondensedOperator(g)
+    d = solve.assembled_diagonal(op)
+    nx1, ny1, _ = mesh.lattice_dims(g)
+    idx = lambda gx, gy, gz: gx + nx1 * (gy + ny1 * gz)
+    assert abs(d[idx(2, 1, 1)] - 2 * float(G["schur_face_diag"])) < 1e-13
+    assert abs(d[idx(2, 2, 1)] - 4 * float(G["schur_edge_diag"])) < 1e-13
+    assert abs(d[idx(2, 2, 2)] - 8 * float(G["schur_vertex_diag"])) < 1e-13
+    assert d[idx(0, 1, 1)] == 0.0                 # Dirichlet face node
+    g = small_grid(3, (3, 2, 2), 0.4, lengths=(1.5, 1.0, 0.8))
+    g.hx = np.array([0.3, 0.7, 0.5])
+    g.hz = np.array([0.35, 0.45])
+    op = operator.AssembledCondensedOperator(g)
+    A = _assembled_dense(op)
+    ref = np.where(op.free, np.diag(A), 0.0)
+    assert np.allclose(solve.assembled_diagonal(op), ref, rtol=0, atol=1e-13 * np.abs(ref).max())

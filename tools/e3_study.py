@@ -48,6 +48,7 @@ def main():
     ap.add_argument("--reps", type=int, default=11)
     ap.add_argument("--k", type=float, default=5.0)
     ap.add_argument("--ns", default="8", help="elements per direction (E4: --ps 16 --alphas 1 --ns 2,4,8,16)")
+    ap.add_argument("--solvers", default="bt", help="bt,bc,dc,uc (P:602-607; UC/DC/BC use TPC, nodal system)")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     import torch
@@ -56,9 +57,10 @@ def main():
     from paper_1601_08179_b200 import context_for_grid
     from synth import e3_grid, e3_u, e3_f
     rows = []
-    cases = [(p, alpha, n) for n in [int(s) for s in a.ns.split(",")] for p in [int(s) for s in a.ps.split(",")]
-             for alpha in [float(s) for s in a.alphas.split(",")]]
-    for p, alpha, n in cases:
+    from paper_1601_08179_b200 import SC_PERM, SC_PRIMAL, SC_DUAL
+    cases = [(p, alpha, n, sv) for n in [int(s) for s in a.ns.split(",")] for p in [int(s) for s in a.ps.split(",")]
+             for alpha in [float(s) for s in a.alphas.split(",")] for sv in a.solvers.split(",")]
+    for p, alpha, n, solver in cases:
         g = e3_grid(p, alpha, n=n)
         xs, ys, zs = lattice_1d(g.hx, p), lattice_1d(g.hy, p), lattice_1d(g.hz, p)
         Z, Y, X = np.meshgrid(zs, ys, xs, indexing="ij")
@@ -72,7 +74,17 @@ def main():
             bt = ctx.skeleton()
             ctx.sc_condense_rhs_dirichlet(f, gd, bt)
             xt = ctx.skeleton()
-            r = ctx.sc_pcg_solve(bt, xt, rtol=1e-12, maxit=20000)
+            if solver == "bt":
+                r = ctx.sc_pcg_solve(bt, xt, rtol=1e-12, maxit=20000)
+            else:   # nodal system: b = Shat^{-1} b~, x~ = Shat^{-T} x (untimed conversions around the solve)
+                lat = ctx.lattice()
+                ctx.sc_from_transformed(bt, lat, SC_DUAL)
+                bs, xs = ctx.skeleton(), ctx.skeleton()
+                ctx.sc_to_transformed(lat, bs, SC_PERM)
+                r = ctx.sc_pcg_solve_nodal(bs, xs, op="tpc", prec={"bc": "block", "dc": "diag", "uc": "none"}[solver],
+                                           rtol=1e-12, maxit=20000)
+                ctx.sc_from_transformed(xs, lat, SC_PERM)
+                ctx.sc_to_transformed(lat, xt, SC_PRIMAL)
             u = ctx.lattice()
             ctx.sc_recover_dirichlet(f, gd, xt, u)
             torch.cuda.synchronize()
@@ -82,16 +94,16 @@ def main():
             ctx.close()
             del ctx
         t = float(np.mean(times[1:])) if len(times) > 1 else times[0]
-        row = dict(p=p, alpha=alpha, n=n, ar_max=float(alpha ** (n - 1)), iters=its, converged=conv,
+        row = dict(solver=solver, p=p, alpha=alpha, n=n, ar_max=float(alpha ** (n - 1)), iters=its, converged=conv,
                    s_per_solve=t, s_pcg=t_pcg, s_per_iter=t_pcg / max(its, 1), max_err=err, kernel=kern,
                    N=int(len(xs) * len(ys) * len(zs)))
         rows.append(row)
         print(json.dumps(row), flush=True)
     summary = {}
-    for p, n in sorted({(r["p"], r["n"]) for r in rows}):
-        it = {r["alpha"]: r["iters"] for r in rows if r["p"] == p and r["n"] == n}
+    for sv, p, n in sorted({(r["solver"], r["p"], r["n"]) for r in rows}):
+        it = {r["alpha"]: r["iters"] for r in rows if r["p"] == p and r["n"] == n and r["solver"] == sv}
         if 1.0 in it and 2.0 in it:
-            summary[f"p{p}_n{n}"] = dict(iters=it, growth_a2_over_a1=it[2.0] / it[1.0])
+            summary[f"{sv}_p{p}_n{n}"] = dict(iters=it, growth_a2_over_a1=it[2.0] / it[1.0])
     out = dict(study="E3 (P:625-687): 8^3 graded, k = 5, lambda = 0, inhomogeneous Dirichlet, rtol 1e-12",
                k=a.k, ns=a.ns, reps=a.reps, rows=rows, iteration_growth=summary,
                paper="iterations grow by about 1.5x from AR_max 1 to 128 for BC and BT (P:684)",
