@@ -429,7 +429,9 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
     // SC_SMALL_V1=0 disables the switch (the parity tests use it to exercise the fast kernels)
     const char* sv = getenv("SC_SMALL_V1");
     const long long ne_local = (long long)nx * ny * nz;
-    const bool small_v1 = !(sv && sv[0] == '0') && ne_local <= (p <= 8 ? 2048 : 256);
+    // thresholds measured at n_e = 512 (profiles/variants_r2.json): v1 0.028 / 0.036 / 0.045 /
+    // 0.059 ms vs the colour launches 0.085 / 0.069 / 0.073 / 0.086 ms at p = 10 / 12 / 14 / 16
+    const bool small_v1 = !(sv && sv[0] == '0') && ne_local <= (p <= 8 ? 2048 : (p <= 16 ? 512 : 256));
     const char* env0 = getenv("SC_APPLY_V1");
     const char* env = small_v1 ? "1" : env0;
     bool sig_ok = true;

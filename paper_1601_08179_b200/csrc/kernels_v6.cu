@@ -480,6 +480,21 @@ __device__ __forceinline__ void edge_phase(const V5Params& P, const View<H>& V, 
 // L2 and costs no DRAM traffic).  The x- / y-face primaries are computed entity-centrically into
 // the owned accumulators before the class phase.
 // =============================================================================================
+// smallest k stride >= pj * p1 such that {si + pj sj + pk sk} (si, sj, sk in {0, 1}) are distinct mod 16
+constexpr bool di_ok(int pj, int pk) {
+  int o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int c = 0; c < 8; ++c) o[c] = ((c & 1) + pj * ((c >> 1) & 1) + pk * (c >> 2)) % 16;
+  for (int a = 0; a < 8; ++a)
+    for (int b = a + 1; b < 8; ++b)
+      if (o[a] == o[b]) return false;
+  return true;
+}
+constexpr int di_pk(int pj, int p1) {
+  for (int pk = pj * p1; pk < pj * p1 + 16; ++pk)
+    if (di_ok(pj, pk)) return pk;
+  return pj * p1;
+}
+
 template <int NI, int H>
 struct L6 {
   using B = L<NI, H>;
@@ -502,7 +517,12 @@ struct L6 {
   // direction) read a 0 there, so they contribute exact zeros to every sum and to the energy
   // (with the unpadded stride NI they would alias real entries)
   static constexpr int P1 = NI + 1;
-  static constexpr int DIN = even(P1 * P1 * P1);
+  // j / k strides of the table: the 8 class bases si + PJ sj + PK sk of a warp's lanes fall on 8
+  // distinct 8-byte bank pairs (distinct mod 16 doubles), so a class-phase D^{-1} load is one
+  // wavefront (with PK = P1^2 the s_k = 0 / 1 classes collided: 2-way conflicts, r2s ncu)
+  static constexpr int PJ = P1;
+  static constexpr int PK = di_pk(P1, P1);
+  static constexpr int DIN = even(PK * P1);
   static constexpr int O_DI = O_CT + CT_N;
   static constexpr int O_SCR = O_DI + DIN;                 // scratch row of stores that own nothing
   static constexpr int O_AZ = O_SCR + even(N2);            // owned z-faces of plane l
@@ -576,7 +596,7 @@ __global__ void __launch_bounds__(64 * H, H == 4 ? 2 : 1) k_apply_v6(const __gri
     ct[L6T::CT_FDY + t] = cf.fdy[t];
   }
   for (int t = tid; t < L6T::DIN; t += NT) {
-    const int i = t % L6T::P1, j = (t / L6T::P1) % L6T::P1, k = t / (L6T::P1 * L6T::P1);
+    const int k = t / L6T::PK, r = t - k * L6T::PK, j = r / L6T::PJ, i = r - j * L6T::PJ;
     sdi[t] = (i < NI && j < NI && k < NI) ? cf.dinv[i + NI * (j + NI * k)] : 0.0;
   }
   if (tid < NROWS) make_row<NI, H>(g, tid, cx0, cy0, rows[tid]);
@@ -668,7 +688,7 @@ __global__ void __launch_bounds__(64 * H, H == 4 ? 2 : 1) k_apply_v6(const __gri
       const double* Nn = V.yf(iy + 1) + ix * N2 + si + NI * sk;
       const double* Bf = V.zf(0, iy) + ix * N2 + si + NI * sj;   // z-face entries (i, j)
       const double* Tf = V.zf(1, iy) + ix * N2 + si + NI * sj;
-      const double* Dc = sdi + si + L6T::P1 * (sj + L6T::P1 * sk);   // D^{-1}(si + 2ii, sj + 2jj, sk + 2kk)
+      const double* Dc = sdi + si + L6T::PJ * sj + L6T::PK * sk;   // D^{-1}(si + 2ii, sj + 2jj, sk + 2kk)
       // primaries (Eq. 26 generalised) of the faces this lane stores: x (s_i = 0 lanes, entries (j, k)),
       // y (s_j = 0, entries (i, k)), plane-l z-face (s_k = 0) / plane-(l+1) z-face (s_k = 1) entries (i, j)
       const double* Wm = W - N2;                                  // x-face fx - 1 (same entries)
@@ -721,7 +741,7 @@ __global__ void __launch_bounds__(64 * H, H == 4 ? 2 : 1) k_apply_v6(const __gri
 #pragma unroll
           for (int ii = 0; ii < M; ++ii) {
             const double u = fma(c1r[ii], xin, fma(c2, yin[ii], c3 * zin[ii][jj]));
-            const double v = u * Dc[2 * ii + 2 * L6T::P1 * jj + 2 * L6T::P1 * L6T::P1 * kk];
+            const double v = u * Dc[2 * ii + 2 * L6T::PJ * jj + 2 * L6T::PK * kk];
             if (DOT) en = fma(u, v, en);
             qx = fma(c1r[ii], v, qx);
             qy[ii] = fma(c2, v, qy[ii]);
