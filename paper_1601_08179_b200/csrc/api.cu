@@ -151,6 +151,8 @@ struct sc_ctx {
   bool use_col = false;
   bool use_big = false;
   bool use_p2 = false;                  // p = 2 row-warp operator (kernels_p2.cu)
+  bool use_p2s = false;                 // p = 2 owner-computes stencil (kernels_p2s.cu, one rank)
+  std::vector<double> p2s_coef;
   bool use_rw = false;                  // p = 3, 4 row-warp operator (kernels_rw.cu)
   bool use_v6 = false;                  // 3 <= p <= 8 halo-recompute tile columns (kernels_v6.cu)
   std::vector<unsigned char> v6_coef;
@@ -469,8 +471,18 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
       ctx->fused_dot = !(fd && fd[0] == '0');
       ctx->use_v6 = true;
     } else if (ni == 1 && uniform && sig_ok && !(env && env[0] == '1') && !(np2 && np2[0] == '1')) {
-      big_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->big_coef);
-      ctx->use_p2 = true;
+      // one rank: the owner-computes stencil (every free node's elements are all local); z-slab
+      // ranks keep the colour-scheduled kernel, whose interface planes hold local partial sums.
+      // SC_P2_COLOUR=1 forces the colour-scheduled kernel.
+      const char* pc = getenv("SC_P2_COLOUR");
+      std::string perr;
+      if (prm->nranks == 1 && !(pc && pc[0] == '1') &&
+          p2s_make_coef(g.d_uni, B.lam[0], B.a0[0], B.ap[0], B.K00, B.K0p, B.w0, ctx->p2s_coef, perr)) {
+        ctx->use_p2s = true;
+      } else {
+        big_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->big_coef);
+        ctx->use_p2 = true;
+      }
     } else if (rw_supported(ni) && uniform && sig_ok && !(env && env[0] == '1') && !(nrw && nrw[0] == '1') &&
                op != "v3") {
       big_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->big_coef);
@@ -505,7 +517,7 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
       ctx->use_col = true;
     }
     // v4 also runs non-uniform grids: each CTA derives its element's coefficients from d_e
-    if (!ctx->use_v6 && !ctx->use_col && !ctx->use_p2 && !ctx->use_rw && big_supported(ni) && sig_ok && !(env && env[0] == '1')) {
+    if (!ctx->use_v6 && !ctx->use_col && !ctx->use_p2 && !ctx->use_p2s && !ctx->use_rw && big_supported(ni) && sig_ok && !(env && env[0] == '1')) {
       const double d_one[4] = {1.0, 1.0, 1.0, 1.0};
       big_make_coef(ni, uniform ? g.d_uni : d_one, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->big_coef);
       ctx->use_big = true;
@@ -775,6 +787,8 @@ static sc_status apply_impl(sc_ctx* ctx, const double* x, double* y, const doubl
     LAUNCH(launch_apply_col_raw(ctx->g, x, y, done, ctx->d_colstate, ctx->d_flags, ctx->d_corner, ctx->d_pending,
                                 ctx->col_ntx, ctx->col_nty, ctx->col_nseg, ctx->col_zseg, ctx->col_coef.data(), dotp,
                                 st, &nl_, ev));
+  else if (ctx->use_p2s)
+    LAUNCH(launch_apply_p2s(ctx->g, x, y, done, ctx->p2s_coef.data(), st, &nl_, ev));
   else if (ctx->use_p2)
     LAUNCH(launch_apply_p2(ctx->g, x, y, done, ctx->big_coef.data(), st, &nl_, ev));
   else if (ctx->use_rw)
@@ -1330,6 +1344,7 @@ extern "C" const char* sc_operator_kernel(const sc_ctx* ctx) {
   if (!ctx) return "";
   if (ctx->use_v6) return ctx->v6_h == 8 ? "v6h8" : "v6";
   if (ctx->use_col) return "v3";
+  if (ctx->use_p2s) return "p2s";
   if (ctx->use_p2) return "p2";
   if (ctx->use_rw) return "rw";
   if (ctx->use_big) return "v4";

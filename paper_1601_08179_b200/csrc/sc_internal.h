@@ -94,6 +94,10 @@ enum {
 int launch_apply(const Geom& g, const double* x, double* y, const double* done, void* stream, int* nlaunch,
                  void* events = nullptr);
 int launch_diag(const Geom& g, double* diag, void* stream, int* nlaunch);
+bool p2s_make_coef(const double d[4], double lam, double a0, double ap, double K00, double K0p, double w0,
+                   std::vector<double>& coef, std::string& err);
+int launch_apply_p2s(const Geom& g, const double* x, double* y, const double* done, const double* coef, void* stream,
+                     int* nlaunch, void* events = nullptr);
 int launch_apply_tpc(const Geom& g, const double* vt, const double* x, double* y, void* stream, int* nlaunch,
                      void* events = nullptr);
 int launch_mmc_columns(const Geom& g, const double* vt, double* H, int nB, long long ngeom, void* stream, int* nlaunch);

@@ -129,3 +129,30 @@ def test_family_v6_bitwise_repeatable(h, monkeypatch):
         ctx.sc_apply_condensed(x, y)
         torch.cuda.synchronize()
         assert torch.equal(y, y0)
+
+
+@pytest.mark.parametrize("ne,lam", [((2, 2, 2), 1.0), ((37, 5, 4), 0.3), ((33, 32, 3), 0.0), ((1, 1, 3), 1.0)])
+def test_p2_owner_stencil(ne, lam, monkeypatch):
+    """p = 2 owner-computes stencil (kernels_p2s.cu, the default on one rank) against the oracle and
+    against the colour-scheduled kernel (SC_P2_COLOUR=1); every entry written once (stale y
+    overwritten, padding 0), repeated applications bitwise equal."""
+    from paper_1601_08179_b200 import Context
+    g = small_grid(2, ne, lam, lengths=(1.3, 0.9, 0.7))
+    x = lattice_random(33, g.ne, g.p).ravel()
+    ctx = Context(g.p, g.ne, (g.hx, g.hy, g.hz), g.lam, device=0)
+    assert ctx.operator_kernel() == "p2s"
+    ref = operator.AssembledCondensedOperator(g).apply(x)
+    assert _rel(_apply_nodal(ctx, x), ref) <= 1e-12
+    xt = ctx.skeleton()
+    ctx.sc_fill_random(4, xt)
+    y1 = ctx.skeleton(fill=float("nan"))
+    ctx.sc_apply_condensed(xt, y1)
+    y2 = ctx.skeleton(fill=5.0)
+    ctx.sc_apply_condensed(xt, y2)
+    assert torch.equal(y1, y2)
+    monkeypatch.setenv("SC_P2_COLOUR", "1")
+    ctx2 = Context(g.p, g.ne, (g.hx, g.hy, g.hz), g.lam, device=0)
+    assert ctx2.operator_kernel() == "p2"
+    y3 = ctx2.skeleton()
+    ctx2.sc_apply_condensed(xt, y3)
+    assert (y1 - y3).norm() <= 1e-13 * y3.norm()
