@@ -263,7 +263,8 @@ sc_status sc_pcg_solve_nodal(sc_ctx* ctx, int op, int prec, const double* d_b, d
                              int maxit, sc_pcg_report* rep, void* stream);
 
 /* Operator kernel family this ctx runs: "v6" / "v6h8" (halo-recompute tile columns,
- * 3 <= p <= 8), "v3" (tile columns with look-back), "rw" / "p2" (row-warp kernels, p <= 4),
+ * 3 <= p <= 8), "v3" (tile columns with look-back), "v7" (two-pass, opt-in), "rw" (row-warp, p = 3, 4),
+ * "p2s" (owner-computes stencil, p = 2, one rank) / "p2" (colour-scheduled row-warp, p = 2),
  * "v4" (colour-scheduled element CTAs, p >= 9), "v1" (one CTA per element, any geometry). */
 const char* sc_operator_kernel(const sc_ctx* ctx);
 

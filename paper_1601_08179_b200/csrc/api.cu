@@ -155,6 +155,9 @@ struct sc_ctx {
   std::vector<double> p2s_coef;
   bool use_rw = false;                  // p = 3, 4 row-warp operator (kernels_rw.cu)
   bool use_v6 = false;                  // 3 <= p <= 8 halo-recompute tile columns (kernels_v6.cu)
+  bool use_v7 = false;                  // 3 <= p <= 8 two-pass operator (kernels_v7.cu, one rank)
+  std::vector<unsigned char> v7_coef;
+  double* d_u7 = nullptr;               // v7 face-part vectors u0 | u1 (2 n_total doubles)
   std::vector<unsigned char> v6_coef;
   int v6_ntx = 0, v6_nty = 0, v6_nseg = 1, v6_zseg = 0;
   int v6_h = 4;                         // compute-tile height: 4 (2 CTAs per SM) or 8 (1 CTA of 16 warps)
@@ -449,7 +452,16 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
     // (7.86 ms at cfg5; v3 kept there: its fused p . q is the one the round-1 bench validated);
     // the row-warp kernels fastest for p = 3, 4
     const bool want_v6 = op == "v6" || (op.empty() && ni >= 4 && ni <= 6);
-    if (v6_supported(ni) && uniform && sig_ok && want_v6 && !(env && env[0] == '1')) {
+    const bool want_v7 = op == "v7";
+    if (v7_supported(ni) && uniform && sig_ok && want_v7 && prm->nranks == 1 && !(env && env[0] == '1')) {
+      v7_make_coef(ni, g.d_uni, B.a0, B.ap, B.lam, B.K00, B.K0p, B.w0, ctx->v7_coef);
+      if (cudaMalloc(&ctx->d_u7, sizeof(double) * 2 * (size_t)g.n_total) != cudaSuccess) return fail("cudaMalloc u7");
+      if (cudaMemset(ctx->d_u7, 0, sizeof(double) * 2 * (size_t)g.n_total) != cudaSuccess) return fail("memset u7");
+      if (cudaMalloc(&ctx->d_dotp, sizeof(double) * (size_t)v7_dot_parts(g)) != cudaSuccess) return fail("cudaMalloc dotp");
+      const char* fd = getenv("SC_FUSED_DOT");
+      ctx->fused_dot = !(fd && fd[0] == '0');
+      ctx->use_v7 = true;
+    } else if (v6_supported(ni) && uniform && sig_ok && want_v6 && !(env && env[0] == '1')) {
       const char* hs = getenv("SC_V6_H");
       ctx->v6_h = (hs && atoi(hs) == 8) ? 8 : ((hs && atoi(hs) == 4) ? 4 : 4);
       v6_make_coef(ni, g.d_uni, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->v6_coef);
@@ -517,7 +529,7 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
       ctx->use_col = true;
     }
     // v4 also runs non-uniform grids: each CTA derives its element's coefficients from d_e
-    if (!ctx->use_v6 && !ctx->use_col && !ctx->use_p2 && !ctx->use_p2s && !ctx->use_rw && big_supported(ni) && sig_ok && !(env && env[0] == '1')) {
+    if (!ctx->use_v6 && !ctx->use_v7 && !ctx->use_col && !ctx->use_p2 && !ctx->use_p2s && !ctx->use_rw && big_supported(ni) && sig_ok && !(env && env[0] == '1')) {
       const double d_one[4] = {1.0, 1.0, 1.0, 1.0};
       big_make_coef(ni, uniform ? g.d_uni : d_one, B.a0, B.lam, B.K00, B.K0p, B.w0, ctx->big_coef);
       ctx->use_big = true;
@@ -561,6 +573,7 @@ extern "C" sc_status sc_destroy(sc_ctx* ctx) {
   if (ctx->d_corner) cudaFree(ctx->d_corner);
   if (ctx->d_pending) cudaFree(ctx->d_pending);
   if (ctx->d_dotp) cudaFree(ctx->d_dotp);
+  if (ctx->d_u7) cudaFree(ctx->d_u7);
   if (ctx->d_vt) cudaFree(ctx->d_vt);
   cublas_destroy(ctx->cublas);
   if (ctx->pcg_graph) cudaGraphExecDestroy(ctx->pcg_graph);
@@ -780,7 +793,10 @@ static sc_status apply_impl(sc_ctx* ctx, const double* x, double* y, const doubl
                             double* dotp = nullptr) {
   const bool rec = ctx->prof_on && ctx->prof_n < (int)ctx->prof_ev.size() / 2;
   cudaEvent_t* ev = rec ? &ctx->prof_ev[2 * ctx->prof_n] : nullptr;
-  if (ctx->use_v6)
+  if (ctx->use_v7)
+    LAUNCH(launch_apply_v7(ctx->g, x, y, ctx->d_u7, ctx->d_u7 + ctx->g.n_total, done, ctx->v7_coef.data(), dotp, st,
+                           &nl_, ev));
+  else if (ctx->use_v6)
     LAUNCH(launch_apply_v6(ctx->g, x, y, done, ctx->v6_ntx, ctx->v6_nty, ctx->v6_nseg, ctx->v6_zseg,
                            ctx->v6_coef.data(), dotp, st, &nl_, ev, ctx->v6_h));
   else if (ctx->use_col)
@@ -831,8 +847,9 @@ static sc_status pcg_iteration(sc_ctx* ctx, cudaStream_t st) {
   // (Early in round 1, with a slower operator, it measured slower: 10.67 vs 9.55 + 0.9 ms.)
   // v6 returns per-CTA partials of x . A x over its owned entities / elements, which sum to p . q on
   // any number of ranks (each rank's partial interface-plane sums included): fused there on every rank.
-  const bool fused = ((ctx->use_col && ctx->prm.nranks == 1) || ctx->use_v6) && ctx->fused_dot;
-  const int nparts = ctx->use_v6 ? ctx->v6_ntx * ctx->v6_nty * ctx->v6_nseg : ctx->col_ntx * ctx->col_nty * ctx->col_nseg;
+  const bool fused = ((ctx->use_col && ctx->prm.nranks == 1) || ctx->use_v6 || ctx->use_v7) && ctx->fused_dot;
+  const int nparts = ctx->use_v7 ? (int)v7_dot_parts(ctx->g)
+                     : ctx->use_v6 ? ctx->v6_ntx * ctx->v6_nty * ctx->v6_nseg : ctx->col_ntx * ctx->col_nty * ctx->col_nseg;
   sc_status s = apply_impl(ctx, ctx->pv, ctx->q, done, st, fused ? ctx->d_dotp : nullptr);
   if (s) return s;
   if (fused) {
@@ -1342,6 +1359,7 @@ extern "C" long long sc_launch_count(const sc_ctx* ctx) { return ctx ? ctx->nlau
 
 extern "C" const char* sc_operator_kernel(const sc_ctx* ctx) {
   if (!ctx) return "";
+  if (ctx->use_v7) return "v7";
   if (ctx->use_v6) return ctx->v6_h == 8 ? "v6h8" : "v6";
   if (ctx->use_col) return "v3";
   if (ctx->use_p2s) return "p2s";

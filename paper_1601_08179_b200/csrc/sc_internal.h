@@ -98,6 +98,12 @@ bool p2s_make_coef(const double d[4], double lam, double a0, double ap, double K
                    std::vector<double>& coef, std::string& err);
 int launch_apply_p2s(const Geom& g, const double* x, double* y, const double* done, const double* coef, void* stream,
                      int* nlaunch, void* events = nullptr);
+bool v7_supported(int ni);
+void v7_make_coef(int ni, const double* d, const double* a0, const double* ap, const double* lam, double K00,
+                  double K0p, double w0, std::vector<unsigned char>& out);
+long long v7_dot_parts(const Geom& g);
+int launch_apply_v7(const Geom& g, const double* x, double* y, double* u0, double* u1, const double* done,
+                    const void* coef, double* dotp, void* stream, int* nlaunch, void* events = nullptr);
 int launch_apply_tpc(const Geom& g, const double* vt, const double* x, double* y, void* stream, int* nlaunch,
                      void* events = nullptr);
 int launch_mmc_columns(const Geom& g, const double* vt, double* H, int nB, long long ngeom, void* stream, int* nlaunch);

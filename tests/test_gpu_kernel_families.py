@@ -25,7 +25,7 @@ def _ctx(g, monkeypatch, op, h=None, **kw):
     if h is not None:
         monkeypatch.setenv("SC_V6_H", str(h))
     ctx = Context(g.p, g.ne, (g.hx, g.hy, g.hz), g.lam, device=0, **kw)
-    want = {"v6": "v6h8" if h == 8 else "v6", "v3": "v3", "rw": "rw"}[op]
+    want = {"v6": "v6h8" if h == 8 else "v6", "v3": "v3", "rw": "rw", "v7": "v7"}[op]
     assert ctx.operator_kernel() == want, (ctx.operator_kernel(), want)
     return ctx
 
@@ -156,3 +156,48 @@ def test_p2_owner_stencil(ne, lam, monkeypatch):
     y3 = ctx2.skeleton()
     ctx2.sc_apply_condensed(xt, y3)
     assert (y1 - y3).norm() <= 1e-13 * y3.norm()
+
+
+V7_CASES = [(3, (17, 9, 3)), (4, (9, 8, 3)), (5, (15, 7, 3)), (6, (9, 10, 2)), (7, (16, 4, 3)), (8, (9, 7, 3)),
+            (8, (33, 5, 4)), (8, (1, 1, 2)), (5, (2, 17, 3))]
+
+
+@pytest.mark.parametrize("p,ne", V7_CASES)
+def test_family_v7_operator_parity(p, ne, monkeypatch):
+    """v7 (two passes: unassembled condensed part, then entity-wise assembly + primary part) against
+    the oracle on ragged multi-run grids; every entry overwritten (stale y), repeatable bitwise."""
+    g = small_grid(p, ne, 0.7, lengths=(1.2, 0.9, 0.6))
+    ref_op = operator.AssembledCondensedOperator(g)
+    x = lattice_random(90 + p, g.ne, g.p).ravel()
+    ctx = _ctx(g, monkeypatch, "v7")
+    assert _rel(_apply_nodal(ctx, x), ref_op.apply(x)) <= 1e-12
+    xt = ctx.skeleton()
+    ctx.sc_fill_random(2, xt)
+    y1 = ctx.skeleton(fill=float("nan"))
+    ctx.sc_apply_condensed(xt, y1)
+    y2 = ctx.skeleton(fill=3.0)
+    ctx.sc_apply_condensed(xt, y2)
+    assert torch.equal(y1, y2)
+
+
+@pytest.mark.parametrize("p,ne", [(5, (15, 7, 4)), (8, (10, 6, 3))])
+def test_family_v7_pcg_fused_dot(p, ne, monkeypatch):
+    """BT-PCG on v7 with p . q from pass B's per-block x . y partials, against the oracle."""
+    from paper_1601_08179_b200 import SC_DUAL
+    g = small_grid(p, ne, 1.0, lengths=(1.3, 0.7, 0.5))
+    ref_op = operator.AssembledCondensedOperator(g)
+    ctx = _ctx(g, monkeypatch, "v7")
+    bt = ctx.skeleton()
+    ctx.sc_fill_random(8, bt)
+    lat = ctx.lattice()
+    ctx.sc_from_transformed(bt, lat, SC_DUAL)
+    b = lat.cpu().numpy()
+    P = solve.BlockJacobi(ref_op)
+    norm = solve.transformed_norm(g, ref_op.skel)
+    res = pcg.pcg(ref_op.apply, P.apply, b, rtol=1e-10, norm=norm)
+    xt = ctx.skeleton()
+    rep = ctx.sc_pcg_solve(bt, xt, rtol=1e-10, maxit=2000)
+    assert rep.converged and abs(rep.iters - res.iters) <= 1, (rep.iters, res.iters)
+    ref = res.x if rep.iters == res.iters else pcg.pcg(ref_op.apply, P.apply, b, rtol=0, norm=norm,
+                                                       fixed_iters=rep.iters).x
+    assert _rel(ctx.to_lattice_nodal(xt).cpu().numpy(), ref) <= 1e-10
