@@ -71,6 +71,12 @@ __host__ __device__ constexpr int di_pk(int pj, int p1) {
   return pj * p1;
 }
 
+// 8-byte global -> shared copy, zero fill when !ok (src-size 0)
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool ok) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
+}
+
 // ------------------------------------------------------------------------------------ pass A
 template <int NI>
 __global__ void __launch_bounds__(128, 4) k_v7_cond(const __grid_constant__ V7Params P) {
@@ -97,11 +103,12 @@ __global__ void __launch_bounds__(128, 4) k_v7_cond(const __grid_constant__ V7Pa
   }
   if (tid < 24) sC[tid / 8][tid % 8] = (tid % 8) < NI ? cf.c[tid / 8][tid % 8] : 0.0;
   // faces of the run (Dirichlet faces and faces beyond the slab read as 0)
-  {
+  {   // asynchronous 8-byte copies (cp.async, zero-filled where masked): all of a thread's loads in flight
     const long long xb = g.off_f[0] + ((long long)ex0 + (long long)(nx + 1) * (ey + (long long)ny * ez)) * N2;
     for (int t = tid; t < (RUN + 1) * N2; t += 128) {
       const int fx = ex0 + t / N2;
-      sX[t] = (t < (cnt + 1) * N2 && fx > 0 && fx < nx) ? P.x[xb + t] : 0.0;
+      const bool ok = t < (cnt + 1) * N2 && fx > 0 && fx < nx;
+      cp_async8(sX + t, P.x + (ok ? xb + t : 0), ok);
     }
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
@@ -113,10 +120,11 @@ __global__ void __launch_bounds__(128, 4) k_v7_cond(const __grid_constant__ V7Pa
       const long long zb = g.off_f[2] + ((long long)ex0 + (long long)nx * (ey + (long long)ny * fz)) * N2;
       for (int t = tid; t < RUN * N2; t += 128) {
         const bool in = t < cnt * N2;
-        sY[s][t] = (in && fok) ? P.x[yb + t] : 0.0;
-        sZ[s][t] = (in && zok) ? P.x[zb + t] : 0.0;
+        cp_async8(sY[s] + t, P.x + ((in && fok) ? yb + t : 0), in && fok);
+        cp_async8(sZ[s] + t, P.x + ((in && zok) ? zb + t : 0), in && zok);
       }
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
   }
   __syncthreads();
   const int warp = tid >> 5, lane = tid & 31;
@@ -229,81 +237,80 @@ __global__ void __launch_bounds__(256) k_v7_assemble(const __grid_constant__ V7P
   const double* __restrict__ x = P.x;
   const int row = blockIdx.y;   // y-ish index + (count) * z-ish index
   double dot = 0.0;
+  // lane-indexed coefficients from shared memory (indexed kernel-parameter loads serialise per address)
+  __shared__ double sfd[49], sa0[8], sap[8], sself[8];
+  {
+    const int f = cls <= 2 ? cls : 0, e = cls >= 3 && cls <= 5 ? cls - 3 : 0;
+    for (int q = threadIdx.x; q < N2; q += blockDim.x) sfd[q] = cf.fd[f][q];
+    if (threadIdx.x < 8) {
+      sa0[threadIdx.x] = cf.a0[threadIdx.x];
+      sap[threadIdx.x] = cf.ap[threadIdx.x];
+      sself[threadIdx.x] = cf.eself[e][threadIdx.x];
+    }
+    __syncthreads();
+  }
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   // all rows are (x-run of entities) x (per-entity entries); decode (a = x index, e = entry)
   if (cls <= 2) {
-    // ---------------- faces
-    const int a = t / N2, e = t - a * N2;
+    // ---------------- faces: one thread per (face, first in-plane entry ea), loop over the second (eb).
+    // y(ea, eb) = fd u + K0p-term (opposite faces) + wA (a0_ea A0[eb] + ap_ea A1[eb]) + wB (a0_eb B0[ea] + ap_eb B1[ea])
+    //             + U0 + U1;  A = the edges along the second in-plane direction, B = along the first.
+    const int a = t / NI, ea = t - a * NI;
     const int rowlen = cls == 0 ? nx + 1 : nx;
     if (a < rowlen) {
-      const int ea = e % NI, eb = e / NI;   // in-plane entry (first, second coordinate)
-      int fx, fy, fz, ex_, ey_, ez_;
-      long long fid;
-      bool fr;
-      double yv = 0.0;
-      if (cls == 0) {
-        const int eyy = row % ny, ezz = row / ny;
-        fx = a; ey_ = eyy; ez_ = ezz;
+      long long fid, so, ia0, ia1, ib0, ib1;
+      bool fr, olo, ohi, oka0, oka1, okb0, okb1;
+      double wA, wB, kf;
+      if (cls == 0) {            // x-face (fx, ey, ez): A = z-edges (fx, ey / ey+1, ez), B = y-edges (fx, ey, ez / ez+1)
+        const int ey_ = row % ny, ez_ = row / ny, fx = a;
         fid = fx + nx1 * (ey_ + (long long)ny * ez_);
         fr = in_f(fx, nx);
-        if (fr) {
-          const long long i0 = g.off_f[0] + fid * N2 + e;
-          const double u = __ldg(x + i0);
-          const double uo = ldv<NI>(x, i0 - N2, fx - 1 > 0) + ldv<NI>(x, i0 + N2, fx + 1 < nx);
-          // z-edges (fx, fy = ey / ey + 1, ez) entry k = eb; y-edges (fx, ey, fz = ez / ez + 1) entry j = ea
-          const long long zs = g.off_e[2] + (fx + nx1 * (ey_ + ny1 * ez_)) * NI + eb;
-          const long long zn = zs + nx1 * NI;
-          const long long yb = g.off_e[1] + (fx + nx1 * (ey_ + (long long)ny * ez_)) * NI + ea;
-          const long long yt = yb + nx1 * ny * NI;
-          const double ze = cf.a0[ea] * ldv<NI>(x, zs, in_f(ey_, ny)) + cf.ap[ea] * ldv<NI>(x, zn, in_f(ey_ + 1, ny));
-          const double ye = cf.a0[eb] * ldv<NI>(x, yb, !zdir(g, ez_)) + cf.ap[eb] * ldv<NI>(x, yt, !zdir(g, ez_ + 1));
-          yv = cf.fd[0][e] * u + cf.kf[0] * uo + cf.ef[0][1] * ze + cf.ef[0][2] * ye + P.u0[i0] + P.u1[i0];
-          if (DOT) dot = u * yv;
-        }
-        P.y[g.off_f[0] + fid * N2 + e] = yv;
-      } else if (cls == 1) {
-        const int fyy = row % (ny + 1), ezz = row / (ny + 1);
-        ex_ = a; fy = fyy; ez_ = ezz;
+        so = N2; olo = fx - 1 > 0; ohi = fx + 1 < nx;
+        ia0 = g.off_e[2] + (fx + nx1 * (ey_ + ny1 * ez_)) * NI; ia1 = ia0 + nx1 * NI;
+        oka0 = in_f(ey_, ny); oka1 = in_f(ey_ + 1, ny);
+        ib0 = g.off_e[1] + (fx + nx1 * (ey_ + (long long)ny * ez_)) * NI + ea; ib1 = ib0 + nx1 * ny * NI;
+        okb0 = !zdir(g, ez_); okb1 = !zdir(g, ez_ + 1);
+        wA = cf.ef[0][1]; wB = cf.ef[0][2]; kf = cf.kf[0];
+      } else if (cls == 1) {     // y-face (ex, fy, ez): A = z-edges (ex / ex+1, fy, ez), B = x-edges (ex, fy, ez / ez+1)
+        const int fy = row % (ny + 1), ez_ = row / (ny + 1), ex_ = a;
         fid = ex_ + (long long)nx * (fy + ny1 * ez_);
         fr = in_f(fy, ny);
-        if (fr) {
-          const long long i0 = g.off_f[1] + fid * N2 + e;
-          const double u = __ldg(x + i0);
-          const double uo = ldv<NI>(x, i0 - (long long)nx * N2, fy - 1 > 0) + ldv<NI>(x, i0 + (long long)nx * N2, fy + 1 < ny);
-          // z-edges (fx = ex / ex + 1, fy, ez) entry k = eb; x-edges (ex, fy, fz = ez / ez + 1) entry i = ea
-          const long long zw = g.off_e[2] + (ex_ + nx1 * (fy + ny1 * ez_)) * NI + eb;
-          const long long zeI = zw + NI;
-          const long long xb = g.off_e[0] + (ex_ + (long long)nx * (fy + ny1 * ez_)) * NI + ea;
-          const long long xt = xb + (long long)nx * ny1 * NI;
-          const double ze = cf.a0[ea] * ldv<NI>(x, zw, in_f(ex_, nx)) + cf.ap[ea] * ldv<NI>(x, zeI, in_f(ex_ + 1, nx));
-          const double xe = cf.a0[eb] * ldv<NI>(x, xb, !zdir(g, ez_)) + cf.ap[eb] * ldv<NI>(x, xt, !zdir(g, ez_ + 1));
-          yv = cf.fd[1][e] * u + cf.kf[1] * uo + cf.ef[1][0] * ze + cf.ef[1][2] * xe + P.u0[i0] + P.u1[i0];
-          if (DOT) dot = u * yv;
-        }
-        P.y[g.off_f[1] + fid * N2 + e] = yv;
-      } else {
-        const int eyy = row % ny, fzz = row / ny;
-        ex_ = a; ey_ = eyy; fz = fzz;
+        so = (long long)nx * N2; olo = fy - 1 > 0; ohi = fy + 1 < ny;
+        ia0 = g.off_e[2] + (ex_ + nx1 * (fy + ny1 * ez_)) * NI; ia1 = ia0 + NI;
+        oka0 = in_f(ex_, nx); oka1 = in_f(ex_ + 1, nx);
+        ib0 = g.off_e[0] + (ex_ + (long long)nx * (fy + ny1 * ez_)) * NI + ea; ib1 = ib0 + (long long)nx * ny1 * NI;
+        okb0 = !zdir(g, ez_); okb1 = !zdir(g, ez_ + 1);
+        wA = cf.ef[1][0]; wB = cf.ef[1][2]; kf = cf.kf[1];
+      } else {                   // z-face (ex, ey, fz): A = y-edges (ex / ex+1, ey, fz), B = x-edges (ex, ey / ey+1, fz)
+        const int ey_ = row % ny, fz = row / ny, ex_ = a;
         fid = ex_ + (long long)nx * (ey_ + (long long)ny * fz);
         fr = !zdir(g, fz);
-        if (fr) {
-          const long long i0 = g.off_f[2] + fid * N2 + e;
-          const double u = __ldg(x + i0);
-          const long long pl = (long long)nx * ny * N2;
-          const double uo = ldv<NI>(x, i0 - pl, fz - 1 >= 0 && !zdir(g, fz - 1)) + ldv<NI>(x, i0 + pl, fz + 1 <= nz && !zdir(g, fz + 1));
-          // y-edges (fx = ex / ex + 1, ey, fz) entry j = eb; x-edges (ex, fy = ey / ey + 1, fz) entry i = ea
-          const long long yw = g.off_e[1] + (ex_ + nx1 * (ey_ + (long long)ny * fz)) * NI + eb;
-          const long long yeI = yw + NI;
-          const long long xs = g.off_e[0] + (ex_ + (long long)nx * (ey_ + ny1 * fz)) * NI + ea;
-          const long long xn = xs + (long long)nx * NI;
-          const double ye = cf.a0[ea] * ldv<NI>(x, yw, in_f(ex_, nx)) + cf.ap[ea] * ldv<NI>(x, yeI, in_f(ex_ + 1, nx));
-          const double xe = cf.a0[eb] * ldv<NI>(x, xs, in_f(ey_, ny)) + cf.ap[eb] * ldv<NI>(x, xn, in_f(ey_ + 1, ny));
-          yv = cf.fd[2][e] * u + cf.kf[2] * uo + cf.ef[2][0] * ye + cf.ef[2][1] * xe + P.u0[i0] + P.u1[i0];
-          if (DOT) dot = u * yv;
-        }
-        P.y[g.off_f[2] + fid * N2 + e] = yv;
+        so = (long long)nx * ny * N2; olo = fz - 1 >= 0 && !zdir(g, fz - 1); ohi = fz + 1 <= nz && !zdir(g, fz + 1);
+        ia0 = g.off_e[1] + (ex_ + nx1 * (ey_ + (long long)ny * fz)) * NI; ia1 = ia0 + NI;
+        oka0 = in_f(ex_, nx); oka1 = in_f(ex_ + 1, nx);
+        ib0 = g.off_e[0] + (ex_ + (long long)nx * (ey_ + ny1 * fz)) * NI + ea; ib1 = ib0 + (long long)nx * NI;
+        okb0 = in_f(ey_, ny); okb1 = in_f(ey_ + 1, ny);
+        wA = cf.ef[2][0]; wB = cf.ef[2][1]; kf = cf.kf[2];
       }
-      (void)fx; (void)fy; (void)fz; (void)ex_; (void)ey_; (void)ez_;
+      const long long i0 = g.off_f[cls] + fid * N2 + ea;
+      if (fr) {
+        const double b0 = ldv<NI>(x, ib0, okb0), b1 = ldv<NI>(x, ib1, okb1);
+        const double a0e = sa0[ea], ape = sap[ea];
+#pragma unroll
+        for (int eb = 0; eb < NI; ++eb) {
+          const long long i = i0 + NI * eb;
+          const double u = __ldg(x + i);
+          const double uo = ldv<NI>(x, i - so, olo) + ldv<NI>(x, i + so, ohi);
+          const double ea_ = a0e * ldv<NI>(x, ia0 + eb, oka0) + ape * ldv<NI>(x, ia1 + eb, oka1);
+          const double eb_ = sa0[eb] * b0 + sap[eb] * b1;
+          const double yv = sfd[ea + NI * eb] * u + kf * uo + wA * ea_ + wB * eb_ + P.u0[i] + P.u1[i];
+          if (DOT) dot = fma(u, yv, dot);
+          P.y[i] = yv;
+        }
+      } else {
+#pragma unroll
+        for (int eb = 0; eb < NI; ++eb) P.y[i0 + NI * eb] = 0.0;
+      }
     }
   } else if (cls <= 5) {
     // ---------------- edges (entry m along the edge)
@@ -336,7 +343,7 @@ __global__ void __launch_bounds__(256) k_v7_assemble(const __grid_constant__ V7P
           const double nb_y = ldv<NI>(x, i0 - (long long)nx * NI, fy - 1 > 0) + ldv<NI>(x, i0 + (long long)nx * NI, fy + 1 < ny);
           const long long pl = (long long)nx * ny1 * NI;
           const double nb_z = ldv<NI>(x, i0 - pl, fz - 1 >= 0 && !zdir(g, fz - 1)) + ldv<NI>(x, i0 + pl, fz + 1 <= nz && !zdir(g, fz + 1));
-          yv = cf.eself[0][m] * u + cf.ev[0] * (cf.a0[m] * vw + cf.ap[m] * ve) + cf.el[0][1] * fma(cf.K0p, nb_y, lz) +
+          yv = sself[m] * u + cf.ev[0] * (sa0[m] * vw + sap[m] * ve) + cf.el[0][1] * fma(cf.K0p, nb_y, lz) +
                cf.el[0][2] * fma(cf.K0p, nb_z, ly);
           if (DOT) dot = u * yv;
         }
@@ -361,7 +368,7 @@ __global__ void __launch_bounds__(256) k_v7_assemble(const __grid_constant__ V7P
           const double nb_x = ldv<NI>(x, i0 - NI, fx - 1 > 0) + ldv<NI>(x, i0 + NI, fx + 1 < nx);
           const long long pl = nx1 * ny * NI;
           const double nb_z = ldv<NI>(x, i0 - pl, fz - 1 >= 0 && !zdir(g, fz - 1)) + ldv<NI>(x, i0 + pl, fz + 1 <= nz && !zdir(g, fz + 1));
-          yv = cf.eself[1][m] * u + cf.ev[1] * (cf.a0[m] * vs + cf.ap[m] * vn) + cf.el[1][0] * fma(cf.K0p, nb_x, lz) +
+          yv = sself[m] * u + cf.ev[1] * (sa0[m] * vs + sap[m] * vn) + cf.el[1][0] * fma(cf.K0p, nb_x, lz) +
                cf.el[1][2] * fma(cf.K0p, nb_z, lx);
           if (DOT) dot = u * yv;
         }
@@ -385,7 +392,7 @@ __global__ void __launch_bounds__(256) k_v7_assemble(const __grid_constant__ V7P
           }
           const double nb_x = ldv<NI>(x, i0 - NI, fx - 1 > 0) + ldv<NI>(x, i0 + NI, fx + 1 < nx);
           const double nb_y = ldv<NI>(x, i0 - nx1 * NI, fy - 1 > 0) + ldv<NI>(x, i0 + nx1 * NI, fy + 1 < ny);
-          yv = cf.eself[2][m] * u + cf.ev[2] * (cf.a0[m] * vb + cf.ap[m] * vt) + cf.el[2][0] * fma(cf.K0p, nb_x, ly) +
+          yv = sself[m] * u + cf.ev[2] * (sa0[m] * vb + sap[m] * vt) + cf.el[2][0] * fma(cf.K0p, nb_x, ly) +
                cf.el[2][1] * fma(cf.K0p, nb_y, lx);
           if (DOT) dot = u * yv;
         }
@@ -491,12 +498,12 @@ void v7_make_coef(int ni, const double* d, const double* a0, const double* ap, c
 
 // Number of pass-B blocks (the p . q partials the PCG sums).
 static void v7_grid(const Geom& g, int cls, dim3& grid) {
-  const int ni = g.ni, n2 = ni * ni, nx = g.nx, ny = g.ny, nz = g.nz;
+  const int ni = g.ni, nx = g.nx, ny = g.ny, nz = g.nz;
   long long len, rows;
   switch (cls) {
-    case 0: len = (long long)(nx + 1) * n2; rows = (long long)ny * nz; break;
-    case 1: len = (long long)nx * n2; rows = (long long)(ny + 1) * nz; break;
-    case 2: len = (long long)nx * n2; rows = (long long)ny * (nz + 1); break;
+    case 0: len = (long long)(nx + 1) * ni; rows = (long long)ny * nz; break;     // faces: thread per (face, entry row)
+    case 1: len = (long long)nx * ni; rows = (long long)(ny + 1) * nz; break;
+    case 2: len = (long long)nx * ni; rows = (long long)ny * (nz + 1); break;
     case 3: len = (long long)nx * ni; rows = (long long)(ny + 1) * (nz + 1); break;
     case 4: len = (long long)(nx + 1) * ni; rows = (long long)ny * (nz + 1); break;
     case 5: len = (long long)(nx + 1) * ni; rows = (long long)(ny + 1) * nz; break;
