@@ -448,11 +448,11 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
     // the measured fastest per p
     const char* opsel = getenv("SC_OP");
     const std::string op = opsel ? opsel : "";
-    // measured (tools/op_time.py, r2 runs): v6 fastest for p = 5, 6, 7; v3 and v6 equal at p = 8
-    // (7.86 ms at cfg5; v3 kept there: its fused p . q is the one the round-1 bench validated);
-    // the row-warp kernels fastest for p = 3, 4
+    // measured (tools/op_time.py, r2 runs): on one rank v7 (two passes) is fastest for every p = 3..8
+    // (cfg5 5.55 ms vs v3 7.89 / v6 7.96; cfg3 p = 3..8); on z-slab ranks (v7 is
+    // one-rank only) v6 for p = 5, 6, 7, v3 for p = 8, the row-warp kernels for p = 3, 4
     const bool want_v6 = op == "v6" || (op.empty() && ni >= 4 && ni <= 6);
-    const bool want_v7 = op == "v7";
+    const bool want_v7 = op == "v7" || op.empty();
     if (v7_supported(ni) && uniform && sig_ok && want_v7 && prm->nranks == 1 && !(env && env[0] == '1')) {
       v7_make_coef(ni, g.d_uni, B.a0, B.ap, B.lam, B.K00, B.K0p, B.w0, ctx->v7_coef);
       if (cudaMalloc(&ctx->d_u7, sizeof(double) * 2 * (size_t)g.n_total) != cudaSuccess) return fail("cudaMalloc u7");

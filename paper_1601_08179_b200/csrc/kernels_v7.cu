@@ -71,163 +71,559 @@ __host__ __device__ constexpr int di_pk(int pj, int p1) {
   return pj * p1;
 }
 
-// 8-byte global -> shared copy, zero fill when !ok (src-size 0)
-__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool ok) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
+// ------------------------------------------------------------------------------------ pass A
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* m, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* m, unsigned bytes) {
+  unsigned long long state;
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 %0, [%1], %2;"
+               : "=l"(state)
+               : "r"(smem_u32(m)), "r"(bytes)
+               : "memory");
+  (void)state;
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* m, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W7: mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W7;\n}\n" ::"r"(smem_u32(m)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* m) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(m))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// A work item is an x-run of RUN elements (ex0 .. ex0 + cnt - 1, ey, ez).  Its inputs are five
+// contiguous skeleton ranges: the x-faces ex0 .. ex0 + cnt (one row), the y-faces of rows ey, ey + 1 and
+// the z-faces of planes ez, ez + 1 (cnt faces each).  Each range is bulk-copied (cp.async.bulk, one
+// mbarrier transaction per item) as its 16-byte aligned superset into a slot, so the range starts at
+// slot + (start & 1).  Dirichlet rows are not copied: the lanes read a zero row instead (as they do for
+// the Dirichlet x-faces fx = 0, nx).
+template <int NI, int STAGES>
+struct V7A {
+  static constexpr int N2 = NI * NI;
+  static constexpr int SX = ((RUN + 1) * N2 + 2 + 1) & ~1;   // x-face row slot (doubles, even)
+  static constexpr int SR = (RUN * N2 + 2 + 1) & ~1;         // y / z row slot
+  static constexpr int STAGE = SX + 4 * SR;
+  static constexpr int PJ = NI + 1, PK = NI + 1;
+  static constexpr int PKK = di_pk(PJ, PK);
+  static constexpr int ND = ((PKK * PK + 2) + 1) & ~1;
+  static constexpr int SMEM = (STAGES * STAGE + SR + ND) * 8;   // the stages, the zero row, D^{-1}
+};
+
+struct Item {
+  int ex0, cnt, ey, ez;
+  long long s[5];   // range starts: x row, y rows ey / ey + 1, z planes ez / ez + 1
+  bool dir[5];      // Dirichlet row (not copied)
+};
+
+template <int NI, int R = RUN>
+__device__ __forceinline__ Item decode(const Geom& g, int item, int nruns) {
+  constexpr int N2 = NI * NI;
+  Item it;
+  // rows (ey, ez) in chunks of 8 layers, ez fastest inside a chunk: the rows that share a y-face are
+  // nruns items apart, those that share a z-face 8 nruns (both inside the L2-resident window)
+  const int rx = item % nruns, rest = item / nruns;
+  const int zc = rest / (g.ny * 8), rr = rest - zc * g.ny * 8;
+  const int nzc = min(8, g.nz - 8 * zc);
+  it.ey = rr / nzc;
+  it.ez = 8 * zc + (rr - it.ey * nzc);
+  it.ex0 = rx * R;
+  it.cnt = min(R, g.nx - it.ex0);
+  const long long nx = g.nx, ny = g.ny;
+  it.s[0] = g.off_f[0] + (it.ex0 + (nx + 1) * (it.ey + ny * it.ez)) * N2;
+  it.dir[0] = false;
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int fy = it.ey + s, fz = it.ez + s;
+    it.s[1 + s] = g.off_f[1] + (it.ex0 + nx * (fy + (ny + 1) * it.ez)) * N2;
+    it.dir[1 + s] = !(fy > 0 && fy < g.ny);
+    it.s[3 + s] = g.off_f[2] + (it.ex0 + nx * (it.ey + ny * fz)) * N2;
+    it.dir[3 + s] = zdir(g, fz);
+  }
+  return it;
 }
 
-// ------------------------------------------------------------------------------------ pass A
-template <int NI>
-__global__ void __launch_bounds__(128, 4) k_v7_cond(const __grid_constant__ V7Params P) {
+template <int NI, int SX, int SR>
+__device__ __forceinline__ void issue_item(const V7Params& P, const Item& it, double* stage, unsigned long long* mb) {
+  constexpr int N2 = NI * NI;
+  unsigned total = 0;
+  long long a[5];
+  unsigned by[5];
+#pragma unroll
+  for (int r = 0; r < 5; ++r) {
+    const long long len = (long long)(r == 0 ? it.cnt + 1 : it.cnt) * N2;
+    a[r] = it.s[r] & ~1LL;
+    by[r] = it.dir[r] ? 0u : (unsigned)((((it.s[r] + len + 1) & ~1LL) - a[r]) * 8);
+    total += by[r];
+  }
+  mbar_arrive_tx(mb, total);
+#pragma unroll
+  for (int r = 0; r < 5; ++r)
+    if (by[r]) bulk_g2s(stage + (r == 0 ? 0 : SX + (r - 1) * SR), P.x + a[r], by[r], mb);
+}
+
+// Pass A: persistent CTAs of 4 warps, items blockIdx.x + n gridDim.x, the loads of item n + 2 in flight
+// while item n computes (two stages).  lane = (element of the run, parity class) as in v6.
+template <int NI, int STAGES>
+__global__ void __launch_bounds__(128, STAGES == 1 ? 4 : 3) k_v7_cond(const __grid_constant__ V7Params P, int nitems, int nruns) {
   if (P.done != nullptr && *P.done != 0.0) return;
+  using A = V7A<NI, STAGES>;
   constexpr int N2 = NI * NI, M = (NI + 1) / 2;
-  constexpr int PJ = NI + 1, PK = NI + 1;   // padded D^{-1} table strides (k: see the bank note below)
+  constexpr int PJ = A::PJ, PKK = A::PKK;
   const Geom& g = P.g;
   const V7Coef& cf = P.cf;
-  const int nx = g.nx, ny = g.ny, nz = g.nz;
-  const int run = blockIdx.x, ey = blockIdx.y, ez = blockIdx.z;
-  const int ex0 = run * RUN;
-  const int cnt = min(RUN, nx - ex0);
-  __shared__ double sX[(RUN + 1) * N2];
-  __shared__ double sY[2][RUN * N2];
-  __shared__ double sZ[2][RUN * N2];
-  // D^{-1} at i + PJ j + PKK k with the 8 class bases on distinct bank pairs (cf. kernels_v6.cu di_pk)
-  constexpr int PKK = di_pk(PJ, PK);
-  __shared__ double sD[PKK * PK + 2];
-  __shared__ double sC[3][8];
+  const int nx = g.nx, ny = g.ny;
+  extern __shared__ __align__(16) double smem[];
+  double* const zrow = smem + STAGES * A::STAGE;
+  double* const sD = zrow + A::SR;
+  __shared__ double sC[3][8], sA0[8], sAP[8];
+  __shared__ unsigned long long mbar[2];
   const int tid = threadIdx.x;
-  for (int t = tid; t < PKK * PK + 2; t += 128) {
+  for (int t = tid; t < A::SR; t += 128) zrow[t] = 0.0;
+  // D^{-1} at i + PJ j + PKK k with the 8 class bases on distinct bank pairs (cf. kernels_v6.cu di_pk)
+  for (int t = tid; t < A::ND; t += 128) {
     const int k = t / PKK, r = t - k * PKK, j = r / PJ, i = r - j * PJ;
     sD[t] = (i < NI && j < NI && k < NI) ? cf.dinv[i + NI * (j + NI * k)] : 0.0;
   }
   if (tid < 24) sC[tid / 8][tid % 8] = (tid % 8) < NI ? cf.c[tid / 8][tid % 8] : 0.0;
-  // faces of the run (Dirichlet faces and faces beyond the slab read as 0)
-  {   // asynchronous 8-byte copies (cp.async, zero-filled where masked): all of a thread's loads in flight
-    const long long xb = g.off_f[0] + ((long long)ex0 + (long long)(nx + 1) * (ey + (long long)ny * ez)) * N2;
-    for (int t = tid; t < (RUN + 1) * N2; t += 128) {
-      const int fx = ex0 + t / N2;
-      const bool ok = t < (cnt + 1) * N2 && fx > 0 && fx < nx;
-      cp_async8(sX + t, P.x + (ok ? xb + t : 0), ok);
-    }
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const int fy = ey + s;
-      const bool fok = fy > 0 && fy < ny;
-      const long long yb = g.off_f[1] + ((long long)ex0 + (long long)nx * (fy + (long long)(ny + 1) * ez)) * N2;
-      const int fz = ez + s;
-      const bool zok = !zdir(g, fz);
-      const long long zb = g.off_f[2] + ((long long)ex0 + (long long)nx * (ey + (long long)ny * fz)) * N2;
-      for (int t = tid; t < RUN * N2; t += 128) {
-        const bool in = t < cnt * N2;
-        cp_async8(sY[s] + t, P.x + ((in && fok) ? yb + t : 0), in && fok);
-        cp_async8(sZ[s] + t, P.x + ((in && zok) ? zb + t : 0), in && zok);
-      }
-    }
-    asm volatile("cp.async.wait_all;" ::: "memory");
+  if (tid < 8) {
+    sA0[tid] = cf.a0[tid];
+    sAP[tid] = cf.ap[tid];
+  }
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      const int item = blockIdx.x + s * gridDim.x;
+      if (item < nitems) issue_item<NI, A::SX, A::SR>(P, decode<NI>(g, item, nruns), smem + s * A::STAGE, &mbar[s]);
+    }
+  }
   const int warp = tid >> 5, lane = tid & 31;
   const int el = warp * 4 + (lane >> 3);          // element of the run
   const int cls = lane & 7, si = cls >> 2, sj = (cls >> 1) & 1, sk = cls & 1;
   const int CI = (NI - si + 1) >> 1, CJ = (NI - sj + 1) >> 1, CK = (NI - sk + 1) >> 1;
   const double gi = si ? -1.0 : 1.0, gj = sj ? -1.0 : 1.0, gk = sk ? -1.0 : 1.0;
-  const bool act = el < cnt;
-  const double* W = sX + el * N2 + sj + NI * sk;      // x-face entries (j, k)
-  const double* E = W + N2;
-  const double* S = sY[0] + el * N2 + si + NI * sk;   // y-face entries (i, k)
-  const double* Nn = sY[1] + el * N2 + si + NI * sk;
-  const double* B = sZ[0] + el * N2 + si + NI * sj;   // z-face entries (i, j)
-  const double* T = sZ[1] + el * N2 + si + NI * sj;
-  const double* Dc = sD + si + PJ * sj + PKK * sk;
-  double c1[M];
+  const double* const Dc = sD + si + PJ * sj + PKK * sk;
+  for (int n = 0;; ++n) {
+    const int item = blockIdx.x + n * gridDim.x;
+    if (item >= nitems) break;
+    const int b = STAGES == 1 ? 0 : (n & 1);
+    const Item it = decode<NI>(g, item, nruns);
+    double* const stage = smem + b * A::STAGE;
+    mbar_wait(&mbar[b], (unsigned)((STAGES == 1 ? n : (n >> 1)) & 1));
+    const bool act = el < it.cnt;
+    const int ex = it.ex0 + el, ey = it.ey, ez = it.ez;
+    // face rows of the element (entries (a, b) at a + NI b); Dirichlet faces / rows read the zero row
+    const double* const X = stage + (it.s[0] & 1);
+    const double* Wf = (ex > 0 && ex < nx) ? X + el * N2 : zrow;
+    const double* Ef = (ex + 1 < nx) ? X + (el + 1) * N2 : zrow;
+    const double* Yf[2];
+    const double* Zf[2];
 #pragma unroll
-  for (int ii = 0; ii < M; ++ii) c1[ii] = sC[0][si + 2 * ii];
-  double zin[M][M], qz[M][M];
-#pragma unroll
-  for (int ii = 0; ii < M; ++ii)
-#pragma unroll
-    for (int jj = 0; jj < M; ++jj) {
-      zin[ii][jj] = (ii < CI && jj < CJ) ? fma(gk, T[2 * ii + 2 * NI * jj], B[2 * ii + 2 * NI * jj]) : 0.0;
-      qz[ii][jj] = 0.0;
+    for (int s = 0; s < 2; ++s) {
+      Yf[s] = it.dir[1 + s] ? zrow : stage + A::SX + s * A::SR + (it.s[1 + s] & 1) + el * N2;
+      Zf[s] = it.dir[3 + s] ? zrow : stage + A::SX + (2 + s) * A::SR + (it.s[3 + s] & 1) + el * N2;
     }
-  const long long ex = ex0 + el;
-  // output rows (entries of the element's faces in U0 / U1), written straight from the lanes (staging
-  // them in shared memory for row-wise stores measured slower: 11.0 -> 12.0 ms at cfg5)
-  double* const uxw = P.u0 + g.off_f[0] + (ex + (long long)(nx + 1) * (ey + (long long)ny * ez)) * N2;   // face ex
-  double* const uxe = P.u1 + g.off_f[0] + (ex + 1 + (long long)(nx + 1) * (ey + (long long)ny * ez)) * N2;
-  double* const uys = P.u0 + g.off_f[1] + (ex + (long long)nx * (ey + (long long)(ny + 1) * ez)) * N2;
-  double* const uyn = P.u1 + g.off_f[1] + (ex + (long long)nx * (ey + 1 + (long long)(ny + 1) * ez)) * N2;
-  double* const uzb = P.u0 + g.off_f[2] + (ex + (long long)nx * (ey + (long long)ny * ez)) * N2;
-  double* const uzt = P.u1 + g.off_f[2] + (ex + (long long)nx * (ey + (long long)ny * (ez + 1))) * N2;
+    {
+      const double* W = Wf + sj + NI * sk;      // x-face entries (j, k)
+      const double* E = Ef + sj + NI * sk;
+      const double* S = Yf[0] + si + NI * sk;   // y-face entries (i, k)
+      const double* Nn = Yf[1] + si + NI * sk;
+      const double* B = Zf[0] + si + NI * sj;   // z-face entries (i, j)
+      const double* T = Zf[1] + si + NI * sj;
+      double c1[M];
 #pragma unroll
-  for (int kk = 0; kk < M; ++kk) {
-    const double c3 = sC[2][sk + 2 * kk];
-    double yin[M], qy[M];
+      for (int ii = 0; ii < M; ++ii) c1[ii] = sC[0][si + 2 * ii];
+      double zin[M][M], qz[M][M];
 #pragma unroll
-    for (int ii = 0; ii < M; ++ii) {
-      yin[ii] = (ii < CI && kk < CK) ? fma(gj, Nn[2 * ii + 2 * NI * kk], S[2 * ii + 2 * NI * kk]) : 0.0;
-      qy[ii] = 0.0;
+      for (int ii = 0; ii < M; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < M; ++jj) {
+          zin[ii][jj] = (ii < CI && jj < CJ) ? fma(gk, T[2 * ii + 2 * NI * jj], B[2 * ii + 2 * NI * jj]) : 0.0;
+          qz[ii][jj] = 0.0;
+        }
+      // output rows (entries of the element's faces in U0 / U1)
+      double* const uxw = P.u0 + g.off_f[0] + (ex + (long long)(nx + 1) * (ey + (long long)ny * ez)) * N2;   // face ex
+      double* const uxe = P.u1 + g.off_f[0] + (ex + 1 + (long long)(nx + 1) * (ey + (long long)ny * ez)) * N2;
+      double* const uys = P.u0 + g.off_f[1] + (ex + (long long)nx * (ey + (long long)(ny + 1) * ez)) * N2;
+      double* const uyn = P.u1 + g.off_f[1] + (ex + (long long)nx * (ey + 1 + (long long)(ny + 1) * ez)) * N2;
+      double* const uzb = P.u0 + g.off_f[2] + (ex + (long long)nx * (ey + (long long)ny * ez)) * N2;
+      double* const uzt = P.u1 + g.off_f[2] + (ex + (long long)nx * (ey + (long long)ny * (ez + 1))) * N2;
+#pragma unroll
+      for (int kk = 0; kk < M; ++kk) {
+        const double c3 = sC[2][sk + 2 * kk];
+        double yin[M], qy[M];
+#pragma unroll
+        for (int ii = 0; ii < M; ++ii) {
+          yin[ii] = (ii < CI && kk < CK) ? fma(gj, Nn[2 * ii + 2 * NI * kk], S[2 * ii + 2 * NI * kk]) : 0.0;
+          qy[ii] = 0.0;
+        }
+        double qx[M];
+#pragma unroll
+        for (int jj = 0; jj < M; ++jj) {
+          const double c2 = sC[1][sj + 2 * jj];
+          const int ox = 2 * jj + 2 * NI * kk;
+          const double xin = (jj < CJ && kk < CK) ? fma(gi, E[ox], W[ox]) : 0.0;
+          qx[jj] = 0.0;
+#pragma unroll
+          for (int ii = 0; ii < M; ++ii) {
+            const double u = fma(c1[ii], xin, fma(c2, yin[ii], c3 * zin[ii][jj]));
+            const double v = u * Dc[2 * ii + 2 * PJ * jj + 2 * PKK * kk];
+            qx[jj] = fma(c1[ii], v, qx[jj]);
+            qy[ii] = fma(c2, v, qy[ii]);
+            qz[ii][jj] = fma(c3, v, qz[ii][jj]);
+          }
+        }
+        // x pair (s_i = 0 / 1: lane ^ 4): W part -(Q0 + Q1) (s_i = 0 lane), E part -(Q0 - Q1) (s_i = 1 lane)
+        double qpx[M];
+#pragma unroll
+        for (int jj = 0; jj < M; ++jj) qpx[jj] = __shfl_xor_sync(0xffffffffu, qx[jj], 4);
+#pragma unroll
+        for (int jj = 0; jj < M; ++jj)
+          if (act && jj < CJ && kk < CK) {
+            if (si == 0) __stcs(uxw + sj + 2 * jj + NI * (sk + 2 * kk), -(qx[jj] + qpx[jj]));
+            else __stcs(uxe + sj + 2 * jj + NI * (sk + 2 * kk), qx[jj] - qpx[jj]);
+          }
+        double qpy[M];   // y pair (lane ^ 2): S -(Q0 + Q1), N -(Q0 - Q1)
+#pragma unroll
+        for (int ii = 0; ii < M; ++ii) qpy[ii] = __shfl_xor_sync(0xffffffffu, qy[ii], 2);
+#pragma unroll
+        for (int ii = 0; ii < M; ++ii)
+          if (act && ii < CI && kk < CK) {
+            if (sj == 0) __stcs(uys + si + 2 * ii + NI * (sk + 2 * kk), -(qy[ii] + qpy[ii]));
+            else __stcs(uyn + si + 2 * ii + NI * (sk + 2 * kk), qy[ii] - qpy[ii]);
+          }
+      }
+#pragma unroll
+      for (int ii = 0; ii < M; ++ii)   // z pair (lane ^ 1): B -(Q0 + Q1), T -(Q0 - Q1)
+#pragma unroll
+        for (int jj = 0; jj < M; ++jj) {
+          const double qp = __shfl_xor_sync(0xffffffffu, qz[ii][jj], 1);
+          if (act && ii < CI && jj < CJ) {
+            if (sk == 0) __stcs(uzb + si + 2 * ii + NI * (sj + 2 * jj), -(qz[ii][jj] + qp));
+            else __stcs(uzt + si + 2 * ii + NI * (sj + 2 * jj), qz[ii][jj] - qp);
+          }
+        }
     }
+    // Edge line sums of the primary part (the K~ rows of an edge couple it to the face
+    // interiors along lines).  An interior edge's four face lines belong to two of its elements: the
+    // element on its high side in both transverse directions gives the a0-weighted lines of its low
+    // faces (stored in U0 at the edge), the element on its low side gives the ap-weighted lines of its
+    // high faces (stored in U1 at the edge).  lane cls = entry m of the edge (cls < NI).
+    if (act && cls < NI) {
+      const int m = cls;
+      const long long nx1 = nx + 1, ny1 = ny + 1;
+      double s0, s1;
+      // x-edges: el01 sum_j w_j F_z(m, j) + el02 sum_k w_k F_y(m, k)
+      s0 = 0.0; s1 = 0.0;
 #pragma unroll
-    for (int jj = 0; jj < M; ++jj) {
-      const double c2 = sC[1][sj + 2 * jj];
-      const int ox = 2 * jj + 2 * NI * kk;
-      const double xin = (jj < CJ && kk < CK) ? fma(gi, E[ox], W[ox]) : 0.0;
-      double qx = 0.0;
-#pragma unroll
-      for (int ii = 0; ii < M; ++ii) {
-        const double u = fma(c1[ii], xin, fma(c2, yin[ii], c3 * zin[ii][jj]));
-        const double v = u * Dc[2 * ii + 2 * PJ * jj + 2 * PKK * kk];
-        qx = fma(c1[ii], v, qx);
-        qy[ii] = fma(c2, v, qy[ii]);
-        qz[ii][jj] = fma(c3, v, qz[ii][jj]);
+      for (int q = 0; q < NI; ++q) {
+        s0 = fma(sA0[q], cf.el[0][1] * Zf[0][m + NI * q] + cf.el[0][2] * Yf[0][m + NI * q], s0);
+        s1 = fma(sAP[q], cf.el[0][1] * Zf[1][m + NI * q] + cf.el[0][2] * Yf[1][m + NI * q], s1);
       }
-      // x pair (s_i = 0 / 1: lane ^ 4): W part -(Q0 + Q1) (s_i = 0 lane), E part -(Q0 - Q1) (s_i = 1 lane)
-      const double qp = __shfl_xor_sync(0xffffffffu, qx, 4);
-      if (act && jj < CJ && kk < CK) {
-        if (si == 0) uxw[sj + 2 * jj + NI * (sk + 2 * kk)] = -(qx + qp);
-        else uxe[sj + 2 * jj + NI * (sk + 2 * kk)] = qx - qp;
+      __stcs(P.u0 + g.off_e[0] + (ex + (long long)nx * (ey + ny1 * ez)) * NI + m, s0);
+      __stcs(P.u1 + g.off_e[0] + (ex + (long long)nx * (ey + 1 + ny1 * (ez + 1))) * NI + m, s1);
+      // y-edges: el10 sum_i w_i F_z(i, m) + el12 sum_k w_k F_x(m, k)
+      s0 = 0.0; s1 = 0.0;
+#pragma unroll
+      for (int q = 0; q < NI; ++q) {
+        s0 = fma(sA0[q], cf.el[1][0] * Zf[0][q + NI * m] + cf.el[1][2] * Wf[m + NI * q], s0);
+        s1 = fma(sAP[q], cf.el[1][0] * Zf[1][q + NI * m] + cf.el[1][2] * Ef[m + NI * q], s1);
+      }
+      __stcs(P.u0 + g.off_e[1] + (ex + nx1 * (ey + (long long)ny * ez)) * NI + m, s0);
+      __stcs(P.u1 + g.off_e[1] + (ex + 1 + nx1 * (ey + (long long)ny * (ez + 1))) * NI + m, s1);
+      // z-edges: el20 sum_i w_i F_y(i, m) + el21 sum_j w_j F_x(j, m)
+      s0 = 0.0; s1 = 0.0;
+#pragma unroll
+      for (int q = 0; q < NI; ++q) {
+        s0 = fma(sA0[q], cf.el[2][0] * Yf[0][q + NI * m] + cf.el[2][1] * Wf[q + NI * m], s0);
+        s1 = fma(sAP[q], cf.el[2][0] * Yf[1][q + NI * m] + cf.el[2][1] * Ef[q + NI * m], s1);
+      }
+      __stcs(P.u0 + g.off_e[2] + (ex + nx1 * (ey + ny1 * ez)) * NI + m, s0);
+      __stcs(P.u1 + g.off_e[2] + (ex + 1 + nx1 * (ey + 1 + ny1 * ez)) * NI + m, s1);
+    }
+    // release the stage: every lane is done reading it; then the loads of item n + 2 go into it
+    fence_proxy_async();
+    __syncthreads();
+    const int nxt = item + STAGES * gridDim.x;
+    if (tid == 0 && nxt < nitems) issue_item<NI, A::SX, A::SR>(P, decode<NI>(g, nxt, nruns), stage, &mbar[b]);
+  }
+}
+
+// ------------------------------------------------------------------------------------ pass A, line form
+// Pass A with lane = (element, x-line (j, k)) instead of (element, parity class): no padded points
+// (n_I^3 points per element instead of 8 ceil(n_I/2)^3), per-lane constants (D^{-1}(., j, k), the y / z
+// coefficients and signs) in registers for the whole kernel, and three phases per item:
+//  X: faces-in + D^{-1} along the lane's x-line (the y / z inputs of the line's points are the face
+//     values (S +- N)(i, k), (B +- T)(i, j); the sign is the parity of the lane's j / k, P:302 sigma), the
+//     x faces-out as the two parity sums Q_even / Q_odd of the line (W part -(Qe + Qo), E part -(Qe - Qo)),
+//     uhat = D^{-1} (...) stored to shared memory;
+//  Y: lane = (i, k): y faces-out = parity sums over j of c2_j uhat(i, j, k);
+//  Z: lane = (i, j): z faces-out over k; and the edge line sums (U0 / U1 at the edges) as in k_v7_cond.
+// Every output row of a group of elements is one contiguous skeleton range: coalesced stores.
+template <int NI, int STAGES>
+struct V8A {
+  static constexpr int N2 = NI * NI, N3 = N2 * NI;
+  static constexpr int R = 8;                                // elements per item (x-run)
+  static constexpr int G = (8 * N2 <= 256) ? 8 : 4;          // elements per thread group
+  static constexpr int NT = ((G * N2 + 31) / 32) * 32;       // threads per CTA
+  static constexpr int SX = ((R + 1) * N2 + 2 + 1) & ~1;
+  static constexpr int SR = (R * N2 + 2 + 1) & ~1;
+  static constexpr int STAGE = SX + 4 * SR;
+  static constexpr int VS = N3 + (N3 % 2 == 0 ? 1 : 0);      // uhat per element (odd stride)
+  static constexpr int SMEM = (STAGES * STAGE + SR + R * VS) * 8;
+};
+
+// Per-lane constants of one edge line sum (output o = kind NI + m of an element, see k_v7_cond):
+// kinds 0 / 1 x-edges, 2 / 3 y-edges, 4 / 5 z-edges; even kinds the a0-weighted lines of the element's low
+// faces (U0 at its low edge), odd kinds the ap = sigma a0 weighted lines of its high faces (U1 at its high
+// edge).  Face rows: 0 / 1 = z-face B / T, 2 / 3 = y-face S / N, 4 / 5 = x-face W / E.
+struct EdgeLane {
+  int f1, f2;             // face rows of the two lines
+  int o1, s1, o2, s2;     // line start / stride inside the face (doubles)
+  double e1, e2, sgn;     // line weights (2 d w0 of the transverse directions), -1 on odd q for odd kinds
+  long long base, dey, dez;   // U index = base + NI ex + dey ey + dez ez
+  bool hi, on;
+};
+
+template <int NI>
+__device__ __forceinline__ EdgeLane edge_lane(const Geom& g, const V7Coef& cf, int o) {
+  EdgeLane E;
+  const int kind = o / NI, m = o - kind * NI;
+  const long long nx = g.nx, ny = g.ny, nx1 = nx + 1, ny1 = ny + 1;
+  E.on = o < 6 * NI;
+  E.hi = kind & 1;
+  const int h = E.hi;
+  E.sgn = h ? -1.0 : 1.0;
+  if (kind < 2) {          // x-edge (ex, ey + h, ez + h): z-face (m, q) over j, y-face (m, q) over k
+    E.f1 = h; E.o1 = m; E.s1 = NI;
+    E.f2 = 2 + h; E.o2 = m; E.s2 = NI;
+    E.e1 = cf.el[0][1]; E.e2 = cf.el[0][2];
+    E.base = g.off_e[0] + (nx * (h + ny1 * h)) * NI + m; E.dey = nx * NI; E.dez = nx * ny1 * NI;
+  } else if (kind < 4) {   // y-edge (ex + h, ey, ez + h): z-face (q, m) over i, x-face (m, q) over k
+    E.f1 = h; E.o1 = NI * m; E.s1 = 1;
+    E.f2 = 4 + h; E.o2 = m; E.s2 = NI;
+    E.e1 = cf.el[1][0]; E.e2 = cf.el[1][2];
+    E.base = g.off_e[1] + (h + nx1 * ny * h) * NI + m; E.dey = nx1 * NI; E.dez = nx1 * ny * NI;
+  } else {                 // z-edge (ex + h, ey + h, ez): y-face (q, m) over i, x-face (q, m) over j
+    E.f1 = 2 + h; E.o1 = NI * m; E.s1 = 1;
+    E.f2 = 4 + h; E.o2 = NI * m; E.s2 = 1;
+    E.e1 = cf.el[2][0]; E.e2 = cf.el[2][1];
+    E.base = g.off_e[2] + (h + nx1 * h) * NI + m; E.dey = nx1 * NI; E.dez = nx1 * ny1 * NI;
+  }
+  return E;
+}
+
+__device__ __forceinline__ const double* sel6(int f, const double* r0, const double* r1, const double* r2,
+                                              const double* r3, const double* r4, const double* r5) {
+  const double* a = (f & 1) ? r1 : r0;
+  const double* b = (f & 1) ? r3 : r2;
+  const double* c = (f & 1) ? r5 : r4;
+  return f < 2 ? a : (f < 4 ? b : c);
+}
+
+template <int NI>
+__device__ __forceinline__ void edge_sum(const V7Params& P, const EdgeLane& E, const double* r0, const double* r1,
+                                         const double* r2, const double* r3, const double* r4, const double* r5, int ex,
+                                         int ey, int ez) {
+  const double* p1 = sel6(E.f1, r0, r1, r2, r3, r4, r5) + E.o1;
+  const double* p2 = sel6(E.f2, r0, r1, r2, r3, r4, r5) + E.o2;
+  double se = 0.0, so = 0.0;
+#pragma unroll
+  for (int q = 0; q < NI; ++q) {
+    const double t = fma(E.e1, p1[E.s1 * q], E.e2 * p2[E.s2 * q]);
+    if (q & 1) so = fma(P.cf.a0[q], t, so);
+    else se = fma(P.cf.a0[q], t, se);
+  }
+  __stcs((E.hi ? P.u1 : P.u0) + E.base + (long long)NI * ex + E.dey * ey + E.dez * ez, fma(E.sgn, so, se));
+}
+
+template <int NI, int STAGES>
+__global__ void __launch_bounds__(V8A<NI, STAGES>::NT) k_v7_lines(const __grid_constant__ V7Params P, int nitems,
+                                                                  int nruns) {
+  if (P.done != nullptr && *P.done != 0.0) return;
+  using A = V8A<NI, STAGES>;
+  constexpr int N2 = NI * NI, G = A::G, R = A::R;
+  constexpr int NE = (6 * NI + N2 - 1) / N2;   // edge line sums per lane
+  const Geom& g = P.g;
+  const V7Coef& cf = P.cf;
+  const int nx = g.nx, ny = g.ny;
+  const long long nx1 = nx + 1, ny1 = ny + 1;
+  extern __shared__ __align__(16) double smem[];
+  double* const zrow = smem + STAGES * A::STAGE;
+  double* const sv = zrow + A::SR;
+  __shared__ unsigned long long mbar[2];
+  __shared__ Item sit[2];   // the decoded item of each stage (written by the issuing thread before its arrive)
+  const int tid = threadIdx.x;
+  for (int t = tid; t < A::SR; t += A::NT) zrow[t] = 0.0;
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int s = 0; s < STAGES; ++s) {
+      const int item = blockIdx.x + s * gridDim.x;
+      if (item < nitems) {
+        sit[s] = decode<NI, R>(g, item, nruns);
+        issue_item<NI, A::SX, A::SR>(P, sit[s], smem + s * A::STAGE, &mbar[s]);
       }
     }
+  // lane constants: line l = a + NI b of the element (phase X: (j, k) = (a, b); Y: (i, k); Z: (i, j))
+  const bool lane_on = tid < G * N2;
+  const int eg = tid / N2, l = tid - eg * N2, la = l % NI, lb = l / NI;
+  double Dl[NI];
 #pragma unroll
-    for (int ii = 0; ii < M; ++ii) {   // y pair (lane ^ 2): S -(Q0 + Q1), N -(Q0 - Q1)
-      const double qp = __shfl_xor_sync(0xffffffffu, qy[ii], 2);
-      if (act && ii < CI && kk < CK) {
-        if (sj == 0) uys[si + 2 * ii + NI * (sk + 2 * kk)] = -(qy[ii] + qp);
-        else uyn[si + 2 * ii + NI * (sk + 2 * kk)] = qy[ii] - qp;
+  for (int i = 0; i < NI; ++i) Dl[i] = lane_on ? cf.dinv[i + NI * l] : 0.0;
+  const double c2j = cf.c[1][la], c3k = cf.c[2][lb];
+  const double gj = (la & 1) ? -1.0 : 1.0, gk = (lb & 1) ? -1.0 : 1.0;
+  EdgeLane EL[NE];
+#pragma unroll
+  for (int r = 0; r < NE; ++r) EL[r] = edge_lane<NI>(g, cf, l + N2 * r);
+  for (int n = 0;; ++n) {
+    const int item = blockIdx.x + n * gridDim.x;
+    if (item >= nitems) break;
+    const int b = STAGES == 1 ? 0 : (n & 1);
+    double* const stage = smem + b * A::STAGE;
+    mbar_wait(&mbar[b], (unsigned)((STAGES == 1 ? n : (n >> 1)) & 1));
+    const Item it = sit[b];
+    const int ey = it.ey, ez = it.ez;
+    const double* const X = stage + (it.s[0] & 1);
+    const double* Yr[2];
+    const double* Zr[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      Yr[s] = it.dir[1 + s] ? zrow : stage + A::SX + s * A::SR + (it.s[1 + s] & 1);
+      Zr[s] = it.dir[3 + s] ? zrow : stage + A::SX + (2 + s) * A::SR + (it.s[3 + s] & 1);
+    }
+    // ---- phase X
+#pragma unroll 1
+    for (int gr = 0; gr < R / G; ++gr) {
+      const int el = gr * G + eg, ex = it.ex0 + el;
+      if (lane_on) {
+        const double* Wf = (ex > 0 && ex < nx) ? X + el * N2 : zrow;
+        const double* Ef = (ex + 1 < nx) ? X + (el + 1) * N2 : zrow;
+        const double w = Wf[l], e = Ef[l];
+        const double xs = w + e, xd = w - e;
+        const double* S = Yr[0] + el * N2 + NI * lb;   // S(i, k), i = 0..NI-1
+        const double* Nn = Yr[1] + el * N2 + NI * lb;
+        const double* B = Zr[0] + el * N2 + NI * la;   // B(i, j)
+        const double* T = Zr[1] + el * N2 + NI * la;
+        double qe = 0.0, qo = 0.0;
+        double* const v = sv + el * A::VS + NI * l;
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+          const double yin = fma(gj, Nn[i], S[i]);
+          const double zin = fma(gk, T[i], B[i]);
+          const double c1 = cf.c[0][i];
+          const double u = fma(c1, (i & 1) ? xd : xs, fma(c2j, yin, c3k * zin));
+          const double vv = u * Dl[i];
+          if (i & 1) qo = fma(c1, vv, qo);
+          else qe = fma(c1, vv, qe);
+          v[i] = vv;
+        }
+        if (el < it.cnt) {
+          const long long fx = g.off_f[0] + (ex + nx1 * (ey + (long long)ny * ez)) * N2 + l;
+          __stcs(P.u0 + fx, -(qe + qo));        // face ex (the element's W face)
+          __stcs(P.u1 + fx + N2, qo - qe);      // face ex + 1 (E)
+        }
       }
+    }
+    __syncthreads();
+    // ---- phases Y, Z and the edge line sums
+#pragma unroll 1
+    for (int gr = 0; gr < R / G; ++gr) {
+      const int el = gr * G + eg, ex = it.ex0 + el;
+      if (lane_on && el < it.cnt) {
+        const double* const v = sv + el * A::VS;
+        double qe = 0.0, qo = 0.0;
+#pragma unroll
+        for (int j = 0; j < NI; ++j) {   // lane (i, k) = (la, lb)
+          const double t = cf.c[1][j] * v[la + NI * (j + NI * lb)];
+          if (j & 1) qo += t;
+          else qe += t;
+        }
+        const long long fy = g.off_f[1] + (ex + (long long)nx * (ey + ny1 * ez)) * N2 + l;
+        __stcs(P.u0 + fy, -(qe + qo));                        // S face (ey)
+        __stcs(P.u1 + fy + (long long)nx * N2, qo - qe);      // N face (ey + 1)
+        qe = 0.0; qo = 0.0;
+#pragma unroll
+        for (int k = 0; k < NI; ++k) {   // lane (i, j) = (la, lb)
+          const double t = cf.c[2][k] * v[l + N2 * k];
+          if (k & 1) qo += t;
+          else qe += t;
+        }
+        const long long fz = g.off_f[2] + (ex + (long long)nx * (ey + (long long)ny * ez)) * N2 + l;
+        __stcs(P.u0 + fz, -(qe + qo));                             // B face (ez)
+        __stcs(P.u1 + fz + (long long)nx * ny * N2, qo - qe);      // T face (ez + 1)
+        const double* Wf = (ex > 0 && ex < nx) ? X + el * N2 : zrow;
+        const double* Ef = (ex + 1 < nx) ? X + (el + 1) * N2 : zrow;
+#pragma unroll
+        for (int r = 0; r < NE; ++r)
+          if (EL[r].on)
+            edge_sum<NI>(P, EL[r], Zr[0] + el * N2, Zr[1] + el * N2, Yr[0] + el * N2, Yr[1] + el * N2, Wf, Ef, ex, ey, ez);
+      }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    const int nxt = item + STAGES * gridDim.x;
+    if (tid == 0 && nxt < nitems) {
+      sit[b] = decode<NI, R>(g, nxt, nruns);
+      issue_item<NI, A::SX, A::SR>(P, sit[b], stage, &mbar[b]);
     }
   }
-#pragma unroll
-  for (int ii = 0; ii < M; ++ii)   // z pair (lane ^ 1): B -(Q0 + Q1), T -(Q0 - Q1)
-#pragma unroll
-    for (int jj = 0; jj < M; ++jj) {
-      const double qp = __shfl_xor_sync(0xffffffffu, qz[ii][jj], 1);
-      if (act && ii < CI && jj < CJ) {
-        if (sk == 0) uzb[si + 2 * ii + NI * (sj + 2 * jj)] = -(qz[ii][jj] + qp);
-        else uzt[si + 2 * ii + NI * (sj + 2 * jj)] = qz[ii][jj] - qp;
-      }
-    }
 }
 
 // ------------------------------------------------------------------------------------ pass B
-// One thread per skeleton entry of class `cls` (0..2 x / y / z faces, 3..5 x / y / z edges, 6
-// vertices); blockIdx.y = entity row (the slow indices), threadIdx / blockIdx.x run over the row's
-// contiguous entries.
-// Free (non-Dirichlet, inside the slab) lattice test for an entity given by its three grid indices
-// and which of them are "face" (f) indices.
+// One CTA per cell row (cy, cz) of the vertex lattice, 0 <= cy <= ny, 0 <= cz <= nz.  The cell
+// (c_x, cy, cz) owns the x-face (c_x, cy, cz), y-face (c_x, cy, cz), z-face (c_x, cy, cz), x-edge,
+// y-edge, z-edge and vertex with the same indices (those that exist), so the cell rows partition the
+// skeleton and each CTA writes seven contiguous skeleton ranges (one per entity kind), one thread per
+// entry, consecutive threads on consecutive entries (coalesced loads of x / U0 / U1, coalesced
+// stores of y).  The values of the neighbouring rows (opposite faces, edge line sums over faces of
+// the rows (cy - 1, cz), (cy, cz - 1)) are read through L2 while they are still resident: rows run
+// in cy-fastest order, so the reuse distance is one row (cy) or one plane of rows (cz).  U0 / U1 are
+// read once (evict-first), y is written once (streaming stores): the resident set stays x.
+// Every entry is a sum in a fixed order; the p . q partial of the CTA is formed in a fixed order.
 __device__ __forceinline__ bool in_f(int v, int n) { return v > 0 && v < n; }
-__device__ __forceinline__ bool in_e(int v, int n) { return v >= 0 && v < n; }
 
-template <int NI>
 __device__ __forceinline__ double ldv(const double* __restrict__ x, long long i, bool ok) {
   const double v = __ldg(x + (ok ? i : 0));   // always a valid address: the load is not predicated
   return ok ? v : 0.0;
 }
 
+// One face entry: y = fd u + kf (u_lo + u_hi) + wA (a0_ea A0[eb] + ap_ea A1[eb]) + wB (a0_eb B0[ea] + ap_eb B1[ea])
+//                     + U0 + U1   (the primary part of Eq. eq:east_east_primary_part_transformed summed over
+// the face's two elements, + the two condensed parts from pass A)
+template <int NI>
+__device__ __forceinline__ double face_entry(const V7Params& P, const double* sfd, const double* sa0, const double* sap,
+                                             long long i, int e, int ea, int eb, long long so, bool olo, bool ohi,
+                                             long long ia0, long long ia1, bool oka0, bool oka1, long long ib0,
+                                             long long ib1, bool okb0, bool okb1, double wA, double wB, double kf,
+                                             double& u) {
+  const double* __restrict__ x = P.x;
+  u = __ldg(x + i);
+  const double uo = ldv(x, i - so, olo) + ldv(x, i + so, ohi);
+  const double ea_ = sa0[ea] * ldv(x, ia0 + eb, oka0) + sap[ea] * ldv(x, ia1 + eb, oka1);
+  const double eb_ = sa0[eb] * ldv(x, ib0 + ea, okb0) + sap[eb] * ldv(x, ib1 + ea, okb1);
+  return sfd[e] * u + kf * uo + wA * ea_ + wB * eb_ + __ldcs(P.u0 + i) + __ldcs(P.u1 + i);
+}
+
 template <int NI, bool DOT>
-__global__ void __launch_bounds__(256) k_v7_assemble(const __grid_constant__ V7Params P, int cls) {
+__global__ void __launch_bounds__(256, 4) k_v7_assemble(const __grid_constant__ V7Params P) {
   if (P.done != nullptr && *P.done != 0.0) return;
   constexpr int N2 = NI * NI;
   const Geom& g = P.g;
@@ -235,182 +631,162 @@ __global__ void __launch_bounds__(256) k_v7_assemble(const __grid_constant__ V7P
   const int nx = g.nx, ny = g.ny, nz = g.nz;
   const long long nx1 = nx + 1, ny1 = ny + 1;
   const double* __restrict__ x = P.x;
-  const int row = blockIdx.y;   // y-ish index + (count) * z-ish index
-  double dot = 0.0;
+  double* __restrict__ y = P.y;
+  const int cy = blockIdx.x % (ny + 1), cz = blockIdx.x / (ny + 1);
   // lane-indexed coefficients from shared memory (indexed kernel-parameter loads serialise per address)
-  __shared__ double sfd[49], sa0[8], sap[8], sself[8];
-  {
-    const int f = cls <= 2 ? cls : 0, e = cls >= 3 && cls <= 5 ? cls - 3 : 0;
-    for (int q = threadIdx.x; q < N2; q += blockDim.x) sfd[q] = cf.fd[f][q];
-    if (threadIdx.x < 8) {
-      sa0[threadIdx.x] = cf.a0[threadIdx.x];
-      sap[threadIdx.x] = cf.ap[threadIdx.x];
-      sself[threadIdx.x] = cf.eself[e][threadIdx.x];
-    }
-    __syncthreads();
+  __shared__ double sfd[3][N2], sa0[8], sap[8], sself[3][8];
+  for (int q = threadIdx.x; q < 3 * N2; q += blockDim.x) sfd[q / N2][q % N2] = cf.fd[q / N2][q % N2];
+  if (threadIdx.x < 8) {
+    sa0[threadIdx.x] = cf.a0[threadIdx.x];
+    sap[threadIdx.x] = cf.ap[threadIdx.x];
+    for (int e = 0; e < 3; ++e) sself[e][threadIdx.x] = cf.eself[e][threadIdx.x];
   }
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  // all rows are (x-run of entities) x (per-entity entries); decode (a = x index, e = entry)
-  if (cls <= 2) {
-    // ---------------- faces: one thread per (face, first in-plane entry ea), loop over the second (eb).
-    // y(ea, eb) = fd u + K0p-term (opposite faces) + wA (a0_ea A0[eb] + ap_ea A1[eb]) + wB (a0_eb B0[ea] + ap_eb B1[ea])
-    //             + U0 + U1;  A = the edges along the second in-plane direction, B = along the first.
-    const int a = t / NI, ea = t - a * NI;
-    const int rowlen = cls == 0 ? nx + 1 : nx;
-    if (a < rowlen) {
-      long long fid, so, ia0, ia1, ib0, ib1;
-      bool fr, olo, ohi, oka0, oka1, okb0, okb1;
-      double wA, wB, kf;
-      if (cls == 0) {            // x-face (fx, ey, ez): A = z-edges (fx, ey / ey+1, ez), B = y-edges (fx, ey, ez / ez+1)
-        const int ey_ = row % ny, ez_ = row / ny, fx = a;
-        fid = fx + nx1 * (ey_ + (long long)ny * ez_);
-        fr = in_f(fx, nx);
-        so = N2; olo = fx - 1 > 0; ohi = fx + 1 < nx;
-        ia0 = g.off_e[2] + (fx + nx1 * (ey_ + ny1 * ez_)) * NI; ia1 = ia0 + nx1 * NI;
-        oka0 = in_f(ey_, ny); oka1 = in_f(ey_ + 1, ny);
-        ib0 = g.off_e[1] + (fx + nx1 * (ey_ + (long long)ny * ez_)) * NI + ea; ib1 = ib0 + nx1 * ny * NI;
-        okb0 = !zdir(g, ez_); okb1 = !zdir(g, ez_ + 1);
-        wA = cf.ef[0][1]; wB = cf.ef[0][2]; kf = cf.kf[0];
-      } else if (cls == 1) {     // y-face (ex, fy, ez): A = z-edges (ex / ex+1, fy, ez), B = x-edges (ex, fy, ez / ez+1)
-        const int fy = row % (ny + 1), ez_ = row / (ny + 1), ex_ = a;
-        fid = ex_ + (long long)nx * (fy + ny1 * ez_);
-        fr = in_f(fy, ny);
-        so = (long long)nx * N2; olo = fy - 1 > 0; ohi = fy + 1 < ny;
-        ia0 = g.off_e[2] + (ex_ + nx1 * (fy + ny1 * ez_)) * NI; ia1 = ia0 + NI;
-        oka0 = in_f(ex_, nx); oka1 = in_f(ex_ + 1, nx);
-        ib0 = g.off_e[0] + (ex_ + (long long)nx * (fy + ny1 * ez_)) * NI + ea; ib1 = ib0 + (long long)nx * ny1 * NI;
-        okb0 = !zdir(g, ez_); okb1 = !zdir(g, ez_ + 1);
-        wA = cf.ef[1][0]; wB = cf.ef[1][2]; kf = cf.kf[1];
-      } else {                   // z-face (ex, ey, fz): A = y-edges (ex / ex+1, ey, fz), B = x-edges (ex, ey / ey+1, fz)
-        const int ey_ = row % ny, fz = row / ny, ex_ = a;
-        fid = ex_ + (long long)nx * (ey_ + (long long)ny * fz);
-        fr = !zdir(g, fz);
-        so = (long long)nx * ny * N2; olo = fz - 1 >= 0 && !zdir(g, fz - 1); ohi = fz + 1 <= nz && !zdir(g, fz + 1);
-        ia0 = g.off_e[1] + (ex_ + nx1 * (ey_ + (long long)ny * fz)) * NI; ia1 = ia0 + NI;
-        oka0 = in_f(ex_, nx); oka1 = in_f(ex_ + 1, nx);
-        ib0 = g.off_e[0] + (ex_ + (long long)nx * (ey_ + ny1 * fz)) * NI + ea; ib1 = ib0 + (long long)nx * NI;
-        okb0 = in_f(ey_, ny); okb1 = in_f(ey_ + 1, ny);
-        wA = cf.ef[2][0]; wB = cf.ef[2][1]; kf = cf.kf[2];
-      }
-      const long long i0 = g.off_f[cls] + fid * N2 + ea;
-      if (fr) {
-        const double b0 = ldv<NI>(x, ib0, okb0), b1 = ldv<NI>(x, ib1, okb1);
-        const double a0e = sa0[ea], ape = sap[ea];
-#pragma unroll
-        for (int eb = 0; eb < NI; ++eb) {
-          const long long i = i0 + NI * eb;
-          const double u = __ldg(x + i);
-          const double uo = ldv<NI>(x, i - so, olo) + ldv<NI>(x, i + so, ohi);
-          const double ea_ = a0e * ldv<NI>(x, ia0 + eb, oka0) + ape * ldv<NI>(x, ia1 + eb, oka1);
-          const double eb_ = sa0[eb] * b0 + sap[eb] * b1;
-          const double yv = sfd[ea + NI * eb] * u + kf * uo + wA * ea_ + wB * eb_ + P.u0[i] + P.u1[i];
-          if (DOT) dot = fma(u, yv, dot);
-          P.y[i] = yv;
-        }
-      } else {
-#pragma unroll
-        for (int eb = 0; eb < NI; ++eb) P.y[i0 + NI * eb] = 0.0;
-      }
-    }
-  } else if (cls <= 5) {
-    // ---------------- edges (entry m along the edge)
-    const int a = t / NI, m = t - a * NI;
-    const int dir = cls - 3;
-    const int rowlen = dir == 0 ? nx : nx + 1;
-    if (a < rowlen) {
-      long long i0;
-      bool fr;
+  __syncthreads();
+  double dot = 0.0;
+  const bool zb0 = !zdir(g, cz), zb1 = !zdir(g, cz + 1);   // planes cz, cz + 1 free (as z-planes)
+  // ---------------- x-faces (fx, ey = cy, ez = cz), fx = 0..nx; in-plane (ea, eb) = (j, k)
+  if (cy < ny && cz < nz) {
+    const long long base = g.off_f[0] + nx1 * (cy + (long long)ny * cz) * N2;
+    const long long za = g.off_e[2] + nx1 * (cy + ny1 * cz) * NI;   // z-edges (fx, cy, cz); (fx, cy + 1, cz) at + nx1 NI
+    const long long yb = g.off_e[1] + nx1 * (cy + (long long)ny * cz) * NI;   // y-edges (fx, cy, cz); cz + 1 at + nx1 ny NI
+    const bool oka0 = in_f(cy, ny), oka1 = in_f(cy + 1, ny);
+    const double wA = cf.ef[0][1], wB = cf.ef[0][2], kf = cf.kf[0];
+    for (int t = threadIdx.x; t < (nx + 1) * N2; t += blockDim.x) {
+      const int fx = t / N2, e = t - fx * N2, eb = e / NI, ea = e - eb * NI;
       double yv = 0.0;
-      if (dir == 0) {   // x-edge (ex, fy, fz): lines in z-faces (ex, fy-1 / fy, fz) over j, y-faces (ex, fy, fz-1 / fz) over k
-        const int fy = row % (ny + 1), fz = row / (ny + 1), ex_ = a;
-        i0 = g.off_e[0] + (ex_ + (long long)nx * (fy + ny1 * fz)) * NI + m;
-        fr = in_f(fy, ny) && !zdir(g, fz);
-        if (fr) {
-          const double u = __ldg(x + i0);
-          const double vw = ldv<NI>(x, g.off_v + ex_ + nx1 * (fy + ny1 * fz), in_f(ex_, nx));
-          const double ve = ldv<NI>(x, g.off_v + ex_ + 1 + nx1 * (fy + ny1 * fz), in_f(ex_ + 1, nx));
-          const long long zlo = g.off_f[2] + (ex_ + (long long)nx * (fy - 1 + (long long)ny * fz)) * N2 + m;   // entries (i = m, j)
-          const long long zhi = zlo + (long long)nx * N2;
-          const long long ylo = g.off_f[1] + (ex_ + (long long)nx * (fy + ny1 * (fz - 1))) * N2 + m;         // entries (i = m, k)
-          const long long yhi = ylo + (long long)nx * ny1 * N2;
-          const bool zf_ok = !zdir(g, fz);
-          double lz = 0.0, ly = 0.0;
-#pragma unroll
-          for (int q = 0; q < NI; ++q) {
-            lz = fma(cf.ap[q], zf_ok ? __ldg(x + zlo + NI * q) : 0.0, fma(cf.a0[q], zf_ok ? __ldg(x + zhi + NI * q) : 0.0, lz));
-            ly = fma(cf.ap[q], __ldg(x + ylo + NI * q), fma(cf.a0[q], __ldg(x + yhi + NI * q), ly));
-          }
-          const double nb_y = ldv<NI>(x, i0 - (long long)nx * NI, fy - 1 > 0) + ldv<NI>(x, i0 + (long long)nx * NI, fy + 1 < ny);
-          const long long pl = (long long)nx * ny1 * NI;
-          const double nb_z = ldv<NI>(x, i0 - pl, fz - 1 >= 0 && !zdir(g, fz - 1)) + ldv<NI>(x, i0 + pl, fz + 1 <= nz && !zdir(g, fz + 1));
-          yv = sself[m] * u + cf.ev[0] * (sa0[m] * vw + sap[m] * ve) + cf.el[0][1] * fma(cf.K0p, nb_y, lz) +
-               cf.el[0][2] * fma(cf.K0p, nb_z, ly);
-          if (DOT) dot = u * yv;
-        }
-      } else if (dir == 1) {   // y-edge (fx, ey, fz): lines in z-faces (fx-1 / fx, ey, fz) over i, x-faces (fx, ey, fz-1 / fz) over k
-        const int ey_ = row % ny, fz = row / ny, fx = a;
-        i0 = g.off_e[1] + (fx + nx1 * (ey_ + (long long)ny * fz)) * NI + m;
-        fr = in_f(fx, nx) && !zdir(g, fz);
-        if (fr) {
-          const double u = __ldg(x + i0);
-          const double vs = ldv<NI>(x, g.off_v + fx + nx1 * (ey_ + ny1 * fz), in_f(ey_, ny));
-          const double vn = ldv<NI>(x, g.off_v + fx + nx1 * (ey_ + 1 + ny1 * fz), in_f(ey_ + 1, ny));
-          const long long zlo = g.off_f[2] + (fx - 1 + (long long)nx * (ey_ + (long long)ny * fz)) * N2 + NI * m;  // entries (i, j = m)
-          const long long zhi = zlo + N2;
-          const long long xlo = g.off_f[0] + (fx + nx1 * (ey_ + (long long)ny * (fz - 1))) * N2 + m;        // entries (j = m, k)
-          const long long xhi = xlo + nx1 * ny * N2;
-          double lz = 0.0, lx = 0.0;
-#pragma unroll
-          for (int q = 0; q < NI; ++q) {
-            lz = fma(cf.ap[q], __ldg(x + zlo + q), fma(cf.a0[q], __ldg(x + zhi + q), lz));
-            lx = fma(cf.ap[q], __ldg(x + xlo + NI * q), fma(cf.a0[q], __ldg(x + xhi + NI * q), lx));
-          }
-          const double nb_x = ldv<NI>(x, i0 - NI, fx - 1 > 0) + ldv<NI>(x, i0 + NI, fx + 1 < nx);
-          const long long pl = nx1 * ny * NI;
-          const double nb_z = ldv<NI>(x, i0 - pl, fz - 1 >= 0 && !zdir(g, fz - 1)) + ldv<NI>(x, i0 + pl, fz + 1 <= nz && !zdir(g, fz + 1));
-          yv = sself[m] * u + cf.ev[1] * (sa0[m] * vs + sap[m] * vn) + cf.el[1][0] * fma(cf.K0p, nb_x, lz) +
-               cf.el[1][2] * fma(cf.K0p, nb_z, lx);
-          if (DOT) dot = u * yv;
-        }
-      } else {   // z-edge (fx, fy, ez): lines in y-faces (fx-1 / fx, fy, ez) over i, x-faces (fx, fy-1 / fy, ez) over j
-        const int fy = row % (ny + 1), ez_ = row / (ny + 1), fx = a;
-        i0 = g.off_e[2] + (fx + nx1 * (fy + ny1 * ez_)) * NI + m;
-        fr = in_f(fx, nx) && in_f(fy, ny);
-        if (fr) {
-          const double u = __ldg(x + i0);
-          const double vb = ldv<NI>(x, g.off_v + fx + nx1 * (fy + ny1 * ez_), !zdir(g, ez_));
-          const double vt = ldv<NI>(x, g.off_v + fx + nx1 * (fy + ny1 * (ez_ + 1)), !zdir(g, ez_ + 1));
-          const long long ylo = g.off_f[1] + (fx - 1 + (long long)nx * (fy + ny1 * ez_)) * N2 + NI * m;   // entries (i, k = m)
-          const long long yhi = ylo + N2;
-          const long long xlo = g.off_f[0] + (fx + nx1 * (fy - 1 + (long long)ny * ez_)) * N2 + NI * m;   // entries (j, k = m)
-          const long long xhi = xlo + nx1 * N2;
-          double ly = 0.0, lx = 0.0;
-#pragma unroll
-          for (int q = 0; q < NI; ++q) {
-            ly = fma(cf.ap[q], __ldg(x + ylo + q), fma(cf.a0[q], __ldg(x + yhi + q), ly));
-            lx = fma(cf.ap[q], __ldg(x + xlo + q), fma(cf.a0[q], __ldg(x + xhi + q), lx));
-          }
-          const double nb_x = ldv<NI>(x, i0 - NI, fx - 1 > 0) + ldv<NI>(x, i0 + NI, fx + 1 < nx);
-          const double nb_y = ldv<NI>(x, i0 - nx1 * NI, fy - 1 > 0) + ldv<NI>(x, i0 + nx1 * NI, fy + 1 < ny);
-          yv = sself[m] * u + cf.ev[2] * (sa0[m] * vb + sap[m] * vt) + cf.el[2][0] * fma(cf.K0p, nb_x, ly) +
-               cf.el[2][1] * fma(cf.K0p, nb_y, lx);
-          if (DOT) dot = u * yv;
-        }
+      if (in_f(fx, nx)) {
+        double u;
+        const long long ia0 = za + (long long)fx * NI, ib0 = yb + (long long)fx * NI;
+        yv = face_entry<NI>(P, sfd[0], sa0, sap, base + t, e, ea, eb, N2, fx - 1 > 0, fx + 1 < nx, ia0, ia0 + nx1 * NI,
+                            oka0, oka1, ib0, ib0 + nx1 * ny * NI, zb0, zb1, wA, wB, kf, u);
+        if (DOT) dot = fma(u, yv, dot);
       }
-      P.y[i0] = yv;
+      __stcs(y + base + t, yv);
     }
-  } else {
-    // ---------------- vertices (fx, fy, fz): lines along the 6 incident edges
-    const int fx = t, fy = row % (ny + 1), fz = row / (ny + 1);
-    if (fx <= nx) {
-      const long long i0 = g.off_v + fx + nx1 * (fy + ny1 * fz);
-      const bool fr = in_f(fx, nx) && in_f(fy, ny) && !zdir(g, fz);
+  }
+  // ---------------- y-faces (ex, fy = cy, ez = cz), ex = 0..nx-1; in-plane (ea, eb) = (i, k)
+  if (cz < nz) {
+    const long long base = g.off_f[1] + (long long)nx * (cy + ny1 * cz) * N2;
+    const long long za = g.off_e[2] + nx1 * (cy + ny1 * cz) * NI;   // z-edges (ex, cy, cz), (ex + 1, ...) at + NI
+    const long long xb = g.off_e[0] + (long long)nx * (cy + ny1 * cz) * NI;   // x-edges (ex, cy, cz); cz + 1 at + nx ny1 NI
+    const bool fr = in_f(cy, ny);
+    const double wA = cf.ef[1][0], wB = cf.ef[1][2], kf = cf.kf[1];
+    for (int t = threadIdx.x; t < nx * N2; t += blockDim.x) {
+      const int ex = t / N2, e = t - ex * N2, eb = e / NI, ea = e - eb * NI;
+      double yv = 0.0;
+      if (fr) {
+        double u;
+        const long long ia0 = za + (long long)ex * NI, ib0 = xb + (long long)ex * NI;
+        yv = face_entry<NI>(P, sfd[1], sa0, sap, base + t, e, ea, eb, (long long)nx * N2, cy - 1 > 0, cy + 1 < ny, ia0,
+                            ia0 + NI, in_f(ex, nx), in_f(ex + 1, nx), ib0, ib0 + (long long)nx * ny1 * NI, zb0, zb1, wA,
+                            wB, kf, u);
+        if (DOT) dot = fma(u, yv, dot);
+      }
+      __stcs(y + base + t, yv);
+    }
+  }
+  // ---------------- z-faces (ex, ey = cy, fz = cz), ex = 0..nx-1; in-plane (ea, eb) = (i, j)
+  if (cy < ny) {
+    const long long base = g.off_f[2] + (long long)nx * (cy + (long long)ny * cz) * N2;
+    const long long ya = g.off_e[1] + nx1 * (cy + (long long)ny * cz) * NI;   // y-edges (ex, cy, cz), (ex + 1, ...) at + NI
+    const long long xb = g.off_e[0] + (long long)nx * (cy + ny1 * cz) * NI;   // x-edges (ex, cy, cz); cy + 1 at + nx NI
+    const bool fr = zb0;
+    const bool olo = cz - 1 >= 0 && !zdir(g, cz - 1), ohi = cz + 1 <= nz && !zdir(g, cz + 1);
+    const bool okb0 = in_f(cy, ny), okb1 = in_f(cy + 1, ny);
+    const double wA = cf.ef[2][0], wB = cf.ef[2][1], kf = cf.kf[2];
+    for (int t = threadIdx.x; t < nx * N2; t += blockDim.x) {
+      const int ex = t / N2, e = t - ex * N2, eb = e / NI, ea = e - eb * NI;
+      double yv = 0.0;
+      if (fr) {
+        double u;
+        const long long ia0 = ya + (long long)ex * NI, ib0 = xb + (long long)ex * NI;
+        yv = face_entry<NI>(P, sfd[2], sa0, sap, base + t, e, ea, eb, (long long)nx * ny * N2, olo, ohi, ia0, ia0 + NI,
+                            in_f(ex, nx), in_f(ex + 1, nx), ib0, ib0 + (long long)nx * NI, okb0, okb1, wA, wB, kf, u);
+        if (DOT) dot = fma(u, yv, dot);
+      }
+      __stcs(y + base + t, yv);
+    }
+  }
+  // ---------------- edges: the face-line sums (z-faces (ex, cy-1 / cy, cz) over j and y-faces (ex, cy, cz-1 / cz)
+  // over k for an x-edge, cyclically for y / z) come from pass A in U0 + U1 at the edge's entries.
+  // x-edges (ex, fy = cy, fz = cz), entry m
+  {
+    const long long base = g.off_e[0] + (long long)nx * (cy + ny1 * cz) * NI;
+    const bool fr = in_f(cy, ny) && zb0;
+    const bool ylo = cz - 1 >= 0 && !zdir(g, cz - 1), yhi = cz + 1 <= nz && !zdir(g, cz + 1);
+    for (int t = threadIdx.x; t < nx * NI; t += blockDim.x) {
+      const int ex = t / NI, m = t - ex * NI;
+      const long long i0 = base + t;
       double yv = 0.0;
       if (fr) {
         const double u = __ldg(x + i0);
-        const long long xw = g.off_e[0] + (fx - 1 + (long long)nx * (fy + ny1 * fz)) * NI, xe = xw + NI;
-        const long long ys = g.off_e[1] + (fx + nx1 * (fy - 1 + (long long)ny * fz)) * NI, yn = ys + nx1 * NI;
-        const long long zb = g.off_e[2] + (fx + nx1 * (fy + ny1 * (fz - 1))) * NI, zt = zb + nx1 * ny1 * NI;
+        const double vw = ldv(x, g.off_v + ex + nx1 * (cy + ny1 * cz), in_f(ex, nx));
+        const double ve = ldv(x, g.off_v + ex + 1 + nx1 * (cy + ny1 * cz), in_f(ex + 1, nx));
+        const double nb_y = ldv(x, i0 - (long long)nx * NI, cy - 1 > 0) + ldv(x, i0 + (long long)nx * NI, cy + 1 < ny);
+        const long long pl = (long long)nx * ny1 * NI;
+        const double nb_z = ldv(x, i0 - pl, ylo) + ldv(x, i0 + pl, yhi);
+        yv = sself[0][m] * u + cf.ev[0] * (sa0[m] * vw + sap[m] * ve) + cf.el[0][1] * cf.K0p * nb_y +
+             cf.el[0][2] * cf.K0p * nb_z + __ldcs(P.u0 + i0) + __ldcs(P.u1 + i0);
+        if (DOT) dot = fma(u, yv, dot);
+      }
+      __stcs(y + i0, yv);
+    }
+  }
+  // ---------------- y-edges (fx, ey = cy, fz = cz)
+  if (cy < ny) {
+    const long long base = g.off_e[1] + nx1 * (cy + (long long)ny * cz) * NI;
+    const bool ylo = cz - 1 >= 0 && !zdir(g, cz - 1), yhi = cz + 1 <= nz && !zdir(g, cz + 1);
+    for (int t = threadIdx.x; t < (nx + 1) * NI; t += blockDim.x) {
+      const int fx = t / NI, m = t - fx * NI;
+      const long long i0 = base + t;
+      double yv = 0.0;
+      if (in_f(fx, nx) && zb0) {
+        const double u = __ldg(x + i0);
+        const double vs = ldv(x, g.off_v + fx + nx1 * (cy + ny1 * cz), in_f(cy, ny));
+        const double vn = ldv(x, g.off_v + fx + nx1 * (cy + 1 + ny1 * cz), in_f(cy + 1, ny));
+        const double nb_x = ldv(x, i0 - NI, fx - 1 > 0) + ldv(x, i0 + NI, fx + 1 < nx);
+        const long long pl = nx1 * ny * NI;
+        const double nb_z = ldv(x, i0 - pl, ylo) + ldv(x, i0 + pl, yhi);
+        yv = sself[1][m] * u + cf.ev[1] * (sa0[m] * vs + sap[m] * vn) + cf.el[1][0] * cf.K0p * nb_x +
+             cf.el[1][2] * cf.K0p * nb_z + __ldcs(P.u0 + i0) + __ldcs(P.u1 + i0);
+        if (DOT) dot = fma(u, yv, dot);
+      }
+      __stcs(y + i0, yv);
+    }
+  }
+  // ---------------- z-edges (fx, fy = cy, ez = cz)
+  if (cz < nz) {
+    const long long base = g.off_e[2] + nx1 * (cy + ny1 * cz) * NI;
+    const bool fry = in_f(cy, ny);
+    for (int t = threadIdx.x; t < (nx + 1) * NI; t += blockDim.x) {
+      const int fx = t / NI, m = t - fx * NI;
+      const long long i0 = base + t;
+      double yv = 0.0;
+      if (in_f(fx, nx) && fry) {
+        const double u = __ldg(x + i0);
+        const double vb = ldv(x, g.off_v + fx + nx1 * (cy + ny1 * cz), zb0);
+        const double vt = ldv(x, g.off_v + fx + nx1 * (cy + ny1 * (cz + 1)), zb1);
+        const double nb_x = ldv(x, i0 - NI, fx - 1 > 0) + ldv(x, i0 + NI, fx + 1 < nx);
+        const double nb_y = ldv(x, i0 - nx1 * NI, cy - 1 > 0) + ldv(x, i0 + nx1 * NI, cy + 1 < ny);
+        yv = sself[2][m] * u + cf.ev[2] * (sa0[m] * vb + sap[m] * vt) + cf.el[2][0] * cf.K0p * nb_x +
+             cf.el[2][1] * cf.K0p * nb_y + __ldcs(P.u0 + i0) + __ldcs(P.u1 + i0);
+        if (DOT) dot = fma(u, yv, dot);
+      }
+      __stcs(y + i0, yv);
+    }
+  }
+  // ---------------- vertices (fx, cy, cz): lines along the 6 incident edges
+  {
+    const bool fr = in_f(cy, ny) && zb0;
+    const bool zlo_ok = cz - 1 >= 0 && !zdir(g, cz - 1), zhi_ok = cz + 1 <= nz && !zdir(g, cz + 1);
+    for (int fx = threadIdx.x; fx <= nx; fx += blockDim.x) {
+      const long long i0 = g.off_v + fx + nx1 * (cy + ny1 * cz);
+      double yv = 0.0;
+      if (fr && in_f(fx, nx)) {
+        const double u = __ldg(x + i0);
+        const long long xw = g.off_e[0] + (fx - 1 + (long long)nx * (cy + ny1 * cz)) * NI, xe = xw + NI;
+        const long long ys = g.off_e[1] + (fx + nx1 * (cy - 1 + (long long)ny * cz)) * NI, yn = ys + nx1 * NI;
+        const long long zb = g.off_e[2] + (fx + nx1 * (cy + ny1 * (cz - 1))) * NI, zt = zb + nx1 * ny1 * NI;
         double lx = 0.0, ly = 0.0, lz = 0.0;
 #pragma unroll
         for (int q = 0; q < NI; ++q) {
@@ -418,14 +794,14 @@ __global__ void __launch_bounds__(256) k_v7_assemble(const __grid_constant__ V7P
           ly = fma(cf.ap[q], __ldg(x + ys + q), fma(cf.a0[q], __ldg(x + yn + q), ly));
           lz = fma(cf.ap[q], __ldg(x + zb + q), fma(cf.a0[q], __ldg(x + zt + q), lz));
         }
-        const double nbx = ldv<NI>(x, i0 - 1, fx - 1 > 0) + ldv<NI>(x, i0 + 1, fx + 1 < nx);
-        const double nby = ldv<NI>(x, i0 - nx1, fy - 1 > 0) + ldv<NI>(x, i0 + nx1, fy + 1 < ny);
+        const double nbx = ldv(x, i0 - 1, fx - 1 > 0) + ldv(x, i0 + 1, fx + 1 < nx);
+        const double nby = ldv(x, i0 - nx1, cy - 1 > 0) + ldv(x, i0 + nx1, cy + 1 < ny);
         const long long pl = nx1 * ny1;
-        const double nbz = ldv<NI>(x, i0 - pl, fz - 1 >= 0 && !zdir(g, fz - 1)) + ldv<NI>(x, i0 + pl, fz + 1 <= nz && !zdir(g, fz + 1));
+        const double nbz = ldv(x, i0 - pl, zlo_ok) + ldv(x, i0 + pl, zhi_ok);
         yv = cf.vself * u + cf.vl[0] * fma(cf.K0p, nbx, lx) + cf.vl[1] * fma(cf.K0p, nby, ly) + cf.vl[2] * fma(cf.K0p, nbz, lz);
-        if (DOT) dot = u * yv;
+        if (DOT) dot = fma(u, yv, dot);
       }
-      P.y[i0] = yv;
+      __stcs(y + i0, yv);
     }
   }
   if (DOT) {
@@ -437,7 +813,7 @@ __global__ void __launch_bounds__(256) k_v7_assemble(const __grid_constant__ V7P
     if (threadIdx.x == 0) {
       double s = 0.0;
       for (int w = 0; w < 8; ++w) s += red[w];
-      P.dotp[(long long)blockIdx.z * gridDim.y * gridDim.x + (long long)blockIdx.y * gridDim.x + blockIdx.x] = s;
+      P.dotp[blockIdx.x] = s;
     }
   }
 }
@@ -496,51 +872,57 @@ void v7_make_coef(int ni, const double* d, const double* a0, const double* ap, c
   memcpy(out.data(), &c, sizeof(c));
 }
 
-// Number of pass-B blocks (the p . q partials the PCG sums).
-static void v7_grid(const Geom& g, int cls, dim3& grid) {
-  const int ni = g.ni, nx = g.nx, ny = g.ny, nz = g.nz;
-  long long len, rows;
-  switch (cls) {
-    case 0: len = (long long)(nx + 1) * ni; rows = (long long)ny * nz; break;     // faces: thread per (face, entry row)
-    case 1: len = (long long)nx * ni; rows = (long long)(ny + 1) * nz; break;
-    case 2: len = (long long)nx * ni; rows = (long long)ny * (nz + 1); break;
-    case 3: len = (long long)nx * ni; rows = (long long)(ny + 1) * (nz + 1); break;
-    case 4: len = (long long)(nx + 1) * ni; rows = (long long)ny * (nz + 1); break;
-    case 5: len = (long long)(nx + 1) * ni; rows = (long long)(ny + 1) * nz; break;
-    default: len = nx + 1; rows = (long long)(ny + 1) * (nz + 1); break;
-  }
-  grid = dim3((unsigned)((len + 255) / 256), (unsigned)rows, 1);
-}
-
-long long v7_dot_parts(const Geom& g) {
-  long long tot = 0;
-  for (int c = 0; c < 7; ++c) {
-    dim3 gr;
-    v7_grid(g, c, gr);
-    tot += (long long)gr.x * gr.y;
-  }
-  return tot;
-}
+// Number of pass-B blocks (the p . q partials the PCG sums): one per cell row.
+long long v7_dot_parts(const Geom& g) { return (long long)(g.ny + 1) * (g.nz + 1); }
 
 template <int NI>
 static int launch_v7_t(V7Params& P, cudaStream_t st, int* nl) {
   const Geom& g = P.g;
-  dim3 ga((unsigned)((g.nx + v7::RUN - 1) / v7::RUN), (unsigned)g.ny, (unsigned)g.nz);
-  v7::k_v7_cond<NI><<<ga, 128, 0, st>>>(P);
-  (*nl)++;
-  double* dotp = P.dotp;
-  for (int c = 0; c < 7; ++c) {
-    dim3 gb;
-    v7_grid(g, c, gb);
-    if (dotp) {
-      v7::k_v7_assemble<NI, true><<<gb, 256, 0, st>>>(P, c);
-      P.dotp += (long long)gb.x * gb.y;
-    } else {
-      v7::k_v7_assemble<NI, false><<<gb, 256, 0, st>>>(P, c);
-    }
-    (*nl)++;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static const char* sg = getenv("SC_V7_STAGES");
+  static const char* sa = getenv("SC_V7_A");
+  const int two = !(sg && sg[0] == '1');
+  const int lines = !(sa && sa[0] == 'c');
+  // per device: dynamic shared memory opt-in and resident CTAs per SM of the chosen pass-A kernel
+  static int attr_done[64][2][2] = {{{0}}}, per_sm[64][2][2] = {{{0}}}, nsm_c[64] = {0};
+  const void* fn;
+  int smem, nthr, run;
+  if (lines) {
+    fn = two ? (const void*)v7::k_v7_lines<NI, 2> : (const void*)v7::k_v7_lines<NI, 1>;
+    smem = two ? v7::V8A<NI, 2>::SMEM : v7::V8A<NI, 1>::SMEM;
+    nthr = v7::V8A<NI, 1>::NT;
+    run = v7::V8A<NI, 1>::R;
+  } else {
+    fn = two ? (const void*)v7::k_v7_cond<NI, 2> : (const void*)v7::k_v7_cond<NI, 1>;
+    smem = two ? v7::V7A<NI, 2>::SMEM : v7::V7A<NI, 1>::SMEM;
+    nthr = 128;
+    run = v7::RUN;
   }
-  P.dotp = dotp;
+  if (dev < 64 && !attr_done[dev][lines][two]) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev][lines][two], fn, nthr, smem);
+    cudaDeviceGetAttribute(&nsm_c[dev], cudaDevAttrMultiProcessorCount, dev);
+    attr_done[dev][lines][two] = 1;
+  }
+  const int nruns = (g.nx + run - 1) / run;
+  const int nitems = nruns * g.ny * g.nz;
+  const int slots = (dev < 64 ? max(per_sm[dev][lines][two], 1) * nsm_c[dev] : 148);
+  const int grid = nitems < slots ? nitems : slots;
+  if (grid > 0) {
+    if (lines) {
+      if (two) v7::k_v7_lines<NI, 2><<<grid, nthr, smem, st>>>(P, nitems, nruns);
+      else v7::k_v7_lines<NI, 1><<<grid, nthr, smem, st>>>(P, nitems, nruns);
+    } else {
+      if (two) v7::k_v7_cond<NI, 2><<<grid, nthr, smem, st>>>(P, nitems, nruns);
+      else v7::k_v7_cond<NI, 1><<<grid, nthr, smem, st>>>(P, nitems, nruns);
+    }
+  }
+  (*nl)++;
+  const unsigned rows = (unsigned)((g.ny + 1) * (g.nz + 1));
+  if (P.dotp) v7::k_v7_assemble<NI, true><<<rows, 256, 0, st>>>(P);
+  else v7::k_v7_assemble<NI, false><<<rows, 256, 0, st>>>(P);
+  (*nl)++;
   v7::k_v7_padding<<<1, 256, 0, st>>>(g, P.y);
   (*nl)++;
   return cudaGetLastError();

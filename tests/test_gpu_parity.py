@@ -251,9 +251,11 @@ def test_pcg_parity_multitile(p, ne, fused, monkeypatch):
     SC_FUSED_DOT=0 selects the separate dot kernel)."""
     from paper_1601_08179_b200 import SC_DUAL
     monkeypatch.setenv("SC_FUSED_DOT", fused)
+    monkeypatch.setenv("SC_OP", "v3")
     g = small_grid(p, ne, 1.0, lengths=(1.3, 0.7, 0.5))
     op = operator.AssembledCondensedOperator(g)
     ctx = ctx_for(g)
+    assert ctx.operator_kernel() == "v3"
     bt = ctx.skeleton()
     ctx.sc_fill_random(8, bt)
     lat = ctx.lattice()
@@ -340,6 +342,7 @@ def test_col_kernel_matches_v1_kernel_large():
 @pytest.mark.parametrize("nseg", ["1", "2", "3", "4", "7"])
 def test_operator_parity_zsegments(p, ne, nseg, monkeypatch):
     monkeypatch.setenv("SC_ZSEG", nseg)
+    monkeypatch.setenv("SC_OP", "v6")   # a tile-column kernel (the one-rank default v7 has no z-segments)
     g = small_grid(p, ne, 0.6, lengths=(1.1, 0.9, 1.4))
     op = operator.AssembledCondensedOperator(g)
     x = lattice_random(40 + p, g.ne, g.p).ravel()
@@ -353,6 +356,7 @@ def test_pcg_parity_zsegments(nseg, fused, monkeypatch):
     from paper_1601_08179_b200 import SC_DUAL
     monkeypatch.setenv("SC_ZSEG", nseg)
     monkeypatch.setenv("SC_FUSED_DOT", fused)
+    monkeypatch.setenv("SC_OP", "v6")
     g = small_grid(6, (10, 6, 8), 1.0, lengths=(1.3, 0.7, 1.5))   # p = 6: a tile-column kernel (v6)
     op = operator.AssembledCondensedOperator(g)
     ctx = ctx_for(g)
