@@ -118,8 +118,9 @@ struct V7A {
   static constexpr int SMEM = (STAGES * STAGE + SR + ND) * 8;   // the stages, the zero row, D^{-1}
 };
 
-struct Item {
+struct __align__(16) Item {
   int ex0, cnt, ey, ez;
+  int par, dirm;    // bit r: range r starts at an odd index / is a Dirichlet row
   long long s[5];   // range starts: x row, y rows ey / ey + 1, z planes ez / ez + 1
   bool dir[5];      // Dirichlet row (not copied)
 };
@@ -147,6 +148,12 @@ __device__ __forceinline__ Item decode(const Geom& g, int item, int nruns) {
     it.dir[1 + s] = !(fy > 0 && fy < g.ny);
     it.s[3 + s] = g.off_f[2] + (it.ex0 + nx * (it.ey + ny * fz)) * N2;
     it.dir[3 + s] = zdir(g, fz);
+  }
+  it.par = 0;
+  it.dirm = 0;
+  for (int r = 0; r < 5; ++r) {
+    it.par |= (int)(it.s[r] & 1) << r;
+    it.dirm |= (int)it.dir[r] << r;
   }
   return it;
 }
@@ -376,9 +383,12 @@ __global__ void __launch_bounds__(128, STAGES == 1 ? 4 : 3) k_v7_cond(const __gr
 template <int NI, int STAGES>
 struct V8A {
   static constexpr int N2 = NI * NI, N3 = N2 * NI;
-  static constexpr int R = 8;                                // elements per item (x-run)
-  static constexpr int G = (8 * N2 <= 256) ? 8 : 4;          // elements per thread group
+  // elements per item (x-run) and per thread group (G N2 <= 256 threads in the line phases)
+  static constexpr int R = NI >= 6 ? 8 : (NI >= 4 ? 16 : 32);
+  static constexpr int G = NI >= 6 ? 4 : (NI == 5 ? 8 : (NI == 4 ? 16 : (NI == 3 ? 16 : 32)));
   static constexpr int NT = ((G * N2 + 31) / 32) * 32;       // threads per CTA
+  static constexpr int EWF = ((R * 2 * NI + 31) / 32) * 32;  // edge-phase slots per family (warp-rounded)
+  static constexpr int MINB = STAGES == 2 ? 3 : (NT <= 128 ? 8 : (NT <= 160 ? 6 : 4));
   static constexpr int SX = ((R + 1) * N2 + 2 + 1) & ~1;
   static constexpr int SR = (R * N2 + 2 + 1) & ~1;
   static constexpr int STAGE = SX + 4 * SR;
@@ -386,77 +396,36 @@ struct V8A {
   static constexpr int SMEM = (STAGES * STAGE + SR + R * VS) * 8;
 };
 
-// Per-lane constants of one edge line sum (output o = kind NI + m of an element, see k_v7_cond):
-// kinds 0 / 1 x-edges, 2 / 3 y-edges, 4 / 5 z-edges; even kinds the a0-weighted lines of the element's low
-// faces (U0 at its low edge), odd kinds the ap = sigma a0 weighted lines of its high faces (U1 at its high
-// edge).  Face rows: 0 / 1 = z-face B / T, 2 / 3 = y-face S / N, 4 / 5 = x-face W / E.
-struct EdgeLane {
-  int f1, f2;             // face rows of the two lines
-  int o1, s1, o2, s2;     // line start / stride inside the face (doubles)
-  double e1, e2, sgn;     // line weights (2 d w0 of the transverse directions), -1 on odd q for odd kinds
-  long long base, dey, dez;   // U index = base + NI ex + dey ey + dez ez
-  bool hi, on;
-};
-
-template <int NI>
-__device__ __forceinline__ EdgeLane edge_lane(const Geom& g, const V7Coef& cf, int o) {
-  EdgeLane E;
-  const int kind = o / NI, m = o - kind * NI;
-  const long long nx = g.nx, ny = g.ny, nx1 = nx + 1, ny1 = ny + 1;
-  E.on = o < 6 * NI;
-  E.hi = kind & 1;
-  const int h = E.hi;
-  E.sgn = h ? -1.0 : 1.0;
-  if (kind < 2) {          // x-edge (ex, ey + h, ez + h): z-face (m, q) over j, y-face (m, q) over k
-    E.f1 = h; E.o1 = m; E.s1 = NI;
-    E.f2 = 2 + h; E.o2 = m; E.s2 = NI;
-    E.e1 = cf.el[0][1]; E.e2 = cf.el[0][2];
-    E.base = g.off_e[0] + (nx * (h + ny1 * h)) * NI + m; E.dey = nx * NI; E.dez = nx * ny1 * NI;
-  } else if (kind < 4) {   // y-edge (ex + h, ey, ez + h): z-face (q, m) over i, x-face (m, q) over k
-    E.f1 = h; E.o1 = NI * m; E.s1 = 1;
-    E.f2 = 4 + h; E.o2 = m; E.s2 = NI;
-    E.e1 = cf.el[1][0]; E.e2 = cf.el[1][2];
-    E.base = g.off_e[1] + (h + nx1 * ny * h) * NI + m; E.dey = nx1 * NI; E.dez = nx1 * ny * NI;
-  } else {                 // z-edge (ex + h, ey + h, ez): y-face (q, m) over i, x-face (q, m) over j
-    E.f1 = 2 + h; E.o1 = NI * m; E.s1 = 1;
-    E.f2 = 4 + h; E.o2 = NI * m; E.s2 = 1;
-    E.e1 = cf.el[2][0]; E.e2 = cf.el[2][1];
-    E.base = g.off_e[2] + (h + nx1 * h) * NI + m; E.dey = nx1 * NI; E.dez = nx1 * ny1 * NI;
-  }
-  return E;
-}
-
-__device__ __forceinline__ const double* sel6(int f, const double* r0, const double* r1, const double* r2,
-                                              const double* r3, const double* r4, const double* r5) {
-  const double* a = (f & 1) ? r1 : r0;
-  const double* b = (f & 1) ? r3 : r2;
-  const double* c = (f & 1) ? r5 : r4;
-  return f < 2 ? a : (f < 4 ? b : c);
-}
-
-template <int NI>
-__device__ __forceinline__ void edge_sum(const V7Params& P, const EdgeLane& E, const double* r0, const double* r1,
-                                         const double* r2, const double* r3, const double* r4, const double* r5, int ex,
-                                         int ey, int ez) {
-  const double* p1 = sel6(E.f1, r0, r1, r2, r3, r4, r5) + E.o1;
-  const double* p2 = sel6(E.f2, r0, r1, r2, r3, r4, r5) + E.o2;
+// Edge line sums of one element family (see k_v7_cond): F = 0 x-edges, 1 y-edges, 2 z-edges; hi = 0: the
+// a0-weighted lines of the element's low faces (U0 at its low edge), hi = 1: the ap = sigma a0 weighted
+// lines of its high faces (U1 at its high edge).  Line q-strides are compile-time per family.
+template <int NI, int F>
+__device__ __forceinline__ double edge_line(const V7Coef& cf, const double* zb, const double* zt, const double* ys,
+                                            const double* yn, const double* w, const double* e, int hi, int m) {
+  // F = 0: z-face (m, q) over j + y-face (m, q) over k; F = 1: z-face (q, m) over i + x-face (m, q) over k;
+  // F = 2: y-face (q, m) over i + x-face (q, m) over j
+  const double* p1 = F == 0 ? (hi ? zt : zb) + m : (F == 1 ? (hi ? zt : zb) + NI * m : (hi ? yn : ys) + NI * m);
+  const double* p2 = F == 0 ? (hi ? yn : ys) + m : (F == 1 ? (hi ? e : w) + m : (hi ? e : w) + NI * m);
+  constexpr int S1 = F == 0 ? NI : 1, S2 = F == 2 ? 1 : NI;
+  const double e1 = F == 0 ? cf.el[0][1] : (F == 1 ? cf.el[1][0] : cf.el[2][0]);
+  const double e2 = F == 0 ? cf.el[0][2] : (F == 1 ? cf.el[1][2] : cf.el[2][1]);
   double se = 0.0, so = 0.0;
 #pragma unroll
   for (int q = 0; q < NI; ++q) {
-    const double t = fma(E.e1, p1[E.s1 * q], E.e2 * p2[E.s2 * q]);
-    if (q & 1) so = fma(P.cf.a0[q], t, so);
-    else se = fma(P.cf.a0[q], t, se);
+    const double t = fma(e1, p1[S1 * q], e2 * p2[S2 * q]);
+    if (q & 1) so = fma(cf.a0[q], t, so);
+    else se = fma(cf.a0[q], t, se);
   }
-  __stcs((E.hi ? P.u1 : P.u0) + E.base + (long long)NI * ex + E.dey * ey + E.dez * ez, fma(E.sgn, so, se));
+  return hi ? se - so : se + so;
 }
 
 template <int NI, int STAGES>
-__global__ void __launch_bounds__(V8A<NI, STAGES>::NT) k_v7_lines(const __grid_constant__ V7Params P, int nitems,
+__global__ void __launch_bounds__(V8A<NI, STAGES>::NT, V8A<NI, STAGES>::MINB) k_v7_lines(const __grid_constant__ V7Params P, int nitems,
                                                                   int nruns) {
   if (P.done != nullptr && *P.done != 0.0) return;
   using A = V8A<NI, STAGES>;
   constexpr int N2 = NI * NI, G = A::G, R = A::R;
-  constexpr int NE = (6 * NI + N2 - 1) / N2;   // edge line sums per lane
+  constexpr int EWF = A::EWF;
   const Geom& g = P.g;
   const V7Coef& cf = P.cf;
   const int nx = g.nx, ny = g.ny;
@@ -490,33 +459,42 @@ __global__ void __launch_bounds__(V8A<NI, STAGES>::NT) k_v7_lines(const __grid_c
   for (int i = 0; i < NI; ++i) Dl[i] = lane_on ? cf.dinv[i + NI * l] : 0.0;
   const double c2j = cf.c[1][la], c3k = cf.c[2][lb];
   const double gj = (la & 1) ? -1.0 : 1.0, gk = (lb & 1) ? -1.0 : 1.0;
-  EdgeLane EL[NE];
-#pragma unroll
-  for (int r = 0; r < NE; ++r) EL[r] = edge_lane<NI>(g, cf, l + N2 * r);
   for (int n = 0;; ++n) {
     const int item = blockIdx.x + n * gridDim.x;
     if (item >= nitems) break;
     const int b = STAGES == 1 ? 0 : (n & 1);
     double* const stage = smem + b * A::STAGE;
     mbar_wait(&mbar[b], (unsigned)((STAGES == 1 ? n : (n >> 1)) & 1));
-    const Item it = sit[b];
-    const int ey = it.ey, ez = it.ez;
-    const double* const X = stage + (it.s[0] & 1);
+    const int4 ih = *reinterpret_cast<const int4*>(&sit[b]);   // ex0, cnt, ey, ez
+    const int par = sit[b].par, dirm = sit[b].dirm;
+    const int ex0 = ih.x, cnt = ih.y, ey = ih.z, ez = ih.w;
+    double* const X = stage + (par & 1);
+    // the Dirichlet x-faces fx = 0, nx of a boundary run read as zero (block-uniform branch)
+    if (ex0 == 0 || ex0 + cnt == nx) {
+      if (tid < N2) {
+        if (ex0 == 0) X[tid] = 0.0;
+        if (ex0 + cnt == nx) X[cnt * N2 + tid] = 0.0;
+      }
+      __syncthreads();
+    }
     const double* Yr[2];
     const double* Zr[2];
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
-      Yr[s] = it.dir[1 + s] ? zrow : stage + A::SX + s * A::SR + (it.s[1 + s] & 1);
-      Zr[s] = it.dir[3 + s] ? zrow : stage + A::SX + (2 + s) * A::SR + (it.s[3 + s] & 1);
+      Yr[s] = ((dirm >> (1 + s)) & 1) ? zrow : stage + A::SX + s * A::SR + ((par >> (1 + s)) & 1);
+      Zr[s] = ((dirm >> (3 + s)) & 1) ? zrow : stage + A::SX + (2 + s) * A::SR + ((par >> (3 + s)) & 1);
     }
+    // output bases of the item's first element (face / edge rows are contiguous along x)
+    const long long d01 = P.u1 - P.u0;
+    double* const ux = P.u0 + g.off_f[0] + (ex0 + nx1 * (ey + (long long)ny * ez)) * N2 + l;
+    double* const uy = P.u0 + g.off_f[1] + (ex0 + (long long)nx * (ey + ny1 * ez)) * N2 + l;
+    double* const uz = P.u0 + g.off_f[2] + (ex0 + (long long)nx * (ey + (long long)ny * ez)) * N2 + l;
     // ---- phase X
-#pragma unroll 1
-    for (int gr = 0; gr < R / G; ++gr) {
-      const int el = gr * G + eg, ex = it.ex0 + el;
-      if (lane_on) {
-        const double* Wf = (ex > 0 && ex < nx) ? X + el * N2 : zrow;
-        const double* Ef = (ex + 1 < nx) ? X + (el + 1) * N2 : zrow;
-        const double w = Wf[l], e = Ef[l];
+    if (lane_on) {
+#pragma unroll
+      for (int gr = 0; gr < R / G; ++gr) {
+        const int el = gr * G + eg;
+        const double w = X[el * N2 + l], e = X[(el + 1) * N2 + l];
         const double xs = w + e, xd = w - e;
         const double* S = Yr[0] + el * N2 + NI * lb;   // S(i, k), i = 0..NI-1
         const double* Nn = Yr[1] + el * N2 + NI * lb;
@@ -535,46 +513,67 @@ __global__ void __launch_bounds__(V8A<NI, STAGES>::NT) k_v7_lines(const __grid_c
           else qe = fma(c1, vv, qe);
           v[i] = vv;
         }
-        if (el < it.cnt) {
-          const long long fx = g.off_f[0] + (ex + nx1 * (ey + (long long)ny * ez)) * N2 + l;
-          __stcs(P.u0 + fx, -(qe + qo));        // face ex (the element's W face)
-          __stcs(P.u1 + fx + N2, qo - qe);      // face ex + 1 (E)
+        if (el < cnt) {
+          __stcs(ux + el * N2, -(qe + qo));              // face ex (the element's W face) in U0
+          __stcs(ux + d01 + (el + 1) * N2, qo - qe);     // face ex + 1 (E) in U1
         }
       }
     }
     __syncthreads();
-    // ---- phases Y, Z and the edge line sums
+    // ---- phases Y, Z
+    if (lane_on) {
+#pragma unroll
+      for (int gr = 0; gr < R / G; ++gr) {
+        const int el = gr * G + eg;
+        if (el < cnt) {
+          const double* const v = sv + el * A::VS;
+          double qe = 0.0, qo = 0.0;
+#pragma unroll
+          for (int j = 0; j < NI; ++j) {   // lane (i, k) = (la, lb)
+            const double t = cf.c[1][j] * v[la + NI * (j + NI * lb)];
+            if (j & 1) qo += t;
+            else qe += t;
+          }
+          __stcs(uy + el * N2, -(qe + qo));                                // S face (ey) in U0
+          __stcs(uy + d01 + (long long)nx * N2 + el * N2, qo - qe);        // N face (ey + 1) in U1
+          qe = 0.0; qo = 0.0;
+#pragma unroll
+          for (int k = 0; k < NI; ++k) {   // lane (i, j) = (la, lb)
+            const double t = cf.c[2][k] * v[l + N2 * k];
+            if (k & 1) qo += t;
+            else qe += t;
+          }
+          __stcs(uz + el * N2, -(qe + qo));                                   // B face (ez) in U0
+          __stcs(uz + d01 + (long long)nx * ny * N2 + el * N2, qo - qe);      // T face (ez + 1) in U1
+        }
+      }
+    }
+    // ---- edge line sums: slot -> (family, element, high side, entry); a warp's slots share the family
 #pragma unroll 1
-    for (int gr = 0; gr < R / G; ++gr) {
-      const int el = gr * G + eg, ex = it.ex0 + el;
-      if (lane_on && el < it.cnt) {
-        const double* const v = sv + el * A::VS;
-        double qe = 0.0, qo = 0.0;
-#pragma unroll
-        for (int j = 0; j < NI; ++j) {   // lane (i, k) = (la, lb)
-          const double t = cf.c[1][j] * v[la + NI * (j + NI * lb)];
-          if (j & 1) qo += t;
-          else qe += t;
+    for (int sl = tid; sl < 3 * EWF; sl += A::NT) {
+      const int ef = sl / EWF, er = sl - ef * EWF;
+      const int el = er / (2 * NI), eo = er - el * (2 * NI), ehi = eo / NI, em = eo - ehi * NI;
+      if (el < cnt) {
+        const int ex = ex0 + el;
+        const double* zb = Zr[0] + el * N2;
+        const double* zt = Zr[1] + el * N2;
+        const double* ys = Yr[0] + el * N2;
+        const double* yn = Yr[1] + el * N2;
+        const double* w = X + el * N2;
+        const double* e = X + (el + 1) * N2;
+        double s;
+        long long dst;
+        if (ef == 0) {
+          s = edge_line<NI, 0>(cf, zb, zt, ys, yn, w, e, ehi, em);
+          dst = g.off_e[0] + (ex + (long long)nx * (ey + ehi + ny1 * (ez + ehi))) * NI + em;
+        } else if (ef == 1) {
+          s = edge_line<NI, 1>(cf, zb, zt, ys, yn, w, e, ehi, em);
+          dst = g.off_e[1] + (ex + ehi + nx1 * (ey + (long long)ny * (ez + ehi))) * NI + em;
+        } else {
+          s = edge_line<NI, 2>(cf, zb, zt, ys, yn, w, e, ehi, em);
+          dst = g.off_e[2] + (ex + ehi + nx1 * (ey + ehi + ny1 * ez)) * NI + em;
         }
-        const long long fy = g.off_f[1] + (ex + (long long)nx * (ey + ny1 * ez)) * N2 + l;
-        __stcs(P.u0 + fy, -(qe + qo));                        // S face (ey)
-        __stcs(P.u1 + fy + (long long)nx * N2, qo - qe);      // N face (ey + 1)
-        qe = 0.0; qo = 0.0;
-#pragma unroll
-        for (int k = 0; k < NI; ++k) {   // lane (i, j) = (la, lb)
-          const double t = cf.c[2][k] * v[l + N2 * k];
-          if (k & 1) qo += t;
-          else qe += t;
-        }
-        const long long fz = g.off_f[2] + (ex + (long long)nx * (ey + (long long)ny * ez)) * N2 + l;
-        __stcs(P.u0 + fz, -(qe + qo));                             // B face (ez)
-        __stcs(P.u1 + fz + (long long)nx * ny * N2, qo - qe);      // T face (ez + 1)
-        const double* Wf = (ex > 0 && ex < nx) ? X + el * N2 : zrow;
-        const double* Ef = (ex + 1 < nx) ? X + (el + 1) * N2 : zrow;
-#pragma unroll
-        for (int r = 0; r < NE; ++r)
-          if (EL[r].on)
-            edge_sum<NI>(P, EL[r], Zr[0] + el * N2, Zr[1] + el * N2, Yr[0] + el * N2, Yr[1] + el * N2, Wf, Ef, ex, ey, ez);
+        __stcs((ehi ? P.u1 : P.u0) + dst, s);
       }
     }
     fence_proxy_async();
@@ -882,7 +881,7 @@ static int launch_v7_t(V7Params& P, cudaStream_t st, int* nl) {
   cudaGetDevice(&dev);
   static const char* sg = getenv("SC_V7_STAGES");
   static const char* sa = getenv("SC_V7_A");
-  const int two = !(sg && sg[0] == '1');
+  const int two = sg && sg[0] == '2';
   const int lines = !(sa && sa[0] == 'c');
   // per device: dynamic shared memory opt-in and resident CTAs per SM of the chosen pass-A kernel
   static int attr_done[64][2][2] = {{{0}}}, per_sm[64][2][2] = {{{0}}}, nsm_c[64] = {0};
