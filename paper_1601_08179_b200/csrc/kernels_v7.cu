@@ -49,12 +49,13 @@ struct V7Params {
   double* u1;
   const double* done;
   double* dotp;           // per-block partials of x . y (PCG p . q), or null
+  int runx;               // pass A x-run length R: x-faces with fx % R == 0 carry a second part in U1
+  int zseg;               // pass A z-segment length Z: z-faces with fz % Z == 0 carry a second part in U1
   V7Coef cf;
 };
 
 namespace v7 {
 
-constexpr int RUN = 16;   // elements per CTA of pass A (a contiguous x-run)
 
 // smallest k stride >= pj * p1 with the 8 class bases si + pj sj + pk sk on distinct bank pairs
 __host__ __device__ constexpr bool di_ok(int pj, int pk) {
@@ -100,42 +101,30 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// A work item is an x-run of RUN elements (ex0 .. ex0 + cnt - 1, ey, ez).  Its inputs are five
+// A work item is an x-run of R elements (ex0 .. ex0 + cnt - 1, ey, ez).  Its inputs are five
 // contiguous skeleton ranges: the x-faces ex0 .. ex0 + cnt (one row), the y-faces of rows ey, ey + 1 and
 // the z-faces of planes ez, ez + 1 (cnt faces each).  Each range is bulk-copied (cp.async.bulk, one
 // mbarrier transaction per item) as its 16-byte aligned superset into a slot, so the range starts at
 // slot + (start & 1).  Dirichlet rows are not copied: the lanes read a zero row instead (as they do for
 // the Dirichlet x-faces fx = 0, nx).
-template <int NI, int STAGES>
-struct V7A {
-  static constexpr int N2 = NI * NI;
-  static constexpr int SX = ((RUN + 1) * N2 + 2 + 1) & ~1;   // x-face row slot (doubles, even)
-  static constexpr int SR = (RUN * N2 + 2 + 1) & ~1;         // y / z row slot
-  static constexpr int STAGE = SX + 4 * SR;
-  static constexpr int PJ = NI + 1, PK = NI + 1;
-  static constexpr int PKK = di_pk(PJ, PK);
-  static constexpr int ND = ((PKK * PK + 2) + 1) & ~1;
-  static constexpr int SMEM = (STAGES * STAGE + SR + ND) * 8;   // the stages, the zero row, D^{-1}
-};
-
 struct __align__(16) Item {
   int ex0, cnt, ey, ez;
+  int step, zc, col, pad;   // step in the column, column length, column
   int par, dirm;    // bit r: range r starts at an odd index / is a Dirichlet row
   long long s[5];   // range starts: x row, y rows ey / ey + 1, z planes ez / ez + 1
   bool dir[5];      // Dirichlet row (not copied)
 };
 
-template <int NI, int R = RUN>
-__device__ __forceinline__ Item decode(const Geom& g, int item, int nruns) {
+// Column c = (rx, ey, zs) = rx + nruns (ey + ny zs), step s: the item (x-run rx, row ey, layer zs Z + s).
+template <int NI, int R>
+__device__ __forceinline__ Item decode(const Geom& g, int c, int step, int nruns, int Z) {
   constexpr int N2 = NI * NI;
   Item it;
-  // rows (ey, ez) in chunks of 8 layers, ez fastest inside a chunk: the rows that share a y-face are
-  // nruns items apart, those that share a z-face 8 nruns (both inside the L2-resident window)
-  const int rx = item % nruns, rest = item / nruns;
-  const int zc = rest / (g.ny * 8), rr = rest - zc * g.ny * 8;
-  const int nzc = min(8, g.nz - 8 * zc);
-  it.ey = rr / nzc;
-  it.ez = 8 * zc + (rr - it.ey * nzc);
+  const int rx = c % nruns, rest = c / nruns;
+  it.ey = rest % g.ny;
+  it.ez = (rest / g.ny) * Z + step;
+  it.step = step;
+  it.col = c;
   it.ex0 = rx * R;
   it.cnt = min(R, g.nx - it.ex0);
   const long long nx = g.nx, ny = g.ny;
@@ -177,228 +166,41 @@ __device__ __forceinline__ void issue_item(const V7Params& P, const Item& it, do
     if (by[r]) bulk_g2s(stage + (r == 0 ? 0 : SX + (r - 1) * SR), P.x + a[r], by[r], mb);
 }
 
-// Pass A: persistent CTAs of 4 warps, items blockIdx.x + n gridDim.x, the loads of item n + 2 in flight
-// while item n computes (two stages).  lane = (element of the run, parity class) as in v6.
-template <int NI, int STAGES>
-__global__ void __launch_bounds__(128, STAGES == 1 ? 4 : 3) k_v7_cond(const __grid_constant__ V7Params P, int nitems, int nruns) {
-  if (P.done != nullptr && *P.done != 0.0) return;
-  using A = V7A<NI, STAGES>;
-  constexpr int N2 = NI * NI, M = (NI + 1) / 2;
-  constexpr int PJ = A::PJ, PKK = A::PKK;
-  const Geom& g = P.g;
-  const V7Coef& cf = P.cf;
-  const int nx = g.nx, ny = g.ny;
-  extern __shared__ __align__(16) double smem[];
-  double* const zrow = smem + STAGES * A::STAGE;
-  double* const sD = zrow + A::SR;
-  __shared__ double sC[3][8], sA0[8], sAP[8];
-  __shared__ unsigned long long mbar[2];
-  const int tid = threadIdx.x;
-  for (int t = tid; t < A::SR; t += 128) zrow[t] = 0.0;
-  // D^{-1} at i + PJ j + PKK k with the 8 class bases on distinct bank pairs (cf. kernels_v6.cu di_pk)
-  for (int t = tid; t < A::ND; t += 128) {
-    const int k = t / PKK, r = t - k * PKK, j = r / PJ, i = r - j * PJ;
-    sD[t] = (i < NI && j < NI && k < NI) ? cf.dinv[i + NI * (j + NI * k)] : 0.0;
-  }
-  if (tid < 24) sC[tid / 8][tid % 8] = (tid % 8) < NI ? cf.c[tid / 8][tid % 8] : 0.0;
-  if (tid < 8) {
-    sA0[tid] = cf.a0[tid];
-    sAP[tid] = cf.ap[tid];
-  }
-  if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      const int item = blockIdx.x + s * gridDim.x;
-      if (item < nitems) issue_item<NI, A::SX, A::SR>(P, decode<NI>(g, item, nruns), smem + s * A::STAGE, &mbar[s]);
-    }
-  }
-  const int warp = tid >> 5, lane = tid & 31;
-  const int el = warp * 4 + (lane >> 3);          // element of the run
-  const int cls = lane & 7, si = cls >> 2, sj = (cls >> 1) & 1, sk = cls & 1;
-  const int CI = (NI - si + 1) >> 1, CJ = (NI - sj + 1) >> 1, CK = (NI - sk + 1) >> 1;
-  const double gi = si ? -1.0 : 1.0, gj = sj ? -1.0 : 1.0, gk = sk ? -1.0 : 1.0;
-  const double* const Dc = sD + si + PJ * sj + PKK * sk;
-  for (int n = 0;; ++n) {
-    const int item = blockIdx.x + n * gridDim.x;
-    if (item >= nitems) break;
-    const int b = STAGES == 1 ? 0 : (n & 1);
-    const Item it = decode<NI>(g, item, nruns);
-    double* const stage = smem + b * A::STAGE;
-    mbar_wait(&mbar[b], (unsigned)((STAGES == 1 ? n : (n >> 1)) & 1));
-    const bool act = el < it.cnt;
-    const int ex = it.ex0 + el, ey = it.ey, ez = it.ez;
-    // face rows of the element (entries (a, b) at a + NI b); Dirichlet faces / rows read the zero row
-    const double* const X = stage + (it.s[0] & 1);
-    const double* Wf = (ex > 0 && ex < nx) ? X + el * N2 : zrow;
-    const double* Ef = (ex + 1 < nx) ? X + (el + 1) * N2 : zrow;
-    const double* Yf[2];
-    const double* Zf[2];
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      Yf[s] = it.dir[1 + s] ? zrow : stage + A::SX + s * A::SR + (it.s[1 + s] & 1) + el * N2;
-      Zf[s] = it.dir[3 + s] ? zrow : stage + A::SX + (2 + s) * A::SR + (it.s[3 + s] & 1) + el * N2;
-    }
-    {
-      const double* W = Wf + sj + NI * sk;      // x-face entries (j, k)
-      const double* E = Ef + sj + NI * sk;
-      const double* S = Yf[0] + si + NI * sk;   // y-face entries (i, k)
-      const double* Nn = Yf[1] + si + NI * sk;
-      const double* B = Zf[0] + si + NI * sj;   // z-face entries (i, j)
-      const double* T = Zf[1] + si + NI * sj;
-      double c1[M];
-#pragma unroll
-      for (int ii = 0; ii < M; ++ii) c1[ii] = sC[0][si + 2 * ii];
-      double zin[M][M], qz[M][M];
-#pragma unroll
-      for (int ii = 0; ii < M; ++ii)
-#pragma unroll
-        for (int jj = 0; jj < M; ++jj) {
-          zin[ii][jj] = (ii < CI && jj < CJ) ? fma(gk, T[2 * ii + 2 * NI * jj], B[2 * ii + 2 * NI * jj]) : 0.0;
-          qz[ii][jj] = 0.0;
-        }
-      // output rows (entries of the element's faces in U0 / U1)
-      double* const uxw = P.u0 + g.off_f[0] + (ex + (long long)(nx + 1) * (ey + (long long)ny * ez)) * N2;   // face ex
-      double* const uxe = P.u1 + g.off_f[0] + (ex + 1 + (long long)(nx + 1) * (ey + (long long)ny * ez)) * N2;
-      double* const uys = P.u0 + g.off_f[1] + (ex + (long long)nx * (ey + (long long)(ny + 1) * ez)) * N2;
-      double* const uyn = P.u1 + g.off_f[1] + (ex + (long long)nx * (ey + 1 + (long long)(ny + 1) * ez)) * N2;
-      double* const uzb = P.u0 + g.off_f[2] + (ex + (long long)nx * (ey + (long long)ny * ez)) * N2;
-      double* const uzt = P.u1 + g.off_f[2] + (ex + (long long)nx * (ey + (long long)ny * (ez + 1))) * N2;
-#pragma unroll
-      for (int kk = 0; kk < M; ++kk) {
-        const double c3 = sC[2][sk + 2 * kk];
-        double yin[M], qy[M];
-#pragma unroll
-        for (int ii = 0; ii < M; ++ii) {
-          yin[ii] = (ii < CI && kk < CK) ? fma(gj, Nn[2 * ii + 2 * NI * kk], S[2 * ii + 2 * NI * kk]) : 0.0;
-          qy[ii] = 0.0;
-        }
-        double qx[M];
-#pragma unroll
-        for (int jj = 0; jj < M; ++jj) {
-          const double c2 = sC[1][sj + 2 * jj];
-          const int ox = 2 * jj + 2 * NI * kk;
-          const double xin = (jj < CJ && kk < CK) ? fma(gi, E[ox], W[ox]) : 0.0;
-          qx[jj] = 0.0;
-#pragma unroll
-          for (int ii = 0; ii < M; ++ii) {
-            const double u = fma(c1[ii], xin, fma(c2, yin[ii], c3 * zin[ii][jj]));
-            const double v = u * Dc[2 * ii + 2 * PJ * jj + 2 * PKK * kk];
-            qx[jj] = fma(c1[ii], v, qx[jj]);
-            qy[ii] = fma(c2, v, qy[ii]);
-            qz[ii][jj] = fma(c3, v, qz[ii][jj]);
-          }
-        }
-        // x pair (s_i = 0 / 1: lane ^ 4): W part -(Q0 + Q1) (s_i = 0 lane), E part -(Q0 - Q1) (s_i = 1 lane)
-        double qpx[M];
-#pragma unroll
-        for (int jj = 0; jj < M; ++jj) qpx[jj] = __shfl_xor_sync(0xffffffffu, qx[jj], 4);
-#pragma unroll
-        for (int jj = 0; jj < M; ++jj)
-          if (act && jj < CJ && kk < CK) {
-            if (si == 0) __stcs(uxw + sj + 2 * jj + NI * (sk + 2 * kk), -(qx[jj] + qpx[jj]));
-            else __stcs(uxe + sj + 2 * jj + NI * (sk + 2 * kk), qx[jj] - qpx[jj]);
-          }
-        double qpy[M];   // y pair (lane ^ 2): S -(Q0 + Q1), N -(Q0 - Q1)
-#pragma unroll
-        for (int ii = 0; ii < M; ++ii) qpy[ii] = __shfl_xor_sync(0xffffffffu, qy[ii], 2);
-#pragma unroll
-        for (int ii = 0; ii < M; ++ii)
-          if (act && ii < CI && kk < CK) {
-            if (sj == 0) __stcs(uys + si + 2 * ii + NI * (sk + 2 * kk), -(qy[ii] + qpy[ii]));
-            else __stcs(uyn + si + 2 * ii + NI * (sk + 2 * kk), qy[ii] - qpy[ii]);
-          }
-      }
-#pragma unroll
-      for (int ii = 0; ii < M; ++ii)   // z pair (lane ^ 1): B -(Q0 + Q1), T -(Q0 - Q1)
-#pragma unroll
-        for (int jj = 0; jj < M; ++jj) {
-          const double qp = __shfl_xor_sync(0xffffffffu, qz[ii][jj], 1);
-          if (act && ii < CI && jj < CJ) {
-            if (sk == 0) __stcs(uzb + si + 2 * ii + NI * (sj + 2 * jj), -(qz[ii][jj] + qp));
-            else __stcs(uzt + si + 2 * ii + NI * (sj + 2 * jj), qz[ii][jj] - qp);
-          }
-        }
-    }
-    // Edge line sums of the primary part (the K~ rows of an edge couple it to the face
-    // interiors along lines).  An interior edge's four face lines belong to two of its elements: the
-    // element on its high side in both transverse directions gives the a0-weighted lines of its low
-    // faces (stored in U0 at the edge), the element on its low side gives the ap-weighted lines of its
-    // high faces (stored in U1 at the edge).  lane cls = entry m of the edge (cls < NI).
-    if (act && cls < NI) {
-      const int m = cls;
-      const long long nx1 = nx + 1, ny1 = ny + 1;
-      double s0, s1;
-      // x-edges: el01 sum_j w_j F_z(m, j) + el02 sum_k w_k F_y(m, k)
-      s0 = 0.0; s1 = 0.0;
-#pragma unroll
-      for (int q = 0; q < NI; ++q) {
-        s0 = fma(sA0[q], cf.el[0][1] * Zf[0][m + NI * q] + cf.el[0][2] * Yf[0][m + NI * q], s0);
-        s1 = fma(sAP[q], cf.el[0][1] * Zf[1][m + NI * q] + cf.el[0][2] * Yf[1][m + NI * q], s1);
-      }
-      __stcs(P.u0 + g.off_e[0] + (ex + (long long)nx * (ey + ny1 * ez)) * NI + m, s0);
-      __stcs(P.u1 + g.off_e[0] + (ex + (long long)nx * (ey + 1 + ny1 * (ez + 1))) * NI + m, s1);
-      // y-edges: el10 sum_i w_i F_z(i, m) + el12 sum_k w_k F_x(m, k)
-      s0 = 0.0; s1 = 0.0;
-#pragma unroll
-      for (int q = 0; q < NI; ++q) {
-        s0 = fma(sA0[q], cf.el[1][0] * Zf[0][q + NI * m] + cf.el[1][2] * Wf[m + NI * q], s0);
-        s1 = fma(sAP[q], cf.el[1][0] * Zf[1][q + NI * m] + cf.el[1][2] * Ef[m + NI * q], s1);
-      }
-      __stcs(P.u0 + g.off_e[1] + (ex + nx1 * (ey + (long long)ny * ez)) * NI + m, s0);
-      __stcs(P.u1 + g.off_e[1] + (ex + 1 + nx1 * (ey + (long long)ny * (ez + 1))) * NI + m, s1);
-      // z-edges: el20 sum_i w_i F_y(i, m) + el21 sum_j w_j F_x(j, m)
-      s0 = 0.0; s1 = 0.0;
-#pragma unroll
-      for (int q = 0; q < NI; ++q) {
-        s0 = fma(sA0[q], cf.el[2][0] * Yf[0][q + NI * m] + cf.el[2][1] * Wf[q + NI * m], s0);
-        s1 = fma(sAP[q], cf.el[2][0] * Yf[1][q + NI * m] + cf.el[2][1] * Ef[q + NI * m], s1);
-      }
-      __stcs(P.u0 + g.off_e[2] + (ex + nx1 * (ey + ny1 * ez)) * NI + m, s0);
-      __stcs(P.u1 + g.off_e[2] + (ex + 1 + nx1 * (ey + 1 + ny1 * ez)) * NI + m, s1);
-    }
-    // release the stage: every lane is done reading it; then the loads of item n + 2 go into it
-    fence_proxy_async();
-    __syncthreads();
-    const int nxt = item + STAGES * gridDim.x;
-    if (tid == 0 && nxt < nitems) issue_item<NI, A::SX, A::SR>(P, decode<NI>(g, nxt, nruns), stage, &mbar[b]);
-  }
-}
-
-// ------------------------------------------------------------------------------------ pass A, line form
-// Pass A with lane = (element, x-line (j, k)) instead of (element, parity class): no padded points
-// (n_I^3 points per element instead of 8 ceil(n_I/2)^3), per-lane constants (D^{-1}(., j, k), the y / z
-// coefficients and signs) in registers for the whole kernel, and three phases per item:
+// ------------------------------------------------------------------------------------ pass A
+// Pass A: lane = (element, x-line (j, k)), three phases per item (an x-run of R elements):
 //  X: faces-in + D^{-1} along the lane's x-line (the y / z inputs of the line's points are the face
 //     values (S +- N)(i, k), (B +- T)(i, j); the sign is the parity of the lane's j / k, P:302 sigma), the
 //     x faces-out as the two parity sums Q_even / Q_odd of the line (W part -(Qe + Qo), E part -(Qe - Qo)),
 //     uhat = D^{-1} (...) stored to shared memory;
 //  Y: lane = (i, k): y faces-out = parity sums over j of c2_j uhat(i, j, k);
-//  Z: lane = (i, j): z faces-out over k; and the edge line sums (U0 / U1 at the edges) as in k_v7_cond.
-// Every output row of a group of elements is one contiguous skeleton range: coalesced stores.
-template <int NI, int STAGES>
+//  Z: lane = (i, j): z faces-out over k; then the edge line sums (U0 / U1 at the edges).
+// Per-lane constants (D^{-1}(., j, k), the y / z coefficients and signs) stay in registers.
+// Assembly on chip: the x-faces inside a run (E part of element e + W part of element e + 1, through
+// shared memory) and the z-faces inside a column (a persistent CTA marches a column of Z items up z; the
+// T part of layer ez stays in the lane's registers and is added to the B part of layer ez + 1).  Only the
+// run-boundary x-faces (fx % R == 0) and segment-boundary z-faces (fz % Z == 0) keep a second part in
+// U1; y-faces are written as U0 (S part) + U1 (N part).  Every output row is a contiguous range.
+template <int NI>
 struct V8A {
   static constexpr int N2 = NI * NI, N3 = N2 * NI;
   // elements per item (x-run) and per thread group (G N2 <= 256 threads in the line phases)
   static constexpr int R = NI >= 6 ? 8 : (NI >= 4 ? 16 : 32);
   static constexpr int G = NI >= 6 ? 4 : (NI == 5 ? 8 : (NI == 4 ? 16 : (NI == 3 ? 16 : 32)));
+  static constexpr int NG = R / G;
   static constexpr int NT = ((G * N2 + 31) / 32) * 32;       // threads per CTA
   static constexpr int EWF = ((R * 2 * NI + 31) / 32) * 32;  // edge-phase slots per family (warp-rounded)
-  static constexpr int MINB = STAGES == 2 ? 3 : (NT <= 128 ? 8 : (NT <= 160 ? 6 : 4));
+  static constexpr int MINB = NT <= 128 ? 8 : (NT <= 160 ? 6 : 4);
   static constexpr int SX = ((R + 1) * N2 + 2 + 1) & ~1;
   static constexpr int SR = (R * N2 + 2 + 1) & ~1;
   static constexpr int STAGE = SX + 4 * SR;
   static constexpr int VS = N3 + (N3 % 2 == 0 ? 1 : 0);      // uhat per element (odd stride)
-  static constexpr int SMEM = (STAGES * STAGE + SR + R * VS) * 8;
+  static constexpr int SMEM = (STAGE + SR + R * VS + R * N2) * 8;   // inputs, zero row, uhat, E parts
 };
 
-// Edge line sums of one element family (see k_v7_cond): F = 0 x-edges, 1 y-edges, 2 z-edges; hi = 0: the
+// Edge line sums of one element family (see the header): F = 0 x-edges, 1 y-edges, 2 z-edges; hi = 0: the
 // a0-weighted lines of the element's low faces (U0 at its low edge), hi = 1: the ap = sigma a0 weighted
-// lines of its high faces (U1 at its high edge).  Line q-strides are compile-time per family.
+// lines of its high faces (U1 at its high edge).  An interior edge's four face lines (the K~ rows of the
+// primary part couple it to the face interiors along lines) belong to exactly these two elements.
 template <int NI, int F>
 __device__ __forceinline__ double edge_line(const V7Coef& cf, const double* zb, const double* zt, const double* ys,
                                             const double* yn, const double* w, const double* e, int hi, int m) {
@@ -419,38 +221,38 @@ __device__ __forceinline__ double edge_line(const V7Coef& cf, const double* zb, 
   return hi ? se - so : se + so;
 }
 
-template <int NI, int STAGES>
-__global__ void __launch_bounds__(V8A<NI, STAGES>::NT, V8A<NI, STAGES>::MINB) k_v7_lines(const __grid_constant__ V7Params P, int nitems,
-                                                                  int nruns) {
+template <int NI>
+__global__ void __launch_bounds__(V8A<NI>::NT, V8A<NI>::MINB) k_v7_lines(const __grid_constant__ V7Params P, int ncols,
+                                                                        int nruns) {
   if (P.done != nullptr && *P.done != 0.0) return;
-  using A = V8A<NI, STAGES>;
-  constexpr int N2 = NI * NI, G = A::G, R = A::R;
+  using A = V8A<NI>;
+  constexpr int N2 = NI * NI, G = A::G, R = A::R, NG = A::NG;
   constexpr int EWF = A::EWF;
   const Geom& g = P.g;
   const V7Coef& cf = P.cf;
-  const int nx = g.nx, ny = g.ny;
+  const int nx = g.nx, ny = g.ny, nz = g.nz, Z = P.zseg;
   const long long nx1 = nx + 1, ny1 = ny + 1;
   extern __shared__ __align__(16) double smem[];
-  double* const zrow = smem + STAGES * A::STAGE;
+  double* const stage = smem;
+  double* const zrow = smem + A::STAGE;
   double* const sv = zrow + A::SR;
-  __shared__ unsigned long long mbar[2];
-  __shared__ Item sit[2];   // the decoded item of each stage (written by the issuing thread before its arrive)
+  double* const sE = sv + R * A::VS;   // E parts of phase X (x-faces assembled inside the run)
+  __shared__ unsigned long long mbar;
+  __shared__ Item sit;
   const int tid = threadIdx.x;
   for (int t = tid; t < A::SR; t += A::NT) zrow[t] = 0.0;
   if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
+    mbar_init(&mbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (tid == 0)
-    for (int s = 0; s < STAGES; ++s) {
-      const int item = blockIdx.x + s * gridDim.x;
-      if (item < nitems) {
-        sit[s] = decode<NI, R>(g, item, nruns);
-        issue_item<NI, A::SX, A::SR>(P, sit[s], smem + s * A::STAGE, &mbar[s]);
-      }
-    }
+  // this CTA's columns: blockIdx.x, + gridDim.x, ...; column length zc = min(Z, nz - zs Z)
+  auto col_len = [&](int c) { const int zs = (c / nruns) / ny; return min(Z, nz - zs * Z); };
+  if (tid == 0 && (int)blockIdx.x < ncols) {
+    sit = decode<NI, R>(g, blockIdx.x, 0, nruns, Z);
+    sit.zc = col_len(blockIdx.x);
+    issue_item<NI, A::SX, A::SR>(P, sit, stage, &mbar);
+  }
   // lane constants: line l = a + NI b of the element (phase X: (j, k) = (a, b); Y: (i, k); Z: (i, j))
   const bool lane_on = tid < G * N2;
   const int eg = tid / N2, l = tid - eg * N2, la = l % NI, lb = l / NI;
@@ -459,15 +261,18 @@ __global__ void __launch_bounds__(V8A<NI, STAGES>::NT, V8A<NI, STAGES>::MINB) k_
   for (int i = 0; i < NI; ++i) Dl[i] = lane_on ? cf.dinv[i + NI * l] : 0.0;
   const double c2j = cf.c[1][la], c3k = cf.c[2][lb];
   const double gj = (la & 1) ? -1.0 : 1.0, gk = (lb & 1) ? -1.0 : 1.0;
+  double wpart[NG], tcarry[NG];
+#pragma unroll
+  for (int r = 0; r < NG; ++r) tcarry[r] = 0.0;
+  const long long d01 = P.u1 - P.u0;
   for (int n = 0;; ++n) {
-    const int item = blockIdx.x + n * gridDim.x;
-    if (item >= nitems) break;
-    const int b = STAGES == 1 ? 0 : (n & 1);
-    double* const stage = smem + b * A::STAGE;
-    mbar_wait(&mbar[b], (unsigned)((STAGES == 1 ? n : (n >> 1)) & 1));
-    const int4 ih = *reinterpret_cast<const int4*>(&sit[b]);   // ex0, cnt, ey, ez
-    const int par = sit[b].par, dirm = sit[b].dirm;
+    if ((int)blockIdx.x >= ncols) break;
+    mbar_wait(&mbar, (unsigned)(n & 1));
+    const int4 ih = *reinterpret_cast<const int4*>(&sit);          // ex0, cnt, ey, ez
+    const int4 ic = *reinterpret_cast<const int4*>(&sit.step);     // step, zc, column
+    const int par = sit.par, dirm = sit.dirm;
     const int ex0 = ih.x, cnt = ih.y, ey = ih.z, ez = ih.w;
+    const int s = ic.x, zc = ic.y, c = ic.z;
     double* const X = stage + (par & 1);
     // the Dirichlet x-faces fx = 0, nx of a boundary run read as zero (block-uniform branch)
     if (ex0 == 0 || ex0 + cnt == nx) {
@@ -480,19 +285,18 @@ __global__ void __launch_bounds__(V8A<NI, STAGES>::NT, V8A<NI, STAGES>::MINB) k_
     const double* Yr[2];
     const double* Zr[2];
 #pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      Yr[s] = ((dirm >> (1 + s)) & 1) ? zrow : stage + A::SX + s * A::SR + ((par >> (1 + s)) & 1);
-      Zr[s] = ((dirm >> (3 + s)) & 1) ? zrow : stage + A::SX + (2 + s) * A::SR + ((par >> (3 + s)) & 1);
+    for (int q = 0; q < 2; ++q) {
+      Yr[q] = ((dirm >> (1 + q)) & 1) ? zrow : stage + A::SX + q * A::SR + ((par >> (1 + q)) & 1);
+      Zr[q] = ((dirm >> (3 + q)) & 1) ? zrow : stage + A::SX + (2 + q) * A::SR + ((par >> (3 + q)) & 1);
     }
-    // output bases of the item's first element (face / edge rows are contiguous along x)
-    const long long d01 = P.u1 - P.u0;
+    // output bases of the item's first element (face rows are contiguous along x)
     double* const ux = P.u0 + g.off_f[0] + (ex0 + nx1 * (ey + (long long)ny * ez)) * N2 + l;
     double* const uy = P.u0 + g.off_f[1] + (ex0 + (long long)nx * (ey + ny1 * ez)) * N2 + l;
     double* const uz = P.u0 + g.off_f[2] + (ex0 + (long long)nx * (ey + (long long)ny * ez)) * N2 + l;
     // ---- phase X
     if (lane_on) {
 #pragma unroll
-      for (int gr = 0; gr < R / G; ++gr) {
+      for (int gr = 0; gr < NG; ++gr) {
         const int el = gr * G + eg;
         const double w = X[el * N2 + l], e = X[(el + 1) * N2 + l];
         const double xs = w + e, xd = w - e;
@@ -513,19 +317,21 @@ __global__ void __launch_bounds__(V8A<NI, STAGES>::NT, V8A<NI, STAGES>::MINB) k_
           else qe = fma(c1, vv, qe);
           v[i] = vv;
         }
-        if (el < cnt) {
-          __stcs(ux + el * N2, -(qe + qo));              // face ex (the element's W face) in U0
-          __stcs(ux + d01 + (el + 1) * N2, qo - qe);     // face ex + 1 (E) in U1
-        }
+        wpart[gr] = -(qe + qo);          // the element's W face
+        sE[el * N2 + l] = qo - qe;       // its E face (added to the W part of element el + 1)
       }
     }
     __syncthreads();
-    // ---- phases Y, Z
+    // ---- x-faces, phases Y, Z
     if (lane_on) {
 #pragma unroll
-      for (int gr = 0; gr < R / G; ++gr) {
+      for (int gr = 0; gr < NG; ++gr) {
         const int el = gr * G + eg;
         if (el < cnt) {
+          // x-face ex0 + el: W part + the E part of element el - 1 (inside the run); the run's first
+          // face keeps the previous run's E part in U1, the run's last E part goes to U1
+          __stcs(ux + el * N2, el > 0 ? wpart[gr] + sE[(el - 1) * N2 + l] : wpart[gr]);
+          if (el == cnt - 1) __stcs(ux + d01 + (el + 1) * N2, sE[el * N2 + l]);
           const double* const v = sv + el * A::VS;
           double qe = 0.0, qo = 0.0;
 #pragma unroll
@@ -543,8 +349,12 @@ __global__ void __launch_bounds__(V8A<NI, STAGES>::NT, V8A<NI, STAGES>::MINB) k_
             if (k & 1) qo += t;
             else qe += t;
           }
-          __stcs(uz + el * N2, -(qe + qo));                                   // B face (ez) in U0
-          __stcs(uz + d01 + (long long)nx * ny * N2 + el * N2, qo - qe);      // T face (ez + 1) in U1
+          // z-face ez: B part + the T part of layer ez - 1 of this column (the column's first face keeps
+          // the previous segment's T part in U1); the column's last T part goes to U1 at ez + 1
+          const double bp = -(qe + qo), tp = qo - qe;
+          __stcs(uz + el * N2, s > 0 ? bp + tcarry[gr] : bp);
+          if (s == zc - 1) __stcs(uz + d01 + (long long)nx * ny * N2 + el * N2, tp);
+          tcarry[gr] = tp;
         }
       }
     }
@@ -561,27 +371,35 @@ __global__ void __launch_bounds__(V8A<NI, STAGES>::NT, V8A<NI, STAGES>::MINB) k_
         const double* yn = Yr[1] + el * N2;
         const double* w = X + el * N2;
         const double* e = X + (el + 1) * N2;
-        double s;
+        double sum;
         long long dst;
         if (ef == 0) {
-          s = edge_line<NI, 0>(cf, zb, zt, ys, yn, w, e, ehi, em);
+          sum = edge_line<NI, 0>(cf, zb, zt, ys, yn, w, e, ehi, em);
           dst = g.off_e[0] + (ex + (long long)nx * (ey + ehi + ny1 * (ez + ehi))) * NI + em;
         } else if (ef == 1) {
-          s = edge_line<NI, 1>(cf, zb, zt, ys, yn, w, e, ehi, em);
+          sum = edge_line<NI, 1>(cf, zb, zt, ys, yn, w, e, ehi, em);
           dst = g.off_e[1] + (ex + ehi + nx1 * (ey + (long long)ny * (ez + ehi))) * NI + em;
         } else {
-          s = edge_line<NI, 2>(cf, zb, zt, ys, yn, w, e, ehi, em);
+          sum = edge_line<NI, 2>(cf, zb, zt, ys, yn, w, e, ehi, em);
           dst = g.off_e[2] + (ex + ehi + nx1 * (ey + ehi + ny1 * ez)) * NI + em;
         }
-        __stcs((ehi ? P.u1 : P.u0) + dst, s);
+        __stcs((ehi ? P.u1 : P.u0) + dst, sum);
       }
     }
     fence_proxy_async();
     __syncthreads();
-    const int nxt = item + STAGES * gridDim.x;
-    if (tid == 0 && nxt < nitems) {
-      sit[b] = decode<NI, R>(g, nxt, nruns);
-      issue_item<NI, A::SX, A::SR>(P, sit[b], stage, &mbar[b]);
+    // next item: the next layer of the column, else the first layer of the CTA's next column
+    int c2 = c, s2 = s + 1;
+    if (s2 >= zc) {
+      c2 = c + gridDim.x;
+      s2 = 0;
+    }
+    if (c2 >= ncols) break;
+    if (tid == 0) {
+      const Item nit = decode<NI, R>(g, c2, s2, nruns, Z);
+      sit = nit;
+      sit.zc = s2 == 0 ? col_len(c2) : zc;
+      issue_item<NI, A::SX, A::SR>(P, sit, stage, &mbar);
     }
   }
 }
@@ -604,27 +422,184 @@ __device__ __forceinline__ double ldv(const double* __restrict__ x, long long i,
   return ok ? v : 0.0;
 }
 
-// One face entry: y = fd u + kf (u_lo + u_hi) + wA (a0_ea A0[eb] + ap_ea A1[eb]) + wB (a0_eb B0[ea] + ap_eb B1[ea])
-//                     + U0 + U1   (the primary part of Eq. eq:east_east_primary_part_transformed summed over
-// the face's two elements, + the two condensed parts from pass A)
-template <int NI>
-__device__ __forceinline__ double face_entry(const V7Params& P, const double* sfd, const double* sa0, const double* sap,
-                                             long long i, int e, int ea, int eb, long long so, bool olo, bool ohi,
-                                             long long ia0, long long ia1, bool oka0, bool oka1, long long ib0,
-                                             long long ib1, bool okb0, bool okb1, double wA, double wB, double kf,
-                                             double& u) {
+// Face rows.  Thread t < FPI N2 keeps one in-face entry e = (ea, eb) = t % N2 (its coefficients in
+// registers) and walks the row's faces f = t / N2 + FPI it, so a warp's accesses are contiguous.  One face
+// entry: y = fd u + kf (u_lo + u_hi) + wA (a0_ea A0[eb] + ap_ea A1[eb]) + wB (a0_eb B0[ea] + ap_eb B1[ea])
+//            + U0 (+ U1)
+// (the primary part of Eq. eq:east_east_primary_part_transformed summed over the face's two elements,
+// P:415-424, + the condensed parts from pass A).  CLS 0 / 1 / 2: x- / y- / z-face row of the cell row.
+template <int NI, bool DOT, int CLS>
+__device__ __forceinline__ void face_row(const V7Params& P, int cy, int cz, double& dot) {
+  constexpr int N2 = NI * NI, FPI = 256 / N2;
+  const int t = threadIdx.x;
+  if (t >= FPI * N2) return;
+  const Geom& g = P.g;
+  const V7Coef& cf = P.cf;
+  const int nx = g.nx, ny = g.ny, nz = g.nz;
+  const long long nx1 = nx + 1, ny1 = ny + 1;
+  const int f0 = t / N2, e = t - f0 * N2, eb = e / NI, ea = e - eb * NI;
+  const double fd = cf.fd[CLS][e];
+  const double a0a = cf.a0[ea], apa = cf.ap[ea], a0b = cf.a0[eb], apb = cf.ap[eb];
+  const bool zb0 = !zdir(g, cz), zb1 = !zdir(g, cz + 1);
+  int nf;
+  long long base, so, A0, A1, B0, B1, astep, bstep;
+  bool rowfree, olo_r = true, ohi_r = true, oka0 = true, oka1 = true, okb0, okb1, u1r = true;
+  double wA, wB, kf;
+  if (CLS == 0) {          // x-faces (fx, cy, cz): A = z-edges (fx, cy / cy + 1, cz), B = y-edges (fx, cy, cz / cz + 1)
+    nf = nx + 1;
+    base = g.off_f[0] + nx1 * (cy + (long long)ny * cz) * N2;
+    so = N2;
+    rowfree = true;
+    A0 = g.off_e[2] + nx1 * (cy + ny1 * cz) * NI; A1 = A0 + nx1 * NI; astep = NI;
+    oka0 = in_f(cy, ny); oka1 = in_f(cy + 1, ny);
+    B0 = g.off_e[1] + nx1 * (cy + (long long)ny * cz) * NI; B1 = B0 + nx1 * ny * NI; bstep = NI;
+    okb0 = zb0; okb1 = zb1;
+    wA = cf.ef[0][1]; wB = cf.ef[0][2]; kf = cf.kf[0];
+  } else if (CLS == 1) {   // y-faces (ex, cy, cz): A = z-edges (ex / ex + 1, cy, cz), B = x-edges (ex, cy, cz / cz + 1)
+    nf = nx;
+    base = g.off_f[1] + (long long)nx * (cy + ny1 * cz) * N2;
+    so = (long long)nx * N2;
+    rowfree = in_f(cy, ny);
+    olo_r = cy - 1 > 0; ohi_r = cy + 1 < ny;
+    A0 = g.off_e[2] + nx1 * (cy + ny1 * cz) * NI; A1 = A0 + NI; astep = NI;
+    B0 = g.off_e[0] + (long long)nx * (cy + ny1 * cz) * NI; B1 = B0 + (long long)nx * ny1 * NI; bstep = NI;
+    okb0 = zb0; okb1 = zb1;
+    wA = cf.ef[1][0]; wB = cf.ef[1][2]; kf = cf.kf[1];
+  } else {                 // z-faces (ex, cy, cz): A = y-edges (ex / ex + 1, cy, cz), B = x-edges (ex, cy / cy + 1, cz)
+    nf = nx;
+    base = g.off_f[2] + (long long)nx * (cy + (long long)ny * cz) * N2;
+    so = (long long)nx * ny * N2;
+    rowfree = zb0;
+    olo_r = cz - 1 >= 0 && !zdir(g, cz - 1); ohi_r = cz + 1 <= nz && !zdir(g, cz + 1);
+    A0 = g.off_e[1] + nx1 * (cy + (long long)ny * cz) * NI; A1 = A0 + NI; astep = NI;
+    B0 = g.off_e[0] + (long long)nx * (cy + ny1 * cz) * NI; B1 = B0 + (long long)nx * NI; bstep = NI;
+    okb0 = in_f(cy, ny); okb1 = in_f(cy + 1, ny);
+    u1r = cz % P.zseg == 0;
+    wA = cf.ef[2][0]; wB = cf.ef[2][1]; kf = cf.kf[2];
+  }
   const double* __restrict__ x = P.x;
-  u = __ldg(x + i);
-  const double uo = ldv(x, i - so, olo) + ldv(x, i + so, ohi);
-  const double ea_ = sa0[ea] * ldv(x, ia0 + eb, oka0) + sap[ea] * ldv(x, ia1 + eb, oka1);
-  const double eb_ = sa0[eb] * ldv(x, ib0 + ea, okb0) + sap[eb] * ldv(x, ib1 + ea, okb1);
-  return sfd[e] * u + kf * uo + wA * ea_ + wB * eb_ + __ldcs(P.u0 + i) + __ldcs(P.u1 + i);
+  const double* xp = x + base + e;
+  const double* u0p = P.u0 + base + e;
+  const double* u1p = P.u1 + base + e;
+  double* yp = P.y + base + e;
+  const double* pa0 = x + A0 + eb;
+  const double* pa1 = x + A1 + eb;
+  const double* pb0 = x + B0 + ea;
+  const double* pb1 = x + B1 + ea;
+#pragma unroll 2
+  for (int f = f0; f < nf; f += FPI) {
+    const long long o = (long long)f * N2;
+    bool fr = rowfree, olo = olo_r, ohi = ohi_r, ka0 = oka0, ka1 = oka1, u1 = u1r;
+    if (CLS == 0) {
+      fr = in_f(f, nx);
+      olo = f - 1 > 0;
+      ohi = f + 1 < nx;
+      u1 = f % P.runx == 0;
+    } else {
+      ka0 = in_f(f, nx);
+      ka1 = in_f(f + 1, nx);
+    }
+    double yv = 0.0;
+    if (fr) {
+      const double u = __ldg(xp + o);
+      const double ulo = __ldg(xp + (olo ? o - so : o));
+      const double uhi = __ldg(xp + (ohi ? o + so : o));
+      const long long oa = (long long)f * astep, ob = (long long)f * bstep;
+      const double va0 = __ldg(pa0 + (ka0 ? oa : 0)), va1 = __ldg(pa1 + (ka1 ? oa : 0));
+      const double vb0 = __ldg(pb0 + (okb0 ? ob : 0)), vb1 = __ldg(pb1 + (okb1 ? ob : 0));
+      const double c0 = __ldcs(u0p + o);
+      const double c1 = u1 ? __ldcs(u1p + o) : 0.0;
+      const double uo = (olo ? ulo : 0.0) + (ohi ? uhi : 0.0);
+      const double ea_ = a0a * (ka0 ? va0 : 0.0) + apa * (ka1 ? va1 : 0.0);
+      const double eb_ = a0b * (okb0 ? vb0 : 0.0) + apb * (okb1 ? vb1 : 0.0);
+      yv = fd * u + kf * uo + wA * ea_ + wB * eb_ + c0 + c1;
+      if (DOT) dot = fma(u, yv, dot);
+    }
+    __stcs(yp + o, yv);
+  }
+}
+
+// Edge rows (entry m = t % NI fixed per thread, edges t / NI + EPI it).  The face-line sums come from
+// pass A in U0 + U1 at the edge's entries; the rest is the K~ arrowhead: self, the two vertices, the
+// K0p couplings to the neighbouring edges along the two transverse directions.
+template <int NI, bool DOT, int DIR>
+__device__ __forceinline__ void edge_row(const V7Params& P, int cy, int cz, double& dot) {
+  constexpr int EPI = 256 / NI;
+  const int t = threadIdx.x;
+  if (t >= EPI * NI) return;
+  const Geom& g = P.g;
+  const V7Coef& cf = P.cf;
+  const int nx = g.nx, ny = g.ny, nz = g.nz;
+  const long long nx1 = nx + 1, ny1 = ny + 1;
+  const int a0i = t / NI, m = t - a0i * NI;
+  const double self = cf.eself[DIR][m], va = cf.a0[m], vp = cf.ap[m];
+  const bool zb0 = !zdir(g, cz), zb1 = !zdir(g, cz + 1);
+  const bool zlo = cz - 1 >= 0 && !zdir(g, cz - 1), zhi = cz + 1 <= nz && !zdir(g, cz + 1);
+  const double* __restrict__ x = P.x;
+  int ne;
+  long long base, vbase, vstep2, s1, s2;
+  bool rowfree, lo1 = true, hi1 = true, lo2, hi2, vok1_r = true, vok2_r = true;
+  double ev, c1, c2;
+  if (DIR == 0) {          // x-edges (ex, cy, cz): vertices (ex / ex + 1, cy, cz); neighbours y (+- nx NI), z (+- nx ny1 NI)
+    ne = nx;
+    base = g.off_e[0] + (long long)nx * (cy + ny1 * cz) * NI;
+    rowfree = in_f(cy, ny) && zb0;
+    vbase = g.off_v + nx1 * (cy + ny1 * cz); vstep2 = 1;
+    s1 = (long long)nx * NI; lo1 = cy - 1 > 0; hi1 = cy + 1 < ny;
+    s2 = (long long)nx * ny1 * NI; lo2 = zlo; hi2 = zhi;
+    ev = cf.ev[0]; c1 = cf.el[0][1] * cf.K0p; c2 = cf.el[0][2] * cf.K0p;
+  } else if (DIR == 1) {   // y-edges (fx, cy, cz): vertices (fx, cy / cy + 1, cz); neighbours x (+- NI), z (+- nx1 ny NI)
+    ne = nx + 1;
+    base = g.off_e[1] + nx1 * (cy + (long long)ny * cz) * NI;
+    rowfree = cy < ny && zb0;
+    vbase = g.off_v + nx1 * (cy + ny1 * cz); vstep2 = nx1;
+    vok1_r = in_f(cy, ny); vok2_r = in_f(cy + 1, ny);
+    s1 = NI;
+    s2 = nx1 * ny * NI; lo2 = zlo; hi2 = zhi;
+    ev = cf.ev[1]; c1 = cf.el[1][0] * cf.K0p; c2 = cf.el[1][2] * cf.K0p;
+  } else {                 // z-edges (fx, cy, cz): vertices (fx, cy, cz / cz + 1); neighbours x (+- NI), y (+- nx1 NI)
+    ne = nx + 1;
+    base = g.off_e[2] + nx1 * (cy + ny1 * cz) * NI;
+    rowfree = in_f(cy, ny) && cz < nz;
+    vbase = g.off_v + nx1 * (cy + ny1 * cz); vstep2 = nx1 * ny1;
+    vok1_r = zb0; vok2_r = zb1;
+    s1 = NI;
+    s2 = nx1 * NI; lo2 = cy - 1 > 0; hi2 = cy + 1 < ny;
+    ev = cf.ev[2]; c1 = cf.el[2][0] * cf.K0p; c2 = cf.el[2][1] * cf.K0p;
+  }
+  const double* xp = x + base + m;
+  double* yp = P.y + base + m;
+  const double* u0p = P.u0 + base + m;
+  const double* u1p = P.u1 + base + m;
+#pragma unroll 2
+  for (int a = a0i; a < ne; a += EPI) {
+    const long long o = (long long)a * NI;
+    bool fr = rowfree, l1 = lo1, h1 = hi1, k1 = vok1_r, k2 = vok2_r;
+    long long v1, v2;
+    if (DIR == 0) {
+      k1 = in_f(a, nx); k2 = in_f(a + 1, nx);
+      v1 = vbase + a; v2 = v1 + 1;
+    } else {
+      fr = fr && in_f(a, nx);
+      l1 = a - 1 > 0; h1 = a + 1 < nx;
+      v1 = vbase + a; v2 = v1 + vstep2;
+    }
+    double yv = 0.0;
+    if (fr) {
+      const double u = __ldg(xp + o);
+      const double w1 = ldv(x, v1, k1), w2 = ldv(x, v2, k2);
+      const double n1 = ldv(xp, o - s1, l1) + ldv(xp, o + s1, h1);
+      const double n2 = ldv(xp, o - s2, lo2) + ldv(xp, o + s2, hi2);
+      yv = self * u + ev * (va * w1 + vp * w2) + c1 * n1 + c2 * n2 + __ldcs(u0p + o) + __ldcs(u1p + o);
+      if (DOT) dot = fma(u, yv, dot);
+    }
+    __stcs(yp + o, yv);
+  }
 }
 
 template <int NI, bool DOT>
 __global__ void __launch_bounds__(256, 4) k_v7_assemble(const __grid_constant__ V7Params P) {
   if (P.done != nullptr && *P.done != 0.0) return;
-  constexpr int N2 = NI * NI;
   const Geom& g = P.g;
   const V7Coef& cf = P.cf;
   const int nx = g.nx, ny = g.ny, nz = g.nz;
@@ -632,163 +607,29 @@ __global__ void __launch_bounds__(256, 4) k_v7_assemble(const __grid_constant__ 
   const double* __restrict__ x = P.x;
   double* __restrict__ y = P.y;
   const int cy = blockIdx.x % (ny + 1), cz = blockIdx.x / (ny + 1);
-  // lane-indexed coefficients from shared memory (indexed kernel-parameter loads serialise per address)
-  __shared__ double sfd[3][N2], sa0[8], sap[8], sself[3][8];
-  for (int q = threadIdx.x; q < 3 * N2; q += blockDim.x) sfd[q / N2][q % N2] = cf.fd[q / N2][q % N2];
-  if (threadIdx.x < 8) {
-    sa0[threadIdx.x] = cf.a0[threadIdx.x];
-    sap[threadIdx.x] = cf.ap[threadIdx.x];
-    for (int e = 0; e < 3; ++e) sself[e][threadIdx.x] = cf.eself[e][threadIdx.x];
-  }
-  __syncthreads();
   double dot = 0.0;
-  const bool zb0 = !zdir(g, cz), zb1 = !zdir(g, cz + 1);   // planes cz, cz + 1 free (as z-planes)
-  // ---------------- x-faces (fx, ey = cy, ez = cz), fx = 0..nx; in-plane (ea, eb) = (j, k)
-  if (cy < ny && cz < nz) {
-    const long long base = g.off_f[0] + nx1 * (cy + (long long)ny * cz) * N2;
-    const long long za = g.off_e[2] + nx1 * (cy + ny1 * cz) * NI;   // z-edges (fx, cy, cz); (fx, cy + 1, cz) at + nx1 NI
-    const long long yb = g.off_e[1] + nx1 * (cy + (long long)ny * cz) * NI;   // y-edges (fx, cy, cz); cz + 1 at + nx1 ny NI
-    const bool oka0 = in_f(cy, ny), oka1 = in_f(cy + 1, ny);
-    const double wA = cf.ef[0][1], wB = cf.ef[0][2], kf = cf.kf[0];
-    for (int t = threadIdx.x; t < (nx + 1) * N2; t += blockDim.x) {
-      const int fx = t / N2, e = t - fx * N2, eb = e / NI, ea = e - eb * NI;
-      double yv = 0.0;
-      if (in_f(fx, nx)) {
-        double u;
-        const long long ia0 = za + (long long)fx * NI, ib0 = yb + (long long)fx * NI;
-        yv = face_entry<NI>(P, sfd[0], sa0, sap, base + t, e, ea, eb, N2, fx - 1 > 0, fx + 1 < nx, ia0, ia0 + nx1 * NI,
-                            oka0, oka1, ib0, ib0 + nx1 * ny * NI, zb0, zb1, wA, wB, kf, u);
-        if (DOT) dot = fma(u, yv, dot);
-      }
-      __stcs(y + base + t, yv);
-    }
-  }
-  // ---------------- y-faces (ex, fy = cy, ez = cz), ex = 0..nx-1; in-plane (ea, eb) = (i, k)
-  if (cz < nz) {
-    const long long base = g.off_f[1] + (long long)nx * (cy + ny1 * cz) * N2;
-    const long long za = g.off_e[2] + nx1 * (cy + ny1 * cz) * NI;   // z-edges (ex, cy, cz), (ex + 1, ...) at + NI
-    const long long xb = g.off_e[0] + (long long)nx * (cy + ny1 * cz) * NI;   // x-edges (ex, cy, cz); cz + 1 at + nx ny1 NI
-    const bool fr = in_f(cy, ny);
-    const double wA = cf.ef[1][0], wB = cf.ef[1][2], kf = cf.kf[1];
-    for (int t = threadIdx.x; t < nx * N2; t += blockDim.x) {
-      const int ex = t / N2, e = t - ex * N2, eb = e / NI, ea = e - eb * NI;
-      double yv = 0.0;
-      if (fr) {
-        double u;
-        const long long ia0 = za + (long long)ex * NI, ib0 = xb + (long long)ex * NI;
-        yv = face_entry<NI>(P, sfd[1], sa0, sap, base + t, e, ea, eb, (long long)nx * N2, cy - 1 > 0, cy + 1 < ny, ia0,
-                            ia0 + NI, in_f(ex, nx), in_f(ex + 1, nx), ib0, ib0 + (long long)nx * ny1 * NI, zb0, zb1, wA,
-                            wB, kf, u);
-        if (DOT) dot = fma(u, yv, dot);
-      }
-      __stcs(y + base + t, yv);
-    }
-  }
-  // ---------------- z-faces (ex, ey = cy, fz = cz), ex = 0..nx-1; in-plane (ea, eb) = (i, j)
-  if (cy < ny) {
-    const long long base = g.off_f[2] + (long long)nx * (cy + (long long)ny * cz) * N2;
-    const long long ya = g.off_e[1] + nx1 * (cy + (long long)ny * cz) * NI;   // y-edges (ex, cy, cz), (ex + 1, ...) at + NI
-    const long long xb = g.off_e[0] + (long long)nx * (cy + ny1 * cz) * NI;   // x-edges (ex, cy, cz); cy + 1 at + nx NI
-    const bool fr = zb0;
-    const bool olo = cz - 1 >= 0 && !zdir(g, cz - 1), ohi = cz + 1 <= nz && !zdir(g, cz + 1);
-    const bool okb0 = in_f(cy, ny), okb1 = in_f(cy + 1, ny);
-    const double wA = cf.ef[2][0], wB = cf.ef[2][1], kf = cf.kf[2];
-    for (int t = threadIdx.x; t < nx * N2; t += blockDim.x) {
-      const int ex = t / N2, e = t - ex * N2, eb = e / NI, ea = e - eb * NI;
-      double yv = 0.0;
-      if (fr) {
-        double u;
-        const long long ia0 = ya + (long long)ex * NI, ib0 = xb + (long long)ex * NI;
-        yv = face_entry<NI>(P, sfd[2], sa0, sap, base + t, e, ea, eb, (long long)nx * ny * N2, olo, ohi, ia0, ia0 + NI,
-                            in_f(ex, nx), in_f(ex + 1, nx), ib0, ib0 + (long long)nx * NI, okb0, okb1, wA, wB, kf, u);
-        if (DOT) dot = fma(u, yv, dot);
-      }
-      __stcs(y + base + t, yv);
-    }
-  }
-  // ---------------- edges: the face-line sums (z-faces (ex, cy-1 / cy, cz) over j and y-faces (ex, cy, cz-1 / cz)
-  // over k for an x-edge, cyclically for y / z) come from pass A in U0 + U1 at the edge's entries.
-  // x-edges (ex, fy = cy, fz = cz), entry m
-  {
-    const long long base = g.off_e[0] + (long long)nx * (cy + ny1 * cz) * NI;
-    const bool fr = in_f(cy, ny) && zb0;
-    const bool ylo = cz - 1 >= 0 && !zdir(g, cz - 1), yhi = cz + 1 <= nz && !zdir(g, cz + 1);
-    for (int t = threadIdx.x; t < nx * NI; t += blockDim.x) {
-      const int ex = t / NI, m = t - ex * NI;
-      const long long i0 = base + t;
-      double yv = 0.0;
-      if (fr) {
-        const double u = __ldg(x + i0);
-        const double vw = ldv(x, g.off_v + ex + nx1 * (cy + ny1 * cz), in_f(ex, nx));
-        const double ve = ldv(x, g.off_v + ex + 1 + nx1 * (cy + ny1 * cz), in_f(ex + 1, nx));
-        const double nb_y = ldv(x, i0 - (long long)nx * NI, cy - 1 > 0) + ldv(x, i0 + (long long)nx * NI, cy + 1 < ny);
-        const long long pl = (long long)nx * ny1 * NI;
-        const double nb_z = ldv(x, i0 - pl, ylo) + ldv(x, i0 + pl, yhi);
-        yv = sself[0][m] * u + cf.ev[0] * (sa0[m] * vw + sap[m] * ve) + cf.el[0][1] * cf.K0p * nb_y +
-             cf.el[0][2] * cf.K0p * nb_z + __ldcs(P.u0 + i0) + __ldcs(P.u1 + i0);
-        if (DOT) dot = fma(u, yv, dot);
-      }
-      __stcs(y + i0, yv);
-    }
-  }
-  // ---------------- y-edges (fx, ey = cy, fz = cz)
-  if (cy < ny) {
-    const long long base = g.off_e[1] + nx1 * (cy + (long long)ny * cz) * NI;
-    const bool ylo = cz - 1 >= 0 && !zdir(g, cz - 1), yhi = cz + 1 <= nz && !zdir(g, cz + 1);
-    for (int t = threadIdx.x; t < (nx + 1) * NI; t += blockDim.x) {
-      const int fx = t / NI, m = t - fx * NI;
-      const long long i0 = base + t;
-      double yv = 0.0;
-      if (in_f(fx, nx) && zb0) {
-        const double u = __ldg(x + i0);
-        const double vs = ldv(x, g.off_v + fx + nx1 * (cy + ny1 * cz), in_f(cy, ny));
-        const double vn = ldv(x, g.off_v + fx + nx1 * (cy + 1 + ny1 * cz), in_f(cy + 1, ny));
-        const double nb_x = ldv(x, i0 - NI, fx - 1 > 0) + ldv(x, i0 + NI, fx + 1 < nx);
-        const long long pl = nx1 * ny * NI;
-        const double nb_z = ldv(x, i0 - pl, ylo) + ldv(x, i0 + pl, yhi);
-        yv = sself[1][m] * u + cf.ev[1] * (sa0[m] * vs + sap[m] * vn) + cf.el[1][0] * cf.K0p * nb_x +
-             cf.el[1][2] * cf.K0p * nb_z + __ldcs(P.u0 + i0) + __ldcs(P.u1 + i0);
-        if (DOT) dot = fma(u, yv, dot);
-      }
-      __stcs(y + i0, yv);
-    }
-  }
-  // ---------------- z-edges (fx, fy = cy, ez = cz)
-  if (cz < nz) {
-    const long long base = g.off_e[2] + nx1 * (cy + ny1 * cz) * NI;
-    const bool fry = in_f(cy, ny);
-    for (int t = threadIdx.x; t < (nx + 1) * NI; t += blockDim.x) {
-      const int fx = t / NI, m = t - fx * NI;
-      const long long i0 = base + t;
-      double yv = 0.0;
-      if (in_f(fx, nx) && fry) {
-        const double u = __ldg(x + i0);
-        const double vb = ldv(x, g.off_v + fx + nx1 * (cy + ny1 * cz), zb0);
-        const double vt = ldv(x, g.off_v + fx + nx1 * (cy + ny1 * (cz + 1)), zb1);
-        const double nb_x = ldv(x, i0 - NI, fx - 1 > 0) + ldv(x, i0 + NI, fx + 1 < nx);
-        const double nb_y = ldv(x, i0 - nx1 * NI, cy - 1 > 0) + ldv(x, i0 + nx1 * NI, cy + 1 < ny);
-        yv = sself[2][m] * u + cf.ev[2] * (sa0[m] * vb + sap[m] * vt) + cf.el[2][0] * cf.K0p * nb_x +
-             cf.el[2][1] * cf.K0p * nb_y + __ldcs(P.u0 + i0) + __ldcs(P.u1 + i0);
-        if (DOT) dot = fma(u, yv, dot);
-      }
-      __stcs(y + i0, yv);
-    }
-  }
+  if (cy < ny && cz < nz) face_row<NI, DOT, 0>(P, cy, cz, dot);
+  if (cz < nz) face_row<NI, DOT, 1>(P, cy, cz, dot);
+  if (cy < ny) face_row<NI, DOT, 2>(P, cy, cz, dot);
+  edge_row<NI, DOT, 0>(P, cy, cz, dot);
+  if (cy < ny) edge_row<NI, DOT, 1>(P, cy, cz, dot);
+  if (cz < nz) edge_row<NI, DOT, 2>(P, cy, cz, dot);
   // ---------------- vertices (fx, cy, cz): lines along the 6 incident edges
   {
-    const bool fr = in_f(cy, ny) && zb0;
+    const bool fr = in_f(cy, ny) && !zdir(g, cz);
     const bool zlo_ok = cz - 1 >= 0 && !zdir(g, cz - 1), zhi_ok = cz + 1 <= nz && !zdir(g, cz + 1);
     for (int fx = threadIdx.x; fx <= nx; fx += blockDim.x) {
       const long long i0 = g.off_v + fx + nx1 * (cy + ny1 * cz);
       double yv = 0.0;
       if (fr && in_f(fx, nx)) {
+        constexpr int NI_ = NI;
         const double u = __ldg(x + i0);
-        const long long xw = g.off_e[0] + (fx - 1 + (long long)nx * (cy + ny1 * cz)) * NI, xe = xw + NI;
-        const long long ys = g.off_e[1] + (fx + nx1 * (cy - 1 + (long long)ny * cz)) * NI, yn = ys + nx1 * NI;
-        const long long zb = g.off_e[2] + (fx + nx1 * (cy + ny1 * (cz - 1))) * NI, zt = zb + nx1 * ny1 * NI;
+        const long long xw = g.off_e[0] + (fx - 1 + (long long)nx * (cy + ny1 * cz)) * NI_, xe = xw + NI_;
+        const long long ys = g.off_e[1] + (fx + nx1 * (cy - 1 + (long long)ny * cz)) * NI_, yn = ys + nx1 * NI_;
+        const long long zb = g.off_e[2] + (fx + nx1 * (cy + ny1 * (cz - 1))) * NI_, zt = zb + nx1 * ny1 * NI_;
         double lx = 0.0, ly = 0.0, lz = 0.0;
 #pragma unroll
-        for (int q = 0; q < NI; ++q) {
+        for (int q = 0; q < NI_; ++q) {
           lx = fma(cf.ap[q], __ldg(x + xw + q), fma(cf.a0[q], __ldg(x + xe + q), lx));
           ly = fma(cf.ap[q], __ldg(x + ys + q), fma(cf.a0[q], __ldg(x + yn + q), ly));
           lz = fma(cf.ap[q], __ldg(x + zb + q), fma(cf.a0[q], __ldg(x + zt + q), lz));
@@ -877,46 +718,37 @@ long long v7_dot_parts(const Geom& g) { return (long long)(g.ny + 1) * (g.nz + 1
 template <int NI>
 static int launch_v7_t(V7Params& P, cudaStream_t st, int* nl) {
   const Geom& g = P.g;
+  using A = v7::V8A<NI>;
   int dev = 0;
   cudaGetDevice(&dev);
-  static const char* sg = getenv("SC_V7_STAGES");
-  static const char* sa = getenv("SC_V7_A");
-  const int two = sg && sg[0] == '2';
-  const int lines = !(sa && sa[0] == 'c');
-  // per device: dynamic shared memory opt-in and resident CTAs per SM of the chosen pass-A kernel
-  static int attr_done[64][2][2] = {{{0}}}, per_sm[64][2][2] = {{{0}}}, nsm_c[64] = {0};
-  const void* fn;
-  int smem, nthr, run;
-  if (lines) {
-    fn = two ? (const void*)v7::k_v7_lines<NI, 2> : (const void*)v7::k_v7_lines<NI, 1>;
-    smem = two ? v7::V8A<NI, 2>::SMEM : v7::V8A<NI, 1>::SMEM;
-    nthr = v7::V8A<NI, 1>::NT;
-    run = v7::V8A<NI, 1>::R;
-  } else {
-    fn = two ? (const void*)v7::k_v7_cond<NI, 2> : (const void*)v7::k_v7_cond<NI, 1>;
-    smem = two ? v7::V7A<NI, 2>::SMEM : v7::V7A<NI, 1>::SMEM;
-    nthr = 128;
-    run = v7::RUN;
-  }
-  if (dev < 64 && !attr_done[dev][lines][two]) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev][lines][two], fn, nthr, smem);
+  // per device: dynamic shared memory opt-in and resident CTAs per SM of pass A
+  static int attr_done[64] = {0}, per_sm[64] = {0}, nsm_c[64] = {0};
+  if (dev < 64 && !attr_done[dev]) {
+    cudaFuncSetAttribute(v7::k_v7_lines<NI>, cudaFuncAttributeMaxDynamicSharedMemorySize, A::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], v7::k_v7_lines<NI>, A::NT, A::SMEM);
     cudaDeviceGetAttribute(&nsm_c[dev], cudaDevAttrMultiProcessorCount, dev);
-    attr_done[dev][lines][two] = 1;
+    attr_done[dev] = 1;
   }
-  const int nruns = (g.nx + run - 1) / run;
-  const int nitems = nruns * g.ny * g.nz;
-  const int slots = (dev < 64 ? max(per_sm[dev][lines][two], 1) * nsm_c[dev] : 148);
-  const int grid = nitems < slots ? nitems : slots;
-  if (grid > 0) {
-    if (lines) {
-      if (two) v7::k_v7_lines<NI, 2><<<grid, nthr, smem, st>>>(P, nitems, nruns);
-      else v7::k_v7_lines<NI, 1><<<grid, nthr, smem, st>>>(P, nitems, nruns);
-    } else {
-      if (two) v7::k_v7_cond<NI, 2><<<grid, nthr, smem, st>>>(P, nitems, nruns);
-      else v7::k_v7_cond<NI, 1><<<grid, nthr, smem, st>>>(P, nitems, nruns);
-    }
+  const int slots = (dev < 64 ? max(per_sm[dev], 1) * nsm_c[dev] : 148);
+  const int nruns = (g.nx + A::R - 1) / A::R;
+  // z-segment length Z: longer columns assemble more z-faces on chip (1 / Z of them keep a U1 part),
+  // but the columns must still balance over the resident CTAs: minimise (waves) x (Z + 1)
+  int Z = 1;
+  long long best = -1;
+  const int cand[6] = {32, 24, 16, 12, 8, 4};
+  for (int q = 0; q < 6; ++q) {
+    const int z = cand[q] < g.nz ? cand[q] : g.nz;
+    const long long cols = (long long)nruns * g.ny * ((g.nz + z - 1) / z);
+    const long long cost = ((cols + slots - 1) / slots) * (long long)(z + 1);
+    if (best < 0 || cost < best) { best = cost; Z = z; }
   }
+  const char* zs = getenv("SC_V7_Z");
+  if (zs && atoi(zs) > 0) Z = atoi(zs) < g.nz ? atoi(zs) : g.nz;
+  P.runx = A::R;
+  P.zseg = Z;
+  const int ncols = nruns * g.ny * ((g.nz + Z - 1) / Z);
+  const int grid = ncols < slots ? ncols : slots;
+  if (grid > 0) v7::k_v7_lines<NI><<<grid, A::NT, A::SMEM, st>>>(P, ncols, nruns);
   (*nl)++;
   const unsigned rows = (unsigned)((g.ny + 1) * (g.nz + 1));
   if (P.dotp) v7::k_v7_assemble<NI, true><<<rows, 256, 0, st>>>(P);

@@ -180,6 +180,20 @@ def test_family_v7_operator_parity(p, ne, monkeypatch):
     assert torch.equal(y1, y2)
 
 
+@pytest.mark.parametrize("p,ne,z", [(8, (9, 7, 5), "2"), (8, (17, 3, 7), "3"), (5, (33, 4, 6), "4"),
+                                    (3, (65, 3, 5), "2"), (4, (17, 2, 9), "1"), (6, (9, 5, 4), "4")])
+def test_family_v7_z_segments(p, ne, z, monkeypatch):
+    """v7 pass A assembles the z-faces inside a column of Z layers (and the x-faces inside a run); the
+    segment-boundary z-faces and run-boundary x-faces keep their second part in U1: every Z, incl. a
+    ragged last segment, and runs split in x (R = 8 / 16 / 32 elements)."""
+    monkeypatch.setenv("SC_V7_Z", z)
+    g = small_grid(p, ne, 0.9, lengths=(1.1, 0.8, 1.3))
+    ref_op = operator.AssembledCondensedOperator(g)
+    x = lattice_random(70 + p, g.ne, g.p).ravel()
+    ctx = _ctx(g, monkeypatch, "v7")
+    assert _rel(_apply_nodal(ctx, x), ref_op.apply(x)) <= 1e-12
+
+
 @pytest.mark.parametrize("p,ne", [(5, (15, 7, 4)), (8, (10, 6, 3))])
 def test_family_v7_pcg_fused_dot(p, ne, monkeypatch):
     """BT-PCG on v7 with p . q from pass B's per-block x . y partials, against the oracle."""
