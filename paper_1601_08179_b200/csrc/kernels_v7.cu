@@ -180,21 +180,22 @@ __device__ __forceinline__ void issue_item(const V7Params& P, const Item& it, do
 // T part of layer ez stays in the lane's registers and is added to the B part of layer ez + 1).  Only the
 // run-boundary x-faces (fx % R == 0) and segment-boundary z-faces (fz % Z == 0) keep a second part in
 // U1; y-faces are written as U0 (S part) + U1 (N part).  Every output row is a contiguous range.
-template <int NI>
+template <int NI, int STAGES>
 struct V8A {
   static constexpr int N2 = NI * NI, N3 = N2 * NI;
-  // elements per item (x-run) and per thread group (G N2 <= 256 threads in the line phases)
+  // elements per item (x-run) and per thread group; one stage: G N2 <= 256 threads and NG groups per
+  // item; two stages (the next item's loads in flight while this one computes): one group per item
   static constexpr int R = NI >= 6 ? 8 : (NI >= 4 ? 16 : 32);
-  static constexpr int G = NI >= 6 ? 4 : (NI == 5 ? 8 : (NI == 4 ? 16 : (NI == 3 ? 16 : 32)));
+  static constexpr int G = STAGES == 2 ? R : (NI >= 6 ? 4 : (NI == 5 ? 8 : (NI == 4 ? 16 : (NI == 3 ? 16 : 32))));
   static constexpr int NG = R / G;
   static constexpr int NT = ((G * N2 + 31) / 32) * 32;       // threads per CTA
   static constexpr int EWF = ((R * 2 * NI + 31) / 32) * 32;  // edge-phase slots per family (warp-rounded)
-  static constexpr int MINB = NT <= 128 ? 8 : (NT <= 160 ? 6 : 4);
-  static constexpr int SX = ((R + 1) * N2 + 2 + 1) & ~1;
-  static constexpr int SR = (R * N2 + 2 + 1) & ~1;
+  static constexpr int MINB = STAGES == 2 ? (NT > 256 ? 2 : 4) : (NT <= 128 ? 8 : (NT <= 160 ? 6 : 4));
+  static constexpr int SX = ((R + 1) * N2 + 1 + 1) & ~1;     // slot >= len + 1 (the 8-byte phase), even
+  static constexpr int SR = (R * N2 + 1 + 1) & ~1;
   static constexpr int STAGE = SX + 4 * SR;
   static constexpr int VS = N3 + (N3 % 2 == 0 ? 1 : 0);      // uhat per element (odd stride)
-  static constexpr int SMEM = (STAGE + SR + R * VS + R * N2) * 8;   // inputs, zero row, uhat, E parts
+  static constexpr int SMEM = (STAGES * STAGE + R * VS + R * N2) * 8;   // inputs, uhat, E parts
 };
 
 // Edge line sums of one element family (see the header): F = 0 x-edges, 1 y-edges, 2 z-edges; hi = 0: the
@@ -221,11 +222,11 @@ __device__ __forceinline__ double edge_line(const V7Coef& cf, const double* zb, 
   return hi ? se - so : se + so;
 }
 
-template <int NI>
-__global__ void __launch_bounds__(V8A<NI>::NT, V8A<NI>::MINB) k_v7_lines(const __grid_constant__ V7Params P, int ncols,
-                                                                        int nruns) {
+template <int NI, int STAGES>
+__global__ void __launch_bounds__(V8A<NI, STAGES>::NT, V8A<NI, STAGES>::MINB) k_v7_lines(const __grid_constant__ V7Params P,
+                                                                                       int ncols, int nruns) {
   if (P.done != nullptr && *P.done != 0.0) return;
-  using A = V8A<NI>;
+  using A = V8A<NI, STAGES>;
   constexpr int N2 = NI * NI, G = A::G, R = A::R, NG = A::NG;
   constexpr int EWF = A::EWF;
   const Geom& g = P.g;
@@ -233,26 +234,32 @@ __global__ void __launch_bounds__(V8A<NI>::NT, V8A<NI>::MINB) k_v7_lines(const _
   const int nx = g.nx, ny = g.ny, nz = g.nz, Z = P.zseg;
   const long long nx1 = nx + 1, ny1 = ny + 1;
   extern __shared__ __align__(16) double smem[];
-  double* const stage = smem;
-  double* const zrow = smem + A::STAGE;
-  double* const sv = zrow + A::SR;
+  double* const sv = smem + STAGES * A::STAGE;
   double* const sE = sv + R * A::VS;   // E parts of phase X (x-faces assembled inside the run)
-  __shared__ unsigned long long mbar;
-  __shared__ Item sit;
+  __shared__ unsigned long long mbar[2];
+  __shared__ Item sit[2];
   const int tid = threadIdx.x;
-  for (int t = tid; t < A::SR; t += A::NT) zrow[t] = 0.0;
   if (tid == 0) {
-    mbar_init(&mbar, 1);
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  // this CTA's columns: blockIdx.x, + gridDim.x, ...; column length zc = min(Z, nz - zs Z)
+  // this CTA's columns: blockIdx.x, + gridDim.x, ...; column length zc = min(Z, nz - zs Z); thread 0
+  // walks the items it issues (ic, is, izc) STAGES ahead of the computation
   auto col_len = [&](int c) { const int zs = (c / nruns) / ny; return min(Z, nz - zs * Z); };
-  if (tid == 0 && (int)blockIdx.x < ncols) {
-    sit = decode<NI, R>(g, blockIdx.x, 0, nruns, Z);
-    sit.zc = col_len(blockIdx.x);
-    issue_item<NI, A::SX, A::SR>(P, sit, stage, &mbar);
-  }
+  int ic = blockIdx.x, is = 0, izc = ic < ncols ? col_len(ic) : 0;
+  if (tid == 0)
+    for (int q = 0; q < STAGES && ic < ncols; ++q) {
+      sit[q] = decode<NI, R>(g, ic, is, nruns, Z);
+      sit[q].zc = izc;
+      issue_item<NI, A::SX, A::SR>(P, sit[q], smem + q * A::STAGE, &mbar[q]);
+      if (++is >= izc) {
+        ic += gridDim.x;
+        is = 0;
+        izc = ic < ncols ? col_len(ic) : 0;
+      }
+    }
   // lane constants: line l = a + NI b of the element (phase X: (j, k) = (a, b); Y: (i, k); Z: (i, j))
   const bool lane_on = tid < G * N2;
   const int eg = tid / N2, l = tid - eg * N2, la = l % NI, lb = l / NI;
@@ -267,27 +274,33 @@ __global__ void __launch_bounds__(V8A<NI>::NT, V8A<NI>::MINB) k_v7_lines(const _
   const long long d01 = P.u1 - P.u0;
   for (int n = 0;; ++n) {
     if ((int)blockIdx.x >= ncols) break;
-    mbar_wait(&mbar, (unsigned)(n & 1));
-    const int4 ih = *reinterpret_cast<const int4*>(&sit);          // ex0, cnt, ey, ez
-    const int4 ic = *reinterpret_cast<const int4*>(&sit.step);     // step, zc, column
-    const int par = sit.par, dirm = sit.dirm;
+    const int b = STAGES == 2 ? (n & 1) : 0;
+    double* const stage = smem + b * A::STAGE;
+    mbar_wait(&mbar[b], (unsigned)((STAGES == 2 ? (n >> 1) : n) & 1));
+    const int4 ih = *reinterpret_cast<const int4*>(&sit[b]);          // ex0, cnt, ey, ez
+    const int4 icq = *reinterpret_cast<const int4*>(&sit[b].step);    // step, zc, column
+    const int par = sit[b].par, dirm = sit[b].dirm;
     const int ex0 = ih.x, cnt = ih.y, ey = ih.z, ez = ih.w;
-    const int s = ic.x, zc = ic.y, c = ic.z;
+    const int s = icq.x, zc = icq.y;
     double* const X = stage + (par & 1);
-    // the Dirichlet x-faces fx = 0, nx of a boundary run read as zero (block-uniform branch)
-    if (ex0 == 0 || ex0 + cnt == nx) {
+    // the Dirichlet x-faces fx = 0, nx of a boundary run and the Dirichlet y / z rows (not copied) read as
+    // zero (block-uniform branch)
+    if (ex0 == 0 || ex0 + cnt == nx || (dirm & 0x1e)) {
       if (tid < N2) {
         if (ex0 == 0) X[tid] = 0.0;
         if (ex0 + cnt == nx) X[cnt * N2 + tid] = 0.0;
       }
+      for (int q = 1; q < 5; ++q)
+        if ((dirm >> q) & 1)
+          for (int t = tid; t < A::SR; t += A::NT) stage[A::SX + (q - 1) * A::SR + t] = 0.0;
       __syncthreads();
     }
     const double* Yr[2];
     const double* Zr[2];
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-      Yr[q] = ((dirm >> (1 + q)) & 1) ? zrow : stage + A::SX + q * A::SR + ((par >> (1 + q)) & 1);
-      Zr[q] = ((dirm >> (3 + q)) & 1) ? zrow : stage + A::SX + (2 + q) * A::SR + ((par >> (3 + q)) & 1);
+      Yr[q] = stage + A::SX + q * A::SR + ((par >> (1 + q)) & 1);
+      Zr[q] = stage + A::SX + (2 + q) * A::SR + ((par >> (3 + q)) & 1);
     }
     // output bases of the item's first element (face rows are contiguous along x)
     double* const ux = P.u0 + g.off_f[0] + (ex0 + nx1 * (ey + (long long)ny * ez)) * N2 + l;
@@ -388,19 +401,19 @@ __global__ void __launch_bounds__(V8A<NI>::NT, V8A<NI>::MINB) k_v7_lines(const _
     }
     fence_proxy_async();
     __syncthreads();
-    // next item: the next layer of the column, else the first layer of the CTA's next column
-    int c2 = c, s2 = s + 1;
-    if (s2 >= zc) {
-      c2 = c + gridDim.x;
-      s2 = 0;
+    // the item STAGES ahead goes into the stage just released
+    const bool more = (s + 1 < zc || (int)(icq.z + gridDim.x) < ncols);
+    if (tid == 0 && ic < ncols) {
+      sit[b] = decode<NI, R>(g, ic, is, nruns, Z);
+      sit[b].zc = izc;
+      issue_item<NI, A::SX, A::SR>(P, sit[b], stage, &mbar[b]);
+      if (++is >= izc) {
+        ic += gridDim.x;
+        is = 0;
+        izc = ic < ncols ? col_len(ic) : 0;
+      }
     }
-    if (c2 >= ncols) break;
-    if (tid == 0) {
-      const Item nit = decode<NI, R>(g, c2, s2, nruns, Z);
-      sit = nit;
-      sit.zc = s2 == 0 ? col_len(c2) : zc;
-      issue_item<NI, A::SX, A::SR>(P, sit, stage, &mbar);
-    }
+    if (!more) break;
   }
 }
 
@@ -718,19 +731,24 @@ long long v7_dot_parts(const Geom& g) { return (long long)(g.ny + 1) * (g.nz + 1
 template <int NI>
 static int launch_v7_t(V7Params& P, cudaStream_t st, int* nl) {
   const Geom& g = P.g;
-  using A = v7::V8A<NI>;
+  static const char* sg = getenv("SC_V7_STAGES");
+  const int two = sg && sg[0] == '2';
   int dev = 0;
   cudaGetDevice(&dev);
   // per device: dynamic shared memory opt-in and resident CTAs per SM of pass A
-  static int attr_done[64] = {0}, per_sm[64] = {0}, nsm_c[64] = {0};
-  if (dev < 64 && !attr_done[dev]) {
-    cudaFuncSetAttribute(v7::k_v7_lines<NI>, cudaFuncAttributeMaxDynamicSharedMemorySize, A::SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev], v7::k_v7_lines<NI>, A::NT, A::SMEM);
+  static int attr_done[64][2] = {{0}}, per_sm[64][2] = {{0}}, nsm_c[64] = {0};
+  const void* fn = two ? (const void*)v7::k_v7_lines<NI, 2> : (const void*)v7::k_v7_lines<NI, 1>;
+  const int smem = two ? v7::V8A<NI, 2>::SMEM : v7::V8A<NI, 1>::SMEM;
+  const int nthr = two ? v7::V8A<NI, 2>::NT : v7::V8A<NI, 1>::NT;
+  const int R = v7::V8A<NI, 1>::R;
+  if (dev < 64 && !attr_done[dev][two]) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[dev][two], fn, nthr, smem);
     cudaDeviceGetAttribute(&nsm_c[dev], cudaDevAttrMultiProcessorCount, dev);
-    attr_done[dev] = 1;
+    attr_done[dev][two] = 1;
   }
-  const int slots = (dev < 64 ? max(per_sm[dev], 1) * nsm_c[dev] : 148);
-  const int nruns = (g.nx + A::R - 1) / A::R;
+  const int slots = (dev < 64 ? max(per_sm[dev][two], 1) * nsm_c[dev] : 148);
+  const int nruns = (g.nx + R - 1) / R;
   // z-segment length Z: longer columns assemble more z-faces on chip (1 / Z of them keep a U1 part),
   // but the columns must still balance over the resident CTAs: minimise (waves) x (Z + 1)
   int Z = 1;
@@ -744,11 +762,14 @@ static int launch_v7_t(V7Params& P, cudaStream_t st, int* nl) {
   }
   const char* zs = getenv("SC_V7_Z");
   if (zs && atoi(zs) > 0) Z = atoi(zs) < g.nz ? atoi(zs) : g.nz;
-  P.runx = A::R;
+  P.runx = R;
   P.zseg = Z;
   const int ncols = nruns * g.ny * ((g.nz + Z - 1) / Z);
   const int grid = ncols < slots ? ncols : slots;
-  if (grid > 0) v7::k_v7_lines<NI><<<grid, A::NT, A::SMEM, st>>>(P, ncols, nruns);
+  if (grid > 0) {
+    if (two) v7::k_v7_lines<NI, 2><<<grid, nthr, smem, st>>>(P, ncols, nruns);
+    else v7::k_v7_lines<NI, 1><<<grid, nthr, smem, st>>>(P, ncols, nruns);
+  }
   (*nl)++;
   const unsigned rows = (unsigned)((g.ny + 1) * (g.nz + 1));
   if (P.dotp) v7::k_v7_assemble<NI, true><<<rows, 256, 0, st>>>(P);

@@ -6,5 +6,5 @@ for S in 1 2; do
 SC_V7_STAGES=$S python tools/op_time.py --ops v7 --cases ${CASES:-cfg5,cfg3:8} --reps 10 > gpurun_out/${TAG}_optime_s$S.log 2>&1
 echo "stages $S"; grep '^{' gpurun_out/${TAG}_optime_s$S.log | cut -c1-110
 SC_V7_STAGES=$S SC_OP=v7 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum,smsp__issue_active.avg.pct_of_peak_sustained_active --clock-control none --csv python tools/op_time.py --ops v7 --cases cfg5 --reps 1 > gpurun_out/${TAG}_ncu_s$S.csv 2>&1
-grep -E "k_v7_(lines|cond)" gpurun_out/${TAG}_ncu_s$S.csv | tail -10 | awk -F'","' '{print $5, $13, $15}' | cut -c1-150
+grep -E "k_v7_(lines|assemble)" gpurun_out/${TAG}_ncu_s$S.csv | tail -10 | awk -F'","' '{print $5, $13, $15}' | cut -c1-150
 done
