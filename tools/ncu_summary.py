@@ -53,16 +53,19 @@ def launches(path):
 
 
 def full(path):
+    """Every kernel of the capture (one operator application: v7 = pass A + pass B): name and metrics."""
     txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
-    h, u, v = rows[0], rows[1], rows[2]
-    res = {}
-    for k, name in KEYS:
-        if k in h:
-            i = h.index(k)
-            res[k] = (name, v[i], u[i])
-    kname = v[h.index("Kernel Name")] if "Kernel Name" in h else "?"
-    return kname, res
+    h, u = rows[0], rows[1]
+    out = []
+    for v in rows[2:]:
+        res = {}
+        for k, name in KEYS:
+            if k in h:
+                i = h.index(k)
+                res[k] = (name, v[i], u[i])
+        out.append((v[h.index("Kernel Name")] if "Kernel Name" in h else "?", res))
+    return out
 
 
 def main():
@@ -93,32 +96,38 @@ def main():
             lines.append(f"| `{k}` | {n} | {t:.3f} | {t / n:.4f} | {t / tot * 100:.1f}% |")
         lines.append("")
     if a.full:
-        kname, res = full(a.full)
-        lines += [f"## `--set full` capture of `{kname[:90]}`", "", f"source: `{os.path.basename(a.full)}`", "",
-                  "| metric | value | unit |", "|---|---|---|"]
-        for k, (name, v, u) in res.items():
-            lines.append(f"| {name} (`{k}`) | {v} | {u} |")
-        lines.append("")
-        try:
-            rd = float(res["dram__bytes_read.sum"][1].replace(",", ""))
-            wr = float(res["dram__bytes_write.sum"][1].replace(",", ""))
-            unit = res["dram__bytes_read.sum"][2]
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
-            traffic = (rd + wr) * scale
-            dur = float(res["gpu__time_duration.sum"][1].replace(",", ""))
-            dunit = res["gpu__time_duration.sum"][2]
-            dsec = dur * {"ns": 1e-9, "nsecond": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3}.get(dunit, 1e-9)
-            lines += [f"DRAM traffic per launch: {traffic / 1e9:.3f} GB"]
+        traffic = 0.0
+        dsec_tot = 0.0
+        for kname, res in full(a.full):
+            lines += [f"## `--set full` capture of `{kname[:90]}`", "", f"source: `{os.path.basename(a.full)}`", "",
+                      "| metric | value | unit |", "|---|---|---|"]
+            for k, (name, v, u) in res.items():
+                lines.append(f"| {name} (`{k}`) | {v} | {u} |")
+            lines.append("")
+            try:
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+                rd = float(res["dram__bytes_read.sum"][1].replace(",", "")) * scale.get(res["dram__bytes_read.sum"][2], 1)
+                wr = float(res["dram__bytes_write.sum"][1].replace(",", "")) * scale.get(res["dram__bytes_write.sum"][2], 1)
+                dur = float(res["gpu__time_duration.sum"][1].replace(",", ""))
+                dunit = res["gpu__time_duration.sum"][2]
+                dsec = dur * {"ns": 1e-9, "nsecond": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3}.get(dunit, 1e-9)
+                traffic += rd + wr
+                dsec_tot += dsec
+                lines += [f"DRAM traffic of this kernel: {(rd + wr) / 1e9:.3f} GB in {dsec * 1e3:.3f} ms "
+                          f"({(rd + wr) / dsec / 1e9:.1f} GB/s)", ""]
+            except Exception as e:  # pragma: no cover
+                lines.append(f"(traffic not computed: {e})")
+        if traffic > 0:
+            lines += [f"## One operator application (all kernels above)", "",
+                      f"DRAM traffic per application: {traffic / 1e9:.3f} GB, {dsec_tot * 1e3:.3f} ms under ncu"]
             if a.n_c:
                 alg = 16 * a.n_c
                 lines += [f"algorithmic bytes (16 N_c): {alg / 1e9:.3f} GB -> traffic / algorithmic = {traffic / alg:.3f}",
-                          f"achieved DRAM bandwidth under ncu (cold, clock-control none): {traffic / dsec / 1e9:.1f} GB/s"]
+                          f"achieved DRAM bandwidth under ncu (cold, clock-control none): {traffic / dsec_tot / 1e9:.1f} GB/s"]
             tpath = os.path.join(ROOT, "profiles", "traffic.json")
             tj = json.load(open(tpath)) if os.path.exists(tpath) else {}
             tj[a.config] = traffic
             json.dump(tj, open(tpath, "w"), indent=1)
-        except Exception as e:  # pragma: no cover
-            lines.append(f"(traffic not computed: {e})")
     out = os.path.join(ROOT, "profiles", f"{a.tag}_summary.md")
     open(out, "w").write("\n".join(lines) + "\n")
     print(out)
