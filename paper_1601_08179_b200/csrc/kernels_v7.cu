@@ -268,6 +268,7 @@ __global__ void __launch_bounds__(V8A<NI, STAGES>::NT, V8A<NI, STAGES>::MINB) k_
   for (int i = 0; i < NI; ++i) Dl[i] = lane_on ? cf.dinv[i + NI * l] : 0.0;
   const double c2j = cf.c[1][la], c3k = cf.c[2][lb];
   const double gj = (la & 1) ? -1.0 : 1.0, gk = (lb & 1) ? -1.0 : 1.0;
+  const double kf0 = cf.kf[0], kf1 = cf.kf[1], kf2 = cf.kf[2];
   double wpart[NG], tcarry[NG];
 #pragma unroll
   for (int r = 0; r < NG; ++r) tcarry[r] = 0.0;
@@ -330,8 +331,11 @@ __global__ void __launch_bounds__(V8A<NI, STAGES>::NT, V8A<NI, STAGES>::MINB) k_
           else qe = fma(c1, vv, qe);
           v[i] = vv;
         }
-        wpart[gr] = -(qe + qo);          // the element's W face
-        sE[el * N2 + l] = qo - qe;       // its E face (added to the W part of element el + 1)
+        // the element's W / E face parts: condensed part + the element's opposite-face coupling of the
+        // primary part (d1 K0p times the element's other x-face; the two elements of a face
+        // give d1 K0p (u_{fx-1} + u_{fx+1}))
+        wpart[gr] = fma(kf0, e, -(qe + qo));            // the element's W face
+        sE[el * N2 + l] = fma(kf0, w, qo - qe);         // its E face (added to the W part of element el + 1)
       }
     }
     __syncthreads();
@@ -353,8 +357,8 @@ __global__ void __launch_bounds__(V8A<NI, STAGES>::NT, V8A<NI, STAGES>::MINB) k_
             if (j & 1) qo += t;
             else qe += t;
           }
-          __stcs(uy + el * N2, -(qe + qo));                                // S face (ey) in U0
-          __stcs(uy + d01 + (long long)nx * N2 + el * N2, qo - qe);        // N face (ey + 1) in U1
+          __stcs(uy + el * N2, fma(kf1, Yr[1][el * N2 + l], -(qe + qo)));                                // S face (ey) in U0
+          __stcs(uy + d01 + (long long)nx * N2 + el * N2, fma(kf1, Yr[0][el * N2 + l], qo - qe));        // N face (ey + 1) in U1
           qe = 0.0; qo = 0.0;
 #pragma unroll
           for (int k = 0; k < NI; ++k) {   // lane (i, j) = (la, lb)
@@ -364,7 +368,7 @@ __global__ void __launch_bounds__(V8A<NI, STAGES>::NT, V8A<NI, STAGES>::MINB) k_
           }
           // z-face ez: B part + the T part of layer ez - 1 of this column (the column's first face keeps
           // the previous segment's T part in U1); the column's last T part goes to U1 at ez + 1
-          const double bp = -(qe + qo), tp = qo - qe;
+          const double bp = fma(kf2, Zr[1][el * N2 + l], -(qe + qo)), tp = fma(kf2, Zr[0][el * N2 + l], qo - qe);
           __stcs(uz + el * N2, s > 0 ? bp + tcarry[gr] : bp);
           if (s == zc - 1) __stcs(uz + d01 + (long long)nx * ny * N2 + el * N2, tp);
           tcarry[gr] = tp;
@@ -437,10 +441,11 @@ __device__ __forceinline__ double ldv(const double* __restrict__ x, long long i,
 
 // Face rows.  Thread t < FPI N2 keeps one in-face entry e = (ea, eb) = t % N2 (its coefficients in
 // registers) and walks the row's faces f = t / N2 + FPI it, so a warp's accesses are contiguous.  One face
-// entry: y = fd u + kf (u_lo + u_hi) + wA (a0_ea A0[eb] + ap_ea A1[eb]) + wB (a0_eb B0[ea] + ap_eb B1[ea])
-//            + U0 (+ U1)
+// entry: y = fd u + wA (a0_ea A0[eb] + ap_ea A1[eb]) + wB (a0_eb B0[ea] + ap_eb B1[ea]) + U0 (+ U1)
 // (the primary part of Eq. eq:east_east_primary_part_transformed summed over the face's two elements,
-// P:415-424, + the condensed parts from pass A).  CLS 0 / 1 / 2: x- / y- / z-face row of the cell row.
+// P:415-424; its opposite-face term kf (u_lo + u_hi) is added per element in pass A, which has both
+// parallel faces of the element on chip, together with the condensed parts).  CLS 0 / 1 / 2: x- / y- /
+// z-face row of the cell row.
 template <int NI, bool DOT, int CLS>
 __device__ __forceinline__ void face_row(const V7Params& P, int cy, int cz, double& dot) {
   constexpr int N2 = NI * NI, FPI = 256 / N2;
@@ -515,17 +520,14 @@ __device__ __forceinline__ void face_row(const V7Params& P, int cy, int cz, doub
     double yv = 0.0;
     if (fr) {
       const double u = __ldg(xp + o);
-      const double ulo = __ldg(xp + (olo ? o - so : o));
-      const double uhi = __ldg(xp + (ohi ? o + so : o));
       const long long oa = (long long)f * astep, ob = (long long)f * bstep;
       const double va0 = __ldg(pa0 + (ka0 ? oa : 0)), va1 = __ldg(pa1 + (ka1 ? oa : 0));
       const double vb0 = __ldg(pb0 + (okb0 ? ob : 0)), vb1 = __ldg(pb1 + (okb1 ? ob : 0));
       const double c0 = __ldcs(u0p + o);
       const double c1 = u1 ? __ldcs(u1p + o) : 0.0;
-      const double uo = (olo ? ulo : 0.0) + (ohi ? uhi : 0.0);
       const double ea_ = a0a * (ka0 ? va0 : 0.0) + apa * (ka1 ? va1 : 0.0);
       const double eb_ = a0b * (okb0 ? vb0 : 0.0) + apb * (okb1 ? vb1 : 0.0);
-      yv = fd * u + kf * uo + wA * ea_ + wB * eb_ + c0 + c1;
+      yv = fd * u + wA * ea_ + wB * eb_ + c0 + c1;
       if (DOT) dot = fma(u, yv, dot);
     }
     __stcs(yp + o, yv);
