@@ -307,7 +307,8 @@ __global__ void __launch_bounds__(V8A<NI, STAGES>::NT, V8A<NI, STAGES>::MINB) k_
     double* const ux = P.u0 + g.off_f[0] + (ex0 + nx1 * (ey + (long long)ny * ez)) * N2 + l;
     double* const uy = P.u0 + g.off_f[1] + (ex0 + (long long)nx * (ey + ny1 * ez)) * N2 + l;
     double* const uz = P.u0 + g.off_f[2] + (ex0 + (long long)nx * (ey + (long long)ny * ez)) * N2 + l;
-    // ---- phase X
+    // ---- phase X (+ the face values the lane's Y / Z outputs couple to, kept in registers)
+    double kfy[NG][2], kfz[NG][2];
     if (lane_on) {
 #pragma unroll
       for (int gr = 0; gr < NG; ++gr) {
@@ -336,43 +337,11 @@ __global__ void __launch_bounds__(V8A<NI, STAGES>::NT, V8A<NI, STAGES>::MINB) k_
         // give d1 K0p (u_{fx-1} + u_{fx+1}))
         wpart[gr] = fma(kf0, e, -(qe + qo));            // the element's W face
         sE[el * N2 + l] = fma(kf0, w, qo - qe);         // its E face (added to the W part of element el + 1)
-      }
-    }
-    __syncthreads();
-    // ---- x-faces, phases Y, Z
-    if (lane_on) {
-#pragma unroll
-      for (int gr = 0; gr < NG; ++gr) {
-        const int el = gr * G + eg;
-        if (el < cnt) {
-          // x-face ex0 + el: W part + the E part of element el - 1 (inside the run); the run's first
-          // face keeps the previous run's E part in U1, the run's last E part goes to U1
-          __stcs(ux + el * N2, el > 0 ? wpart[gr] + sE[(el - 1) * N2 + l] : wpart[gr]);
-          if (el == cnt - 1) __stcs(ux + d01 + (el + 1) * N2, sE[el * N2 + l]);
-          const double* const v = sv + el * A::VS;
-          double qe = 0.0, qo = 0.0;
-#pragma unroll
-          for (int j = 0; j < NI; ++j) {   // lane (i, k) = (la, lb)
-            const double t = cf.c[1][j] * v[la + NI * (j + NI * lb)];
-            if (j & 1) qo += t;
-            else qe += t;
-          }
-          __stcs(uy + el * N2, fma(kf1, Yr[1][el * N2 + l], -(qe + qo)));                                // S face (ey) in U0
-          __stcs(uy + d01 + (long long)nx * N2 + el * N2, fma(kf1, Yr[0][el * N2 + l], qo - qe));        // N face (ey + 1) in U1
-          qe = 0.0; qo = 0.0;
-#pragma unroll
-          for (int k = 0; k < NI; ++k) {   // lane (i, j) = (la, lb)
-            const double t = cf.c[2][k] * v[l + N2 * k];
-            if (k & 1) qo += t;
-            else qe += t;
-          }
-          // z-face ez: B part + the T part of layer ez - 1 of this column (the column's first face keeps
-          // the previous segment's T part in U1); the column's last T part goes to U1 at ez + 1
-          const double bp = fma(kf2, Zr[1][el * N2 + l], -(qe + qo)), tp = fma(kf2, Zr[0][el * N2 + l], qo - qe);
-          __stcs(uz + el * N2, s > 0 ? bp + tcarry[gr] : bp);
-          if (s == zc - 1) __stcs(uz + d01 + (long long)nx * ny * N2 + el * N2, tp);
-          tcarry[gr] = tp;
-        }
+        // the same coupling for the y / z faces (entry l = (i, k) / (i, j) of the Y / Z phases)
+        kfy[gr][0] = kf1 * Yr[1][el * N2 + l];   // into S: the element's N face
+        kfy[gr][1] = kf1 * Yr[0][el * N2 + l];   // into N: its S face
+        kfz[gr][0] = kf2 * Zr[1][el * N2 + l];   // into B: its T face
+        kfz[gr][1] = kf2 * Zr[0][el * N2 + l];   // into T: its B face
       }
     }
     // ---- edge line sums: slot -> (family, element, high side, entry); a warp's slots share the family
@@ -403,9 +372,10 @@ __global__ void __launch_bounds__(V8A<NI, STAGES>::NT, V8A<NI, STAGES>::MINB) k_
         __stcs((ehi ? P.u1 : P.u0) + dst, sum);
       }
     }
+    // the stage is no longer read (the Y / Z phases use uhat, the E parts and registers): release it and
+    // issue the item STAGES ahead into it, so its loads overlap the Y / Z phases
     fence_proxy_async();
     __syncthreads();
-    // the item STAGES ahead goes into the stage just released
     const bool more = (s + 1 < zc || (int)(icq.z + gridDim.x) < ncols);
     if (tid == 0 && ic < ncols) {
       sit[b] = decode<NI, R>(g, ic, is, nruns, Z);
@@ -417,6 +387,44 @@ __global__ void __launch_bounds__(V8A<NI, STAGES>::NT, V8A<NI, STAGES>::MINB) k_
         izc = ic < ncols ? col_len(ic) : 0;
       }
     }
+    // ---- x-faces, phases Y, Z
+    if (lane_on) {
+#pragma unroll
+      for (int gr = 0; gr < NG; ++gr) {
+        const int el = gr * G + eg;
+        if (el < cnt) {
+          // x-face ex0 + el: W part + the E part of element el - 1 (inside the run); the run's first
+          // face keeps the previous run's E part in U1, the run's last E part goes to U1
+          __stcs(ux + el * N2, el > 0 ? wpart[gr] + sE[(el - 1) * N2 + l] : wpart[gr]);
+          if (el == cnt - 1) __stcs(ux + d01 + (el + 1) * N2, sE[el * N2 + l]);
+          const double* const v = sv + el * A::VS;
+          double qe = 0.0, qo = 0.0;
+#pragma unroll
+          for (int j = 0; j < NI; ++j) {   // lane (i, k) = (la, lb)
+            const double t = cf.c[1][j] * v[la + NI * (j + NI * lb)];
+            if (j & 1) qo += t;
+            else qe += t;
+          }
+          __stcs(uy + el * N2, kfy[gr][0] - (qe + qo));                                // S face (ey) in U0
+          __stcs(uy + d01 + (long long)nx * N2 + el * N2, kfy[gr][1] + (qo - qe));     // N face (ey + 1) in U1
+          qe = 0.0; qo = 0.0;
+#pragma unroll
+          for (int k = 0; k < NI; ++k) {   // lane (i, j) = (la, lb)
+            const double t = cf.c[2][k] * v[l + N2 * k];
+            if (k & 1) qo += t;
+            else qe += t;
+          }
+          // z-face ez: B part + the T part of layer ez - 1 of this column (the column's first face keeps
+          // the previous segment's T part in U1); the column's last T part goes to U1 at ez + 1
+          const double bp = kfz[gr][0] - (qe + qo), tp = kfz[gr][1] + (qo - qe);
+          __stcs(uz + el * N2, s > 0 ? bp + tcarry[gr] : bp);
+          if (s == zc - 1) __stcs(uz + d01 + (long long)nx * ny * N2 + el * N2, tp);
+          tcarry[gr] = tp;
+        }
+      }
+    }
+    // uhat and the E parts are rewritten by the next item's phase X
+    __syncthreads();
     if (!more) break;
   }
 }
