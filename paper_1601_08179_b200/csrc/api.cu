@@ -448,15 +448,21 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
     // the measured fastest per p
     const char* opsel = getenv("SC_OP");
     const std::string op = opsel ? opsel : "";
-    // measured (tools/op_time.py, r2 runs): on one rank v7 (two passes) is fastest for every p = 3..8
-    // (cfg5 5.55 ms vs v3 7.89 / v6 7.96; cfg3 p = 3..8); on z-slab ranks (v7 is
-    // one-rank only) v6 for p = 5, 6, 7, v3 for p = 8, the row-warp kernels for p = 3, 4
+    // measured (tools/op_time.py, r2 runs): on one rank v7 (two passes) is fastest for every p = 3..16
+    // (cfg5 5.24 ms vs v3 7.89 / v6 7.96; cfg3 p = 12 0.92 vs v4 1.57 ms); on z-slab ranks
+    // (v7 is one-rank only) v6 for p = 5, 6, 7, v3 for p = 8, the row-warp kernels for p = 3, 4, v4 above
     const bool want_v6 = op == "v6" || (op.empty() && ni >= 4 && ni <= 6);
     const bool want_v7 = op == "v7" || op.empty();
     if (v7_supported(ni) && uniform && sig_ok && want_v7 && prm->nranks == 1 && !(env && env[0] == '1')) {
-      v7_make_coef(ni, g.d_uni, B.a0, B.ap, B.lam, B.K00, B.K0p, B.w0, ctx->v7_coef);
-      if (cudaMalloc(&ctx->d_u7, sizeof(double) * 2 * (size_t)g.n_total) != cudaSuccess) return fail("cudaMalloc u7");
-      if (cudaMemset(ctx->d_u7, 0, sizeof(double) * 2 * (size_t)g.n_total) != cudaSuccess) return fail("memset u7");
+      std::vector<double> dinv;
+      v7_make_coef(ni, g.d_uni, B.a0, B.ap, B.lam, B.K00, B.K0p, B.w0, ctx->v7_coef, dinv);
+      // U0 | U1 (2 n_total) followed by the D^{-1} table (n_I^3)
+      const size_t nu = 2 * (size_t)g.n_total;
+      if (cudaMalloc(&ctx->d_u7, sizeof(double) * (nu + dinv.size())) != cudaSuccess) return fail("cudaMalloc u7");
+      if (cudaMemset(ctx->d_u7, 0, sizeof(double) * nu) != cudaSuccess) return fail("memset u7");
+      if (cudaMemcpy(ctx->d_u7 + nu, dinv.data(), sizeof(double) * dinv.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+        return fail("copy dinv");
+      v7_set_dinv(ctx->v7_coef, ctx->d_u7 + nu);
       if (cudaMalloc(&ctx->d_dotp, sizeof(double) * (size_t)v7_dot_parts(g)) != cudaSuccess) return fail("cudaMalloc dotp");
       const char* fd = getenv("SC_FUSED_DOT");
       ctx->fused_dot = !(fd && fd[0] == '0');

@@ -26,14 +26,16 @@
 
 namespace sc {
 
+constexpr int V7_MAXNI = 15;   // v7 covers 2 <= n_I <= 15 (p = 3..16)
+
 struct V7Coef {
-  double c[3][8];         // d_{d+1} a0_m  (faces in / out, parity form)
-  double dinv[343];       // D^{-1}(i,j,k), i fastest (n_I^3 <= 343)
-  double a0[8], ap[8], lam[8];
-  double fd[3][49];       // face self: 2 (d0 w0 + d_n K00 + d_a w0 Lam_a + d_b w0 Lam_b), in-plane (a, b)
+  double c[3][16];        // d_{d+1} a0_m  (faces in / out, parity form)
+  const double* dinv;     // device table D^{-1}(i,j,k), i fastest (n_I^3 doubles, owned by the context)
+  double a0[16], ap[16], lam[16];
+  double fd[3][225];      // face self: 2 (d0 w0 + d_n K00 + d_a w0 Lam_a + d_b w0 Lam_b), in-plane (a, b)
   double kf[3];           // d_n K0p (opposite faces)
   double ef[3][3];        // face <- edge: 2 d w0 (per direction d, for the face normal n)
-  double eself[3][8];     // edge self: 4 d0 w0^2 + 4 d_e w0^2 Lam_m + 4 (d_o1 + d_o2) w0 K00
+  double eself[3][16];    // edge self: 4 d0 w0^2 + 4 d_e w0^2 Lam_m + 4 (d_o1 + d_o2) w0 K00
   double ev[3];           // edge <- vertex: 4 d_e w0^2
   double el[3][3];        // edge line sums: 2 d w0 for the transverse directions
   double vself;           // vertex: 8 d0 w0^3 + 8 (d1 + d2 + d3) w0^2 K00
@@ -185,12 +187,15 @@ struct V8A {
   static constexpr int N2 = NI * NI, N3 = N2 * NI;
   // elements per item (x-run) and per thread group; one stage: G N2 <= 256 threads and NG groups per
   // item; two stages (the next item's loads in flight while this one computes): one group per item
-  static constexpr int R = NI >= 6 ? 8 : (NI >= 4 ? 16 : 32);
-  static constexpr int G = STAGES == 2 ? R : (NI >= 6 ? 4 : (NI == 5 ? 8 : (NI == 4 ? 16 : (NI == 3 ? 16 : 32))));
+  // n_I >= 8: one group per item, the largest power of two G with G n_I^2 <= 256 (R must be a power of
+  // two: pass B tests the run-boundary x-faces with fx & (R - 1))
+  static constexpr int GB = N2 <= 64 ? 4 : (N2 <= 128 ? 2 : 1);
+  static constexpr int R = NI >= 8 ? GB : (NI >= 6 ? 8 : (NI >= 4 ? 16 : 32));
+  static constexpr int G = NI >= 8 ? GB : (STAGES == 2 ? R : (NI >= 6 ? 4 : (NI == 5 ? 8 : (NI == 4 ? 16 : (NI == 3 ? 16 : 32)))));
   static constexpr int NG = R / G;
   static constexpr int NT = ((G * N2 + 31) / 32) * 32;       // threads per CTA
   static constexpr int EWF = ((R * 2 * NI + 31) / 32) * 32;  // edge-phase slots per family (warp-rounded)
-  static constexpr int MINB = STAGES == 2 ? (NT > 256 ? 2 : 4) : (NT <= 128 ? 8 : (NT <= 160 ? 6 : 4));
+  static constexpr int MINB = NI >= 8 ? 3 : (STAGES == 2 ? (NT > 256 ? 2 : 4) : (NT <= 128 ? 8 : (NT <= 160 ? 6 : 4)));
   static constexpr int SX = ((R + 1) * N2 + 1 + 1) & ~1;     // slot >= len + 1 (the 8-byte phase), even
   static constexpr int SR = (R * N2 + 1 + 1) & ~1;
   static constexpr int STAGE = SX + 4 * SR;
@@ -694,10 +699,10 @@ __global__ void k_v7_padding(Geom g, double* __restrict__ y) {
 
 }  // namespace v7
 
-bool v7_supported(int ni) { return ni >= 2 && ni <= 7; }
+bool v7_supported(int ni) { return ni >= 2 && ni <= V7_MAXNI; }
 
 void v7_make_coef(int ni, const double* d, const double* a0, const double* ap, const double* lam, double K00,
-                  double K0p, double w0, std::vector<unsigned char>& out) {
+                  double K0p, double w0, std::vector<unsigned char>& out, std::vector<double>& dinv) {
   V7Coef c;
   memset(&c, 0, sizeof(c));
   const double w02 = w0 * w0, w03 = w02 * w0;
@@ -712,9 +717,11 @@ void v7_make_coef(int ni, const double* d, const double* a0, const double* ap, c
       c.eself[e][m] = 4.0 * (d[0] * w02 + d[1 + e] * w02 * lam[m] + (d[1 + o1] + d[1 + o2]) * w0 * K00);
     }
   }
+  dinv.assign((size_t)ni * ni * ni, 0.0);
   for (int k = 0; k < ni; ++k)
     for (int j = 0; j < ni; ++j)
-      for (int i = 0; i < ni; ++i) c.dinv[i + ni * (j + ni * k)] = 1.0 / (d[0] + d[1] * lam[i] + d[2] * lam[j] + d[3] * lam[k]);
+      for (int i = 0; i < ni; ++i) dinv[i + ni * (j + ni * k)] = 1.0 / (d[0] + d[1] * lam[i] + d[2] * lam[j] + d[3] * lam[k]);
+  c.dinv = nullptr;
   // face with normal n, in-plane directions (a, b) in increasing order: 2 (d0 w0 + d_n K00 + d_a w0 Lam_a + d_b w0 Lam_b)
   for (int n = 0; n < 3; ++n) {
     const int a = n == 0 ? 1 : 0, b = n == 2 ? 1 : 2;
@@ -733,6 +740,13 @@ void v7_make_coef(int ni, const double* d, const double* a0, const double* ap, c
   c.K0p = K0p;
   out.resize(sizeof(c));
   memcpy(out.data(), &c, sizeof(c));
+}
+
+void v7_set_dinv(std::vector<unsigned char>& coef, const double* d_dinv) {
+  V7Coef c;
+  memcpy(&c, coef.data(), sizeof(c));
+  c.dinv = d_dinv;
+  memcpy(coef.data(), &c, sizeof(c));
 }
 
 // Number of pass-B blocks (the p . q partials the PCG sums): one per cell row.
@@ -807,6 +821,14 @@ int launch_apply_v7(const Geom& g, const double* x, double* y, double* u0, doubl
     case 5: e = launch_v7_t<5>(P, st, nl); break;
     case 6: e = launch_v7_t<6>(P, st, nl); break;
     case 7: e = launch_v7_t<7>(P, st, nl); break;
+    case 8: e = launch_v7_t<8>(P, st, nl); break;
+    case 9: e = launch_v7_t<9>(P, st, nl); break;
+    case 10: e = launch_v7_t<10>(P, st, nl); break;
+    case 11: e = launch_v7_t<11>(P, st, nl); break;
+    case 12: e = launch_v7_t<12>(P, st, nl); break;
+    case 13: e = launch_v7_t<13>(P, st, nl); break;
+    case 14: e = launch_v7_t<14>(P, st, nl); break;
+    case 15: e = launch_v7_t<15>(P, st, nl); break;
     default: return (int)cudaErrorInvalidValue;
   }
   if (ev) cudaEventRecord(ev[1], st);

@@ -100,7 +100,8 @@ int launch_apply_p2s(const Geom& g, const double* x, double* y, const double* do
                      int* nlaunch, void* events = nullptr);
 bool v7_supported(int ni);
 void v7_make_coef(int ni, const double* d, const double* a0, const double* ap, const double* lam, double K00,
-                  double K0p, double w0, std::vector<unsigned char>& out);
+                  double K0p, double w0, std::vector<unsigned char>& out, std::vector<double>& dinv);
+void v7_set_dinv(std::vector<unsigned char>& coef, const double* d_dinv);
 long long v7_dot_parts(const Geom& g);
 int launch_apply_v7(const Geom& g, const double* x, double* y, double* u0, double* u1, const double* done,
                     const void* coef, double* dotp, void* stream, int* nlaunch, void* events = nullptr);

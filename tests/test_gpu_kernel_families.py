@@ -159,7 +159,8 @@ def test_p2_owner_stencil(ne, lam, monkeypatch):
 
 
 V7_CASES = [(3, (17, 9, 3)), (4, (9, 8, 3)), (5, (15, 7, 3)), (6, (9, 10, 2)), (7, (16, 4, 3)), (8, (9, 7, 3)),
-            (8, (33, 5, 4)), (8, (1, 1, 2)), (5, (2, 17, 3))]
+            (8, (33, 5, 4)), (8, (1, 1, 2)), (5, (2, 17, 3)), (9, (9, 4, 3)), (10, (5, 3, 3)), (11, (3, 4, 2)),
+            (12, (4, 3, 2)), (13, (3, 2, 3)), (14, (2, 3, 2)), (15, (3, 2, 2)), (16, (2, 3, 2))]
 
 
 @pytest.mark.parametrize("p,ne", V7_CASES)
@@ -181,7 +182,8 @@ def test_family_v7_operator_parity(p, ne, monkeypatch):
 
 
 @pytest.mark.parametrize("p,ne,z", [(8, (9, 7, 5), "2"), (8, (17, 3, 7), "3"), (5, (33, 4, 6), "4"),
-                                    (3, (65, 3, 5), "2"), (4, (17, 2, 9), "1"), (6, (9, 5, 4), "4")])
+                                    (3, (65, 3, 5), "2"), (4, (17, 2, 9), "1"), (6, (9, 5, 4), "4"),
+                                    (10, (5, 3, 5), "2"), (12, (3, 2, 4), "3")])
 def test_family_v7_z_segments(p, ne, z, monkeypatch):
     """v7 pass A assembles the z-faces inside a column of Z layers (and the x-faces inside a run); the
     segment-boundary z-faces and run-boundary x-faces keep their second part in U1: every Z, incl. a
@@ -194,7 +196,7 @@ def test_family_v7_z_segments(p, ne, z, monkeypatch):
     assert _rel(_apply_nodal(ctx, x), ref_op.apply(x)) <= 1e-12
 
 
-@pytest.mark.parametrize("p,ne", [(5, (15, 7, 4)), (8, (10, 6, 3))])
+@pytest.mark.parametrize("p,ne", [(5, (15, 7, 4)), (8, (10, 6, 3)), (12, (3, 3, 3))])
 def test_family_v7_pcg_fused_dot(p, ne, monkeypatch):
     """BT-PCG on v7 with p . q from pass B's per-block x . y partials, against the oracle."""
     from paper_1601_08179_b200 import SC_DUAL

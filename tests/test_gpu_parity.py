@@ -377,7 +377,8 @@ def test_pcg_parity_zsegments(nseg, fused, monkeypatch):
 # ---- v4 operator (n_I >= 8): colour-scheduled one-CTA-per-element kernels -----------------
 @pytest.mark.parametrize("p,ne", [(9, (3, 2, 3)), (12, (2, 3, 2)), (16, (3, 2, 2)), (17, (2, 2, 3)),
                                   (18, (2, 3, 2)), (20, (2, 2, 2))])
-def test_big_operator_parity(p, ne):
+def test_big_operator_parity(p, ne, monkeypatch):
+    monkeypatch.setenv("SC_OP", "big")   # v4 (the one-rank default for p <= 16 is v7, tested in test_gpu_kernel_families)
     g = small_grid(p, ne, 0.8, lengths=(1.2, 0.9, 1.1))
     op = operator.AssembledCondensedOperator(g)
     x = lattice_random(60 + p, g.ne, g.p).ravel()
@@ -411,8 +412,9 @@ def test_big_operator_matches_v1_and_is_symmetric(p):
     assert abs(a - b) <= 1e-12 * abs(a)
 
 
-def test_big_pcg_parity():
+def test_big_pcg_parity(monkeypatch):
     from paper_1601_08179_b200 import SC_DUAL
+    monkeypatch.setenv("SC_OP", "big")
     g = small_grid(12, (3, 2, 2), 1.0, lengths=(1.3, 0.7, 1.5))
     op = operator.AssembledCondensedOperator(g)
     ctx = ctx_for(g)
@@ -476,6 +478,7 @@ def test_big_pipelined_build_bitwise(p, ne, uniform, monkeypatch):
     2), picked per n_I by occupancy.  Both perform the same operations in the same order, so
     forcing either (SC_V4_PIPE=0 / 1) gives bitwise identical results, on uniform and non-uniform
     grids."""
+    monkeypatch.setenv("SC_OP", "big")
     g = small_grid(p, ne, 1.0) if uniform else nonuniform(p, ne, 1.0, seed=p)
     ctx = ctx_for(g)
     x = ctx.skeleton()
@@ -587,7 +590,7 @@ def test_cfg5_full_size_properties():
 @pytest.mark.parametrize("p", [2, 4, 8, 12, 16, 24, 32])
 def test_cfg3_full_size_against_v1(p):
     """BASELINE configs[2] (cfg3, (n p)^3 ~ 2.1e8 nodes per p) at full size with the kernel
-    p_sweep.py times for each p (p2 row-warp, rw row-warp, v3 tile-column, v4 colour element-CTA):
+    p_sweep.py times for each p (p2s owner stencil, v7 two-pass for p = 4..16, v4 colour element-CTA above):
     equal to the independent v1 kernel on the same seeded input, symmetric, and exactly 0 on the
     Dirichlet entries."""
     import os
