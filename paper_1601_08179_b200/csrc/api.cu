@@ -453,7 +453,7 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
     // (v7 is one-rank only) v6 for p = 5, 6, 7, v3 for p = 8, the row-warp kernels for p = 3, 4, v4 above
     const bool want_v6 = op == "v6" || (op.empty() && ni >= 4 && ni <= 6);
     const bool want_v7 = op == "v7" || op.empty();
-    if (v7_supported(ni) && uniform && sig_ok && want_v7 && prm->nranks == 1 && !(env && env[0] == '1')) {
+    if (v7_supported(ni) && uniform && sig_ok && want_v7 && !(env && env[0] == '1')) {
       std::vector<double> dinv;
       v7_make_coef(ni, g.d_uni, B.a0, B.ap, B.lam, B.K00, B.K0p, B.w0, ctx->v7_coef, dinv);
       // U0 | U1 (2 n_total) followed by the D^{-1} table (n_I^3)

@@ -17,8 +17,14 @@
 //    opposite faces, rank-1 face <-> edge couplings, arrowhead rows of K~ for edges / vertices),
 //    summed over all elements containing the entry, + U0 + U1 for faces.  Each entry is written
 //    once, in a fixed order; the p . q partials of PCG are formed here (fused dot).
-// Every free entry's elements lie inside the domain on one rank, so the primary coefficients are
-// the uniform-grid constants; Dirichlet entries are written as 0 and read as 0.
+// On one rank every free entry's elements lie inside the domain, so the primary coefficients are the
+// uniform-grid constants; Dirichlet entries are written as 0 and read as 0.  On z-slab ranks the
+// operator returns local partial sums on the interface planes (the halo exchange adds the neighbour's):
+// the condensed parts and edge line sums of pass A are local by construction (written by the local
+// elements only; U0 / U1 entries no local element writes stay 0), pass B forms the local half of the
+// interface entities' symmetric primary terms.  An interface edge's face-line sums are split between
+// the ranks by element (each line belongs to one element), not halved: only the halo sum is the
+// operator's value there.
 #include <cuda_runtime.h>
 #include <string.h>
 #include <vector>
@@ -469,7 +475,12 @@ __device__ __forceinline__ void face_row(const V7Params& P, int cy, int cz, doub
   const int nx = g.nx, ny = g.ny, nz = g.nz;
   const long long nx1 = nx + 1, ny1 = ny + 1;
   const int f0 = t / N2, e = t - f0 * N2, eb = e / NI, ea = e - eb * NI;
-  const double fd = cf.fd[CLS][e];
+  // a z-slab interface plane (cz = 0 / nz not Dirichlet): this rank holds one of the plane's two element
+  // layers, so it forms the local half of the symmetric primary-part terms; the halo exchange adds the
+  // neighbour's half (the condensed parts in U0 / U1 are local by construction)
+  const bool ifc = (cz == 0 && !g.dir_bot) || (cz == g.nz && !g.dir_top);
+  const double hf = (CLS == 2 && ifc) ? 0.5 : 1.0;
+  const double fd = hf * cf.fd[CLS][e];
   const double a0a = cf.a0[ea], apa = cf.ap[ea], a0b = cf.a0[eb], apb = cf.ap[eb];
   const bool zb0 = !zdir(g, cz), zb1 = !zdir(g, cz + 1);
   int nf;
@@ -505,8 +516,8 @@ __device__ __forceinline__ void face_row(const V7Params& P, int cy, int cz, doub
     A0 = g.off_e[1] + nx1 * (cy + (long long)ny * cz) * NI; A1 = A0 + NI; astep = NI;
     B0 = g.off_e[0] + (long long)nx * (cy + ny1 * cz) * NI; B1 = B0 + (long long)nx * NI; bstep = NI;
     okb0 = in_f(cy, ny); okb1 = in_f(cy + 1, ny);
-    u1r = cz % P.zseg == 0;
-    wA = cf.ef[2][0]; wB = cf.ef[2][1]; kf = cf.kf[2];
+    u1r = cz % P.zseg == 0 || cz == g.nz;
+    wA = hf * cf.ef[2][0]; wB = hf * cf.ef[2][1]; kf = cf.kf[2];
   }
   const double* __restrict__ x = P.x;
   const double* xp = x + base + e;
@@ -560,7 +571,9 @@ __device__ __forceinline__ void edge_row(const V7Params& P, int cy, int cz, doub
   const int nx = g.nx, ny = g.ny, nz = g.nz;
   const long long nx1 = nx + 1, ny1 = ny + 1;
   const int a0i = t / NI, m = t - a0i * NI;
-  const double self = cf.eself[DIR][m], va = cf.a0[m], vp = cf.ap[m];
+  const bool ifc = DIR < 2 && ((cz == 0 && !g.dir_bot) || (cz == g.nz && !g.dir_top));
+  const double hf = ifc ? 0.5 : 1.0;   // interface plane: the local half (see face_row)
+  const double self = hf * cf.eself[DIR][m], va = cf.a0[m], vp = cf.ap[m];
   const bool zb0 = !zdir(g, cz), zb1 = !zdir(g, cz + 1);
   const bool zlo = cz - 1 >= 0 && !zdir(g, cz - 1), zhi = cz + 1 <= nz && !zdir(g, cz + 1);
   const double* __restrict__ x = P.x;
@@ -575,7 +588,7 @@ __device__ __forceinline__ void edge_row(const V7Params& P, int cy, int cz, doub
     vbase = g.off_v + nx1 * (cy + ny1 * cz); vstep2 = 1;
     s1 = (long long)nx * NI; lo1 = cy - 1 > 0; hi1 = cy + 1 < ny;
     s2 = (long long)nx * ny1 * NI; lo2 = zlo; hi2 = zhi;
-    ev = cf.ev[0]; c1 = cf.el[0][1] * cf.K0p; c2 = cf.el[0][2] * cf.K0p;
+    ev = hf * cf.ev[0]; c1 = hf * cf.el[0][1] * cf.K0p; c2 = cf.el[0][2] * cf.K0p;
   } else if (DIR == 1) {   // y-edges (fx, cy, cz): vertices (fx, cy / cy + 1, cz); neighbours x (+- NI), z (+- nx1 ny NI)
     ne = nx + 1;
     base = g.off_e[1] + nx1 * (cy + (long long)ny * cz) * NI;
@@ -584,7 +597,7 @@ __device__ __forceinline__ void edge_row(const V7Params& P, int cy, int cz, doub
     vok1_r = in_f(cy, ny); vok2_r = in_f(cy + 1, ny);
     s1 = NI;
     s2 = nx1 * ny * NI; lo2 = zlo; hi2 = zhi;
-    ev = cf.ev[1]; c1 = cf.el[1][0] * cf.K0p; c2 = cf.el[1][2] * cf.K0p;
+    ev = hf * cf.ev[1]; c1 = hf * cf.el[1][0] * cf.K0p; c2 = cf.el[1][2] * cf.K0p;
   } else {                 // z-edges (fx, cy, cz): vertices (fx, cy, cz / cz + 1); neighbours x (+- NI), y (+- nx1 NI)
     ne = nx + 1;
     base = g.off_e[2] + nx1 * (cy + ny1 * cz) * NI;
@@ -646,6 +659,11 @@ __global__ void __launch_bounds__(256, 4) k_v7_assemble(const __grid_constant__ 
   {
     const bool fr = in_f(cy, ny) && !zdir(g, cz);
     const bool zlo_ok = cz - 1 >= 0 && !zdir(g, cz - 1), zhi_ok = cz + 1 <= nz && !zdir(g, cz + 1);
+    // interface plane: the in-plane terms are halved (two of the vertex's four element layers' worth
+    // are local), the z-edge on the other rank's side is not local (see face_row)
+    const bool ifc = (cz == 0 && !g.dir_bot) || (cz == nz && !g.dir_top);
+    const double hf = ifc ? 0.5 : 1.0;
+    const bool zbm = cz > 0, ztm = cz < nz;
     for (int fx = threadIdx.x; fx <= nx; fx += blockDim.x) {
       const long long i0 = g.off_v + fx + nx1 * (cy + ny1 * cz);
       double yv = 0.0;
@@ -660,13 +678,14 @@ __global__ void __launch_bounds__(256, 4) k_v7_assemble(const __grid_constant__ 
         for (int q = 0; q < NI_; ++q) {
           lx = fma(cf.ap[q], __ldg(x + xw + q), fma(cf.a0[q], __ldg(x + xe + q), lx));
           ly = fma(cf.ap[q], __ldg(x + ys + q), fma(cf.a0[q], __ldg(x + yn + q), ly));
-          lz = fma(cf.ap[q], __ldg(x + zb + q), fma(cf.a0[q], __ldg(x + zt + q), lz));
+          lz = fma(cf.ap[q], ldv(x, zb + q, zbm), fma(cf.a0[q], ldv(x, zt + q, ztm), lz));
         }
         const double nbx = ldv(x, i0 - 1, fx - 1 > 0) + ldv(x, i0 + 1, fx + 1 < nx);
         const double nby = ldv(x, i0 - nx1, cy - 1 > 0) + ldv(x, i0 + nx1, cy + 1 < ny);
         const long long pl = nx1 * ny1;
         const double nbz = ldv(x, i0 - pl, zlo_ok) + ldv(x, i0 + pl, zhi_ok);
-        yv = cf.vself * u + cf.vl[0] * fma(cf.K0p, nbx, lx) + cf.vl[1] * fma(cf.K0p, nby, ly) + cf.vl[2] * fma(cf.K0p, nbz, lz);
+        yv = hf * (cf.vself * u + cf.vl[0] * fma(cf.K0p, nbx, lx) + cf.vl[1] * fma(cf.K0p, nby, ly)) +
+             cf.vl[2] * fma(cf.K0p, nbz, lz);
         if (DOT) dot = fma(u, yv, dot);
       }
       __stcs(y + i0, yv);

@@ -181,6 +181,39 @@ def test_family_v7_operator_parity(p, ne, monkeypatch):
     assert torch.equal(y1, y2)
 
 
+@pytest.mark.parametrize("p,ne,R,z", [(8, (9, 5, 5), 2, None), (5, (10, 7, 6), 3, "2"), (3, (17, 4, 4), 2, None),
+                                      (12, (3, 2, 4), 2, "1"), (7, (9, 4, 9), 3, "2")])
+def test_family_v7_slab_ranks(p, ne, R, z, monkeypatch):
+    """v7 on z-slab ranks (SC_TEST_LOCAL_SLAB: no halo exchange): every entry off the interface planes
+    against the oracle's slab operator (non-Dirichlet interface planes), every z-segment split.  On the
+    interface planes v7 splits an edge's face-line couplings between the two ranks differently from
+    the oracle's element-by-element split (each line goes to one of the two elements of its face, see
+    kernels_v7.cu), so only the halo-summed value is comparable there: test_gpu_loopback checks it
+    against the global oracle."""
+    import copy
+    monkeypatch.setenv("SC_TEST_LOCAL_SLAB", "1")
+    if z:
+        monkeypatch.setenv("SC_V7_Z", z)
+    g = small_grid(p, ne, 0.9, lengths=(1.2, 0.8, 1.1))
+    for r in range(R):
+        ctx = _ctx(g, monkeypatch, "v7", rank=r, nranks=R)
+        z0, z1 = ctx.layout.z_begin, ctx.layout.z_end
+        gs = copy.deepcopy(g)
+        gs.ne = (g.ne[0], g.ne[1], z1 - z0)
+        gs.hz = g.hz[z0:z1]
+        gs.extra = dict(g.extra, dirichlet_z=(r == 0, r == R - 1))
+        xg = lattice_random(75 + p, g.ne, g.p)
+        xs = np.ascontiguousarray(xg[z0 * p:z1 * p + 1])
+        ref = operator.AssembledCondensedOperator(gs).apply(xs.ravel()).reshape(xs.shape)
+        y = _apply_nodal(ctx, xs.ravel()).reshape(xs.shape)
+        keep = np.ones(xs.shape[0], bool)
+        if r > 0:
+            keep[0] = False
+        if r < R - 1:
+            keep[-1] = False
+        assert _rel(y[keep], ref[keep]) <= 1e-12, (r, z0, z1)
+
+
 @pytest.mark.parametrize("p,ne,z", [(8, (9, 7, 5), "2"), (8, (17, 3, 7), "3"), (5, (33, 4, 6), "4"),
                                     (3, (65, 3, 5), "2"), (4, (17, 2, 9), "1"), (6, (9, 5, 4), "4"),
                                     (10, (5, 3, 5), "2"), (12, (3, 2, 4), "3")])

@@ -68,13 +68,17 @@ def stitch(g, parts):
     return glob.ravel()
 
 
-CASES = [(5, (10, 6, 6), 2, "v6"), (6, (9, 5, 7), 3, "v6"), (8, (9, 5, 5), 3, None), (3, (12, 7, 6), 3, None),
-         (2, (11, 6, 5), 2, None), (10, (3, 3, 4), 2, None)]
+CASES = [(5, (10, 6, 6), 2, "v6"), (6, (9, 5, 7), 3, "v6"), (8, (9, 5, 5), 3, "v3"), (3, (12, 7, 6), 3, "rw"),
+         (2, (11, 6, 5), 2, None), (10, (3, 3, 4), 2, "big"), (5, (10, 6, 6), 2, "v7"), (8, (9, 5, 5), 3, "v7"),
+         (3, (12, 7, 6), 3, "v7"), (12, (3, 3, 4), 2, "v7"), (7, (9, 4, 9), 3, None)]
 
 
 @pytest.mark.parametrize("p,ne,R,kernel", CASES)
-def test_loopback_ranks_against_global_oracle(p, ne, R, kernel):
+def test_loopback_ranks_against_global_oracle(p, ne, R, kernel, monkeypatch):
+    """kernel: the operator family forced with SC_OP (None: the default, v7 for 3 <= p <= 16)."""
     from paper_1601_08179_b200 import Context, LoopbackGroup, SC_PERM
+    if kernel:
+        monkeypatch.setenv("SC_OP", kernel)
     g = small_grid(p, ne, 0.8, lengths=(1.1, 0.9, 1.3))
     op = operator.AssembledCondensedOperator(g)
     xg = lattice_random(40 + p, g.ne, g.p)
@@ -117,8 +121,9 @@ def test_loopback_ranks_against_global_oracle(p, ne, R, kernel):
         out = run_ranks(R, rank)
     finally:
         grp.close()
-    if kernel:
-        assert all(o["kernel"].startswith(kernel) for o in out), [o["kernel"] for o in out]
+    want = {"big": "v4"}.get(kernel, kernel) or ("v7" if 3 <= p <= 16 else None)
+    if want:
+        assert all(o["kernel"].startswith(want) for o in out), [o["kernel"] for o in out]
     # halo-summed operator, condensed right-hand side
     assert _rel(stitch(g, [o["y"] for o in out]), y_ref) <= 1e-12
     assert _rel(stitch(g, [o["b"] for o in out]), b_ref) <= 1e-12
