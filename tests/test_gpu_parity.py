@@ -434,11 +434,16 @@ def test_big_pcg_parity(monkeypatch):
 # ---- z-slab ranks on one GPU (SC_TEST_LOCAL_SLAB: no communicator, the operator returns the
 # slab's local partial sums on its interface planes): every kernel family against the oracle's
 # slab operator with non-Dirichlet interface planes (the multi-GPU path before the NCCL halo sum)
-@pytest.mark.parametrize("p,ne,R", [(2, (37, 5, 5), 2), (3, (10, 7, 5), 2), (6, (9, 5, 4), 2), (8, (9, 6, 7), 3), (12, (3, 2, 4), 2)])
-def test_slab_rank_operator_parity(p, ne, R, monkeypatch):
+@pytest.mark.parametrize("p,ne,R,op", [(2, (37, 5, 5), 2, None), (3, (10, 7, 5), 2, "rw"), (6, (9, 5, 4), 2, "v6"),
+                                       (8, (9, 6, 7), 3, "v3"), (12, (3, 2, 4), 2, "big")])
+def test_slab_rank_operator_parity(p, ne, R, op, monkeypatch):
+    """The tile / colour / row-warp families (SC_OP; v7's slab split is tested in
+    test_gpu_kernel_families and test_gpu_loopback)."""
     import copy
     from paper_1601_08179_b200 import Context
     monkeypatch.setenv("SC_TEST_LOCAL_SLAB", "1")
+    if op:
+        monkeypatch.setenv("SC_OP", op)
     g = small_grid(p, ne, 0.9, lengths=(1.2, 0.8, 1.1))
     for r in range(R):
         ctx = Context(g.p, g.ne, (g.hx, g.hy, g.hz), g.lam, device=0, rank=r, nranks=R)
