@@ -201,7 +201,7 @@ struct V8A {
   static constexpr int NG = R / G;
   static constexpr int NT = ((G * N2 + 31) / 32) * 32;       // threads per CTA
   static constexpr int EWF = ((R * 2 * NI + 31) / 32) * 32;  // edge-phase slots per family (warp-rounded)
-  static constexpr int MINB = NI >= 8 ? 3 : (STAGES == 2 ? (NT > 256 ? 2 : 4) : (NT <= 128 ? 8 : (NT <= 160 ? 6 : 4)));
+  static constexpr int MINB = NI >= 7 ? 3 : (STAGES == 2 ? (NT > 256 ? 2 : 4) : (NT <= 128 ? 8 : (NT <= 160 ? 6 : 4)));
   static constexpr int SX = ((R + 1) * N2 + 1 + 1) & ~1;     // slot >= len + 1 (the 8-byte phase), even
   static constexpr int SR = (R * N2 + 1 + 1) & ~1;
   static constexpr int STAGE = SX + 4 * SR;
