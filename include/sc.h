@@ -262,10 +262,12 @@ enum { SC_PREC_NONE = 0, SC_PREC_DIAG = 1, SC_PREC_BLOCK = 2 };
 sc_status sc_pcg_solve_nodal(sc_ctx* ctx, int op, int prec, const double* d_b, double* d_x, double rtol,
                              int maxit, sc_pcg_report* rep, void* stream);
 
-/* Operator kernel family this ctx runs: "v6" / "v6h8" (halo-recompute tile columns,
- * 3 <= p <= 8), "v3" (tile columns with look-back), "v7" (two-pass, opt-in), "rw" (row-warp, p = 3, 4),
+/* Operator kernel family this ctx runs: "v7" (two passes: element condensed parts, then
+ * entity-wise primary part + assembly; the default for 3 <= p <= 16 on uniform grids), "v6" / "v6h8"
+ * (halo-recompute tile columns, 3 <= p <= 8), "v3" (tile columns with look-back), "rw" (row-warp, p = 3, 4),
  * "p2s" (owner-computes stencil, p = 2, one rank) / "p2" (colour-scheduled row-warp, p = 2),
- * "v4" (colour-scheduled element CTAs, p >= 9), "v1" (one CTA per element, any geometry). */
+ * "v4" (colour-scheduled element CTAs, p >= 9; the default for p >= 17 and non-uniform grids), "v1" (one CTA
+ * per element, any geometry). */
 const char* sc_operator_kernel(const sc_ctx* ctx);
 
 /* Number of kernels launched by this ctx since setup (for the bench's gpu_launches). */
