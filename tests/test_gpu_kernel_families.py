@@ -158,7 +158,7 @@ def test_p2_owner_stencil(ne, lam, monkeypatch):
     assert (y1 - y3).norm() <= 1e-13 * y3.norm()
 
 
-V7_CASES = [(3, (17, 9, 3)), (4, (9, 8, 3)), (5, (15, 7, 3)), (6, (9, 10, 2)), (7, (16, 4, 3)), (8, (9, 7, 3)),
+V7_CASES = [(3, (1, 1, 1)), (8, (1, 1, 1)), (4, (40, 1, 1)), (6, (1, 37, 2)), (16, (1, 1, 3)), (3, (17, 9, 3)), (4, (9, 8, 3)), (5, (15, 7, 3)), (6, (9, 10, 2)), (7, (16, 4, 3)), (8, (9, 7, 3)),
             (8, (33, 5, 4)), (8, (1, 1, 2)), (5, (2, 17, 3)), (9, (9, 4, 3)), (10, (5, 3, 3)), (11, (3, 4, 2)),
             (12, (4, 3, 2)), (13, (3, 2, 3)), (14, (2, 3, 2)), (15, (3, 2, 2)), (16, (2, 3, 2))]
 
@@ -171,7 +171,11 @@ def test_family_v7_operator_parity(p, ne, monkeypatch):
     ref_op = operator.AssembledCondensedOperator(g)
     x = lattice_random(90 + p, g.ne, g.p).ravel()
     ctx = _ctx(g, monkeypatch, "v7")
-    assert _rel(_apply_nodal(ctx, x), ref_op.apply(x)) <= 1e-12
+    y, ref = _apply_nodal(ctx, x), ref_op.apply(x)
+    if np.linalg.norm(ref) == 0.0:   # a single element: every skeleton entity is Dirichlet
+        assert np.linalg.norm(y) == 0.0
+    else:
+        assert _rel(y, ref) <= 1e-12
     xt = ctx.skeleton()
     ctx.sc_fill_random(2, xt)
     y1 = ctx.skeleton(fill=float("nan"))

@@ -70,7 +70,7 @@ def stitch(g, parts):
 
 CASES = [(5, (10, 6, 6), 2, "v6"), (6, (9, 5, 7), 3, "v6"), (8, (9, 5, 5), 3, "v3"), (3, (12, 7, 6), 3, "rw"),
          (2, (11, 6, 5), 2, None), (10, (3, 3, 4), 2, "big"), (5, (10, 6, 6), 2, "v7"), (8, (9, 5, 5), 3, "v7"),
-         (3, (12, 7, 6), 3, "v7"), (12, (3, 3, 4), 2, "v7"), (7, (9, 4, 9), 3, None)]
+         (3, (12, 7, 6), 3, "v7"), (12, (3, 3, 4), 2, "v7"), (7, (9, 4, 9), 3, None), (5, (6, 5, 3), 3, "v7")]
 
 
 @pytest.mark.parametrize("p,ne,R,kernel", CASES)
