@@ -196,8 +196,8 @@ struct V8A {
   // n_I >= 8: one group per item, the largest power of two G with G n_I^2 <= 256 (R must be a power of
   // two: pass B tests the run-boundary x-faces with fx & (R - 1))
   static constexpr int GB = N2 <= 64 ? 4 : (N2 <= 128 ? 2 : 1);
-  static constexpr int R = NI >= 8 ? GB : (NI >= 6 ? 8 : (NI >= 4 ? 16 : 32));
-  static constexpr int G = NI >= 8 ? GB : (STAGES == 2 ? R : (NI >= 6 ? 4 : (NI == 5 ? 8 : (NI == 4 ? 16 : (NI == 3 ? 16 : 32)))));
+  static constexpr int R = NI >= 8 ? GB : (NI == 7 ? 10 : (NI >= 6 ? 8 : (NI >= 4 ? 16 : 32)));
+  static constexpr int G = NI >= 8 ? GB : (STAGES == 2 ? R : (NI == 7 ? 5 : (NI >= 6 ? 4 : (NI == 5 ? 8 : (NI == 4 ? 16 : (NI == 3 ? 16 : 32))))));
   static constexpr int NG = R / G;
   static constexpr int NT = ((G * N2 + 31) / 32) * 32;       // threads per CTA
   static constexpr int EWF = ((R * 2 * NI + 31) / 32) * 32;  // edge-phase slots per family (warp-rounded)
