@@ -233,6 +233,18 @@ def test_family_v7_z_segments(p, ne, z, monkeypatch):
     assert _rel(_apply_nodal(ctx, x), ref_op.apply(x)) <= 1e-12
 
 
+@pytest.mark.parametrize("p,ne", [(4, (33, 5, 4)), (8, (21, 6, 5)), (12, (5, 3, 3))])
+def test_family_v7_two_stage_variant(p, ne, monkeypatch):
+    """The opt-in two-stage pass A (SC_V7_STAGES=2: one element group per item, the next item's loads in
+    flight while this one computes) against the oracle."""
+    monkeypatch.setenv("SC_V7_STAGES", "2")
+    g = small_grid(p, ne, 0.7, lengths=(1.2, 0.9, 0.6))
+    ref_op = operator.AssembledCondensedOperator(g)
+    x = lattice_random(95 + p, g.ne, g.p).ravel()
+    ctx = _ctx(g, monkeypatch, "v7")
+    assert _rel(_apply_nodal(ctx, x), ref_op.apply(x)) <= 1e-12
+
+
 @pytest.mark.parametrize("p,ne", [(5, (15, 7, 4)), (8, (10, 6, 3)), (12, (3, 3, 3))])
 def test_family_v7_pcg_fused_dot(p, ne, monkeypatch):
     """BT-PCG on v7 with p . q from pass B's per-block x . y partials, against the oracle."""
