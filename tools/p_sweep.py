@@ -59,7 +59,7 @@ def main():
                "hbm_floor_ms": t_hbm, "fp64_floor_ms": t_fp64,
                "hbm_frac": t_hbm / ms, "fp64_frac": t_fp64 / ms,
                "bound": "hbm" if t_hbm >= t_fp64 else "fp64", "roofline_frac": max(t_hbm, t_fp64) / ms,
-               "kernel": os.environ.get("SC_KERNEL_NOTE", "")}
+               "kernel": ctx.operator_kernel()}
         rows.append(row)
         print(json.dumps(row), flush=True)
         del ctx, x, y
