@@ -449,16 +449,25 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
     const char* opsel = getenv("SC_OP");
     const std::string op = opsel ? opsel : "";
     // measured (tools/op_time.py, r2 runs): on one rank v7 (two passes) is fastest for every p = 3..16
-    // (cfg5 5.24 ms vs v3 7.89 / v6 7.96; cfg3 p = 12 0.92 vs v4 1.57 ms); on z-slab ranks
-    // (v7 is one-rank only) v6 for p = 5, 6, 7, v3 for p = 8, the row-warp kernels for p = 3, 4, v4 above
+    // (cfg5 5.16 ms vs v3 7.89 / v6 7.96; cfg3 p = 12 0.93 vs v4 1.57 ms), on any number of
+    // ranks; without the memory for v7's two face-part vectors: v6 for p = 5, 6, 7, v3 for p = 8, the
+    // row-warp kernels for p = 3, 4, v4 above
     const bool want_v6 = op == "v6" || (op.empty() && ni >= 4 && ni <= 6);
     const bool want_v7 = op == "v7" || op.empty();
-    if (v7_supported(ni) && uniform && sig_ok && want_v7 && !(env && env[0] == '1')) {
-      std::vector<double> dinv;
+    bool v7_ok = v7_supported(ni) && uniform && sig_ok && want_v7 && !(env && env[0] == '1');
+    std::vector<double> dinv;
+    const size_t nu = 2 * (size_t)g.n_total;   // U0 | U1, then the D^{-1} table (n_I^3)
+    if (v7_ok) {
       v7_make_coef(ni, g.d_uni, B.a0, B.ap, B.lam, B.K00, B.K0p, B.w0, ctx->v7_coef, dinv);
-      // U0 | U1 (2 n_total) followed by the D^{-1} table (n_I^3)
-      const size_t nu = 2 * (size_t)g.n_total;
-      if (cudaMalloc(&ctx->d_u7, sizeof(double) * (nu + dinv.size())) != cudaSuccess) return fail("cudaMalloc u7");
+      const char* nm = getenv("SC_TEST_V7_NOMEM");   // tests: behave as if the allocation failed
+      if ((nm && nm[0] == '1') || cudaMalloc(&ctx->d_u7, sizeof(double) * (nu + dinv.size())) != cudaSuccess) {
+        (void)cudaGetLastError();   // out of memory for U0 / U1: fall back to a one-pass family
+        ctx->d_u7 = nullptr;
+        if (op == "v7") return fail("cudaMalloc u7 (SC_OP=v7)");
+        v7_ok = false;
+      }
+    }
+    if (v7_ok) {
       if (cudaMemset(ctx->d_u7, 0, sizeof(double) * nu) != cudaSuccess) return fail("memset u7");
       if (cudaMemcpy(ctx->d_u7 + nu, dinv.data(), sizeof(double) * dinv.size(), cudaMemcpyHostToDevice) != cudaSuccess)
         return fail("copy dinv");

@@ -233,6 +233,21 @@ def test_family_v7_z_segments(p, ne, z, monkeypatch):
     assert _rel(_apply_nodal(ctx, x), ref_op.apply(x)) <= 1e-12
 
 
+@pytest.mark.parametrize("p,ne,want", [(4, (33, 5, 4), "rw"), (8, (21, 6, 5), "v3"), (6, (9, 5, 4), "v6"),
+                                       (12, (5, 3, 3), "v4")])
+def test_v7_out_of_memory_falls_back(p, ne, want, monkeypatch):
+    """Without the memory for v7's two face-part vectors (SC_TEST_V7_NOMEM simulates the failed
+    allocation) the context falls back to the one-pass family of that p, still exact."""
+    from paper_1601_08179_b200 import Context
+    monkeypatch.setenv("SC_TEST_V7_NOMEM", "1")
+    g = small_grid(p, ne, 0.7, lengths=(1.2, 0.9, 0.6))
+    ref_op = operator.AssembledCondensedOperator(g)
+    x = lattice_random(97 + p, g.ne, g.p).ravel()
+    ctx = Context(g.p, g.ne, (g.hx, g.hy, g.hz), g.lam, device=0)
+    assert ctx.operator_kernel() == want, ctx.operator_kernel()
+    assert _rel(_apply_nodal(ctx, x), ref_op.apply(x)) <= 1e-12
+
+
 @pytest.mark.parametrize("p,ne", [(4, (33, 5, 4)), (8, (21, 6, 5)), (12, (5, 3, 3))])
 def test_family_v7_two_stage_variant(p, ne, monkeypatch):
     """The opt-in two-stage pass A (SC_V7_STAGES=2: one element group per item, the next item's loads in
