@@ -453,7 +453,7 @@ extern "C" sc_status sc_setup(const sc_params* prm, sc_ctx** out) {
     // ranks; without the memory for v7's two face-part vectors: v6 for p = 5, 6, 7, v3 for p = 8, the
     // row-warp kernels for p = 3, 4, v4 above
     const bool want_v6 = op == "v6" || (op.empty() && ni >= 4 && ni <= 6);
-    const bool want_v7 = op == "v7" || op.empty();
+    const bool want_v7 = op == "v7" || (op.empty() && ni <= 15);
     bool v7_ok = v7_supported(ni) && uniform && sig_ok && want_v7 && !(env && env[0] == '1');
     std::vector<double> dinv;
     const size_t nu = 2 * (size_t)g.n_total;   // U0 | U1, then the D^{-1} table (n_I^3)

@@ -32,16 +32,22 @@
 
 namespace sc {
 
-constexpr int V7_MAXNI = 15;   // v7 covers 2 <= n_I <= 15 (p = 3..16)
+constexpr int V7_MAXNI = 23;   // v7 covers 2 <= n_I <= 23 (p = 3..24; n_I^3 uhat of an element in shared memory)
+
+// pass B block size: 256 threads, or one face (n_I^2 entries, warp-rounded) when that is larger
+template <int NI>
+struct V7B {
+  static constexpr int BT = NI * NI > 256 ? ((NI * NI + 31) / 32) * 32 : 256;
+};
 
 struct V7Coef {
-  double c[3][16];        // d_{d+1} a0_m  (faces in / out, parity form)
+  double c[3][24];        // d_{d+1} a0_m  (faces in / out, parity form)
   const double* dinv;     // device table D^{-1}(i,j,k), i fastest (n_I^3 doubles, owned by the context)
-  double a0[16], ap[16], lam[16];
-  double fd[3][225];      // face self: 2 (d0 w0 + d_n K00 + d_a w0 Lam_a + d_b w0 Lam_b), in-plane (a, b)
+  double a0[24], ap[24], lam[24];
+  double fd[3][529];      // face self: 2 (d0 w0 + d_n K00 + d_a w0 Lam_a + d_b w0 Lam_b), in-plane (a, b)
   double kf[3];           // d_n K0p (opposite faces)
   double ef[3][3];        // face <- edge: 2 d w0 (per direction d, for the face normal n)
-  double eself[3][16];    // edge self: 4 d0 w0^2 + 4 d_e w0^2 Lam_m + 4 (d_o1 + d_o2) w0 K00
+  double eself[3][24];    // edge self: 4 d0 w0^2 + 4 d_e w0^2 Lam_m + 4 (d_o1 + d_o2) w0 K00
   double ev[3];           // edge <- vertex: 4 d_e w0^2
   double el[3][3];        // edge line sums: 2 d w0 for the transverse directions
   double vself;           // vertex: 8 d0 w0^3 + 8 (d1 + d2 + d3) w0^2 K00
@@ -195,13 +201,13 @@ struct V8A {
   // item; two stages (the next item's loads in flight while this one computes): one group per item
   // n_I >= 8: one group per item, the largest power of two G with G n_I^2 <= 256 (R must be a power of
   // two: pass B tests the run-boundary x-faces with fx & (R - 1))
-  static constexpr int GB = N2 <= 64 ? 4 : (N2 <= 128 ? 2 : 1);
+  static constexpr int GB = N2 <= 64 ? 4 : (N2 <= 128 ? 2 : 1);   // n_I >= 16: one element, one lane per line
   static constexpr int R = NI >= 8 ? GB : (NI == 7 ? 10 : (NI >= 6 ? 8 : (NI >= 4 ? 16 : 32)));
   static constexpr int G = NI >= 8 ? GB : (STAGES == 2 ? R : (NI == 7 ? 5 : (NI >= 6 ? 4 : (NI == 5 ? 8 : (NI == 4 ? 16 : (NI == 3 ? 16 : 32))))));
   static constexpr int NG = R / G;
   static constexpr int NT = ((G * N2 + 31) / 32) * 32;       // threads per CTA
   static constexpr int EWF = ((R * 2 * NI + 31) / 32) * 32;  // edge-phase slots per family (warp-rounded)
-  static constexpr int MINB = NI >= 7 ? 3 : (STAGES == 2 ? (NT > 256 ? 2 : 4) : (NT <= 128 ? 8 : (NT <= 160 ? 6 : 4)));
+  static constexpr int MINB = NI >= 16 ? 1 : NI >= 7 ? 3 : (STAGES == 2 ? (NT > 256 ? 2 : 4) : (NT <= 128 ? 8 : (NT <= 160 ? 6 : 4)));
   static constexpr int SX = ((R + 1) * N2 + 1 + 1) & ~1;     // slot >= len + 1 (the 8-byte phase), even
   static constexpr int SR = (R * N2 + 1 + 1) & ~1;
   static constexpr int STAGE = SX + 4 * SR;
@@ -467,7 +473,7 @@ __device__ __forceinline__ double ldv(const double* __restrict__ x, long long i,
 // z-face row of the cell row.
 template <int NI, bool DOT, int CLS>
 __device__ __forceinline__ void face_row(const V7Params& P, int cy, int cz, double& dot) {
-  constexpr int N2 = NI * NI, FPI = 256 / N2;
+  constexpr int N2 = NI * NI, FPI = V7B<NI>::BT / N2;
   const int t = threadIdx.x;
   if (t >= FPI * N2) return;
   const Geom& g = P.g;
@@ -563,7 +569,7 @@ __device__ __forceinline__ void face_row(const V7Params& P, int cy, int cz, doub
 // K0p couplings to the neighbouring edges along the two transverse directions.
 template <int NI, bool DOT, int DIR>
 __device__ __forceinline__ void edge_row(const V7Params& P, int cy, int cz, double& dot) {
-  constexpr int EPI = 256 / NI;
+  constexpr int EPI = V7B<NI>::BT / NI;
   const int t = threadIdx.x;
   if (t >= EPI * NI) return;
   const Geom& g = P.g;
@@ -639,7 +645,7 @@ __device__ __forceinline__ void edge_row(const V7Params& P, int cy, int cz, doub
 }
 
 template <int NI, bool DOT>
-__global__ void __launch_bounds__(256, 4) k_v7_assemble(const __grid_constant__ V7Params P) {
+__global__ void __launch_bounds__(V7B<NI>::BT, V7B<NI>::BT > 256 ? 2 : 4) k_v7_assemble(const __grid_constant__ V7Params P) {
   if (P.done != nullptr && *P.done != 0.0) return;
   const Geom& g = P.g;
   const V7Coef& cf = P.cf;
@@ -693,13 +699,13 @@ __global__ void __launch_bounds__(256, 4) k_v7_assemble(const __grid_constant__ 
   }
   if (DOT) {
     // block partial of x . y in a fixed order (warp shuffles, then warps in order)
-    __shared__ double red[8];
+    __shared__ double red[V7B<NI>::BT / 32];
     for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dot;
     __syncthreads();
     if (threadIdx.x == 0) {
       double s = 0.0;
-      for (int w = 0; w < 8; ++w) s += red[w];
+      for (int w = 0; w < V7B<NI>::BT / 32; ++w) s += red[w];
       P.dotp[blockIdx.x] = s;
     }
   }
@@ -815,8 +821,8 @@ static int launch_v7_t(V7Params& P, cudaStream_t st, int* nl) {
   }
   (*nl)++;
   const unsigned rows = (unsigned)((g.ny + 1) * (g.nz + 1));
-  if (P.dotp) v7::k_v7_assemble<NI, true><<<rows, 256, 0, st>>>(P);
-  else v7::k_v7_assemble<NI, false><<<rows, 256, 0, st>>>(P);
+  if (P.dotp) v7::k_v7_assemble<NI, true><<<rows, V7B<NI>::BT, 0, st>>>(P);
+  else v7::k_v7_assemble<NI, false><<<rows, V7B<NI>::BT, 0, st>>>(P);
   (*nl)++;
   v7::k_v7_padding<<<1, 256, 0, st>>>(g, P.y);
   (*nl)++;
@@ -848,6 +854,14 @@ int launch_apply_v7(const Geom& g, const double* x, double* y, double* u0, doubl
     case 13: e = launch_v7_t<13>(P, st, nl); break;
     case 14: e = launch_v7_t<14>(P, st, nl); break;
     case 15: e = launch_v7_t<15>(P, st, nl); break;
+    case 16: e = launch_v7_t<16>(P, st, nl); break;
+    case 17: e = launch_v7_t<17>(P, st, nl); break;
+    case 18: e = launch_v7_t<18>(P, st, nl); break;
+    case 19: e = launch_v7_t<19>(P, st, nl); break;
+    case 20: e = launch_v7_t<20>(P, st, nl); break;
+    case 21: e = launch_v7_t<21>(P, st, nl); break;
+    case 22: e = launch_v7_t<22>(P, st, nl); break;
+    case 23: e = launch_v7_t<23>(P, st, nl); break;
     default: return (int)cudaErrorInvalidValue;
   }
   if (ev) cudaEventRecord(ev[1], st);

@@ -160,7 +160,8 @@ def test_p2_owner_stencil(ne, lam, monkeypatch):
 
 V7_CASES = [(3, (1, 1, 1)), (8, (1, 1, 1)), (4, (40, 1, 1)), (6, (1, 37, 2)), (16, (1, 1, 3)), (3, (17, 9, 3)), (4, (9, 8, 3)), (5, (15, 7, 3)), (6, (9, 10, 2)), (7, (16, 4, 3)), (8, (9, 7, 3)),
             (8, (33, 5, 4)), (8, (1, 1, 2)), (5, (2, 17, 3)), (9, (9, 4, 3)), (10, (5, 3, 3)), (11, (3, 4, 2)),
-            (12, (4, 3, 2)), (13, (3, 2, 3)), (14, (2, 3, 2)), (15, (3, 2, 2)), (16, (2, 3, 2))]
+            (12, (4, 3, 2)), (13, (3, 2, 3)), (14, (2, 3, 2)), (15, (3, 2, 2)), (16, (2, 3, 2)), (18, (3, 2, 2)),
+            (24, (2, 2, 2))]
 
 
 @pytest.mark.parametrize("p,ne", V7_CASES)
